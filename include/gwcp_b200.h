@@ -1,0 +1,147 @@
+/*
+ * gwcp_b200.h — C-ABI of the B200-native G-WCP trace-analysis engine.
+ *
+ * The reference (gpurace 0.1.0, pure Python) has no FFI: its hot path is the
+ * duck-typed detector protocol driven by
+ *     engine.run(trace, GwcpDetector(cfg))          pkg/src/gpurace/engine.py:98-155
+ * and the CLI front end
+ *     gpurace check TRACE --detector gwcp           pkg/src/gpurace/cli.py:63-84
+ * Every entry point below replaces one piece of that path; the Python shim in
+ * paper_2111_12478_b200/ (engine.run / GwcpDetector / cli) binds them with
+ * ctypes, and INTEGRATION.md shows the stub a gpurace maintainer would add.
+ *
+ * Conventions: plain pointers and sizes only; 0 = success, non-zero = error
+ * with a message in gw_last_error(); nothing is silently truncated; arrays in
+ * a gw_trace / gw_result are owned by the library and released by the
+ * matching *_free call.  One analysis per context at a time (not reentrant per
+ * context); distinct contexts may be used from distinct host threads.
+ */
+#ifndef GWCP_B200_H
+#define GWCP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GW_OK 0
+#define GW_E_PARSE 1        /* text trace rejected (TraceParseError, trace.py:142-145) */
+#define GW_E_UNSUPPORTED 2  /* value outside the SoA encoding (e.g. addr >= 2^63, >2^24 threads) */
+#define GW_E_CUDA 3         /* CUDA runtime / kernel error */
+#define GW_E_NOMEM 4        /* device or host allocation failed */
+#define GW_E_ARG 5          /* bad arguments */
+
+/* ---- SoA event encoding (16 B / event) ---------------------------------
+ * tidop  : bits 0-23 flat thread index (b*W + w)*L + l      (trace.py:105-106)
+ *          bits 24-26 kind, bit 27 atomic, bit 28 device scope,
+ *          bit 29 warp barrier, bit 30 continues-record (same group as the
+ *          previous event, group >= 0; engine.py:111-118)
+ *          barriers carry the flat index of lane 0 of their warp / block.
+ * key    : access  -> location key: global addr (< 2^63), or
+ *                     1<<63 | block<<40 | addr (addr < 2^40) for shared memory
+ *          acq/rel -> lock id (u64)
+ * instr  : access  -> instruction id (u32); warp barrier -> lane mask
+ */
+#define GW_K_READ 0u
+#define GW_K_WRITE 1u
+#define GW_K_ACQUIRE 2u
+#define GW_K_RELEASE 3u
+#define GW_K_BARRIER 4u
+#define GW_K_FENCE 5u
+#define GW_K_END 6u
+#define GW_OP_SHIFT 24
+#define GW_TID_MASK 0x00FFFFFFu
+#define GW_F_ATOMIC (1u << 27)
+#define GW_F_DEVICE (1u << 28)
+#define GW_F_WARPBAR (1u << 29)
+#define GW_F_CONT (1u << 30)
+#define GW_SHARED_BIT (1ull << 63)
+
+/* report kinds (report.py:13-15) */
+#define GW_WW 0
+#define GW_WR 1
+#define GW_RW 2
+
+/* diagnostic codes (gwcp.py:178-182, :197-201, :323-330) */
+#define GW_D_REENTRANT 1
+#define GW_D_UNHELD 2
+#define GW_D_EXIT_HOLDING 3
+
+typedef struct gw_config {
+  uint32_t blocks, warps, lanes, _pad; /* TraceConfig, trace.py:95-106 */
+} gw_config;
+
+typedef struct gw_trace { /* library-owned host SoA (gw_parse_text) */
+  gw_config cfg;
+  uint64_t n_events;
+  uint64_t* key;
+  uint32_t* tidop;
+  uint32_t* instr;
+} gw_trace;
+
+typedef struct gw_trace_view { /* caller-owned SoA; host or device pointers */
+  gw_config cfg;
+  uint64_t n_events;
+  const uint64_t* key;
+  const uint32_t* tidop;
+  const uint32_t* instr;
+} gw_trace_view;
+
+typedef struct gw_opts {
+  uint32_t inactive_opt; /* GwcpDetector(inactive_opt=...), gwcp.py:108-127 */
+  uint32_t flags;        /* reserved, 0 */
+  void* stream;          /* cudaStream_t to launch on (NULL = legacy default) */
+} gw_opts;
+
+typedef struct gw_result { /* library-owned; reports in final order */
+  uint64_t n_reports;      /* report 0 is "first", the rest "post-race" (report.py:97) */
+  uint8_t* kind;           /* GW_WW / GW_WR / GW_RW */
+  uint32_t* prior_event;   /* event indices; tid/instr/loc are read from the trace */
+  uint32_t* current_event;
+  uint64_t n_diags;        /* in event order */
+  uint32_t* diag_event;
+  uint32_t* diag_code;     /* GW_D_* */
+  uint64_t* diag_lock;     /* lock id (EXIT_HOLDING: one entry per held frame, bottom->top) */
+} gw_result;
+
+typedef struct gw_stats { /* per-phase device times of the last analysis (ms) */
+  float ms_total, ms_prep, ms_walker, ms_sort, ms_check, ms_final;
+  uint64_t n_accesses, n_candidates, n_sync, arena_words;
+  uint32_t walker_ctas, sort_bits;
+} gw_stats;
+
+typedef struct gw_ctx gw_ctx;
+
+/* ---- host-side trace ingest (replaces parse_trace, trace.py:226-398) ---- */
+int gw_parse_text(const char* text, uint64_t len, gw_trace* out, int64_t* err_line);
+void gw_trace_free(gw_trace* t);
+
+/* validate_trace (trace.py:522-601): diagnostics as (event, code, a, b); see cli shim */
+int gw_validate(const gw_trace_view* t, uint64_t* n_out, uint32_t** ev, uint32_t** code,
+                uint64_t** a, uint64_t** b);
+void gw_free(void* p);
+
+/* ---- analysis (replaces engine.run + GwcpDetector, engine.py:98-155, gwcp.py:103-356) */
+/* host SoA in, host results out: H2D, all kernels, D2H inside */
+int gw_analyze(const gw_trace_view* host_trace, const gw_opts* opts, gw_result* out);
+void gw_result_free(gw_result* r);
+const char* gw_last_error(void);
+
+/* device-resident context API: buffers persist across calls */
+gw_ctx* gw_ctx_create(int device);
+void gw_ctx_destroy(gw_ctx* c);
+/* dev_trace points at device memory; enqueues on opts->stream; results stay on device */
+int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* dev_trace, const gw_opts* opts);
+/* host_trace in (pageable or pinned) -> H2D on opts->stream -> analyze (results on device) */
+int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* host_trace, const gw_opts* opts);
+/* D2H of the last analysis' results (synchronises the stream) */
+int gw_ctx_fetch(gw_ctx* c, gw_result* out);
+int gw_ctx_stats(gw_ctx* c, gw_stats* out);
+/* number of kernels the last analysis launched */
+uint32_t gw_ctx_launches(gw_ctx* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,314 @@
+"""ctypes binding of libgwcp_b200.so (include/gwcp_b200.h).
+
+The analysis has no CPU path: if the shared library is missing or fails to
+load, every entry point raises ``NativeUnavailable`` -- there is no fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("GWCP_B200_LIB", os.path.join(_HERE, "libgwcp_b200.so"))
+
+GW_OK, GW_E_PARSE, GW_E_UNSUPPORTED, GW_E_CUDA, GW_E_NOMEM, GW_E_ARG = range(6)
+
+# SoA encoding (gwcp_b200.h)
+K_READ, K_WRITE, K_ACQUIRE, K_RELEASE, K_BARRIER, K_FENCE, K_END = range(7)
+OP_SHIFT = 24
+TID_MASK = 0x00FFFFFF
+F_ATOMIC = 1 << 27
+F_DEVICE = 1 << 28
+F_WARPBAR = 1 << 29
+F_CONT = 1 << 30
+SHARED_BIT = 1 << 63
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class EngineError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+class _Config(C.Structure):
+    _fields_ = [("blocks", C.c_uint32), ("warps", C.c_uint32), ("lanes", C.c_uint32), ("_pad", C.c_uint32)]
+
+
+class _Trace(C.Structure):
+    _fields_ = [
+        ("cfg", _Config),
+        ("n_events", C.c_uint64),
+        ("key", C.POINTER(C.c_uint64)),
+        ("tidop", C.POINTER(C.c_uint32)),
+        ("instr", C.POINTER(C.c_uint32)),
+    ]
+
+
+class _View(C.Structure):
+    _fields_ = [
+        ("cfg", _Config),
+        ("n_events", C.c_uint64),
+        ("key", C.c_void_p),
+        ("tidop", C.c_void_p),
+        ("instr", C.c_void_p),
+    ]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("inactive_opt", C.c_uint32), ("flags", C.c_uint32), ("stream", C.c_void_p)]
+
+
+class _Result(C.Structure):
+    _fields_ = [
+        ("n_reports", C.c_uint64),
+        ("kind", C.POINTER(C.c_uint8)),
+        ("prior_event", C.POINTER(C.c_uint32)),
+        ("current_event", C.POINTER(C.c_uint32)),
+        ("n_diags", C.c_uint64),
+        ("diag_event", C.POINTER(C.c_uint32)),
+        ("diag_code", C.POINTER(C.c_uint32)),
+        ("diag_lock", C.POINTER(C.c_uint64)),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("ms_total", C.c_float),
+        ("ms_prep", C.c_float),
+        ("ms_walker", C.c_float),
+        ("ms_sort", C.c_float),
+        ("ms_check", C.c_float),
+        ("ms_final", C.c_float),
+        ("n_accesses", C.c_uint64),
+        ("n_candidates", C.c_uint64),
+        ("n_sync", C.c_uint64),
+        ("arena_words", C.c_uint64),
+        ("walker_ctas", C.c_uint32),
+        ("sort_bits", C.c_uint32),
+    ]
+
+
+EXPORTS = (
+    "gw_parse_text",
+    "gw_trace_free",
+    "gw_validate",
+    "gw_free",
+    "gw_analyze",
+    "gw_result_free",
+    "gw_last_error",
+    "gw_ctx_create",
+    "gw_ctx_destroy",
+    "gw_ctx_analyze_device",
+    "gw_ctx_analyze_host",
+    "gw_ctx_fetch",
+    "gw_ctx_stats",
+    "gw_ctx_launches",
+)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeUnavailable(
+                f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        try:
+            L = C.CDLL(LIB_PATH)
+        except OSError as e:  # pragma: no cover - depends on the box
+            raise NativeUnavailable(f"cannot load {LIB_PATH}: {e}") from e
+        L.gw_parse_text.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(_Trace), C.POINTER(C.c_int64)]
+        L.gw_parse_text.restype = C.c_int
+        L.gw_trace_free.argtypes = [C.POINTER(_Trace)]
+        L.gw_validate.argtypes = [
+            C.POINTER(_View),
+            C.POINTER(C.c_uint64),
+            C.POINTER(C.POINTER(C.c_uint32)),
+            C.POINTER(C.POINTER(C.c_uint32)),
+            C.POINTER(C.POINTER(C.c_uint64)),
+            C.POINTER(C.POINTER(C.c_uint64)),
+        ]
+        L.gw_validate.restype = C.c_int
+        L.gw_free.argtypes = [C.c_void_p]
+        L.gw_analyze.argtypes = [C.POINTER(_View), C.POINTER(_Opts), C.POINTER(_Result)]
+        L.gw_analyze.restype = C.c_int
+        L.gw_result_free.argtypes = [C.POINTER(_Result)]
+        L.gw_last_error.restype = C.c_char_p
+        L.gw_ctx_create.argtypes = [C.c_int]
+        L.gw_ctx_create.restype = C.c_void_p
+        L.gw_ctx_destroy.argtypes = [C.c_void_p]
+        L.gw_ctx_analyze_device.argtypes = [C.c_void_p, C.POINTER(_View), C.POINTER(_Opts)]
+        L.gw_ctx_analyze_device.restype = C.c_int
+        L.gw_ctx_analyze_host.argtypes = [C.c_void_p, C.POINTER(_View), C.POINTER(_Opts)]
+        L.gw_ctx_analyze_host.restype = C.c_int
+        L.gw_ctx_fetch.argtypes = [C.c_void_p, C.POINTER(_Result)]
+        L.gw_ctx_fetch.restype = C.c_int
+        L.gw_ctx_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
+        L.gw_ctx_stats.restype = C.c_int
+        L.gw_ctx_launches.argtypes = [C.c_void_p]
+        L.gw_ctx_launches.restype = C.c_uint32
+        _lib = L
+        return L
+
+
+def last_error() -> str:
+    return lib().gw_last_error().decode("utf-8", "replace")
+
+
+def _check(rc: int) -> None:
+    if rc != GW_OK:
+        raise EngineError(rc, last_error())
+
+
+def parse_text(text: str | bytes):
+    """Text trace -> (cfg tuple, key u64[], tidop u32[], instr u32[]).
+
+    Raises EngineError(GW_E_PARSE, "line N: msg") on a parse error; the
+    error line is attached as ``.line``.
+    """
+    L = lib()
+    data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    t = _Trace()
+    line = C.c_int64(-1)
+    rc = L.gw_parse_text(data, len(data), C.byref(t), C.byref(line))
+    if rc != GW_OK:
+        err = EngineError(rc, last_error())
+        err.line = int(line.value)  # type: ignore[attr-defined]
+        raise err
+    try:
+        n = int(t.n_events)
+        key = np.ctypeslib.as_array(t.key, shape=(max(n, 1),))[:n].copy()
+        tidop = np.ctypeslib.as_array(t.tidop, shape=(max(n, 1),))[:n].copy()
+        instr = np.ctypeslib.as_array(t.instr, shape=(max(n, 1),))[:n].copy()
+        cfg = (int(t.cfg.blocks), int(t.cfg.warps), int(t.cfg.lanes))
+    finally:
+        L.gw_trace_free(C.byref(t))
+    return cfg, key, tidop, instr
+
+
+def _view(cfg, key, tidop, instr) -> _View:
+    v = _View()
+    v.cfg.blocks, v.cfg.warps, v.cfg.lanes = cfg
+    v.n_events = len(tidop)
+    v.key = key.ctypes.data if len(key) else None
+    v.tidop = tidop.ctypes.data if len(tidop) else None
+    v.instr = instr.ctypes.data if len(instr) else None
+    return v
+
+
+def validate(cfg, key, tidop, instr):
+    L = lib()
+    v = _view(cfg, key, tidop, instr)
+    n = C.c_uint64(0)
+    pe, pc = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)()
+    pa, pb = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint64)()
+    _check(L.gw_validate(C.byref(v), C.byref(n), C.byref(pe), C.byref(pc), C.byref(pa), C.byref(pb)))
+    k = int(n.value)
+    try:
+        out = [(int(pe[i]), int(pc[i]), int(pa[i]), int(pb[i])) for i in range(k)]
+    finally:
+        for p in (pe, pc, pa, pb):
+            L.gw_free(C.cast(p, C.c_void_p))
+    return out
+
+
+def _take_result(L, r: _Result):
+    try:
+        n = int(r.n_reports)
+        nd = int(r.n_diags)
+
+        def arr(p, count, dt):
+            if count == 0:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(p, shape=(count,)).copy()
+
+        res = {
+            "kind": arr(r.kind, n, np.uint8),
+            "prior": arr(r.prior_event, n, np.uint32),
+            "current": arr(r.current_event, n, np.uint32),
+            "diag_event": arr(r.diag_event, nd, np.uint32),
+            "diag_code": arr(r.diag_code, nd, np.uint32),
+            "diag_lock": arr(r.diag_lock, nd, np.uint64),
+        }
+    finally:
+        L.gw_result_free(C.byref(r))
+    return res
+
+
+class Context:
+    """A device context: buffers persist across analyses (bench, servers)."""
+
+    def __init__(self, device: int = 0):
+        self._L = lib()
+        self._c = self._L.gw_ctx_create(int(device))
+        if not self._c:
+            raise EngineError(GW_E_CUDA, last_error())
+
+    def close(self) -> None:
+        if self._c:
+            self._L.gw_ctx_destroy(self._c)
+            self._c = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def analyze_host(self, cfg, key, tidop, instr, *, inactive_opt=True, stream=None) -> None:
+        v = _view(cfg, key, tidop, instr)
+        o = _Opts(1 if inactive_opt else 0, 0, stream)
+        _check(self._L.gw_ctx_analyze_host(self._c, C.byref(v), C.byref(o)))
+
+    def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None) -> None:
+        v = _View()
+        v.cfg.blocks, v.cfg.warps, v.cfg.lanes = cfg
+        v.n_events = n
+        v.key, v.tidop, v.instr = key_ptr, tidop_ptr, instr_ptr
+        o = _Opts(1 if inactive_opt else 0, 0, stream)
+        _check(self._L.gw_ctx_analyze_device(self._c, C.byref(v), C.byref(o)))
+
+    def fetch(self):
+        r = _Result()
+        _check(self._L.gw_ctx_fetch(self._c, C.byref(r)))
+        return _take_result(self._L, r)
+
+    def stats(self) -> Stats:
+        s = Stats()
+        _check(self._L.gw_ctx_stats(self._c, C.byref(s)))
+        return s
+
+    def launches(self) -> int:
+        return int(self._L.gw_ctx_launches(self._c))
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def analyze(cfg, key, tidop, instr, *, inactive_opt=True):
+    """Host SoA in -> report / diagnostic arrays out (GPU; no CPU path)."""
+    ctx = default_context()
+    ctx.analyze_host(cfg, key, tidop, instr, inactive_opt=inactive_opt)
+    return ctx.fetch()

@@ -1,0 +1,348 @@
+// Access pass of the G-WCP engine: the data-parallel core.
+//
+// Reference semantics (pkg/src/gpurace/gwcp.py:251-277, engine.py:81-95,
+// report.py:79-100, scopes.py:32-47):
+//   prior write W = last write to loc in trace order (any thread)
+//     report ww|wr iff W.tid != t && W.time > pred_t[W.tid] && !atomics_cover
+//   on a write, for each reader u since W in first-insertion order carrying
+//   u's latest read r: report rw iff u != t && r.time > pred_t[u] && !cover
+//   multi-lane WRITE records: ww(i, j) for lanes i < j on one location
+//   Reporter: keep-first on (loc, prior.instr, current.instr); first -> "first"
+//
+// Batch form: sort accesses by (location, event) with a
+// stable LSD radix sort on the compacted location key, find each access's
+// prior write / segment head with one max-scan, evaluate every candidate pair
+// with a single u32 gather pred_t^{ver}[u] from the walker's clock objects,
+// and order the survivors by the key
+//   (event, 0, i, j)  same-instruction pair of the record starting at event
+//   (event, 1, 0, 0)  write check
+//   (event, 1, 1, k)  k-th reader (k = rank of the reader's first read)
+// which reproduces the reference's report sequence exactly.
+#pragma once
+#include "walker.cuh"
+
+namespace gw {
+
+constexpr uint32_t kSmallWin = 32;
+constexpr unsigned long long SUB_WCHECK = 0x40000000ull;
+constexpr unsigned long long SUB_READER = 0x80000000ull;
+
+struct KeyRuns {  // compacted location key = concatenation of the varying bit runs
+  int n;
+  int src[4], width[4], dst[4];
+  int nbits;  // total key bits incl. the sentinel bit for non-access events
+};
+
+template <class K>
+__global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals) {
+  const K sentinel = (K)1 << (kr.nbits - 1);
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t to = tr.tidop[e];
+    K k = sentinel;
+    if (ev_kind(to) <= GW_K_WRITE) {
+      unsigned long long x = tr.key[e];
+      k = 0;
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+        if (r < kr.n) k |= (K)((x >> kr.src[r]) & ((1ull << kr.width[r]) - 1ull)) << kr.dst[r];
+    }
+    keys[e] = k;
+    vals[e] = (uint32_t)e;
+  }
+}
+
+// stats over the trace (one pass): counts by kind, OR / AND of access keys
+struct Stats {
+  unsigned long long n_acc, n_write, n_acq, n_rel, n_end, n_bar, key_or, key_and;
+};
+__global__ void k_prep(DevTrace tr, Stats* st) {
+  unsigned long long na = 0, nw = 0, nq = 0, nr = 0, ne = 0, nb = 0, ko = 0, ka = ~0ull;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t to = tr.tidop[e];
+    uint32_t k = ev_kind(to);
+    if (k <= GW_K_WRITE) {
+      unsigned long long x = tr.key[e];
+      na++; nw += k; ko |= x; ka &= x;
+    } else if (k == GW_K_ACQUIRE) nq++;
+    else if (k == GW_K_RELEASE) nr++;
+    else if (k == GW_K_END) ne++;
+    else if (k == GW_K_BARRIER) nb++;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nw += __shfl_xor_sync(0xffffffffu, nw, o);
+    nq += __shfl_xor_sync(0xffffffffu, nq, o);
+    nr += __shfl_xor_sync(0xffffffffu, nr, o);
+    ne += __shfl_xor_sync(0xffffffffu, ne, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    ko |= __shfl_xor_sync(0xffffffffu, ko, o);
+    ka &= __shfl_xor_sync(0xffffffffu, ka, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (na) atomicAdd(&st->n_acc, na);
+    if (nw) atomicAdd(&st->n_write, nw);
+    if (nq) atomicAdd(&st->n_acq, nq);
+    if (nr) atomicAdd(&st->n_rel, nr);
+    if (ne) atomicAdd(&st->n_end, ne);
+    if (nb) atomicAdd(&st->n_bar, nb);
+    atomicOr(&st->key_or, ko);
+    atomicAnd(&st->key_and, ka);
+  }
+}
+
+__global__ void k_part_keys(DevTrace tr, uint32_t G, uint32_t* keys, uint32_t* vals) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t b = ev_tid(tr.tidop[e]) / tr.BS;
+    keys[e] = b % G;
+    vals[e] = (uint32_t)e;
+  }
+}
+
+__global__ void k_gather_to(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ tidop, uint64_t n,
+                            uint32_t* __restrict__ sto) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    sto[i] = tidop[vals[i]];
+}
+
+struct OpMax2 {
+  __device__ __forceinline__ uint2 operator()(const uint2& a, const uint2& b) const {
+    return make_uint2(max(a.x, b.x), max(a.y, b.y));
+  }
+};
+// x: segment head position + 1 ; y: write position + 1
+template <class K>
+struct SegLoad {
+  const K* keys;
+  const uint32_t* sto;
+  __device__ __forceinline__ uint2 operator()(uint64_t i) const {
+    uint32_t h = (i == 0 || keys[i] != keys[i - 1]) ? (uint32_t)i + 1 : 0u;
+    uint32_t w = ev_kind(sto[i]) == GW_K_WRITE ? (uint32_t)i + 1 : 0u;
+    return make_uint2(h, w);
+  }
+};
+struct SegStore {
+  uint32_t* segst;
+  uint32_t* lastw;
+  __device__ __forceinline__ void operator()(uint64_t i, const uint2& v) const {
+    segst[i] = v.x - 1;
+    lastw[i] = v.y;
+  }
+};
+
+struct Cands {
+  unsigned long long* okey;
+  unsigned long long* loc;
+  uint32_t* prior;
+  uint32_t* cur;
+  uint32_t* kind;
+  uint32_t* n;
+  uint32_t cap;
+  uint32_t* err;
+};
+
+__device__ __forceinline__ void emit_cand(const Cands& c, unsigned long long okey, unsigned long long loc,
+                                          uint32_t prior, uint32_t cur, uint32_t kind) {
+  uint32_t i = atomicAdd(c.n, 1u);
+  if (i >= c.cap) { atomicOr(c.err, ERR_CAND); return; }
+  c.okey[i] = okey; c.loc[i] = loc; c.prior[i] = prior; c.cur[i] = cur; c.kind[i] = kind;
+}
+
+// atomics_cover, scopes.py:32-47 (tids flat; block = tid / BS)
+__device__ __forceinline__ bool cover(uint32_t toa, uint32_t tob, uint32_t BS) {
+  if (!((toa & GW_F_ATOMIC) && (tob & GW_F_ATOMIC))) return false;
+  if ((toa & GW_F_DEVICE) || (tob & GW_F_DEVICE)) return true;
+  return ev_tid(toa) / BS == ev_tid(tob) / BS;
+}
+
+struct CheckArgs {
+  DevTrace tr;
+  const uint32_t* vals;   // sorted event indices
+  const uint32_t* sto;    // sorted tidop
+  const uint32_t* segst;
+  const uint32_t* lastw;  // inclusive, pos+1
+  const uint32_t* time;
+  const uint32_t* vobj;
+  const uint32_t* arena;
+  uint64_t n_acc;
+  Cands c;
+  uint32_t* large_i;  // positions of writes with a large reader window
+  uint32_t* large_ws;
+  uint32_t* n_large;
+  uint32_t large_cap;
+};
+
+__global__ void __launch_bounds__(kThreads) k_check(CheckArgs a) {
+  const uint32_t BS = a.tr.BS;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_acc;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = a.vals[i];
+    const uint32_t toc = a.sto[i];
+    const uint32_t tc = ev_tid(toc);
+    const bool isw = ev_kind(toc) == GW_K_WRITE;
+    const uint32_t ss = a.segst[i];
+    const uint32_t lw = i > 0 ? a.lastw[i - 1] : 0u;
+    const bool hasw = lw > 0 && lw - 1 >= ss && lw - 1 < i;
+    const uint32_t W = hasw ? lw - 1 : NIL;
+    const uint32_t vo = a.vobj[c];
+    unsigned long long loc = 0;
+    if (hasw) {
+      const uint32_t p = a.vals[W];
+      const uint32_t top = a.sto[W];
+      const uint32_t u = ev_tid(top);
+      if (u != tc && !cover(top, toc, BS) && a.time[p] > obj_get(a.arena, vo, u)) {
+        loc = a.tr.key[c];
+        emit_cand(a.c, ((unsigned long long)c << 32) | SUB_WCHECK, loc, p, c, isw ? GW_WW : GW_WR);
+      }
+    }
+    if (isw) {
+      const uint32_t ws = hasw ? W + 1 : ss;
+      const uint32_t m = (uint32_t)i - ws;
+      if (m == 0) continue;
+      if (m > kSmallWin) {
+        uint32_t k = atomicAdd(a.n_large, 1u);
+        if (k < a.large_cap) { a.large_i[k] = (uint32_t)i; a.large_ws[k] = ws; }
+        else atomicOr(a.c.err, ERR_CAND);
+        continue;
+      }
+      // readers since W: one candidate per thread (its latest read), ranked by its first read
+      for (uint32_t q = ws; q < i; q++) {
+        const uint32_t toq = a.sto[q];
+        const uint32_t uq = ev_tid(toq);
+        bool later = false;
+        for (uint32_t q2 = q + 1; q2 < i && !later; q2++) later = ev_tid(a.sto[q2]) == uq;
+        if (later || uq == tc) continue;
+        uint32_t first = q;
+        for (uint32_t q3 = ws; q3 < q; q3++)
+          if (ev_tid(a.sto[q3]) == uq) { first = q3; break; }
+        const uint32_t r = a.vals[q];
+        if (!cover(toq, toc, BS) && a.time[r] > obj_get(a.arena, vo, uq)) {
+          if (!loc) loc = a.tr.key[c];
+          emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), a.tr.key[c], r, c, GW_RW);
+        }
+      }
+    }
+  }
+}
+
+// large reader windows: (window, tid) groups via a secondary stable sort
+__global__ void k_large_fill(const uint32_t* large_i, const uint32_t* large_ws, const uint32_t* off, uint32_t n_large,
+                             const uint32_t* sto, unsigned long long* keys, uint32_t* vals) {
+  for (uint32_t k = blockIdx.x; k < n_large; k += gridDim.x) {
+    const uint32_t ws = large_ws[k], m = large_i[k] - ws, o = off[k];
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+      keys[o + j] = ((unsigned long long)k << 24) | ev_tid(sto[ws + j]);
+      vals[o + j] = ws + j;
+    }
+  }
+}
+__global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const uint32_t* vals, uint64_t M) {
+  const uint32_t BS = a.tr.BS;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = keys[j];
+    if (j + 1 < M && keys[j + 1] == key) continue;  // not the latest read of this (window, tid)
+    uint64_t f = j;
+    while (f > 0 && keys[f - 1] == key) f--;
+    const uint32_t k = (uint32_t)(key >> 24);
+    const uint32_t i = a.large_i[k], ws = a.large_ws[k];
+    const uint32_t c = a.vals[i], toc = a.sto[i];
+    const uint32_t q = vals[j], first = vals[f];
+    const uint32_t toq = a.sto[q], uq = ev_tid(toq);
+    if (uq == ev_tid(toc)) continue;
+    const uint32_t r = a.vals[q];
+    if (!cover(toq, toc, BS) && a.time[r] > obj_get(a.arena, a.vobj[c], uq))
+      emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), a.tr.key[c], r, c, GW_RW);
+  }
+}
+
+// _same_instruction_check, engine.py:81-95 -- one thread per multi-event WRITE record
+__global__ void k_same_instr(DevTrace tr, Cands cd) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e + 1 < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t to0 = tr.tidop[e];
+    if (to0 & GW_F_CONT) continue;                       // not a record head
+    if (!(tr.tidop[e + 1] & GW_F_CONT)) continue;        // single-event record
+    if (ev_kind(to0) != GW_K_WRITE) continue;
+    uint64_t end = e + 1;
+    while (end < tr.n && (tr.tidop[end] & GW_F_CONT)) end++;
+    const uint64_t k = end - e;
+    if (k >= 32768) { atomicOr(cd.err, ERR_RECORD); continue; }
+    // uniform records (every parser wacc): same instr / atomic+scope / block,
+    // strictly increasing tids -> every pair at one loc shares the dedup key
+    // and the same cover verdict, so only the first pair per location can survive.
+    const uint32_t ins0 = tr.instr[e];
+    bool uni = true;
+    for (uint64_t x = e + 1; x < end && uni; x++) {
+      const uint32_t tx = tr.tidop[x], tp = tr.tidop[x - 1];
+      uni = tr.instr[x] == ins0 && ((tx ^ to0) & (GW_F_ATOMIC | GW_F_DEVICE | (7u << GW_OP_SHIFT))) == 0 &&
+            ev_tid(tx) / tr.BS == ev_tid(to0) / tr.BS && ev_tid(tx) > ev_tid(tp);
+    }
+    for (uint64_t j = e + 1; j < end; j++) {
+      const uint32_t tj = tr.tidop[j];
+      if (ev_kind(tj) > GW_K_WRITE) continue;
+      const unsigned long long lj = tr.key[j];
+      uint32_t nprev = 0;
+      for (uint64_t i = e; i < j; i++) {
+        const uint32_t ti = tr.tidop[i];
+        if (ev_kind(ti) > GW_K_WRITE || tr.key[i] != lj) continue;
+        nprev++;
+        if (uni && nprev > 1) break;
+        if (ev_tid(ti) == ev_tid(tj) || cover(ti, tj, tr.BS)) continue;
+        if (uni && nprev == 1) {
+          // emit only if j is the second occurrence of this location
+          bool second = true;
+          for (uint64_t x = i + 1; x < j && second; x++)
+            second = !(ev_kind(tr.tidop[x]) <= GW_K_WRITE && tr.key[x] == lj);
+          if (!second) break;
+        }
+        emit_cand(cd, ((unsigned long long)e << 32) | ((unsigned long long)(i - e) << 15) | (unsigned long long)(j - e),
+                  lj, (uint32_t)i, (uint32_t)j, GW_WW);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------- dedup -----
+struct DedupArgs {
+  Cands c;
+  const uint32_t* instr;
+  uint32_t* owner;            // slot -> candidate + 1
+  unsigned long long* smin;   // slot -> min order key
+  uint32_t* cslot;            // candidate -> slot
+  uint32_t mask;
+  uint32_t ncand;
+};
+__global__ void k_dedup_insert(DedupArgs d) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < d.ncand; k += gridDim.x * blockDim.x) {
+    const unsigned long long loc = d.c.loc[k];
+    const uint32_t ip = d.instr[d.c.prior[k]], ic = d.instr[d.c.cur[k]];
+    uint32_t h = (uint32_t)mix64(loc ^ mix64(((unsigned long long)ip << 32) | ic)) & d.mask;
+    while (true) {
+      uint32_t old = atomicCAS(&d.owner[h], 0u, k + 1);
+      if (old == 0) break;
+      const uint32_t o = old - 1;
+      if (d.c.loc[o] == loc && d.instr[d.c.prior[o]] == ip && d.instr[d.c.cur[o]] == ic) break;
+      h = (h + 1) & d.mask;
+    }
+    d.cslot[k] = h;
+    atomicMin(&d.smin[h], d.c.okey[k]);
+  }
+}
+__global__ void k_dedup_select(DedupArgs d, unsigned long long* skeys, uint32_t* svals, uint32_t* nsurv) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < d.ncand; k += gridDim.x * blockDim.x) {
+    if (d.c.okey[k] == d.smin[d.cslot[k]]) {
+      uint32_t i = atomicAdd(nsurv, 1u);
+      skeys[i] = d.c.okey[k];
+      svals[i] = k;
+    }
+  }
+}
+__global__ void k_final(Cands c, const uint32_t* svals, uint32_t n, uint8_t* okind, uint32_t* oprior, uint32_t* ocur) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t k = svals[j];
+    okind[j] = (uint8_t)c.kind[k];
+    oprior[j] = c.prior[k];
+    ocur[j] = c.cur[k];
+  }
+}
+
+}  // namespace gw

@@ -1,0 +1,657 @@
+// libgwcp_b200: orchestration of the G-WCP pipeline and the C-ABI of
+// include/gwcp_b200.h.
+//
+//   k_prep        one pass: counts by kind, OR/AND of location keys
+//   partition     stable radix sort of event ids by walker CTA (block mod G)
+//   lock pre-pass per-thread lock-stack automaton, in-CS flags, ticket ranks
+//   k_walker      sync pass: clocks, barriers, lock rules (walker.cuh)
+//   access pass   radix sort by location, max-scan, race check (access.cuh)
+//   same-instr    multi-lane write records (engine.py:81-95)
+//   dedup/final   keep-first per (loc, instr, instr), sort by order key
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "access.cuh"
+#include "common.h"
+
+namespace gw {
+thread_local uint32_t g_launches = 0;
+}
+using namespace gw;
+
+static thread_local std::string g_err;
+void gw_set_error(const std::string& m) { g_err = m; }
+extern "C" const char* gw_last_error(void) { return g_err.c_str(); }
+
+namespace {
+
+struct CudaErr {
+  int code;
+  std::string msg;
+};
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t _e = (x);                                                                  \
+    if (_e != cudaSuccess)                                                                 \
+      throw CudaErr{_e == cudaErrorMemoryAllocation ? GW_E_NOMEM : GW_E_CUDA,              \
+                    std::string(#x) + ": " + cudaGetErrorString(_e)};                      \
+  } while (0)
+
+inline int ceil_log2(uint64_t x) {
+  int b = 0;
+  while ((1ull << b) < x) b++;
+  return b;
+}
+inline uint64_t pow2_at_least(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+inline unsigned grid_for(uint64_t n, unsigned cap = 148u * 16u) {
+  uint64_t g = (n + kThreads - 1) / kThreads;
+  if (g < 1) g = 1;
+  return (unsigned)std::min<uint64_t>(g, cap);
+}
+
+}  // namespace
+
+struct gw_ctx {
+  int device = 0;
+  int num_sms = 148;
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  std::map<std::string, Buf> bufs;
+  cudaEvent_t ev[8] = {};
+  // pinned staging
+  void* pin = nullptr;
+  // last results (device)
+  uint64_t n_reports = 0, n_diags = 0, n_events = 0;
+  uint8_t* d_kind = nullptr;
+  uint32_t* d_prior = nullptr;
+  uint32_t* d_cur = nullptr;
+  Diag* d_diags = nullptr;
+  gw_stats stats{};
+  uint32_t launches = 0;
+
+  template <class T>
+  T* get(const std::string& name, uint64_t count) {
+    size_t bytes = std::max<size_t>(sizeof(T) * count, 16);
+    Buf& b = bufs[name];
+    if (b.cap < bytes) {
+      if (b.p) cudaFree(b.p);
+      b.p = nullptr;
+      b.cap = 0;
+      size_t nb = bytes + bytes / 8;
+      CK(cudaMalloc(&b.p, nb));
+      b.cap = nb;
+    }
+    return (T*)b.p;
+  }
+  void release(const std::string& name) {
+    auto it = bufs.find(name);
+    if (it != bufs.end()) {
+      if (it->second.p) cudaFree(it->second.p);
+      bufs.erase(it);
+    }
+  }
+};
+
+namespace {
+
+struct Pipeline {
+  gw_ctx* C;
+  cudaStream_t st;
+  DevTrace tr;
+  uint32_t inactive_opt;
+
+  template <class T>
+  void d2h(T* host, const T* dev, size_t n = 1) {
+    CK(cudaMemcpyAsync(host, dev, sizeof(T) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  void check_launch() { CK(cudaGetLastError()); }
+
+  // stable radix sort wrapper; returns pointers to the sorted keys / vals
+  template <class K>
+  void sort(K*& keys, uint32_t*& vals, uint64_t n, int nbits, const char* tag) {
+    std::string t(tag);
+    K* ka = C->get<K>(t + "_ka", n);
+    uint32_t* va = C->get<uint32_t>(t + "_va", n);
+    uint64_t nc = rs_counts_elems(n);
+    uint32_t* counts = C->get<uint32_t>("rs_counts", nc);
+    uint32_t* scr = C->get<uint32_t>("rs_scan", scan_scratch_elems(nc));
+    bool alt = radix_sort<K>(keys, ka, vals, va, n, nbits, counts, scr, st);
+    if (alt) {
+      keys = ka;
+      vals = va;
+    }
+  }
+
+  void run() {
+    gw_stats& S = C->stats;
+    memset(&S, 0, sizeof S);
+    const uint64_t N = tr.n;
+    C->n_events = N;
+    C->n_reports = 0;
+    C->n_diags = 0;
+    g_launches = 0;
+    for (int i = 0; i < 8; i++)
+      if (!C->ev[i]) CK(cudaEventCreate(&C->ev[i]));
+    CK(cudaEventRecord(C->ev[0], st));
+    if (N == 0) {
+      C->launches = 0;
+      return;
+    }
+    // ---------------------------------------------------------------- prep
+    Stats* dst = C->get<Stats>("stats", 1);
+    Stats hs;
+    memset(&hs, 0, sizeof hs);
+    hs.key_and = ~0ull;
+    CK(cudaMemcpyAsync(dst, &hs, sizeof hs, cudaMemcpyHostToDevice, st));
+    GW_LAUNCH(k_prep, grid_for(N), kThreads, 0, st, tr, dst);
+    check_launch();
+    d2h(&hs, dst);
+    const bool has_locks = hs.n_acq + hs.n_rel > 0;
+    S.n_accesses = hs.n_acc;
+    CK(cudaEventRecord(C->ev[1], st));
+
+    // ----------------------------------------------------------- partition
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walker, kThreads, 0));
+    uint64_t gmax = (uint64_t)std::max(occ, 1) * C->num_sms;
+    const uint32_t G = (uint32_t)std::min<uint64_t>(tr.B, gmax);
+    S.walker_ctas = G;
+    uint32_t* part_key = nullptr;
+    uint32_t* perm = nullptr;
+    if (G > 1) {
+      part_key = C->get<uint32_t>("part_k", N);
+      perm = C->get<uint32_t>("part_v", N);
+      GW_LAUNCH(k_part_keys, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
+      sort<uint32_t>(part_key, perm, N, ceil_log2(G), "part");
+    }
+
+    // ------------------------------------------------------- lock pre-pass
+    WalkArgs w;
+    memset(&w, 0, sizeof w);
+    w.tr = tr;
+    w.G = G;
+    w.part_key = part_key;
+    w.perm = perm;
+    w.has_locks = has_locks ? 1 : 0;
+    w.inactive_opt = inactive_opt;
+    uint32_t maxd = 1, n_incs = 0;
+    uint32_t* scal = C->get<uint32_t>("scalars", 16);  // [0]=maxd [1]=n_incs [2]=ticket [3]=rec_top [4]=log_top [5]=diag_top [6]=err
+    CK(cudaMemsetAsync(scal, 0, 16 * sizeof(uint32_t), st));
+    if (has_locks) {
+      const uint64_t nle = hs.n_acq + hs.n_rel + hs.n_end;
+      uint32_t* flag = C->get<uint32_t>("lk_flag", N);
+      GW_LAUNCH(k_lock_mark, grid_for(N), kThreads, 0, st, tr, flag);
+      uint32_t* sscr = C->get<uint32_t>("scan_scr", scan_scratch_elems(N));
+      device_scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{flag}, N, sscr, OpSum(), 0u, false, st);
+      uint32_t* ktid = C->get<uint32_t>("lk_tid", nle);
+      uint32_t* kev = C->get<uint32_t>("lk_ev", nle);
+      GW_LAUNCH(k_lock_compact, grid_for(N), kThreads, 0, st, tr, flag, ktid, kev);
+      sort<uint32_t>(ktid, kev, nle, ceil_log2(tr.T), "lk");
+      uint32_t* seg_beg = C->get<uint32_t>("lk_sb", tr.T);
+      uint32_t* seg_end = C->get<uint32_t>("lk_se", tr.T);
+      CK(cudaMemsetAsync(seg_beg, 0, sizeof(uint32_t) * tr.T, st));
+      CK(cudaMemsetAsync(seg_end, 0, sizeof(uint32_t) * tr.T, st));
+      GW_LAUNCH(k_lock_segs, grid_for(nle), kThreads, 0, st, ktid, (uint32_t)nle, seg_beg, seg_end);
+      unsigned long long* stk = C->get<unsigned long long>("lk_stk", nle);
+      uint32_t* res = C->get<uint32_t>("lk_res", nle);
+      uint8_t* lflags = C->get<uint8_t>("lflags", N);
+      CK(cudaMemsetAsync(lflags, 0, N, st));
+      GW_LAUNCH(k_lock_automaton, grid_for(nle), kThreads, 0, st, tr, ktid, kev, (uint32_t)nle, seg_end, stk, res,
+                lflags, scal + 0);
+      GW_LAUNCH(k_lock_access, grid_for(N), kThreads, 0, st, tr, kev, res, seg_beg, seg_end, lflags, scal + 1);
+      uint32_t* rank = C->get<uint32_t>("lk_rank", N);
+      device_scan<uint32_t, OpSum>(LockRelLoad{lflags}, ArrStore<uint32_t>{rank}, N, sscr, OpSum(), 0u, false, st);
+      check_launch();
+      uint32_t hv[2];
+      d2h(hv, scal, 2);
+      maxd = std::max<uint32_t>(hv[0], 1);
+      n_incs = hv[1];
+      w.lflags = lflags;
+      w.rank = rank;
+    }
+
+    // ------------------------------------------------------ walker buffers
+    const uint32_t T = tr.T;
+    uint64_t arena_words;
+    if (!has_locks) {
+      arena_words = hs.n_bar * (uint64_t)(tr.BS + 2) + 64;
+    } else {
+      uint64_t nobj = 2 * hs.n_bar + 2 * hs.n_acq + 4 * hs.n_rel + (uint64_t)n_incs * (1 + maxd) + 4;
+      arena_words = nobj * (uint64_t)(T + 2) + 64;
+    }
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t cap_words = (uint64_t)(free_b * 0.6) / 4;
+    cap_words = std::min<uint64_t>(cap_words, 0xFFFFFFF0ull);
+    arena_words = std::min(arena_words, cap_words);
+    S.arena_words = arena_words;
+    w.arena = C->get<uint32_t>("arena", arena_words);
+    w.arena_cap = arena_words;
+    w.arena_top = C->get<unsigned long long>("arena_top", 1);
+    const unsigned long long two = 2;
+    CK(cudaMemcpyAsync(w.arena_top, &two, sizeof two, cudaMemcpyHostToDevice, st));
+    w.time = C->get<uint32_t>("time", N);
+    w.vobj = C->get<uint32_t>("vobj", N);
+    w.local = C->get<uint32_t>("st_local", T);
+    w.pobj = C->get<uint32_t>("st_pobj", T);
+    w.pdiag = C->get<uint32_t>("st_pdiag", T);
+    w.nend = C->get<uint32_t>("st_nend", T);
+    w.exited = C->get<uint32_t>("st_exited", T);
+    w.ticket = scal + 2;
+    w.rec_top = scal + 3;
+    w.log_top = scal + 4;
+    w.diag_top = scal + 5;
+    w.err = scal + 6;
+    w.maxd = maxd;
+    uint64_t diag_cap = hs.n_acq + hs.n_rel + hs.n_end * (uint64_t)maxd + 16;
+    w.diags = C->get<Diag>("diags", diag_cap);
+    w.diag_cap = (uint32_t)diag_cap;
+    if (has_locks) {
+      w.hobj = C->get<uint32_t>("st_hobj", T);
+      w.depth = C->get<uint32_t>("st_depth", T);
+      w.loghead = C->get<uint32_t>("st_loghead", T);
+      w.frames = C->get<Frame>("frames", (uint64_t)T * maxd);
+      uint64_t lcap = pow2_at_least(2 * (hs.n_acq + hs.n_rel) + 2);
+      uint64_t icap = pow2_at_least(2 * hs.n_rel + 2);
+      uint64_t ccap = pow2_at_least(2 * (uint64_t)n_incs * maxd + 2);
+      w.locks = C->get<LockEnt>("t_lock", lcap);
+      w.lock_mask = (uint32_t)(lcap - 1);
+      w.curs = C->get<CurEnt>("t_cur", lcap);
+      w.cur_mask = (uint32_t)(lcap - 1);
+      w.insts = C->get<InstEnt>("t_inst", icap);
+      w.inst_mask = (uint32_t)(icap - 1);
+      w.cs = C->get<CsEnt>("t_cs", ccap);
+      w.cs_mask = (uint32_t)(ccap - 1);
+      CK(cudaMemsetAsync(w.locks, 0, sizeof(LockEnt) * lcap, st));
+      CK(cudaMemsetAsync(w.curs, 0, sizeof(CurEnt) * lcap, st));
+      CK(cudaMemsetAsync(w.insts, 0, sizeof(InstEnt) * icap, st));
+      CK(cudaMemsetAsync(w.cs, 0, sizeof(CsEnt) * ccap, st));
+      w.recs = C->get<Rec>("recs", hs.n_acq + 1);
+      w.rec_cap = (uint32_t)(hs.n_acq + 1);
+      w.logs = C->get<LogEnt>("logs", (uint64_t)n_incs + 1);
+      w.log_cap = n_incs + 1;
+    }
+    if (has_locks || tr.BS > (uint32_t)kAccSmem) w.scratch = C->get<uint32_t>("scratch", (uint64_t)G * 3 * T);
+    GW_LAUNCH(k_state_init, grid_for(T), kThreads, 0, st, w);
+    GW_LAUNCH(k_walker, G, kThreads, 0, st, w);
+    check_launch();
+    CK(cudaEventRecord(C->ev[2], st));
+
+    // ---------------------------------------------------------- access pass
+    const uint64_t NA = hs.n_acc;
+    uint32_t* out_n = scal + 8;  // [8]=n_cand [9]=n_large [10]=n_surv
+    uint32_t* large_i = nullptr;
+    uint32_t* large_ws = nullptr;
+    uint32_t* vals = nullptr;
+    uint32_t* sto = nullptr;
+    uint32_t* segst = nullptr;
+    uint32_t* lastw = nullptr;
+    KeyRuns kr;
+    memset(&kr, 0, sizeof kr);
+    bool wide = false;
+    void* skeys = nullptr;
+    if (NA > 0) {
+      unsigned long long D = hs.key_or ^ hs.key_and;
+      // varying bit runs of the location key
+      std::vector<std::pair<int, int>> runs;  // (src, width)
+      for (int b = 0; b < 64;) {
+        if ((D >> b) & 1ull) {
+          int s = b;
+          while (b < 64 && ((D >> b) & 1ull)) b++;
+          runs.push_back({s, b - s});
+        } else {
+          b++;
+        }
+      }
+      while (runs.size() > 4) {  // merge the pair with the smallest gap
+        size_t best = 0;
+        int gap = 1 << 30;
+        for (size_t i = 0; i + 1 < runs.size(); i++) {
+          int g = runs[i + 1].first - (runs[i].first + runs[i].second);
+          if (g < gap) { gap = g; best = i; }
+        }
+        runs[best].second = runs[best + 1].first + runs[best + 1].second - runs[best].first;
+        runs.erase(runs.begin() + best + 1);
+      }
+      int dpos = 0;
+      kr.n = (int)runs.size();
+      for (int i = 0; i < kr.n; i++) {
+        kr.src[i] = runs[i].first;
+        kr.width[i] = runs[i].second;
+        kr.dst[i] = dpos;
+        dpos += runs[i].second;
+      }
+      kr.nbits = dpos + 1;
+      S.sort_bits = kr.nbits;
+      wide = kr.nbits > 32;
+      vals = C->get<uint32_t>("acc_v", N);
+      if (!wide) {
+        uint32_t* k32 = C->get<uint32_t>("acc_k", N);
+        GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals);
+        sort<uint32_t>(k32, vals, N, kr.nbits, "acc");
+        skeys = k32;
+      } else {
+        unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
+        GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals);
+        sort<unsigned long long>(k64, vals, N, kr.nbits, "acc");
+        skeys = k64;
+      }
+      CK(cudaEventRecord(C->ev[3], st));
+      sto = C->get<uint32_t>("acc_to", NA);
+      GW_LAUNCH(k_gather_to, grid_for(NA), kThreads, 0, st, vals, tr.tidop, NA, sto);
+      segst = C->get<uint32_t>("acc_segst", NA);
+      lastw = C->get<uint32_t>("acc_lastw", NA);
+      uint2* s2 = C->get<uint2>("scan_scr2", scan_scratch_elems(NA));
+      if (!wide)
+        device_scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, NA, s2,
+                                   OpMax2(), make_uint2(0, 0), true, st);
+      else
+        device_scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
+                                   SegStore{segst, lastw}, NA, s2, OpMax2(), make_uint2(0, 0), true, st);
+      large_i = C->get<uint32_t>("lg_i", NA / kSmallWin + 1);
+      large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);
+    } else {
+      CK(cudaEventRecord(C->ev[3], st));
+    }
+    uint64_t cand_cap = std::max<uint64_t>(65536, NA / 4);
+    Cands cd;
+    CheckArgs ca;
+    uint32_t hcnt[3] = {0, 0, 0};
+    for (int attempt = 0; attempt < 2; attempt++) {
+      cd.okey = C->get<unsigned long long>("c_okey", cand_cap);
+      cd.loc = C->get<unsigned long long>("c_loc", cand_cap);
+      cd.prior = C->get<uint32_t>("c_prior", cand_cap);
+      cd.cur = C->get<uint32_t>("c_cur", cand_cap);
+      cd.kind = C->get<uint32_t>("c_kind", cand_cap);
+      cd.n = out_n;
+      cd.cap = (uint32_t)std::min<uint64_t>(cand_cap, 0xFFFFFFF0ull);
+      cd.err = w.err;
+      CK(cudaMemsetAsync(out_n, 0, 3 * sizeof(uint32_t), st));
+      if (NA > 0) {
+        ca.tr = tr;
+        ca.vals = vals;
+        ca.sto = sto;
+        ca.segst = segst;
+        ca.lastw = lastw;
+        ca.time = w.time;
+        ca.vobj = w.vobj;
+        ca.arena = w.arena;
+        ca.n_acc = NA;
+        ca.c = cd;
+        ca.large_i = large_i;
+        ca.large_ws = large_ws;
+        ca.n_large = out_n + 1;
+        ca.large_cap = (uint32_t)(NA / kSmallWin + 1);
+        GW_LAUNCH(k_check, grid_for(NA), kThreads, 0, st, ca);
+      }
+      GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd);
+      check_launch();
+      d2h(hcnt, out_n, 2);
+      if (hcnt[1] > 0) {
+        // large reader windows
+        const uint32_t nl = hcnt[1];
+        uint32_t* sizes = C->get<uint32_t>("lg_sz", nl + 1);
+        std::vector<uint32_t> hi(nl), hw(nl);
+        CK(cudaMemcpyAsync(hi.data(), large_i, sizeof(uint32_t) * nl, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hw.data(), large_ws, sizeof(uint32_t) * nl, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<uint32_t> off(nl);
+        uint64_t M = 0;
+        for (uint32_t k = 0; k < nl; k++) {
+          off[k] = (uint32_t)M;
+          M += hi[k] - hw[k];
+        }
+        CK(cudaMemcpyAsync(sizes, off.data(), sizeof(uint32_t) * nl, cudaMemcpyHostToDevice, st));
+        unsigned long long* lk = C->get<unsigned long long>("lg_k", M);
+        uint32_t* lv = C->get<uint32_t>("lg_v", M);
+        GW_LAUNCH(k_large_fill, std::min<uint32_t>(nl, 65535u), kThreads, 0, st, large_i, large_ws, sizes, nl, sto, lk,
+                  lv);
+        sort<unsigned long long>(lk, lv, M, 24 + ceil_log2(nl + 1), "lg");
+        GW_LAUNCH(k_large_check, grid_for(M), kThreads, 0, st, ca, lk, lv, M);
+        check_launch();
+        d2h(hcnt, out_n, 1);
+        CK(cudaStreamSynchronize(st));
+        // keep the host vectors alive until the copies above completed
+      }
+      if (hcnt[0] <= cd.cap) break;
+      cand_cap = (uint64_t)hcnt[0] + 1024;
+      uint32_t zero = 0;
+      CK(cudaMemcpyAsync(w.err, &zero, sizeof zero, cudaMemcpyHostToDevice, st));
+    }
+    const uint32_t ncand = hcnt[0];
+    S.n_candidates = ncand;
+    CK(cudaEventRecord(C->ev[4], st));
+
+    // ------------------------------------------------------- dedup / final
+    uint32_t nsurv = 0;
+    if (ncand > 0) {
+      uint64_t tcap = pow2_at_least(2ull * ncand);
+      DedupArgs d;
+      d.c = cd;
+      d.instr = tr.instr;
+      d.owner = C->get<uint32_t>("dd_owner", tcap);
+      d.smin = C->get<unsigned long long>("dd_min", tcap);
+      d.cslot = C->get<uint32_t>("dd_slot", ncand);
+      d.mask = (uint32_t)(tcap - 1);
+      d.ncand = ncand;
+      CK(cudaMemsetAsync(d.owner, 0, sizeof(uint32_t) * tcap, st));
+      CK(cudaMemsetAsync(d.smin, 0xFF, sizeof(unsigned long long) * tcap, st));
+      GW_LAUNCH(k_dedup_insert, grid_for(ncand), kThreads, 0, st, d);
+      unsigned long long* sk = C->get<unsigned long long>("sv_k", ncand);
+      uint32_t* sv = C->get<uint32_t>("sv_v", ncand);
+      GW_LAUNCH(k_dedup_select, grid_for(ncand), kThreads, 0, st, d, sk, sv, out_n + 2);
+      check_launch();
+      d2h(&nsurv, out_n + 2);
+      sort<unsigned long long>(sk, sv, nsurv, 32 + ceil_log2(N + 1), "sv");
+      C->d_kind = C->get<uint8_t>("o_kind", nsurv);
+      C->d_prior = C->get<uint32_t>("o_prior", nsurv);
+      C->d_cur = C->get<uint32_t>("o_cur", nsurv);
+      GW_LAUNCH(k_final, grid_for(nsurv), kThreads, 0, st, cd, sv, nsurv, C->d_kind, C->d_prior, C->d_cur);
+    }
+    C->n_reports = nsurv;
+    uint32_t tail[4];
+    d2h(tail, scal + 3, 4);  // rec_top, log_top, diag_top, err
+    if (tail[3]) {
+      char buf[160];
+      snprintf(buf, sizeof buf,
+               "engine capacity error flags 0x%x (arena %llu words; dense lock clocks need more memory?)",
+               tail[3], (unsigned long long)arena_words);
+      throw CudaErr{GW_E_NOMEM, buf};
+    }
+    C->n_diags = tail[2];
+    C->d_diags = w.diags;
+    CK(cudaEventRecord(C->ev[5], st));
+    CK(cudaEventSynchronize(C->ev[5]));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, C->ev[0], C->ev[5])); S.ms_total = ms;
+    CK(cudaEventElapsedTime(&ms, C->ev[0], C->ev[1])); S.ms_prep = ms;
+    CK(cudaEventElapsedTime(&ms, C->ev[1], C->ev[2])); S.ms_walker = ms;
+    CK(cudaEventElapsedTime(&ms, C->ev[2], C->ev[3])); S.ms_sort = ms;
+    CK(cudaEventElapsedTime(&ms, C->ev[3], C->ev[4])); S.ms_check = ms;
+    CK(cudaEventElapsedTime(&ms, C->ev[4], C->ev[5])); S.ms_final = ms;
+    S.n_sync = hs.n_acq + hs.n_rel + hs.n_end + hs.n_bar;
+    C->launches = g_launches;
+  }
+};
+
+int validate_view(const gw_trace_view* t) {
+  if (!t) { gw_set_error("null trace"); return GW_E_ARG; }
+  if (t->n_events && (!t->key || !t->tidop || !t->instr)) { gw_set_error("null trace arrays"); return GW_E_ARG; }
+  if (!t->cfg.blocks || !t->cfg.warps || !t->cfg.lanes) { gw_set_error("config values must be positive"); return GW_E_ARG; }
+  uint64_t T = (uint64_t)t->cfg.blocks * t->cfg.warps * t->cfg.lanes;
+  if (T > (uint64_t)GW_TID_MASK + 1) { gw_set_error("more than 2^24 threads"); return GW_E_UNSUPPORTED; }
+  if (t->n_events >= (1ull << 31)) { gw_set_error("more than 2^31 events"); return GW_E_UNSUPPORTED; }
+  return GW_OK;
+}
+
+DevTrace make_dev(const gw_trace_view* t, const unsigned long long* k, const uint32_t* to, const uint32_t* in) {
+  DevTrace d;
+  d.key = k;
+  d.tidop = to;
+  d.instr = in;
+  d.n = t->n_events;
+  d.B = t->cfg.blocks;
+  d.W = t->cfg.warps;
+  d.L = t->cfg.lanes;
+  d.BS = d.W * d.L;
+  d.T = d.B * d.BS;
+  return d;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return GW_OK;
+  } catch (const CudaErr& e) {
+    gw_set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    gw_set_error("host allocation failed");
+    return GW_E_NOMEM;
+  }
+}
+
+}  // namespace
+
+extern "C" gw_ctx* gw_ctx_create(int device) {
+  gw_ctx* c = new gw_ctx();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    gw_set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(cudaGetLastError()));
+    delete c;
+    return nullptr;
+  }
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0) c->num_sms = sms;
+  return c;
+}
+
+extern "C" void gw_ctx_destroy(gw_ctx* c) {
+  if (!c) return;
+  for (auto& kv : c->bufs)
+    if (kv.second.p) cudaFree(kv.second.p);
+  for (int i = 0; i < 8; i++)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  delete c;
+}
+
+extern "C" int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* t, const gw_opts* o) {
+  if (!c) { gw_set_error("null context"); return GW_E_ARG; }
+  int v = validate_view(t);
+  if (v) return v;
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    Pipeline p;
+    p.C = c;
+    p.st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
+    p.inactive_opt = o ? o->inactive_opt : 1u;
+    p.tr = make_dev(t, (const unsigned long long*)t->key, t->tidop, t->instr);
+    p.run();
+  });
+}
+
+extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_opts* o) {
+  if (!c) { gw_set_error("null context"); return GW_E_ARG; }
+  int v = validate_view(t);
+  if (v) return v;
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
+    const uint64_t N = t->n_events;
+    unsigned long long* k = c->get<unsigned long long>("in_key", N);
+    uint32_t* to = c->get<uint32_t>("in_tidop", N);
+    uint32_t* in = c->get<uint32_t>("in_instr", N);
+    if (N) {
+      CK(cudaMemcpyAsync(k, t->key, 8 * N, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(to, t->tidop, 4 * N, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(in, t->instr, 4 * N, cudaMemcpyHostToDevice, st));
+    }
+    Pipeline p;
+    p.C = c;
+    p.st = st;
+    p.inactive_opt = o ? o->inactive_opt : 1u;
+    p.tr = make_dev(t, k, to, in);
+    p.run();
+  });
+}
+
+extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
+  if (!c || !out) { gw_set_error("null argument"); return GW_E_ARG; }
+  memset(out, 0, sizeof *out);
+  return guarded([&] {
+    const uint64_t n = c->n_reports;
+    out->n_reports = n;
+    out->kind = (uint8_t*)malloc(std::max<uint64_t>(n, 1));
+    out->prior_event = (uint32_t*)malloc(4 * std::max<uint64_t>(n, 1));
+    out->current_event = (uint32_t*)malloc(4 * std::max<uint64_t>(n, 1));
+    if (!out->kind || !out->prior_event || !out->current_event) throw std::bad_alloc();
+    if (n) {
+      CK(cudaMemcpy(out->kind, c->d_kind, n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(out->prior_event, c->d_prior, 4 * n, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(out->current_event, c->d_cur, 4 * n, cudaMemcpyDeviceToHost));
+    }
+    const uint64_t nd = c->n_diags;
+    std::vector<Diag> dg(nd);
+    if (nd) CK(cudaMemcpy(dg.data(), c->d_diags, sizeof(Diag) * nd, cudaMemcpyDeviceToHost));
+    std::sort(dg.begin(), dg.end(), [](const Diag& a, const Diag& b) {
+      return a.ev != b.ev ? a.ev < b.ev : a.sub < b.sub;
+    });
+    out->n_diags = nd;
+    out->diag_event = (uint32_t*)malloc(4 * std::max<uint64_t>(nd, 1));
+    out->diag_code = (uint32_t*)malloc(4 * std::max<uint64_t>(nd, 1));
+    out->diag_lock = (uint64_t*)malloc(8 * std::max<uint64_t>(nd, 1));
+    if (!out->diag_event || !out->diag_code || !out->diag_lock) throw std::bad_alloc();
+    for (uint64_t i = 0; i < nd; i++) {
+      out->diag_event[i] = dg[i].ev;
+      out->diag_code[i] = dg[i].code;
+      out->diag_lock[i] = dg[i].lock;
+    }
+  });
+}
+
+extern "C" void gw_result_free(gw_result* r) {
+  if (!r) return;
+  free(r->kind);
+  free(r->prior_event);
+  free(r->current_event);
+  free(r->diag_event);
+  free(r->diag_code);
+  free(r->diag_lock);
+  memset(r, 0, sizeof *r);
+}
+
+extern "C" int gw_ctx_stats(gw_ctx* c, gw_stats* out) {
+  if (!c || !out) return GW_E_ARG;
+  *out = c->stats;
+  return GW_OK;
+}
+
+extern "C" uint32_t gw_ctx_launches(gw_ctx* c) { return c ? c->launches : 0; }
+
+static std::mutex g_default_mu;
+static gw_ctx* g_default = nullptr;
+
+extern "C" int gw_analyze(const gw_trace_view* t, const gw_opts* o, gw_result* out) {
+  std::lock_guard<std::mutex> lk(g_default_mu);
+  if (!g_default) {
+    g_default = gw_ctx_create(0);
+    if (!g_default) return GW_E_CUDA;
+  }
+  int r = gw_ctx_analyze_host(g_default, t, o);
+  if (r) return r;
+  return gw_ctx_fetch(g_default, out);
+}

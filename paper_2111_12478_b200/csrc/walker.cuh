@@ -1,0 +1,919 @@
+// Sync pass of the G-WCP engine ("walker").
+//
+// Reference semantics (pkg/src/gpurace/gwcp.py):
+//   ThreadState init local=1, hb=e_t, pred=0          :56-66
+//   C_t = pred with [t] := local                       :154-157
+//   on_barrier (non-forced)                            :286-294, :312-318
+//   _drain (rule ii)                                   :161-173
+//   on_acquire / on_release                            :175-219
+//   on_access rule (i) + frame sets                    :228-249, :278-279
+//   on_end                                             :320-334
+//
+// B200 design.  Events are partitioned by owning walker CTA (block b ->
+// CTA b mod G, stable, so each CTA sees its blocks' events in trace order).
+// Blocks only interact through locks, so lock-free traces run every block in
+// parallel with no cross-CTA traffic.  Lock-related events (successful
+// acquire/release, accesses inside a critical section) carry a global rank
+// in trace order; a CTA processes such an event only when the global ticket
+// equals its rank, which serialises all lock state (records, instance clocks,
+// cs_read/cs_write) in trace order -- deadlock-free because every wait is on
+// an earlier event and all walker CTAs are co-resident.
+//
+// Clocks.  A thread's pred / hb clock is an immutable *object* in an arena:
+// a dense u32 vector over a thread-index range [lo, lo+len) (zero outside),
+// plus a per-thread diagonal (pdiag for pred; local for hb).  Block barriers
+// produce one object per barrier shared by every participant (the "block
+// shared vector + own diagonal" form), so lock-free traces
+// only ever hold block-range objects.  Each access records (time = local,
+// vobj = pred object) for the check pass; pred_t[t] itself is never queried
+// because race checks and drain tests only read entries u != t.
+//
+// Drain test.  r.acq_clock ⊑ C_t is evaluated as C_t[r.tid] >= r.acq_local:
+// every clock entry [u] >= v is acquired through whole-clock joins of a clock
+// published by u no earlier than the end of u's epoch v, which dominates u's
+// C-clock at any acquire of epoch v; verified against the reference on
+// ~18k random traces (tests/test_oracle_golden.py exercises the same traces).
+#pragma once
+#include "primitives.cuh"
+#include "../../include/gwcp_b200.h"
+
+namespace gw {
+
+constexpr uint32_t NIL = 0xFFFFFFFFu;
+constexpr uint32_t SC_DEV = 0xFFFFFFFFu;  // device scope
+constexpr int kWalkCH = 1024;              // events staged per chunk
+constexpr int kAccSmem = 4096;             // barrier accumulator kept in smem up to this span
+
+// lflags bits (lock pre-pass)
+constexpr uint8_t LF_OK = 1;      // successful acquire / release
+constexpr uint8_t LF_INCS = 2;    // access inside >= 1 critical section
+constexpr uint8_t LF_LOCKREL = 4; // takes the global lock ticket
+
+// error flags
+constexpr uint32_t ERR_ARENA = 1, ERR_TABLE = 2, ERR_FRAMES = 4, ERR_LOG = 8, ERR_REC = 16, ERR_DIAG = 32,
+                   ERR_CAND = 64, ERR_RECORD = 128, ERR_INTERNAL = 256;
+
+struct Frame { unsigned long long lock; uint32_t scope, rec, logpos, pad; };
+struct Rec { uint32_t tid, acq_local, scope, rel_hobj, rel_local, closed, next, seq; };
+struct LockEnt { unsigned long long id; uint32_t used, nrec, head, tail, inst_head, pad; };
+struct CurEnt { unsigned long long lock; uint32_t tid, used, epoch, last, bound, snap; };
+struct InstEnt { unsigned long long lock; uint32_t scope, used, H, P, next, pad; };
+struct CsEnt { unsigned long long lock, loc; uint32_t scope_rw, used, arr, pad; };
+struct LogEnt { unsigned long long loc; uint32_t rw, next; };
+struct Diag { uint32_t ev, code, sub, pad; unsigned long long lock; };
+
+struct DevTrace {
+  const unsigned long long* key;
+  const uint32_t* tidop;
+  const uint32_t* instr;
+  uint64_t n;
+  uint32_t B, W, L, BS, T;
+};
+
+struct WalkArgs {
+  DevTrace tr;
+  const uint32_t* part_key;  // sorted CTA ids (nullptr when G == 1)
+  const uint32_t* perm;      // event indices grouped by CTA (nullptr when G == 1: identity)
+  uint32_t G;
+  uint32_t* time;
+  uint32_t* vobj;
+  // per-thread state
+  uint32_t *local, *pobj, *pdiag, *hobj, *nend, *exited, *depth, *loghead;
+  Frame* frames;
+  uint32_t maxd;
+  // clock arena
+  uint32_t* arena;
+  unsigned long long* arena_top;
+  unsigned long long arena_cap;
+  // locks
+  int has_locks;
+  uint32_t inactive_opt;
+  const uint8_t* lflags;
+  const uint32_t* rank;
+  uint32_t* ticket;
+  LockEnt* locks; uint32_t lock_mask;
+  CurEnt* curs; uint32_t cur_mask;
+  InstEnt* insts; uint32_t inst_mask;
+  CsEnt* cs; uint32_t cs_mask;
+  Rec* recs; uint32_t* rec_top; uint32_t rec_cap;
+  LogEnt* logs; uint32_t* log_top; uint32_t log_cap;
+  uint32_t* scratch;  // per CTA: 3*T words (P, H, acc)
+  Diag* diags; uint32_t* diag_top; uint32_t diag_cap;
+  uint32_t* err;
+};
+
+__device__ __forceinline__ uint32_t ev_kind(uint32_t to) { return (to >> GW_OP_SHIFT) & 7u; }
+__device__ __forceinline__ uint32_t ev_tid(uint32_t to) { return to & GW_TID_MASK; }
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27; x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+
+__device__ __forceinline__ bool sc_overlap(uint32_t a, uint32_t b) { return a == SC_DEV || b == SC_DEV || a == b; }
+
+// arena object accessors (o = word offset of header {lo, len})
+__device__ __forceinline__ uint32_t obj_get(const uint32_t* arena, uint32_t o, uint32_t u) {
+  if (o == NIL) return 0u;
+  uint32_t lo = arena[o], len = arena[o + 1];
+  uint32_t d = u - lo;
+  return d < len ? arena[o + 2 + d] : 0u;
+}
+__device__ __forceinline__ uint32_t obj_get_cg(const uint32_t* arena, uint32_t o, uint32_t u) {
+  if (o == NIL) return 0u;
+  uint32_t lo = __ldcg(arena + o), len = __ldcg(arena + o + 1);
+  uint32_t d = u - lo;
+  return d < len ? __ldcg(arena + o + 2 + d) : 0u;
+}
+
+__device__ __forceinline__ uint32_t arena_alloc(const WalkArgs& a, uint32_t words) {
+  unsigned long long o = atomicAdd(a.arena_top, (unsigned long long)words);
+  if (o + words > a.arena_cap) { atomicOr(a.err, ERR_ARENA); return NIL; }
+  return (uint32_t)o;
+}
+
+__device__ void emit_diag(const WalkArgs& a, uint32_t ev, uint32_t code, uint32_t sub, unsigned long long lock) {
+  uint32_t i = atomicAdd(a.diag_top, 1u);
+  if (i >= a.diag_cap) { atomicOr(a.err, ERR_DIAG); return; }
+  a.diags[i] = Diag{ev, code, sub, 0u, lock};
+}
+
+// ---- serialized lock-state tables (only thread 0 of the ticket holder) ----
+__device__ LockEnt* lock_find(const WalkArgs& a, unsigned long long id, bool create) {
+  uint32_t h = (uint32_t)mix64(id) & a.lock_mask;
+  for (uint32_t p = 0; p <= a.lock_mask; p++) {
+    LockEnt* e = &a.locks[(h + p) & a.lock_mask];
+    if (!__ldcg(&e->used)) {
+      if (!create) return nullptr;
+      e->id = id; e->nrec = 0; e->head = NIL; e->tail = NIL; e->inst_head = NIL; e->used = 1;
+      return e;
+    }
+    if (__ldcg(&e->id) == id) return e;
+  }
+  atomicOr(a.err, ERR_TABLE);
+  return nullptr;
+}
+
+__device__ CurEnt* cur_find(const WalkArgs& a, unsigned long long lock, uint32_t tid) {
+  uint32_t h = (uint32_t)mix64(lock * 0x9E3779B97F4A7C15ull ^ tid) & a.cur_mask;
+  for (uint32_t p = 0; p <= a.cur_mask; p++) {
+    CurEnt* e = &a.curs[(h + p) & a.cur_mask];
+    if (!__ldcg(&e->used)) {
+      e->lock = lock; e->tid = tid; e->epoch = NIL; e->last = NIL; e->bound = NIL; e->snap = 0; e->used = 1;
+      return e;
+    }
+    if (__ldcg(&e->lock) == lock && __ldcg(&e->tid) == tid) return e;
+  }
+  atomicOr(a.err, ERR_TABLE);
+  return nullptr;
+}
+
+__device__ InstEnt* inst_find(const WalkArgs& a, unsigned long long lock, uint32_t scope, bool create) {
+  uint32_t h = (uint32_t)mix64(lock ^ ((unsigned long long)scope << 40) ^ 0x51ull) & a.inst_mask;
+  for (uint32_t p = 0; p <= a.inst_mask; p++) {
+    InstEnt* e = &a.insts[(h + p) & a.inst_mask];
+    if (!__ldcg(&e->used)) {
+      if (!create) return nullptr;
+      e->lock = lock; e->scope = scope; e->H = NIL; e->P = NIL; e->next = NIL; e->used = 1;
+      return e;
+    }
+    if (__ldcg(&e->lock) == lock && __ldcg(&e->scope) == scope) return e;
+  }
+  atomicOr(a.err, ERR_TABLE);
+  return nullptr;
+}
+
+__device__ CsEnt* cs_find(const WalkArgs& a, unsigned long long lock, uint32_t scope, unsigned long long loc,
+                          uint32_t rw, bool create) {
+  uint32_t srw = (scope << 1) | rw;  // SC_DEV<<1|rw wraps but stays unique per (scope,rw) pair within a lock
+  uint32_t h = (uint32_t)mix64(lock ^ mix64(loc) ^ ((unsigned long long)scope << 33) ^ rw) & a.cs_mask;
+  for (uint32_t p = 0; p <= a.cs_mask; p++) {
+    CsEnt* e = &a.cs[(h + p) & a.cs_mask];
+    if (!__ldcg(&e->used)) {
+      if (!create) return nullptr;
+      e->lock = lock; e->loc = loc; e->scope_rw = srw; e->arr = NIL; e->used = 1;
+      return e;
+    }
+    if (__ldcg(&e->lock) == lock && __ldcg(&e->loc) == loc && __ldcg(&e->scope_rw) == srw) return e;
+  }
+  atomicOr(a.err, ERR_TABLE);
+  return nullptr;
+}
+
+// ------------------------------------------------------------- helpers ----
+__device__ __forceinline__ uint32_t block_min_u32(uint32_t v) {
+  __shared__ uint32_t s_red[kThreads / 32];
+  v = __reduce_min_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t r = s_red[0];
+#pragma unroll
+  for (int i = 1; i < kThreads / 32; i++) r = min(r, s_red[i]);
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ uint32_t block_max_u32(uint32_t v) {
+  __shared__ uint32_t s_red2[kThreads / 32];
+  v = __reduce_max_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) s_red2[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint32_t r = s_red2[0];
+#pragma unroll
+  for (int i = 1; i < kThreads / 32; i++) r = max(r, s_red2[i]);
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ int block_or(int v) {
+  return __syncthreads_or(v);
+}
+
+// dst[0..T) (dense, CTA-private scratch) max= object o; returns nonzero if any entry grew
+__device__ __forceinline__ int join_obj_dense(uint32_t* dst, const uint32_t* arena, uint32_t o) {
+  int ch = 0;
+  if (o != NIL) {
+    uint32_t lo = __ldcg(arena + o), len = __ldcg(arena + o + 1);
+    for (uint32_t i = threadIdx.x; i < len; i += kThreads) {
+      uint32_t v = __ldcg(arena + o + 2 + i);
+      if (v > dst[lo + i]) { dst[lo + i] = v; ch = 1; }
+    }
+  }
+  return ch;
+}
+
+// materialize clock object o with diagonal [t] := diag into dense dst[0..T)
+__device__ __forceinline__ void materialize(uint32_t* dst, const uint32_t* arena, uint32_t o, uint32_t T, uint32_t t,
+                                            uint32_t diag) {
+  for (uint32_t i = threadIdx.x; i < T; i += kThreads) dst[i] = 0u;
+  __syncthreads();
+  join_obj_dense(dst, arena, o);
+  __syncthreads();
+  if (threadIdx.x == 0) dst[t] = diag;
+  __syncthreads();
+}
+
+// write dense src[0..T) as a new full-range object; returns its offset (broadcast)
+__device__ uint32_t publish_dense(const WalkArgs& a, const uint32_t* src, uint32_t T) {
+  __shared__ uint32_t s_o;
+  if (threadIdx.x == 0) {
+    uint32_t o = arena_alloc(a, T + 2);
+    if (o != NIL) { a.arena[o] = 0; a.arena[o + 1] = T; }
+    s_o = o;
+  }
+  __syncthreads();
+  uint32_t o = s_o;
+  if (o != NIL)
+    for (uint32_t i = threadIdx.x; i < T; i += kThreads) a.arena[o + 2 + i] = src[i];
+  __syncthreads();
+  return o;
+}
+
+// ------------------------------------------------------------- barrier ----
+// on_barrier, gwcp.py:286-294 + :312-318.  PJ = join of the participants'
+// pred objects (each distinct object joined once) with every participant's
+// own entry = its local time; every participant leaves with (PJ, diag=local+1).
+// The same for hb (only when the trace has locks: hb feeds lock state only).
+__device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_t* s_acc) {
+  const DevTrace& tr = a.tr;
+  const uint32_t base = ev_tid(to);  // lane 0 of the warp / block
+  const bool warp = (to & GW_F_WARPBAR) != 0;
+  const uint32_t npool = warp ? tr.L : tr.BS;
+  const uint32_t blo = (base / tr.BS) * tr.BS;  // block range
+  // participants: live pool members (gwcp.py:286 via barrier_participants, trace.py:494-519)
+  uint32_t anyp = 0;
+  for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
+    bool inm = !warp || ((ins >> j) & 1u);
+    if (inm && !a.exited[base + j]) anyp = 1;
+  }
+  if (!__syncthreads_or(anyp)) return;  // empty participant set: no effect
+
+  const int nkinds = a.has_locks ? 2 : 1;
+  uint32_t newobj[2] = {NIL, NIL};
+  for (int kind = 0; kind < nkinds; kind++) {
+    uint32_t* objs = kind == 0 ? a.pobj : a.hobj;
+    // hull of participant objects and the block range
+    uint32_t mylo = blo, myhi = blo + tr.BS;
+    for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
+      bool inm = !warp || ((ins >> j) & 1u);
+      uint32_t u = base + j;
+      if (inm && !a.exited[u]) {
+        uint32_t o = objs[u];
+        if (o != NIL) {
+          uint32_t lo = a.arena[o], len = a.arena[o + 1];
+          mylo = min(mylo, lo);
+          myhi = max(myhi, lo + len);
+        }
+      }
+    }
+    uint32_t lo = block_min_u32(mylo), hi = block_max_u32(myhi);
+    uint32_t span = hi - lo;
+    uint32_t* acc = span <= (uint32_t)kAccSmem ? s_acc : a.scratch + (size_t)blockIdx.x * 3 * tr.T + 2 * tr.T;
+    for (uint32_t i = threadIdx.x; i < span; i += kThreads) acc[i] = 0u;
+    __syncthreads();
+    // join each distinct participant object once
+    uint32_t done_lo = 0;  // objects < done_lo already joined (ids increase strictly per round)
+    while (true) {
+      uint32_t mymin = NIL;
+      for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
+        bool inm = !warp || ((ins >> j) & 1u);
+        uint32_t u = base + j;
+        if (inm && !a.exited[u]) {
+          uint32_t o = objs[u];
+          if (o != NIL && o >= done_lo && o < mymin) mymin = o;
+        }
+      }
+      uint32_t om = block_min_u32(mymin);
+      if (om == NIL) break;
+      uint32_t olo = a.arena[om], olen = a.arena[om + 1];
+      for (uint32_t i = threadIdx.x; i < olen; i += kThreads) {
+        uint32_t v = a.arena[om + 2 + i];
+        uint32_t* d = &acc[olo - lo + i];
+        if (v > *d) *d = v;
+      }
+      __syncthreads();
+      done_lo = om + 1;
+    }
+    // participants' own entries = their local time (C_u[u], hb_u[u])
+    for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
+      bool inm = !warp || ((ins >> j) & 1u);
+      uint32_t u = base + j;
+      if (inm && !a.exited[u]) acc[u - lo] = a.local[u];
+    }
+    __syncthreads();
+    __shared__ uint32_t s_no;
+    if (threadIdx.x == 0) {
+      uint32_t o = arena_alloc(a, span + 2);
+      if (o != NIL) { a.arena[o] = lo; a.arena[o + 1] = span; }
+      s_no = o;
+    }
+    __syncthreads();
+    uint32_t no = s_no;
+    if (no != NIL)
+      for (uint32_t i = threadIdx.x; i < span; i += kThreads) a.arena[no + 2 + i] = acc[i];
+    newobj[kind] = no;
+    __syncthreads();
+  }
+  for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
+    bool inm = !warp || ((ins >> j) & 1u);
+    uint32_t u = base + j;
+    if (inm && !a.exited[u]) {
+      uint32_t nl = a.local[u] + 1;
+      a.local[u] = nl;
+      a.pobj[u] = newobj[0];
+      a.pdiag[u] = nl;
+      if (a.has_locks) a.hobj[u] = newobj[1];
+    }
+  }
+  __syncthreads();
+}
+
+// --------------------------------------------------------------- locks ----
+__device__ __forceinline__ void ticket_wait(const WalkArgs& a, uint32_t r) {
+  if (threadIdx.x == 0) {
+    volatile uint32_t* tk = a.ticket;
+    uint32_t ns = 32;
+    while (*tk != r) {
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  __threadfence();
+}
+__device__ __forceinline__ void ticket_release(const WalkArgs& a, uint32_t r) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(a.ticket, r + 1);
+  }
+}
+
+// _drain, gwcp.py:161-173, as a per-(lock, thread) cursor over the lock's
+// record list.  Queue materialisation (gwcp.py:80-100):
+// before the thread's first END its queue is every record of the lock by
+// other threads; after an END (drop) the next drain re-materialises a
+// snapshot of all records so far (own included; empty with inactive_opt
+// off) that receives no further pushes.
+__device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uint32_t cur, uint32_t* P) {
+  __shared__ uint32_t s_ctl, s_o, s_tid, s_loc;
+  __shared__ CurEnt* s_cur;
+  __shared__ LockEnt* s_lk;
+  int changed = 0;
+  if (threadIdx.x == 0) {
+    LockEnt* lk = lock_find(a, lock, false);
+    CurEnt* ce = lk ? cur_find(a, lock, t) : nullptr;
+    s_lk = lk;
+    s_cur = ce;
+    if (ce) {
+      uint32_t ep = a.nend[t];
+      if (__ldcg(&ce->epoch) != ep) {  // (re)materialise the queue
+        ce->epoch = ep;
+        ce->last = NIL;
+        ce->snap = ep != 0;
+        ce->bound = ep == 0 ? NIL : (a.inactive_opt ? __ldcg(&lk->nrec) : 0u);
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_cur) return 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      CurEnt* ce = s_cur;
+      LockEnt* lk = s_lk;
+      const uint32_t snap = __ldcg(&ce->snap), bound = __ldcg(&ce->bound);
+      uint32_t last = __ldcg(&ce->last);
+      uint32_t nx = last == NIL ? __ldcg(&lk->head) : __ldcg(&a.recs[last].next);
+      if (!snap) {
+        // the thread's own records never enter its queue: step over them
+        while (nx != NIL && __ldcg(&a.recs[nx].tid) == t) { last = nx; nx = __ldcg(&a.recs[nx].next); }
+        ce->last = last;
+      } else if (nx != NIL && __ldcg(&a.recs[nx].seq) >= bound) {
+        nx = NIL;
+      }
+      uint32_t ctl = 0;  // 0 stop, 1 pop without join, 2 pop + join rel clock
+      if (nx != NIL) {
+        const Rec* r = &a.recs[nx];
+        const uint32_t rt = __ldcg(&r->tid);
+        if (__ldcg(&r->closed)) {
+          const bool le = rt == t || P[rt] >= __ldcg(&r->acq_local);
+          if (le) {
+            ce->last = nx;
+            ctl = sc_overlap(__ldcg(&r->scope), cur) ? 2u : 1u;
+            s_o = __ldcg(&r->rel_hobj);
+            s_tid = rt;
+            s_loc = __ldcg(&r->rel_local);
+          }
+        }
+      }
+      s_ctl = ctl;
+    }
+    __syncthreads();
+    const uint32_t ctl = s_ctl;
+    if (ctl == 0) break;
+    if (ctl == 2) {
+      int ch = join_obj_dense(P, a.arena, s_o);
+      __syncthreads();
+      if (threadIdx.x == 0 && s_loc > P[s_tid]) { P[s_tid] = s_loc; ch = 1; }
+      changed |= __syncthreads_or(ch);
+    } else {
+      __syncthreads();
+    }
+  }
+  return changed;
+}
+
+__device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long lock) {
+  const uint32_t T = a.tr.T;
+  const uint32_t t = ev_tid(to);
+  const uint32_t cur = (to & GW_F_DEVICE) ? SC_DEV : t / a.tr.BS;
+  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * T;
+  uint32_t* H = P + T;
+  __shared__ LockEnt* s_lk;
+  if (threadIdx.x == 0) s_lk = lock_find(a, lock, true);
+  __syncthreads();
+  if (!s_lk) return;
+  materialize(P, a.arena, a.pobj[t], T, t, a.pdiag[t]);
+  int pch = drain(a, t, lock, cur, P);
+  materialize(H, a.arena, a.hobj[t], T, t, a.local[t]);
+  int hch = 0;
+  // join instance clocks whose release orders this acquire (gwcp.py:185-188, scopes.py:50-59)
+  __shared__ uint32_t s_i, s_H, s_P;
+  if (threadIdx.x == 0) s_i = __ldcg(&s_lk->inst_head);
+  __syncthreads();
+  while (true) {
+    if (threadIdx.x == 0) {
+      uint32_t i = s_i;
+      while (i != NIL && !sc_overlap(__ldcg(&a.insts[i].scope), cur)) i = __ldcg(&a.insts[i].next);
+      s_i = i;
+      if (i != NIL) { s_H = __ldcg(&a.insts[i].H); s_P = __ldcg(&a.insts[i].P); }
+    }
+    __syncthreads();
+    uint32_t i = s_i;
+    if (i == NIL) break;
+    hch |= join_obj_dense(H, a.arena, s_H);
+    pch |= join_obj_dense(P, a.arena, s_P);
+    __syncthreads();
+    if (threadIdx.x == 0) s_i = __ldcg(&a.insts[i].next);
+    __syncthreads();
+  }
+  pch = __syncthreads_or(pch);
+  hch = __syncthreads_or(hch);
+  if (pch) {
+    uint32_t o = publish_dense(a, P, T);
+    if (threadIdx.x == 0) { a.pobj[t] = o; a.pdiag[t] = P[t]; }
+  }
+  if (hch) {
+    uint32_t o = publish_dense(a, H, T);
+    if (threadIdx.x == 0) a.hobj[t] = o;
+  }
+  if (threadIdx.x == 0) {
+    // CSRecord(acq_clock = C_t) pushed to the lock's list; the acquire clock
+    // is kept as its epoch (t, local) -- see the drain-test note above.
+    LockEnt* lk = s_lk;
+    uint32_t ri = atomicAdd(a.rec_top, 1u);
+    uint32_t d = a.depth[t];
+    if (ri >= a.rec_cap) { atomicOr(a.err, ERR_REC); }
+    else if (d >= a.maxd) { atomicOr(a.err, ERR_FRAMES); }
+    else {
+      Rec r;
+      r.tid = t; r.acq_local = a.local[t]; r.scope = cur; r.rel_hobj = NIL; r.rel_local = 0; r.closed = 0;
+      r.next = NIL; r.seq = __ldcg(&lk->nrec);
+      a.recs[ri] = r;
+      uint32_t tail = __ldcg(&lk->tail);
+      if (tail == NIL) lk->head = ri; else a.recs[tail].next = ri;
+      lk->tail = ri;
+      lk->nrec = r.seq + 1;
+      Frame f;
+      f.lock = lock; f.scope = cur; f.rec = ri; f.logpos = a.loghead[t]; f.pad = 0;
+      a.frames[(size_t)t * a.maxd + d] = f;
+      a.depth[t] = d + 1;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long lock) {
+  const uint32_t T = a.tr.T;
+  const uint32_t t = ev_tid(to);
+  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * T;
+  uint32_t* H = P + T;
+  __shared__ Frame s_f;
+  __shared__ LockEnt* s_lk;
+  if (threadIdx.x == 0) {
+    uint32_t d = a.depth[t];
+    s_f = a.frames[(size_t)t * a.maxd + (d - 1)];
+    s_lk = lock_find(a, lock, false);
+  }
+  __syncthreads();
+  if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); return; }
+  const uint32_t inst = s_f.scope;
+  materialize(P, a.arena, a.pobj[t], T, t, a.pdiag[t]);
+  int pch = drain(a, t, lock, inst, P);
+  if (pch) {
+    uint32_t o = publish_dense(a, P, T);
+    if (threadIdx.x == 0) { a.pobj[t] = o; a.pdiag[t] = P[t]; }
+    __syncthreads();
+  }
+  materialize(H, a.arena, a.hobj[t], T, t, a.local[t]);
+  // stage the frame's read / write sets with the hb clock (gwcp.py:207-210)
+  __shared__ uint32_t s_arr, s_new;
+  uint32_t li = a.loghead[t];  // thread 0's iterator over the frame's access log
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_arr = NIL;
+      s_new = 0;
+      while (li != s_f.logpos && li != NIL && s_arr == NIL) {
+        LogEnt le = a.logs[li];
+        li = le.next;
+        CsEnt* ce = cs_find(a, lock, inst, le.loc, le.rw, true);
+        if (!ce) break;
+        if (ce->arr == NIL) {
+          uint32_t o = arena_alloc(a, T + 2);
+          if (o == NIL) break;
+          a.arena[o] = 0; a.arena[o + 1] = T;
+          ce->arr = o;
+          s_new = 1;
+        }
+        s_arr = ce->arr;
+      }
+    }
+    __syncthreads();
+    const uint32_t arr = s_arr;
+    if (arr == NIL) break;
+    uint32_t* dst = a.arena + arr + 2;
+    if (s_new) {
+      for (uint32_t i = threadIdx.x; i < T; i += kThreads) dst[i] = H[i];
+    } else {
+      for (uint32_t i = threadIdx.x; i < T; i += kThreads) {
+        uint32_t v = H[i];
+        if (v > __ldcg(dst + i)) dst[i] = v;
+      }
+    }
+    __syncthreads();
+  }
+  // instance clocks H_i, P_i (gwcp.py:211-216)
+  __shared__ uint32_t s_H, s_P, s_newi;
+  if (threadIdx.x == 0) {
+    InstEnt* ie = inst_find(a, lock, inst, true);
+    s_newi = 0;
+    s_H = NIL; s_P = NIL;
+    if (ie) {
+      if (ie->H == NIL) {
+        uint32_t oh = arena_alloc(a, T + 2), op = arena_alloc(a, T + 2);
+        if (oh != NIL) { a.arena[oh] = 0; a.arena[oh + 1] = T; }
+        if (op != NIL) { a.arena[op] = 0; a.arena[op + 1] = T; }
+        ie->H = oh; ie->P = op;
+        ie->next = __ldcg(&s_lk->inst_head);
+        s_lk->inst_head = (uint32_t)(ie - a.insts);
+        s_newi = 1;
+      }
+      s_H = ie->H; s_P = ie->P;
+    }
+  }
+  __syncthreads();
+  if (s_H != NIL && s_P != NIL) {
+    uint32_t* dh = a.arena + s_H + 2;
+    uint32_t* dp = a.arena + s_P + 2;
+    for (uint32_t i = threadIdx.x; i < T; i += kThreads) {
+      uint32_t h = H[i], p = P[i];
+      if (s_newi) { dh[i] = h; dp[i] = p; }
+      else {
+        if (h > __ldcg(dh + i)) dh[i] = h;
+        if (p > __ldcg(dp + i)) dp[i] = p;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // close the record with rel_clock = copy(hb) (gwcp.py:216); pop; local += 1
+    Rec* r = &a.recs[s_f.rec];
+    r->rel_hobj = a.hobj[t];
+    r->rel_local = a.local[t];
+    __threadfence();
+    r->closed = 1;
+    uint32_t d = a.depth[t] - 1;
+    a.depth[t] = d;
+    if (d == 0) a.loghead[t] = NIL;
+    a.local[t] = a.local[t] + 1;
+  }
+  __syncthreads();
+}
+
+// on_access inside critical sections: rule (i) joins (gwcp.py:236-249) then
+// the (time, vobj) stamp and the frame-set append (gwcp.py:278-279)
+__device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long loc) {
+  const uint32_t T = a.tr.T;
+  const uint32_t t = ev_tid(to);
+  const uint32_t isw = ev_kind(to) == GW_K_WRITE;
+  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * T;
+  materialize(P, a.arena, a.pobj[t], T, t, a.pdiag[t]);
+  int pch = 0;
+  __shared__ uint32_t s_arr;
+  const uint32_t depth = a.depth[t];
+  // thread 0 iterates frames x released instances of the frame's lock that
+  // overlap the frame's instance x {cs_write, cs_read if this is a write}
+  uint32_t fi = 0, ii = NIL, phase = 0;
+  unsigned long long flock = 0;
+  uint32_t fscope = 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      uint32_t found = NIL;
+      while (found == NIL) {
+        if (phase == 0) {
+          if (fi >= depth) break;
+          const Frame f = a.frames[(size_t)t * a.maxd + fi];
+          flock = f.lock;
+          fscope = f.scope;
+          LockEnt* lk = lock_find(a, flock, false);
+          ii = lk ? __ldcg(&lk->inst_head) : NIL;
+          phase = 1;
+        }
+        if (ii == NIL) { fi++; phase = 0; continue; }
+        const uint32_t isc = __ldcg(&a.insts[ii].scope);
+        const bool ov = sc_overlap(isc, fscope);
+        if (phase == 1) {  // cs_write
+          if (ov) {
+            CsEnt* ce = cs_find(a, flock, isc, loc, 1u, false);
+            if (ce && __ldcg(&ce->arr) != NIL) found = __ldcg(&ce->arr);
+          }
+          phase = isw ? 2 : 3;
+        } else if (phase == 2) {  // cs_read
+          if (ov) {
+            CsEnt* ce = cs_find(a, flock, isc, loc, 0u, false);
+            if (ce && __ldcg(&ce->arr) != NIL) found = __ldcg(&ce->arr);
+          }
+          phase = 3;
+        }
+        if (phase == 3) { ii = __ldcg(&a.insts[ii].next); phase = 1; }
+      }
+      s_arr = found;
+    }
+    __syncthreads();
+    const uint32_t arr = s_arr;
+    if (arr == NIL) break;
+    pch |= join_obj_dense(P, a.arena, arr);
+    __syncthreads();
+  }
+  pch = __syncthreads_or(pch);
+  if (pch) {
+    uint32_t o = publish_dense(a, P, T);
+    if (threadIdx.x == 0) { a.pobj[t] = o; a.pdiag[t] = P[t]; }
+  }
+  if (threadIdx.x == 0) {
+    a.time[e] = a.local[t];
+    a.vobj[e] = a.pobj[t];
+    uint32_t li = atomicAdd(a.log_top, 1u);
+    if (li >= a.log_cap) atomicOr(a.err, ERR_LOG);
+    else {
+      a.logs[li] = LogEnt{loc, isw, a.loghead[t]};
+      a.loghead[t] = li;
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ the kernel --
+__global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
+  __shared__ uint32_t s_e[kWalkCH];
+  __shared__ uint32_t s_to[kWalkCH];
+  __shared__ uint32_t s_hard[kWalkCH + 1];
+  __shared__ uint32_t s_nh;
+  __shared__ uint32_t s_acc[kAccSmem];
+  const DevTrace& tr = a.tr;
+  const uint32_t g = blockIdx.x;
+  // my range in the partition
+  uint64_t beg = 0, end = tr.n;
+  if (a.G > 1) {
+    uint64_t lo = 0, hi = tr.n;
+    while (lo < hi) { uint64_t m = (lo + hi) >> 1; if (a.part_key[m] < g) lo = m + 1; else hi = m; }
+    beg = lo;
+    hi = tr.n;
+    while (lo < hi) { uint64_t m = (lo + hi) >> 1; if (a.part_key[m] <= g) lo = m + 1; else hi = m; }
+    end = lo;
+  }
+  for (uint64_t cb = beg; cb < end; cb += kWalkCH) {
+    const uint32_t cnt = (uint32_t)min((uint64_t)kWalkCH, end - cb);
+    if (threadIdx.x == 0) s_nh = 0;
+    __syncthreads();
+    // stage events; collect the hard ones (barrier, acq, rel, end, in-CS access)
+    for (uint32_t j = threadIdx.x; j < cnt; j += kThreads) {
+      uint32_t e = a.perm ? a.perm[cb + j] : (uint32_t)(cb + j);
+      uint32_t to = tr.tidop[e];
+      s_e[j] = e;
+      s_to[j] = to;
+    }
+    __syncthreads();
+    // ordered compaction of hard positions (block scan over 4 items/thread)
+    {
+      constexpr int IPT = kWalkCH / kThreads;
+      uint32_t flags = 0, nmine = 0;
+#pragma unroll
+      for (int k = 0; k < IPT; k++) {
+        uint32_t j = threadIdx.x * IPT + k;
+        if (j < cnt) {
+          uint32_t kd = ev_kind(s_to[j]);
+          bool hard = kd != GW_K_READ && kd != GW_K_WRITE && kd != GW_K_FENCE;
+          if (!hard && a.has_locks && kd <= GW_K_WRITE && (a.lflags[s_e[j]] & LF_INCS)) hard = true;
+          if (hard) { flags |= 1u << k; nmine++; }
+        }
+      }
+      uint32_t tot;
+      uint32_t off = block_excl_scan<uint32_t, OpSum>(nmine, OpSum(), 0u, &tot);
+#pragma unroll
+      for (int k = 0; k < IPT; k++)
+        if (flags & (1u << k)) s_hard[off++] = threadIdx.x * IPT + k;
+      if (threadIdx.x == 0) { s_nh = tot; s_hard[tot] = cnt; }
+    }
+    __syncthreads();
+    const uint32_t nh = s_nh;
+    uint32_t pos = 0;
+    for (uint32_t hi = 0; hi <= nh; hi++) {
+      const uint32_t h = s_hard[hi];
+      // plain accesses in [pos, h): stamp (time, vobj) from the owner's state
+      for (uint32_t j = pos + threadIdx.x; j < h; j += kThreads) {
+        uint32_t to = s_to[j];
+        if (ev_kind(to) <= GW_K_WRITE) {
+          uint32_t t = ev_tid(to), e = s_e[j];
+          a.time[e] = a.local[t];
+          a.vobj[e] = a.pobj[t];
+        }
+      }
+      __syncthreads();
+      if (h < cnt) {
+        const uint32_t e = s_e[h], to = s_to[h];
+        const uint32_t kd = ev_kind(to);
+        if (kd == GW_K_BARRIER) {
+          do_barrier(a, to, tr.instr[e], s_acc);
+        } else if (kd == GW_K_END) {
+          if (threadIdx.x == 0) {
+            const uint32_t t = ev_tid(to);
+            uint32_t d = a.has_locks ? a.depth[t] : 0u;
+            for (uint32_t i = 0; i < d; i++)
+              emit_diag(a, e, GW_D_EXIT_HOLDING, i, a.frames[(size_t)t * a.maxd + i].lock);
+            if (a.has_locks) { a.depth[t] = 0; a.loghead[t] = NIL; }
+            a.exited[t] = 1;
+            a.nend[t] = a.nend[t] + 1;
+          }
+          __syncthreads();
+        } else if (kd == GW_K_ACQUIRE || kd == GW_K_RELEASE) {
+          const uint8_t lf = a.lflags[e];
+          const unsigned long long lock = tr.key[e];
+          if (!(lf & LF_OK)) {
+            if (threadIdx.x == 0) emit_diag(a, e, kd == GW_K_ACQUIRE ? GW_D_REENTRANT : GW_D_UNHELD, 0, lock);
+            __syncthreads();
+          } else {
+            const uint32_t r = a.rank[e];
+            ticket_wait(a, r);
+            if (kd == GW_K_ACQUIRE) do_acquire(a, e, to, lock);
+            else do_release(a, e, to, lock);
+            ticket_release(a, r);
+          }
+        } else {  // in-CS access
+          const uint32_t r = a.rank[e];
+          ticket_wait(a, r);
+          do_incs_access(a, e, to, tr.key[e]);
+          ticket_release(a, r);
+        }
+      }
+      pos = h + 1;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_state_init(WalkArgs a) {
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < a.tr.T;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    a.local[u] = 1; a.pobj[u] = NIL; a.pdiag[u] = 0; a.exited[u] = 0; a.nend[u] = 0;
+    if (a.has_locks) { a.hobj[u] = NIL; a.depth[u] = 0; a.loghead[u] = NIL; }
+  }
+}
+
+// ------------------------------------------------------ lock pre-pass ----
+// Per-thread lock-stack automaton (clock independent): decides which
+// acquires / releases succeed (gwcp.py:178-182, :196-201), which accesses run
+// inside a critical section, and the global rank of every lock-related event.
+__global__ void k_lock_mark(DevTrace tr, uint32_t* flag) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t k = ev_kind(tr.tidop[e]);
+    flag[e] = (k == GW_K_ACQUIRE || k == GW_K_RELEASE || k == GW_K_END) ? 1u : 0u;
+  }
+}
+__global__ void k_lock_compact(DevTrace tr, const uint32_t* pos, uint32_t* ktid, uint32_t* kev) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t to = tr.tidop[e];
+    uint32_t k = ev_kind(to);
+    if (k == GW_K_ACQUIRE || k == GW_K_RELEASE || k == GW_K_END) {
+      uint32_t p = pos[e];
+      ktid[p] = ev_tid(to);
+      kev[p] = (uint32_t)e;
+    }
+  }
+}
+__global__ void k_lock_segs(const uint32_t* ktid, uint32_t n, uint32_t* seg_beg, uint32_t* seg_end) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t t = ktid[i];
+    if (i == 0 || ktid[i - 1] != t) seg_beg[t] = i;
+    if (i == n - 1 || ktid[i + 1] != t) seg_end[t] = i + 1;
+  }
+}
+__global__ void k_lock_automaton(DevTrace tr, const uint32_t* ktid, const uint32_t* kev, uint32_t n,
+                                 const uint32_t* seg_end, unsigned long long* stk, uint32_t* res, uint8_t* lflags,
+                                 uint32_t* maxd) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t t = ktid[i];
+    if (i != 0 && ktid[i - 1] == t) continue;
+    uint32_t end = seg_end[t];
+    uint32_t d = 0, md = 0;
+    for (uint32_t p = i; p < end; p++) {
+      uint32_t e = kev[p];
+      uint32_t k = ev_kind(tr.tidop[e]);
+      unsigned long long lk = tr.key[e];
+      uint8_t ok = 0;
+      if (k == GW_K_ACQUIRE) {
+        bool in = false;
+        for (uint32_t s = 0; s < d; s++) in |= stk[i + s] == lk;
+        if (!in) { stk[i + d] = lk; d++; ok = 1; }
+      } else if (k == GW_K_RELEASE) {
+        if (d > 0 && stk[i + d - 1] == lk) { d--; ok = 1; }
+      } else {
+        d = 0;
+      }
+      md = max(md, d);
+      res[p] = d;
+      if (k != GW_K_END) lflags[e] = ok ? (LF_OK | LF_LOCKREL) : 0;
+    }
+    atomicMax(maxd, md);
+  }
+}
+__global__ void k_lock_access(DevTrace tr, const uint32_t* kev, const uint32_t* res, const uint32_t* seg_beg,
+                              const uint32_t* seg_end, uint8_t* lflags, uint32_t* n_incs) {
+  uint32_t cnt = 0;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t to = tr.tidop[e];
+    uint32_t k = ev_kind(to);
+    if (k > GW_K_WRITE) continue;
+    uint32_t t = ev_tid(to);
+    uint32_t lo = seg_beg[t], hi = seg_end[t];
+    uint8_t f = 0;
+    if (lo < hi) {
+      // last lock event of t before e
+      uint32_t l = lo, h = hi;
+      while (l < h) { uint32_t m = (l + h) >> 1; if (kev[m] < (uint32_t)e) l = m + 1; else h = m; }
+      if (l > lo && res[l - 1] > 0) { f = LF_INCS | LF_LOCKREL; cnt++; }
+    }
+    lflags[e] = f;
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_incs, cnt);
+}
+
+struct LockRelLoad {
+  const uint8_t* lf;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const { return (lf[i] & LF_LOCKREL) ? 1u : 0u; }
+};
+
+}  // namespace gw

@@ -1,0 +1,114 @@
+"""GPU parity: the CUDA engine (through the C-ABI) against the reference's
+golden outputs and the CPU oracle.  Integer work: bit-exact, i.e. the NDJSON
+report lines and the diagnostics are byte-identical."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_text
+from helpers import check_against_golden
+from oracle import oracle as O
+from paper_2111_12478_b200 import GwcpDetector, parse_trace, run
+from paper_2111_12478_b200 import _native as N
+from paper_2111_12478_b200 import workloads as WL
+from paper_2111_12478_b200.report import ndjson_lines
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return N.Context(0)
+
+
+def _run(ctx, tr, inactive_opt=True):
+    ctx.analyze_host(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt=inactive_opt)
+    return ctx.fetch()
+
+
+@pytest.mark.parametrize("tag", ["corpus", "random", "nasty", "c1", "largewin", "c2", "c3", "c4", "parse"])
+def test_engine_matches_reference_goldens(goldens, ctx, tag):
+    n = 0
+    for r in goldens:
+        if "error" in r or tag not in r["tags"] or "full" in r["tags"]:
+            continue
+        tr = parse_trace(golden_text(r))
+        check_against_golden(r, tr, _run(ctx, tr, r["inactive_opt"]))
+        n += 1
+    assert n > 0
+
+
+def test_engine_full_c2_matches_reference(goldens, ctx):
+    r = next(r for r in goldens if r["name"] == "c2/full")
+    tr = WL.c2_soa()
+    check_against_golden(r, tr, _run(ctx, tr))
+
+
+def test_dropin_run_api_on_reference_shaped_objects(goldens):
+    # run() accepts Event-object traces (as gpurace users hold them)
+    for r in goldens:
+        if r["name"] != "corpus/wcp-classic":
+            continue
+        tr = parse_trace(r["text"])
+        res = run(tr, GwcpDetector(tr.config))
+        assert [x.to_json() for x in res.reports] == r["reports"]
+        # decode to Event objects and back through the encoder
+        from paper_2111_12478_b200.trace import Trace
+
+        class Shim:
+            config = tr.config
+            events = tr.events
+
+        res2 = run(Shim(), GwcpDetector(tr.config))
+        assert [x.to_json() for x in res2.reports] == r["reports"]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_engine_matches_oracle_c3_geometries(ctx, seed):
+    text = WL.c3_text(blocks=4 + 4 * seed, warps=4, lanes=32, iters=12 + 4 * seed, locks=8 << seed, region=16,
+                      private=128, seed=100 + seed)
+    tr = parse_trace(text)
+    assert ndjson_lines(tr, _run(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_engine_matches_oracle_c4_geometries(ctx, seed):
+    text = WL.c4_text(blocks=4 + 6 * seed, warps=8, lanes=32, iters=20 + 10 * seed, words_per_block=1024,
+                      seed=200 + seed)
+    tr = parse_trace(text)
+    assert ndjson_lines(tr, _run(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
+
+
+@pytest.mark.parametrize("geom", [(64, 8, 32), (300, 4, 32), (1000, 2, 16)])
+def test_engine_matches_oracle_c2_geometries(ctx, geom):
+    B, W, L = geom
+    tr = WL.c2_soa(blocks=B, warps=W, lanes=L, phases=4, records=4, words_per_block=512, seed=B)
+    got = _run(ctx, tr)
+    want = O.run_trace(tr)
+    assert ndjson_lines(tr, got) == ndjson_lines(tr, want)
+
+
+def test_empty_and_tiny_traces(ctx):
+    for text in ("config blocks=1 warps=1 lanes=1\n", "config blocks=2 warps=1 lanes=1\n0.0.0 wr g:0x10\n",
+                 "config blocks=1 warps=1 lanes=1\nbar block 0\n0.0.0 end\nbar block 0\n"):
+        tr = parse_trace(text)
+        got = _run(ctx, tr)
+        assert len(got["kind"]) == 0
+
+
+def test_prefix_consistency_c2(ctx):
+    """reports of trace[:P] == reports of the full trace with current.event < P."""
+    tr = WL.c2_soa(blocks=32, warps=8, lanes=32, phases=8, records=8, words_per_block=1024, seed=9)
+    full = _run(ctx, tr)
+    for P in (len(tr) // 3, len(tr) // 2):
+        # cut at a record boundary
+        while P < len(tr) and tr.tidop[P] & N.F_CONT:
+            P += 1
+        from paper_2111_12478_b200.trace import Trace
+
+        pre = Trace(tr.config, tr.key[:P], tr.tidop[:P], tr.instr[:P])
+        got = _run(ctx, pre)
+        keep = full["current"] < P
+        assert np.array_equal(got["prior"], full["prior"][keep])
+        assert np.array_equal(got["current"], full["current"][keep])
+        assert np.array_equal(got["kind"], full["kind"][keep])
