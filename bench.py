@@ -1,0 +1,358 @@
+"""Benchmark: trace events/s of G-WCP race analysis (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload c2|c5s]
+
+One step = one complete analysis of one synthetic trace (the workload) with
+the final report list on the host.  ``value`` is device-resident throughput
+(SoA already in HBM); ``e2e`` is the same metric through the public C-ABI
+call with HOST buffers (pinned H2D of the SoA and D2H of the reports inside
+the timed region).  L2 is flushed (256 MiB write) before every timed step;
+each step is timed with CUDA events on the launching stream and the K step
+times are summed.  For N > 1 (torchrun, one rank per GPU) every rank analyses
+its own trace (independent objects: weak scaling, no data-path collective);
+the time is the max over ranks.
+
+``--impl reference`` times the CPU restatement of the reference (oracle/,
+single-threaded like the reference) on this host: rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "trace events/sec analysed (1/2/4/8 B200) vs CPU ref; race-pair set bit-exact"
+UNIT = "events/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_workload(name: str, rank: int):
+    from paper_2111_12478_b200 import workloads as WL
+
+    if name == "c2":
+        tr = WL.c2_soa(seed=2 + rank)
+        desc = {"workload": "C2", "threads": "64x8x32", "addresses": 65536, "phases": 8,
+                "sync": "__syncthreads only", "injected_random_words": "1%"}
+    elif name == "c5s":  # C5 recipe at reduced depth (fits host RAM for the e2e leg)
+        tr = WL.c2_soa(blocks=1024, warps=8, lanes=32, phases=4, records=8, words_per_block=262144, seed=5 + rank)
+        desc = {"workload": "C5-shallow", "threads": "1024x8x32", "addresses": 268435456, "phases": 4}
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    return tr, desc
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    def __init__(self, device: int):
+        self.samples: list[int] = []
+        self.reasons: set[str] = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        return {
+            "sm_mhz": int(statistics.median(self.samples)) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+def cpu_oracle_run(tr, max_seconds=25.0):
+    """Time the oracle port on one core over the largest prefix fitting ~max_seconds."""
+    from oracle import oracle as O
+    from paper_2111_12478_b200 import _native as N
+    from paper_2111_12478_b200.trace import Trace
+
+    n = len(tr)
+    P = n
+    while True:
+        while P < n and tr.tidop[P] & N.F_CONT:
+            P += 1
+        sub = tr if P >= n else Trace(tr.config, tr.key[:P], tr.tidop[:P], tr.instr[:P])
+        t0 = time.perf_counter()
+        O.run_trace(sub)
+        dt = time.perf_counter() - t0
+        if dt <= max_seconds or P < 10000:
+            return P, dt
+        P = int(P * max_seconds / dt * 0.8)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    tr, desc = make_workload(args.workload, 0)
+    n = len(tr)
+    times = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        P, dt = cpu_oracle_run(tr, max_seconds=args.ref_seconds)
+        sample = P
+        if i >= args.warmup:
+            times.append((P, dt))
+    evs = sum(p for p, _ in times) / sum(d for _, d in times)
+    cores = 1
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": evs,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * sum(d for _, d in times) / len(times),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic",
+        "config": dict(desc, events=n, parallelism="single host core"),
+        "cpu_baseline": {
+            "value": evs,
+            "unit": UNIT,
+            "cores": cores,
+            "kind": "port",
+            "sample": f"first {sample} of {n} events of the workload per step (record-aligned prefix), "
+                      f"oracle/gwcp_oracle.cpp (C++ restatement of the reference, dense clocks)",
+        },
+        "e2e": {"value": evs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_b200(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2111_12478_b200 import _native as N
+
+    tr, desc = make_workload(args.workload, rank)
+    n = len(tr)
+    n_acc = int(np.count_nonzero(((tr.tidop >> np.uint32(N.OP_SHIFT)) & np.uint32(7)) <= 1))
+    cfg = tr.cfg_tuple
+    # device-resident inputs (value) and pinned host inputs (e2e)
+    key_h = torch.from_numpy(tr.key.view(np.int64)).pin_memory()
+    to_h = torch.from_numpy(tr.tidop.view(np.int32)).pin_memory()
+    in_h = torch.from_numpy(tr.instr.view(np.int32)).pin_memory()
+    key_d, to_d, in_d = key_h.to(dev), to_h.to(dev), in_h.to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    ctx = N.Context(local)
+
+    def step_device():
+        ctx.analyze_device(cfg, n, key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), stream=sptr)
+        return ctx.fetch()
+
+    def step_host():
+        ctx.analyze_host(cfg, key_h.numpy().view(np.uint64), to_h.numpy().view(np.uint32),
+                         in_h.numpy().view(np.uint32), stream=sptr)
+        return ctx.fetch()
+
+    def timed(fn, steps):
+        tot = 0.0
+        res = None
+        for _ in range(steps):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            res = fn()
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        return tot, res
+
+    for _ in range(args.warmup):
+        step_device()
+        step_host()
+    launches = ctx.launches()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    phase = {"prep": 0.0, "walker": 0.0, "sort": 0.0, "check": 0.0, "final": 0.0}
+    with ClockSampler(local) as clk:
+        barrier()
+        ms_dev = 0.0
+        for _ in range(args.steps):
+            t, res = timed(step_device, 1)
+            ms_dev += t
+            s = ctx.stats()
+            for k in phase:
+                phase[k] += getattr(s, "ms_" + k)
+        barrier()
+        ms_dev = max_over_ranks(ms_dev)
+        barrier()
+        ms_e2e, res_e2e = timed(step_host, args.steps)
+        barrier()
+        ms_e2e = max_over_ranks(ms_e2e)
+    n_rep = len(res["kind"])
+    stats = ctx.stats()
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    total_events = n * world * args.steps
+    value = total_events / (ms_dev / 1000.0)
+    e2e = total_events / (ms_e2e / 1000.0)
+    peak, peak_kind = load_peaks()
+    alg_bytes = 16 * n + 36 * n_acc  # 16 B per event + 36 B per access
+    step_s = ms_dev / args.steps / 1000.0
+    achieved = alg_bytes / step_s / 1e9
+    phases_ms = {k: round(v / args.steps, 4) for k, v in phase.items()}
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_dev / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic",
+        "config": dict(desc, events=n, accesses=n_acc, reports=n_rep, parallelism=f"replicas x{world}",
+                       l2="flushed before every timed step (256 MiB write)"),
+        "e2e": {
+            "value": e2e,
+            "unit": UNIT,
+            "h2d_bytes_per_step": 16 * n,
+            "d2h_bytes_per_step": 9 * n_rep + 64,
+            "ms_per_step": ms_e2e / args.steps,
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": None,
+            "kernel": "whole analysis (all kernels of one step); algorithmic bytes B = 16N + 36A (SURVEY 8d)",
+            "peak_source": peak_kind,
+        },
+        "phases_ms": phases_ms,
+        "gpu_launches": launches * args.steps,
+        "walker_ctas": stats.walker_ctas,
+        "sort_bits": stats.sort_bits,
+    }
+    line["clocks"] = clk.summary()
+    if not args.no_cpu_baseline:
+        P, dt = cpu_oracle_run(tr, max_seconds=args.ref_seconds)
+        line["cpu_baseline"] = {
+            "value": P / dt,
+            "unit": UNIT,
+            "cores": 1,
+            "kind": "port",
+            "sample": f"first {P} of {n} events (record-aligned prefix), oracle/gwcp_oracle.cpp, 1 run",
+        }
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--ref-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -55,39 +55,49 @@ __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals) {
 struct Stats {
   unsigned long long n_acc, n_write, n_acq, n_rel, n_end, n_bar, key_or, key_and;
 };
-__global__ void k_prep(DevTrace tr, Stats* st) {
-  unsigned long long na = 0, nw = 0, nq = 0, nr = 0, ne = 0, nb = 0, ko = 0, ka = ~0ull;
+__global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
+  unsigned long long v[6] = {0, 0, 0, 0, 0, 0};  // acc, write, acq, rel, end, bar
+  unsigned long long ko = 0, ka = ~0ull;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t to = tr.tidop[e];
-    uint32_t k = ev_kind(to);
+    const uint32_t to = tr.tidop[e];
+    const uint32_t k = ev_kind(to);
     if (k <= GW_K_WRITE) {
-      unsigned long long x = tr.key[e];
-      na++; nw += k; ko |= x; ka &= x;
-    } else if (k == GW_K_ACQUIRE) nq++;
-    else if (k == GW_K_RELEASE) nr++;
-    else if (k == GW_K_END) ne++;
-    else if (k == GW_K_BARRIER) nb++;
+      const unsigned long long x = tr.key[e];
+      v[0]++; v[1] += k; ko |= x; ka &= x;
+    } else if (k == GW_K_ACQUIRE) v[2]++;
+    else if (k == GW_K_RELEASE) v[3]++;
+    else if (k == GW_K_END) v[4]++;
+    else if (k == GW_K_BARRIER) v[5]++;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    na += __shfl_xor_sync(0xffffffffu, na, o);
-    nw += __shfl_xor_sync(0xffffffffu, nw, o);
-    nq += __shfl_xor_sync(0xffffffffu, nq, o);
-    nr += __shfl_xor_sync(0xffffffffu, nr, o);
-    ne += __shfl_xor_sync(0xffffffffu, ne, o);
-    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+#pragma unroll
+    for (int i = 0; i < 6; i++) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
     ko |= __shfl_xor_sync(0xffffffffu, ko, o);
     ka &= __shfl_xor_sync(0xffffffffu, ka, o);
   }
+  __shared__ unsigned long long s_v[kThreads / 32][8];
+  const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
-    if (na) atomicAdd(&st->n_acc, na);
-    if (nw) atomicAdd(&st->n_write, nw);
-    if (nq) atomicAdd(&st->n_acq, nq);
-    if (nr) atomicAdd(&st->n_rel, nr);
-    if (ne) atomicAdd(&st->n_end, ne);
-    if (nb) atomicAdd(&st->n_bar, nb);
-    atomicOr(&st->key_or, ko);
-    atomicAnd(&st->key_and, ka);
+#pragma unroll
+    for (int i = 0; i < 6; i++) s_v[w][i] = v[i];
+    s_v[w][6] = ko;
+    s_v[w][7] = ka;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const int i = threadIdx.x;
+    unsigned long long r = i == 7 ? ~0ull : 0ull;
+    for (int x = 0; x < kThreads / 32; x++) {
+      if (i < 6) r += s_v[x][i];
+      else if (i == 6) r |= s_v[x][i];
+      else r &= s_v[x][i];
+    }
+    unsigned long long* dst[8] = {&st->n_acc, &st->n_write, &st->n_acq, &st->n_rel, &st->n_end, &st->n_bar,
+                                  &st->key_or, &st->key_and};
+    if (i < 6) { if (r) atomicAdd(dst[i], r); }
+    else if (i == 6) atomicOr(dst[i], r);
+    else atomicAnd(dst[i], r);
   }
 }
 
@@ -255,47 +265,66 @@ __global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const
   }
 }
 
-// _same_instruction_check, engine.py:81-95 -- one thread per multi-event WRITE record
-__global__ void k_same_instr(DevTrace tr, Cands cd) {
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e + 1 < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t to0 = tr.tidop[e];
-    if (to0 & GW_F_CONT) continue;                       // not a record head
-    if (!(tr.tidop[e + 1] & GW_F_CONT)) continue;        // single-event record
-    if (ev_kind(to0) != GW_K_WRITE) continue;
-    uint64_t end = e + 1;
-    while (end < tr.n && (tr.tidop[end] & GW_F_CONT)) end++;
-    const uint64_t k = end - e;
-    if (k >= 32768) { atomicOr(cd.err, ERR_RECORD); continue; }
-    // uniform records (every parser wacc): same instr / atomic+scope / block,
-    // strictly increasing tids -> every pair at one loc shares the dedup key
-    // and the same cover verdict, so only the first pair per location can survive.
-    const uint32_t ins0 = tr.instr[e];
+// _same_instruction_check, engine.py:81-95.  One thread per event j that
+// continues a record: it scans its record (coalesced across the warp: the
+// neighbours scan the same lines) and emits the pairs (i, j), i < j.
+// Uniform records (every parser wacc: same instr / atomic+scope / block,
+// strictly increasing tids) share one dedup key and one cover verdict per
+// location, so only the pair (first, second occurrence) can survive the
+// keep-first dedup; other records emit every pair.
+__device__ __forceinline__ bool rec_uniform_step(uint32_t prev, uint32_t cur, uint32_t iprev, uint32_t icur,
+                                                 uint32_t BS) {
+  return icur == iprev && ((cur ^ prev) & (GW_F_ATOMIC | GW_F_DEVICE | (7u << GW_OP_SHIFT))) == 0 &&
+         ev_tid(cur) / BS == ev_tid(prev) / BS && ev_tid(cur) > ev_tid(prev);
+}
+__global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < tr.n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t tj = tr.tidop[j];
+    if (!(tj & GW_F_CONT) || ev_kind(tj) > GW_K_WRITE) continue;
+    const unsigned long long lj = tr.key[j];
+    // backward: head, matches, uniformity of [head, j]
+    uint64_t head = j, first = NIL;
+    uint32_t cnt = 0;
     bool uni = true;
-    for (uint64_t x = e + 1; x < end && uni; x++) {
-      const uint32_t tx = tr.tidop[x], tp = tr.tidop[x - 1];
-      uni = tr.instr[x] == ins0 && ((tx ^ to0) & (GW_F_ATOMIC | GW_F_DEVICE | (7u << GW_OP_SHIFT))) == 0 &&
-            ev_tid(tx) / tr.BS == ev_tid(to0) / tr.BS && ev_tid(tx) > ev_tid(tp);
+    uint32_t nxt_to = tj, nxt_in = tr.instr[j];
+    while (head > 0) {
+      const uint64_t i = head - 1;
+      const uint32_t ti = tr.tidop[i];
+      const uint32_t ii = tr.instr[i];
+      uni = uni && rec_uniform_step(ti, nxt_to, ii, nxt_in, tr.BS);
+      if (ev_kind(ti) <= GW_K_WRITE && tr.key[i] == lj) { cnt++; first = i; }
+      head = i;
+      nxt_to = ti;
+      nxt_in = ii;
+      if (!(ti & GW_F_CONT)) break;
     }
-    for (uint64_t j = e + 1; j < end; j++) {
-      const uint32_t tj = tr.tidop[j];
-      if (ev_kind(tj) > GW_K_WRITE) continue;
-      const unsigned long long lj = tr.key[j];
-      uint32_t nprev = 0;
-      for (uint64_t i = e; i < j; i++) {
+    if (ev_kind(tr.tidop[head]) != GW_K_WRITE || cnt == 0) continue;
+    // forward: uniformity of the rest of the record
+    {
+      uint32_t pto = tj, pin = tr.instr[j];
+      for (uint64_t x = j + 1; uni && x < tr.n; x++) {
+        const uint32_t tx = tr.tidop[x];
+        if (!(tx & GW_F_CONT)) break;
+        const uint32_t ix = tr.instr[x];
+        uni = rec_uniform_step(pto, tx, pin, ix, tr.BS);
+        pto = tx;
+        pin = ix;
+      }
+    }
+    if (j - head >= 32768) { atomicOr(cd.err, ERR_RECORD); continue; }
+    if (uni) {
+      if (cnt != 1) continue;  // j is not the second occurrence of its location
+      const uint32_t ti = tr.tidop[first];
+      if (ev_tid(ti) == ev_tid(tj) || cover(ti, tj, tr.BS)) continue;
+      emit_cand(cd, ((unsigned long long)head << 32) | ((first - head) << 15) | (j - head), lj, (uint32_t)first,
+                (uint32_t)j, GW_WW);
+    } else {
+      for (uint64_t i = head; i < j; i++) {
         const uint32_t ti = tr.tidop[i];
         if (ev_kind(ti) > GW_K_WRITE || tr.key[i] != lj) continue;
-        nprev++;
-        if (uni && nprev > 1) break;
         if (ev_tid(ti) == ev_tid(tj) || cover(ti, tj, tr.BS)) continue;
-        if (uni && nprev == 1) {
-          // emit only if j is the second occurrence of this location
-          bool second = true;
-          for (uint64_t x = i + 1; x < j && second; x++)
-            second = !(ev_kind(tr.tidop[x]) <= GW_K_WRITE && tr.key[x] == lj);
-          if (!second) break;
-        }
-        emit_cand(cd, ((unsigned long long)e << 32) | ((unsigned long long)(i - e) << 15) | (unsigned long long)(j - e),
-                  lj, (uint32_t)i, (uint32_t)j, GW_WW);
+        emit_cand(cd, ((unsigned long long)head << 32) | ((i - head) << 15) | (j - head), lj, (uint32_t)i,
+                  (uint32_t)j, GW_WW);
       }
     }
   }

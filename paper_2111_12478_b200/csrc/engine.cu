@@ -81,6 +81,8 @@ struct gw_ctx {
   gw_stats stats{};
   uint32_t launches = 0;
 
+  uint32_t epoch = 1;  // look-back flag epochs (never reused within 2^24 passes)
+
   template <class T>
   T* get(const std::string& name, uint64_t count) {
     size_t bytes = std::max<size_t>(sizeof(T) * count, 16);
@@ -91,6 +93,7 @@ struct gw_ctx {
       b.cap = 0;
       size_t nb = bytes + bytes / 8;
       CK(cudaMalloc(&b.p, nb));
+      CK(cudaMemset(b.p, 0, nb));  // look-back flags must never alias a live epoch
       b.cap = nb;
     }
     return (T*)b.p;
@@ -119,20 +122,55 @@ struct Pipeline {
   }
   void check_launch() { CK(cudaGetLastError()); }
 
+  // per-analysis zeroed block: look-back tile counters + radix histograms
+  static constexpr uint32_t kZeroWords = 1u << 16;
+  uint32_t* zero_blk = nullptr;
+  uint32_t zero_next = 0;
+  uint32_t* zeroed(uint32_t words) {
+    if (zero_next + words > kZeroWords) throw CudaErr{GW_E_ARG, "zeroed scratch block exhausted"};
+    uint32_t* p = zero_blk + zero_next;
+    zero_next += words;
+    return p;
+  }
+  uint32_t take_epochs(uint32_t k) {
+    if (C->epoch + k >= (1u << 24)) {  // wrap: clear every flag / status word
+      for (auto& kv : C->bufs)
+        if (kv.first == "lb_flag" || kv.first == "rs_status") CK(cudaMemsetAsync(kv.second.p, 0, kv.second.cap, st));
+      C->epoch = 1;
+    }
+    uint32_t e = C->epoch;
+    C->epoch += k;
+    return e;
+  }
+
   // stable radix sort wrapper; returns pointers to the sorted keys / vals
   template <class K>
   void sort(K*& keys, uint32_t*& vals, uint64_t n, int nbits, const char* tag) {
+    if (n <= 1 || nbits <= 0) return;
     std::string t(tag);
     K* ka = C->get<K>(t + "_ka", n);
     uint32_t* va = C->get<uint32_t>(t + "_va", n);
-    uint64_t nc = rs_counts_elems(n);
-    uint32_t* counts = C->get<uint32_t>("rs_counts", nc);
-    uint32_t* scr = C->get<uint32_t>("rs_scan", scan_scratch_elems(nc));
-    bool alt = radix_sort<K>(keys, ka, vals, va, n, nbits, counts, scr, st);
+    SortScratch sc;
+    const int npass = (nbits + 7) / 8;
+    sc.ghist = zeroed(kRsMaxPass * 256);
+    sc.ctrs = zeroed(npass);
+    sc.status = C->get<unsigned long long>("rs_status", lb_tiles(n) * 256);
+    bool alt = radix_sort<K>(keys, ka, vals, va, n, nbits, sc, take_epochs(npass), st);
     if (alt) {
       keys = ka;
       vals = va;
     }
+  }
+
+  template <class T, class Op, class Load, class Store>
+  void scan(Load load, Store store, uint64_t n, Op op, T identity, bool inclusive, const char* tag) {
+    if (n == 0) return;
+    std::string t(tag);
+    const uint64_t nt = lb_tiles(n);
+    T* agg = C->get<T>(t + "_agg", nt);
+    T* inc = C->get<T>(t + "_inc", nt);
+    uint32_t* flag = C->get<uint32_t>("lb_flag", nt);
+    scan_lb<T, Op>(load, store, n, agg, inc, flag, zeroed(1), take_epochs(1), op, identity, inclusive, st);
   }
 
   void run() {
@@ -151,6 +189,9 @@ struct Pipeline {
       return;
     }
     // ---------------------------------------------------------------- prep
+    zero_blk = C->get<uint32_t>("zero_blk", kZeroWords);
+    zero_next = 0;
+    CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
     Stats* dst = C->get<Stats>("stats", 1);
     Stats hs;
     memset(&hs, 0, sizeof hs);
@@ -194,8 +235,7 @@ struct Pipeline {
       const uint64_t nle = hs.n_acq + hs.n_rel + hs.n_end;
       uint32_t* flag = C->get<uint32_t>("lk_flag", N);
       GW_LAUNCH(k_lock_mark, grid_for(N), kThreads, 0, st, tr, flag);
-      uint32_t* sscr = C->get<uint32_t>("scan_scr", scan_scratch_elems(N));
-      device_scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{flag}, N, sscr, OpSum(), 0u, false, st);
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{flag}, N, OpSum(), 0u, false, "sc_u32");
       uint32_t* ktid = C->get<uint32_t>("lk_tid", nle);
       uint32_t* kev = C->get<uint32_t>("lk_ev", nle);
       GW_LAUNCH(k_lock_compact, grid_for(N), kThreads, 0, st, tr, flag, ktid, kev);
@@ -213,7 +253,7 @@ struct Pipeline {
                 lflags, scal + 0);
       GW_LAUNCH(k_lock_access, grid_for(N), kThreads, 0, st, tr, kev, res, seg_beg, seg_end, lflags, scal + 1);
       uint32_t* rank = C->get<uint32_t>("lk_rank", N);
-      device_scan<uint32_t, OpSum>(LockRelLoad{lflags}, ArrStore<uint32_t>{rank}, N, sscr, OpSum(), 0u, false, st);
+      scan<uint32_t, OpSum>(LockRelLoad{lflags}, ArrStore<uint32_t>{rank}, N, OpSum(), 0u, false, "sc_u32");
       check_launch();
       uint32_t hv[2];
       d2h(hv, scal, 2);
@@ -354,13 +394,12 @@ struct Pipeline {
       GW_LAUNCH(k_gather_to, grid_for(NA), kThreads, 0, st, vals, tr.tidop, NA, sto);
       segst = C->get<uint32_t>("acc_segst", NA);
       lastw = C->get<uint32_t>("acc_lastw", NA);
-      uint2* s2 = C->get<uint2>("scan_scr2", scan_scratch_elems(NA));
       if (!wide)
-        device_scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, NA, s2,
-                                   OpMax2(), make_uint2(0, 0), true, st);
+        scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, NA, OpMax2(),
+                            make_uint2(0, 0), true, "sc_u2");
       else
-        device_scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
-                                   SegStore{segst, lastw}, NA, s2, OpMax2(), make_uint2(0, 0), true, st);
+        scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
+                            SegStore{segst, lastw}, NA, OpMax2(), make_uint2(0, 0), true, "sc_u2");
       large_i = C->get<uint32_t>("lg_i", NA / kSmallWin + 1);
       large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);
     } else {

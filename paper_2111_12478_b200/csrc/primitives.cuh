@@ -1,11 +1,12 @@
 // Device-wide primitives for the G-WCP pipeline, hand-written for sm_100a:
-//   * a reduce-then-scan exclusive/inclusive scan over a user load/store functor
-//   * a stable LSD radix sort (8-bit digits) of (u32|u64 key, u32 value) pairs
+//   * a single-pass (decoupled look-back) scan over a user load/store functor
+//   * a stable one-sweep LSD radix sort (8-bit digits) of (u32|u64 key, u32 value)
 // Both are HBM-streaming kernels: 256-thread CTAs, 16 items per thread, grids
 // sized in tiles so a 1e9-element pass fills all 148 SMs many times over.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <algorithm>
 
 namespace gw {
 
@@ -74,45 +75,6 @@ __device__ __forceinline__ T block_excl_scan(T v, Op op, T identity, T* total) {
   return op(wpre, exc);
 }
 
-template <class T, class Op, class Load>
-__global__ void __launch_bounds__(kThreads) k_scan_reduce(Load load, uint64_t n, T* aggs, Op op, T identity) {
-  const uint64_t base = (uint64_t)blockIdx.x * kTile;
-  T acc = identity;
-#pragma unroll
-  for (int k = 0; k < kItems; k++) {
-    uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
-    if (i < n) acc = op(acc, load(i));
-  }
-  T tot;
-  block_excl_scan<T, Op>(acc, op, identity, &tot);
-  if (threadIdx.x == 0) aggs[blockIdx.x] = tot;
-}
-
-// per tile: blocked arrangement (thread t owns items [t*kItems, (t+1)*kItems))
-template <class T, class Op, class Load, class Store>
-__global__ void __launch_bounds__(kThreads) k_scan_down(Load load, Store store, uint64_t n, const T* tile_prefix,
-                                                       Op op, T identity, int inclusive) {
-  const uint64_t base = (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kItems;
-  T v[kItems];
-  T acc = identity;
-#pragma unroll
-  for (int k = 0; k < kItems; k++) {
-    uint64_t i = base + k;
-    v[k] = i < n ? load(i) : identity;
-    acc = op(acc, v[k]);
-  }
-  T tot;
-  T run = block_excl_scan<T, Op>(acc, op, identity, &tot);
-  if (tile_prefix) run = op(tile_prefix[blockIdx.x], run);
-#pragma unroll
-  for (int k = 0; k < kItems; k++) {
-    uint64_t i = base + k;
-    T nx = op(run, v[k]);
-    if (i < n) store(i, inclusive ? nx : run);
-    run = nx;
-  }
-}
-
 template <class T>
 struct ArrLoad {
   const T* p;
@@ -124,110 +86,201 @@ struct ArrStore {
   __device__ __forceinline__ void operator()(uint64_t i, const T& v) const { p[i] = v; }
 };
 
-// Scan over n items.  scratch must hold scan_scratch_elems(n) elements of T.
-inline uint64_t scan_scratch_elems(uint64_t n) {
-  uint64_t tot = 0;
-  uint64_t t = (n + kTile - 1) / kTile;
-  while (t > 1) {
-    tot += t;
-    t = (t + kTile - 1) / kTile;
-  }
-  return tot + 1;
+// ------------------------------------------------ single-pass scan ----
+// Decoupled look-back (chained) scan: one launch, tiles taken in launch order
+// from an atomic counter, each tile publishes its aggregate and then its
+// inclusive prefix; flags carry a per-call epoch so nothing needs clearing.
+constexpr uint32_t LB_AGG = 1u, LB_INC = 2u;
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  return *(volatile const uint32_t*)p;
+}
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  return *(volatile const unsigned long long*)p;
 }
 
 template <class T, class Op, class Load, class Store>
-void device_scan(Load load, Store store, uint64_t n, T* scratch, Op op, T identity, bool inclusive,
-                 cudaStream_t st) {
-  if (n == 0) return;
-  uint64_t ntiles = (n + kTile - 1) / kTile;
-  if (ntiles == 1) {
-    GW_LAUNCH((k_scan_down<T, Op, Load, Store>), 1, kThreads, 0, st, load, store, n, (const T*)nullptr, op,
-              identity, (int)inclusive);
-    return;
+__global__ void __launch_bounds__(kThreads) k_scan_lb(Load load, Store store, uint64_t n, T* agg, T* inc,
+                                                     uint32_t* flag, uint32_t* ctr, uint32_t epoch, Op op,
+                                                     T identity, int inclusive) {
+  __shared__ uint32_t s_tile;
+  __shared__ T s_pre;
+  __shared__ T s_buf[kTile];
+  if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = (uint64_t)tile * kTile;
+  // striped (coalesced) load -> smem -> blocked per thread
+#pragma unroll
+  for (int k = 0; k < kItems; k++) {
+    const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+    s_buf[k * kThreads + threadIdx.x] = i < n ? load(i) : identity;
   }
-  T* aggs = scratch;
-  GW_LAUNCH((k_scan_reduce<T, Op, Load>), (unsigned)ntiles, kThreads, 0, st, load, n, aggs, op, identity);
-  // exclusive scan of tile aggregates, in place
-  device_scan<T, Op>(ArrLoad<T>{aggs}, ArrStore<T>{aggs}, ntiles, scratch + ntiles, op, identity, false, st);
-  GW_LAUNCH((k_scan_down<T, Op, Load, Store>), (unsigned)ntiles, kThreads, 0, st, load, store, n,
-            (const T*)aggs, op, identity, (int)inclusive);
+  __syncthreads();
+  T v[kItems];
+  T acc = identity;
+#pragma unroll
+  for (int k = 0; k < kItems; k++) {
+    v[k] = s_buf[threadIdx.x * kItems + k];
+    acc = op(acc, v[k]);
+  }
+  T tot;
+  T run = block_excl_scan<T, Op>(acc, op, identity, &tot);
+  if (threadIdx.x == 0) {
+    T pre = identity;
+    if (tile == 0) {
+      inc[0] = tot;
+      __threadfence();
+      atomicExch(&flag[0], (epoch << 2) | LB_INC);
+    } else {
+      agg[tile] = tot;
+      __threadfence();
+      atomicExch(&flag[tile], (epoch << 2) | LB_AGG);
+      int64_t p = (int64_t)tile - 1;
+      while (true) {
+        uint32_t f;
+        do { f = ld_volatile_u32(&flag[p]); } while ((f >> 2) != epoch);
+        __threadfence();
+        if ((f & 3u) == LB_INC) { pre = op(__ldcg(&inc[p]), pre); break; }
+        pre = op(__ldcg(&agg[p]), pre);
+        p--;
+      }
+      inc[tile] = op(pre, tot);
+      __threadfence();
+      atomicExch(&flag[tile], (epoch << 2) | LB_INC);
+    }
+    s_pre = pre;
+  }
+  __syncthreads();
+  run = op(s_pre, run);
+#pragma unroll
+  for (int k = 0; k < kItems; k++) {
+    T nx = op(run, v[k]);
+    s_buf[threadIdx.x * kItems + k] = inclusive ? nx : run;
+    run = nx;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kItems; k++) {
+    const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+    if (i < n) store(i, s_buf[k * kThreads + threadIdx.x]);
+  }
+}
+
+// scratch for scan_lb: agg/inc hold lb_tiles(n) elements of T, flag lb_tiles(n) u32
+inline uint64_t lb_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
+
+template <class T, class Op, class Load, class Store>
+void scan_lb(Load load, Store store, uint64_t n, T* agg, T* inc, uint32_t* flag, uint32_t* ctr, uint32_t epoch,
+             Op op, T identity, bool inclusive, cudaStream_t st) {
+  if (n == 0) return;
+  const uint64_t nt = lb_tiles(n);
+  GW_LAUNCH((k_scan_lb<T, Op, Load, Store>), (unsigned)nt, kThreads, 0, st, load, store, n, agg, inc, flag, ctr, epoch,
+            op, identity, (int)inclusive);
 }
 
 // --------------------------------------------------------- radix sort ----
-// Stable LSD radix sort, 8-bit digits.  Per pass: tile histograms (digit-major,
-// so one exclusive scan yields every tile's scatter base), then a stable
-// scatter in which each warp owns a contiguous 512-item sub-tile and ranks
-// equal digits with __match_any_sync.
 constexpr int kRsWarps = kThreads / 32;
 constexpr int kRsPerWarp = kTile / kRsWarps;      // 512
 constexpr int kRsRounds = kRsPerWarp / 32;        // 16
 
+// One-sweep LSD radix sort: one histogram kernel for every pass up front,
+// then ONE kernel per 8-bit pass whose tiles chain their per-digit counts
+// through decoupled look-back (status word = epoch:24 | state:2 | count:38).
+constexpr int kRsMaxPass = 8;
+
 template <class K>
-__global__ void __launch_bounds__(kThreads) k_rs_hist(const K* __restrict__ keys, uint64_t n, int shift,
-                                                     uint32_t* __restrict__ counts, uint64_t ntiles) {
-  __shared__ uint32_t h[256];
-  h[threadIdx.x] = 0;
+__global__ void __launch_bounds__(kThreads) k_rs_ghist(const K* __restrict__ keys, uint64_t n, int npass,
+                                                      uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[kRsMaxPass][256];
+  for (int i = threadIdx.x; i < kRsMaxPass * 256; i += kThreads) (&h[0][0])[i] = 0;
   __syncthreads();
-  const uint64_t base = (uint64_t)blockIdx.x * kTile;
-#pragma unroll 4
-  for (int k = 0; k < kItems; k++) {
-    uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
-    if (i < n) {
-      uint32_t d = (uint32_t)(keys[i] >> shift) & 255u;
-      atomicAdd(&h[d], 1u);
-    }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const K k = keys[i];
+    for (int p = 0; p < npass; p++) atomicAdd(&h[p][(uint32_t)(k >> (8 * p)) & 255u], 1u);
   }
   __syncthreads();
-  counts[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+  for (int p = 0; p < npass; p++) {
+    const uint32_t c = h[p][threadIdx.x];
+    if (c) atomicAdd(&ghist[p * 256 + threadIdx.x], c);
+  }
 }
 
 template <class K>
-__global__ void __launch_bounds__(kThreads) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                        K* __restrict__ kout, uint32_t* __restrict__ vout, uint64_t n,
-                                                        int shift, const uint32_t* __restrict__ offs, uint64_t ntiles) {
+__global__ void __launch_bounds__(kThreads) k_rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                         K* __restrict__ kout, uint32_t* __restrict__ vout, uint64_t n,
+                                                         int pass, const uint32_t* __restrict__ ghist,
+                                                         unsigned long long* status, uint32_t* ctr, uint32_t epoch) {
   __shared__ uint32_t s_wc[kRsWarps][256];
+  __shared__ uint32_t s_base[256];
+  __shared__ uint32_t s_tile;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int shift = 8 * pass;
   for (int d = threadIdx.x; d < kRsWarps * 256; d += kThreads) (&s_wc[0][0])[d] = 0;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ctr, 1u);
   __syncthreads();
-  const uint64_t wbase = (uint64_t)blockIdx.x * kTile + (uint64_t)w * kRsPerWarp;
+  const uint32_t tile = s_tile;
+  const uint64_t wbase = (uint64_t)tile * kTile + (uint64_t)w * kRsPerWarp;
   K kk[kRsRounds];
   uint32_t vv[kRsRounds];
   uint32_t dd[kRsRounds];
 #pragma unroll
   for (int r = 0; r < kRsRounds; r++) {
-    uint64_t i = wbase + (uint64_t)r * 32 + lane;
-    bool ok = i < n;
+    const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+    const bool ok = i < n;
     kk[r] = ok ? kin[i] : (K)0;
     vv[r] = ok ? vin[i] : 0u;
     dd[r] = ok ? ((uint32_t)(kk[r] >> shift) & 255u) : 256u;
   }
 #pragma unroll
   for (int r = 0; r < kRsRounds; r++) {
-    uint32_t peers = __match_any_sync(0xffffffffu, dd[r]);
-    int leader = __ffs(peers) - 1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, dd[r]);
+    const int leader = __ffs(peers) - 1;
     if (lane == leader && dd[r] < 256u) s_wc[w][dd[r]] += __popc(peers);
     __syncwarp();
   }
   __syncthreads();
   {
     const int d = threadIdx.x;
-    uint32_t run = offs[(uint64_t)d * ntiles + blockIdx.x];
+    // exclusive prefix of the digit counts (global base of digit d in this pass)
+    uint32_t g = ghist[pass * 256 + d];
+    uint32_t tot;
+    const uint32_t gex = block_excl_scan<uint32_t, OpSum>(g, OpSum(), 0u, &tot);
+    uint32_t cnt = 0;
 #pragma unroll
     for (int ww = 0; ww < kRsWarps; ww++) {
-      uint32_t t = s_wc[ww][d];
-      s_wc[ww][d] = run;
-      run += t;
+      const uint32_t t = s_wc[ww][d];
+      s_wc[ww][d] = cnt;
+      cnt += t;
     }
+    const unsigned long long EP = (unsigned long long)epoch << 40;
+    unsigned long long* my = &status[(uint64_t)tile * 256 + d];
+    unsigned long long pre = 0;
+    if (tile == 0) {
+      atomicExch(my, EP | (2ull << 38) | cnt);
+    } else {
+      atomicExch(my, EP | (1ull << 38) | cnt);
+      int64_t p = (int64_t)tile - 1;
+      while (true) {
+        unsigned long long s;
+        do { s = ld_volatile_u64(&status[(uint64_t)p * 256 + d]); } while ((s >> 40) != epoch);
+        pre += s & ((1ull << 38) - 1);
+        if (((s >> 38) & 3ull) == 2ull) break;
+        p--;
+      }
+      atomicExch(my, EP | (2ull << 38) | (pre + cnt));
+    }
+    s_base[d] = gex + (uint32_t)pre;
   }
   __syncthreads();
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int r = 0; r < kRsRounds; r++) {
-    uint32_t d = dd[r];
-    uint32_t peers = __match_any_sync(0xffffffffu, d);
-    int leader = __ffs(peers) - 1;
+    const uint32_t d = dd[r];
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int leader = __ffs(peers) - 1;
     if (d < 256u) {
-      uint32_t pos = s_wc[w][d] + __popc(peers & lt);
+      const uint32_t pos = s_base[d] + s_wc[w][d] + __popc(peers & lt);
       kout[pos] = kk[r];
       vout[pos] = vv[r];
     }
@@ -237,27 +290,29 @@ __global__ void __launch_bounds__(kThreads) k_rs_scatter(const K* __restrict__ k
   }
 }
 
-inline uint64_t rs_counts_elems(uint64_t n) { return 256ull * ((n + kTile - 1) / kTile); }
+struct SortScratch {
+  uint32_t* ghist;              // kRsMaxPass * 256
+  unsigned long long* status;   // lb_tiles(n) * 256
+  uint32_t* ctrs;               // one zeroed counter per pass
+};
 
-// Sorts (keys,vals) by bits [0, nbits) of the key.  Ping-pongs between the
-// primary and alternate buffers; returns true if the result is in the
-// alternate buffers.  counts/scan_scratch sized by rs_counts_elems /
-// scan_scratch_elems(rs_counts_elems(n)).
+// Sorts (keys, vals) by key bits [0, nbits); returns true if the result is in
+// the alternate buffers.  ghist must be zeroed by the caller.
 template <class K>
-bool radix_sort(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint64_t n, int nbits, uint32_t* counts,
-                uint32_t* scan_scratch, cudaStream_t st) {
+bool radix_sort(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint64_t n, int nbits, SortScratch sc,
+                uint32_t epoch, cudaStream_t st) {
   if (n <= 1 || nbits <= 0) return false;
-  uint64_t ntiles = (n + kTile - 1) / kTile;
+  const int npass = (nbits + 7) / 8;
+  const uint64_t nt = lb_tiles(n);
+  GW_LAUNCH(k_rs_ghist<K>, (unsigned)std::min<uint64_t>(nt, 148ull * 8), kThreads, 0, st, keys, n, npass, sc.ghist);
   bool alt = false;
-  for (int shift = 0; shift < nbits; shift += 8) {
+  for (int p = 0; p < npass; p++) {
     const K* ki = alt ? keys_alt : keys;
     const uint32_t* vi = alt ? vals_alt : vals;
     K* ko = alt ? keys : keys_alt;
     uint32_t* vo = alt ? vals : vals_alt;
-    GW_LAUNCH(k_rs_hist<K>, (unsigned)ntiles, kThreads, 0, st, ki, n, shift, counts, ntiles);
-    device_scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, 256ull * ntiles,
-                                 scan_scratch, OpSum(), 0u, false, st);
-    GW_LAUNCH(k_rs_scatter<K>, (unsigned)ntiles, kThreads, 0, st, ki, vi, ko, vo, n, shift, counts, ntiles);
+    GW_LAUNCH(k_rs_onesweep<K>, (unsigned)nt, kThreads, 0, st, ki, vi, ko, vo, n, p, sc.ghist, sc.status, sc.ctrs + p,
+              epoch + (uint32_t)p);
     alt = !alt;
   }
   return alt;

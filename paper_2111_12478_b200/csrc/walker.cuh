@@ -41,7 +41,7 @@ namespace gw {
 
 constexpr uint32_t NIL = 0xFFFFFFFFu;
 constexpr uint32_t SC_DEV = 0xFFFFFFFFu;  // device scope
-constexpr int kWalkCH = 1024;              // events staged per chunk
+constexpr int kWalkCH = 2048;              // events staged per chunk
 constexpr int kAccSmem = 4096;             // barrier accumulator kept in smem up to this span
 
 // lflags bits (lock pre-pass)
