@@ -265,66 +265,111 @@ __global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const
   }
 }
 
-// _same_instruction_check, engine.py:81-95.  One thread per event j that
-// continues a record: it scans its record (coalesced across the warp: the
-// neighbours scan the same lines) and emits the pairs (i, j), i < j.
-// Uniform records (every parser wacc: same instr / atomic+scope / block,
-// strictly increasing tids) share one dedup key and one cover verdict per
-// location, so only the pair (first, second occurrence) can survive the
-// keep-first dedup; other records emit every pair.
+// _same_instruction_check, engine.py:81-95: ww(i, j) for events i < j of a
+// multi-event WRITE record on one location (distinct threads, !cover), before
+// the record's own events.  One warp per record: the warp owning the record
+// head's 32-event window loads the record (one event per lane, coalesced)
+// and matches locations with __match_any_sync.  Uniform records (every
+// parser wacc: same instr / atomic+scope / block, strictly increasing tids)
+// share one dedup key and one cover verdict per location, so only the pair
+// (first, second occurrence) can survive keep-first; others emit every pair.
 __device__ __forceinline__ bool rec_uniform_step(uint32_t prev, uint32_t cur, uint32_t iprev, uint32_t icur,
                                                  uint32_t BS) {
   return icur == iprev && ((cur ^ prev) & (GW_F_ATOMIC | GW_F_DEVICE | (7u << GW_OP_SHIFT))) == 0 &&
          ev_tid(cur) / BS == ev_tid(prev) / BS && ev_tid(cur) > ev_tid(prev);
 }
-__global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd) {
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < tr.n; j += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t tj = tr.tidop[j];
-    if (!(tj & GW_F_CONT) || ev_kind(tj) > GW_K_WRITE) continue;
-    const unsigned long long lj = tr.key[j];
-    // backward: head, matches, uniformity of [head, j]
-    uint64_t head = j, first = NIL;
-    uint32_t cnt = 0;
-    bool uni = true;
-    uint32_t nxt_to = tj, nxt_in = tr.instr[j];
-    while (head > 0) {
-      const uint64_t i = head - 1;
-      const uint32_t ti = tr.tidop[i];
-      const uint32_t ii = tr.instr[i];
-      uni = uni && rec_uniform_step(ti, nxt_to, ii, nxt_in, tr.BS);
-      if (ev_kind(ti) <= GW_K_WRITE && tr.key[i] == lj) { cnt++; first = i; }
-      head = i;
-      nxt_to = ti;
-      nxt_in = ii;
-      if (!(ti & GW_F_CONT)) break;
-    }
-    if (ev_kind(tr.tidop[head]) != GW_K_WRITE || cnt == 0) continue;
-    // forward: uniformity of the rest of the record
-    {
-      uint32_t pto = tj, pin = tr.instr[j];
-      for (uint64_t x = j + 1; uni && x < tr.n; x++) {
-        const uint32_t tx = tr.tidop[x];
-        if (!(tx & GW_F_CONT)) break;
-        const uint32_t ix = tr.instr[x];
-        uni = rec_uniform_step(pto, tx, pin, ix, tr.BS);
-        pto = tx;
-        pin = ix;
-      }
-    }
-    if (j - head >= 32768) { atomicOr(cd.err, ERR_RECORD); continue; }
-    if (uni) {
-      if (cnt != 1) continue;  // j is not the second occurrence of its location
-      const uint32_t ti = tr.tidop[first];
-      if (ev_tid(ti) == ev_tid(tj) || cover(ti, tj, tr.BS)) continue;
-      emit_cand(cd, ((unsigned long long)head << 32) | ((first - head) << 15) | (j - head), lj, (uint32_t)first,
+__device__ __forceinline__ unsigned long long sub_pair(uint64_t i, uint64_t j) {
+  return ((unsigned long long)i << 15) | (unsigned long long)j;
+}
+// slow path for records longer than 32 events: event j scans its record
+__device__ void same_instr_long(const DevTrace& tr, const Cands& cd, uint64_t head, uint64_t end, uint64_t j,
+                                bool uni) {
+  const uint32_t tj = tr.tidop[j];
+  if (ev_kind(tj) > GW_K_WRITE) return;
+  const unsigned long long lj = tr.key[j];
+  uint32_t cnt = 0;
+  uint64_t first = 0;
+  for (uint64_t i = head; i < j; i++) {
+    const uint32_t ti = tr.tidop[i];
+    if (ev_kind(ti) > GW_K_WRITE || tr.key[i] != lj) continue;
+    cnt++;
+    if (cnt == 1) first = i;
+    if (!uni && ev_tid(ti) != ev_tid(tj) && !cover(ti, tj, tr.BS))
+      emit_cand(cd, ((unsigned long long)head << 32) | sub_pair(i - head, j - head), lj, (uint32_t)i, (uint32_t)j,
+                GW_WW);
+  }
+  if (uni && cnt == 1) {
+    const uint32_t ti = tr.tidop[first];
+    if (ev_tid(ti) != ev_tid(tj) && !cover(ti, tj, tr.BS))
+      emit_cand(cd, ((unsigned long long)head << 32) | sub_pair(first - head, j - head), lj, (uint32_t)first,
                 (uint32_t)j, GW_WW);
-    } else {
-      for (uint64_t i = head; i < j; i++) {
-        const uint32_t ti = tr.tidop[i];
-        if (ev_kind(ti) > GW_K_WRITE || tr.key[i] != lj) continue;
-        if (ev_tid(ti) == ev_tid(tj) || cover(ti, tj, tr.BS)) continue;
-        emit_cand(cd, ((unsigned long long)head << 32) | ((i - head) << 15) | (j - head), lj, (uint32_t)i,
-                  (uint32_t)j, GW_WW);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t wb = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; wb < tr.n; wb += nwarps * 32) {
+    // heads of multi-event WRITE records in this window
+    const uint64_t e = wb + lane;
+    bool is_head = false;
+    if (e + 1 < tr.n) {
+      const uint32_t t0 = tr.tidop[e];
+      is_head = !(t0 & GW_F_CONT) && ev_kind(t0) == GW_K_WRITE && (tr.tidop[e + 1] & GW_F_CONT);
+    }
+    uint32_t heads = __ballot_sync(0xffffffffu, is_head);
+    while (heads) {
+      const int hl = __ffs(heads) - 1;
+      heads &= heads - 1;
+      const uint64_t head = wb + hl;
+      // load the record, 32 events at a time
+      const uint64_t x = head + lane;
+      const bool inr = x < tr.n;
+      const uint32_t tx = inr ? tr.tidop[x] : 0u;
+      const uint32_t cm = __ballot_sync(0xffffffffu, inr && (tx & GW_F_CONT)) | 1u;  // lane 0 is the head
+      const uint32_t stop = ~cm;                                                    // first non-CONT lane
+      const int len = stop ? __ffs(stop) - 1 : 32;
+      const uint32_t ix = inr ? tr.instr[x] : 0u;
+      const uint32_t tprev = __shfl_up_sync(0xffffffffu, tx, 1);
+      const uint32_t iprev = __shfl_up_sync(0xffffffffu, ix, 1);
+      const bool stepok = lane == 0 || lane >= len || rec_uniform_step(tprev, tx, iprev, ix, tr.BS);
+      bool uni = __all_sync(0xffffffffu, stepok);
+      if (len == 32 && head + 32 < tr.n && (tr.tidop[head + 32] & GW_F_CONT)) {
+        // long record (> 32 events): per-event scan, record by record
+        uint64_t end = head + 32;
+        while (end < tr.n && (tr.tidop[end] & GW_F_CONT)) end++;
+        if (end - head >= 32768) {
+          if (lane == 0) atomicOr(cd.err, ERR_RECORD);
+          continue;
+        }
+        bool u2 = uni;
+        for (uint64_t c = head + 32 + lane; c < end; c += 32)
+          u2 = u2 && rec_uniform_step(tr.tidop[c - 1], tr.tidop[c], tr.instr[c - 1], tr.instr[c], tr.BS);
+        uni = __all_sync(0xffffffffu, u2);
+        for (uint64_t j = head + 1 + lane; j < end; j += 32) same_instr_long(tr, cd, head, end, j, uni);
+        continue;
+      }
+      const bool acc = lane < len && ev_kind(tx) <= GW_K_WRITE;
+      const unsigned long long kx = acc ? tr.key[x] : 0ull;
+      const uint32_t accm = __ballot_sync(0xffffffffu, acc);
+      const uint32_t peers = __match_any_sync(0xffffffffu, kx) & accm;
+      const uint32_t earlier = peers & lanemask_lt();
+      if (!acc || !earlier) continue;
+      if (uni) {
+        if (__popc(earlier) != 1) continue;  // not the second occurrence of this location
+        const int fl = __ffs(earlier) - 1;
+        const uint32_t tf = tr.tidop[head + fl];
+        if (ev_tid(tf) != ev_tid(tx) && !cover(tf, tx, tr.BS))
+          emit_cand(cd, ((unsigned long long)head << 32) | sub_pair(fl, lane), kx, (uint32_t)(head + fl),
+                    (uint32_t)x, GW_WW);
+      } else {
+        for (uint32_t m = earlier; m; m &= m - 1) {
+          const int il = __ffs(m) - 1;
+          const uint32_t ti = tr.tidop[head + il];
+          if (ev_tid(ti) != ev_tid(tx) && !cover(ti, tx, tr.BS))
+            emit_cand(cd, ((unsigned long long)head << 32) | sub_pair(il, lane), kx, (uint32_t)(head + il),
+                      (uint32_t)x, GW_WW);
+        }
       }
     }
   }
@@ -356,16 +401,23 @@ __global__ void k_dedup_insert(DedupArgs d) {
     atomicMin(&d.smin[h], d.c.okey[k]);
   }
 }
-__global__ void k_dedup_select(DedupArgs d, unsigned long long* skeys, uint32_t* svals, uint32_t* nsurv) {
+// survivors keep their order key, losers get the sort sentinel (they sort last)
+__global__ void k_dedup_select(DedupArgs d, unsigned long long sentinel, unsigned long long* skeys, uint32_t* svals,
+                               uint32_t* nsurv) {
+  uint32_t cnt = 0;
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < d.ncand; k += gridDim.x * blockDim.x) {
-    if (d.c.okey[k] == d.smin[d.cslot[k]]) {
-      uint32_t i = atomicAdd(nsurv, 1u);
-      skeys[i] = d.c.okey[k];
-      svals[i] = k;
-    }
+    const unsigned long long ok = d.c.okey[k];
+    const bool surv = ok == d.smin[d.cslot[k]];
+    skeys[k] = surv ? ok : sentinel;
+    svals[k] = k;
+    cnt += surv;
   }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nsurv, cnt);
 }
-__global__ void k_final(Cands c, const uint32_t* svals, uint32_t n, uint8_t* okind, uint32_t* oprior, uint32_t* ocur) {
+__global__ void k_final(Cands c, const uint32_t* svals, const uint32_t* nsurv, uint8_t* okind, uint32_t* oprior,
+                        uint32_t* ocur) {
+  const uint32_t n = *nsurv;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint32_t k = svals[j];
     okind[j] = (uint8_t)c.kind[k];

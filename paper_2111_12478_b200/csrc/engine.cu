@@ -79,7 +79,26 @@ struct gw_ctx {
   uint32_t* d_cur = nullptr;
   Diag* d_diags = nullptr;
   gw_stats stats{};
+  bool stats_pending = false;
   uint32_t launches = 0;
+  uint32_t* d_scal = nullptr;   // device scalars: [3..6] rec/log/diag tops, err
+  uint32_t* d_nsurv = nullptr;  // device report count
+  uint32_t ncand = 0;
+  uint64_t arena_words = 0;
+  cudaStream_t last_stream = 0;
+
+  void finish_stats() {
+    if (!stats_pending) return;
+    stats_pending = false;
+    CK(cudaEventSynchronize(ev[5]));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[5])); stats.ms_total = ms;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); stats.ms_prep = ms;
+    CK(cudaEventElapsedTime(&ms, ev[1], ev[2])); stats.ms_walker = ms;
+    CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); stats.ms_sort = ms;
+    CK(cudaEventElapsedTime(&ms, ev[3], ev[4])); stats.ms_check = ms;
+    CK(cudaEventElapsedTime(&ms, ev[4], ev[5])); stats.ms_final = ms;
+  }
 
   uint32_t epoch = 1;  // look-back flag epochs (never reused within 2^24 passes)
 
@@ -184,6 +203,10 @@ struct Pipeline {
     for (int i = 0; i < 8; i++)
       if (!C->ev[i]) CK(cudaEventCreate(&C->ev[i]));
     CK(cudaEventRecord(C->ev[0], st));
+    C->d_scal = nullptr;
+    C->d_nsurv = nullptr;
+    C->stats_pending = false;
+    C->last_stream = st;
     if (N == 0) {
       C->launches = 0;
       return;
@@ -475,7 +498,12 @@ struct Pipeline {
     CK(cudaEventRecord(C->ev[4], st));
 
     // ------------------------------------------------------- dedup / final
-    uint32_t nsurv = 0;
+    // no host sync from here on: counts stay on the device until gw_ctx_fetch
+    uint32_t* d_nsurv = out_n + 2;
+    C->d_scal = scal;
+    C->d_nsurv = d_nsurv;
+    C->n_reports = 0;
+    C->ncand = ncand;
     if (ncand > 0) {
       uint64_t tcap = pow2_at_least(2ull * ncand);
       DedupArgs d;
@@ -491,38 +519,22 @@ struct Pipeline {
       GW_LAUNCH(k_dedup_insert, grid_for(ncand), kThreads, 0, st, d);
       unsigned long long* sk = C->get<unsigned long long>("sv_k", ncand);
       uint32_t* sv = C->get<uint32_t>("sv_v", ncand);
-      GW_LAUNCH(k_dedup_select, grid_for(ncand), kThreads, 0, st, d, sk, sv, out_n + 2);
+      const int kbits = 32 + ceil_log2(N + 1);
+      const unsigned long long sentinel = (kbits >= 64) ? ~0ull : ((1ull << kbits) - 1);
+      GW_LAUNCH(k_dedup_select, grid_for(ncand), kThreads, 0, st, d, sentinel, sk, sv, d_nsurv);
+      sort<unsigned long long>(sk, sv, ncand, kbits, "sv");
+      C->d_kind = C->get<uint8_t>("o_kind", ncand);
+      C->d_prior = C->get<uint32_t>("o_prior", ncand);
+      C->d_cur = C->get<uint32_t>("o_cur", ncand);
+      GW_LAUNCH(k_final, grid_for(ncand), kThreads, 0, st, cd, sv, d_nsurv, C->d_kind, C->d_prior, C->d_cur);
       check_launch();
-      d2h(&nsurv, out_n + 2);
-      sort<unsigned long long>(sk, sv, nsurv, 32 + ceil_log2(N + 1), "sv");
-      C->d_kind = C->get<uint8_t>("o_kind", nsurv);
-      C->d_prior = C->get<uint32_t>("o_prior", nsurv);
-      C->d_cur = C->get<uint32_t>("o_cur", nsurv);
-      GW_LAUNCH(k_final, grid_for(nsurv), kThreads, 0, st, cd, sv, nsurv, C->d_kind, C->d_prior, C->d_cur);
     }
-    C->n_reports = nsurv;
-    uint32_t tail[4];
-    d2h(tail, scal + 3, 4);  // rec_top, log_top, diag_top, err
-    if (tail[3]) {
-      char buf[160];
-      snprintf(buf, sizeof buf,
-               "engine capacity error flags 0x%x (arena %llu words; dense lock clocks need more memory?)",
-               tail[3], (unsigned long long)arena_words);
-      throw CudaErr{GW_E_NOMEM, buf};
-    }
-    C->n_diags = tail[2];
     C->d_diags = w.diags;
+    C->arena_words = arena_words;
     CK(cudaEventRecord(C->ev[5], st));
-    CK(cudaEventSynchronize(C->ev[5]));
-    float ms;
-    CK(cudaEventElapsedTime(&ms, C->ev[0], C->ev[5])); S.ms_total = ms;
-    CK(cudaEventElapsedTime(&ms, C->ev[0], C->ev[1])); S.ms_prep = ms;
-    CK(cudaEventElapsedTime(&ms, C->ev[1], C->ev[2])); S.ms_walker = ms;
-    CK(cudaEventElapsedTime(&ms, C->ev[2], C->ev[3])); S.ms_sort = ms;
-    CK(cudaEventElapsedTime(&ms, C->ev[3], C->ev[4])); S.ms_check = ms;
-    CK(cudaEventElapsedTime(&ms, C->ev[4], C->ev[5])); S.ms_final = ms;
     S.n_sync = hs.n_acq + hs.n_rel + hs.n_end + hs.n_bar;
     C->launches = g_launches;
+    C->stats_pending = true;
   }
 };
 
@@ -632,20 +644,38 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
   if (!c || !out) { gw_set_error("null argument"); return GW_E_ARG; }
   memset(out, 0, sizeof *out);
   return guarded([&] {
-    const uint64_t n = c->n_reports;
+    CK(cudaSetDevice(c->device));
+    uint64_t n = 0, nd = 0;
+    if (c->d_scal) {
+      uint32_t tail[4] = {0, 0, 0, 0}, ns = 0;
+      CK(cudaMemcpyAsync(tail, c->d_scal + 3, sizeof tail, cudaMemcpyDeviceToHost, c->last_stream));
+      CK(cudaMemcpyAsync(&ns, c->d_nsurv, sizeof ns, cudaMemcpyDeviceToHost, c->last_stream));
+      CK(cudaStreamSynchronize(c->last_stream));
+      if (tail[3]) {
+        char buf[200];
+        snprintf(buf, sizeof buf,
+                 "engine capacity error flags 0x%x (arena %llu words; dense lock clocks need more memory?)", tail[3],
+                 (unsigned long long)c->arena_words);
+        throw CudaErr{GW_E_NOMEM, buf};
+      }
+      n = c->ncand ? ns : 0;
+      nd = tail[2];
+    }
+    c->n_reports = n;
+    c->n_diags = nd;
     out->n_reports = n;
     out->kind = (uint8_t*)malloc(std::max<uint64_t>(n, 1));
     out->prior_event = (uint32_t*)malloc(4 * std::max<uint64_t>(n, 1));
     out->current_event = (uint32_t*)malloc(4 * std::max<uint64_t>(n, 1));
     if (!out->kind || !out->prior_event || !out->current_event) throw std::bad_alloc();
-    if (n) {
-      CK(cudaMemcpy(out->kind, c->d_kind, n, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(out->prior_event, c->d_prior, 4 * n, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(out->current_event, c->d_cur, 4 * n, cudaMemcpyDeviceToHost));
-    }
-    const uint64_t nd = c->n_diags;
     std::vector<Diag> dg(nd);
-    if (nd) CK(cudaMemcpy(dg.data(), c->d_diags, sizeof(Diag) * nd, cudaMemcpyDeviceToHost));
+    if (n) {
+      CK(cudaMemcpyAsync(out->kind, c->d_kind, n, cudaMemcpyDeviceToHost, c->last_stream));
+      CK(cudaMemcpyAsync(out->prior_event, c->d_prior, 4 * n, cudaMemcpyDeviceToHost, c->last_stream));
+      CK(cudaMemcpyAsync(out->current_event, c->d_cur, 4 * n, cudaMemcpyDeviceToHost, c->last_stream));
+    }
+    if (nd) CK(cudaMemcpyAsync(dg.data(), c->d_diags, sizeof(Diag) * nd, cudaMemcpyDeviceToHost, c->last_stream));
+    CK(cudaStreamSynchronize(c->last_stream));
     std::sort(dg.begin(), dg.end(), [](const Diag& a, const Diag& b) {
       return a.ev != b.ev ? a.ev < b.ev : a.sub < b.sub;
     });
@@ -675,8 +705,10 @@ extern "C" void gw_result_free(gw_result* r) {
 
 extern "C" int gw_ctx_stats(gw_ctx* c, gw_stats* out) {
   if (!c || !out) return GW_E_ARG;
-  *out = c->stats;
-  return GW_OK;
+  return guarded([&] {
+    c->finish_stats();
+    *out = c->stats;
+  });
 }
 
 extern "C" uint32_t gw_ctx_launches(gw_ctx* c) { return c ? c->launches : 0; }

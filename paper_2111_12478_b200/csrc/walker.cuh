@@ -739,11 +739,23 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
     if (threadIdx.x == 0) s_nh = 0;
     __syncthreads();
     // stage events; collect the hard ones (barrier, acq, rel, end, in-CS access)
-    for (uint32_t j = threadIdx.x; j < cnt; j += kThreads) {
-      uint32_t e = a.perm ? a.perm[cb + j] : (uint32_t)(cb + j);
-      uint32_t to = tr.tidop[e];
-      s_e[j] = e;
-      s_to[j] = to;
+    {
+      // unrolled so every thread has kWalkCH/kThreads independent loads in flight
+      constexpr int IPT = kWalkCH / kThreads;
+      uint32_t ee[IPT];
+#pragma unroll
+      for (int k = 0; k < IPT; k++) {
+        const uint32_t j = threadIdx.x + k * kThreads;
+        ee[k] = j < cnt ? (a.perm ? __ldg(a.perm + cb + j) : (uint32_t)(cb + j)) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < IPT; k++) {
+        const uint32_t j = threadIdx.x + k * kThreads;
+        if (j < cnt) {
+          s_e[j] = ee[k];
+          s_to[j] = __ldg(tr.tidop + ee[k]);
+        }
+      }
     }
     __syncthreads();
     // ordered compaction of hard positions (block scan over 4 items/thread)
@@ -773,13 +785,27 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
     for (uint32_t hi = 0; hi <= nh; hi++) {
       const uint32_t h = s_hard[hi];
       // plain accesses in [pos, h): stamp (time, vobj) from the owner's state
-      for (uint32_t j = pos + threadIdx.x; j < h; j += kThreads) {
-        uint32_t to = s_to[j];
-        if (ev_kind(to) <= GW_K_WRITE) {
-          uint32_t t = ev_tid(to), e = s_e[j];
-          a.time[e] = a.local[t];
-          a.vobj[e] = a.pobj[t];
+      for (uint32_t j0 = pos; j0 < h; j0 += 4 * kThreads) {
+        uint32_t tt[4], lv[4], ov[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const uint32_t j = j0 + threadIdx.x + k * kThreads;
+          tt[k] = NIL;
+          if (j < h) {
+            const uint32_t to = s_to[j];
+            if (ev_kind(to) <= GW_K_WRITE) tt[k] = ev_tid(to);
+          }
         }
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (tt[k] != NIL) { lv[k] = a.local[tt[k]]; ov[k] = a.pobj[tt[k]]; }
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (tt[k] != NIL) {
+            const uint32_t e = s_e[j0 + threadIdx.x + k * kThreads];
+            a.time[e] = lv[k];
+            a.vobj[e] = ov[k];
+          }
       }
       __syncthreads();
       if (h < cnt) {
