@@ -233,9 +233,13 @@ struct Pipeline {
     uint64_t gmax = (uint64_t)std::max(occ, 1) * C->num_sms;
     const uint32_t G = (uint32_t)std::min<uint64_t>(tr.B, gmax);
     S.walker_ctas = G;
+    // snapshot mode: lock-free and the per-hard-event block snapshots are small
+    const uint64_t n_hard = hs.n_bar + hs.n_end;
+    const uint64_t snap_entries = (n_hard + tr.B) * (uint64_t)tr.BS;
+    const bool snap_mode = !has_locks && snap_entries * 8 <= std::max<uint64_t>(256ull << 20, 8 * N);
     uint32_t* part_key = nullptr;
     uint32_t* perm = nullptr;
-    if (G > 1) {
+    if (G > 1 && !snap_mode) {
       part_key = C->get<uint32_t>("part_k", N);
       perm = C->get<uint32_t>("part_v", N);
       GW_LAUNCH(k_part_keys, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
@@ -349,7 +353,33 @@ struct Pipeline {
     }
     if (has_locks || tr.BS > (uint32_t)kAccSmem) w.scratch = C->get<uint32_t>("scratch", (uint64_t)G * 3 * T);
     GW_LAUNCH(k_state_init, grid_for(T), kThreads, 0, st, w);
-    GW_LAUNCH(k_walker, G, kThreads, 0, st, w);
+    if (snap_mode) {
+      SnapArgs sa;
+      uint32_t* hflag = C->get<uint32_t>("hd_flag", N);
+      GW_LAUNCH(k_hard_mark, grid_for(N), kThreads, 0, st, tr, hflag);
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hflag}, ArrStore<uint32_t>{hflag}, N, OpSum(), 0u, false, "sc_u32");
+      uint32_t* hkey = C->get<uint32_t>("hd_key", n_hard + 1);
+      uint32_t* hev = C->get<uint32_t>("hd_ev", n_hard + 1);
+      uint32_t* hbeg = C->get<uint32_t>("hd_beg", tr.B);
+      uint32_t* hend = C->get<uint32_t>("hd_end", tr.B);
+      uint32_t* hcnt = C->get<uint32_t>("hd_cnt", tr.B);
+      CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
+      if (n_hard) {
+        GW_LAUNCH(k_hard_compact, grid_for(N), kThreads, 0, st, tr, hflag, hkey, hev, hcnt);
+        sort<uint32_t>(hkey, hev, n_hard, ceil_log2(tr.B), "hd");
+      }
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hcnt}, HardSegStore{hcnt, hbeg, hend}, tr.B, OpSum(), 0u, false,
+                            "sc_u32");
+      sa.hard_ev = hev;
+      sa.hb_beg = hbeg;
+      sa.hb_end = hend;
+      sa.snap = C->get<uint2>("snap", snap_entries);
+      GW_LAUNCH(k_walker_snap, std::min<uint32_t>(tr.B, (uint32_t)gmax), kThreads, 0, st, w, sa);
+      GW_LAUNCH(k_stamp, grid_for(N), kThreads, 0, st, w, sa);
+      S.walker_ctas = std::min<uint32_t>(tr.B, (uint32_t)gmax);
+    } else {
+      GW_LAUNCH(k_walker, G, kThreads, 0, st, w);
+    }
     check_launch();
     CK(cudaEventRecord(C->ev[2], st));
 
@@ -519,10 +549,16 @@ struct Pipeline {
       GW_LAUNCH(k_dedup_insert, grid_for(ncand), kThreads, 0, st, d);
       unsigned long long* sk = C->get<unsigned long long>("sv_k", ncand);
       uint32_t* sv = C->get<uint32_t>("sv_v", ncand);
-      const int kbits = 32 + ceil_log2(N + 1);
-      const unsigned long long sentinel = (kbits >= 64) ? ~0ull : ((1ull << kbits) - 1);
-      GW_LAUNCH(k_dedup_select, grid_for(ncand), kThreads, 0, st, d, sentinel, sk, sv, d_nsurv);
-      sort<unsigned long long>(sk, sv, ncand, kbits, "sv");
+      uint32_t* ccnt = C->get<uint32_t>("sv_cnt", N);
+      CK(cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * N, st));
+      uint32_t* coff = C->get<uint32_t>("sv_off", N);
+      uint32_t* big = C->get<uint32_t>("sv_big", ncand / (kGroupSmall + 1) + 1);
+      uint32_t* nbig = zeroed(1);
+      GW_LAUNCH(k_dedup_count, grid_for(ncand), kThreads, 0, st, d, ccnt, d_nsurv);
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{ccnt}, ArrStore<uint32_t>{coff}, N, OpSum(), 0u, false, "sc_u32");
+      GW_LAUNCH(k_dedup_place, grid_for(ncand), kThreads, 0, st, d, ccnt, coff, sk, sv);
+      GW_LAUNCH(k_group_sort, grid_for(N), kThreads, 0, st, coff, N, d_nsurv, sk, sv, big, nbig);
+      GW_LAUNCH(k_group_sort_big, 148u, kThreads, 0, st, coff, N, d_nsurv, sk, sv, big, nbig);
       C->d_kind = C->get<uint8_t>("o_kind", ncand);
       C->d_prior = C->get<uint32_t>("o_prior", ncand);
       C->d_cur = C->get<uint32_t>("o_cur", ncand);

@@ -850,6 +850,96 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
   }
 }
 
+// ---------------------------------------------- snapshot mode (lock-free) --
+// Lock-free traces: blocks never interact, and plain accesses only read
+// their thread's state.  The walker then visits only the hard events
+// (barriers, ENDs) of each block -- a few per block -- and writes the whole
+// block state {local, pred object} after each one; k_stamp stamps every
+// access in parallel from snapshot k = #hard events of its block before it.
+struct SnapArgs {
+  const uint32_t* hard_ev;   // hard event indices grouped by block, trace order within a block
+  const uint32_t* hb_beg;    // per block [beg, end) into hard_ev
+  const uint32_t* hb_end;
+  uint2* snap;               // per block: (K_b + 1) x BS entries at (hb_beg[b] + b) * BS
+};
+
+__global__ void __launch_bounds__(kThreads) k_walker_snap(WalkArgs a, SnapArgs s) {
+  __shared__ uint32_t s_acc[kAccSmem];
+  const DevTrace& tr = a.tr;
+  for (uint32_t b = blockIdx.x; b < tr.B; b += gridDim.x) {
+    const uint32_t beg = s.hb_beg[b], end = s.hb_end[b];
+    uint2* sp = s.snap + (size_t)(beg + b) * tr.BS;
+    const uint32_t t0 = b * tr.BS;
+    for (uint32_t j = threadIdx.x; j < tr.BS; j += kThreads) sp[j] = make_uint2(a.local[t0 + j], a.pobj[t0 + j]);
+    for (uint32_t h = beg; h < end; h++) {
+      const uint32_t e = s.hard_ev[h];
+      const uint32_t to = tr.tidop[e];
+      __syncthreads();
+      if (ev_kind(to) == GW_K_BARRIER) {
+        do_barrier(a, to, tr.instr[e], s_acc);
+      } else {  // END (lock-free: no frames)
+        if (threadIdx.x == 0) {
+          const uint32_t t = ev_tid(to);
+          a.exited[t] = 1;
+          a.nend[t] = a.nend[t] + 1;
+        }
+        __syncthreads();
+      }
+      sp += tr.BS;
+      for (uint32_t j = threadIdx.x; j < tr.BS; j += kThreads) sp[j] = make_uint2(a.local[t0 + j], a.pobj[t0 + j]);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_stamp(WalkArgs a, SnapArgs s) {
+  const DevTrace& tr = a.tr;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t to = __ldg(tr.tidop + e);
+    if (ev_kind(to) > GW_K_WRITE) continue;
+    const uint32_t t = ev_tid(to), b = t / tr.BS;
+    uint32_t lo = __ldg(s.hb_beg + b), hi = __ldg(s.hb_end + b);
+    const uint32_t base = lo;
+    while (lo < hi) {  // #hard events of block b before e
+      const uint32_t m = (lo + hi) >> 1;
+      if (__ldg(s.hard_ev + m) < (uint32_t)e) lo = m + 1; else hi = m;
+    }
+    const uint2 st = s.snap[(size_t)(base + b + (lo - base)) * tr.BS + (t - b * tr.BS)];
+    a.time[e] = st.x;
+    a.vobj[e] = st.y;
+  }
+}
+
+__global__ void k_hard_mark(DevTrace tr, uint32_t* flag) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = ev_kind(tr.tidop[e]);
+    flag[e] = (k == GW_K_BARRIER || k == GW_K_END) ? 1u : 0u;
+  }
+}
+__global__ void k_hard_compact(DevTrace tr, const uint32_t* pos, uint32_t* hkey, uint32_t* hev, uint32_t* hcnt) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t to = tr.tidop[e];
+    const uint32_t k = ev_kind(to);
+    if (k == GW_K_BARRIER || k == GW_K_END) {
+      const uint32_t p = pos[e];
+      const uint32_t b = ev_tid(to) / tr.BS;
+      hkey[p] = b;
+      hev[p] = (uint32_t)e;
+      atomicAdd(hcnt + b, 1u);
+    }
+  }
+}
+// exclusive scan of per-block hard-event counts -> [beg, end)
+struct HardSegStore {
+  const uint32_t* cnt;
+  uint32_t* beg;
+  uint32_t* end;
+  __device__ __forceinline__ void operator()(uint64_t i, const uint32_t& v) const {
+    beg[i] = v;
+    end[i] = v + cnt[i];
+  }
+};
+
 __global__ void k_state_init(WalkArgs a) {
   for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < a.tr.T;
        u += (uint64_t)gridDim.x * blockDim.x) {

@@ -112,3 +112,29 @@ def test_prefix_consistency_c2(ctx):
         assert np.array_equal(got["prior"], full["prior"][keep])
         assert np.array_equal(got["current"], full["current"][keep])
         assert np.array_equal(got["kind"], full["kind"][keep])
+
+
+def _many_readers_text(nthreads=300, seed=0):
+    import random
+
+    rng = random.Random(seed)
+    lines = ["config blocks=4 warps=4 lanes=32"]
+    tids = [(b, w, l) for b in range(4) for w in range(4) for l in range(32)]
+    rng.shuffle(tids)
+    for i, (b, w, l) in enumerate(tids[:nthreads]):
+        lines.append(f"{b}.{w}.{l} rd g:0x10 instr {1000 + i}")
+        if rng.random() < 0.3:
+            lines.append(f"{b}.{w}.{l} rd g:0x10 instr {5000 + i}")
+    b, w, l = tids[-1]
+    lines.append(f"{b}.{w}.{l} wr g:0x10 instr 7")
+    lines.append(f"wacc 1 1 0xffffffff wr " + ",".join(["g:0x10"] * 32) + " instr 8")
+    return "\n".join(lines) + "\n"
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_many_reports_at_one_event(ctx, seed):
+    """> 64 surviving reports at one current event (the big-group ordering path)."""
+    tr = parse_trace(_many_readers_text(120 + 150 * seed, seed))
+    got = ndjson_lines(tr, _run(ctx, tr))
+    assert got == ndjson_lines(tr, O.run_trace(tr))
+    assert len(got) > 100
