@@ -88,10 +88,12 @@ typedef struct gw_trace_view { /* caller-owned SoA; host or device pointers */
   const uint32_t* instr;
 } gw_trace_view;
 
+#define GW_OPT_EAGER 1u /* never capture / replay a CUDA graph for this analysis */
+
 typedef struct gw_opts {
   uint32_t inactive_opt; /* GwcpDetector(inactive_opt=...), gwcp.py:108-127 */
-  uint32_t flags;        /* reserved, 0 */
-  void* stream;          /* cudaStream_t to launch on (NULL = legacy default) */
+  uint32_t flags;        /* GW_OPT_* */
+  void* stream;          /* cudaStream_t to launch on (NULL = legacy default; never graph-replayed) */
 } gw_opts;
 
 typedef struct gw_result { /* library-owned; reports in final order */
@@ -128,7 +130,11 @@ int gw_analyze(const gw_trace_view* host_trace, const gw_opts* opts, gw_result* 
 void gw_result_free(gw_result* r);
 const char* gw_last_error(void);
 
-/* device-resident context API: buffers persist across calls */
+/* device-resident context API: buffers persist across calls.  Lock-free
+ * traces analysed repeatedly with the same shape, input buffers and
+ * (non-default) stream are replayed from a captured CUDA graph; the plan is
+ * re-verified on the device and a mismatch falls back to an eager run inside
+ * gw_ctx_fetch, so results never depend on the cache. */
 gw_ctx* gw_ctx_create(int device);
 void gw_ctx_destroy(gw_ctx* c);
 /* dev_trace points at device memory; enqueues on opts->stream; results stay on device */

@@ -26,6 +26,7 @@ F_DEVICE = 1 << 28
 F_WARPBAR = 1 << 29
 F_CONT = 1 << 30
 SHARED_BIT = 1 << 63
+OPT_EAGER = 1
 
 
 class NativeUnavailable(RuntimeError):
@@ -270,17 +271,18 @@ class Context:
         except Exception:
             pass
 
-    def analyze_host(self, cfg, key, tidop, instr, *, inactive_opt=True, stream=None) -> None:
+    def analyze_host(self, cfg, key, tidop, instr, *, inactive_opt=True, stream=None, eager=False) -> None:
         v = _view(cfg, key, tidop, instr)
-        o = _Opts(1 if inactive_opt else 0, 0, stream)
+        o = _Opts(1 if inactive_opt else 0, OPT_EAGER if eager else 0, stream)
         _check(self._L.gw_ctx_analyze_host(self._c, C.byref(v), C.byref(o)))
 
-    def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None) -> None:
+    def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None,
+                       eager=False) -> None:
         v = _View()
         v.cfg.blocks, v.cfg.warps, v.cfg.lanes = cfg
         v.n_events = n
         v.key, v.tidop, v.instr = key_ptr, tidop_ptr, instr_ptr
-        o = _Opts(1 if inactive_opt else 0, 0, stream)
+        o = _Opts(1 if inactive_opt else 0, OPT_EAGER if eager else 0, stream)
         _check(self._L.gw_ctx_analyze_device(self._c, C.byref(v), C.byref(o)))
 
     def fetch(self):

@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(kThreads) k_check(CheckArgs a) {
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = a.vals[i];
     const uint32_t toc = a.sto[i];
+    if (ev_kind(toc) > GW_K_WRITE) continue;  // non-access events sort last (sentinel key)
     const uint32_t tc = ev_tid(toc);
     const bool isw = ev_kind(toc) == GW_K_WRITE;
     const uint32_t ss = a.segst[i];
@@ -383,10 +384,13 @@ struct DedupArgs {
   unsigned long long* smin;   // slot -> min order key
   uint32_t* cslot;            // candidate -> slot
   uint32_t mask;
-  uint32_t ncand;
+  uint32_t ncand;     // capacity the grids are sized for
+  const uint32_t* dn; // device candidate count
 };
+__device__ __forceinline__ uint32_t dd_count(const DedupArgs& d) { return min(*d.dn, d.ncand); }
 __global__ void k_dedup_insert(DedupArgs d) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < d.ncand; k += gridDim.x * blockDim.x) {
+  const uint32_t nc = dd_count(d);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
     const unsigned long long loc = d.c.loc[k];
     const uint32_t ip = d.instr[d.c.prior[k]], ic = d.instr[d.c.cur[k]];
     uint32_t h = (uint32_t)mix64(loc ^ mix64(((unsigned long long)ip << 32) | ic)) & d.mask;
@@ -408,7 +412,8 @@ __global__ void k_dedup_insert(DedupArgs d) {
 // ordered by the low 32 key bits.
 __global__ void k_dedup_count(DedupArgs d, uint32_t* ccnt, uint32_t* nsurv) {
   uint32_t cnt = 0;
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < d.ncand; k += gridDim.x * blockDim.x) {
+  const uint32_t nc = dd_count(d);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
     const unsigned long long ok = d.c.okey[k];
     if (ok == d.smin[d.cslot[k]]) {
       atomicAdd(ccnt + (ok >> 32), 1u);
@@ -420,7 +425,8 @@ __global__ void k_dedup_count(DedupArgs d, uint32_t* ccnt, uint32_t* nsurv) {
 }
 __global__ void k_dedup_place(DedupArgs d, uint32_t* ccnt, const uint32_t* coff, unsigned long long* sk,
                               uint32_t* sv) {
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < d.ncand; k += gridDim.x * blockDim.x) {
+  const uint32_t nc = dd_count(d);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
     const unsigned long long ok = d.c.okey[k];
     if (ok == d.smin[d.cslot[k]]) {
       const uint32_t c = (uint32_t)(ok >> 32);

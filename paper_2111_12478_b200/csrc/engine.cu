@@ -61,6 +61,23 @@ inline unsigned grid_for(uint64_t n, unsigned cap = 148u * 16u) {
 
 }  // namespace
 
+// Plan of a lock-free analysis, cached so that repeated analyses of traces
+// with the same shape replay one CUDA graph (no host syncs, no per-kernel
+// launch cost).  Every value the eager pipeline reads back from the device
+// is fixed here and re-verified ON the device by k_plan_check / k_guard; a
+// mismatch raises the abort flag and gw_ctx_fetch re-runs eagerly.
+struct Plan {
+  bool valid = false;
+  uint64_t N = 0;
+  uint32_t B = 0, W = 0, L = 0, inactive_opt = 1;
+  const void *key = nullptr, *tidop = nullptr, *instr = nullptr;
+  cudaStream_t stream = 0;
+  unsigned long long n_bar = 0, n_end = 0, D = 0;
+  uint64_t cand_cap = 0;
+  uint32_t launches = 0;
+  cudaGraphExec_t exec = nullptr;
+};
+
 struct gw_ctx {
   int device = 0;
   int num_sms = 148;
@@ -70,8 +87,6 @@ struct gw_ctx {
   };
   std::map<std::string, Buf> bufs;
   cudaEvent_t ev[8] = {};
-  // pinned staging
-  void* pin = nullptr;
   // last results (device)
   uint64_t n_reports = 0, n_diags = 0, n_events = 0;
   uint8_t* d_kind = nullptr;
@@ -80,27 +95,19 @@ struct gw_ctx {
   Diag* d_diags = nullptr;
   gw_stats stats{};
   bool stats_pending = false;
+  bool phases = false;
   uint32_t launches = 0;
-  uint32_t* d_scal = nullptr;   // device scalars: [3..6] rec/log/diag tops, err
+  uint32_t* d_scal = nullptr;   // device scalars (see Pipeline::run)
   uint32_t* d_nsurv = nullptr;  // device report count
-  uint32_t ncand = 0;
+  bool have_cands = false;
   uint64_t arena_words = 0;
   cudaStream_t last_stream = 0;
-
-  void finish_stats() {
-    if (!stats_pending) return;
-    stats_pending = false;
-    CK(cudaEventSynchronize(ev[5]));
-    float ms;
-    CK(cudaEventElapsedTime(&ms, ev[0], ev[5])); stats.ms_total = ms;
-    CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); stats.ms_prep = ms;
-    CK(cudaEventElapsedTime(&ms, ev[1], ev[2])); stats.ms_walker = ms;
-    CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); stats.ms_sort = ms;
-    CK(cudaEventElapsedTime(&ms, ev[3], ev[4])); stats.ms_check = ms;
-    CK(cudaEventElapsedTime(&ms, ev[4], ev[5])); stats.ms_final = ms;
-  }
-
   uint32_t epoch = 1;  // look-back flag epochs (never reused within 2^24 passes)
+  // last analysis, for an eager re-run after a graph abort
+  DevTrace last_tr{};
+  uint32_t last_inactive = 1;
+  bool last_graph = false;
+  Plan plan;
 
   template <class T>
   T* get(const std::string& name, uint64_t count) {
@@ -117,22 +124,54 @@ struct gw_ctx {
     }
     return (T*)b.p;
   }
-  void release(const std::string& name) {
-    auto it = bufs.find(name);
-    if (it != bufs.end()) {
-      if (it->second.p) cudaFree(it->second.p);
-      bufs.erase(it);
+  void drop_plan() {
+    if (plan.exec) cudaGraphExecDestroy(plan.exec);
+    plan = Plan();
+  }
+  void finish_stats() {
+    if (!stats_pending) return;
+    stats_pending = false;
+    CK(cudaEventSynchronize(ev[5]));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[5])); stats.ms_total = ms;
+    if (phases) {
+      CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); stats.ms_prep = ms;
+      CK(cudaEventElapsedTime(&ms, ev[1], ev[2])); stats.ms_walker = ms;
+      CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); stats.ms_sort = ms;
+      CK(cudaEventElapsedTime(&ms, ev[3], ev[4])); stats.ms_check = ms;
+      CK(cudaEventElapsedTime(&ms, ev[4], ev[5])); stats.ms_final = ms;
     }
   }
 };
 
 namespace {
 
+// scalar slots of the "scalars" buffer
+enum : int { SC_MAXD = 0, SC_NINCS, SC_TICKET, SC_REC, SC_LOG, SC_DIAG, SC_ERR, SC_ABORT, SC_NCAND, SC_NLARGE,
+             SC_NSURV, SC_COUNT = 16 };
+
+__global__ void k_init_stats(Stats* s) {
+  memset(s, 0, sizeof(Stats));
+  s->key_and = ~0ull;
+}
+// graph mode: the trace must have the shape the plan was built for
+__global__ void k_plan_check(const Stats* s, unsigned long long n_bar, unsigned long long n_end,
+                             unsigned long long D, uint32_t* abort_flag) {
+  const bool ok = s->n_acq == 0 && s->n_rel == 0 && s->n_bar == n_bar && s->n_end == n_end &&
+                  ((s->key_or ^ s->key_and) & ~D) == 0ull;
+  if (!ok) atomicOr(abort_flag, 1u);
+}
+__global__ void k_guard(const uint32_t* ncand, uint32_t cap, const uint32_t* nlarge, uint32_t* abort_flag) {
+  if (*ncand > cap || *nlarge > 0) atomicOr(abort_flag, 1u);
+}
+
 struct Pipeline {
   gw_ctx* C;
   cudaStream_t st;
   DevTrace tr;
   uint32_t inactive_opt;
+  bool gmode = false;  // graph mode: plan values, no host syncs
+  const Plan* P = nullptr;
 
   template <class T>
   void d2h(T* host, const T* dev, size_t n = 1) {
@@ -140,6 +179,9 @@ struct Pipeline {
     CK(cudaStreamSynchronize(st));
   }
   void check_launch() { CK(cudaGetLastError()); }
+  void event(int i) {
+    if (!gmode) CK(cudaEventRecord(C->ev[i], st));
+  }
 
   // per-analysis zeroed block: look-back tile counters + radix histograms
   static constexpr uint32_t kZeroWords = 1u << 16;
@@ -152,6 +194,12 @@ struct Pipeline {
     return p;
   }
   uint32_t take_epochs(uint32_t k) {
+    if (gmode) {  // graph mode clears every flag / status word at graph start: fixed epochs
+      static const uint32_t base = 1;
+      uint32_t e = base + gepoch;
+      gepoch += k;
+      return e;
+    }
     if (C->epoch + k >= (1u << 24)) {  // wrap: clear every flag / status word
       for (auto& kv : C->bufs)
         if (kv.first == "lb_flag" || kv.first == "rs_status") CK(cudaMemsetAsync(kv.second.p, 0, kv.second.cap, st));
@@ -161,6 +209,7 @@ struct Pipeline {
     C->epoch += k;
     return e;
   }
+  uint32_t gepoch = 0;
 
   // stable radix sort wrapper; returns pointers to the sorted keys / vals
   template <class K>
@@ -188,9 +237,50 @@ struct Pipeline {
     const uint64_t nt = lb_tiles(n);
     T* agg = C->get<T>(t + "_agg", nt);
     T* inc = C->get<T>(t + "_inc", nt);
-    uint32_t* flag = C->get<uint32_t>("lb_flag", nt);
+    uint32_t* flag = C->get<uint32_t>("lb_flag", std::max<uint64_t>(nt, lb_tiles(tr.n)));
     scan_lb<T, Op>(load, store, n, agg, inc, flag, zeroed(1), take_epochs(1), op, identity, inclusive, st);
   }
+
+  static KeyRuns key_runs(unsigned long long D) {
+    KeyRuns kr;
+    memset(&kr, 0, sizeof kr);
+    std::vector<std::pair<int, int>> runs;  // (src, width) of the varying bit runs
+    for (int b = 0; b < 64;) {
+      if ((D >> b) & 1ull) {
+        int s = b;
+        while (b < 64 && ((D >> b) & 1ull)) b++;
+        runs.push_back({s, b - s});
+      } else {
+        b++;
+      }
+    }
+    while (runs.size() > 4) {  // merge the pair with the smallest gap
+      size_t best = 0;
+      int gap = 1 << 30;
+      for (size_t i = 0; i + 1 < runs.size(); i++) {
+        int g = runs[i + 1].first - (runs[i].first + runs[i].second);
+        if (g < gap) { gap = g; best = i; }
+      }
+      runs[best].second = runs[best + 1].first + runs[best + 1].second - runs[best].first;
+      runs.erase(runs.begin() + best + 1);
+    }
+    int dpos = 0;
+    kr.n = (int)runs.size();
+    for (int i = 0; i < kr.n; i++) {
+      kr.src[i] = runs[i].first;
+      kr.width[i] = runs[i].second;
+      kr.dst[i] = dpos;
+      dpos += runs[i].second;
+    }
+    kr.nbits = dpos + 1;  // + sentinel bit for non-access events
+    return kr;
+  }
+
+  // observed by an eager run, used to build a Plan
+  Stats obs{};
+  uint32_t obs_ncand = 0, obs_nlarge = 0;
+  uint64_t obs_cand_cap = 0;
+  bool obs_snap = false;
 
   void run() {
     gw_stats& S = C->stats;
@@ -202,11 +292,13 @@ struct Pipeline {
     g_launches = 0;
     for (int i = 0; i < 8; i++)
       if (!C->ev[i]) CK(cudaEventCreate(&C->ev[i]));
-    CK(cudaEventRecord(C->ev[0], st));
+    event(0);
     C->d_scal = nullptr;
     C->d_nsurv = nullptr;
     C->stats_pending = false;
+    C->phases = !gmode;
     C->last_stream = st;
+    C->have_cands = false;
     if (N == 0) {
       C->launches = 0;
       return;
@@ -214,18 +306,34 @@ struct Pipeline {
     // ---------------------------------------------------------------- prep
     zero_blk = C->get<uint32_t>("zero_blk", kZeroWords);
     zero_next = 0;
+    uint32_t* scal = C->get<uint32_t>("scalars", SC_COUNT);
     CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
+    CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
+    if (gmode) {  // fixed epochs in the graph: start from clean flags
+      uint32_t* f = C->get<uint32_t>("lb_flag", lb_tiles(N));
+      unsigned long long* rs = C->get<unsigned long long>("rs_status", lb_tiles(N) * 256);
+      CK(cudaMemsetAsync(f, 0, C->bufs["lb_flag"].cap, st));
+      CK(cudaMemsetAsync(rs, 0, C->bufs["rs_status"].cap, st));
+    }
     Stats* dst = C->get<Stats>("stats", 1);
-    Stats hs;
-    memset(&hs, 0, sizeof hs);
-    hs.key_and = ~0ull;
-    CK(cudaMemcpyAsync(dst, &hs, sizeof hs, cudaMemcpyHostToDevice, st));
+    GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
     GW_LAUNCH(k_prep, grid_for(N), kThreads, 0, st, tr, dst);
     check_launch();
-    d2h(&hs, dst);
+    Stats hs;
+    if (gmode) {
+      memset(&hs, 0, sizeof hs);
+      hs.n_bar = P->n_bar;
+      hs.n_end = P->n_end;
+      hs.key_or = P->D;
+      hs.key_and = 0;
+      GW_LAUNCH(k_plan_check, 1, 1, 0, st, dst, P->n_bar, P->n_end, P->D, scal + SC_ABORT);
+    } else {
+      d2h(&hs, dst);
+      obs = hs;
+    }
     const bool has_locks = hs.n_acq + hs.n_rel > 0;
     S.n_accesses = hs.n_acc;
-    CK(cudaEventRecord(C->ev[1], st));
+    event(1);
 
     // ----------------------------------------------------------- partition
     int occ = 0;
@@ -237,6 +345,7 @@ struct Pipeline {
     const uint64_t n_hard = hs.n_bar + hs.n_end;
     const uint64_t snap_entries = (n_hard + tr.B) * (uint64_t)tr.BS;
     const bool snap_mode = !has_locks && snap_entries * 8 <= std::max<uint64_t>(256ull << 20, 8 * N);
+    obs_snap = snap_mode;
     uint32_t* part_key = nullptr;
     uint32_t* perm = nullptr;
     if (G > 1 && !snap_mode) {
@@ -255,9 +364,8 @@ struct Pipeline {
     w.perm = perm;
     w.has_locks = has_locks ? 1 : 0;
     w.inactive_opt = inactive_opt;
+    w.abort_flag = scal + SC_ABORT;
     uint32_t maxd = 1, n_incs = 0;
-    uint32_t* scal = C->get<uint32_t>("scalars", 16);  // [0]=maxd [1]=n_incs [2]=ticket [3]=rec_top [4]=log_top [5]=diag_top [6]=err
-    CK(cudaMemsetAsync(scal, 0, 16 * sizeof(uint32_t), st));
     if (has_locks) {
       const uint64_t nle = hs.n_acq + hs.n_rel + hs.n_end;
       uint32_t* flag = C->get<uint32_t>("lk_flag", N);
@@ -277,8 +385,8 @@ struct Pipeline {
       uint8_t* lflags = C->get<uint8_t>("lflags", N);
       CK(cudaMemsetAsync(lflags, 0, N, st));
       GW_LAUNCH(k_lock_automaton, grid_for(nle), kThreads, 0, st, tr, ktid, kev, (uint32_t)nle, seg_end, stk, res,
-                lflags, scal + 0);
-      GW_LAUNCH(k_lock_access, grid_for(N), kThreads, 0, st, tr, kev, res, seg_beg, seg_end, lflags, scal + 1);
+                lflags, scal + SC_MAXD);
+      GW_LAUNCH(k_lock_access, grid_for(N), kThreads, 0, st, tr, kev, res, seg_beg, seg_end, lflags, scal + SC_NINCS);
       uint32_t* rank = C->get<uint32_t>("lk_rank", N);
       scan<uint32_t, OpSum>(LockRelLoad{lflags}, ArrStore<uint32_t>{rank}, N, OpSum(), 0u, false, "sc_u32");
       check_launch();
@@ -298,18 +406,17 @@ struct Pipeline {
     } else {
       uint64_t nobj = 2 * hs.n_bar + 2 * hs.n_acq + 4 * hs.n_rel + (uint64_t)n_incs * (1 + maxd) + 4;
       arena_words = nobj * (uint64_t)(T + 2) + 64;
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      uint64_t cap_words = (uint64_t)(free_b * 0.6) / 4;
+      cap_words = std::min<uint64_t>(cap_words, 0xFFFFFFF0ull);
+      arena_words = std::min(arena_words, cap_words);
     }
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
-    uint64_t cap_words = (uint64_t)(free_b * 0.6) / 4;
-    cap_words = std::min<uint64_t>(cap_words, 0xFFFFFFF0ull);
-    arena_words = std::min(arena_words, cap_words);
     S.arena_words = arena_words;
     w.arena = C->get<uint32_t>("arena", arena_words);
     w.arena_cap = arena_words;
     w.arena_top = C->get<unsigned long long>("arena_top", 1);
-    const unsigned long long two = 2;
-    CK(cudaMemcpyAsync(w.arena_top, &two, sizeof two, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(w.arena_top, 0, sizeof(unsigned long long), st));
     w.time = C->get<uint32_t>("time", N);
     w.vobj = C->get<uint32_t>("vobj", N);
     w.local = C->get<uint32_t>("st_local", T);
@@ -317,11 +424,11 @@ struct Pipeline {
     w.pdiag = C->get<uint32_t>("st_pdiag", T);
     w.nend = C->get<uint32_t>("st_nend", T);
     w.exited = C->get<uint32_t>("st_exited", T);
-    w.ticket = scal + 2;
-    w.rec_top = scal + 3;
-    w.log_top = scal + 4;
-    w.diag_top = scal + 5;
-    w.err = scal + 6;
+    w.ticket = scal + SC_TICKET;
+    w.rec_top = scal + SC_REC;
+    w.log_top = scal + SC_LOG;
+    w.diag_top = scal + SC_DIAG;
+    w.err = scal + SC_ERR;
     w.maxd = maxd;
     uint64_t diag_cap = hs.n_acq + hs.n_rel + hs.n_end * (uint64_t)maxd + 16;
     w.diags = C->get<Diag>("diags", diag_cap);
@@ -381,87 +488,47 @@ struct Pipeline {
       GW_LAUNCH(k_walker, G, kThreads, 0, st, w);
     }
     check_launch();
-    CK(cudaEventRecord(C->ev[2], st));
+    event(2);
 
     // ---------------------------------------------------------- access pass
-    const uint64_t NA = hs.n_acc;
-    uint32_t* out_n = scal + 8;  // [8]=n_cand [9]=n_large [10]=n_surv
-    uint32_t* large_i = nullptr;
-    uint32_t* large_ws = nullptr;
-    uint32_t* vals = nullptr;
-    uint32_t* sto = nullptr;
-    uint32_t* segst = nullptr;
-    uint32_t* lastw = nullptr;
-    KeyRuns kr;
-    memset(&kr, 0, sizeof kr);
-    bool wide = false;
+    // All N positions are sorted; non-access events carry the top sentinel key
+    // and sort last, and every access-pass kernel skips them, so no kernel
+    // needs the access count on the host.
+    uint32_t* out_n = scal + SC_NCAND;  // [NCAND], [NLARGE], [NSURV]
+    const uint64_t NA = N;
+    const KeyRuns kr = key_runs(hs.key_or ^ hs.key_and);
+    S.sort_bits = kr.nbits;
+    const bool wide = kr.nbits > 32;
+    uint32_t* vals = C->get<uint32_t>("acc_v", N);
     void* skeys = nullptr;
-    if (NA > 0) {
-      unsigned long long D = hs.key_or ^ hs.key_and;
-      // varying bit runs of the location key
-      std::vector<std::pair<int, int>> runs;  // (src, width)
-      for (int b = 0; b < 64;) {
-        if ((D >> b) & 1ull) {
-          int s = b;
-          while (b < 64 && ((D >> b) & 1ull)) b++;
-          runs.push_back({s, b - s});
-        } else {
-          b++;
-        }
-      }
-      while (runs.size() > 4) {  // merge the pair with the smallest gap
-        size_t best = 0;
-        int gap = 1 << 30;
-        for (size_t i = 0; i + 1 < runs.size(); i++) {
-          int g = runs[i + 1].first - (runs[i].first + runs[i].second);
-          if (g < gap) { gap = g; best = i; }
-        }
-        runs[best].second = runs[best + 1].first + runs[best + 1].second - runs[best].first;
-        runs.erase(runs.begin() + best + 1);
-      }
-      int dpos = 0;
-      kr.n = (int)runs.size();
-      for (int i = 0; i < kr.n; i++) {
-        kr.src[i] = runs[i].first;
-        kr.width[i] = runs[i].second;
-        kr.dst[i] = dpos;
-        dpos += runs[i].second;
-      }
-      kr.nbits = dpos + 1;
-      S.sort_bits = kr.nbits;
-      wide = kr.nbits > 32;
-      vals = C->get<uint32_t>("acc_v", N);
-      if (!wide) {
-        uint32_t* k32 = C->get<uint32_t>("acc_k", N);
-        GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals);
-        sort<uint32_t>(k32, vals, N, kr.nbits, "acc");
-        skeys = k32;
-      } else {
-        unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
-        GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals);
-        sort<unsigned long long>(k64, vals, N, kr.nbits, "acc");
-        skeys = k64;
-      }
-      CK(cudaEventRecord(C->ev[3], st));
-      sto = C->get<uint32_t>("acc_to", NA);
-      GW_LAUNCH(k_gather_to, grid_for(NA), kThreads, 0, st, vals, tr.tidop, NA, sto);
-      segst = C->get<uint32_t>("acc_segst", NA);
-      lastw = C->get<uint32_t>("acc_lastw", NA);
-      if (!wide)
-        scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, NA, OpMax2(),
-                            make_uint2(0, 0), true, "sc_u2");
-      else
-        scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
-                            SegStore{segst, lastw}, NA, OpMax2(), make_uint2(0, 0), true, "sc_u2");
-      large_i = C->get<uint32_t>("lg_i", NA / kSmallWin + 1);
-      large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);
+    if (!wide) {
+      uint32_t* k32 = C->get<uint32_t>("acc_k", N);
+      GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals);
+      sort<uint32_t>(k32, vals, N, kr.nbits, "acc");
+      skeys = k32;
     } else {
-      CK(cudaEventRecord(C->ev[3], st));
+      unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
+      GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals);
+      sort<unsigned long long>(k64, vals, N, kr.nbits, "acc");
+      skeys = k64;
     }
-    uint64_t cand_cap = std::max<uint64_t>(65536, NA / 4);
+    event(3);
+    uint32_t* sto = C->get<uint32_t>("acc_to", NA);
+    GW_LAUNCH(k_gather_to, grid_for(NA), kThreads, 0, st, vals, tr.tidop, NA, sto);
+    uint32_t* segst = C->get<uint32_t>("acc_segst", NA);
+    uint32_t* lastw = C->get<uint32_t>("acc_lastw", NA);
+    if (!wide)
+      scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, NA, OpMax2(),
+                          make_uint2(0, 0), true, "sc_u2");
+    else
+      scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
+                          SegStore{segst, lastw}, NA, OpMax2(), make_uint2(0, 0), true, "sc_u2");
+    uint32_t* large_i = C->get<uint32_t>("lg_i", NA / kSmallWin + 1);
+    uint32_t* large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);
+    uint64_t cand_cap = gmode ? P->cand_cap : std::max<uint64_t>(65536, NA / 4);
     Cands cd;
     CheckArgs ca;
-    uint32_t hcnt[3] = {0, 0, 0};
+    uint32_t hcnt[2] = {0, 0};
     for (int attempt = 0; attempt < 2; attempt++) {
       cd.okey = C->get<unsigned long long>("c_okey", cand_cap);
       cd.loc = C->get<unsigned long long>("c_loc", cand_cap);
@@ -472,28 +539,30 @@ struct Pipeline {
       cd.cap = (uint32_t)std::min<uint64_t>(cand_cap, 0xFFFFFFF0ull);
       cd.err = w.err;
       CK(cudaMemsetAsync(out_n, 0, 3 * sizeof(uint32_t), st));
-      if (NA > 0) {
-        ca.tr = tr;
-        ca.vals = vals;
-        ca.sto = sto;
-        ca.segst = segst;
-        ca.lastw = lastw;
-        ca.time = w.time;
-        ca.vobj = w.vobj;
-        ca.arena = w.arena;
-        ca.n_acc = NA;
-        ca.c = cd;
-        ca.large_i = large_i;
-        ca.large_ws = large_ws;
-        ca.n_large = out_n + 1;
-        ca.large_cap = (uint32_t)(NA / kSmallWin + 1);
-        GW_LAUNCH(k_check, grid_for(NA), kThreads, 0, st, ca);
-      }
+      ca.tr = tr;
+      ca.vals = vals;
+      ca.sto = sto;
+      ca.segst = segst;
+      ca.lastw = lastw;
+      ca.time = w.time;
+      ca.vobj = w.vobj;
+      ca.arena = w.arena;
+      ca.n_acc = NA;
+      ca.c = cd;
+      ca.large_i = large_i;
+      ca.large_ws = large_ws;
+      ca.n_large = out_n + 1;
+      ca.large_cap = (uint32_t)(NA / kSmallWin + 1);
+      GW_LAUNCH(k_check, grid_for(NA), kThreads, 0, st, ca);
       GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd);
       check_launch();
+      if (gmode) {
+        GW_LAUNCH(k_guard, 1, 1, 0, st, out_n, cd.cap, out_n + 1, scal + SC_ABORT);
+        break;
+      }
       d2h(hcnt, out_n, 2);
       if (hcnt[1] > 0) {
-        // large reader windows
+        // large reader windows (> kSmallWin reads between two writes)
         const uint32_t nl = hcnt[1];
         uint32_t* sizes = C->get<uint32_t>("lg_sz", nl + 1);
         std::vector<uint32_t> hi(nl), hw(nl);
@@ -514,63 +583,63 @@ struct Pipeline {
         sort<unsigned long long>(lk, lv, M, 24 + ceil_log2(nl + 1), "lg");
         GW_LAUNCH(k_large_check, grid_for(M), kThreads, 0, st, ca, lk, lv, M);
         check_launch();
-        d2h(hcnt, out_n, 1);
-        CK(cudaStreamSynchronize(st));
-        // keep the host vectors alive until the copies above completed
+        d2h(hcnt, out_n, 1);  // also keeps off / hi / hw alive until the copies completed
       }
       if (hcnt[0] <= cd.cap) break;
       cand_cap = (uint64_t)hcnt[0] + 1024;
-      uint32_t zero = 0;
-      CK(cudaMemcpyAsync(w.err, &zero, sizeof zero, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(w.err, 0, sizeof(uint32_t), st));
     }
-    const uint32_t ncand = hcnt[0];
-    S.n_candidates = ncand;
-    CK(cudaEventRecord(C->ev[4], st));
+    obs_ncand = hcnt[0];
+    obs_nlarge = hcnt[1];
+    obs_cand_cap = cand_cap;
+    // graph mode sizes everything for the plan's capacity; counts stay on the device
+    const uint32_t ncap = gmode ? cd.cap : hcnt[0];
+    S.n_candidates = hcnt[0];
+    event(4);
 
     // ------------------------------------------------------- dedup / final
-    // no host sync from here on: counts stay on the device until gw_ctx_fetch
     uint32_t* d_nsurv = out_n + 2;
     C->d_scal = scal;
     C->d_nsurv = d_nsurv;
-    C->n_reports = 0;
-    C->ncand = ncand;
-    if (ncand > 0) {
-      uint64_t tcap = pow2_at_least(2ull * ncand);
+    C->have_cands = ncap > 0;
+    if (ncap > 0) {
+      uint64_t tcap = pow2_at_least(2ull * ncap);
       DedupArgs d;
       d.c = cd;
       d.instr = tr.instr;
       d.owner = C->get<uint32_t>("dd_owner", tcap);
       d.smin = C->get<unsigned long long>("dd_min", tcap);
-      d.cslot = C->get<uint32_t>("dd_slot", ncand);
+      d.cslot = C->get<uint32_t>("dd_slot", ncap);
       d.mask = (uint32_t)(tcap - 1);
-      d.ncand = ncand;
+      d.ncand = ncap;
+      d.dn = out_n;
       CK(cudaMemsetAsync(d.owner, 0, sizeof(uint32_t) * tcap, st));
       CK(cudaMemsetAsync(d.smin, 0xFF, sizeof(unsigned long long) * tcap, st));
-      GW_LAUNCH(k_dedup_insert, grid_for(ncand), kThreads, 0, st, d);
-      unsigned long long* sk = C->get<unsigned long long>("sv_k", ncand);
-      uint32_t* sv = C->get<uint32_t>("sv_v", ncand);
+      GW_LAUNCH(k_dedup_insert, grid_for(ncap), kThreads, 0, st, d);
+      unsigned long long* sk = C->get<unsigned long long>("sv_k", ncap);
+      uint32_t* sv = C->get<uint32_t>("sv_v", ncap);
       uint32_t* ccnt = C->get<uint32_t>("sv_cnt", N);
       CK(cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * N, st));
       uint32_t* coff = C->get<uint32_t>("sv_off", N);
-      uint32_t* big = C->get<uint32_t>("sv_big", ncand / (kGroupSmall + 1) + 1);
+      uint32_t* big = C->get<uint32_t>("sv_big", ncap / (kGroupSmall + 1) + 1);
       uint32_t* nbig = zeroed(1);
-      GW_LAUNCH(k_dedup_count, grid_for(ncand), kThreads, 0, st, d, ccnt, d_nsurv);
+      GW_LAUNCH(k_dedup_count, grid_for(ncap), kThreads, 0, st, d, ccnt, d_nsurv);
       scan<uint32_t, OpSum>(ArrLoad<uint32_t>{ccnt}, ArrStore<uint32_t>{coff}, N, OpSum(), 0u, false, "sc_u32");
-      GW_LAUNCH(k_dedup_place, grid_for(ncand), kThreads, 0, st, d, ccnt, coff, sk, sv);
+      GW_LAUNCH(k_dedup_place, grid_for(ncap), kThreads, 0, st, d, ccnt, coff, sk, sv);
       GW_LAUNCH(k_group_sort, grid_for(N), kThreads, 0, st, coff, N, d_nsurv, sk, sv, big, nbig);
       GW_LAUNCH(k_group_sort_big, 148u, kThreads, 0, st, coff, N, d_nsurv, sk, sv, big, nbig);
-      C->d_kind = C->get<uint8_t>("o_kind", ncand);
-      C->d_prior = C->get<uint32_t>("o_prior", ncand);
-      C->d_cur = C->get<uint32_t>("o_cur", ncand);
-      GW_LAUNCH(k_final, grid_for(ncand), kThreads, 0, st, cd, sv, d_nsurv, C->d_kind, C->d_prior, C->d_cur);
+      C->d_kind = C->get<uint8_t>("o_kind", ncap);
+      C->d_prior = C->get<uint32_t>("o_prior", ncap);
+      C->d_cur = C->get<uint32_t>("o_cur", ncap);
+      GW_LAUNCH(k_final, grid_for(ncap), kThreads, 0, st, cd, sv, d_nsurv, C->d_kind, C->d_prior, C->d_cur);
       check_launch();
     }
     C->d_diags = w.diags;
     C->arena_words = arena_words;
-    CK(cudaEventRecord(C->ev[5], st));
+    event(5);
     S.n_sync = hs.n_acq + hs.n_rel + hs.n_end + hs.n_bar;
     C->launches = g_launches;
-    C->stats_pending = true;
+    C->stats_pending = !gmode;
   }
 };
 
@@ -629,11 +698,81 @@ extern "C" gw_ctx* gw_ctx_create(int device) {
 
 extern "C" void gw_ctx_destroy(gw_ctx* c) {
   if (!c) return;
+  c->drop_plan();
   for (auto& kv : c->bufs)
     if (kv.second.p) cudaFree(kv.second.p);
   for (int i = 0; i < 8; i++)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   delete c;
+}
+
+// Eager analysis, then (lock-free traces without large reader windows) build
+// the Plan and capture the graph-mode pipeline for later replays.
+static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_t inactive, const void* kp,
+                         const void* tp, const void* ip, bool eager) {
+  Plan& P = c->plan;
+  c->last_tr = tr;
+  c->last_inactive = inactive;
+  c->last_stream = st;
+  const bool match = !eager && P.valid && P.N == tr.n && P.B == tr.B && P.W == tr.W && P.L == tr.L && P.key == kp &&
+                     P.tidop == tp && P.instr == ip && P.stream == st && P.inactive_opt == inactive;
+  if (match) {
+    for (int i = 0; i < 8; i++)
+      if (!c->ev[i]) CK(cudaEventCreate(&c->ev[i]));
+    CK(cudaEventRecord(c->ev[0], st));
+    CK(cudaGraphLaunch(P.exec, st));
+    CK(cudaEventRecord(c->ev[5], st));
+    c->last_graph = true;
+    c->launches = P.launches;
+    c->stats_pending = true;
+    c->phases = false;
+    return;
+  }
+  c->drop_plan();
+  c->last_graph = false;
+  Pipeline p;
+  p.C = c;
+  p.st = st;
+  p.inactive_opt = inactive;
+  p.tr = tr;
+  p.run();
+  if (eager || tr.n == 0 || !p.obs_snap || p.obs_nlarge > 0 || st == 0) return;
+  // build the plan; run the graph-mode pipeline once for real (allocates every
+  // buffer at its final size), then capture it
+  Plan np;
+  np.N = tr.n; np.B = tr.B; np.W = tr.W; np.L = tr.L; np.inactive_opt = inactive;
+  np.key = kp; np.tidop = tp; np.instr = ip; np.stream = st;
+  np.n_bar = p.obs.n_bar; np.n_end = p.obs.n_end; np.D = p.obs.key_or ^ p.obs.key_and;
+  np.cand_cap = std::max<uint64_t>(p.obs_cand_cap, 2ull * p.obs_ncand + 4096);
+  c->plan = np;
+  Pipeline g;
+  g.C = c; g.st = st; g.inactive_opt = inactive; g.tr = tr; g.gmode = true; g.P = &c->plan;
+  g.run();
+  CK(cudaStreamSynchronize(st));
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  Pipeline q;
+  q.C = c; q.st = st; q.inactive_opt = inactive; q.tr = tr; q.gmode = true; q.P = &c->plan;
+  try {
+    q.run();
+  } catch (...) {
+    cudaStreamEndCapture(st, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    c->drop_plan();
+    throw;
+  }
+  CK(cudaStreamEndCapture(st, &graph));
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {
+    c->drop_plan();
+    return;  // keep eager mode
+  }
+  c->plan.exec = exec;
+  c->plan.launches = c->launches;
+  c->plan.valid = true;
+  c->last_graph = true;  // the buffers hold the graph-mode run's results
 }
 
 extern "C" int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* t, const gw_opts* o) {
@@ -642,12 +781,10 @@ extern "C" int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* t, const gw
   if (v) return v;
   return guarded([&] {
     CK(cudaSetDevice(c->device));
-    Pipeline p;
-    p.C = c;
-    p.st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
-    p.inactive_opt = o ? o->inactive_opt : 1u;
-    p.tr = make_dev(t, (const unsigned long long*)t->key, t->tidop, t->instr);
-    p.run();
+    cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
+    const uint32_t inactive = o ? o->inactive_opt : 1u;
+    DevTrace tr = make_dev(t, (const unsigned long long*)t->key, t->tidop, t->instr);
+    analyze_impl(c, tr, st, inactive, t->key, t->tidop, t->instr, o && (o->flags & GW_OPT_EAGER));
   });
 }
 
@@ -658,6 +795,7 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
   return guarded([&] {
     CK(cudaSetDevice(c->device));
     cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
+    const uint32_t inactive = o ? o->inactive_opt : 1u;
     const uint64_t N = t->n_events;
     unsigned long long* k = c->get<unsigned long long>("in_key", N);
     uint32_t* to = c->get<uint32_t>("in_tidop", N);
@@ -667,12 +805,8 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
       CK(cudaMemcpyAsync(to, t->tidop, 4 * N, cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(in, t->instr, 4 * N, cudaMemcpyHostToDevice, st));
     }
-    Pipeline p;
-    p.C = c;
-    p.st = st;
-    p.inactive_opt = o ? o->inactive_opt : 1u;
-    p.tr = make_dev(t, k, to, in);
-    p.run();
+    DevTrace tr = make_dev(t, k, to, in);
+    analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER));
   });
 }
 
@@ -683,19 +817,28 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
     CK(cudaSetDevice(c->device));
     uint64_t n = 0, nd = 0;
     if (c->d_scal) {
-      uint32_t tail[4] = {0, 0, 0, 0}, ns = 0;
-      CK(cudaMemcpyAsync(tail, c->d_scal + 3, sizeof tail, cudaMemcpyDeviceToHost, c->last_stream));
-      CK(cudaMemcpyAsync(&ns, c->d_nsurv, sizeof ns, cudaMemcpyDeviceToHost, c->last_stream));
+      uint32_t sc[SC_COUNT];
+      CK(cudaMemcpyAsync(sc, c->d_scal, sizeof sc, cudaMemcpyDeviceToHost, c->last_stream));
       CK(cudaStreamSynchronize(c->last_stream));
-      if (tail[3]) {
+      if (sc[SC_ABORT] && c->last_graph) {
+        // the trace no longer matches the cached plan: re-run eagerly
+        c->drop_plan();
+        c->last_graph = false;
+        Pipeline p;
+        p.C = c; p.st = c->last_stream; p.inactive_opt = c->last_inactive; p.tr = c->last_tr;
+        p.run();
+        CK(cudaMemcpyAsync(sc, c->d_scal, sizeof sc, cudaMemcpyDeviceToHost, c->last_stream));
+        CK(cudaStreamSynchronize(c->last_stream));
+      }
+      if (sc[SC_ERR]) {
         char buf[200];
         snprintf(buf, sizeof buf,
-                 "engine capacity error flags 0x%x (arena %llu words; dense lock clocks need more memory?)", tail[3],
-                 (unsigned long long)c->arena_words);
+                 "engine capacity error flags 0x%x (arena %llu words; dense lock clocks need more memory?)",
+                 sc[SC_ERR], (unsigned long long)c->arena_words);
         throw CudaErr{GW_E_NOMEM, buf};
       }
-      n = c->ncand ? ns : 0;
-      nd = tail[2];
+      n = c->have_cands ? sc[SC_NSURV] : 0;
+      nd = sc[SC_DIAG];
     }
     c->n_reports = n;
     c->n_diags = nd;

@@ -41,6 +41,19 @@ __device__ __forceinline__ uint2 shfl_up<uint2>(uint2 v, int o) {
   return make_uint2(__shfl_up_sync(0xffffffffu, v.x, o), __shfl_up_sync(0xffffffffu, v.y, o));
 }
 
+template <class T>
+__device__ __forceinline__ T shfl_down(T v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
+template <>
+__device__ __forceinline__ uint2 shfl_down<uint2>(uint2 v, int o) {
+  return make_uint2(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
+}
+template <class T>
+__device__ __forceinline__ T shfl_idx(T v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+template <>
+__device__ __forceinline__ uint2 shfl_idx<uint2>(uint2 v, int l) {
+  return make_uint2(__shfl_sync(0xffffffffu, v.x, l), __shfl_sync(0xffffffffu, v.y, l));
+}
+
 // warp-inclusive scan via shuffles
 template <class T, class Op>
 __device__ __forceinline__ T warp_incl_scan(T v, Op op) {
@@ -126,30 +139,47 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(Load load, Store store, ui
   }
   T tot;
   T run = block_excl_scan<T, Op>(acc, op, identity, &tot);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp-wide decoupled look-back: 32 predecessors per round trip
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+      if (tile == 0) inc[0] = tot; else agg[tile] = tot;
+      __threadfence();
+      atomicExch(&flag[tile], (epoch << 2) | (tile == 0 ? LB_INC : LB_AGG));
+    }
     T pre = identity;
-    if (tile == 0) {
-      inc[0] = tot;
-      __threadfence();
-      atomicExch(&flag[0], (epoch << 2) | LB_INC);
-    } else {
-      agg[tile] = tot;
-      __threadfence();
-      atomicExch(&flag[tile], (epoch << 2) | LB_AGG);
+    if (tile > 0) {
       int64_t p = (int64_t)tile - 1;
       while (true) {
-        uint32_t f;
-        do { f = ld_volatile_u32(&flag[p]); } while ((f >> 2) != epoch);
+        const int64_t q = p - lane;
+        uint32_t f = (epoch << 2) | LB_INC;  // q < 0: virtual inclusive identity
+        if (q >= 0) {
+          do { f = ld_volatile_u32(&flag[q]); } while ((f >> 2) != epoch);
+        }
         __threadfence();
-        if ((f & 3u) == LB_INC) { pre = op(__ldcg(&inc[p]), pre); break; }
-        pre = op(__ldcg(&agg[p]), pre);
-        p--;
+        const bool isinc = (f & 3u) == LB_INC;
+        const uint32_t incm = __ballot_sync(0xffffffffu, isinc);
+        const int lim = __ffs(incm) - 1;  // nearest inclusive predecessor (incm != 0 once q < 0)
+        T val = identity;
+        if (q >= 0 && (incm == 0 || lane <= lim)) val = isinc ? __ldcg(&inc[q]) : __ldcg(&agg[q]);
+        // reduce lanes 0..lim (commutative ops: sum, max)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          T other = shfl_down(val, o);
+          if (lane + o < 32) val = op(val, other);
+        }
+        val = shfl_idx(val, 0);
+        pre = op(val, pre);
+        if (incm) break;
+        p -= 32;
       }
-      inc[tile] = op(pre, tot);
-      __threadfence();
-      atomicExch(&flag[tile], (epoch << 2) | LB_INC);
+      if (lane == 0) {
+        inc[tile] = op(pre, tot);
+        __threadfence();
+        atomicExch(&flag[tile], (epoch << 2) | LB_INC);
+      }
     }
-    s_pre = pre;
+    if (lane == 0) s_pre = pre;
   }
   __syncthreads();
   run = op(s_pre, run);
@@ -261,12 +291,33 @@ __global__ void __launch_bounds__(kThreads) k_rs_onesweep(const K* __restrict__ 
     } else {
       atomicExch(my, EP | (1ull << 38) | cnt);
       int64_t p = (int64_t)tile - 1;
+      constexpr int B8 = 8;
       while (true) {
-        unsigned long long s;
-        do { s = ld_volatile_u64(&status[(uint64_t)p * 256 + d]); } while ((s >> 40) != epoch);
-        pre += s & ((1ull << 38) - 1);
-        if (((s >> 38) & 3ull) == 2ull) break;
-        p--;
+        unsigned long long sv[B8];
+        bool ready;
+        int lim;
+        do {  // batch of up to 8 predecessors; retry until the needed ones are published
+#pragma unroll
+          for (int k = 0; k < B8; k++)
+            sv[k] = (p - k >= 0) ? ld_volatile_u64(&status[(uint64_t)(p - k) * 256 + d]) : (EP | (2ull << 38));
+          ready = true;
+          lim = B8 - 1;
+#pragma unroll
+          for (int k = B8 - 1; k >= 0; k--) {
+            if ((sv[k] >> 40) != epoch) ready = false;
+            else if (((sv[k] >> 38) & 3ull) == 2ull) { lim = k; ready = true; }
+          }
+          // ready iff every entry up to the nearest inclusive one is published
+          ready = true;
+          for (int k = 0; k <= lim; k++) if ((sv[k] >> 40) != epoch) ready = false;
+        } while (!ready);
+        bool found = false;
+        for (int k = 0; k <= lim; k++) {
+          pre += sv[k] & ((1ull << 38) - 1);
+          if (((sv[k] >> 38) & 3ull) == 2ull) { found = true; break; }
+        }
+        if (found) break;
+        p -= B8;
       }
       atomicExch(my, EP | (2ull << 38) | (pre + cnt));
     }

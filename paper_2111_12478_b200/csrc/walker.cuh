@@ -100,6 +100,7 @@ struct WalkArgs {
   uint32_t* scratch;  // per CTA: 3*T words (P, H, acc)
   Diag* diags; uint32_t* diag_top; uint32_t diag_cap;
   uint32_t* err;
+  const uint32_t* abort_flag;  // graph mode: plan mismatch -> skip
 };
 
 __device__ __forceinline__ uint32_t ev_kind(uint32_t to) { return (to >> GW_OP_SHIFT) & 7u; }
@@ -866,6 +867,7 @@ struct SnapArgs {
 __global__ void __launch_bounds__(kThreads) k_walker_snap(WalkArgs a, SnapArgs s) {
   __shared__ uint32_t s_acc[kAccSmem];
   const DevTrace& tr = a.tr;
+  if (*(volatile const uint32_t*)a.abort_flag) return;
   for (uint32_t b = blockIdx.x; b < tr.B; b += gridDim.x) {
     const uint32_t beg = s.hb_beg[b], end = s.hb_end[b];
     uint2* sp = s.snap + (size_t)(beg + b) * tr.BS;

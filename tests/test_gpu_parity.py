@@ -138,3 +138,43 @@ def test_many_reports_at_one_event(ctx, seed):
     got = ndjson_lines(tr, _run(ctx, tr))
     assert got == ndjson_lines(tr, O.run_trace(tr))
     assert len(got) > 100
+
+
+def test_graph_replay_and_plan_mismatch_fallback():
+    """Repeated analyses of one shape on a non-default stream replay a captured
+    CUDA graph; contents change every call and one call breaks the plan (more
+    address bits -> device-side abort -> eager re-run inside fetch)."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = N.Context(0)
+    geo = dict(blocks=16, warps=8, lanes=32, phases=4, records=4)
+    traces = [WL.c2_soa(**geo, words_per_block=512, seed=s) for s in (11, 12, 13)]
+    traces.append(WL.c2_soa(**geo, words_per_block=4096, seed=14))  # wider keys: plan check aborts
+    traces.append(WL.c2_soa(**geo, words_per_block=512, seed=15))
+    n = len(traces[0])
+    bufs = [torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
+            torch.empty(n, dtype=torch.int32, device=dev)]
+    for rep in range(2):
+        for tr in traces:
+            assert len(tr) == n
+            bufs[0].copy_(torch.from_numpy(tr.key.view(np.int64)))
+            bufs[1].copy_(torch.from_numpy(tr.tidop.view(np.int32)))
+            bufs[2].copy_(torch.from_numpy(tr.instr.view(np.int32)))
+            torch.cuda.synchronize()
+            ctx.analyze_device(tr.cfg_tuple, n, bufs[0].data_ptr(), bufs[1].data_ptr(), bufs[2].data_ptr(),
+                               stream=stream.cuda_stream)
+            got = ctx.fetch()
+            assert ndjson_lines(tr, got) == ndjson_lines(tr, O.run_trace(tr))
+
+
+def test_graph_replay_host_path():
+    import torch
+
+    stream = torch.cuda.Stream(device=torch.device("cuda", 0))
+    ctx = N.Context(0)
+    for s in range(4):
+        tr = WL.c2_soa(blocks=8, warps=4, lanes=32, phases=4, records=4, words_per_block=256, seed=30 + s)
+        ctx.analyze_host(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, stream=stream.cuda_stream)
+        assert ndjson_lines(tr, ctx.fetch()) == ndjson_lines(tr, O.run_trace(tr))
