@@ -250,7 +250,8 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # per-phase breakdown from one eager (non-graph) analysis, outside the timed region
+    # per-phase breakdown from one warm eager (non-graph) analysis, outside the timed region
+    step_device(eager=True)
     step_device(eager=True)
     s = ctx.stats()
     phase = {k: round(getattr(s, "ms_" + k), 4) for k in ("prep", "walker", "sort", "check", "final")}

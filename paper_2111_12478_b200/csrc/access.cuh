@@ -30,15 +30,17 @@ constexpr unsigned long long SUB_READER = 0x80000000ull;
 struct KeyRuns {  // compacted location key = concatenation of the varying bit runs
   int n;
   int src[4], width[4], dst[4];
-  int nbits;  // total key bits incl. the sentinel bit for non-access events
+  int nbits;  // total varying key bits
 };
 
+// Non-access events get key 0: they sort among the accesses of compacted
+// location 0 and every access-pass kernel skips them (no sentinel bit, so the
+// compacted key never needs more than the 64 varying bits).
 template <class K>
 __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals) {
-  const K sentinel = (K)1 << (kr.nbits - 1);
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t to = tr.tidop[e];
-    K k = sentinel;
+    K k = 0;
     if (ev_kind(to) <= GW_K_WRITE) {
       unsigned long long x = tr.key[e];
       k = 0;
@@ -219,13 +221,19 @@ __global__ void __launch_bounds__(kThreads) k_check(CheckArgs a) {
       // readers since W: one candidate per thread (its latest read), ranked by its first read
       for (uint32_t q = ws; q < i; q++) {
         const uint32_t toq = a.sto[q];
+        if (ev_kind(toq) > GW_K_WRITE) continue;  // non-access event sharing key 0
         const uint32_t uq = ev_tid(toq);
         bool later = false;
-        for (uint32_t q2 = q + 1; q2 < i && !later; q2++) later = ev_tid(a.sto[q2]) == uq;
+        for (uint32_t q2 = q + 1; q2 < i && !later; q2++) {
+          const uint32_t t2 = a.sto[q2];
+          later = ev_kind(t2) <= GW_K_WRITE && ev_tid(t2) == uq;
+        }
         if (later || uq == tc) continue;
         uint32_t first = q;
-        for (uint32_t q3 = ws; q3 < q; q3++)
-          if (ev_tid(a.sto[q3]) == uq) { first = q3; break; }
+        for (uint32_t q3 = ws; q3 < q; q3++) {
+          const uint32_t t3 = a.sto[q3];
+          if (ev_kind(t3) <= GW_K_WRITE && ev_tid(t3) == uq) { first = q3; break; }
+        }
         const uint32_t r = a.vals[q];
         if (!cover(toq, toc, BS) && a.time[r] > obj_get(a.arena, vo, uq)) {
           if (!loc) loc = a.tr.key[c];
@@ -242,12 +250,16 @@ __global__ void k_large_fill(const uint32_t* large_i, const uint32_t* large_ws, 
   for (uint32_t k = blockIdx.x; k < n_large; k += gridDim.x) {
     const uint32_t ws = large_ws[k], m = large_i[k] - ws, o = off[k];
     for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-      keys[o + j] = ((unsigned long long)k << 24) | ev_tid(sto[ws + j]);
+      const uint32_t t = sto[ws + j];
+      // non-access events (key-0 location) go to a virtual window past the last one
+      const unsigned long long kk = ev_kind(t) <= GW_K_WRITE ? k : n_large;
+      keys[o + j] = (kk << 24) | ev_tid(t);
       vals[o + j] = ws + j;
     }
   }
 }
-__global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const uint32_t* vals, uint64_t M) {
+__global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const uint32_t* vals, uint64_t M,
+                              uint32_t nlarge) {
   const uint32_t BS = a.tr.BS;
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned long long key = keys[j];
@@ -255,6 +267,7 @@ __global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const
     uint64_t f = j;
     while (f > 0 && keys[f - 1] == key) f--;
     const uint32_t k = (uint32_t)(key >> 24);
+    if (k >= nlarge) continue;  // non-access events
     const uint32_t i = a.large_i[k], ws = a.large_ws[k];
     const uint32_t c = a.vals[i], toc = a.sto[i];
     const uint32_t q = vals[j], first = vals[f];

@@ -272,13 +272,14 @@ struct Pipeline {
       kr.dst[i] = dpos;
       dpos += runs[i].second;
     }
-    kr.nbits = dpos + 1;  // + sentinel bit for non-access events
+    kr.nbits = dpos;
     return kr;
   }
 
   // observed by an eager run, used to build a Plan
   Stats obs{};
   uint32_t obs_ncand = 0, obs_nlarge = 0;
+  unsigned long long obs_D = 0;
   uint64_t obs_cand_cap = 0;
   bool obs_snap = false;
 
@@ -496,9 +497,11 @@ struct Pipeline {
     // needs the access count on the host.
     uint32_t* out_n = scal + SC_NCAND;  // [NCAND], [NLARGE], [NSURV]
     const uint64_t NA = N;
-    const KeyRuns kr = key_runs(hs.key_or ^ hs.key_and);
+    // varying location-key bits (none when the trace has no access at all)
+    const KeyRuns kr = key_runs(gmode ? P->D : (hs.n_acc ? hs.key_or ^ hs.key_and : 0ull));
     S.sort_bits = kr.nbits;
     const bool wide = kr.nbits > 32;
+    obs_D = hs.n_acc ? hs.key_or ^ hs.key_and : 0ull;
     uint32_t* vals = C->get<uint32_t>("acc_v", N);
     void* skeys = nullptr;
     if (!wide) {
@@ -581,7 +584,7 @@ struct Pipeline {
         GW_LAUNCH(k_large_fill, std::min<uint32_t>(nl, 65535u), kThreads, 0, st, large_i, large_ws, sizes, nl, sto, lk,
                   lv);
         sort<unsigned long long>(lk, lv, M, 24 + ceil_log2(nl + 1), "lg");
-        GW_LAUNCH(k_large_check, grid_for(M), kThreads, 0, st, ca, lk, lv, M);
+        GW_LAUNCH(k_large_check, grid_for(M), kThreads, 0, st, ca, lk, lv, M, nl);
         check_launch();
         d2h(hcnt, out_n, 1);  // also keeps off / hi / hw alive until the copies completed
       }
@@ -742,7 +745,7 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   Plan np;
   np.N = tr.n; np.B = tr.B; np.W = tr.W; np.L = tr.L; np.inactive_opt = inactive;
   np.key = kp; np.tidop = tp; np.instr = ip; np.stream = st;
-  np.n_bar = p.obs.n_bar; np.n_end = p.obs.n_end; np.D = p.obs.key_or ^ p.obs.key_and;
+  np.n_bar = p.obs.n_bar; np.n_end = p.obs.n_end; np.D = p.obs_D;
   np.cand_cap = std::max<uint64_t>(p.obs_cand_cap, 2ull * p.obs_ncand + 4096);
   c->plan = np;
   Pipeline g;
