@@ -30,17 +30,20 @@ constexpr unsigned long long SUB_READER = 0x80000000ull;
 struct KeyRuns {  // compacted location key = concatenation of the varying bit runs
   int n;
   int src[4], width[4], dst[4];
-  int nbits;  // total varying key bits
+  int nbits;     // sort bits: varying location bits (+1 sentinel bit when it fits)
+  int sentinel;  // non-access events carry bit nbits-1
 };
 
-// Non-access events get key 0: they sort among the accesses of compacted
-// location 0 and every access-pass kernel skips them (no sentinel bit, so the
-// compacted key never needs more than the 64 varying bits).
+// Non-access events get the sentinel key (bit nbits-1, one past the varying
+// location bits) and sort last; in the corner case of 64 varying bits there is
+// no spare bit and they take key 0 instead.  Either way every access-pass
+// kernel skips them.
 template <class K>
 __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals) {
+  const K sentinel = kr.sentinel ? ((K)1 << (kr.nbits - 1)) : (K)0;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t to = tr.tidop[e];
-    K k = 0;
+    K k = sentinel;
     if (ev_kind(to) <= GW_K_WRITE) {
       unsigned long long x = tr.key[e];
       k = 0;

@@ -272,7 +272,8 @@ struct Pipeline {
       kr.dst[i] = dpos;
       dpos += runs[i].second;
     }
-    kr.nbits = dpos;
+    kr.sentinel = dpos < 64;
+    kr.nbits = dpos + (kr.sentinel ? 1 : 0);
     return kr;
   }
 
