@@ -1,6 +1,6 @@
 """Benchmark: trace events/s of G-WCP race analysis (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload c2|c5s]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--workload c2|c5]
 
 One step = one complete analysis of one synthetic trace (the workload) with
 the final report list on the host.  ``value`` is device-resident throughput
@@ -44,19 +44,53 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def make_workload(name: str, rank: int):
-    from paper_2111_12478_b200 import workloads as WL
+WORKLOADS = {
+    # C2 (configs[1]): 64 x 256 threads, __syncthreads only, 64K words, ~1 % random words
+    "c2": dict(blocks=64, warps=8, lanes=32, phases=8, records=8, words_per_block=1024, seed=2),
+    # C5 (configs[4]): the C2 recipe at 1024 x 256 threads, 256M words, 16 phases x 240 records = 1.007e9 events
+    "c5": dict(blocks=1024, warps=8, lanes=32, phases=16, records=240, words_per_block=262144, seed=5),
+}
 
-    if name == "c2":
-        tr = WL.c2_soa(seed=2 + rank)
-        desc = {"workload": "C2", "threads": "64x8x32", "addresses": 65536, "phases": 8,
-                "sync": "__syncthreads only", "injected_random_words": "1%"}
-    elif name == "c5s":  # C5 recipe at reduced depth (fits host RAM for the e2e leg)
-        tr = WL.c2_soa(blocks=1024, warps=8, lanes=32, phases=4, records=8, words_per_block=262144, seed=5 + rank)
-        desc = {"workload": "C5-shallow", "threads": "1024x8x32", "addresses": 268435456, "phases": 4}
-    else:
-        raise SystemExit(f"unknown workload {name}")
-    return tr, desc
+
+def workload_desc(name, p, n, n_acc):
+    return {"workload": name.upper(), "threads": f"{p['blocks']}x{p['warps']}x{p['lanes']}",
+            "addresses": p["blocks"] * p["words_per_block"], "phases": p["phases"],
+            "records_per_warp_phase": p["records"], "sync": "__syncthreads only",
+            "injected_random_words": "1%", "events": n, "accesses": n_acc}
+
+
+def make_workload(name: str, rank: int, dev):
+    """Generate the workload trace directly in HBM (device generator; identical
+    to paper_2111_12478_b200.workloads.c2_soa for the same parameters)."""
+    import torch
+    from paper_2111_12478_b200 import _native as N
+
+    p = dict(WORKLOADS[name])
+    p["seed"] += rank
+    n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
+    key_d = torch.empty(n, dtype=torch.int64, device=dev)
+    to_d = torch.empty(n, dtype=torch.int32, device=dev)
+    in_d = torch.empty(n, dtype=torch.int32, device=dev)
+    N.gen_c2_device(key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), **p)
+    torch.cuda.synchronize(dev)
+    cfg = (p["blocks"], p["warps"], p["lanes"])
+    n_acc = n - p["phases"] * p["blocks"]
+    return cfg, n, n_acc, (key_d, to_d, in_d), workload_desc(name, p, n, n_acc)
+
+
+def host_prefix(cfg, dev_bufs, P):
+    """Record-aligned host copy of the first ~P events (for the CPU oracle)."""
+    from paper_2111_12478_b200 import _native as N
+    from paper_2111_12478_b200.trace import Trace, TraceConfig
+
+    key_d, to_d, in_d = dev_bufs
+    n = key_d.numel()
+    P = min(P, n)
+    to = to_d[: min(n, P + 64)].cpu().numpy().view(np.uint32)
+    while P < len(to) and to[P] & N.F_CONT:
+        P += 1
+    return Trace(TraceConfig(*cfg), key_d[:P].cpu().numpy().view(np.uint64), to[:P].copy(),
+                 in_d[:P].cpu().numpy().view(np.uint32))
 
 
 class ClockSampler:
@@ -118,39 +152,59 @@ class ClockSampler:
         }
 
 
-def cpu_oracle_run(tr, max_seconds=25.0):
-    """Time the oracle port on one core over the largest prefix fitting ~max_seconds."""
+def cpu_oracle_run(cfg, dev_bufs, max_seconds=25.0, start=1 << 20):
+    """Time the oracle port on one core over the largest record-aligned prefix
+    that fits ~max_seconds (the full trace when it does)."""
     from oracle import oracle as O
-    from paper_2111_12478_b200 import _native as N
-    from paper_2111_12478_b200.trace import Trace
 
-    n = len(tr)
-    P = n
+    n = dev_bufs[0].numel()
+    P = min(n, start)
     while True:
-        while P < n and tr.tidop[P] & N.F_CONT:
-            P += 1
-        sub = tr if P >= n else Trace(tr.config, tr.key[:P], tr.tidop[:P], tr.instr[:P])
+        sub = host_prefix(cfg, dev_bufs, P)
         t0 = time.perf_counter()
         O.run_trace(sub)
         dt = time.perf_counter() - t0
-        if dt <= max_seconds or P < 10000:
-            return P, dt
-        P = int(P * max_seconds / dt * 0.8)
+        if dt > max_seconds and len(sub) > 10000:
+            P = int(len(sub) * max_seconds / dt * 0.8)
+            continue
+        if dt < max_seconds / 4 and len(sub) < n:
+            P = min(n, int(len(sub) * max_seconds / max(dt, 1e-3) * 0.5))
+            continue
+        return len(sub), dt
 
 
 def run_reference(args):
+    """The reference arm: the CPU restatement of the reference (oracle/) on
+    this host's cores, on the same workload recipe (host numpy generator, so
+    nothing of the B200 engine runs on this path)."""
+    from oracle import oracle as O
+    from paper_2111_12478_b200 import workloads as WL
+
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    tr, desc = make_workload(args.workload, 0)
-    n = len(tr)
+    p = WORKLOADS[args.workload]
+    n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
+    n_acc = n - p["phases"] * p["blocks"]
+    desc = workload_desc(args.workload, p, n, n_acc)
     times = []
     sample = None
+    P = 1 << 20
     for i in range(args.warmup + args.steps):
-        P, dt = cpu_oracle_run(tr, max_seconds=args.ref_seconds)
-        sample = P
+        while True:
+            tr = WL.c2_soa_prefix(P, **p)
+            t0 = time.perf_counter()
+            O.run_trace(tr)
+            dt = time.perf_counter() - t0
+            if dt > args.ref_seconds and len(tr) > 10000:
+                P = int(len(tr) * args.ref_seconds / dt * 0.8)
+            elif dt < args.ref_seconds / 4 and len(tr) < n:
+                P = min(n, int(len(tr) * args.ref_seconds / max(dt, 1e-3) * 0.5))
+            else:
+                break
+        sample = len(tr)
         if i >= args.warmup:
-            times.append((P, dt))
+            times.append((len(tr), dt))
     evs = sum(p for p, _ in times) / sum(d for _, d in times)
     cores = 1
     line = {
@@ -167,7 +221,7 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic",
-        "config": dict(desc, events=n, parallelism="single host core"),
+        "config": dict(desc, parallelism="single host core"),
         "cpu_baseline": {
             "value": evs,
             "unit": UNIT,
@@ -199,15 +253,14 @@ def run_b200(args):
 
     from paper_2111_12478_b200 import _native as N
 
-    tr, desc = make_workload(args.workload, rank)
-    n = len(tr)
-    n_acc = int(np.count_nonzero(((tr.tidop >> np.uint32(N.OP_SHIFT)) & np.uint32(7)) <= 1))
-    cfg = tr.cfg_tuple
-    # device-resident inputs (value) and pinned host inputs (e2e)
-    key_h = torch.from_numpy(tr.key.view(np.int64)).pin_memory()
-    to_h = torch.from_numpy(tr.tidop.view(np.int32)).pin_memory()
-    in_h = torch.from_numpy(tr.instr.view(np.int32)).pin_memory()
-    key_d, to_d, in_d = key_h.to(dev), to_h.to(dev), in_h.to(dev)
+    cfg, n, n_acc, (key_d, to_d, in_d), desc = make_workload(args.workload, rank, dev)
+    # pinned host copy of the same trace for the end-to-end leg
+    key_h = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    to_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    in_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    key_h.copy_(key_d)
+    to_h.copy_(to_d)
+    in_h.copy_(in_d)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     # a dedicated stream: repeated analyses of one trace shape replay a captured CUDA graph
     stream = torch.cuda.Stream(device=dev)
@@ -299,7 +352,7 @@ def run_b200(args):
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic",
-        "config": dict(desc, events=n, accesses=n_acc, reports=n_rep, parallelism=f"replicas x{world}",
+        "config": dict(desc, reports=n_rep, parallelism=f"replicas x{world}",
                        l2="flushed before every timed step (256 MiB write)"),
         "e2e": {
             "value": e2e,
@@ -325,7 +378,7 @@ def run_b200(args):
     }
     line["clocks"] = clk.summary()
     if not args.no_cpu_baseline:
-        P, dt = cpu_oracle_run(tr, max_seconds=args.ref_seconds)
+        P, dt = cpu_oracle_run(cfg, (key_d, to_d, in_d), max_seconds=args.ref_seconds)
         line["cpu_baseline"] = {
             "value": P / dt,
             "unit": UNIT,

@@ -147,6 +147,12 @@ int gw_ctx_stats(gw_ctx* c, gw_stats* out);
 /* number of kernels the last analysis launched */
 uint32_t gw_ctx_launches(gw_ctx* c);
 
+/* bench / test infrastructure: generate the C2 / C5 synthetic trace (SURVEY
+ * §8(d)) directly into device buffers of phases*(records*B*W*L + B) events */
+int gw_gen_c2_device(uint32_t blocks, uint32_t warps, uint32_t lanes, uint32_t phases, uint32_t records,
+                     uint64_t words_per_block, uint64_t seed, uint64_t* key, uint32_t* tidop, uint32_t* instr,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

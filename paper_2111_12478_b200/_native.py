@@ -112,6 +112,7 @@ EXPORTS = (
     "gw_ctx_fetch",
     "gw_ctx_stats",
     "gw_ctx_launches",
+    "gw_gen_c2_device",
 )
 
 _lib = None
@@ -163,6 +164,9 @@ def lib():
         L.gw_ctx_stats.restype = C.c_int
         L.gw_ctx_launches.argtypes = [C.c_void_p]
         L.gw_ctx_launches.restype = C.c_uint32
+        L.gw_gen_c2_device.argtypes = [C.c_uint32] * 5 + [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                                          C.c_void_p, C.c_void_p]
+        L.gw_gen_c2_device.restype = C.c_int
         _lib = L
         return L
 
@@ -314,3 +318,11 @@ def analyze(cfg, key, tidop, instr, *, inactive_opt=True):
     ctx = default_context()
     ctx.analyze_host(cfg, key, tidop, instr, inactive_opt=inactive_opt)
     return ctx.fetch()
+
+
+def gen_c2_device(key_ptr, tidop_ptr, instr_ptr, *, blocks, warps, lanes, phases, records, words_per_block, seed,
+                  stream=None) -> int:
+    """Write the C2/C5 recipe trace into device buffers; returns the event count."""
+    _check(lib().gw_gen_c2_device(blocks, warps, lanes, phases, records, words_per_block, seed, key_ptr, tidop_ptr,
+                                  instr_ptr, stream))
+    return phases * (records * blocks * warps * lanes + blocks)

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "access.cuh"
+#include "workloads.cuh"
 #include "common.h"
 
 namespace gw {
@@ -908,4 +909,16 @@ extern "C" int gw_analyze(const gw_trace_view* t, const gw_opts* o, gw_result* o
   int r = gw_ctx_analyze_host(g_default, t, o);
   if (r) return r;
   return gw_ctx_fetch(g_default, out);
+}
+
+// Device-side C2/C5 workload generator (bench / test infrastructure).
+extern "C" int gw_gen_c2_device(uint32_t blocks, uint32_t warps, uint32_t lanes, uint32_t phases, uint32_t records,
+                                uint64_t words_per_block, uint64_t seed, uint64_t* key, uint32_t* tidop,
+                                uint32_t* instr, void* stream) {
+  return guarded([&] {
+    C2Params p{blocks, warps, lanes, phases, records, words_per_block, seed};
+    const uint64_t n = (uint64_t)phases * ((uint64_t)records * blocks * warps * lanes + blocks);
+    GW_LAUNCH(k_gen_c2, 148u * 16u, kThreads, 0, (cudaStream_t)stream, p, (unsigned long long*)key, tidop, instr, n);
+    CK(cudaGetLastError());
+  });
 }

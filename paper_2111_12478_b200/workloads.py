@@ -60,6 +60,43 @@ def c2_params(blocks=64, warps=8, lanes=32, phases=8, records=8, words_per_block
                 words_per_block=words_per_block, seed=seed)
 
 
+def c2_soa_prefix(max_events, blocks=64, warps=8, lanes=32, phases=8, records=8, words_per_block=1024,
+                  seed=2) -> Trace:
+    """The record-aligned prefix (>= min(max_events, N) events, whole records)
+    of :func:`c2_soa` without materialising the whole trace."""
+    per_rec_round = blocks * warps * lanes
+    per_phase = records * per_rec_round + blocks
+    if max_events >= phases * per_phase:
+        return c2_soa(blocks, warps, lanes, phases, records, words_per_block, seed)
+    full = max_events // per_phase
+    head = c2_soa(blocks, warps, lanes, full, records, words_per_block, seed) if full else None
+    rem = max_events - full * per_phase
+    rr = min(records, -(-rem // per_rec_round))  # records of the partial phase
+    part = _c2_phase(blocks, warps, lanes, full, rr, records, words_per_block, seed)
+    parts = [t for t in (head, part) if t is not None]
+    key = np.concatenate([t.key for t in parts])
+    to = np.concatenate([t.tidop for t in parts])
+    ins = np.concatenate([t.instr for t in parts])
+    return Trace(TraceConfig(blocks, warps, lanes), key, to, ins)
+
+
+def _c2_phase(B, W, L, ph, rr, R, WB, seed) -> Trace:
+    """Records r < rr of phase ph (no barriers) -- the C2 recipe."""
+    with np.errstate(over="ignore"):
+        r, b, w, l = np.meshgrid(np.arange(rr), np.arange(B), np.arange(W), np.arange(L), indexing="ij")
+        p = np.uint64(ph)
+        r, b, w, l = (x.astype(np.uint64).ravel() for x in (r, b, w, l))
+        hh = h_np(seed, p, r, b, w, l)
+        own = b * np.uint64(WB) + ((np.uint64(256) * p + np.uint64(L) * w + l) % np.uint64(WB))
+        rnd = h_np(hh, 7) % np.uint64(B * WB)
+        word = np.where(hh < np.uint64(P01), rnd, own)
+        iswr = ((p + r + w) % np.uint64(2)) == 0
+        flat = ((b * np.uint64(W) + w) * np.uint64(L) + l).astype(np.uint32)
+        op = np.where(iswr, np.uint32(N.K_WRITE), np.uint32(N.K_READ)).astype(np.uint32) << np.uint32(N.OP_SHIFT)
+        cont = np.where(l > 0, np.uint32(N.F_CONT), np.uint32(0))
+        return Trace(TraceConfig(B, W, L), word * np.uint64(4), flat | op | cont, (np.uint64(16) * r + w).astype(np.uint32))
+
+
 def c2_soa(blocks=64, warps=8, lanes=32, phases=8, records=8, words_per_block=1024, seed=2) -> Trace:
     """C2: barrier-only trace, one full-mask wacc per (phase, record, block, warp)."""
     with np.errstate(over="ignore"):

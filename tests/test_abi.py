@@ -11,7 +11,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     hdr = open(os.path.join(REPO, "include", "gwcp_b200.h")).read()
-    return sorted(set(re.findall(r"\b(gw_[a-z_]+)\s*\(", hdr)))
+    return sorted(set(re.findall(r"\b(gw_[a-z0-9_]+)\s*\(", hdr)))
 
 
 def test_header_declares_the_bound_symbols():

@@ -178,3 +178,20 @@ def test_graph_replay_host_path():
         tr = WL.c2_soa(blocks=8, warps=4, lanes=32, phases=4, records=4, words_per_block=256, seed=30 + s)
         ctx.analyze_host(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, stream=stream.cuda_stream)
         assert ndjson_lines(tr, ctx.fetch()) == ndjson_lines(tr, O.run_trace(tr))
+
+
+def test_device_generator_matches_numpy_recipe():
+    import torch
+
+    dev = torch.device("cuda", 0)
+    p = dict(blocks=12, warps=4, lanes=32, phases=3, records=5, words_per_block=300, seed=77)
+    want = WL.c2_soa(**p)
+    n = len(want)
+    k = torch.empty(n, dtype=torch.int64, device=dev)
+    t = torch.empty(n, dtype=torch.int32, device=dev)
+    i = torch.empty(n, dtype=torch.int32, device=dev)
+    assert N.gen_c2_device(k.data_ptr(), t.data_ptr(), i.data_ptr(), **p) == n
+    torch.cuda.synchronize()
+    assert np.array_equal(k.cpu().numpy().view(np.uint64), want.key)
+    assert np.array_equal(t.cpu().numpy().view(np.uint32), want.tidop)
+    assert np.array_equal(i.cpu().numpy().view(np.uint32), want.instr)
