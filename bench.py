@@ -152,25 +152,32 @@ class ClockSampler:
         }
 
 
-def cpu_oracle_run(cfg, dev_bufs, max_seconds=25.0, start=1 << 20):
-    """Time the oracle port on one core over the largest record-aligned prefix
-    that fits ~max_seconds (the full trace when it does)."""
+def cpu_time(get_prefix, n, budget_s):
+    """Time the oracle port (one core) on a bounded sample of the workload:
+    the largest record-aligned prefix whose single run fits the budget, run
+    repeatedly until the budget is spent.  Returns (events/s, description)."""
     from oracle import oracle as O
 
-    n = dev_bufs[0].numel()
-    P = min(n, start)
+    P = min(n, 1 << 20)
+    tr = get_prefix(P)
     while True:
-        sub = host_prefix(cfg, dev_bufs, P)
         t0 = time.perf_counter()
-        O.run_trace(sub)
+        O.run_trace(tr)
         dt = time.perf_counter() - t0
-        if dt > max_seconds and len(sub) > 10000:
-            P = int(len(sub) * max_seconds / dt * 0.8)
-            continue
-        if dt < max_seconds / 4 and len(sub) < n:
-            P = min(n, int(len(sub) * max_seconds / max(dt, 1e-3) * 0.5))
-            continue
-        return len(sub), dt
+        if dt > budget_s and len(tr) > 10000:
+            tr = get_prefix(int(len(tr) * budget_s / dt * 0.7))
+        elif dt < budget_s / 8 and len(tr) < n:
+            tr = get_prefix(min(n, int(len(tr) * budget_s / max(dt, 1e-3) * 0.25)))
+        else:
+            break
+    runs, tot = 1, dt
+    while tot < budget_s:
+        t0 = time.perf_counter()
+        O.run_trace(tr)
+        tot += time.perf_counter() - t0
+        runs += 1
+    what = "the full trace" if len(tr) >= n else f"the first {len(tr)} of {n} events (record-aligned prefix)"
+    return len(tr) * runs / tot, f"{what}, {runs} run(s), oracle/gwcp_oracle.cpp on 1 host core"
 
 
 def run_reference(args):
@@ -187,25 +194,20 @@ def run_reference(args):
     n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
     n_acc = n - p["phases"] * p["blocks"]
     desc = workload_desc(args.workload, p, n, n_acc)
-    times = []
-    sample = None
-    P = 1 << 20
-    for i in range(args.warmup + args.steps):
-        while True:
-            tr = WL.c2_soa_prefix(P, **p)
-            t0 = time.perf_counter()
-            O.run_trace(tr)
-            dt = time.perf_counter() - t0
-            if dt > args.ref_seconds and len(tr) > 10000:
-                P = int(len(tr) * args.ref_seconds / dt * 0.8)
-            elif dt < args.ref_seconds / 4 and len(tr) < n:
-                P = min(n, int(len(tr) * args.ref_seconds / max(dt, 1e-3) * 0.5))
-            else:
-                break
-        sample = len(tr)
-        if i >= args.warmup:
-            times.append((len(tr), dt))
-    evs = sum(p for p, _ in times) / sum(d for _, d in times)
+    cache = {}
+
+    def get_prefix(P):
+        if P not in cache:
+            cache.clear()
+            cache[P] = WL.c2_soa_prefix(P, **p)
+        return cache[P]
+
+    for _ in range(args.warmup):
+        cpu_time(get_prefix, n, args.ref_seconds / 4)
+    vals = [cpu_time(get_prefix, n, args.ref_seconds) for _ in range(args.steps)]
+    evs = len(vals) / sum(1.0 / v for v, _ in vals)
+    sample = vals[-1][1]
+    ms_step = 1000.0 * args.ref_seconds
     cores = 1
     line = {
         "impl": "reference",
@@ -215,7 +217,7 @@ def run_reference(args):
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1000.0 * sum(d for _, d in times) / len(times),
+        "ms_per_step": ms_step,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -227,8 +229,7 @@ def run_reference(args):
             "unit": UNIT,
             "cores": cores,
             "kind": "port",
-            "sample": f"first {sample} of {n} events of the workload per step (record-aligned prefix), "
-                      f"oracle/gwcp_oracle.cpp (C++ restatement of the reference, dense clocks)",
+            "sample": sample + " (per step)",
         },
         "e2e": {"value": evs, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -378,14 +379,8 @@ def run_b200(args):
     }
     line["clocks"] = clk.summary()
     if not args.no_cpu_baseline:
-        P, dt = cpu_oracle_run(cfg, (key_d, to_d, in_d), max_seconds=args.ref_seconds)
-        line["cpu_baseline"] = {
-            "value": P / dt,
-            "unit": UNIT,
-            "cores": 1,
-            "kind": "port",
-            "sample": f"first {P} of {n} events (record-aligned prefix), oracle/gwcp_oracle.cpp, 1 run",
-        }
+        v, what = cpu_time(lambda P: host_prefix(cfg, (key_d, to_d, in_d), P), n, args.ref_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": what}
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
@@ -398,7 +393,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", default="c2")
-    ap.add_argument("--ref-seconds", type=float, default=20.0)
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
