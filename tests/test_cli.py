@@ -1,0 +1,60 @@
+"""CLI drop-in: exit codes, NDJSON, stderr (reference cli.py:20-84, pkg/tests/test_cli.py)."""
+
+import json
+import subprocess
+import sys
+
+import pytest
+
+from conftest import REPO, golden_records
+
+
+def _corpus(name):
+    return next(r for r in golden_records() if r["name"] == f"corpus/{name}")
+
+
+def _cli(tmp_path, text, *extra):
+    p = tmp_path / "t.trace"
+    p.write_text(text)
+    return subprocess.run([sys.executable, "-m", "paper_2111_12478_b200.cli", "check", str(p), *extra],
+                          capture_output=True, text=True, cwd=REPO)
+
+
+def test_parse_error_exits_two(tmp_path):
+    r = _cli(tmp_path, "nonsense\n")
+    assert r.returncode == 2
+    assert "line 1: first line must be a config line" in r.stderr
+
+
+def test_validation_error_exits_three(tmp_path):
+    r = _cli(tmp_path, "config blocks=1 warps=1 lanes=1\n0.0.0 end\n0.0.0 wr g:0x10\n")
+    assert r.returncode == 3
+    assert "event 1: event after end of thread 0.0.0" in r.stderr
+    assert "trace is not well formed" in r.stderr
+
+
+def test_other_detectors_are_not_on_the_accelerated_path(tmp_path):
+    r = _cli(tmp_path, _corpus("wcp-classic")["text"], "--detector", "hb")
+    assert r.returncode == 2
+
+
+@pytest.mark.gpu
+def test_racy_trace_exits_one_with_reference_ndjson(tmp_path):
+    rec = _corpus("wcp-classic")
+    r = _cli(tmp_path, rec["text"])
+    assert r.returncode == 1
+    assert r.stdout.splitlines() == rec["reports"]
+    rep = json.loads(r.stdout.splitlines()[0])
+    assert rep["location"] == {"space": "global", "addr": "0x10"} and rep["class"] == "interblock"
+
+
+@pytest.mark.gpu
+def test_clean_trace_exits_zero(tmp_path):
+    r = _cli(tmp_path, _corpus("barrier-separated")["text"])
+    assert r.returncode == 0 and r.stdout == ""
+
+
+@pytest.mark.gpu
+def test_shared_location_carries_block(tmp_path):
+    r = _cli(tmp_path, _corpus("scoped-cs")["text"])
+    assert json.loads(r.stdout.splitlines()[0])["location"] == {"space": "shared", "block": 0, "addr": "0x10"}
