@@ -185,7 +185,7 @@ struct Pipeline {
   }
 
   // per-analysis zeroed block: look-back tile counters + radix histograms
-  static constexpr uint32_t kZeroWords = 1u << 16;
+  static constexpr uint32_t kZeroWords = 1u << 17;
   uint32_t* zero_blk = nullptr;
   uint32_t zero_next = 0;
   uint32_t* zeroed(uint32_t words) {
@@ -220,10 +220,10 @@ struct Pipeline {
     K* ka = C->get<K>(t + "_ka", n);
     uint32_t* va = C->get<uint32_t>(t + "_va", n);
     SortScratch sc;
-    const int npass = (nbits + 7) / 8;
-    sc.ghist = zeroed(kRsMaxPass * 256);
+    const int npass = rs_passes(nbits);
+    sc.ghist = zeroed(kRsMaxPass * 1024);
     sc.ctrs = zeroed(npass);
-    sc.status = C->get<unsigned long long>("rs_status", lb_tiles(n) * 256);
+    sc.status = C->get<unsigned long long>("rs_status", std::max(lb_tiles(n), lb_tiles(tr.n)) * 1024);
     bool alt = radix_sort<K>(keys, ka, vals, va, n, nbits, sc, take_epochs(npass), st);
     if (alt) {
       keys = ka;
@@ -314,7 +314,7 @@ struct Pipeline {
     CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
     if (gmode) {  // fixed epochs in the graph: start from clean flags
       uint32_t* f = C->get<uint32_t>("lb_flag", lb_tiles(N));
-      unsigned long long* rs = C->get<unsigned long long>("rs_status", lb_tiles(N) * 256);
+      unsigned long long* rs = C->get<unsigned long long>("rs_status", lb_tiles(N) * 1024);
       CK(cudaMemsetAsync(f, 0, C->bufs["lb_flag"].cap, st));
       CK(cudaMemsetAsync(rs, 0, C->bufs["rs_status"].cap, st));
     }
