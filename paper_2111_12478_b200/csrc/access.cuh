@@ -56,6 +56,18 @@ __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals) {
   }
 }
 
+// compact arbitrary u64 keys to their varying bit runs
+__global__ void k_compact_u64(const unsigned long long* in, uint64_t n, KeyRuns kr, unsigned long long* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long x = in[i];
+    unsigned long long k = 0;
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+      if (r < kr.n) k |= ((x >> kr.src[r]) & ((kr.width[r] >= 64) ? ~0ull : ((1ull << kr.width[r]) - 1ull))) << kr.dst[r];
+    out[i] = k;
+  }
+}
+
 // stats over the trace (one pass): counts by kind, OR / AND of access keys
 struct Stats {
   unsigned long long n_acc, n_write, n_acq, n_rel, n_end, n_bar, key_or, key_and;

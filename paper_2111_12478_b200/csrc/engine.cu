@@ -369,6 +369,7 @@ struct Pipeline {
     w.inactive_opt = inactive_opt;
     w.abort_flag = scal + SC_ABORT;
     uint32_t maxd = 1, n_incs = 0;
+    uint64_t lcap = 1;
     if (has_locks) {
       const uint64_t nle = hs.n_acq + hs.n_rel + hs.n_end;
       uint32_t* flag = C->get<uint32_t>("lk_flag", N);
@@ -383,22 +384,58 @@ struct Pipeline {
       CK(cudaMemsetAsync(seg_beg, 0, sizeof(uint32_t) * tr.T, st));
       CK(cudaMemsetAsync(seg_end, 0, sizeof(uint32_t) * tr.T, st));
       GW_LAUNCH(k_lock_segs, grid_for(nle), kThreads, 0, st, ktid, (uint32_t)nle, seg_beg, seg_end);
-      unsigned long long* stk = C->get<unsigned long long>("lk_stk", nle);
-      uint32_t* res = C->get<uint32_t>("lk_res", nle);
+      unsigned long long* node_lock = C->get<unsigned long long>("lk_nlock", nle);
+      uint32_t* node_parent = C->get<uint32_t>("lk_nparent", nle);
+      uint32_t* top_after = C->get<uint32_t>("lk_top", nle);
       uint8_t* lflags = C->get<uint8_t>("lflags", N);
       CK(cudaMemsetAsync(lflags, 0, N, st));
-      GW_LAUNCH(k_lock_automaton, grid_for(nle), kThreads, 0, st, tr, ktid, kev, (uint32_t)nle, seg_end, stk, res,
-                lflags, scal + SC_MAXD);
-      GW_LAUNCH(k_lock_access, grid_for(N), kThreads, 0, st, tr, kev, res, seg_beg, seg_end, lflags, scal + SC_NINCS);
-      uint32_t* rank = C->get<uint32_t>("lk_rank", N);
-      scan<uint32_t, OpSum>(LockRelLoad{lflags}, ArrStore<uint32_t>{rank}, N, OpSum(), 0u, false, "sc_u32");
+      GW_LAUNCH(k_lock_automaton, grid_for(nle), kThreads, 0, st, tr, ktid, kev, (uint32_t)nle, seg_end, node_lock,
+                node_parent, top_after, lflags, scal + SC_MAXD);
+      uint32_t* etop = C->get<uint32_t>("lk_etop", N);
+      uint32_t* npair = C->get<uint32_t>("lk_npair", N);
+      GW_LAUNCH(k_lock_access, grid_for(N), kThreads, 0, st, tr, kev, top_after, seg_beg, seg_end, node_parent,
+                lflags, etop, npair, scal + SC_NINCS);
+      uint32_t* poff = C->get<uint32_t>("lk_poff", N);
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{npair}, ArrStore<uint32_t>{poff}, N, OpSum(), 0u, false, "sc_u32");
+      uint32_t hv[4];
+      CK(cudaMemcpyAsync(hv, poff + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hv + 1, npair + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hv + 2, scal, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const uint64_t P = (uint64_t)hv[0] + hv[1];
+      maxd = std::max<uint32_t>(hv[2], 1);
+      n_incs = hv[3];
+      unsigned long long* plock = C->get<unsigned long long>("lk_plock", P + 1);
+      unsigned long long* pk = C->get<unsigned long long>("lk_pk", P + 1);
+      uint32_t* pv = C->get<uint32_t>("lk_pv", P + 1);
+      unsigned long long* orand = C->get<unsigned long long>("lk_orand", 2);
+      GW_LAUNCH(k_orand_init, 1, 1, 0, st, orand);
+      GW_LAUNCH(k_lock_pairs, grid_for(N), kThreads, 0, st, tr, poff, npair, etop, node_lock, node_parent, plock, pv,
+                orand);
+      unsigned long long ho[2];
+      d2h(ho, orand, 2);
+      KeyRuns lkr = key_runs(P ? ho[0] ^ ho[1] : 0ull);
+      lkr.sentinel = 0;
+      lkr.nbits = 0;
+      for (int i = 0; i < lkr.n; i++) lkr.nbits += lkr.width[i];
+      GW_LAUNCH(k_compact_u64, grid_for(P + 1), kThreads, 0, st, plock, P, lkr, pk);
+      sort<unsigned long long>(pk, pv, P, lkr.nbits, "lkp");
+      uint32_t* segstart = C->get<uint32_t>("lk_pseg", P + 1);
+      scan<uint32_t, OpMaxU32>(LockSegLoad{pk}, ArrStore<uint32_t>{segstart}, P, OpMaxU32(), 0u, true, "sc_u32");
+      uint32_t* prank = C->get<uint32_t>("lk_prank", P + 1);
+      // lock table (created here, one entry + ticket per lock) before the ranks kernel inserts into it
+      lcap = pow2_at_least(2 * (hs.n_acq + hs.n_rel) + 2);
+      w.locks = C->get<LockEnt>("t_lock", lcap);
+      w.lock_mask = (uint32_t)(lcap - 1);
+      w.err = scal + SC_ERR;
+      CK(cudaMemsetAsync(w.locks, 0, sizeof(LockEnt) * lcap, st));
+      w.plock = plock;
+      GW_LAUNCH(k_lock_ranks, grid_for(P + 1), kThreads, 0, st, w, pk, pv, segstart, P, prank);
       check_launch();
-      uint32_t hv[2];
-      d2h(hv, scal, 2);
-      maxd = std::max<uint32_t>(hv[0], 1);
-      n_incs = hv[1];
       w.lflags = lflags;
-      w.rank = rank;
+      w.poff = poff;
+      w.npair = npair;
+      w.prank = prank;
     }
 
     // ------------------------------------------------------ walker buffers
@@ -427,7 +464,6 @@ struct Pipeline {
     w.pdiag = C->get<uint32_t>("st_pdiag", T);
     w.nend = C->get<uint32_t>("st_nend", T);
     w.exited = C->get<uint32_t>("st_exited", T);
-    w.ticket = scal + SC_TICKET;
     w.rec_top = scal + SC_REC;
     w.log_top = scal + SC_LOG;
     w.diag_top = scal + SC_DIAG;
@@ -441,18 +477,14 @@ struct Pipeline {
       w.depth = C->get<uint32_t>("st_depth", T);
       w.loghead = C->get<uint32_t>("st_loghead", T);
       w.frames = C->get<Frame>("frames", (uint64_t)T * maxd);
-      uint64_t lcap = pow2_at_least(2 * (hs.n_acq + hs.n_rel) + 2);
       uint64_t icap = pow2_at_least(2 * hs.n_rel + 2);
       uint64_t ccap = pow2_at_least(2 * (uint64_t)n_incs * maxd + 2);
-      w.locks = C->get<LockEnt>("t_lock", lcap);
-      w.lock_mask = (uint32_t)(lcap - 1);
       w.curs = C->get<CurEnt>("t_cur", lcap);
       w.cur_mask = (uint32_t)(lcap - 1);
       w.insts = C->get<InstEnt>("t_inst", icap);
       w.inst_mask = (uint32_t)(icap - 1);
       w.cs = C->get<CsEnt>("t_cs", ccap);
       w.cs_mask = (uint32_t)(ccap - 1);
-      CK(cudaMemsetAsync(w.locks, 0, sizeof(LockEnt) * lcap, st));
       CK(cudaMemsetAsync(w.curs, 0, sizeof(CurEnt) * lcap, st));
       CK(cudaMemsetAsync(w.insts, 0, sizeof(InstEnt) * icap, st));
       CK(cudaMemsetAsync(w.cs, 0, sizeof(CsEnt) * ccap, st));

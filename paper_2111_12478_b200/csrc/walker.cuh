@@ -55,7 +55,7 @@ constexpr uint32_t ERR_ARENA = 1, ERR_TABLE = 2, ERR_FRAMES = 4, ERR_LOG = 8, ER
 
 struct Frame { unsigned long long lock; uint32_t scope, rec, logpos, pad; };
 struct Rec { uint32_t tid, acq_local, scope, rel_hobj, rel_local, closed, next, seq; };
-struct LockEnt { unsigned long long id; uint32_t used, nrec, head, tail, inst_head, pad; };
+struct LockEnt { unsigned long long id; uint32_t used, nrec, head, tail, inst_head, ticket; };
 struct CurEnt { unsigned long long lock; uint32_t tid, used, epoch, last, bound, snap; };
 struct InstEnt { unsigned long long lock; uint32_t scope, used, H, P, next, pad; };
 struct CsEnt { unsigned long long lock, loc; uint32_t scope_rw, used, arr, pad; };
@@ -89,8 +89,10 @@ struct WalkArgs {
   int has_locks;
   uint32_t inactive_opt;
   const uint8_t* lflags;
-  const uint32_t* rank;
-  uint32_t* ticket;
+  const uint32_t* poff;   // lock-related event -> its (lock, rank) pairs
+  const uint32_t* npair;
+  const unsigned long long* plock;
+  const uint32_t* prank;
   LockEnt* locks; uint32_t lock_mask;
   CurEnt* curs; uint32_t cur_mask;
   InstEnt* insts; uint32_t inst_mask;
@@ -141,66 +143,69 @@ __device__ void emit_diag(const WalkArgs& a, uint32_t ev, uint32_t code, uint32_
   a.diags[i] = Diag{ev, code, sub, 0u, lock};
 }
 
-// ---- serialized lock-state tables (only thread 0 of the ticket holder) ----
-__device__ LockEnt* lock_find(const WalkArgs& a, unsigned long long id, bool create) {
-  uint32_t h = (uint32_t)mix64(id) & a.lock_mask;
-  for (uint32_t p = 0; p <= a.lock_mask; p++) {
-    LockEnt* e = &a.locks[(h + p) & a.lock_mask];
-    if (!__ldcg(&e->used)) {
+// ---- lock-state tables -------------------------------------------------
+// Open addressing; a slot's `used` word is 0 empty, 1 being initialised, 2
+// ready.  Different CTAs insert different keys concurrently (keys of lock l are
+// only created under l's ticket), so inserts claim slots with atomicCAS and
+// lookups wait for a claimed slot to become ready before comparing its key.
+__device__ __forceinline__ uint32_t slot_state(const uint32_t* used) { return ld_volatile_u32(used); }
+
+template <class Ent, class Eq, class Init>
+__device__ Ent* ht_find(const WalkArgs& a, Ent* tab, uint32_t mask, uint32_t h, bool create, Eq eq, Init init) {
+  for (uint32_t p = 0; p <= mask; p++) {
+    Ent* e = &tab[(h + p) & mask];
+    uint32_t st = slot_state(&e->used);
+    if (st == 0) {
       if (!create) return nullptr;
-      e->id = id; e->nrec = 0; e->head = NIL; e->tail = NIL; e->inst_head = NIL; e->used = 1;
-      return e;
+      if (atomicCAS(&e->used, 0u, 1u) == 0u) {
+        init(e);
+        __threadfence();
+        atomicExch(&e->used, 2u);
+        return e;
+      }
+      st = slot_state(&e->used);
     }
-    if (__ldcg(&e->id) == id) return e;
+    while (st == 1) st = slot_state(&e->used);
+    __threadfence();
+    if (eq(e)) return e;
   }
   atomicOr(a.err, ERR_TABLE);
   return nullptr;
+}
+
+__device__ LockEnt* lock_find(const WalkArgs& a, unsigned long long id, bool create) {
+  const uint32_t h = (uint32_t)mix64(id) & a.lock_mask;
+  return ht_find(a, a.locks, a.lock_mask, h, create, [&](LockEnt* e) { return __ldcg(&e->id) == id; },
+                 [&](LockEnt* e) {
+                   e->id = id; e->nrec = 0; e->head = NIL; e->tail = NIL; e->inst_head = NIL; e->ticket = 0;
+                 });
 }
 
 __device__ CurEnt* cur_find(const WalkArgs& a, unsigned long long lock, uint32_t tid) {
-  uint32_t h = (uint32_t)mix64(lock * 0x9E3779B97F4A7C15ull ^ tid) & a.cur_mask;
-  for (uint32_t p = 0; p <= a.cur_mask; p++) {
-    CurEnt* e = &a.curs[(h + p) & a.cur_mask];
-    if (!__ldcg(&e->used)) {
-      e->lock = lock; e->tid = tid; e->epoch = NIL; e->last = NIL; e->bound = NIL; e->snap = 0; e->used = 1;
-      return e;
-    }
-    if (__ldcg(&e->lock) == lock && __ldcg(&e->tid) == tid) return e;
-  }
-  atomicOr(a.err, ERR_TABLE);
-  return nullptr;
+  const uint32_t h = (uint32_t)mix64(lock * 0x9E3779B97F4A7C15ull ^ tid) & a.cur_mask;
+  return ht_find(a, a.curs, a.cur_mask, h, true,
+                 [&](CurEnt* e) { return __ldcg(&e->lock) == lock && __ldcg(&e->tid) == tid; },
+                 [&](CurEnt* e) {
+                   e->lock = lock; e->tid = tid; e->epoch = NIL; e->last = NIL; e->bound = NIL; e->snap = 0;
+                 });
 }
 
 __device__ InstEnt* inst_find(const WalkArgs& a, unsigned long long lock, uint32_t scope, bool create) {
-  uint32_t h = (uint32_t)mix64(lock ^ ((unsigned long long)scope << 40) ^ 0x51ull) & a.inst_mask;
-  for (uint32_t p = 0; p <= a.inst_mask; p++) {
-    InstEnt* e = &a.insts[(h + p) & a.inst_mask];
-    if (!__ldcg(&e->used)) {
-      if (!create) return nullptr;
-      e->lock = lock; e->scope = scope; e->H = NIL; e->P = NIL; e->next = NIL; e->used = 1;
-      return e;
-    }
-    if (__ldcg(&e->lock) == lock && __ldcg(&e->scope) == scope) return e;
-  }
-  atomicOr(a.err, ERR_TABLE);
-  return nullptr;
+  const uint32_t h = (uint32_t)mix64(lock ^ ((unsigned long long)scope << 40) ^ 0x51ull) & a.inst_mask;
+  return ht_find(a, a.insts, a.inst_mask, h, create,
+                 [&](InstEnt* e) { return __ldcg(&e->lock) == lock && __ldcg(&e->scope) == scope; },
+                 [&](InstEnt* e) { e->lock = lock; e->scope = scope; e->H = NIL; e->P = NIL; e->next = NIL; });
 }
 
 __device__ CsEnt* cs_find(const WalkArgs& a, unsigned long long lock, uint32_t scope, unsigned long long loc,
                           uint32_t rw, bool create) {
-  uint32_t srw = (scope << 1) | rw;  // SC_DEV<<1|rw wraps but stays unique per (scope,rw) pair within a lock
-  uint32_t h = (uint32_t)mix64(lock ^ mix64(loc) ^ ((unsigned long long)scope << 33) ^ rw) & a.cs_mask;
-  for (uint32_t p = 0; p <= a.cs_mask; p++) {
-    CsEnt* e = &a.cs[(h + p) & a.cs_mask];
-    if (!__ldcg(&e->used)) {
-      if (!create) return nullptr;
-      e->lock = lock; e->loc = loc; e->scope_rw = srw; e->arr = NIL; e->used = 1;
-      return e;
-    }
-    if (__ldcg(&e->lock) == lock && __ldcg(&e->loc) == loc && __ldcg(&e->scope_rw) == srw) return e;
-  }
-  atomicOr(a.err, ERR_TABLE);
-  return nullptr;
+  const uint32_t srw = (scope << 1) | rw;
+  const uint32_t h = (uint32_t)mix64(lock ^ mix64(loc) ^ ((unsigned long long)scope << 33) ^ rw) & a.cs_mask;
+  return ht_find(a, a.cs, a.cs_mask, h, create,
+                 [&](CsEnt* e) {
+                   return __ldcg(&e->lock) == lock && __ldcg(&e->loc) == loc && __ldcg(&e->scope_rw) == srw;
+                 },
+                 [&](CsEnt* e) { e->lock = lock; e->loc = loc; e->scope_rw = srw; e->arr = NIL; });
 }
 
 // ------------------------------------------------------------- helpers ----
@@ -370,25 +375,41 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
 }
 
 // --------------------------------------------------------------- locks ----
-__device__ __forceinline__ void ticket_wait(const WalkArgs& a, uint32_t r) {
+// Per-lock tickets.  A lock-related event e (successful acquire / release of
+// l, or an access inside critical sections of l1..ld) may touch the state of
+// lock l only when l's ticket equals e's rank among the l-events in trace
+// order.  Every wait is for an earlier event, and an earlier event never
+// waits for a later one, so the walk is deadlock-free with all walker CTAs
+// co-resident; events on different locks proceed in parallel.
+__device__ void tickets_wait(const WalkArgs& a, uint32_t e) {
   if (threadIdx.x == 0) {
-    volatile uint32_t* tk = a.ticket;
-    uint32_t ns = 32;
-    while (*tk != r) {
-      __nanosleep(ns);
-      if (ns < 1024) ns <<= 1;
+    const uint32_t off = a.poff[e], np = a.npair[e];
+    for (uint32_t j = 0; j < np; j++) {
+      LockEnt* lk = lock_find(a, a.plock[off + j], false);
+      if (!lk) { atomicOr(a.err, ERR_INTERNAL); continue; }
+      const uint32_t r = a.prank[off + j];
+      volatile uint32_t* tk = &lk->ticket;
+      uint32_t ns = 32;
+      while (*tk != r) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
     }
     __threadfence();
   }
   __syncthreads();
   __threadfence();
 }
-__device__ __forceinline__ void ticket_release(const WalkArgs& a, uint32_t r) {
+__device__ void tickets_release(const WalkArgs& a, uint32_t e) {
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    atomicExch(a.ticket, r + 1);
+    const uint32_t off = a.poff[e], np = a.npair[e];
+    for (uint32_t j = 0; j < np; j++) {
+      LockEnt* lk = lock_find(a, a.plock[off + j], false);
+      if (lk) atomicExch(&lk->ticket, a.prank[off + j] + 1);
+    }
   }
 }
 
@@ -473,9 +494,9 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * T;
   uint32_t* H = P + T;
   __shared__ LockEnt* s_lk;
-  if (threadIdx.x == 0) s_lk = lock_find(a, lock, true);
+  if (threadIdx.x == 0) s_lk = lock_find(a, lock, false);  // created by the pre-pass
   __syncthreads();
-  if (!s_lk) return;
+  if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); return; }
   materialize(P, a.arena, a.pobj[t], T, t, a.pdiag[t]);
   int pch = drain(a, t, lock, cur, P);
   materialize(H, a.arena, a.hobj[t], T, t, a.local[t]);
@@ -832,17 +853,15 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
             if (threadIdx.x == 0) emit_diag(a, e, kd == GW_K_ACQUIRE ? GW_D_REENTRANT : GW_D_UNHELD, 0, lock);
             __syncthreads();
           } else {
-            const uint32_t r = a.rank[e];
-            ticket_wait(a, r);
+            tickets_wait(a, e);
             if (kd == GW_K_ACQUIRE) do_acquire(a, e, to, lock);
             else do_release(a, e, to, lock);
-            ticket_release(a, r);
+            tickets_release(a, e);
           }
         } else {  // in-CS access
-          const uint32_t r = a.rank[e];
-          ticket_wait(a, r);
+          tickets_wait(a, e);
           do_incs_access(a, e, to, tr.key[e]);
-          ticket_release(a, r);
+          tickets_release(a, e);
         }
       }
       pos = h + 1;
@@ -978,55 +997,138 @@ __global__ void k_lock_segs(const uint32_t* ktid, uint32_t n, uint32_t* seg_beg,
     if (i == n - 1 || ktid[i + 1] != t) seg_end[t] = i + 1;
   }
 }
+// The per-thread lock stacks form a persistent tree: a successful acquire at
+// sorted position p creates node p = (lock, parent = current top); a
+// successful release pops to the parent; END resets the stack.  top[p] is the
+// stack after lock event p, so any event's lock set is a walk to the root.
 __global__ void k_lock_automaton(DevTrace tr, const uint32_t* ktid, const uint32_t* kev, uint32_t n,
-                                 const uint32_t* seg_end, unsigned long long* stk, uint32_t* res, uint8_t* lflags,
-                                 uint32_t* maxd) {
+                                 const uint32_t* seg_end, unsigned long long* node_lock, uint32_t* node_parent,
+                                 uint32_t* top_after, uint8_t* lflags, uint32_t* maxd) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    uint32_t t = ktid[i];
+    const uint32_t t = ktid[i];
     if (i != 0 && ktid[i - 1] == t) continue;
-    uint32_t end = seg_end[t];
-    uint32_t d = 0, md = 0;
+    const uint32_t end = seg_end[t];
+    uint32_t top = NIL, d = 0, md = 0;
     for (uint32_t p = i; p < end; p++) {
-      uint32_t e = kev[p];
-      uint32_t k = ev_kind(tr.tidop[e]);
-      unsigned long long lk = tr.key[e];
+      const uint32_t e = kev[p];
+      const uint32_t k = ev_kind(tr.tidop[e]);
+      const unsigned long long lk = tr.key[e];
       uint8_t ok = 0;
-      if (k == GW_K_ACQUIRE) {
+      if (k == GW_K_ACQUIRE) {  // reentrant iff lk is anywhere on the stack (gwcp.py:178)
         bool in = false;
-        for (uint32_t s = 0; s < d; s++) in |= stk[i + s] == lk;
-        if (!in) { stk[i + d] = lk; d++; ok = 1; }
-      } else if (k == GW_K_RELEASE) {
-        if (d > 0 && stk[i + d - 1] == lk) { d--; ok = 1; }
-      } else {
+        for (uint32_t q = top; q != NIL && !in; q = node_parent[q]) in = node_lock[q] == lk;
+        if (!in) {
+          node_lock[p] = lk;
+          node_parent[p] = top;
+          top = p;
+          d++;
+          ok = 1;
+        }
+      } else if (k == GW_K_RELEASE) {  // only the top frame can be released (gwcp.py:197)
+        if (top != NIL && node_lock[top] == lk) {
+          top = node_parent[top];
+          d--;
+          ok = 1;
+        }
+      } else {  // END clears the frames (gwcp.py:322-330)
+        top = NIL;
         d = 0;
       }
       md = max(md, d);
-      res[p] = d;
+      top_after[p] = top;
       if (k != GW_K_END) lflags[e] = ok ? (LF_OK | LF_LOCKREL) : 0;
     }
     atomicMax(maxd, md);
   }
 }
-__global__ void k_lock_access(DevTrace tr, const uint32_t* kev, const uint32_t* res, const uint32_t* seg_beg,
-                              const uint32_t* seg_end, uint8_t* lflags, uint32_t* n_incs) {
+// accesses: in a critical section iff the thread's stack is non-empty; npair =
+// number of locks the event synchronises on (stack depth for accesses, 1 for a
+// successful acquire / release)
+__global__ void k_lock_access(DevTrace tr, const uint32_t* kev, const uint32_t* top_after, const uint32_t* seg_beg,
+                              const uint32_t* seg_end, const uint32_t* node_parent, uint8_t* lflags, uint32_t* etop,
+                              uint32_t* npair, uint32_t* n_incs) {
   uint32_t cnt = 0;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t to = tr.tidop[e];
-    uint32_t k = ev_kind(to);
-    if (k > GW_K_WRITE) continue;
-    uint32_t t = ev_tid(to);
-    uint32_t lo = seg_beg[t], hi = seg_end[t];
-    uint8_t f = 0;
-    if (lo < hi) {
-      // last lock event of t before e
-      uint32_t l = lo, h = hi;
-      while (l < h) { uint32_t m = (l + h) >> 1; if (kev[m] < (uint32_t)e) l = m + 1; else h = m; }
-      if (l > lo && res[l - 1] > 0) { f = LF_INCS | LF_LOCKREL; cnt++; }
+    const uint32_t to = tr.tidop[e];
+    const uint32_t k = ev_kind(to);
+    uint32_t np = 0, top = NIL;
+    if (k <= GW_K_WRITE) {
+      const uint32_t t = ev_tid(to);
+      const uint32_t lo = seg_beg[t], hi = seg_end[t];
+      uint8_t f = 0;
+      if (lo < hi) {  // last lock event of t before e
+        uint32_t l = lo, h = hi;
+        while (l < h) { const uint32_t m = (l + h) >> 1; if (kev[m] < (uint32_t)e) l = m + 1; else h = m; }
+        if (l > lo) top = top_after[l - 1];
+        if (top != NIL) {
+          f = LF_INCS | LF_LOCKREL;
+          cnt++;
+          for (uint32_t q = top; q != NIL; q = node_parent[q]) np++;
+        }
+      }
+      lflags[e] = f;
+    } else if (k == GW_K_ACQUIRE || k == GW_K_RELEASE) {
+      np = (lflags[e] & LF_OK) ? 1u : 0u;
     }
-    lflags[e] = f;
+    etop[e] = top;
+    npair[e] = np;
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_incs, cnt);
+}
+// emit (lock, event) pairs in event order (+ OR/AND of the lock ids for key compaction)
+__global__ void k_lock_pairs(DevTrace tr, const uint32_t* poff, const uint32_t* npair, const uint32_t* etop,
+                             const unsigned long long* node_lock, const uint32_t* node_parent,
+                             unsigned long long* plock, uint32_t* pv, unsigned long long* orand) {
+  unsigned long long ko = 0, ka = ~0ull;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t np = npair[e];
+    if (!np) continue;
+    const uint32_t off = poff[e];
+    const uint32_t k = ev_kind(tr.tidop[e]);
+    if (k == GW_K_ACQUIRE || k == GW_K_RELEASE) {
+      plock[off] = tr.key[e];
+    } else {
+      uint32_t j = 0;
+      for (uint32_t q = etop[e]; q != NIL; q = node_parent[q]) plock[off + j++] = node_lock[q];
+    }
+    for (uint32_t j = 0; j < np; j++) {
+      ko |= plock[off + j];
+      ka &= plock[off + j];
+      pv[off + j] = off + j;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ko |= __shfl_xor_sync(0xffffffffu, ko, o);
+    ka &= __shfl_xor_sync(0xffffffffu, ka, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicOr(orand, ko);
+    atomicAnd(orand + 1, ka);
+  }
+}
+// sorted by lock (stable => event order within a lock): rank within the lock
+struct LockSegLoad {
+  const unsigned long long* k;
+  __device__ __forceinline__ uint32_t operator()(uint64_t i) const {
+    return (i == 0 || k[i] != k[i - 1]) ? (uint32_t)i : 0u;
+  }
+};
+struct OpMaxU32 {
+  __device__ __forceinline__ uint32_t operator()(const uint32_t& a, const uint32_t& b) const { return max(a, b); }
+};
+__global__ void k_lock_ranks(const WalkArgs a, const unsigned long long* sk, const uint32_t* sv,
+                             const uint32_t* segstart, uint64_t P, uint32_t* prank) {
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t pair = sv[q];
+    prank[pair] = (uint32_t)(q - segstart[q]);
+    if (q == 0 || sk[q] != sk[q - 1]) lock_find(a, a.plock[pair], true);  // one table entry (+ ticket) per lock
+  }
+}
+__global__ void k_orand_init(unsigned long long* orand) {
+  orand[0] = 0ull;
+  orand[1] = ~0ull;
 }
 
 struct LockRelLoad {
