@@ -442,10 +442,10 @@ struct Pipeline {
     const uint32_t T = tr.T;
     uint64_t arena_words;
     if (!has_locks) {
-      arena_words = hs.n_bar * (uint64_t)(tr.BS + 2) + 64;
+      arena_words = hs.n_bar * (uint64_t)(tr.BS + OBJ_HDR + 3) + 64;
     } else {
       uint64_t nobj = 2 * hs.n_bar + 2 * hs.n_acq + 4 * hs.n_rel + (uint64_t)n_incs * (1 + maxd) + 4;
-      arena_words = nobj * (uint64_t)(T + 2) + 64;
+      arena_words = nobj * (uint64_t)(T + OBJ_HDR + 3) + 64;
       size_t free_b = 0, total_b = 0;
       CK(cudaMemGetInfo(&free_b, &total_b));
       uint64_t cap_words = (uint64_t)(free_b * 0.6) / 4;

@@ -43,6 +43,7 @@ constexpr uint32_t NIL = 0xFFFFFFFFu;
 constexpr uint32_t SC_DEV = 0xFFFFFFFFu;  // device scope
 constexpr int kWalkCH = 2048;              // events staged per chunk
 constexpr int kAccSmem = 4096;             // barrier accumulator kept in smem up to this span
+constexpr uint32_t OBJ_HDR = 4;            // object header {lo, len, pad, pad}: data 16-byte aligned
 
 // lflags bits (lock pre-pass)
 constexpr uint8_t LF_OK = 1;      // successful acquire / release
@@ -122,16 +123,17 @@ __device__ __forceinline__ uint32_t obj_get(const uint32_t* arena, uint32_t o, u
   if (o == NIL) return 0u;
   uint32_t lo = arena[o], len = arena[o + 1];
   uint32_t d = u - lo;
-  return d < len ? arena[o + 2 + d] : 0u;
+  return d < len ? arena[o + OBJ_HDR + d] : 0u;
 }
 __device__ __forceinline__ uint32_t obj_get_cg(const uint32_t* arena, uint32_t o, uint32_t u) {
   if (o == NIL) return 0u;
   uint32_t lo = __ldcg(arena + o), len = __ldcg(arena + o + 1);
   uint32_t d = u - lo;
-  return d < len ? __ldcg(arena + o + 2 + d) : 0u;
+  return d < len ? __ldcg(arena + o + OBJ_HDR + d) : 0u;
 }
 
 __device__ __forceinline__ uint32_t arena_alloc(const WalkArgs& a, uint32_t words) {
+  words = (words + 3u) & ~3u;  // keep every object 16-byte aligned
   unsigned long long o = atomicAdd(a.arena_top, (unsigned long long)words);
   if (o + words > a.arena_cap) { atomicOr(a.err, ERR_ARENA); return NIL; }
   return (uint32_t)o;
@@ -235,25 +237,77 @@ __device__ __forceinline__ int block_or(int v) {
   return __syncthreads_or(v);
 }
 
-// dst[0..T) (dense, CTA-private scratch) max= object o; returns nonzero if any entry grew
-__device__ __forceinline__ int join_obj_dense(uint32_t* dst, const uint32_t* arena, uint32_t o) {
+// ---- CTA-wide dense vector ops (uint4 when 16-byte aligned) -------------
+__device__ __forceinline__ bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+__device__ __forceinline__ uint4 max4(uint4 a, uint4 b) {
+  return make_uint4(max(a.x, b.x), max(a.y, b.y), max(a.z, b.z), max(a.w, b.w));
+}
+__device__ __forceinline__ bool gt4(uint4 a, uint4 b) { return a.x > b.x || a.y > b.y || a.z > b.z || a.w > b.w; }
+
+// dst[0..n) max= src[0..n) (src read through L2); returns nonzero if dst grew
+__device__ __forceinline__ int vjoin(uint32_t* dst, const uint32_t* src, uint32_t n) {
   int ch = 0;
-  if (o != NIL) {
-    uint32_t lo = __ldcg(arena + o), len = __ldcg(arena + o + 1);
-    for (uint32_t i = threadIdx.x; i < len; i += kThreads) {
-      uint32_t v = __ldcg(arena + o + 2 + i);
-      if (v > dst[lo + i]) { dst[lo + i] = v; ch = 1; }
+  if (al16(dst) && al16(src)) {
+    const uint32_t n4 = n >> 2;
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < n4; i += kThreads) {
+      const uint4 v = __ldcg(s4 + i), o = d4[i];
+      if (gt4(v, o)) { d4[i] = max4(v, o); ch = 1; }
+    }
+    for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) {
+      const uint32_t v = __ldcg(src + i);
+      if (v > dst[i]) { dst[i] = v; ch = 1; }
+    }
+  } else {
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+      const uint32_t v = __ldcg(src + i);
+      if (v > dst[i]) { dst[i] = v; ch = 1; }
     }
   }
   return ch;
+}
+__device__ __forceinline__ void vcopy(uint32_t* dst, const uint32_t* src, uint32_t n) {
+  if (al16(dst) && al16(src)) {
+    const uint32_t n4 = n >> 2;
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < n4; i += kThreads)
+      reinterpret_cast<uint4*>(dst)[i] = __ldcg(reinterpret_cast<const uint4*>(src) + i);
+    for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) dst[i] = __ldcg(src + i);
+  } else {
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) dst[i] = __ldcg(src + i);
+  }
+}
+__device__ __forceinline__ void vfill0(uint32_t* dst, uint32_t n) {
+  if (al16(dst)) {
+    const uint32_t n4 = n >> 2;
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < n4; i += kThreads) reinterpret_cast<uint4*>(dst)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) dst[i] = 0u;
+  } else {
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) dst[i] = 0u;
+  }
+}
+
+// dst[0..T) (dense, CTA-private scratch) max= object o; returns nonzero if any entry grew
+__device__ __forceinline__ int join_obj_dense(uint32_t* dst, const uint32_t* arena, uint32_t o) {
+  if (o == NIL) return 0;
+  const uint32_t lo = __ldcg(arena + o), len = __ldcg(arena + o + 1);
+  return vjoin(dst + lo, arena + o + OBJ_HDR, len);
 }
 
 // materialize clock object o with diagonal [t] := diag into dense dst[0..T)
 __device__ __forceinline__ void materialize(uint32_t* dst, const uint32_t* arena, uint32_t o, uint32_t T, uint32_t t,
                                             uint32_t diag) {
-  for (uint32_t i = threadIdx.x; i < T; i += kThreads) dst[i] = 0u;
-  __syncthreads();
-  join_obj_dense(dst, arena, o);
+  if (o != NIL && __ldcg(arena + o) == 0 && __ldcg(arena + o + 1) == T) {
+    vcopy(dst, arena + o + OBJ_HDR, T);  // full-range object: plain copy
+  } else {
+    vfill0(dst, T);
+    __syncthreads();
+    join_obj_dense(dst, arena, o);
+  }
   __syncthreads();
   if (threadIdx.x == 0) dst[t] = diag;
   __syncthreads();
@@ -263,14 +317,13 @@ __device__ __forceinline__ void materialize(uint32_t* dst, const uint32_t* arena
 __device__ uint32_t publish_dense(const WalkArgs& a, const uint32_t* src, uint32_t T) {
   __shared__ uint32_t s_o;
   if (threadIdx.x == 0) {
-    uint32_t o = arena_alloc(a, T + 2);
+    uint32_t o = arena_alloc(a, T + OBJ_HDR);
     if (o != NIL) { a.arena[o] = 0; a.arena[o + 1] = T; }
     s_o = o;
   }
   __syncthreads();
   uint32_t o = s_o;
-  if (o != NIL)
-    for (uint32_t i = threadIdx.x; i < T; i += kThreads) a.arena[o + 2 + i] = src[i];
+  if (o != NIL) vcopy(a.arena + o + OBJ_HDR, src, T);
   __syncthreads();
   return o;
 }
@@ -315,7 +368,7 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
     uint32_t lo = block_min_u32(mylo), hi = block_max_u32(myhi);
     uint32_t span = hi - lo;
     uint32_t* acc = span <= (uint32_t)kAccSmem ? s_acc : a.scratch + (size_t)blockIdx.x * 3 * tr.T + 2 * tr.T;
-    for (uint32_t i = threadIdx.x; i < span; i += kThreads) acc[i] = 0u;
+    vfill0(acc, span);
     __syncthreads();
     // join each distinct participant object once
     uint32_t done_lo = 0;  // objects < done_lo already joined (ids increase strictly per round)
@@ -331,12 +384,8 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
       }
       uint32_t om = block_min_u32(mymin);
       if (om == NIL) break;
-      uint32_t olo = a.arena[om], olen = a.arena[om + 1];
-      for (uint32_t i = threadIdx.x; i < olen; i += kThreads) {
-        uint32_t v = a.arena[om + 2 + i];
-        uint32_t* d = &acc[olo - lo + i];
-        if (v > *d) *d = v;
-      }
+      const uint32_t olo = a.arena[om], olen = a.arena[om + 1];
+      vjoin(acc + (olo - lo), a.arena + om + OBJ_HDR, olen);
       __syncthreads();
       done_lo = om + 1;
     }
@@ -349,14 +398,13 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
     __syncthreads();
     __shared__ uint32_t s_no;
     if (threadIdx.x == 0) {
-      uint32_t o = arena_alloc(a, span + 2);
+      uint32_t o = arena_alloc(a, span + OBJ_HDR);
       if (o != NIL) { a.arena[o] = lo; a.arena[o + 1] = span; }
       s_no = o;
     }
     __syncthreads();
     uint32_t no = s_no;
-    if (no != NIL)
-      for (uint32_t i = threadIdx.x; i < span; i += kThreads) a.arena[no + 2 + i] = acc[i];
+    if (no != NIL) vcopy(a.arena + no + OBJ_HDR, acc, span);
     newobj[kind] = no;
     __syncthreads();
   }
@@ -593,7 +641,7 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
         CsEnt* ce = cs_find(a, lock, inst, le.loc, le.rw, true);
         if (!ce) break;
         if (ce->arr == NIL) {
-          uint32_t o = arena_alloc(a, T + 2);
+          uint32_t o = arena_alloc(a, T + OBJ_HDR);
           if (o == NIL) break;
           a.arena[o] = 0; a.arena[o + 1] = T;
           ce->arr = o;
@@ -605,15 +653,9 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     __syncthreads();
     const uint32_t arr = s_arr;
     if (arr == NIL) break;
-    uint32_t* dst = a.arena + arr + 2;
-    if (s_new) {
-      for (uint32_t i = threadIdx.x; i < T; i += kThreads) dst[i] = H[i];
-    } else {
-      for (uint32_t i = threadIdx.x; i < T; i += kThreads) {
-        uint32_t v = H[i];
-        if (v > __ldcg(dst + i)) dst[i] = v;
-      }
-    }
+    uint32_t* dst = a.arena + arr + OBJ_HDR;
+    if (s_new) vcopy(dst, H, T);
+    else vjoin(dst, H, T);
     __syncthreads();
   }
   // instance clocks H_i, P_i (gwcp.py:211-216)
@@ -624,7 +666,7 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     s_H = NIL; s_P = NIL;
     if (ie) {
       if (ie->H == NIL) {
-        uint32_t oh = arena_alloc(a, T + 2), op = arena_alloc(a, T + 2);
+        uint32_t oh = arena_alloc(a, T + OBJ_HDR), op = arena_alloc(a, T + OBJ_HDR);
         if (oh != NIL) { a.arena[oh] = 0; a.arena[oh + 1] = T; }
         if (op != NIL) { a.arena[op] = 0; a.arena[op + 1] = T; }
         ie->H = oh; ie->P = op;
@@ -637,16 +679,10 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   }
   __syncthreads();
   if (s_H != NIL && s_P != NIL) {
-    uint32_t* dh = a.arena + s_H + 2;
-    uint32_t* dp = a.arena + s_P + 2;
-    for (uint32_t i = threadIdx.x; i < T; i += kThreads) {
-      uint32_t h = H[i], p = P[i];
-      if (s_newi) { dh[i] = h; dp[i] = p; }
-      else {
-        if (h > __ldcg(dh + i)) dh[i] = h;
-        if (p > __ldcg(dp + i)) dp[i] = p;
-      }
-    }
+    uint32_t* dh = a.arena + s_H + OBJ_HDR;
+    uint32_t* dp = a.arena + s_P + OBJ_HDR;
+    if (s_newi) { vcopy(dh, H, T); vcopy(dp, P, T); }
+    else { vjoin(dh, H, T); vjoin(dp, P, T); }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -743,7 +779,7 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
   __shared__ uint32_t s_to[kWalkCH];
   __shared__ uint32_t s_hard[kWalkCH + 1];
   __shared__ uint32_t s_nh;
-  __shared__ uint32_t s_acc[kAccSmem];
+  __shared__ __align__(16) uint32_t s_acc[kAccSmem];
   const DevTrace& tr = a.tr;
   const uint32_t g = blockIdx.x;
   // my range in the partition
@@ -884,7 +920,7 @@ struct SnapArgs {
 };
 
 __global__ void __launch_bounds__(kThreads) k_walker_snap(WalkArgs a, SnapArgs s) {
-  __shared__ uint32_t s_acc[kAccSmem];
+  __shared__ __align__(16) uint32_t s_acc[kAccSmem];
   const DevTrace& tr = a.tr;
   if (*(volatile const uint32_t*)a.abort_flag) return;
   for (uint32_t b = blockIdx.x; b < tr.B; b += gridDim.x) {
