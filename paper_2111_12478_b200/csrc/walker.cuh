@@ -244,7 +244,16 @@ __device__ __forceinline__ uint4 max4(uint4 a, uint4 b) {
 }
 __device__ __forceinline__ bool gt4(uint4 a, uint4 b) { return a.x > b.x || a.y > b.y || a.z > b.z || a.w > b.w; }
 
-// dst[0..n) max= src[0..n) (src read through L2); returns nonzero if dst grew
+// Loads through L2 (ld.global.cg) for data other CTAs wrote (arena objects,
+// lock-state clocks); plain loads for CTA-private scratch or shared memory.
+template <bool CG, class T>
+__device__ __forceinline__ T ldx(const T* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return *p;
+}
+
+// dst[0..n) max= src[0..n); returns nonzero if dst grew
+template <bool SRC_CG, bool DST_CG>
 __device__ __forceinline__ int vjoin(uint32_t* dst, const uint32_t* src, uint32_t n) {
   int ch = 0;
   if (al16(dst) && al16(src)) {
@@ -253,31 +262,32 @@ __device__ __forceinline__ int vjoin(uint32_t* dst, const uint32_t* src, uint32_
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < n4; i += kThreads) {
-      const uint4 v = __ldcg(s4 + i), o = d4[i];
+      const uint4 v = ldx<SRC_CG>(s4 + i), o = ldx<DST_CG>(d4 + i);
       if (gt4(v, o)) { d4[i] = max4(v, o); ch = 1; }
     }
     for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) {
-      const uint32_t v = __ldcg(src + i);
-      if (v > dst[i]) { dst[i] = v; ch = 1; }
+      const uint32_t v = ldx<SRC_CG>(src + i);
+      if (v > ldx<DST_CG>(dst + i)) { dst[i] = v; ch = 1; }
     }
   } else {
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
-      const uint32_t v = __ldcg(src + i);
-      if (v > dst[i]) { dst[i] = v; ch = 1; }
+      const uint32_t v = ldx<SRC_CG>(src + i);
+      if (v > ldx<DST_CG>(dst + i)) { dst[i] = v; ch = 1; }
     }
   }
   return ch;
 }
+template <bool SRC_CG>
 __device__ __forceinline__ void vcopy(uint32_t* dst, const uint32_t* src, uint32_t n) {
   if (al16(dst) && al16(src)) {
     const uint32_t n4 = n >> 2;
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < n4; i += kThreads)
-      reinterpret_cast<uint4*>(dst)[i] = __ldcg(reinterpret_cast<const uint4*>(src) + i);
-    for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) dst[i] = __ldcg(src + i);
+      reinterpret_cast<uint4*>(dst)[i] = ldx<SRC_CG>(reinterpret_cast<const uint4*>(src) + i);
+    for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) dst[i] = ldx<SRC_CG>(src + i);
   } else {
-    for (uint32_t i = threadIdx.x; i < n; i += kThreads) dst[i] = __ldcg(src + i);
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) dst[i] = ldx<SRC_CG>(src + i);
   }
 }
 __device__ __forceinline__ void vfill0(uint32_t* dst, uint32_t n) {
@@ -295,14 +305,14 @@ __device__ __forceinline__ void vfill0(uint32_t* dst, uint32_t n) {
 __device__ __forceinline__ int join_obj_dense(uint32_t* dst, const uint32_t* arena, uint32_t o) {
   if (o == NIL) return 0;
   const uint32_t lo = __ldcg(arena + o), len = __ldcg(arena + o + 1);
-  return vjoin(dst + lo, arena + o + OBJ_HDR, len);
+  return vjoin<true, false>(dst + lo, arena + o + OBJ_HDR, len);
 }
 
 // materialize clock object o with diagonal [t] := diag into dense dst[0..T)
 __device__ __forceinline__ void materialize(uint32_t* dst, const uint32_t* arena, uint32_t o, uint32_t T, uint32_t t,
                                             uint32_t diag) {
   if (o != NIL && __ldcg(arena + o) == 0 && __ldcg(arena + o + 1) == T) {
-    vcopy(dst, arena + o + OBJ_HDR, T);  // full-range object: plain copy
+    vcopy<true>(dst, arena + o + OBJ_HDR, T);  // full-range object: plain copy
   } else {
     vfill0(dst, T);
     __syncthreads();
@@ -323,7 +333,7 @@ __device__ uint32_t publish_dense(const WalkArgs& a, const uint32_t* src, uint32
   }
   __syncthreads();
   uint32_t o = s_o;
-  if (o != NIL) vcopy(a.arena + o + OBJ_HDR, src, T);
+  if (o != NIL) vcopy<false>(a.arena + o + OBJ_HDR, src, T);
   __syncthreads();
   return o;
 }
@@ -385,7 +395,7 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
       uint32_t om = block_min_u32(mymin);
       if (om == NIL) break;
       const uint32_t olo = a.arena[om], olen = a.arena[om + 1];
-      vjoin(acc + (olo - lo), a.arena + om + OBJ_HDR, olen);
+      vjoin<true, false>(acc + (olo - lo), a.arena + om + OBJ_HDR, olen);
       __syncthreads();
       done_lo = om + 1;
     }
@@ -404,7 +414,7 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
     }
     __syncthreads();
     uint32_t no = s_no;
-    if (no != NIL) vcopy(a.arena + no + OBJ_HDR, acc, span);
+    if (no != NIL) vcopy<false>(a.arena + no + OBJ_HDR, acc, span);
     newobj[kind] = no;
     __syncthreads();
   }
@@ -654,8 +664,8 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     const uint32_t arr = s_arr;
     if (arr == NIL) break;
     uint32_t* dst = a.arena + arr + OBJ_HDR;
-    if (s_new) vcopy(dst, H, T);
-    else vjoin(dst, H, T);
+    if (s_new) vcopy<false>(dst, H, T);
+    else vjoin<false, true>(dst, H, T);
     __syncthreads();
   }
   // instance clocks H_i, P_i (gwcp.py:211-216)
@@ -681,8 +691,8 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   if (s_H != NIL && s_P != NIL) {
     uint32_t* dh = a.arena + s_H + OBJ_HDR;
     uint32_t* dp = a.arena + s_P + OBJ_HDR;
-    if (s_newi) { vcopy(dh, H, T); vcopy(dp, P, T); }
-    else { vjoin(dh, H, T); vjoin(dp, P, T); }
+    if (s_newi) { vcopy<false>(dh, H, T); vcopy<false>(dp, P, T); }
+    else { vjoin<false, true>(dh, H, T); vjoin<false, true>(dp, P, T); }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
