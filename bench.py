@@ -46,36 +46,80 @@ def load_peaks():
 
 WORKLOADS = {
     # C2 (configs[1]): 64 x 256 threads, __syncthreads only, 64K words, ~1 % random words
-    "c2": dict(blocks=64, warps=8, lanes=32, phases=8, records=8, words_per_block=1024, seed=2),
+    "c2": dict(gen="c2", blocks=64, warps=8, lanes=32, phases=8, records=8, words_per_block=1024, seed=2),
+    # C4 (configs[3]): 1024 x 256 threads, ITS-divergent warps (single-lane accesses in random lane order,
+    # random-mask warp barriers every 4 iterations, block barriers every 64), 16M words, 1.0e9 events
+    "c4": dict(gen="c4", blocks=1024, warps=8, lanes=32, iters=3786, words_per_block=16384, seed=4),
     # C5 (configs[4]): the C2 recipe at 1024 x 256 threads, 256M words, 16 phases x 240 records = 1.007e9 events
-    "c5": dict(blocks=1024, warps=8, lanes=32, phases=16, records=240, words_per_block=262144, seed=5),
+    "c5": dict(gen="c2", blocks=1024, warps=8, lanes=32, phases=16, records=240, words_per_block=262144, seed=5),
 }
 
 
+def workload_events(p):
+    from paper_2111_12478_b200 import _native as N
+
+    if p["gen"] == "c4":
+        n = N.c4_events(p["blocks"], p["warps"], p["iters"])
+        n_acc = p["iters"] * p["blocks"] * p["warps"] * 32
+    else:
+        n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
+        n_acc = n - p["phases"] * p["blocks"]
+    return n, n_acc
+
+
 def workload_desc(name, p, n, n_acc):
-    return {"workload": name.upper(), "threads": f"{p['blocks']}x{p['warps']}x{p['lanes']}",
-            "addresses": p["blocks"] * p["words_per_block"], "phases": p["phases"],
-            "records_per_warp_phase": p["records"], "sync": "__syncthreads only",
-            "injected_random_words": "1%", "events": n, "accesses": n_acc}
+    d = {"workload": name.upper(), "threads": f"{p['blocks']}x{p['warps']}x{p['lanes']}",
+         "addresses": p["blocks"] * p["words_per_block"], "events": n, "accesses": n_acc}
+    if p["gen"] == "c4":
+        d.update(iterations=p["iters"], sync="warp barriers (random masks) / 4 it, block barriers / 64 it",
+                 divergence="ITS: ~half the lanes issue single-lane accesses in random order")
+    else:
+        d.update(phases=p["phases"], records_per_warp_phase=p["records"], sync="__syncthreads only",
+                 injected_random_words="1%")
+    return d
 
 
 def make_workload(name: str, rank: int, dev):
-    """Generate the workload trace directly in HBM (device generator; identical
-    to paper_2111_12478_b200.workloads.c2_soa for the same parameters)."""
+    """Generate the workload trace directly in HBM (device generators; identical
+    to paper_2111_12478_b200.workloads.c2_soa / c4_text for the same parameters)."""
     import torch
     from paper_2111_12478_b200 import _native as N
 
     p = dict(WORKLOADS[name])
     p["seed"] += rank
-    n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
+    n, n_acc = workload_events(p)
     key_d = torch.empty(n, dtype=torch.int64, device=dev)
     to_d = torch.empty(n, dtype=torch.int32, device=dev)
     in_d = torch.empty(n, dtype=torch.int32, device=dev)
-    N.gen_c2_device(key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), **p)
+    gp = {k: v for k, v in p.items() if k != "gen"}
+    if p["gen"] == "c4":
+        del gp["lanes"]
+        N.gen_c4_device(key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), **gp)
+    else:
+        N.gen_c2_device(key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), **gp)
     torch.cuda.synchronize(dev)
     cfg = (p["blocks"], p["warps"], p["lanes"])
-    n_acc = n - p["phases"] * p["blocks"]
     return cfg, n, n_acc, (key_d, to_d, in_d), workload_desc(name, p, n, n_acc)
+
+
+def host_workload_prefix(p, P):
+    """Record-aligned host prefix of >= min(P, N) events (numpy / text recipe)."""
+    from paper_2111_12478_b200 import workloads as WL
+    from paper_2111_12478_b200.trace import Trace, parse_trace
+
+    gp = {k: v for k, v in p.items() if k != "gen"}
+    if p["gen"] != "c4":
+        return WL.c2_soa_prefix(P, **gp)
+    per_it = p["blocks"] * p["warps"] * 33
+    its = min(p["iters"], max(1, -(-P // per_it)))
+    gp["iters"] = its
+    tr = parse_trace(WL.c4_text(**gp))
+    from paper_2111_12478_b200 import _native as N
+
+    m = min(P, len(tr))
+    while m < len(tr) and tr.tidop[m] & N.F_CONT:
+        m += 1
+    return Trace(tr.config, tr.key[:m], tr.tidop[:m], tr.instr[:m])
 
 
 def host_prefix(cfg, dev_bufs, P):
@@ -191,15 +235,14 @@ def run_reference(args):
     if rank != 0:
         return
     p = WORKLOADS[args.workload]
-    n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
-    n_acc = n - p["phases"] * p["blocks"]
+    n, n_acc = workload_events(p)
     desc = workload_desc(args.workload, p, n, n_acc)
     cache = {}
 
     def get_prefix(P):
         if P not in cache:
             cache.clear()
-            cache[P] = WL.c2_soa_prefix(P, **p)
+            cache[P] = host_workload_prefix(p, P)
         return cache[P]
 
     for _ in range(args.warmup):

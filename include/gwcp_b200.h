@@ -152,6 +152,10 @@ uint32_t gw_ctx_launches(gw_ctx* c);
 int gw_gen_c2_device(uint32_t blocks, uint32_t warps, uint32_t lanes, uint32_t phases, uint32_t records,
                      uint64_t words_per_block, uint64_t seed, uint64_t* key, uint32_t* tidop, uint32_t* instr,
                      void* stream);
+/* C4 (ITS divergence, lanes = 32): iters*(B*W*32) accesses + B*W*(iters/4) warp
+ * barriers + B*(iters/64) block barriers */
+int gw_gen_c4_device(uint32_t blocks, uint32_t warps, uint32_t iters, uint64_t words_per_block, uint64_t seed,
+                     uint64_t* key, uint32_t* tidop, uint32_t* instr, void* stream);
 
 #ifdef __cplusplus
 }

@@ -113,6 +113,7 @@ EXPORTS = (
     "gw_ctx_stats",
     "gw_ctx_launches",
     "gw_gen_c2_device",
+    "gw_gen_c4_device",
 )
 
 _lib = None
@@ -167,6 +168,9 @@ def lib():
         L.gw_gen_c2_device.argtypes = [C.c_uint32] * 5 + [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                                                           C.c_void_p, C.c_void_p]
         L.gw_gen_c2_device.restype = C.c_int
+        L.gw_gen_c4_device.argtypes = [C.c_uint32] * 3 + [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                                          C.c_void_p, C.c_void_p]
+        L.gw_gen_c4_device.restype = C.c_int
         _lib = L
         return L
 
@@ -326,3 +330,14 @@ def gen_c2_device(key_ptr, tidop_ptr, instr_ptr, *, blocks, warps, lanes, phases
     _check(lib().gw_gen_c2_device(blocks, warps, lanes, phases, records, words_per_block, seed, key_ptr, tidop_ptr,
                                   instr_ptr, stream))
     return phases * (records * blocks * warps * lanes + blocks)
+
+
+def c4_events(blocks, warps, iters) -> int:
+    g = blocks * warps
+    return iters * g * 32 + (iters // 4) * g + (iters // 64) * blocks
+
+
+def gen_c4_device(key_ptr, tidop_ptr, instr_ptr, *, blocks, warps, iters, words_per_block, seed, stream=None) -> int:
+    """Write the C4 recipe trace (workloads.c4_text, lanes=32) into device buffers."""
+    _check(lib().gw_gen_c4_device(blocks, warps, iters, words_per_block, seed, key_ptr, tidop_ptr, instr_ptr, stream))
+    return c4_events(blocks, warps, iters)

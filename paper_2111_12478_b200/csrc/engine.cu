@@ -954,3 +954,15 @@ extern "C" int gw_gen_c2_device(uint32_t blocks, uint32_t warps, uint32_t lanes,
     CK(cudaGetLastError());
   });
 }
+
+extern "C" int gw_gen_c4_device(uint32_t blocks, uint32_t warps, uint32_t iters, uint64_t words_per_block,
+                                uint64_t seed, uint64_t* key, uint32_t* tidop, uint32_t* instr, void* stream) {
+  return guarded([&] {
+    C4Params p{blocks, warps, 32u, iters, words_per_block, seed};
+    const uint64_t groups = (uint64_t)blocks * warps * iters;
+    const uint64_t g = groups * 32ull;
+    GW_LAUNCH(k_gen_c4, (unsigned)std::min<uint64_t>((g + kThreads - 1) / kThreads, 148ull * 64), kThreads, 0,
+              (cudaStream_t)stream, p, (unsigned long long*)key, tidop, instr);
+    CK(cudaGetLastError());
+  });
+}

@@ -24,7 +24,7 @@ struct C2Params {
 __global__ void k_gen_c2(C2Params p, unsigned long long* key, uint32_t* tidop, uint32_t* instr, uint64_t n) {
   const uint64_t acc = (uint64_t)p.R * p.B * p.W * p.L;
   const uint64_t per = acc + p.B;
-  const unsigned long long P01 = 184467440737095516ull;  // int(0.01 * 2**64)
+  const unsigned long long P01 = 184467440737095520ull;  // int(0.01 * 2**64) as Python computes it
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t ph = e / per, o = e % per;
     if (o >= acc) {
@@ -56,6 +56,108 @@ __global__ void k_gen_c2(C2Params p, unsigned long long* key, uint32_t* tidop, u
     key[e] = word * 4ull;
     tidop[e] = ((b * p.W + w) * p.L + l) | ((wr ? GW_K_WRITE : GW_K_READ) << GW_OP_SHIFT) | (l > 0 ? GW_F_CONT : 0u);
     instr[e] = 16u * r + w;
+  }
+}
+
+}  // namespace gw
+
+namespace gw {
+
+__device__ __forceinline__ unsigned long long wl_h2(unsigned long long a, unsigned long long b) {
+  return wl_mix(wl_mix(a) ^ b);
+}
+__device__ __forceinline__ unsigned long long wl_h3(unsigned long long a, unsigned long long b, unsigned long long c) {
+  return wl_mix(wl_h2(a, b) ^ c);
+}
+__device__ __forceinline__ unsigned long long wl_h4(unsigned long long a, unsigned long long b, unsigned long long c,
+                                                    unsigned long long d) {
+  return wl_mix(wl_h3(a, b, c) ^ d);
+}
+
+// C4 (ITS divergence), the recipe of workloads.py:c4_text.  Per iteration `it`,
+// for b, for w: the lanes with bit 63 of h(hh,l,4) set issue single-lane
+// accesses in order of h(hh,l,5), then the other lanes one wacc; every 4th
+// iteration a warp barrier with a random mask; every 64th, block barriers.
+// One warp per (it, b, w) group; its 32 (or 33) events sit at a closed-form
+// offset, so the whole trace is generated in parallel.
+struct C4Params {
+  uint32_t B, W, L, iters;
+  unsigned long long words_per_block, seed;
+};
+
+__device__ __forceinline__ uint64_t c4_iter_base(const C4Params& p, uint64_t it) {
+  // events before iteration it: per iteration B*W*32 accesses, B*W warp barriers
+  // when it%4==3, B block barriers when it%64==63
+  const uint64_t g = (uint64_t)p.B * p.W;
+  const uint64_t nbar_w = (it + 0) / 4;   // iterations j < it with j%4==3
+  const uint64_t nbar_b = (it + 0) / 64;  // iterations j < it with j%64==63
+  return it * g * 32ull + nbar_w * g + nbar_b * p.B;
+}
+
+__global__ void k_gen_c4(C4Params p, unsigned long long* key, uint32_t* tidop, uint32_t* instr) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t g = (uint64_t)p.B * p.W;
+  const uint64_t ngroups = g * p.iters;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  // thresholds exactly as Python computes int(x * 2**64)
+  const unsigned long long T99 = 18262276632972455936ull;
+  const unsigned long long T9999 = 18444899399302180864ull;
+  const unsigned long long T60 = 11068046444225730560ull;
+  for (uint64_t gi = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < ngroups; gi += nwarps) {
+    const uint64_t it = gi / g, bw = gi % g;
+    const uint32_t b = (uint32_t)(bw / p.W), w = (uint32_t)(bw % p.W);
+    const uint64_t base = c4_iter_base(p, it) + bw * (32ull + ((it % 4) == 3 ? 1ull : 0ull));
+    const unsigned long long hh = wl_h4(p.seed, it, b, w);
+    const unsigned long long words = (unsigned long long)p.B * p.words_per_block;
+    const uint32_t l = (uint32_t)lane;
+    // word(l)
+    const unsigned long long x = wl_h3(hh, l, 1ull);
+    const unsigned long long own = (unsigned long long)b * p.words_per_block +
+                                   (((unsigned long long)p.L * p.W * it + (unsigned long long)p.L * w + l) % p.words_per_block);
+    unsigned long long word;
+    if (x < T99) word = own;
+    else if (x < T9999) word = (unsigned long long)b * p.words_per_block + wl_h2(x, 2ull) % p.words_per_block;
+    else word = wl_h2(x, 3ull) % words;
+    const bool single = (wl_h3(hh, l, 4ull) >> 63) & 1ull;
+    const unsigned long long ok = wl_h3(hh, l, 5ull);
+    const bool isw = (hh >> 7) & 1ull;
+    const uint32_t smask = __ballot_sync(0xffffffffu, single);
+    const uint32_t nsingle = __popc(smask);
+    // rank among the single lanes by (order key, lane): every lane runs the shuffles
+    uint32_t r = 0;
+    for (int o = 0; o < 32; o++) {
+      const unsigned long long ko = __shfl_sync(0xffffffffu, ok, o);
+      if (((smask >> o) & 1u) && (ko < ok || (ko == ok && o < lane))) r++;
+    }
+    const uint32_t pos = single ? r : nsingle + __popc(~smask & ((1u << lane) - 1u));
+    const uint64_t e = base + pos;
+    key[e] = 4ull * word;
+    const uint32_t flat = (b * p.W + w) * p.L + l;
+    if (single) {
+      tidop[e] = flat | ((isw ? GW_K_WRITE : GW_K_READ) << GW_OP_SHIFT);
+      instr[e] = 20u + l;
+    } else {
+      const bool cont = pos > nsingle;
+      tidop[e] = flat | ((isw ? GW_K_READ : GW_K_WRITE) << GW_OP_SHIFT) | (cont ? GW_F_CONT : 0u);
+      instr[e] = 19u;
+    }
+    if ((it % 4) == 3 && lane == 0) {
+      uint32_t m = 0;
+      for (uint32_t q = 0; q < 32; q++)
+        if (wl_h3(hh, q, 6ull) < T60) m |= 1u << q;
+      if (m == 0) m = 1;
+      key[base + 32] = 0;
+      tidop[base + 32] = ((b * p.W + w) * p.L) | (GW_K_BARRIER << GW_OP_SHIFT) | GW_F_WARPBAR;
+      instr[base + 32] = m;
+    }
+    if ((it % 64) == 63 && bw == 0) {  // block barriers after all warps of the iteration
+      const uint64_t bb = c4_iter_base(p, it) + g * (32ull + ((it % 4) == 3 ? 1ull : 0ull));
+      for (uint32_t q = lane; q < p.B; q += 32) {
+        key[bb + q] = 0;
+        tidop[bb + q] = (q * p.W * p.L) | (GW_K_BARRIER << GW_OP_SHIFT);
+        instr[bb + q] = 0;
+      }
+    }
   }
 }
 

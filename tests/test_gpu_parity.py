@@ -195,3 +195,22 @@ def test_device_generator_matches_numpy_recipe():
     assert np.array_equal(k.cpu().numpy().view(np.uint64), want.key)
     assert np.array_equal(t.cpu().numpy().view(np.uint32), want.tidop)
     assert np.array_equal(i.cpu().numpy().view(np.uint32), want.instr)
+
+
+@pytest.mark.parametrize("geom", [(3, 2, 9), (4, 8, 70)])
+def test_device_c4_generator_matches_text_recipe(geom):
+    import torch
+
+    B, W, it = geom
+    want = parse_trace(WL.c4_text(blocks=B, warps=W, lanes=32, iters=it, words_per_block=512, seed=41))
+    n = N.c4_events(B, W, it)
+    assert n == len(want)
+    dev = torch.device("cuda", 0)
+    k = torch.empty(n, dtype=torch.int64, device=dev)
+    t = torch.empty(n, dtype=torch.int32, device=dev)
+    i = torch.empty(n, dtype=torch.int32, device=dev)
+    N.gen_c4_device(k.data_ptr(), t.data_ptr(), i.data_ptr(), blocks=B, warps=W, iters=it, words_per_block=512, seed=41)
+    torch.cuda.synchronize()
+    assert np.array_equal(t.cpu().numpy().view(np.uint32), want.tidop)
+    assert np.array_equal(k.cpu().numpy().view(np.uint64), want.key)
+    assert np.array_equal(i.cpu().numpy().view(np.uint32), want.instr)
