@@ -146,7 +146,7 @@ __global__ void k_gen_c4(C4Params p, unsigned long long* key, uint32_t* tidop, u
       for (uint32_t q = 0; q < 32; q++)
         if (wl_h3(hh, q, 6ull) < T60) m |= 1u << q;
       if (m == 0) m = 1;
-      key[base + 32] = 0;
+      key[base + 32] = ((unsigned long long)b << 32) | w;  // as the parser encodes `bar warp b w m`
       tidop[base + 32] = ((b * p.W + w) * p.L) | (GW_K_BARRIER << GW_OP_SHIFT) | GW_F_WARPBAR;
       instr[base + 32] = m;
     }
