@@ -432,6 +432,62 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
   __syncthreads();
 }
 
+// Warp barriers of lock-free traces (<= 32 participants, block-range objects):
+// the same join as do_barrier, done by warp 0 alone with warp reductions
+// (no CTA-wide barrier inside).  Caller: threadIdx.x < 32, then __syncthreads.
+__device__ void do_barrier_warp(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_t* s_acc) {
+  const DevTrace& tr = a.tr;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t base = ev_tid(to);
+  const uint32_t blo = (base / tr.BS) * tr.BS;
+  const uint32_t u = base + lane;
+  const bool part = lane < tr.L && ((ins >> lane) & 1u) && !a.exited[u];
+  if (!__any_sync(0xffffffffu, part)) return;
+  const uint32_t o = part ? a.pobj[u] : NIL;
+  uint32_t mylo = blo, myhi = blo + tr.BS;
+  if (o != NIL) {
+    const uint32_t olo = a.arena[o], olen = a.arena[o + 1];
+    mylo = min(mylo, olo);
+    myhi = max(myhi, olo + olen);
+  }
+  const uint32_t lo = __reduce_min_sync(0xffffffffu, mylo), hi = __reduce_max_sync(0xffffffffu, myhi);
+  const uint32_t span = hi - lo;
+  uint32_t* acc = span <= (uint32_t)kAccSmem ? s_acc : a.scratch + (size_t)blockIdx.x * 3 * tr.T + 2 * tr.T;
+  for (uint32_t i = lane; i < span; i += 32) acc[i] = 0u;
+  __syncwarp();
+  uint32_t done = 0;
+  while (true) {  // each distinct participant object once
+    const uint32_t om = __reduce_min_sync(0xffffffffu, (o != NIL && o >= done) ? o : NIL);
+    if (om == NIL) break;
+    const uint32_t olo = a.arena[om], olen = a.arena[om + 1];
+    const uint32_t* src = a.arena + om + OBJ_HDR;
+    uint32_t* dst = acc + (olo - lo);
+    for (uint32_t i = lane; i < olen; i += 32) {
+      const uint32_t v = src[i];
+      if (v > dst[i]) dst[i] = v;
+    }
+    __syncwarp();
+    done = om + 1;
+  }
+  const uint32_t lu = part ? a.local[u] : 0u;
+  if (part) acc[u - lo] = lu;
+  __syncwarp();
+  uint32_t no = NIL;
+  if (lane == 0) {
+    no = arena_alloc(a, span + OBJ_HDR);
+    if (no != NIL) { a.arena[no] = lo; a.arena[no + 1] = span; }
+  }
+  no = __shfl_sync(0xffffffffu, no, 0);
+  if (no != NIL)
+    for (uint32_t i = lane; i < span; i += 32) a.arena[no + OBJ_HDR + i] = acc[i];
+  if (part) {
+    a.local[u] = lu + 1;
+    a.pobj[u] = no;
+    a.pdiag[u] = lu + 1;
+  }
+  __syncwarp();
+}
+
 // --------------------------------------------------------------- locks ----
 // Per-lock tickets.  A lock-related event e (successful acquire / release of
 // l, or an access inside critical sections of l1..ld) may touch the state of
@@ -880,7 +936,12 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
         const uint32_t e = s_e[h], to = s_to[h];
         const uint32_t kd = ev_kind(to);
         if (kd == GW_K_BARRIER) {
-          do_barrier(a, to, tr.instr[e], s_acc);
+          if ((to & GW_F_WARPBAR) && !a.has_locks && tr.L <= 32) {
+            if (threadIdx.x < 32) do_barrier_warp(a, to, tr.instr[e], s_acc);
+            __syncthreads();
+          } else {
+            do_barrier(a, to, tr.instr[e], s_acc);
+          }
         } else if (kd == GW_K_END) {
           if (threadIdx.x == 0) {
             const uint32_t t = ev_tid(to);
@@ -943,7 +1004,12 @@ __global__ void __launch_bounds__(kThreads) k_walker_snap(WalkArgs a, SnapArgs s
       const uint32_t to = tr.tidop[e];
       __syncthreads();
       if (ev_kind(to) == GW_K_BARRIER) {
-        do_barrier(a, to, tr.instr[e], s_acc);
+        if ((to & GW_F_WARPBAR) && tr.L <= 32) {
+          if (threadIdx.x < 32) do_barrier_warp(a, to, tr.instr[e], s_acc);
+          __syncthreads();
+        } else {
+          do_barrier(a, to, tr.instr[e], s_acc);
+        }
       } else {  // END (lock-free: no frames)
         if (threadIdx.x == 0) {
           const uint32_t t = ev_tid(to);
