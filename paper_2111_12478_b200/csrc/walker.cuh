@@ -462,9 +462,18 @@ __device__ void do_barrier_warp(const WalkArgs& a, uint32_t to, uint32_t ins, ui
     const uint32_t olo = a.arena[om], olen = a.arena[om + 1];
     const uint32_t* src = a.arena + om + OBJ_HDR;
     uint32_t* dst = acc + (olo - lo);
-    for (uint32_t i = lane; i < olen; i += 32) {
-      const uint32_t v = src[i];
-      if (v > dst[i]) dst[i] = v;
+    for (uint32_t i0 = 0; i0 < olen; i0 += 32 * 8) {  // 8 independent loads in flight per lane
+      uint32_t v[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const uint32_t i = i0 + lane + 32 * k;
+        v[k] = i < olen ? src[i] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const uint32_t i = i0 + lane + 32 * k;
+        if (i < olen && v[k] > dst[i]) dst[i] = v[k];
+      }
     }
     __syncwarp();
     done = om + 1;
