@@ -157,6 +157,12 @@ int gw_gen_c2_device(uint32_t blocks, uint32_t warps, uint32_t lanes, uint32_t p
 int gw_gen_c4_device(uint32_t blocks, uint32_t warps, uint32_t iters, uint64_t words_per_block, uint64_t seed,
                      uint64_t* key, uint32_t* tidop, uint32_t* instr, void* stream);
 
+/* C3 (spin locks, lanes <= 32): group_offsets[g] (device, u64) = first event of
+ * group g = (it*B + b)*W + w, from workloads.c3_group_offsets */
+int gw_gen_c3_device(uint32_t blocks, uint32_t warps, uint32_t lanes, uint32_t iters, uint32_t locks,
+                     uint32_t region, uint32_t priv, uint64_t seed, const uint64_t* group_offsets, uint64_t* key,
+                     uint32_t* tidop, uint32_t* instr, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

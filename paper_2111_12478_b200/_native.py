@@ -114,6 +114,7 @@ EXPORTS = (
     "gw_ctx_launches",
     "gw_gen_c2_device",
     "gw_gen_c4_device",
+    "gw_gen_c3_device",
 )
 
 _lib = None
@@ -171,6 +172,8 @@ def lib():
         L.gw_gen_c4_device.argtypes = [C.c_uint32] * 3 + [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                                                           C.c_void_p, C.c_void_p]
         L.gw_gen_c4_device.restype = C.c_int
+        L.gw_gen_c3_device.argtypes = [C.c_uint32] * 7 + [C.c_uint64] + [C.c_void_p] * 5
+        L.gw_gen_c3_device.restype = C.c_int
         _lib = L
         return L
 
@@ -341,3 +344,11 @@ def gen_c4_device(key_ptr, tidop_ptr, instr_ptr, *, blocks, warps, iters, words_
     """Write the C4 recipe trace (workloads.c4_text, lanes=32) into device buffers."""
     _check(lib().gw_gen_c4_device(blocks, warps, iters, words_per_block, seed, key_ptr, tidop_ptr, instr_ptr, stream))
     return c4_events(blocks, warps, iters)
+
+
+def gen_c3_device(key_ptr, tidop_ptr, instr_ptr, offsets_ptr, *, blocks, warps, lanes, iters, locks, region,
+                  private, seed, stream=None) -> None:
+    """Write the C3 recipe trace (workloads.c3_text) into device buffers, given
+    the device copy of workloads.c3_group_offsets(...)[:-1]."""
+    _check(lib().gw_gen_c3_device(blocks, warps, lanes, iters, locks, region, private, seed, offsets_ptr, key_ptr,
+                                  tidop_ptr, instr_ptr, stream))

@@ -197,7 +197,11 @@ struct CheckArgs {
   uint32_t* large_ws;
   uint32_t* n_large;
   uint32_t large_cap;
+  int defer;  // lock mode: emit every structural candidate; the walker answers pred_t[u] later
 };
+__device__ __forceinline__ bool clock_says_race(const CheckArgs& a, uint32_t prior_ev, uint32_t vo, uint32_t u) {
+  return a.defer || a.time[prior_ev] > obj_get(a.arena, vo, u);
+}
 
 __global__ void __launch_bounds__(kThreads) k_check(CheckArgs a) {
   const uint32_t BS = a.tr.BS;
@@ -212,13 +216,13 @@ __global__ void __launch_bounds__(kThreads) k_check(CheckArgs a) {
     const uint32_t lw = i > 0 ? a.lastw[i - 1] : 0u;
     const bool hasw = lw > 0 && lw - 1 >= ss && lw - 1 < i;
     const uint32_t W = hasw ? lw - 1 : NIL;
-    const uint32_t vo = a.vobj[c];
+    const uint32_t vo = a.defer ? NIL : a.vobj[c];
     unsigned long long loc = 0;
     if (hasw) {
       const uint32_t p = a.vals[W];
       const uint32_t top = a.sto[W];
       const uint32_t u = ev_tid(top);
-      if (u != tc && !cover(top, toc, BS) && a.time[p] > obj_get(a.arena, vo, u)) {
+      if (u != tc && !cover(top, toc, BS) && clock_says_race(a, p, vo, u)) {
         loc = a.tr.key[c];
         emit_cand(a.c, ((unsigned long long)c << 32) | SUB_WCHECK, loc, p, c, isw ? GW_WW : GW_WR);
       }
@@ -250,12 +254,43 @@ __global__ void __launch_bounds__(kThreads) k_check(CheckArgs a) {
           if (ev_kind(t3) <= GW_K_WRITE && ev_tid(t3) == uq) { first = q3; break; }
         }
         const uint32_t r = a.vals[q];
-        if (!cover(toq, toc, BS) && a.time[r] > obj_get(a.arena, vo, uq)) {
+        if (!cover(toq, toc, BS) && clock_says_race(a, r, vo, uq)) {
           if (!loc) loc = a.tr.key[c];
           emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), a.tr.key[c], r, c, GW_RW);
         }
       }
     }
+  }
+}
+
+// ---- lock mode: deferred clock checks -------------------------------------
+// Q = threads whose clock entry is ever read: prior-access threads of the
+// structural candidates and record owners (successful acquires).  Also flags
+// the current events that carry queries and lays out the (cur, candidate)
+// pairs for the sort that orders the queries by event.
+__global__ void k_q_mark_cands(Cands c, const uint32_t* tidop, uint32_t* qflag, uint8_t* lflags, uint32_t* qk,
+                               uint32_t* qvals) {
+  const uint32_t n = min(*c.n, c.cap);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const uint32_t cur = c.cur[k];
+    qflag[ev_tid(tidop[c.prior[k]])] = 1u;
+    lflags[cur] = lflags[cur] | LF_QUERY;  // every writer stores the same value
+    qk[k] = cur;
+    qvals[k] = k;
+  }
+}
+__global__ void k_q_mark_acq(DevTrace tr, const uint8_t* lflags, uint32_t* qflag) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t to = tr.tidop[e];
+    if (ev_kind(to) == GW_K_ACQUIRE && (lflags[e] & LF_OK)) qflag[ev_tid(to)] = 1u;
+  }
+}
+// the clock half of the checks (gwcp.py:256, :265): race iff prior.time > pred_t[u]
+__global__ void k_resolve(Cands in, const uint32_t* qv, const uint32_t* time, Cands out) {
+  const uint32_t n = min(*in.n, in.cap);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const uint32_t p = in.prior[k];
+    if (time[p] > qv[k]) emit_cand(out, in.okey[k], in.loc[k], p, in.cur[k], in.kind[k]);
   }
 }
 
@@ -289,7 +324,7 @@ __global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const
     const uint32_t toq = a.sto[q], uq = ev_tid(toq);
     if (uq == ev_tid(toc)) continue;
     const uint32_t r = a.vals[q];
-    if (!cover(toq, toc, BS) && a.time[r] > obj_get(a.arena, a.vobj[c], uq))
+    if (!cover(toq, toc, BS) && clock_says_race(a, r, a.defer ? NIL : a.vobj[c], uq))
       emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), a.tr.key[c], r, c, GW_RW);
   }
 }

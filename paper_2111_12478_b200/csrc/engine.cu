@@ -87,7 +87,10 @@ struct gw_ctx {
     size_t cap = 0;
   };
   std::map<std::string, Buf> bufs;
-  cudaEvent_t ev[8] = {};
+  // ev[0] / ev[1]: whole analysis; ev[2 + 2*(2*phase + k) + {0,1}]: interval k of a phase
+  static constexpr int kEv = 22;
+  cudaEvent_t ev[kEv] = {};
+  int nint[5] = {0, 0, 0, 0, 0};
   // last results (device)
   uint64_t n_reports = 0, n_diags = 0, n_events = 0;
   uint8_t* d_kind = nullptr;
@@ -120,7 +123,10 @@ struct gw_ctx {
       b.cap = 0;
       size_t nb = bytes + bytes / 8;
       CK(cudaMalloc(&b.p, nb));
-      CK(cudaMemset(b.p, 0, nb));  // look-back flags must never alias a live epoch
+      // zeroed on the analysis stream (look-back flags must never alias a live
+      // epoch): a legacy-stream memset would not be ordered before kernels on
+      // a non-blocking stream
+      CK(cudaMemsetAsync(b.p, 0, nb, last_stream));
       b.cap = nb;
     }
     return (T*)b.p;
@@ -132,15 +138,19 @@ struct gw_ctx {
   void finish_stats() {
     if (!stats_pending) return;
     stats_pending = false;
-    CK(cudaEventSynchronize(ev[5]));
+    CK(cudaEventSynchronize(ev[1]));
     float ms;
-    CK(cudaEventElapsedTime(&ms, ev[0], ev[5])); stats.ms_total = ms;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); stats.ms_total = ms;
     if (phases) {
-      CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); stats.ms_prep = ms;
-      CK(cudaEventElapsedTime(&ms, ev[1], ev[2])); stats.ms_walker = ms;
-      CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); stats.ms_sort = ms;
-      CK(cudaEventElapsedTime(&ms, ev[3], ev[4])); stats.ms_check = ms;
-      CK(cudaEventElapsedTime(&ms, ev[4], ev[5])); stats.ms_final = ms;
+      float* dst[5] = {&stats.ms_prep, &stats.ms_walker, &stats.ms_sort, &stats.ms_check, &stats.ms_final};
+      for (int p = 0; p < 5; p++) {
+        *dst[p] = 0.f;
+        for (int k = 0; k < nint[p]; k++) {
+          const int i = 2 + 2 * (2 * p + k);
+          CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+          *dst[p] += ms;
+        }
+      }
     }
   }
 };
@@ -149,7 +159,7 @@ namespace {
 
 // scalar slots of the "scalars" buffer
 enum : int { SC_MAXD = 0, SC_NINCS, SC_TICKET, SC_REC, SC_LOG, SC_DIAG, SC_ERR, SC_ABORT, SC_NCAND, SC_NLARGE,
-             SC_NSURV, SC_COUNT = 16 };
+             SC_NSURV, SC_NQ, SC_NQLARGE, SC_COUNT = 16 };
 
 __global__ void k_init_stats(Stats* s) {
   memset(s, 0, sizeof(Stats));
@@ -180,8 +190,16 @@ struct Pipeline {
     CK(cudaStreamSynchronize(st));
   }
   void check_launch() { CK(cudaGetLastError()); }
+  enum { PH_PREP = 0, PH_WALKER, PH_SORT, PH_CHECK, PH_FINAL };
   void event(int i) {
     if (!gmode) CK(cudaEventRecord(C->ev[i], st));
+  }
+  void pbeg(int p) {
+    if (!gmode && C->nint[p] < 2) CK(cudaEventRecord(C->ev[2 + 2 * (2 * p + C->nint[p])], st));
+  }
+  void pend(int p) {
+    if (!gmode && C->nint[p] < 2) CK(cudaEventRecord(C->ev[2 + 2 * (2 * p + C->nint[p]) + 1], st));
+    C->nint[p]++;
   }
 
   // per-analysis zeroed block: look-back tile counters + radix histograms
@@ -293,8 +311,9 @@ struct Pipeline {
     C->n_reports = 0;
     C->n_diags = 0;
     g_launches = 0;
-    for (int i = 0; i < 8; i++)
+    for (int i = 0; i < gw_ctx::kEv; i++)
       if (!C->ev[i]) CK(cudaEventCreate(&C->ev[i]));
+    for (int p = 0; p < 5; p++) C->nint[p] = 0;
     event(0);
     C->d_scal = nullptr;
     C->d_nsurv = nullptr;
@@ -307,9 +326,10 @@ struct Pipeline {
       return;
     }
     // ---------------------------------------------------------------- prep
+    pbeg(PH_PREP);
     zero_blk = C->get<uint32_t>("zero_blk", kZeroWords);
     zero_next = 0;
-    uint32_t* scal = C->get<uint32_t>("scalars", SC_COUNT);
+    scal = C->get<uint32_t>("scalars", SC_COUNT);
     CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
     CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
     if (gmode) {  // fixed epochs in the graph: start from clean flags
@@ -322,7 +342,6 @@ struct Pipeline {
     GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
     GW_LAUNCH(k_prep, grid_for(N), kThreads, 0, st, tr, dst);
     check_launch();
-    Stats hs;
     if (gmode) {
       memset(&hs, 0, sizeof hs);
       hs.n_bar = P->n_bar;
@@ -334,307 +353,72 @@ struct Pipeline {
       d2h(&hs, dst);
       obs = hs;
     }
-    const bool has_locks = hs.n_acq + hs.n_rel > 0;
+    has_locks = hs.n_acq + hs.n_rel > 0;
     S.n_accesses = hs.n_acc;
-    event(1);
 
     // ----------------------------------------------------------- partition
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walker, kThreads, 0));
-    uint64_t gmax = (uint64_t)std::max(occ, 1) * C->num_sms;
-    const uint32_t G = (uint32_t)std::min<uint64_t>(tr.B, gmax);
+    gmax = (uint64_t)std::max(occ, 1) * C->num_sms;
+    G = (uint32_t)std::min<uint64_t>(tr.B, gmax);
     S.walker_ctas = G;
     // snapshot mode: lock-free and the per-hard-event block snapshots are small
-    const uint64_t n_hard = hs.n_bar + hs.n_end;
-    const uint64_t snap_entries = (n_hard + tr.B) * (uint64_t)tr.BS;
-    const bool snap_mode = !has_locks && snap_entries * 8 <= std::max<uint64_t>(256ull << 20, 8 * N);
+    n_hard = hs.n_bar + hs.n_end;
+    snap_entries = (n_hard + tr.B) * (uint64_t)tr.BS;
+    snap_mode = !has_locks && snap_entries * 8 <= std::max<uint64_t>(256ull << 20, 8 * N);
     obs_snap = snap_mode;
-    uint32_t* part_key = nullptr;
-    uint32_t* perm = nullptr;
-    if (G > 1 && !snap_mode) {
-      part_key = C->get<uint32_t>("part_k", N);
-      perm = C->get<uint32_t>("part_v", N);
-      GW_LAUNCH(k_part_keys, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
-      sort<uint32_t>(part_key, perm, N, ceil_log2(G), "part");
-    }
-
-    // ------------------------------------------------------- lock pre-pass
-    WalkArgs w;
     memset(&w, 0, sizeof w);
     w.tr = tr;
     w.G = G;
-    w.part_key = part_key;
-    w.perm = perm;
     w.has_locks = has_locks ? 1 : 0;
     w.inactive_opt = inactive_opt;
     w.abort_flag = scal + SC_ABORT;
-    uint32_t maxd = 1, n_incs = 0;
-    uint64_t lcap = 1;
-    if (has_locks) {
-      const uint64_t nle = hs.n_acq + hs.n_rel + hs.n_end;
-      uint32_t* flag = C->get<uint32_t>("lk_flag", N);
-      GW_LAUNCH(k_lock_mark, grid_for(N), kThreads, 0, st, tr, flag);
-      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{flag}, N, OpSum(), 0u, false, "sc_u32");
-      uint32_t* ktid = C->get<uint32_t>("lk_tid", nle);
-      uint32_t* kev = C->get<uint32_t>("lk_ev", nle);
-      GW_LAUNCH(k_lock_compact, grid_for(N), kThreads, 0, st, tr, flag, ktid, kev);
-      sort<uint32_t>(ktid, kev, nle, ceil_log2(tr.T), "lk");
-      uint32_t* seg_beg = C->get<uint32_t>("lk_sb", tr.T);
-      uint32_t* seg_end = C->get<uint32_t>("lk_se", tr.T);
-      CK(cudaMemsetAsync(seg_beg, 0, sizeof(uint32_t) * tr.T, st));
-      CK(cudaMemsetAsync(seg_end, 0, sizeof(uint32_t) * tr.T, st));
-      GW_LAUNCH(k_lock_segs, grid_for(nle), kThreads, 0, st, ktid, (uint32_t)nle, seg_beg, seg_end);
-      unsigned long long* node_lock = C->get<unsigned long long>("lk_nlock", nle);
-      uint32_t* node_parent = C->get<uint32_t>("lk_nparent", nle);
-      uint32_t* top_after = C->get<uint32_t>("lk_top", nle);
-      uint8_t* lflags = C->get<uint8_t>("lflags", N);
-      CK(cudaMemsetAsync(lflags, 0, N, st));
-      GW_LAUNCH(k_lock_automaton, grid_for(nle), kThreads, 0, st, tr, ktid, kev, (uint32_t)nle, seg_end, node_lock,
-                node_parent, top_after, lflags, scal + SC_MAXD);
-      uint32_t* etop = C->get<uint32_t>("lk_etop", N);
-      uint32_t* npair = C->get<uint32_t>("lk_npair", N);
-      GW_LAUNCH(k_lock_access, grid_for(N), kThreads, 0, st, tr, kev, top_after, seg_beg, seg_end, node_parent,
-                lflags, etop, npair, scal + SC_NINCS);
-      uint32_t* poff = C->get<uint32_t>("lk_poff", N);
-      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{npair}, ArrStore<uint32_t>{poff}, N, OpSum(), 0u, false, "sc_u32");
-      uint32_t hv[4];
-      CK(cudaMemcpyAsync(hv, poff + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(hv + 1, npair + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(hv + 2, scal, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      const uint64_t P = (uint64_t)hv[0] + hv[1];
-      maxd = std::max<uint32_t>(hv[2], 1);
-      n_incs = hv[3];
-      unsigned long long* plock = C->get<unsigned long long>("lk_plock", P + 1);
-      unsigned long long* pk = C->get<unsigned long long>("lk_pk", P + 1);
-      uint32_t* pv = C->get<uint32_t>("lk_pv", P + 1);
-      unsigned long long* orand = C->get<unsigned long long>("lk_orand", 2);
-      GW_LAUNCH(k_orand_init, 1, 1, 0, st, orand);
-      GW_LAUNCH(k_lock_pairs, grid_for(N), kThreads, 0, st, tr, poff, npair, etop, node_lock, node_parent, plock, pv,
-                orand);
-      unsigned long long ho[2];
-      d2h(ho, orand, 2);
-      KeyRuns lkr = key_runs(P ? ho[0] ^ ho[1] : 0ull);
-      lkr.sentinel = 0;
-      lkr.nbits = 0;
-      for (int i = 0; i < lkr.n; i++) lkr.nbits += lkr.width[i];
-      GW_LAUNCH(k_compact_u64, grid_for(P + 1), kThreads, 0, st, plock, P, lkr, pk);
-      sort<unsigned long long>(pk, pv, P, lkr.nbits, "lkp");
-      uint32_t* segstart = C->get<uint32_t>("lk_pseg", P + 1);
-      scan<uint32_t, OpMaxU32>(LockSegLoad{pk}, ArrStore<uint32_t>{segstart}, P, OpMaxU32(), 0u, true, "sc_u32");
-      uint32_t* prank = C->get<uint32_t>("lk_prank", P + 1);
-      // lock table (created here, one entry + ticket per lock) before the ranks kernel inserts into it
-      lcap = pow2_at_least(2 * (hs.n_acq + hs.n_rel) + 2);
-      w.locks = C->get<LockEnt>("t_lock", lcap);
-      w.lock_mask = (uint32_t)(lcap - 1);
-      w.err = scal + SC_ERR;
-      CK(cudaMemsetAsync(w.locks, 0, sizeof(LockEnt) * lcap, st));
-      w.plock = plock;
-      GW_LAUNCH(k_lock_ranks, grid_for(P + 1), kThreads, 0, st, w, pk, pv, segstart, P, prank);
-      check_launch();
-      w.lflags = lflags;
-      w.poff = poff;
-      w.npair = npair;
-      w.prank = prank;
-    }
-
-    // ------------------------------------------------------ walker buffers
-    const uint32_t T = tr.T;
-    uint64_t arena_words;
-    if (!has_locks) {
-      arena_words = hs.n_bar * (uint64_t)(tr.BS + OBJ_HDR + 3) + 64;
-    } else {
-      uint64_t nobj = 2 * hs.n_bar + 2 * hs.n_acq + 4 * hs.n_rel + (uint64_t)n_incs * (1 + maxd) + 4;
-      arena_words = nobj * (uint64_t)(T + OBJ_HDR + 3) + 64;
-      size_t free_b = 0, total_b = 0;
-      CK(cudaMemGetInfo(&free_b, &total_b));
-      uint64_t cap_words = (uint64_t)(free_b * 0.6) / 4;
-      cap_words = std::min<uint64_t>(cap_words, 0xFFFFFFF0ull);
-      arena_words = std::min(arena_words, cap_words);
-    }
-    S.arena_words = arena_words;
-    w.arena = C->get<uint32_t>("arena", arena_words);
-    w.arena_cap = arena_words;
-    w.arena_top = C->get<unsigned long long>("arena_top", 1);
-    CK(cudaMemsetAsync(w.arena_top, 0, sizeof(unsigned long long), st));
-    w.time = C->get<uint32_t>("time", N);
-    w.vobj = C->get<uint32_t>("vobj", N);
-    w.local = C->get<uint32_t>("st_local", T);
-    w.pobj = C->get<uint32_t>("st_pobj", T);
-    w.pdiag = C->get<uint32_t>("st_pdiag", T);
-    w.nend = C->get<uint32_t>("st_nend", T);
-    w.exited = C->get<uint32_t>("st_exited", T);
-    w.rec_top = scal + SC_REC;
-    w.log_top = scal + SC_LOG;
-    w.diag_top = scal + SC_DIAG;
     w.err = scal + SC_ERR;
-    w.maxd = maxd;
-    uint64_t diag_cap = hs.n_acq + hs.n_rel + hs.n_end * (uint64_t)maxd + 16;
-    w.diags = C->get<Diag>("diags", diag_cap);
-    w.diag_cap = (uint32_t)diag_cap;
-    if (has_locks) {
-      w.hobj = C->get<uint32_t>("st_hobj", T);
-      w.depth = C->get<uint32_t>("st_depth", T);
-      w.loghead = C->get<uint32_t>("st_loghead", T);
-      w.frames = C->get<Frame>("frames", (uint64_t)T * maxd);
-      uint64_t icap = pow2_at_least(2 * hs.n_rel + 2);
-      uint64_t ccap = pow2_at_least(2 * (uint64_t)n_incs * maxd + 2);
-      w.curs = C->get<CurEnt>("t_cur", lcap);
-      w.cur_mask = (uint32_t)(lcap - 1);
-      w.insts = C->get<InstEnt>("t_inst", icap);
-      w.inst_mask = (uint32_t)(icap - 1);
-      w.cs = C->get<CsEnt>("t_cs", ccap);
-      w.cs_mask = (uint32_t)(ccap - 1);
-      CK(cudaMemsetAsync(w.curs, 0, sizeof(CurEnt) * lcap, st));
-      CK(cudaMemsetAsync(w.insts, 0, sizeof(InstEnt) * icap, st));
-      CK(cudaMemsetAsync(w.cs, 0, sizeof(CsEnt) * ccap, st));
-      w.recs = C->get<Rec>("recs", hs.n_acq + 1);
-      w.rec_cap = (uint32_t)(hs.n_acq + 1);
-      w.logs = C->get<LogEnt>("logs", (uint64_t)n_incs + 1);
-      w.log_cap = n_incs + 1;
+    if (G > 1 && !snap_mode) {
+      uint32_t* part_key = C->get<uint32_t>("part_k", N);
+      uint32_t* perm = C->get<uint32_t>("part_v", N);
+      GW_LAUNCH(k_part_keys, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
+      sort<uint32_t>(part_key, perm, N, ceil_log2(G), "part");
+      w.part_key = part_key;
+      w.perm = perm;
     }
-    if (has_locks || tr.BS > (uint32_t)kAccSmem) w.scratch = C->get<uint32_t>("scratch", (uint64_t)G * 3 * T);
-    GW_LAUNCH(k_state_init, grid_for(T), kThreads, 0, st, w);
-    if (snap_mode) {
-      SnapArgs sa;
-      uint32_t* hflag = C->get<uint32_t>("hd_flag", N);
-      GW_LAUNCH(k_hard_mark, grid_for(N), kThreads, 0, st, tr, hflag);
-      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hflag}, ArrStore<uint32_t>{hflag}, N, OpSum(), 0u, false, "sc_u32");
-      uint32_t* hkey = C->get<uint32_t>("hd_key", n_hard + 1);
-      uint32_t* hev = C->get<uint32_t>("hd_ev", n_hard + 1);
-      uint32_t* hbeg = C->get<uint32_t>("hd_beg", tr.B);
-      uint32_t* hend = C->get<uint32_t>("hd_end", tr.B);
-      uint32_t* hcnt = C->get<uint32_t>("hd_cnt", tr.B);
-      CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
-      if (n_hard) {
-        GW_LAUNCH(k_hard_compact, grid_for(N), kThreads, 0, st, tr, hflag, hkey, hev, hcnt);
-        sort<uint32_t>(hkey, hev, n_hard, ceil_log2(tr.B), "hd");
-      }
-      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hcnt}, HardSegStore{hcnt, hbeg, hend}, tr.B, OpSum(), 0u, false,
-                            "sc_u32");
-      sa.hard_ev = hev;
-      sa.hb_beg = hbeg;
-      sa.hb_end = hend;
-      sa.snap = C->get<uint2>("snap", snap_entries);
-      GW_LAUNCH(k_walker_snap, std::min<uint32_t>(tr.B, (uint32_t)gmax), kThreads, 0, st, w, sa);
-      GW_LAUNCH(k_stamp, grid_for(N), kThreads, 0, st, w, sa);
-      S.walker_ctas = std::min<uint32_t>(tr.B, (uint32_t)gmax);
-    } else {
-      GW_LAUNCH(k_walker, G, kThreads, 0, st, w);
-    }
-    check_launch();
-    event(2);
+    if (has_locks) lock_prepass();
+    pend(PH_PREP);
 
-    // ---------------------------------------------------------- access pass
-    // All N positions are sorted; non-access events carry the top sentinel key
-    // and sort last, and every access-pass kernel skips them, so no kernel
-    // needs the access count on the host.
-    uint32_t* out_n = scal + SC_NCAND;  // [NCAND], [NLARGE], [NSURV]
-    const uint64_t NA = N;
-    // varying location-key bits (none when the trace has no access at all)
-    const KeyRuns kr = key_runs(gmode ? P->D : (hs.n_acc ? hs.key_or ^ hs.key_and : 0ull));
-    S.sort_bits = kr.nbits;
-    const bool wide = kr.nbits > 32;
-    obs_D = hs.n_acc ? hs.key_or ^ hs.key_and : 0ull;
-    uint32_t* vals = C->get<uint32_t>("acc_v", N);
-    void* skeys = nullptr;
-    if (!wide) {
-      uint32_t* k32 = C->get<uint32_t>("acc_k", N);
-      GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals);
-      sort<uint32_t>(k32, vals, N, kr.nbits, "acc");
-      skeys = k32;
-    } else {
-      unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
-      GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals);
-      sort<unsigned long long>(k64, vals, N, kr.nbits, "acc");
-      skeys = k64;
-    }
-    event(3);
-    uint32_t* sto = C->get<uint32_t>("acc_to", NA);
-    GW_LAUNCH(k_gather_to, grid_for(NA), kThreads, 0, st, vals, tr.tidop, NA, sto);
-    uint32_t* segst = C->get<uint32_t>("acc_segst", NA);
-    uint32_t* lastw = C->get<uint32_t>("acc_lastw", NA);
-    if (!wide)
-      scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, NA, OpMax2(),
-                          make_uint2(0, 0), true, "sc_u2");
-    else
-      scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
-                          SegStore{segst, lastw}, NA, OpMax2(), make_uint2(0, 0), true, "sc_u2");
-    uint32_t* large_i = C->get<uint32_t>("lg_i", NA / kSmallWin + 1);
-    uint32_t* large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);
-    uint64_t cand_cap = gmode ? P->cand_cap : std::max<uint64_t>(65536, NA / 4);
     Cands cd;
-    CheckArgs ca;
-    uint32_t hcnt[2] = {0, 0};
-    for (int attempt = 0; attempt < 2; attempt++) {
-      cd.okey = C->get<unsigned long long>("c_okey", cand_cap);
-      cd.loc = C->get<unsigned long long>("c_loc", cand_cap);
-      cd.prior = C->get<uint32_t>("c_prior", cand_cap);
-      cd.cur = C->get<uint32_t>("c_cur", cand_cap);
-      cd.kind = C->get<uint32_t>("c_kind", cand_cap);
-      cd.n = out_n;
-      cd.cap = (uint32_t)std::min<uint64_t>(cand_cap, 0xFFFFFFF0ull);
-      cd.err = w.err;
-      CK(cudaMemsetAsync(out_n, 0, 3 * sizeof(uint32_t), st));
-      ca.tr = tr;
-      ca.vals = vals;
-      ca.sto = sto;
-      ca.segst = segst;
-      ca.lastw = lastw;
-      ca.time = w.time;
-      ca.vobj = w.vobj;
-      ca.arena = w.arena;
-      ca.n_acc = NA;
-      ca.c = cd;
-      ca.large_i = large_i;
-      ca.large_ws = large_ws;
-      ca.n_large = out_n + 1;
-      ca.large_cap = (uint32_t)(NA / kSmallWin + 1);
-      GW_LAUNCH(k_check, grid_for(NA), kThreads, 0, st, ca);
-      GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd);
-      check_launch();
-      if (gmode) {
-        GW_LAUNCH(k_guard, 1, 1, 0, st, out_n, cd.cap, out_n + 1, scal + SC_ABORT);
-        break;
-      }
-      d2h(hcnt, out_n, 2);
-      if (hcnt[1] > 0) {
-        // large reader windows (> kSmallWin reads between two writes)
-        const uint32_t nl = hcnt[1];
-        uint32_t* sizes = C->get<uint32_t>("lg_sz", nl + 1);
-        std::vector<uint32_t> hi(nl), hw(nl);
-        CK(cudaMemcpyAsync(hi.data(), large_i, sizeof(uint32_t) * nl, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hw.data(), large_ws, sizeof(uint32_t) * nl, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        std::vector<uint32_t> off(nl);
-        uint64_t M = 0;
-        for (uint32_t k = 0; k < nl; k++) {
-          off[k] = (uint32_t)M;
-          M += hi[k] - hw[k];
-        }
-        CK(cudaMemcpyAsync(sizes, off.data(), sizeof(uint32_t) * nl, cudaMemcpyHostToDevice, st));
-        unsigned long long* lk = C->get<unsigned long long>("lg_k", M);
-        uint32_t* lv = C->get<uint32_t>("lg_v", M);
-        GW_LAUNCH(k_large_fill, std::min<uint32_t>(nl, 65535u), kThreads, 0, st, large_i, large_ws, sizes, nl, sto, lk,
-                  lv);
-        sort<unsigned long long>(lk, lv, M, 24 + ceil_log2(nl + 1), "lg");
-        GW_LAUNCH(k_large_check, grid_for(M), kThreads, 0, st, ca, lk, lv, M, nl);
-        check_launch();
-        d2h(hcnt, out_n, 1);  // also keeps off / hi / hw alive until the copies completed
-      }
-      if (hcnt[0] <= cd.cap) break;
-      cand_cap = (uint64_t)hcnt[0] + 1024;
-      CK(cudaMemsetAsync(w.err, 0, sizeof(uint32_t), st));
+    if (!has_locks) {
+      pbeg(PH_WALKER);
+      walker_phase();
+      pend(PH_WALKER);
+      pbeg(PH_SORT);
+      access_sort();
+      pend(PH_SORT);
+      pbeg(PH_CHECK);
+      cd = check_pass(false, "c", SC_NCAND);
+      pend(PH_CHECK);
+    } else {
+      // lock mode: the structural candidates first (clock independent), then
+      // the walker answers their clock half in trace order
+      pbeg(PH_SORT);
+      access_sort();
+      pend(PH_SORT);
+      pbeg(PH_CHECK);
+      Cands cq = check_pass(true, "q", SC_NQ);
+      pend(PH_CHECK);
+      pbeg(PH_WALKER);
+      const uint64_t nq = obs_nq;
+      query_setup(cq, nq);
+      walker_phase();
+      pend(PH_WALKER);
+      pbeg(PH_CHECK);
+      cd = resolve_pass(cq, nq);
+      pend(PH_CHECK);
     }
-    obs_ncand = hcnt[0];
-    obs_nlarge = hcnt[1];
-    obs_cand_cap = cand_cap;
-    // graph mode sizes everything for the plan's capacity; counts stay on the device
-    const uint32_t ncap = gmode ? cd.cap : hcnt[0];
-    S.n_candidates = hcnt[0];
-    event(4);
 
     // ------------------------------------------------------- dedup / final
+    pbeg(PH_FINAL);
+    const uint32_t ncap = gmode ? cd.cap : obs_ncand;
+    uint32_t* out_n = scal + SC_NCAND;  // [NCAND], [NLARGE], [NSURV]
     uint32_t* d_nsurv = out_n + 2;
     C->d_scal = scal;
     C->d_nsurv = d_nsurv;
@@ -672,11 +456,366 @@ struct Pipeline {
       check_launch();
     }
     C->d_diags = w.diags;
-    C->arena_words = arena_words;
-    event(5);
+    C->arena_words = arena_units << OBJ_USHIFT;
+    pend(PH_FINAL);
+    event(1);
     S.n_sync = hs.n_acq + hs.n_rel + hs.n_end + hs.n_bar;
     C->launches = g_launches;
     C->stats_pending = !gmode;
+  }
+
+  // ---- pipeline state shared by the phases --------------------------------
+  uint32_t* scal = nullptr;
+  Stats hs{};
+  bool has_locks = false, snap_mode = false;
+  uint64_t gmax = 1, n_hard = 0, snap_entries = 0, lcap = 1, arena_units = 0;
+  uint32_t G = 1, maxd = 1, n_incs = 0;
+  WalkArgs w;
+  KeyRuns kr{};
+  bool wide = false;
+  uint32_t* vals = nullptr;  // access pass: sorted event indices
+  void* skeys = nullptr;
+  uint32_t *sto = nullptr, *segst = nullptr, *lastw = nullptr;
+  uint64_t obs_nq = 0;
+
+  // ------------------------------------------------------- lock pre-pass
+  void lock_prepass() {
+    const uint64_t N = tr.n;
+    const uint64_t nle = hs.n_acq + hs.n_rel + hs.n_end;
+    uint32_t* flag = C->get<uint32_t>("lk_flag", N);
+    GW_LAUNCH(k_lock_mark, grid_for(N), kThreads, 0, st, tr, flag);
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{flag}, N, OpSum(), 0u, false, "sc_u32");
+    uint32_t* ktid = C->get<uint32_t>("lk_tid", nle);
+    uint32_t* kev = C->get<uint32_t>("lk_ev", nle);
+    GW_LAUNCH(k_lock_compact, grid_for(N), kThreads, 0, st, tr, flag, ktid, kev);
+    sort<uint32_t>(ktid, kev, nle, ceil_log2(tr.T), "lk");
+    uint32_t* seg_beg = C->get<uint32_t>("lk_sb", tr.T);
+    uint32_t* seg_end = C->get<uint32_t>("lk_se", tr.T);
+    CK(cudaMemsetAsync(seg_beg, 0, sizeof(uint32_t) * tr.T, st));
+    CK(cudaMemsetAsync(seg_end, 0, sizeof(uint32_t) * tr.T, st));
+    GW_LAUNCH(k_lock_segs, grid_for(nle), kThreads, 0, st, ktid, (uint32_t)nle, seg_beg, seg_end);
+    unsigned long long* node_lock = C->get<unsigned long long>("lk_nlock", nle);
+    uint32_t* node_parent = C->get<uint32_t>("lk_nparent", nle);
+    uint32_t* top_after = C->get<uint32_t>("lk_top", nle);
+    uint8_t* lflags = C->get<uint8_t>("lflags", N);
+    CK(cudaMemsetAsync(lflags, 0, N, st));
+    GW_LAUNCH(k_lock_automaton, grid_for(nle), kThreads, 0, st, tr, ktid, kev, (uint32_t)nle, seg_end, node_lock,
+              node_parent, top_after, lflags, scal + SC_MAXD);
+    uint32_t* etop = C->get<uint32_t>("lk_etop", N);
+    uint32_t* npair = C->get<uint32_t>("lk_npair", N);
+    GW_LAUNCH(k_lock_access, grid_for(N), kThreads, 0, st, tr, kev, top_after, seg_beg, seg_end, node_parent,
+              lflags, etop, npair, scal + SC_NINCS);
+    uint32_t* poff = C->get<uint32_t>("lk_poff", N);
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{npair}, ArrStore<uint32_t>{poff}, N, OpSum(), 0u, false, "sc_u32");
+    uint32_t hv[4];
+    CK(cudaMemcpyAsync(hv, poff + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hv + 1, npair + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hv + 2, scal, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t NP = (uint64_t)hv[0] + hv[1];
+    maxd = std::max<uint32_t>(hv[2], 1);
+    n_incs = hv[3];
+    unsigned long long* plock = C->get<unsigned long long>("lk_plock", NP + 1);
+    unsigned long long* pk = C->get<unsigned long long>("lk_pk", NP + 1);
+    uint32_t* pv = C->get<uint32_t>("lk_pv", NP + 1);
+    unsigned long long* orand = C->get<unsigned long long>("lk_orand", 2);
+    GW_LAUNCH(k_orand_init, 1, 1, 0, st, orand);
+    GW_LAUNCH(k_lock_pairs, grid_for(N), kThreads, 0, st, tr, poff, npair, etop, node_lock, node_parent, plock, pv,
+              orand);
+    unsigned long long ho[2];
+    d2h(ho, orand, 2);
+    KeyRuns lkr = key_runs(NP ? ho[0] ^ ho[1] : 0ull);
+    lkr.sentinel = 0;
+    lkr.nbits = 0;
+    for (int i = 0; i < lkr.n; i++) lkr.nbits += lkr.width[i];
+    GW_LAUNCH(k_compact_u64, grid_for(NP + 1), kThreads, 0, st, plock, NP, lkr, pk);
+    sort<unsigned long long>(pk, pv, NP, lkr.nbits, "lkp");
+    uint32_t* segstart = C->get<uint32_t>("lk_pseg", NP + 1);
+    scan<uint32_t, OpMaxU32>(LockSegLoad{pk}, ArrStore<uint32_t>{segstart}, NP, OpMaxU32(), 0u, true, "sc_u32");
+    uint32_t* prank = C->get<uint32_t>("lk_prank", NP + 1);
+    // lock table (created here, one entry + ticket per lock) before the ranks kernel inserts into it
+    lcap = pow2_at_least(2 * (hs.n_acq + hs.n_rel) + 2);
+    w.locks = C->get<LockEnt>("t_lock", lcap);
+    w.lock_mask = (uint32_t)(lcap - 1);
+    CK(cudaMemsetAsync(w.locks, 0, sizeof(LockEnt) * lcap, st));
+    w.plock = plock;
+    GW_LAUNCH(k_lock_ranks, grid_for(NP + 1), kThreads, 0, st, w, pk, pv, segstart, NP, prank);
+    check_launch();
+    w.lflags = lflags;
+    w.poff = poff;
+    w.npair = npair;
+    w.prank = prank;
+  }
+
+  // ------------------------------------------------- access sort + scan
+  void access_sort() {
+    const uint64_t N = tr.n;
+    // All N positions are sorted; non-access events carry the top sentinel key
+    // and sort last, and every access-pass kernel skips them, so no kernel
+    // needs the access count on the host.
+    kr = key_runs(gmode ? P->D : (hs.n_acc ? hs.key_or ^ hs.key_and : 0ull));
+    C->stats.sort_bits = kr.nbits;
+    wide = kr.nbits > 32;
+    obs_D = hs.n_acc ? hs.key_or ^ hs.key_and : 0ull;
+    vals = C->get<uint32_t>("acc_v", N);
+    if (!wide) {
+      uint32_t* k32 = C->get<uint32_t>("acc_k", N);
+      GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals);
+      sort<uint32_t>(k32, vals, N, kr.nbits, "acc");
+      skeys = k32;
+    } else {
+      unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
+      GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals);
+      sort<unsigned long long>(k64, vals, N, kr.nbits, "acc");
+      skeys = k64;
+    }
+    sto = C->get<uint32_t>("acc_to", N);
+    GW_LAUNCH(k_gather_to, grid_for(N), kThreads, 0, st, vals, tr.tidop, N, sto);
+    segst = C->get<uint32_t>("acc_segst", N);
+    lastw = C->get<uint32_t>("acc_lastw", N);
+    if (!wide)
+      scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, N, OpMax2(),
+                          make_uint2(0, 0), true, "sc_u2");
+    else
+      scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
+                          SegStore{segst, lastw}, N, OpMax2(), make_uint2(0, 0), true, "sc_u2");
+  }
+
+  Cands make_cands(const std::string& tag, uint64_t cap, uint32_t* cnt) {
+    Cands c;
+    c.okey = C->get<unsigned long long>(tag + "_okey", cap);
+    c.loc = C->get<unsigned long long>(tag + "_loc", cap);
+    c.prior = C->get<uint32_t>(tag + "_prior", cap);
+    c.cur = C->get<uint32_t>(tag + "_cur", cap);
+    c.kind = C->get<uint32_t>(tag + "_kind", cap);
+    c.n = cnt;
+    c.cap = (uint32_t)std::min<uint64_t>(cap, 0xFFFFFFF0ull);
+    c.err = scal + SC_ERR;
+    return c;
+  }
+
+  // ------------------------------------------------------------ check pass
+  // Candidates of the write check and the reader windows (+ the same-
+  // instruction pairs when !defer).  defer: emit every structural candidate
+  // (u != t, !cover) and leave the clock comparison to the walker's queries.
+  // Counts at scal[slot] (candidates) and scal[slot + 1] (large windows).
+  Cands check_pass(bool defer, const char* tag, int slot) {
+    const uint64_t N = tr.n, NA = N;
+    uint32_t* cnt = scal + slot;
+    uint32_t* large_i = C->get<uint32_t>("lg_i", NA / kSmallWin + 1);
+    uint32_t* large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);
+    uint64_t cand_cap = gmode ? P->cand_cap : std::max<uint64_t>(65536, NA / 4);
+    Cands cd;
+    CheckArgs ca;
+    memset(&ca, 0, sizeof ca);
+    uint32_t hcnt[2] = {0, 0};
+    for (int attempt = 0; attempt < 2; attempt++) {
+      cd = make_cands(tag, cand_cap, cnt);
+      CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t), st));
+      if (!defer) CK(cudaMemsetAsync(scal + SC_NSURV, 0, sizeof(uint32_t), st));
+      ca.tr = tr;
+      ca.vals = vals;
+      ca.sto = sto;
+      ca.segst = segst;
+      ca.lastw = lastw;
+      ca.time = defer ? nullptr : w.time;
+      ca.vobj = defer ? nullptr : w.vobj;
+      ca.arena = defer ? nullptr : w.arena;
+      ca.n_acc = NA;
+      ca.c = cd;
+      ca.large_i = large_i;
+      ca.large_ws = large_ws;
+      ca.n_large = cnt + 1;
+      ca.large_cap = (uint32_t)(NA / kSmallWin + 1);
+      ca.defer = defer ? 1 : 0;
+      GW_LAUNCH(k_check, grid_for(NA), kThreads, 0, st, ca);
+      if (!defer) GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd);
+      check_launch();
+      if (gmode) {
+        GW_LAUNCH(k_guard, 1, 1, 0, st, cnt, cd.cap, cnt + 1, scal + SC_ABORT);
+        break;
+      }
+      d2h(hcnt, cnt, 2);
+      if (hcnt[1] > 0) {
+        // large reader windows (> kSmallWin reads between two writes)
+        const uint32_t nl = hcnt[1];
+        uint32_t* sizes = C->get<uint32_t>("lg_sz", nl + 1);
+        std::vector<uint32_t> hi(nl), hw(nl);
+        CK(cudaMemcpyAsync(hi.data(), large_i, sizeof(uint32_t) * nl, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hw.data(), large_ws, sizeof(uint32_t) * nl, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<uint32_t> off(nl);
+        uint64_t M = 0;
+        for (uint32_t k = 0; k < nl; k++) {
+          off[k] = (uint32_t)M;
+          M += hi[k] - hw[k];
+        }
+        CK(cudaMemcpyAsync(sizes, off.data(), sizeof(uint32_t) * nl, cudaMemcpyHostToDevice, st));
+        unsigned long long* lk = C->get<unsigned long long>("lg_k", M);
+        uint32_t* lv = C->get<uint32_t>("lg_v", M);
+        GW_LAUNCH(k_large_fill, std::min<uint32_t>(nl, 65535u), kThreads, 0, st, large_i, large_ws, sizes, nl, sto, lk,
+                  lv);
+        sort<unsigned long long>(lk, lv, M, 24 + ceil_log2(nl + 1), "lg");
+        GW_LAUNCH(k_large_check, grid_for(M), kThreads, 0, st, ca, lk, lv, M, nl);
+        check_launch();
+        d2h(hcnt, cnt, 1);  // also keeps off / hi / hw alive until the copies completed
+      }
+      if (hcnt[0] <= cd.cap) break;
+      cand_cap = (uint64_t)hcnt[0] + 1024;
+      CK(cudaMemsetAsync(w.err, 0, sizeof(uint32_t), st));
+    }
+    if (defer) {
+      obs_nq = hcnt[0];
+    } else {
+      obs_ncand = hcnt[0];
+      obs_nlarge = hcnt[1];
+      obs_cand_cap = cand_cap;
+      C->stats.n_candidates = hcnt[0];
+    }
+    return cd;
+  }
+
+  // --------------------------------------- lock mode: Q set and queries
+  void query_setup(const Cands& cq, uint64_t nq) {
+    const uint64_t N = tr.n;
+    const uint32_t T = tr.T;
+    uint32_t* qflag = C->get<uint32_t>("q_flag", (uint64_t)T + 1);
+    uint32_t* qoff = C->get<uint32_t>("q_off", (uint64_t)T + 1);
+    CK(cudaMemsetAsync(qflag, 0, sizeof(uint32_t) * ((uint64_t)T + 1), st));
+    GW_LAUNCH(k_q_mark_acq, grid_for(N), kThreads, 0, st, tr, w.lflags, qflag);
+    uint32_t* qk = C->get<uint32_t>("q_sk", nq + 1);
+    uint32_t* qi = C->get<uint32_t>("q_sv", nq + 1);
+    if (nq) GW_LAUNCH(k_q_mark_cands, grid_for(nq), kThreads, 0, st, cq, tr.tidop, qflag, (uint8_t*)w.lflags, qk, qi);
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{qflag}, ArrStore<uint32_t>{qoff}, (uint64_t)T + 1, OpSum(), 0u, false,
+                          "sc_u32");
+    uint32_t Q = 0;
+    d2h(&Q, qoff + T);
+    sort<uint32_t>(qk, qi, nq, ceil_log2(N), "qs");
+    w.qoff = qoff;
+    w.Q = Q;
+    w.q_cur = qk;
+    w.q_idx = qi;
+    w.nq = nq;
+    w.c_prior = cq.prior;
+    w.qv = C->get<uint32_t>("q_v", nq + 1);
+    C->stats.n_candidates = nq;
+  }
+
+  // ------------------------------------------------- lock mode: resolve
+  Cands resolve_pass(const Cands& cq, uint64_t nq) {
+    const uint64_t N = tr.n;
+    uint32_t* cnt = scal + SC_NCAND;
+    uint64_t cap = std::max<uint64_t>(65536, nq + N / 8);
+    Cands cd;
+    uint32_t hc = 0;
+    for (int attempt = 0; attempt < 2; attempt++) {
+      cd = make_cands("c", cap, cnt);
+      CK(cudaMemsetAsync(cnt, 0, 3 * sizeof(uint32_t), st));
+      if (nq) GW_LAUNCH(k_resolve, grid_for(nq), kThreads, 0, st, cq, w.qv, w.time, cd);
+      GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd);
+      check_launch();
+      d2h(&hc, cnt);
+      if (hc <= cd.cap) break;
+      cap = (uint64_t)hc + 1024;
+      CK(cudaMemsetAsync(w.err, 0, sizeof(uint32_t), st));
+    }
+    obs_ncand = hc;
+    return cd;
+  }
+
+  // ----------------------------------------------------------- walker
+  void walker_phase() {
+    const uint64_t N = tr.n;
+    const uint32_t T = tr.T;
+    const bool lockq = w.qoff != nullptr;
+    const uint32_t VL = lockq ? w.Q : T;  // clock vector length
+    if (!lockq) {
+      arena_units = hs.n_bar * (uint64_t)((tr.BS + OBJ_HDR + 15) >> OBJ_USHIFT) + 4;
+    } else {
+      // fixed-size slots; live objects: records (pinned hb clocks), instance
+      // and cs clocks, thread states (<= 2 per thread) + per-CTA slack
+      w.slot_units = (VL + OBJ_HDR + 15) >> OBJ_USHIFT;
+      w.fcap = 1024;
+      w.fstack = C->get<uint32_t>("f_stack", (uint64_t)G * w.fcap);
+      w.ftop = C->get<uint32_t>("f_top", G);
+      CK(cudaMemsetAsync(w.ftop, 0, sizeof(uint32_t) * G, st));
+      const uint64_t slots = 3 * hs.n_rel + (uint64_t)n_incs * maxd + 2ull * T + 4ull * G + 64;
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      const uint64_t slot_bytes = (uint64_t)w.slot_units << (OBJ_USHIFT + 2);
+      const uint64_t cap_slots = (uint64_t)(free_b * 0.6) / slot_bytes;
+      arena_units = std::min<uint64_t>(std::min(slots, cap_slots) * w.slot_units, 0xFFFFFFF0ull);
+    }
+    C->stats.arena_words = arena_units << OBJ_USHIFT;
+    w.arena = C->get<uint32_t>("arena", arena_units << OBJ_USHIFT);
+    w.arena_cap = arena_units;
+    w.arena_top = C->get<unsigned long long>("arena_top", 1);
+    CK(cudaMemsetAsync(w.arena_top, 0, sizeof(unsigned long long), st));
+    w.time = C->get<uint32_t>("time", N);
+    w.vobj = lockq ? nullptr : C->get<uint32_t>("vobj", N);
+    w.local = C->get<uint32_t>("st_local", T);
+    w.pobj = C->get<uint32_t>("st_pobj", T);
+    w.pdiag = C->get<uint32_t>("st_pdiag", T);
+    w.nend = C->get<uint32_t>("st_nend", T);
+    w.exited = C->get<uint32_t>("st_exited", T);
+    w.rec_top = scal + SC_REC;
+    w.log_top = scal + SC_LOG;
+    w.diag_top = scal + SC_DIAG;
+    w.maxd = maxd;
+    uint64_t diag_cap = hs.n_acq + hs.n_rel + hs.n_end * (uint64_t)maxd + 16;
+    w.diags = C->get<Diag>("diags", diag_cap);
+    w.diag_cap = (uint32_t)diag_cap;
+    if (has_locks) {
+      w.hobj = C->get<uint32_t>("st_hobj", T);
+      w.depth = C->get<uint32_t>("st_depth", T);
+      w.loghead = C->get<uint32_t>("st_loghead", T);
+      w.frames = C->get<Frame>("frames", (uint64_t)T * maxd);
+      uint64_t icap = pow2_at_least(2 * hs.n_rel + 2);
+      uint64_t ccap = pow2_at_least(2 * (uint64_t)n_incs * maxd + 2);
+      w.curs = C->get<CurEnt>("t_cur", lcap);
+      w.cur_mask = (uint32_t)(lcap - 1);
+      w.insts = C->get<InstEnt>("t_inst", icap);
+      w.inst_mask = (uint32_t)(icap - 1);
+      w.cs = C->get<CsEnt>("t_cs", ccap);
+      w.cs_mask = (uint32_t)(ccap - 1);
+      CK(cudaMemsetAsync(w.curs, 0, sizeof(CurEnt) * lcap, st));
+      CK(cudaMemsetAsync(w.insts, 0, sizeof(InstEnt) * icap, st));
+      CK(cudaMemsetAsync(w.cs, 0, sizeof(CsEnt) * ccap, st));
+      w.recs = C->get<Rec>("recs", hs.n_acq + 1);
+      w.rec_cap = (uint32_t)(hs.n_acq + 1);
+      w.logs = C->get<LogEnt>("logs", (uint64_t)n_incs + 1);
+      w.log_cap = n_incs + 1;
+    }
+    if (has_locks || tr.BS > (uint32_t)kAccSmem) w.scratch = C->get<uint32_t>("scratch", (uint64_t)G * 3 * VL);
+    GW_LAUNCH(k_state_init, grid_for(T), kThreads, 0, st, w);
+    if (snap_mode) {
+      SnapArgs sa;
+      uint32_t* hflag = C->get<uint32_t>("hd_flag", N);
+      GW_LAUNCH(k_hard_mark, grid_for(N), kThreads, 0, st, tr, hflag);
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hflag}, ArrStore<uint32_t>{hflag}, N, OpSum(), 0u, false, "sc_u32");
+      uint32_t* hkey = C->get<uint32_t>("hd_key", n_hard + 1);
+      uint32_t* hev = C->get<uint32_t>("hd_ev", n_hard + 1);
+      uint32_t* hbeg = C->get<uint32_t>("hd_beg", tr.B);
+      uint32_t* hend = C->get<uint32_t>("hd_end", tr.B);
+      uint32_t* hcnt = C->get<uint32_t>("hd_cnt", tr.B);
+      CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
+      if (n_hard) {
+        GW_LAUNCH(k_hard_compact, grid_for(N), kThreads, 0, st, tr, hflag, hkey, hev, hcnt);
+        sort<uint32_t>(hkey, hev, n_hard, ceil_log2(tr.B), "hd");
+      }
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hcnt}, HardSegStore{hcnt, hbeg, hend}, tr.B, OpSum(), 0u, false,
+                            "sc_u32");
+      sa.hard_ev = hev;
+      sa.hb_beg = hbeg;
+      sa.hb_end = hend;
+      sa.snap = C->get<uint2>("snap", snap_entries);
+      GW_LAUNCH(k_walker_snap, std::min<uint32_t>(tr.B, (uint32_t)gmax), kThreads, 0, st, w, sa);
+      GW_LAUNCH(k_stamp, grid_for(N), kThreads, 0, st, w, sa);
+      C->stats.walker_ctas = std::min<uint32_t>(tr.B, (uint32_t)gmax);
+    } else {
+      GW_LAUNCH(k_walker, G, kThreads, 0, st, w);
+    }
+    check_launch();
   }
 };
 
@@ -738,7 +877,7 @@ extern "C" void gw_ctx_destroy(gw_ctx* c) {
   c->drop_plan();
   for (auto& kv : c->bufs)
     if (kv.second.p) cudaFree(kv.second.p);
-  for (int i = 0; i < 8; i++)
+  for (int i = 0; i < gw_ctx::kEv; i++)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   delete c;
 }
@@ -754,11 +893,11 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   const bool match = !eager && P.valid && P.N == tr.n && P.B == tr.B && P.W == tr.W && P.L == tr.L && P.key == kp &&
                      P.tidop == tp && P.instr == ip && P.stream == st && P.inactive_opt == inactive;
   if (match) {
-    for (int i = 0; i < 8; i++)
+    for (int i = 0; i < gw_ctx::kEv; i++)
       if (!c->ev[i]) CK(cudaEventCreate(&c->ev[i]));
     CK(cudaEventRecord(c->ev[0], st));
     CK(cudaGraphLaunch(P.exec, st));
-    CK(cudaEventRecord(c->ev[5], st));
+    CK(cudaEventRecord(c->ev[1], st));
     c->last_graph = true;
     c->launches = P.launches;
     c->stats_pending = true;
@@ -834,6 +973,7 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
     cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
     const uint32_t inactive = o ? o->inactive_opt : 1u;
     const uint64_t N = t->n_events;
+    c->last_stream = st;
     unsigned long long* k = c->get<unsigned long long>("in_key", N);
     uint32_t* to = c->get<uint32_t>("in_tidop", N);
     uint32_t* in = c->get<uint32_t>("in_instr", N);
@@ -963,6 +1103,20 @@ extern "C" int gw_gen_c4_device(uint32_t blocks, uint32_t warps, uint32_t iters,
     const uint64_t g = groups * 32ull;
     GW_LAUNCH(k_gen_c4, (unsigned)std::min<uint64_t>((g + kThreads - 1) / kThreads, 148ull * 64), kThreads, 0,
               (cudaStream_t)stream, p, (unsigned long long*)key, tidop, instr);
+    CK(cudaGetLastError());
+  });
+}
+
+extern "C" int gw_gen_c3_device(uint32_t blocks, uint32_t warps, uint32_t lanes, uint32_t iters, uint32_t locks,
+                                uint32_t region, uint32_t priv, uint64_t seed, const uint64_t* group_offsets,
+                                uint64_t* key, uint32_t* tidop, uint32_t* instr, void* stream) {
+  if (lanes == 0 || lanes > 32) { gw_set_error("C3 generator: lanes must be in [1, 32]"); return GW_E_ARG; }
+  return guarded([&] {
+    C3Params p{blocks, warps, lanes, iters, locks, region, priv, seed};
+    const uint64_t g = (uint64_t)blocks * warps * iters * 32ull;
+    GW_LAUNCH(k_gen_c3, (unsigned)std::min<uint64_t>((g + kThreads - 1) / kThreads, 148ull * 64), kThreads, 0,
+              (cudaStream_t)stream, p, (const unsigned long long*)group_offsets, (unsigned long long*)key, tidop,
+              instr);
     CK(cudaGetLastError());
   });
 }

@@ -43,12 +43,15 @@ constexpr uint32_t NIL = 0xFFFFFFFFu;
 constexpr uint32_t SC_DEV = 0xFFFFFFFFu;  // device scope
 constexpr int kWalkCH = 2048;              // events staged per chunk
 constexpr int kAccSmem = 4096;             // barrier accumulator kept in smem up to this span
-constexpr uint32_t OBJ_HDR = 4;            // object header {lo, len, pad, pad}: data 16-byte aligned
+constexpr uint32_t OBJ_HDR = 4;            // object header {lo, len, ref, pad}: data 16-byte aligned
+constexpr int OBJ_USHIFT = 4;              // object handles count 64-byte units (2^32 units = 256 GiB)
+constexpr uint32_t REF_PERM = 0x40000000u; // reference count of objects that are never collected
 
 // lflags bits (lock pre-pass)
 constexpr uint8_t LF_OK = 1;      // successful acquire / release
 constexpr uint8_t LF_INCS = 2;    // access inside >= 1 critical section
 constexpr uint8_t LF_LOCKREL = 4; // takes the global lock ticket
+constexpr uint8_t LF_QUERY = 8;   // access with race-check queries (lock mode)
 
 // error flags
 constexpr uint32_t ERR_ARENA = 1, ERR_TABLE = 2, ERR_FRAMES = 4, ERR_LOG = 8, ERR_REC = 16, ERR_DIAG = 32,
@@ -82,10 +85,25 @@ struct WalkArgs {
   uint32_t *local, *pobj, *pdiag, *hobj, *nend, *exited, *depth, *loghead;
   Frame* frames;
   uint32_t maxd;
-  // clock arena
+  // clock arena (handles in 64-byte units)
   uint32_t* arena;
   unsigned long long* arena_top;
   unsigned long long arena_cap;
+  // lock mode: clocks are projected onto the queried thread set Q (qoff =
+  // exclusive prefix of the Q membership flags over T+1 threads), objects are
+  // fixed-size slots with reference counts, recycled through per-CTA stacks
+  const uint32_t* qoff;
+  uint32_t Q;
+  uint32_t slot_units;
+  uint32_t* fstack;
+  uint32_t* ftop;
+  uint32_t fcap;
+  // lock mode: race-check queries answered in trace order by the walker
+  const uint32_t* q_cur;    // query current events, sorted
+  const uint32_t* q_idx;    // candidate index of each sorted query
+  uint64_t nq;
+  const uint32_t* c_prior;  // candidate prior event
+  uint32_t* qv;             // out: pred_t[u] of the current thread at the query
   // locks
   int has_locks;
   uint32_t inactive_opt;
@@ -118,25 +136,77 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 
 __device__ __forceinline__ bool sc_overlap(uint32_t a, uint32_t b) { return a == SC_DEV || b == SC_DEV || a == b; }
 
-// arena object accessors (o = word offset of header {lo, len})
+// arena object accessors (o = handle: 64-byte unit index of the header {lo, len, ref})
+__device__ __forceinline__ uint32_t* optr(uint32_t* arena, uint32_t o) { return arena + ((size_t)o << OBJ_USHIFT); }
+__device__ __forceinline__ const uint32_t* optr(const uint32_t* arena, uint32_t o) {
+  return arena + ((size_t)o << OBJ_USHIFT);
+}
 __device__ __forceinline__ uint32_t obj_get(const uint32_t* arena, uint32_t o, uint32_t u) {
   if (o == NIL) return 0u;
-  uint32_t lo = arena[o], len = arena[o + 1];
+  const uint32_t* h = optr(arena, o);
+  uint32_t lo = h[0], len = h[1];
   uint32_t d = u - lo;
-  return d < len ? arena[o + OBJ_HDR + d] : 0u;
+  return d < len ? h[OBJ_HDR + d] : 0u;
 }
 __device__ __forceinline__ uint32_t obj_get_cg(const uint32_t* arena, uint32_t o, uint32_t u) {
   if (o == NIL) return 0u;
-  uint32_t lo = __ldcg(arena + o), len = __ldcg(arena + o + 1);
+  const uint32_t* h = optr(arena, o);
+  uint32_t lo = __ldcg(h), len = __ldcg(h + 1);
   uint32_t d = u - lo;
-  return d < len ? __ldcg(arena + o + OBJ_HDR + d) : 0u;
+  return d < len ? __ldcg(h + OBJ_HDR + d) : 0u;
 }
 
+// clock coordinates: thread index (lock-free traces) or Q index (lock mode)
+__device__ __forceinline__ bool lockmode(const WalkArgs& a) { return a.qoff != nullptr; }
+__device__ __forceinline__ uint32_t vlen(const WalkArgs& a) { return a.qoff ? a.Q : a.tr.T; }
+__device__ __forceinline__ uint32_t vidx(const WalkArgs& a, uint32_t u) {
+  if (!a.qoff) return u;
+  const uint32_t x = a.qoff[u];
+  return a.qoff[u + 1] != x ? x : NIL;
+}
+// coordinate range of block b's threads
+__device__ __forceinline__ void vblock(const WalkArgs& a, uint32_t b, uint32_t& lo, uint32_t& hi) {
+  if (!a.qoff) { lo = b * a.tr.BS; hi = lo + a.tr.BS; }
+  else { lo = a.qoff[(size_t)b * a.tr.BS]; hi = a.qoff[(size_t)(b + 1) * a.tr.BS]; }
+}
+
+// Allocation.  Lock mode: one fixed-size slot, recycled from this CTA's stack
+// (caller: a single thread, with no concurrent frees in the CTA).  Objects are
+// created, referenced and freed by one walker CTA only (the one owning the
+// threads that hold them; records pin theirs forever), so the stacks are
+// CTA-private.  Lock-free traces: bump allocation, never freed.
 __device__ __forceinline__ uint32_t arena_alloc(const WalkArgs& a, uint32_t words) {
-  words = (words + 3u) & ~3u;  // keep every object 16-byte aligned
-  unsigned long long o = atomicAdd(a.arena_top, (unsigned long long)words);
-  if (o + words > a.arena_cap) { atomicOr(a.err, ERR_ARENA); return NIL; }
+  unsigned long long units;
+  if (a.slot_units) {
+    uint32_t n = a.ftop[blockIdx.x];
+    if (n > a.fcap) n = a.fcap;  // pushes past the capacity were dropped (leaked)
+    if (n > 0) {
+      a.ftop[blockIdx.x] = n - 1;
+      return a.fstack[(size_t)blockIdx.x * a.fcap + n - 1];
+    }
+    units = a.slot_units;
+  } else {
+    units = (words + (1u << OBJ_USHIFT) - 1) >> OBJ_USHIFT;
+  }
+  unsigned long long o = atomicAdd(a.arena_top, units);
+  if (o + units > a.arena_cap) { atomicOr(a.err, ERR_ARENA); return NIL; }
   return (uint32_t)o;
+}
+// reference counts (lock mode only)
+__device__ __forceinline__ void obj_retain(const WalkArgs& a, uint32_t o, uint32_t n = 1) {
+  if (a.slot_units && o != NIL) atomicAdd(optr(a.arena, o) + 2, n);
+}
+__device__ __forceinline__ void obj_release(const WalkArgs& a, uint32_t o) {
+  if (!a.slot_units || o == NIL) return;
+  if (atomicSub(optr(a.arena, o) + 2, 1u) == 1u) {
+    const uint32_t i = atomicAdd(a.ftop + blockIdx.x, 1u);
+    if (i < a.fcap) a.fstack[(size_t)blockIdx.x * a.fcap + i] = o;
+  }
+}
+// initialise a new object's header
+__device__ __forceinline__ void obj_init(const WalkArgs& a, uint32_t o, uint32_t lo, uint32_t len, uint32_t ref) {
+  uint32_t* h = optr(a.arena, o);
+  h[0] = lo; h[1] = len; h[2] = ref;
 }
 
 __device__ void emit_diag(const WalkArgs& a, uint32_t ev, uint32_t code, uint32_t sub, unsigned long long lock) {
@@ -301,39 +371,41 @@ __device__ __forceinline__ void vfill0(uint32_t* dst, uint32_t n) {
   }
 }
 
-// dst[0..T) (dense, CTA-private scratch) max= object o; returns nonzero if any entry grew
+// dst[0..n) (dense, CTA-private scratch) max= object o; returns nonzero if any entry grew
 __device__ __forceinline__ int join_obj_dense(uint32_t* dst, const uint32_t* arena, uint32_t o) {
   if (o == NIL) return 0;
-  const uint32_t lo = __ldcg(arena + o), len = __ldcg(arena + o + 1);
-  return vjoin<true, false>(dst + lo, arena + o + OBJ_HDR, len);
+  const uint32_t* h = optr(arena, o);
+  const uint32_t lo = __ldcg(h), len = __ldcg(h + 1);
+  return vjoin<true, false>(dst + lo, h + OBJ_HDR, len);
 }
 
-// materialize clock object o with diagonal [t] := diag into dense dst[0..T)
-__device__ __forceinline__ void materialize(uint32_t* dst, const uint32_t* arena, uint32_t o, uint32_t T, uint32_t t,
+// materialize clock object o with diagonal [vt] := diag (vt = NIL: none) into dense dst[0..n)
+__device__ __forceinline__ void materialize(uint32_t* dst, const uint32_t* arena, uint32_t o, uint32_t n, uint32_t vt,
                                             uint32_t diag) {
-  if (o != NIL && __ldcg(arena + o) == 0 && __ldcg(arena + o + 1) == T) {
-    vcopy<true>(dst, arena + o + OBJ_HDR, T);  // full-range object: plain copy
+  if (o != NIL && __ldcg(optr(arena, o)) == 0 && __ldcg(optr(arena, o) + 1) == n) {
+    vcopy<true>(dst, optr(arena, o) + OBJ_HDR, n);  // full-range object: plain copy
   } else {
-    vfill0(dst, T);
+    vfill0(dst, n);
     __syncthreads();
     join_obj_dense(dst, arena, o);
   }
   __syncthreads();
-  if (threadIdx.x == 0) dst[t] = diag;
+  if (threadIdx.x == 0 && vt != NIL) dst[vt] = diag;
   __syncthreads();
 }
 
-// write dense src[0..T) as a new full-range object; returns its offset (broadcast)
-__device__ uint32_t publish_dense(const WalkArgs& a, const uint32_t* src, uint32_t T) {
+// write dense src[0..n) as a new full-range object (reference count `ref`);
+// returns its handle (broadcast)
+__device__ uint32_t publish_dense(const WalkArgs& a, const uint32_t* src, uint32_t n, uint32_t ref) {
   __shared__ uint32_t s_o;
   if (threadIdx.x == 0) {
-    uint32_t o = arena_alloc(a, T + OBJ_HDR);
-    if (o != NIL) { a.arena[o] = 0; a.arena[o + 1] = T; }
+    uint32_t o = arena_alloc(a, n + OBJ_HDR);
+    if (o != NIL) obj_init(a, o, 0, n, ref);
     s_o = o;
   }
   __syncthreads();
   uint32_t o = s_o;
-  if (o != NIL) vcopy<false>(a.arena + o + OBJ_HDR, src, T);
+  if (o != NIL) vcopy<false>(optr(a.arena, o) + OBJ_HDR, src, n);
   __syncthreads();
   return o;
 }
@@ -348,28 +420,40 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
   const uint32_t base = ev_tid(to);  // lane 0 of the warp / block
   const bool warp = (to & GW_F_WARPBAR) != 0;
   const uint32_t npool = warp ? tr.L : tr.BS;
-  const uint32_t blo = (base / tr.BS) * tr.BS;  // block range
+  uint32_t blo, bhi;  // the block's coordinate range
+  vblock(a, base / tr.BS, blo, bhi);
   // participants: live pool members (gwcp.py:286 via barrier_participants, trace.py:494-519)
   uint32_t anyp = 0;
   for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
     bool inm = !warp || ((ins >> j) & 1u);
-    if (inm && !a.exited[base + j]) anyp = 1;
+    if (inm && !a.exited[base + j]) anyp++;
   }
-  if (!__syncthreads_or(anyp)) return;  // empty participant set: no effect
+  uint32_t npart = 0;  // participant count = the new objects' reference count
+  {
+    __shared__ uint32_t s_np;
+    if (threadIdx.x == 0) s_np = 0;
+    __syncthreads();
+    if (anyp) atomicAdd(&s_np, anyp);
+    __syncthreads();
+    npart = s_np;
+    __syncthreads();
+  }
+  if (!npart) return;  // empty participant set: no effect
 
   const int nkinds = a.has_locks ? 2 : 1;
   uint32_t newobj[2] = {NIL, NIL};
   for (int kind = 0; kind < nkinds; kind++) {
     uint32_t* objs = kind == 0 ? a.pobj : a.hobj;
     // hull of participant objects and the block range
-    uint32_t mylo = blo, myhi = blo + tr.BS;
+    uint32_t mylo = blo, myhi = bhi;
     for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
       bool inm = !warp || ((ins >> j) & 1u);
       uint32_t u = base + j;
       if (inm && !a.exited[u]) {
         uint32_t o = objs[u];
         if (o != NIL) {
-          uint32_t lo = a.arena[o], len = a.arena[o + 1];
+          const uint32_t* h = optr(a.arena, o);
+          uint32_t lo = h[0], len = h[1];
           mylo = min(mylo, lo);
           myhi = max(myhi, lo + len);
         }
@@ -377,11 +461,11 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
     }
     uint32_t lo = block_min_u32(mylo), hi = block_max_u32(myhi);
     uint32_t span = hi - lo;
-    uint32_t* acc = span <= (uint32_t)kAccSmem ? s_acc : a.scratch + (size_t)blockIdx.x * 3 * tr.T + 2 * tr.T;
+    uint32_t* acc = span <= (uint32_t)kAccSmem ? s_acc : a.scratch + (size_t)blockIdx.x * 3 * vlen(a) + 2 * vlen(a);
     vfill0(acc, span);
     __syncthreads();
     // join each distinct participant object once
-    uint32_t done_lo = 0;  // objects < done_lo already joined (ids increase strictly per round)
+    uint32_t done_lo = 0;  // handles < done_lo already joined (enumerated in increasing order)
     while (true) {
       uint32_t mymin = NIL;
       for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
@@ -394,8 +478,9 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
       }
       uint32_t om = block_min_u32(mymin);
       if (om == NIL) break;
-      const uint32_t olo = a.arena[om], olen = a.arena[om + 1];
-      vjoin<true, false>(acc + (olo - lo), a.arena + om + OBJ_HDR, olen);
+      const uint32_t* h = optr(a.arena, om);
+      const uint32_t olo = h[0], olen = h[1];
+      vjoin<true, false>(acc + (olo - lo), h + OBJ_HDR, olen);
       __syncthreads();
       done_lo = om + 1;
     }
@@ -403,18 +488,21 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
     for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
       bool inm = !warp || ((ins >> j) & 1u);
       uint32_t u = base + j;
-      if (inm && !a.exited[u]) acc[u - lo] = a.local[u];
+      if (inm && !a.exited[u]) {
+        const uint32_t vu = vidx(a, u);
+        if (vu != NIL) acc[vu - lo] = a.local[u];
+      }
     }
     __syncthreads();
     __shared__ uint32_t s_no;
     if (threadIdx.x == 0) {
       uint32_t o = arena_alloc(a, span + OBJ_HDR);
-      if (o != NIL) { a.arena[o] = lo; a.arena[o + 1] = span; }
+      if (o != NIL) obj_init(a, o, lo, span, npart);
       s_no = o;
     }
     __syncthreads();
     uint32_t no = s_no;
-    if (no != NIL) vcopy<false>(a.arena + no + OBJ_HDR, acc, span);
+    if (no != NIL) vcopy<false>(optr(a.arena, no) + OBJ_HDR, acc, span);
     newobj[kind] = no;
     __syncthreads();
   }
@@ -424,9 +512,15 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
     if (inm && !a.exited[u]) {
       uint32_t nl = a.local[u] + 1;
       a.local[u] = nl;
+      const uint32_t op = a.pobj[u];
       a.pobj[u] = newobj[0];
+      obj_release(a, op);
       a.pdiag[u] = nl;
-      if (a.has_locks) a.hobj[u] = newobj[1];
+      if (a.has_locks) {
+        const uint32_t oh = a.hobj[u];
+        a.hobj[u] = newobj[1];
+        obj_release(a, oh);
+      }
     }
   }
   __syncthreads();
@@ -446,7 +540,7 @@ __device__ void do_barrier_warp(const WalkArgs& a, uint32_t to, uint32_t ins, ui
   const uint32_t o = part ? a.pobj[u] : NIL;
   uint32_t mylo = blo, myhi = blo + tr.BS;
   if (o != NIL) {
-    const uint32_t olo = a.arena[o], olen = a.arena[o + 1];
+    const uint32_t olo = optr(a.arena, o)[0], olen = optr(a.arena, o)[1];
     mylo = min(mylo, olo);
     myhi = max(myhi, olo + olen);
   }
@@ -459,8 +553,8 @@ __device__ void do_barrier_warp(const WalkArgs& a, uint32_t to, uint32_t ins, ui
   while (true) {  // each distinct participant object once
     const uint32_t om = __reduce_min_sync(0xffffffffu, (o != NIL && o >= done) ? o : NIL);
     if (om == NIL) break;
-    const uint32_t olo = a.arena[om], olen = a.arena[om + 1];
-    const uint32_t* src = a.arena + om + OBJ_HDR;
+    const uint32_t olo = optr(a.arena, om)[0], olen = optr(a.arena, om)[1];
+    const uint32_t* src = optr(a.arena, om) + OBJ_HDR;
     uint32_t* dst = acc + (olo - lo);
     for (uint32_t i0 = 0; i0 < olen; i0 += 32 * 8) {  // 8 independent loads in flight per lane
       uint32_t v[8];
@@ -484,11 +578,11 @@ __device__ void do_barrier_warp(const WalkArgs& a, uint32_t to, uint32_t ins, ui
   uint32_t no = NIL;
   if (lane == 0) {
     no = arena_alloc(a, span + OBJ_HDR);
-    if (no != NIL) { a.arena[no] = lo; a.arena[no + 1] = span; }
+    if (no != NIL) obj_init(a, no, lo, span, 0);
   }
   no = __shfl_sync(0xffffffffu, no, 0);
   if (no != NIL)
-    for (uint32_t i = lane; i < span; i += 32) a.arena[no + OBJ_HDR + i] = acc[i];
+    for (uint32_t i = lane; i < span; i += 32) optr(a.arena, no)[OBJ_HDR + i] = acc[i];
   if (part) {
     a.local[u] = lu + 1;
     a.pobj[u] = no;
@@ -543,7 +637,7 @@ __device__ void tickets_release(const WalkArgs& a, uint32_t e) {
 // snapshot of all records so far (own included; empty with inactive_opt
 // off) that receives no further pushes.
 __device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uint32_t cur, uint32_t* P) {
-  __shared__ uint32_t s_ctl, s_o, s_tid, s_loc;
+  __shared__ uint32_t s_ctl, s_o, s_vid, s_loc;
   __shared__ CurEnt* s_cur;
   __shared__ LockEnt* s_lk;
   int changed = 0;
@@ -583,12 +677,14 @@ __device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uin
         const Rec* r = &a.recs[nx];
         const uint32_t rt = __ldcg(&r->tid);
         if (__ldcg(&r->closed)) {
-          const bool le = rt == t || P[rt] >= __ldcg(&r->acq_local);
+          // record owners are in Q (lock mode), so C_t[rt] is a coordinate
+          const uint32_t vr = vidx(a, rt);
+          const bool le = rt == t || (vr != NIL && P[vr] >= __ldcg(&r->acq_local));
           if (le) {
             ce->last = nx;
             ctl = sc_overlap(__ldcg(&r->scope), cur) ? 2u : 1u;
             s_o = __ldcg(&r->rel_hobj);
-            s_tid = rt;
+            s_vid = vr;
             s_loc = __ldcg(&r->rel_local);
           }
         }
@@ -601,7 +697,7 @@ __device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uin
     if (ctl == 2) {
       int ch = join_obj_dense(P, a.arena, s_o);
       __syncthreads();
-      if (threadIdx.x == 0 && s_loc > P[s_tid]) { P[s_tid] = s_loc; ch = 1; }
+      if (threadIdx.x == 0 && s_vid != NIL && s_loc > P[s_vid]) { P[s_vid] = s_loc; ch = 1; }
       changed |= __syncthreads_or(ch);
     } else {
       __syncthreads();
@@ -610,19 +706,42 @@ __device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uin
   return changed;
 }
 
+// replace thread t's pred / hb object (thread 0; lock mode reference counts)
+__device__ __forceinline__ void set_obj(const WalkArgs& a, uint32_t* objs, uint32_t t, uint32_t o) {
+  const uint32_t old = objs[t];
+  objs[t] = o;
+  obj_release(a, old);
+}
+
+// race-check queries of access e by thread t against its pred object o
+// (gwcp.py:251-269: pred_t[u] for the prior access' thread u != t)
+__device__ void answer_queries(const WalkArgs& a, uint32_t e, uint32_t o) {
+  uint64_t lo = 0, hi = a.nq;
+  while (lo < hi) {
+    const uint64_t m = (lo + hi) >> 1;
+    if (a.q_cur[m] < e) lo = m + 1; else hi = m;
+  }
+  for (uint64_t j = lo; j < a.nq && a.q_cur[j] == e; j++) {
+    const uint32_t k = a.q_idx[j];
+    const uint32_t u = ev_tid(a.tr.tidop[a.c_prior[k]]);
+    a.qv[k] = obj_get_cg(a.arena, o, vidx(a, u));
+  }
+}
+
 __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long lock) {
-  const uint32_t T = a.tr.T;
+  const uint32_t n = vlen(a);
   const uint32_t t = ev_tid(to);
+  const uint32_t vt = vidx(a, t);
   const uint32_t cur = (to & GW_F_DEVICE) ? SC_DEV : t / a.tr.BS;
-  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * T;
-  uint32_t* H = P + T;
+  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * n;
+  uint32_t* H = P + n;
   __shared__ LockEnt* s_lk;
   if (threadIdx.x == 0) s_lk = lock_find(a, lock, false);  // created by the pre-pass
   __syncthreads();
   if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); return; }
-  materialize(P, a.arena, a.pobj[t], T, t, a.pdiag[t]);
+  materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]);
   int pch = drain(a, t, lock, cur, P);
-  materialize(H, a.arena, a.hobj[t], T, t, a.local[t]);
+  materialize(H, a.arena, a.hobj[t], n, vt, a.local[t]);
   int hch = 0;
   // join instance clocks whose release orders this acquire (gwcp.py:185-188, scopes.py:50-59)
   __shared__ uint32_t s_i, s_H, s_P;
@@ -647,12 +766,12 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   pch = __syncthreads_or(pch);
   hch = __syncthreads_or(hch);
   if (pch) {
-    uint32_t o = publish_dense(a, P, T);
-    if (threadIdx.x == 0) { a.pobj[t] = o; a.pdiag[t] = P[t]; }
+    uint32_t o = publish_dense(a, P, n, 1);
+    if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
   }
   if (hch) {
-    uint32_t o = publish_dense(a, H, T);
-    if (threadIdx.x == 0) a.hobj[t] = o;
+    uint32_t o = publish_dense(a, H, n, 1);
+    if (threadIdx.x == 0) set_obj(a, a.hobj, t, o);
   }
   if (threadIdx.x == 0) {
     // CSRecord(acq_clock = C_t) pushed to the lock's list; the acquire clock
@@ -680,11 +799,19 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   __syncthreads();
 }
 
+// a new never-collected full-range object (instance / cs clocks), initialised from src
+__device__ __forceinline__ uint32_t alloc_perm(const WalkArgs& a, uint32_t n) {
+  uint32_t o = arena_alloc(a, n + OBJ_HDR);
+  if (o != NIL) obj_init(a, o, 0, n, REF_PERM);
+  return o;
+}
+
 __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long lock) {
-  const uint32_t T = a.tr.T;
+  const uint32_t n = vlen(a);
   const uint32_t t = ev_tid(to);
-  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * T;
-  uint32_t* H = P + T;
+  const uint32_t vt = vidx(a, t);
+  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * n;
+  uint32_t* H = P + n;
   __shared__ Frame s_f;
   __shared__ LockEnt* s_lk;
   if (threadIdx.x == 0) {
@@ -695,14 +822,14 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   __syncthreads();
   if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); return; }
   const uint32_t inst = s_f.scope;
-  materialize(P, a.arena, a.pobj[t], T, t, a.pdiag[t]);
+  materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]);
   int pch = drain(a, t, lock, inst, P);
   if (pch) {
-    uint32_t o = publish_dense(a, P, T);
-    if (threadIdx.x == 0) { a.pobj[t] = o; a.pdiag[t] = P[t]; }
+    uint32_t o = publish_dense(a, P, n, 1);
+    if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
     __syncthreads();
   }
-  materialize(H, a.arena, a.hobj[t], T, t, a.local[t]);
+  materialize(H, a.arena, a.hobj[t], n, vt, a.local[t]);
   // stage the frame's read / write sets with the hb clock (gwcp.py:207-210)
   __shared__ uint32_t s_arr, s_new;
   uint32_t li = a.loghead[t];  // thread 0's iterator over the frame's access log
@@ -716,9 +843,8 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
         CsEnt* ce = cs_find(a, lock, inst, le.loc, le.rw, true);
         if (!ce) break;
         if (ce->arr == NIL) {
-          uint32_t o = arena_alloc(a, T + OBJ_HDR);
+          uint32_t o = alloc_perm(a, n);
           if (o == NIL) break;
-          a.arena[o] = 0; a.arena[o + 1] = T;
           ce->arr = o;
           s_new = 1;
         }
@@ -728,9 +854,9 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     __syncthreads();
     const uint32_t arr = s_arr;
     if (arr == NIL) break;
-    uint32_t* dst = a.arena + arr + OBJ_HDR;
-    if (s_new) vcopy<false>(dst, H, T);
-    else vjoin<false, true>(dst, H, T);
+    uint32_t* dst = optr(a.arena, arr) + OBJ_HDR;
+    if (s_new) vcopy<false>(dst, H, n);
+    else vjoin<false, true>(dst, H, n);
     __syncthreads();
   }
   // instance clocks H_i, P_i (gwcp.py:211-216)
@@ -741,10 +867,8 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     s_H = NIL; s_P = NIL;
     if (ie) {
       if (ie->H == NIL) {
-        uint32_t oh = arena_alloc(a, T + OBJ_HDR), op = arena_alloc(a, T + OBJ_HDR);
-        if (oh != NIL) { a.arena[oh] = 0; a.arena[oh + 1] = T; }
-        if (op != NIL) { a.arena[op] = 0; a.arena[op + 1] = T; }
-        ie->H = oh; ie->P = op;
+        ie->H = alloc_perm(a, n);
+        ie->P = alloc_perm(a, n);
         ie->next = __ldcg(&s_lk->inst_head);
         s_lk->inst_head = (uint32_t)(ie - a.insts);
         s_newi = 1;
@@ -754,16 +878,19 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   }
   __syncthreads();
   if (s_H != NIL && s_P != NIL) {
-    uint32_t* dh = a.arena + s_H + OBJ_HDR;
-    uint32_t* dp = a.arena + s_P + OBJ_HDR;
-    if (s_newi) { vcopy<false>(dh, H, T); vcopy<false>(dp, P, T); }
-    else { vjoin<false, true>(dh, H, T); vjoin<false, true>(dp, P, T); }
+    uint32_t* dh = optr(a.arena, s_H) + OBJ_HDR;
+    uint32_t* dp = optr(a.arena, s_P) + OBJ_HDR;
+    if (s_newi) { vcopy<false>(dh, H, n); vcopy<false>(dp, P, n); }
+    else { vjoin<false, true>(dh, H, n); vjoin<false, true>(dp, P, n); }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    // close the record with rel_clock = copy(hb) (gwcp.py:216); pop; local += 1
+    // close the record with rel_clock = copy(hb) (gwcp.py:216): the record
+    // pins the thread's current hb object; pop; local += 1
     Rec* r = &a.recs[s_f.rec];
-    r->rel_hobj = a.hobj[t];
+    const uint32_t ho = a.hobj[t];
+    obj_retain(a, ho);
+    r->rel_hobj = ho;
     r->rel_local = a.local[t];
     __threadfence();
     r->closed = 1;
@@ -775,14 +902,15 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   __syncthreads();
 }
 
-// on_access inside critical sections: rule (i) joins (gwcp.py:236-249) then
-// the (time, vobj) stamp and the frame-set append (gwcp.py:278-279)
+// on_access inside critical sections: rule (i) joins (gwcp.py:236-249), then
+// the time stamp, the race-check queries and the frame-set append (gwcp.py:278-279)
 __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long loc) {
-  const uint32_t T = a.tr.T;
+  const uint32_t n = vlen(a);
   const uint32_t t = ev_tid(to);
+  const uint32_t vt = vidx(a, t);
   const uint32_t isw = ev_kind(to) == GW_K_WRITE;
-  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * T;
-  materialize(P, a.arena, a.pobj[t], T, t, a.pdiag[t]);
+  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * n;
+  materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]);
   int pch = 0;
   __shared__ uint32_t s_arr;
   const uint32_t depth = a.depth[t];
@@ -832,12 +960,13 @@ __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsig
   }
   pch = __syncthreads_or(pch);
   if (pch) {
-    uint32_t o = publish_dense(a, P, T);
-    if (threadIdx.x == 0) { a.pobj[t] = o; a.pdiag[t] = P[t]; }
+    uint32_t o = publish_dense(a, P, n, 1);
+    if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
   }
   if (threadIdx.x == 0) {
     a.time[e] = a.local[t];
-    a.vobj[e] = a.pobj[t];
+    if (a.vobj) a.vobj[e] = a.pobj[t];
+    if (a.lflags[e] & LF_QUERY) answer_queries(a, e, a.pobj[t]);
     uint32_t li = atomicAdd(a.log_top, 1u);
     if (li >= a.log_cap) atomicOr(a.err, ERR_LOG);
     else {
@@ -937,7 +1066,8 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
           if (tt[k] != NIL) {
             const uint32_t e = s_e[j0 + threadIdx.x + k * kThreads];
             a.time[e] = lv[k];
-            a.vobj[e] = ov[k];
+            if (a.vobj) a.vobj[e] = ov[k];
+            else if (a.lflags[e] & LF_QUERY) answer_queries(a, e, ov[k]);
           }
       }
       __syncthreads();

@@ -162,3 +162,83 @@ __global__ void k_gen_c4(C4Params p, unsigned long long* key, uint32_t* tidop, u
 }
 
 }  // namespace gw
+
+namespace gw {
+
+// C3 (spin-lock critical sections), the recipe of workloads.py:c3_text.  Per
+// iteration `it`, for b, for w (group g = (it*B + b)*W + w): a full-mask rd
+// then wr wacc on the warp's private region, a warp barrier, lane 0 polls the
+// lock word with 0-3 failed-CAS atomic reads, acquires lock k = hh % locks,
+// accesses 1-4 words of lock k's region, fences, releases, a warp barrier;
+// 1 % of groups add an atomic counter write (lane 1), 0.1 % an unprotected
+// write into lock k's region (lane 1); block barriers after every 16th
+// iteration.  Group offsets come from the host (workloads.c3_group_offsets);
+// one warp writes one group.
+struct C3Params {
+  uint32_t B, W, L, iters, locks, region, priv;
+  unsigned long long seed;
+};
+
+__global__ void k_gen_c3(C3Params p, const unsigned long long* goff, unsigned long long* key, uint32_t* tidop,
+                         uint32_t* instr) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gpi = (uint64_t)p.B * p.W;
+  const uint64_t ngroups = gpi * p.iters;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned long long lock_base = 0x10000000ull, region_base = 0x20000000ull, counter = 0x30000000ull;
+  for (uint64_t gi = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gi < ngroups; gi += nwarps) {
+    const uint64_t it = gi / gpi, bw = gi % gpi;
+    const uint32_t b = (uint32_t)(bw / p.W), w = (uint32_t)(bw % p.W);
+    uint64_t e = goff[gi];
+    const uint32_t f0 = (b * p.W + w) * p.L;
+    const unsigned long long pw = ((unsigned long long)(b * p.W + w) * p.priv) * 4ull;
+    for (uint32_t l = lane; l < p.L; l += 32) {
+      const unsigned long long a = pw + (((unsigned long long)p.L * it + l) % p.priv) * 4ull;
+      const uint32_t cont = l > 0 ? GW_F_CONT : 0u;
+      key[e + l] = a;
+      tidop[e + l] = (f0 + l) | (GW_K_READ << GW_OP_SHIFT) | cont;
+      instr[e + l] = 1u;
+      key[e + p.L + l] = a;
+      tidop[e + p.L + l] = (f0 + l) | (GW_K_WRITE << GW_OP_SHIFT) | cont;
+      instr[e + p.L + l] = 2u;
+    }
+    if (lane != 0) continue;
+    e += 2ull * p.L;
+    const uint32_t full = p.L >= 32 ? 0xffffffffu : ((1u << p.L) - 1u);
+    auto push = [&](unsigned long long k, uint32_t to, uint32_t in) {
+      key[e] = k; tidop[e] = to; instr[e] = in; e++;
+    };
+    const unsigned long long warpkey = ((unsigned long long)b << 32) | w;
+    const uint32_t barto = f0 | (GW_K_BARRIER << GW_OP_SHIFT) | GW_F_WARPBAR;
+    push(warpkey, barto, full);
+    const unsigned long long hh = wl_h4(p.seed, it, b, w);
+    const unsigned long long k = hh % p.locks;
+    const unsigned long long lw = lock_base + 4ull * k;
+    const uint32_t npoll = (uint32_t)((hh >> 20) % 4);
+    for (uint32_t q = 0; q < npoll; q++)
+      push(lw, f0 | (GW_K_READ << GW_OP_SHIFT) | GW_F_ATOMIC | GW_F_DEVICE, 3u);
+    push(lw, f0 | (GW_K_ACQUIRE << GW_OP_SHIFT) | GW_F_DEVICE, 0u);
+    const uint32_t nacc = 1u + (uint32_t)((hh >> 24) % 4);
+    for (uint32_t a = 0; a < nacc; a++) {
+      const unsigned long long x = region_base + 4ull * (k * p.region + wl_h2(hh, a) % p.region);
+      const bool wr = (hh >> (28 + a)) & 1ull;
+      push(x, f0 | ((wr ? GW_K_WRITE : GW_K_READ) << GW_OP_SHIFT), 4u + a);
+    }
+    push(0ull, f0 | (GW_K_FENCE << GW_OP_SHIFT) | GW_F_DEVICE, 0u);
+    push(lw, f0 | (GW_K_RELEASE << GW_OP_SHIFT) | GW_F_DEVICE, 0u);
+    push(warpkey, barto, full);
+    const uint32_t l1 = 1u % p.L;
+    if ((hh >> 40) % 100 == 0) {
+      const bool dev = ((hh >> 48) % 10) != 0;
+      push(counter, (f0 + l1) | (GW_K_WRITE << GW_OP_SHIFT) | GW_F_ATOMIC | (dev ? GW_F_DEVICE : 0u), 9u);
+    }
+    if ((hh >> 32) % 1000 == 0 && p.L > 1) {
+      const unsigned long long x = region_base + 4ull * (k * p.region + (hh >> 8) % p.region);
+      push(x, (f0 + 1) | (GW_K_WRITE << GW_OP_SHIFT), 10u);
+    }
+    if ((it % 16) == 15 && bw == gpi - 1)
+      for (uint32_t q = 0; q < p.B; q++) push(0ull, (q * p.W * p.L) | (GW_K_BARRIER << GW_OP_SHIFT), 0u);
+  }
+}
+
+}  // namespace gw

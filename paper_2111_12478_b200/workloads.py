@@ -231,6 +231,27 @@ def c3_text(blocks=16, warps=8, lanes=32, iters=24, locks=256, region=64, privat
     return "\n".join(lines) + "\n"
 
 
+def c3_group_offsets(blocks=16, warps=8, lanes=32, iters=24, locks=256, region=64, private=512, seed=3):
+    """First event of every (it, b, w) group of :func:`c3_text` (uint64,
+    length iters*B*W + 1, the last entry = the event count); the block barriers
+    of every 16th iteration are counted with the iteration's last group."""
+    B, W, L = blocks, warps, lanes
+    with np.errstate(over="ignore"):
+        it, b, w = np.meshgrid(np.arange(iters), np.arange(B), np.arange(W), indexing="ij")
+        it, b, w = (x.astype(np.uint64).ravel() for x in (it, b, w))
+        hh = h_np(seed, it, b, w)
+        npoll = (hh >> np.uint64(20)) % np.uint64(4)
+        nacc = np.uint64(1) + (hh >> np.uint64(24)) % np.uint64(4)
+        cnt = ((hh >> np.uint64(40)) % np.uint64(100) == 0).astype(np.uint64)
+        inj = ((hh >> np.uint64(32)) % np.uint64(1000) == 0).astype(np.uint64) * np.uint64(L > 1)
+        size = np.uint64(2 * L + 5) + npoll + nacc + cnt + inj
+        last = (b == np.uint64(B - 1)) & (w == np.uint64(W - 1)) & (it % np.uint64(16) == np.uint64(15))
+        size = size + np.where(last, np.uint64(B), np.uint64(0))
+    off = np.zeros(len(size) + 1, np.uint64)
+    np.cumsum(size, out=off[1:])
+    return off
+
+
 # ------------------------------------------------------------------ C4 ----
 def c4_text(blocks=16, warps=8, lanes=32, iters=16, words_per_block=16384, seed=4) -> str:
     """C4: Volta-ITS divergent warps -- a random lane subset issues single-lane

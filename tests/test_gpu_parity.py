@@ -214,3 +214,44 @@ def test_device_c4_generator_matches_text_recipe(geom):
     assert np.array_equal(t.cpu().numpy().view(np.uint32), want.tidop)
     assert np.array_equal(k.cpu().numpy().view(np.uint64), want.key)
     assert np.array_equal(i.cpu().numpy().view(np.uint32), want.instr)
+
+
+def _dev_c3(p):
+    import torch
+
+    dev = torch.device("cuda", 0)
+    off = WL.c3_group_offsets(**p)
+    n = int(off[-1])
+    k = torch.empty(n, dtype=torch.int64, device=dev)
+    t = torch.empty(n, dtype=torch.int32, device=dev)
+    i = torch.empty(n, dtype=torch.int32, device=dev)
+    o = torch.from_numpy(off[:-1].view(np.int64)).to(dev)
+    N.gen_c3_device(k.data_ptr(), t.data_ptr(), i.data_ptr(), o.data_ptr(), **p)
+    torch.cuda.synchronize()
+    return k, t, i
+
+
+@pytest.mark.parametrize("geom", [(3, 2, 32, 17), (5, 3, 8, 33)])
+def test_device_c3_generator_matches_text_recipe(geom):
+    B, W, L, it = geom
+    p = dict(blocks=B, warps=W, lanes=L, iters=it, locks=16, region=8, private=64, seed=43)
+    want = parse_trace(WL.c3_text(**p))
+    k, t, i = _dev_c3(p)
+    assert np.array_equal(t.cpu().numpy().view(np.uint32), want.tidop)
+    assert np.array_equal(k.cpu().numpy().view(np.uint64), want.key)
+    assert np.array_equal(i.cpu().numpy().view(np.uint32), want.instr)
+
+
+@pytest.mark.parametrize("iters", [1, 3])
+def test_engine_matches_oracle_c3_full_geometry(ctx, iters):
+    """The C3 config's geometry (1024 x 8 x 32 threads, 4096 locks): the first
+    iterations of the full trace are a prefix of it."""
+    tr = parse_trace(WL.c3_text(blocks=1024, warps=8, lanes=32, iters=iters, locks=4096, region=64, private=512))
+    assert ndjson_lines(tr, _run(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
+
+
+def test_engine_c3_denser_races(ctx):
+    """Fewer locks and a small private region: many conflicting critical sections."""
+    tr = parse_trace(WL.c3_text(blocks=24, warps=4, lanes=32, iters=40, locks=6, region=4, private=32, seed=9))
+    got = ndjson_lines(tr, _run(ctx, tr))
+    assert got == ndjson_lines(tr, O.run_trace(tr))
