@@ -50,6 +50,8 @@ WORKLOADS = {
     # C4 (configs[3]): 1024 x 256 threads, ITS-divergent warps (single-lane accesses in random lane order,
     # random-mask warp barriers every 4 iterations, block barriers every 64), 16M words, 1.0e9 events
     "c4": dict(gen="c4", blocks=1024, warps=8, lanes=32, iters=3786, words_per_block=16384, seed=4),
+    # C3 (configs[2]): 1024 x 256 threads, 4096 device-scope spin locks, fences, atomics, 1.005e8 events
+    "c3": dict(gen="c3", blocks=1024, warps=8, lanes=32, iters=168, locks=4096, region=64, private=512, seed=3),
     # C5 (configs[4]): the C2 recipe at 1024 x 256 threads, 256M words, 16 phases x 240 records = 1.007e9 events
     "c5": dict(gen="c2", blocks=1024, warps=8, lanes=32, phases=16, records=240, words_per_block=262144, seed=5),
 }
@@ -61,6 +63,10 @@ def workload_events(p):
     if p["gen"] == "c4":
         n = N.c4_events(p["blocks"], p["warps"], p["iters"])
         n_acc = p["iters"] * p["blocks"] * p["warps"] * 32
+    elif p["gen"] == "c3":
+        from paper_2111_12478_b200 import workloads as WL
+
+        n, n_acc, _ = WL.c3_counts(**{k: v for k, v in p.items() if k != "gen"})
     else:
         n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
         n_acc = n - p["phases"] * p["blocks"]
@@ -69,10 +75,16 @@ def workload_events(p):
 
 def workload_desc(name, p, n, n_acc):
     d = {"workload": name.upper(), "threads": f"{p['blocks']}x{p['warps']}x{p['lanes']}",
-         "addresses": p["blocks"] * p["words_per_block"], "events": n, "accesses": n_acc}
+         "addresses": p["blocks"] * p.get("words_per_block", 0), "events": n, "accesses": n_acc}
     if p["gen"] == "c4":
         d.update(iterations=p["iters"], sync="warp barriers (random masks) / 4 it, block barriers / 64 it",
                  divergence="ITS: ~half the lanes issue single-lane accesses in random order")
+    elif p["gen"] == "c3":
+        d.update(addresses=p["blocks"] * p["warps"] * p["private"] + p["locks"] * (p["region"] + 1) + 1,
+                 iterations=p["iters"], locks=p["locks"],
+                 sync="device-scope spin locks (lane 0, 1-4 protected accesses), failed-CAS polling, device fences, "
+                      "warp barriers, block barriers / 16 it",
+                 injected="1% atomic counter writes (10% block scope), 0.1% unprotected lock-region writes")
     else:
         d.update(phases=p["phases"], records_per_warp_phase=p["records"], sync="__syncthreads only",
                  injected_random_words="1%")
@@ -95,6 +107,13 @@ def make_workload(name: str, rank: int, dev):
     if p["gen"] == "c4":
         del gp["lanes"]
         N.gen_c4_device(key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), **gp)
+    elif p["gen"] == "c3":
+        from paper_2111_12478_b200 import workloads as WL
+
+        off = torch.from_numpy(WL.c3_group_offsets(**gp)[:-1].view(np.int64)).to(dev)
+        N.gen_c3_device(key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), off.data_ptr(), **gp)
+        torch.cuda.synchronize(dev)
+        del off
     else:
         N.gen_c2_device(key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), **gp)
     torch.cuda.synchronize(dev)
@@ -108,6 +127,16 @@ def host_workload_prefix(p, P):
     from paper_2111_12478_b200.trace import Trace, parse_trace
 
     gp = {k: v for k, v in p.items() if k != "gen"}
+    if p["gen"] == "c3":  # iteration-major: the first iterations are a prefix of the full trace
+        per_it = WL.c3_counts(**dict(gp, iters=1))[0]
+        gp["iters"] = min(p["iters"], max(1, -(-P // per_it)))
+        tr = parse_trace(WL.c3_text(**gp))
+        from paper_2111_12478_b200 import _native as N
+
+        m = min(P, len(tr))
+        while m < len(tr) and tr.tidop[m] & N.F_CONT:
+            m += 1
+        return Trace(tr.config, tr.key[:m], tr.tidop[:m], tr.instr[:m])
     if p["gen"] != "c4":
         return WL.c2_soa_prefix(P, **gp)
     per_it = p["blocks"] * p["warps"] * 33

@@ -10,6 +10,7 @@
 //   dedup/final   keep-first per (loc, instr, instr), sort by order key
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -518,10 +519,11 @@ struct Pipeline {
     unsigned long long* plock = C->get<unsigned long long>("lk_plock", NP + 1);
     unsigned long long* pk = C->get<unsigned long long>("lk_pk", NP + 1);
     uint32_t* pv = C->get<uint32_t>("lk_pv", NP + 1);
+    uint8_t* pacq = C->get<uint8_t>("lk_pacq", NP + 1);
     unsigned long long* orand = C->get<unsigned long long>("lk_orand", 2);
     GW_LAUNCH(k_orand_init, 1, 1, 0, st, orand);
     GW_LAUNCH(k_lock_pairs, grid_for(N), kThreads, 0, st, tr, poff, npair, etop, node_lock, node_parent, plock, pv,
-              orand);
+              pacq, orand);
     unsigned long long ho[2];
     d2h(ho, orand, 2);
     KeyRuns lkr = key_runs(NP ? ho[0] ^ ho[1] : 0ull);
@@ -533,18 +535,22 @@ struct Pipeline {
     uint32_t* segstart = C->get<uint32_t>("lk_pseg", NP + 1);
     scan<uint32_t, OpMaxU32>(LockSegLoad{pk}, ArrStore<uint32_t>{segstart}, NP, OpMaxU32(), 0u, true, "sc_u32");
     uint32_t* prank = C->get<uint32_t>("lk_prank", NP + 1);
+    uint32_t* gacq = C->get<uint32_t>("lk_gacq", NP + 1);
+    uint32_t* rix = C->get<uint32_t>("lk_rix", NP + 1);
+    scan<uint32_t, OpSum>(AcqFlagLoad{pacq, pv}, ArrStore<uint32_t>{gacq}, NP, OpSum(), 0u, false, "sc_u32");
     // lock table (created here, one entry + ticket per lock) before the ranks kernel inserts into it
     lcap = pow2_at_least(2 * (hs.n_acq + hs.n_rel) + 2);
     w.locks = C->get<LockEnt>("t_lock", lcap);
     w.lock_mask = (uint32_t)(lcap - 1);
     CK(cudaMemsetAsync(w.locks, 0, sizeof(LockEnt) * lcap, st));
     w.plock = plock;
-    GW_LAUNCH(k_lock_ranks, grid_for(NP + 1), kThreads, 0, st, w, pk, pv, segstart, NP, prank);
+    GW_LAUNCH(k_lock_ranks, grid_for(NP + 1), kThreads, 0, st, w, pk, pv, segstart, pacq, gacq, NP, prank, rix);
     check_launch();
     w.lflags = lflags;
     w.poff = poff;
     w.npair = npair;
     w.prank = prank;
+    w.rix = rix;
   }
 
   // ------------------------------------------------- access sort + scan
@@ -742,8 +748,18 @@ struct Pipeline {
       const uint64_t slots = 3 * hs.n_rel + (uint64_t)n_incs * maxd + 2ull * T + 4ull * G + 64;
       size_t free_b = 0, total_b = 0;
       CK(cudaMemGetInfo(&free_b, &total_b));
+      {  // the arena buffer of an earlier analysis is reused: count it as free
+        auto it = C->bufs.find("arena");
+        if (it != C->bufs.end()) free_b += it->second.cap;
+      }
       const uint64_t slot_bytes = (uint64_t)w.slot_units << (OBJ_USHIFT + 2);
       const uint64_t cap_slots = (uint64_t)(free_b * 0.6) / slot_bytes;
+      if (getenv("GW_DEBUG_MEM")) {
+        fprintf(stderr, "[gw] lock mode: Q=%u slot=%llu B, bound %llu slots, free %.1f GB, cap %llu slots\n", VL,
+                (unsigned long long)slot_bytes, (unsigned long long)slots, free_b / 1e9, (unsigned long long)cap_slots);
+        for (auto& kv : C->bufs)
+          if (kv.second.cap > (64u << 20)) fprintf(stderr, "[gw]   %-12s %.2f GB\n", kv.first.c_str(), kv.second.cap / 1e9);
+      }
       arena_units = std::min<uint64_t>(std::min(slots, cap_slots) * w.slot_units, 0xFFFFFFF0ull);
     }
     C->stats.arena_words = arena_units << OBJ_USHIFT;

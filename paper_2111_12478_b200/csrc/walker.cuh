@@ -58,8 +58,12 @@ constexpr uint32_t ERR_ARENA = 1, ERR_TABLE = 2, ERR_FRAMES = 4, ERR_LOG = 8, ER
                    ERR_CAND = 64, ERR_RECORD = 128, ERR_INTERNAL = 256;
 
 struct Frame { unsigned long long lock; uint32_t scope, rec, logpos, pad; };
-struct Rec { uint32_t tid, acq_local, scope, rel_hobj, rel_local, closed, next, seq; };
-struct LockEnt { unsigned long long id; uint32_t used, nrec, head, tail, inst_head, ticket; };
+// CSRecord (gwcp.py:32-43): the acquire clock kept as its epoch (tid, acq_local),
+// the release clock as the releaser's hb object + diagonal.  domall: this
+// record's release clock dominates every earlier record's of the lock.
+struct Rec { uint32_t tid, acq_local, scope, rel_hobj, rel_local, closed, domall, pad; };
+// a lock's records occupy [rec_base, rec_base + nrec) in acquire order
+struct LockEnt { unsigned long long id; uint32_t used, nrec, rec_base, pad, inst_head, ticket; };
 struct CurEnt { unsigned long long lock; uint32_t tid, used, epoch, last, bound, snap; };
 struct InstEnt { unsigned long long lock; uint32_t scope, used, H, P, next, pad; };
 struct CsEnt { unsigned long long lock, loc; uint32_t scope_rw, used, arr, pad; };
@@ -117,6 +121,7 @@ struct WalkArgs {
   InstEnt* insts; uint32_t inst_mask;
   CsEnt* cs; uint32_t cs_mask;
   Rec* recs; uint32_t* rec_top; uint32_t rec_cap;
+  const uint32_t* rix;  // lock pair -> record slot (successful acquires)
   LogEnt* logs; uint32_t* log_top; uint32_t log_cap;
   uint32_t* scratch;  // per CTA: 3*T words (P, H, acc)
   Diag* diags; uint32_t* diag_top; uint32_t diag_cap;
@@ -249,7 +254,7 @@ __device__ LockEnt* lock_find(const WalkArgs& a, unsigned long long id, bool cre
   const uint32_t h = (uint32_t)mix64(id) & a.lock_mask;
   return ht_find(a, a.locks, a.lock_mask, h, create, [&](LockEnt* e) { return __ldcg(&e->id) == id; },
                  [&](LockEnt* e) {
-                   e->id = id; e->nrec = 0; e->head = NIL; e->tail = NIL; e->inst_head = NIL; e->ticket = 0;
+                   e->id = id; e->nrec = 0; e->rec_base = 0; e->inst_head = NIL; e->ticket = 0;
                  });
 }
 
@@ -631,16 +636,33 @@ __device__ void tickets_release(const WalkArgs& a, uint32_t e) {
 }
 
 // _drain, gwcp.py:161-173, as a per-(lock, thread) cursor over the lock's
-// record list.  Queue materialisation (gwcp.py:80-100):
+// record array.  Queue materialisation (gwcp.py:80-100):
 // before the thread's first END its queue is every record of the lock by
 // other threads; after an END (drop) the next drain re-materialises a
 // snapshot of all records so far (own included; empty with inactive_opt
 // off) that receives no further pushes.
+//
+// The sequential pop loop (test C_t[r.tid] >= r.acq_local on the clock that
+// includes every earlier pop's release clock, then join) runs 32 records at a
+// time on warp 0: each lane evaluates its record's test on P plus the
+// release clocks of the records before it, found by walking back to the
+// nearest joined record whose release clock dominates all earlier ones
+// (Rec::domall), so the walk is short and the joins themselves are deferred:
+// a drain ends with one join of the last dominating record (+ the few
+// non-dominating ones after it).  Other warps wait at the CTA barrier.
+constexpr int kDrainJ = 16;  // deferred non-dominating joins before a flush
+
+__device__ __forceinline__ uint32_t relpt(const WalkArgs& a, uint32_t rel_hobj, uint32_t rtid, uint32_t rel_local,
+                                          uint32_t u, uint32_t vu) {
+  const uint32_t v = obj_get_cg(a.arena, rel_hobj, vu);
+  return rtid == u ? max(v, rel_local) : v;
+}
+
 __device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uint32_t cur, uint32_t* P) {
-  __shared__ uint32_t s_ctl, s_o, s_vid, s_loc;
   __shared__ CurEnt* s_cur;
   __shared__ LockEnt* s_lk;
-  int changed = 0;
+  __shared__ uint32_t s_tid[32], s_acq[32], s_ho[32], s_loc[32], s_flags[32];
+  __shared__ uint32_t s_m, s_nj, s_j[kDrainJ], s_stop, s_pos, s_end;
   if (threadIdx.x == 0) {
     LockEnt* lk = lock_find(a, lock, false);
     CurEnt* ce = lk ? cur_find(a, lock, t) : nullptr;
@@ -654,54 +676,115 @@ __device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uin
         ce->snap = ep != 0;
         ce->bound = ep == 0 ? NIL : (a.inactive_opt ? __ldcg(&lk->nrec) : 0u);
       }
+      const uint32_t base = __ldcg(&lk->rec_base), nrec = __ldcg(&lk->nrec);
+      const uint32_t last = __ldcg(&ce->last);
+      s_pos = last == NIL ? base : last + 1;
+      s_end = base + (ce->snap ? min(nrec, __ldcg(&ce->bound)) : nrec);
     }
+    s_m = NIL;
+    s_nj = 0;
   }
   __syncthreads();
   if (!s_cur) return 0;
+  const bool snap = __ldcg(&s_cur->snap) != 0;
+  int changed = 0;
   while (true) {
-    if (threadIdx.x == 0) {
-      CurEnt* ce = s_cur;
-      LockEnt* lk = s_lk;
-      const uint32_t snap = __ldcg(&ce->snap), bound = __ldcg(&ce->bound);
-      uint32_t last = __ldcg(&ce->last);
-      uint32_t nx = last == NIL ? __ldcg(&lk->head) : __ldcg(&a.recs[last].next);
-      if (!snap) {
-        // the thread's own records never enter its queue: step over them
-        while (nx != NIL && __ldcg(&a.recs[nx].tid) == t) { last = nx; nx = __ldcg(&a.recs[nx].next); }
-        ce->last = last;
-      } else if (nx != NIL && __ldcg(&a.recs[nx].seq) >= bound) {
-        nx = NIL;
-      }
-      uint32_t ctl = 0;  // 0 stop, 1 pop without join, 2 pop + join rel clock
-      if (nx != NIL) {
-        const Rec* r = &a.recs[nx];
-        const uint32_t rt = __ldcg(&r->tid);
-        if (__ldcg(&r->closed)) {
-          // record owners are in Q (lock mode), so C_t[rt] is a coordinate
-          const uint32_t vr = vidx(a, rt);
-          const bool le = rt == t || (vr != NIL && P[vr] >= __ldcg(&r->acq_local));
-          if (le) {
-            ce->last = nx;
-            ctl = sc_overlap(__ldcg(&r->scope), cur) ? 2u : 1u;
-            s_o = __ldcg(&r->rel_hobj);
-            s_vid = vr;
-            s_loc = __ldcg(&r->rel_local);
-          }
+    if (threadIdx.x < 32) {
+      const uint32_t lane = threadIdx.x;
+      uint32_t pos = s_pos;
+      const uint32_t end = s_end;
+      uint32_t m = s_m, nj = s_nj;
+      bool stop = false, flush = false;
+      while (!stop && !flush && pos < end) {
+        const uint32_t idx = pos + lane;
+        const bool in = idx < end;
+        uint32_t fl = 0;  // bit0 in, bit1 own (skipped), bit2 closed, bit3 joinable, bit4 domall
+        if (in) {
+          const Rec* r = a.recs + idx;
+          const uint32_t rt = __ldcg(&r->tid);
+          s_tid[lane] = rt;
+          s_acq[lane] = __ldcg(&r->acq_local);
+          s_ho[lane] = __ldcg(&r->rel_hobj);
+          s_loc[lane] = __ldcg(&r->rel_local);
+          const bool own = !snap && rt == t;
+          const bool closed = __ldcg(&r->closed) != 0;
+          fl = 1u | (own ? 2u : 0u) | (closed ? 4u : 0u) |
+               ((!own && closed && sc_overlap(__ldcg(&r->scope), cur)) ? 8u : 0u) | (__ldcg(&r->domall) ? 16u : 0u);
         }
+        s_flags[lane] = fl;
+        __syncwarp();
+        // my test, assuming every record before me in the window is popped
+        bool pass = false;
+        if (fl & 2u) pass = true;          // own record: not in the queue, stepped over
+        else if (!(fl & 4u)) pass = false;  // open (or past the end): the drain stops here
+        else if (s_tid[lane] == t) pass = true;
+        else {
+          const uint32_t u = s_tid[lane], vu = vidx(a, u);
+          uint32_t v = vu != NIL ? P[vu] : 0u;
+          bool dom = false;
+          for (int i = (int)lane - 1; i >= 0 && !dom; i--) {
+            const uint32_t fi = s_flags[i];
+            if (!(fi & 8u)) continue;
+            v = max(v, relpt(a, s_ho[i], s_tid[i], s_loc[i], u, vu));
+            dom = (fi & 16u) != 0;
+          }
+          if (!dom) {  // carried, not yet applied joins of earlier windows
+            for (uint32_t k = 0; k < nj; k++) {
+              const Rec* r = a.recs + s_j[k];
+              v = max(v, relpt(a, __ldcg(&r->rel_hobj), __ldcg(&r->tid), __ldcg(&r->rel_local), u, vu));
+            }
+            if (m != NIL) {
+              const Rec* r = a.recs + m;
+              v = max(v, relpt(a, __ldcg(&r->rel_hobj), __ldcg(&r->tid), __ldcg(&r->rel_local), u, vu));
+            }
+          }
+          pass = v >= s_acq[lane];
+        }
+        const uint32_t fails = __ballot_sync(0xffffffffu, !(in && pass));
+        uint32_t f = fails ? (uint32_t)(__ffs(fails) - 1) : 32u;  // records [pos, pos + f) are popped
+        // carry the popped joinable records (uniform over the warp)
+        for (uint32_t i = 0; i < f; i++) {
+          const uint32_t fi = s_flags[i];
+          if (!(fi & 8u)) continue;
+          if (fi & 16u) { m = pos + i; nj = 0; }
+          else if (nj < (uint32_t)kDrainJ) { if (lane == 0) s_j[nj] = pos + i; nj++; }
+          else { f = i; flush = true; break; }  // pop it after applying the deferred joins
+        }
+        if (f < 32u && !flush) stop = true;
+        pos += f;
+        __syncwarp();
       }
-      s_ctl = ctl;
+      if (lane == 0) {
+        s_pos = pos;
+        s_m = m;
+        s_nj = nj;
+        s_stop = (stop || pos >= end) ? 1u : 0u;
+        if (pos > __ldcg(&s_lk->rec_base)) s_cur->last = pos - 1;
+      }
     }
     __syncthreads();
-    const uint32_t ctl = s_ctl;
-    if (ctl == 0) break;
-    if (ctl == 2) {
-      int ch = join_obj_dense(P, a.arena, s_o);
+    // apply the deferred joins (block-wide)
+    int ch = 0;
+    const uint32_t nj = s_nj;
+    for (int k = -1; k < (int)nj; k++) {
+      const uint32_t ri = k < 0 ? s_m : s_j[k];
+      if (ri == NIL) continue;
+      const Rec* r = a.recs + ri;
+      ch |= join_obj_dense(P, a.arena, __ldcg(&r->rel_hobj));
       __syncthreads();
-      if (threadIdx.x == 0 && s_vid != NIL && s_loc > P[s_vid]) { P[s_vid] = s_loc; ch = 1; }
-      changed |= __syncthreads_or(ch);
-    } else {
+      if (threadIdx.x == 0) {
+        const uint32_t vr = vidx(a, __ldcg(&r->tid));
+        const uint32_t loc = __ldcg(&r->rel_local);
+        if (vr != NIL && loc > P[vr]) { P[vr] = loc; ch = 1; }
+      }
       __syncthreads();
     }
+    changed |= __syncthreads_or(ch);
+    const bool done = s_stop != 0;
+    __syncthreads();
+    if (threadIdx.x == 0) { s_m = NIL; s_nj = 0; }
+    __syncthreads();
+    if (done) break;
   }
   return changed;
 }
@@ -774,22 +857,29 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     if (threadIdx.x == 0) set_obj(a, a.hobj, t, o);
   }
   if (threadIdx.x == 0) {
-    // CSRecord(acq_clock = C_t) pushed to the lock's list; the acquire clock
-    // is kept as its epoch (t, local) -- see the drain-test note above.
+    // CSRecord(acq_clock = C_t) appended to the lock's records; the acquire
+    // clock is kept as its epoch (t, local) -- see the drain-test note above.
     LockEnt* lk = s_lk;
-    uint32_t ri = atomicAdd(a.rec_top, 1u);
+    const uint32_t ri = a.rix[a.poff[e]];
     uint32_t d = a.depth[t];
     if (ri >= a.rec_cap) { atomicOr(a.err, ERR_REC); }
     else if (d >= a.maxd) { atomicOr(a.err, ERR_FRAMES); }
     else {
+      const uint32_t base = __ldcg(&lk->rec_base);
+      // domall: the previous record was closed, dominated all before it, and
+      // its instance orders this acquire, so this acquire joined its release
+      // clock into hb (gwcp.py:185-188) and this record's release clock
+      // (hb at release) dominates every earlier record's
+      uint32_t domall = 1;
+      if (ri > base) {
+        const Rec* pr = a.recs + ri - 1;
+        domall = __ldcg(&pr->closed) && __ldcg(&pr->domall) && sc_overlap(__ldcg(&pr->scope), cur);
+      }
       Rec r;
       r.tid = t; r.acq_local = a.local[t]; r.scope = cur; r.rel_hobj = NIL; r.rel_local = 0; r.closed = 0;
-      r.next = NIL; r.seq = __ldcg(&lk->nrec);
+      r.domall = domall; r.pad = 0;
       a.recs[ri] = r;
-      uint32_t tail = __ldcg(&lk->tail);
-      if (tail == NIL) lk->head = ri; else a.recs[tail].next = ri;
-      lk->tail = ri;
-      lk->nrec = r.seq + 1;
+      lk->nrec = ri - base + 1;
       Frame f;
       f.lock = lock; f.scope = cur; f.rec = ri; f.logpos = a.loghead[t]; f.pad = 0;
       a.frames[(size_t)t * a.maxd + d] = f;
@@ -1330,7 +1420,7 @@ __global__ void k_lock_access(DevTrace tr, const uint32_t* kev, const uint32_t* 
 // emit (lock, event) pairs in event order (+ OR/AND of the lock ids for key compaction)
 __global__ void k_lock_pairs(DevTrace tr, const uint32_t* poff, const uint32_t* npair, const uint32_t* etop,
                              const unsigned long long* node_lock, const uint32_t* node_parent,
-                             unsigned long long* plock, uint32_t* pv, unsigned long long* orand) {
+                             unsigned long long* plock, uint32_t* pv, uint8_t* pacq, unsigned long long* orand) {
   unsigned long long ko = 0, ka = ~0ull;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t np = npair[e];
@@ -1339,9 +1429,10 @@ __global__ void k_lock_pairs(DevTrace tr, const uint32_t* poff, const uint32_t* 
     const uint32_t k = ev_kind(tr.tidop[e]);
     if (k == GW_K_ACQUIRE || k == GW_K_RELEASE) {
       plock[off] = tr.key[e];
+      pacq[off] = k == GW_K_ACQUIRE ? 1 : 0;
     } else {
       uint32_t j = 0;
-      for (uint32_t q = etop[e]; q != NIL; q = node_parent[q]) plock[off + j++] = node_lock[q];
+      for (uint32_t q = etop[e]; q != NIL; q = node_parent[q]) { pacq[off + j] = 0; plock[off + j++] = node_lock[q]; }
     }
     for (uint32_t j = 0; j < np; j++) {
       ko |= plock[off + j];
@@ -1369,12 +1460,25 @@ struct LockSegLoad {
 struct OpMaxU32 {
   __device__ __forceinline__ uint32_t operator()(const uint32_t& a, const uint32_t& b) const { return max(a, b); }
 };
+// sorted pairs: is-acquire flags, for the record slots (exclusive scan = slot)
+struct AcqFlagLoad {
+  const uint8_t* pacq;
+  const uint32_t* sv;
+  __device__ __forceinline__ uint32_t operator()(uint64_t q) const { return pacq[sv[q]]; }
+};
+// per pair: rank within its lock (ticket order) and, for successful acquires,
+// the record slot; per lock: one table entry (+ ticket) and its first slot
 __global__ void k_lock_ranks(const WalkArgs a, const unsigned long long* sk, const uint32_t* sv,
-                             const uint32_t* segstart, uint64_t P, uint32_t* prank) {
+                             const uint32_t* segstart, const uint8_t* pacq, const uint32_t* gacq, uint64_t P,
+                             uint32_t* prank, uint32_t* rix) {
   for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < P; q += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t pair = sv[q];
     prank[pair] = (uint32_t)(q - segstart[q]);
-    if (q == 0 || sk[q] != sk[q - 1]) lock_find(a, a.plock[pair], true);  // one table entry (+ ticket) per lock
+    if (pacq[pair]) rix[pair] = gacq[q];
+    if (q == 0 || sk[q] != sk[q - 1]) {
+      LockEnt* e = lock_find(a, a.plock[pair], true);
+      if (e) e->rec_base = gacq[q];
+    }
   }
 }
 __global__ void k_orand_init(unsigned long long* orand) {

@@ -252,6 +252,18 @@ def c3_group_offsets(blocks=16, warps=8, lanes=32, iters=24, locks=256, region=6
     return off
 
 
+def c3_counts(blocks=16, warps=8, lanes=32, iters=24, locks=256, region=64, private=512, seed=3):
+    """(events, accesses, acquires) of :func:`c3_text` without generating it."""
+    B, W, L = blocks, warps, lanes
+    with np.errstate(over="ignore"):
+        it, b, w = np.meshgrid(np.arange(iters), np.arange(B), np.arange(W), indexing="ij")
+        hh = h_np(seed, *(x.astype(np.uint64).ravel() for x in (it, b, w)))
+        acc = (np.uint64(2 * L) + (hh >> np.uint64(20)) % np.uint64(4) + np.uint64(1) + (hh >> np.uint64(24)) % np.uint64(4)
+               + ((hh >> np.uint64(40)) % np.uint64(100) == 0) + ((hh >> np.uint64(32)) % np.uint64(1000) == 0) * (L > 1))
+    off = c3_group_offsets(blocks, warps, lanes, iters, locks, region, private, seed)
+    return int(off[-1]), int(acc.sum()), int(iters * B * W)
+
+
 # ------------------------------------------------------------------ C4 ----
 def c4_text(blocks=16, warps=8, lanes=32, iters=16, words_per_block=16384, seed=4) -> str:
     """C4: Volta-ITS divergent warps -- a random lane subset issues single-lane
