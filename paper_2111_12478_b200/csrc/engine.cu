@@ -829,7 +829,24 @@ struct Pipeline {
       GW_LAUNCH(k_stamp, grid_for(N), kThreads, 0, st, w, sa);
       C->stats.walker_ctas = std::min<uint32_t>(tr.B, (uint32_t)gmax);
     } else {
+      const bool prof = getenv("GW_PROF_WALKER") != nullptr;
+      if (prof) {
+        w.prof = C->get<unsigned long long>("prof", (uint64_t)G * 8);
+        CK(cudaMemsetAsync(w.prof, 0, sizeof(unsigned long long) * G * 8, st));
+      }
       GW_LAUNCH(k_walker, G, kThreads, 0, st, w);
+      if (prof) {
+        std::vector<unsigned long long> hp((size_t)G * 8);
+        d2h(hp.data(), w.prof, hp.size());
+        double sum[8] = {0}, mx[8] = {0};
+        for (uint32_t g = 0; g < G; g++)
+          for (int k = 0; k < 8; k++) { sum[k] += hp[g * 8 + k]; mx[k] = std::max(mx[k], (double)hp[g * 8 + k]); }
+        const char* nm[8] = {"stamp", "barrier", "ticket", "acquire", "release", "incs", "-", "lockev"};
+        fprintf(stderr, "[gw] walker G=%u Q=%u per-CTA avg / max ms:", G, w.Q);
+        for (int k = 0; k < 6; k++) fprintf(stderr, " %s %.2f/%.2f", nm[k], sum[k] / G / 1e6, mx[k] / 1e6);
+        fprintf(stderr, "; lock events %.0f\n", sum[7]);
+      }
+      w.prof = nullptr;
     }
     check_launch();
   }

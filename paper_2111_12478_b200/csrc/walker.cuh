@@ -122,6 +122,7 @@ struct WalkArgs {
   CsEnt* cs; uint32_t cs_mask;
   Rec* recs; uint32_t* rec_top; uint32_t rec_cap;
   const uint32_t* rix;  // lock pair -> record slot (successful acquires)
+  unsigned long long* prof;  // optional per-CTA time split (GW_PROF_WALKER): ns per event class
   LogEnt* logs; uint32_t* log_top; uint32_t log_cap;
   uint32_t* scratch;  // per CTA: 3*T words (P, H, acc)
   Diag* diags; uint32_t* diag_top; uint32_t diag_cap;
@@ -1068,6 +1069,25 @@ __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsig
 }
 
 // ------------------------------------------------------------ the kernel --
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// prof slots: 0 stamp, 1 barrier, 2 ticket wait, 3 acquire, 4 release, 5 in-CS access, 6 total, 7 #lock events
+struct ProfT {
+  const WalkArgs& a;
+  unsigned long long t;
+  __device__ ProfT(const WalkArgs& a_) : a(a_), t(a_.prof && threadIdx.x == 0 ? gtime() : 0ull) {}
+  __device__ void lap(int slot) {
+    if (a.prof && threadIdx.x == 0) {
+      const unsigned long long n = gtime();
+      a.prof[blockIdx.x * 8 + slot] += n - t;
+      t = n;
+    }
+  }
+};
+
 __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
   __shared__ uint32_t s_e[kWalkCH];
   __shared__ uint32_t s_to[kWalkCH];
@@ -1134,6 +1154,7 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
     __syncthreads();
     const uint32_t nh = s_nh;
     uint32_t pos = 0;
+    ProfT pf(a);
     for (uint32_t hi = 0; hi <= nh; hi++) {
       const uint32_t h = s_hard[hi];
       // plain accesses in [pos, h): stamp (time, vobj) from the owner's state
@@ -1161,6 +1182,7 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
           }
       }
       __syncthreads();
+      pf.lap(0);
       if (h < cnt) {
         const uint32_t e = s_e[h], to = s_to[h];
         const uint32_t kd = ev_kind(to);
@@ -1171,6 +1193,7 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
           } else {
             do_barrier(a, to, tr.instr[e], s_acc);
           }
+          pf.lap(1);
         } else if (kd == GW_K_END) {
           if (threadIdx.x == 0) {
             const uint32_t t = ev_tid(to);
@@ -1190,14 +1213,20 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
             __syncthreads();
           } else {
             tickets_wait(a, e);
+            pf.lap(2);
             if (kd == GW_K_ACQUIRE) do_acquire(a, e, to, lock);
             else do_release(a, e, to, lock);
             tickets_release(a, e);
+            pf.lap(kd == GW_K_ACQUIRE ? 3 : 4);
+            if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 8 + 7]++;
           }
         } else {  // in-CS access
           tickets_wait(a, e);
+          pf.lap(2);
           do_incs_access(a, e, to, tr.key[e]);
           tickets_release(a, e);
+          pf.lap(5);
+          if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 8 + 7]++;
         }
       }
       pos = h + 1;
