@@ -240,9 +240,9 @@ struct Pipeline {
     uint32_t* va = C->get<uint32_t>(t + "_va", n);
     SortScratch sc;
     const int npass = rs_passes(nbits);
-    sc.ghist = zeroed(kRsMaxPass * 1024);
+    sc.ghist = zeroed(kRsMaxPass * kRsDigits);
     sc.ctrs = zeroed(npass);
-    sc.status = C->get<unsigned long long>("rs_status", std::max(lb_tiles(n), lb_tiles(tr.n)) * 1024);
+    sc.status = C->get<unsigned long long>("rs_status", std::max(lb_tiles(n), lb_tiles(tr.n)) * kRsDigits);
     bool alt = radix_sort<K>(keys, ka, vals, va, n, nbits, sc, take_epochs(npass), st);
     if (alt) {
       keys = ka;
@@ -335,7 +335,7 @@ struct Pipeline {
     CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
     if (gmode) {  // fixed epochs in the graph: start from clean flags
       uint32_t* f = C->get<uint32_t>("lb_flag", lb_tiles(N));
-      unsigned long long* rs = C->get<unsigned long long>("rs_status", lb_tiles(N) * 1024);
+      unsigned long long* rs = C->get<unsigned long long>("rs_status", lb_tiles(N) * kRsDigits);
       CK(cudaMemsetAsync(f, 0, C->bufs["lb_flag"].cap, st));
       CK(cudaMemsetAsync(rs, 0, C->bufs["rs_status"].cap, st));
     }

@@ -210,172 +210,151 @@ void scan_lb(Load load, Store store, uint64_t n, T* agg, T* inc, uint32_t* flag,
 }
 
 // --------------------------------------------------------- radix sort ----
+// One-sweep LSD radix sort of (u32|u64 key, u32 value), 8-bit digits: one
+// histogram kernel for every pass up front, then ONE kernel per pass whose
+// tiles chain their per-digit counts through decoupled look-back (status word
+// = epoch:24 | state:2 | count:38; thread d of a tile owns digit d).  Each
+// tile ranks its 4096 items stably in one sweep (per-warp digit counters,
+// warp peers found with 8 ballots), stages them in shared memory in digit
+// order and writes every digit run with consecutive threads -> coalesced
+// stores.  Global traffic per pass: the keys + values read once and written
+// once, + 2 KB of status per tile.
 constexpr int kRsWarps = kThreads / 32;
 constexpr int kRsPerWarp = kTile / kRsWarps;      // 512
 constexpr int kRsRounds = kRsPerWarp / 32;        // 16
-
-// One-sweep LSD radix sort: one histogram kernel for every pass up front,
-// then ONE kernel per pass (RB = 8 or 10 bit digits) whose tiles chain their
-// per-digit counts through decoupled look-back (status word = epoch:24 |
-// state:2 | count:38).  Each tile ranks its 4096 items stably (warp-private
-// counters + __match_any_sync), stages them in shared memory in digit order
-// and writes every digit run with consecutive threads -> coalesced stores.
+constexpr int kRsBits = 8;
+constexpr int kRsDigits = 1 << kRsBits;           // 256 = kThreads: one digit per thread
 constexpr int kRsMaxPass = 8;
+static_assert(kRsDigits == kThreads, "one digit per thread");
 
-template <class K, int RB>
+template <class K>
 __global__ void __launch_bounds__(kThreads) k_rs_ghist(const K* __restrict__ keys, uint64_t n, int npass,
                                                       uint32_t* __restrict__ ghist) {
-  constexpr int ND = 1 << RB;
-  __shared__ uint32_t h[kRsMaxPass * ND];
-  for (int i = threadIdx.x; i < npass * ND; i += kThreads) h[i] = 0;
+  __shared__ uint32_t h[kRsMaxPass * kRsDigits];
+  for (int i = threadIdx.x; i < npass * kRsDigits; i += kThreads) h[i] = 0;
   __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = keys[i];
-    for (int p = 0; p < npass; p++) atomicAdd(&h[p * ND + ((uint32_t)(k >> (RB * p)) & (ND - 1))], 1u);
+    for (int p = 0; p < npass; p++) atomicAdd(&h[p * kRsDigits + ((uint32_t)(k >> (kRsBits * p)) & (kRsDigits - 1))], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < npass * ND; i += kThreads)
+  for (int i = threadIdx.x; i < npass * kRsDigits; i += kThreads)
     if (h[i]) atomicAdd(&ghist[i], h[i]);
 }
 
-template <class K, int RB>
+template <class K>
 struct RsSmem {
-  static constexpr int ND = 1 << RB;
-  uint32_t wc[kRsWarps][ND];  // per-warp digit counts -> per-warp offsets within the digit
-  uint32_t toff[ND];          // tile-local start of digit d
-  uint32_t gbase[ND];         // global start of this tile's digit-d run
+  uint32_t wc[kRsWarps][kRsDigits];  // per-warp digit counts -> per-warp offsets within the digit
+  uint32_t toff[kRsDigits];          // tile-local start of digit d
+  uint32_t gbase[kRsDigits];         // global start of this tile's digit-d run
   K sk[kTile];
   uint32_t sv[kTile];
   uint32_t tile;
 };
 
-template <class K, int RB>
-__global__ void __launch_bounds__(kThreads) k_rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                         K* __restrict__ kout, uint32_t* __restrict__ vout, uint64_t n,
-                                                         int pass, const uint32_t* __restrict__ ghist,
-                                                         unsigned long long* status, uint32_t* ctr, uint32_t epoch) {
-  constexpr int ND = 1 << RB;
-  constexpr int DPT = ND / kThreads;  // digits per thread
+// lanes with the same digit (NB low bits of d) among the warp's lanes
+template <int NB>
+__device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
+  uint32_t peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < NB; b++) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
+template <class K>
+__global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                            K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                            uint64_t n, int pass, const uint32_t* __restrict__ ghist,
+                                                            unsigned long long* status, uint32_t* ctr, uint32_t epoch) {
+  constexpr int ND = kRsDigits;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  RsSmem<K, RB>& S = *reinterpret_cast<RsSmem<K, RB>*>(smem_raw);
+  RsSmem<K>& S = *reinterpret_cast<RsSmem<K>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int shift = RB * pass;
+  const int shift = kRsBits * pass;
   for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
   if (threadIdx.x == 0) S.tile = atomicAdd(ctr, 1u);
   __syncthreads();
   const uint32_t tile = S.tile;
   const uint64_t tbase = (uint64_t)tile * kTile;
   const uint64_t wbase = tbase + (uint64_t)w * kRsPerWarp;
+  const bool full = tbase + kTile <= n;
   K kk[kRsRounds];
   uint32_t vv[kRsRounds];
-  uint32_t dd[kRsRounds];
+  uint32_t rd[kRsRounds];  // rank within the warp's digit run (bits 0-15) | digit (bits 16-24, 256 = none)
 #pragma unroll
   for (int r = 0; r < kRsRounds; r++) {
     const uint64_t i = wbase + (uint64_t)r * 32 + lane;
-    const bool ok = i < n;
+    const bool ok = full || i < n;
     kk[r] = ok ? kin[i] : (K)0;
     vv[r] = ok ? vin[i] : 0u;
-    dd[r] = ok ? ((uint32_t)(kk[r] >> shift) & (ND - 1)) : (uint32_t)ND;
+    rd[r] = ok ? (((uint32_t)(kk[r] >> shift) & (ND - 1)) << 16) : ((uint32_t)ND << 16);
   }
+  // stable ranks within the warp: rounds in order, lanes in order
+  const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int r = 0; r < kRsRounds; r++) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, dd[r]);
-    const int leader = __ffs(peers) - 1;
-    if (lane == leader && dd[r] < (uint32_t)ND) S.wc[w][dd[r]] += __popc(peers);
+    const uint32_t d = rd[r] >> 16;
+    const uint32_t peers = full ? warp_peers<kRsBits>(d) : warp_peers<kRsBits + 1>(d);
+    const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
+    __syncwarp();
+    if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+    rd[r] |= before + __popc(peers & lt);
     __syncwarp();
   }
   __syncthreads();
   {
-    // thread t owns digits [t*DPT, (t+1)*DPT): global prefix, tile prefix, per-warp offsets
-    uint32_t g[DPT], c[DPT];
-    uint32_t gsum = 0, csum = 0;
+    // thread d owns digit d: per-warp offsets, tile count, look-back, global base
+    const int d = threadIdx.x;
+    uint32_t run = 0;
 #pragma unroll
-    for (int j = 0; j < DPT; j++) {
-      const int d = threadIdx.x * DPT + j;
-      g[j] = ghist[pass * ND + d];
-      uint32_t run = 0;
-#pragma unroll
-      for (int ww = 0; ww < kRsWarps; ww++) {
-        const uint32_t t = S.wc[ww][d];
-        S.wc[ww][d] = run;
-        run += t;
-      }
-      c[j] = run;
-      gsum += g[j];
-      csum += c[j];
+    for (int ww = 0; ww < kRsWarps; ww++) {
+      const uint32_t t = S.wc[ww][d];
+      S.wc[ww][d] = run;
+      run += t;
     }
-    uint32_t gt, ct;
-    uint32_t gex = block_excl_scan<uint32_t, OpSum>(gsum, OpSum(), 0u, &gt);
-    uint32_t cex = block_excl_scan<uint32_t, OpSum>(csum, OpSum(), 0u, &ct);
+    const uint32_t c = run;
     const unsigned long long EP = (unsigned long long)epoch << 40;
-#pragma unroll
-    for (int j = 0; j < DPT; j++) {
-      const int d = threadIdx.x * DPT + j;
-      S.toff[d] = cex;
-      unsigned long long* my = &status[(uint64_t)tile * ND + d];
-      unsigned long long pre = 0;
-      if (tile == 0) {
-        atomicExch(my, EP | (2ull << 38) | c[j]);
-      } else {
-        atomicExch(my, EP | (1ull << 38) | c[j]);
-        int64_t p = (int64_t)tile - 1;
-        constexpr int B8 = 8;
-        while (true) {
-          unsigned long long sv[B8];
-          int lim;
-          bool ready;
-          do {  // up to 8 predecessors per round trip; retry until the needed ones are published
-#pragma unroll
-            for (int k = 0; k < B8; k++)
-              sv[k] = (p - k >= 0) ? ld_volatile_u64(&status[(uint64_t)(p - k) * ND + d]) : (EP | (2ull << 38));
-            lim = B8 - 1;
-#pragma unroll
-            for (int k = B8 - 1; k >= 0; k--)
-              if ((sv[k] >> 40) == epoch && ((sv[k] >> 38) & 3ull) == 2ull) lim = k;
-            ready = true;
-#pragma unroll
-            for (int k = 0; k < B8; k++)
-              if (k <= lim && (sv[k] >> 40) != epoch) ready = false;
-          } while (!ready);
-          bool found = false;
-#pragma unroll
-          for (int k = 0; k < B8; k++) {
-            if (k <= lim && !found) {
-              pre += sv[k] & ((1ull << 38) - 1);
-              if (((sv[k] >> 38) & 3ull) == 2ull) found = true;
-            }
-          }
-          if (found) break;
-          p -= B8;
-        }
-        atomicExch(my, EP | (2ull << 38) | (pre + c[j]));
+    unsigned long long* my = &status[(uint64_t)tile * ND + d];
+    atomicExch(my, EP | ((tile == 0 ? 2ull : 1ull) << 38) | c);
+    const uint32_t g = ghist[pass * ND + d];
+    uint32_t gt, ct;
+    const uint32_t gex = block_excl_scan<uint32_t, OpSum>(g, OpSum(), 0u, &gt);
+    const uint32_t cex = block_excl_scan<uint32_t, OpSum>(c, OpSum(), 0u, &ct);
+    S.toff[d] = cex;
+    unsigned long long pre = 0;
+    if (tile > 0) {
+      int64_t p = (int64_t)tile - 1;
+      while (true) {
+        unsigned long long sv;
+        do { sv = ld_volatile_u64(&status[(uint64_t)p * ND + d]); } while ((sv >> 40) != epoch);
+        pre += sv & ((1ull << 38) - 1);
+        if (((sv >> 38) & 3ull) == 2ull) break;
+        p--;
       }
-      S.gbase[d] = gex + (uint32_t)pre;
-      gex += g[j];
-      cex += c[j];
+      atomicExch(my, EP | (2ull << 38) | (pre + c));
     }
+    S.gbase[d] = gex + (uint32_t)pre;
   }
   __syncthreads();
-  // stable rank -> stage in digit order
-  const uint32_t lt = lanemask_lt();
+  // stage in digit order
 #pragma unroll
   for (int r = 0; r < kRsRounds; r++) {
-    const uint32_t d = dd[r];
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const int leader = __ffs(peers) - 1;
+    const uint32_t d = rd[r] >> 16;
     if (d < (uint32_t)ND) {
-      const uint32_t pos = S.toff[d] + S.wc[w][d] + __popc(peers & lt);
+      const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
       S.sk[pos] = kk[r];
       S.sv[pos] = vv[r];
     }
-    __syncwarp();
-    if (lane == leader && d < (uint32_t)ND) S.wc[w][d] += __popc(peers);
-    __syncwarp();
   }
   __syncthreads();
   // coalesced write-out: consecutive threads write consecutive slots of a digit run
   const uint64_t rem = n > tbase ? n - tbase : 0ull;
   const uint32_t cnt = rem < (uint64_t)kTile ? (uint32_t)rem : (uint32_t)kTile;
+#pragma unroll 4
   for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
     const K k = S.sk[i];
     const uint32_t d = (uint32_t)(k >> shift) & (ND - 1);
@@ -391,40 +370,16 @@ struct SortScratch {
   uint32_t* ctrs;               // one zeroed counter per pass
 };
 
-template <class K, int RB>
+template <class K>
 inline void rs_setup() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(k_rs_onesweep<K, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(RsSmem<K, RB>));
+    cudaFuncSetAttribute(k_rs_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RsSmem<K>));
     done = true;
   }
 }
 
-// digit width: 10-bit digits when they save a pass
-inline int rs_radix_bits(int nbits) { return ((nbits + 9) / 10 < (nbits + 7) / 8) ? 10 : 8; }
-inline int rs_passes(int nbits) { int rb = rs_radix_bits(nbits); return (nbits + rb - 1) / rb; }
-
-template <class K, int RB>
-bool radix_sort_rb(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint64_t n, int nbits, SortScratch sc,
-                   uint32_t epoch, cudaStream_t st) {
-  rs_setup<K, RB>();
-  const int npass = (nbits + RB - 1) / RB;
-  const uint64_t nt = lb_tiles(n);
-  GW_LAUNCH((k_rs_ghist<K, RB>), (unsigned)std::min<uint64_t>(nt, 148ull * 8), kThreads, 0, st, keys, n, npass,
-            sc.ghist);
-  bool alt = false;
-  for (int p = 0; p < npass; p++) {
-    const K* ki = alt ? keys_alt : keys;
-    const uint32_t* vi = alt ? vals_alt : vals;
-    K* ko = alt ? keys : keys_alt;
-    uint32_t* vo = alt ? vals : vals_alt;
-    GW_LAUNCH((k_rs_onesweep<K, RB>), (unsigned)nt, kThreads, sizeof(RsSmem<K, RB>), st, ki, vi, ko, vo, n, p,
-              sc.ghist, sc.status, sc.ctrs + p, epoch + (uint32_t)p);
-    alt = !alt;
-  }
-  return alt;
-}
+inline int rs_passes(int nbits) { return (nbits + kRsBits - 1) / kRsBits; }
 
 // Sorts (keys, vals) by key bits [0, nbits); returns true if the result is in
 // the alternate buffers.  ghist must be zeroed by the caller.
@@ -432,9 +387,21 @@ template <class K>
 bool radix_sort(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint64_t n, int nbits, SortScratch sc,
                 uint32_t epoch, cudaStream_t st) {
   if (n <= 1 || nbits <= 0) return false;
-  if (rs_radix_bits(nbits) == 10)
-    return radix_sort_rb<K, 10>(keys, keys_alt, vals, vals_alt, n, nbits, sc, epoch, st);
-  return radix_sort_rb<K, 8>(keys, keys_alt, vals, vals_alt, n, nbits, sc, epoch, st);
+  rs_setup<K>();
+  const int npass = rs_passes(nbits);
+  const uint64_t nt = lb_tiles(n);
+  GW_LAUNCH((k_rs_ghist<K>), (unsigned)std::min<uint64_t>(nt, 148ull * 8), kThreads, 0, st, keys, n, npass, sc.ghist);
+  bool alt = false;
+  for (int p = 0; p < npass; p++) {
+    const K* ki = alt ? keys_alt : keys;
+    const uint32_t* vi = alt ? vals_alt : vals;
+    K* ko = alt ? keys : keys_alt;
+    uint32_t* vo = alt ? vals : vals_alt;
+    GW_LAUNCH((k_rs_onesweep<K>), (unsigned)nt, kThreads, sizeof(RsSmem<K>), st, ki, vi, ko, vo, n, p, sc.ghist,
+              sc.status, sc.ctrs + p, epoch + (uint32_t)p);
+    alt = !alt;
+  }
+  return alt;
 }
 
 }  // namespace gw
