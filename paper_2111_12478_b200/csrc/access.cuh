@@ -468,98 +468,24 @@ __global__ void k_dedup_insert(DedupArgs d) {
     atomicMin(&d.smin[h], d.c.okey[k]);
   }
 }
-// Report order.  Survivors are bucketed by their current event c (order key
-// bits 63..32) with a counting sort -- counts, one scan over the N events,
-// placement with self-cleaning atomics -- and the few survivors sharing a c
-// (same-instruction pairs of one record, the readers of one write) are then
-// ordered by the low 32 key bits.
-__global__ void k_dedup_count(DedupArgs d, uint32_t* ccnt, uint32_t* nsurv) {
-  uint32_t cnt = 0;
+// Report order: every candidate gets its order key if it is the keep-first
+// survivor of its dedup slot, else a key past every event (sorted last); one
+// radix sort of the candidates then yields the survivors in report order.
+__global__ void k_dedup_keys(DedupArgs d, unsigned long long n_events, unsigned long long* sk, uint32_t* sv,
+                             uint32_t* nsurv) {
   const uint32_t nc = dd_count(d);
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
-    const unsigned long long ok = d.c.okey[k];
-    if (ok == d.smin[d.cslot[k]]) {
-      atomicAdd(ccnt + (ok >> 32), 1u);
-      cnt++;
+  for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < d.ncand; k0 += gridDim.x * blockDim.x) {
+    const uint32_t k = k0 + threadIdx.x;
+    bool surv = false;
+    unsigned long long key = n_events << 32;
+    if (k < nc) {
+      const unsigned long long ok = d.c.okey[k];
+      surv = ok == d.smin[d.cslot[k]];
+      if (surv) key = ok;
     }
-  }
-  cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nsurv, cnt);
-}
-__global__ void k_dedup_place(DedupArgs d, uint32_t* ccnt, const uint32_t* coff, unsigned long long* sk,
-                              uint32_t* sv) {
-  const uint32_t nc = dd_count(d);
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
-    const unsigned long long ok = d.c.okey[k];
-    if (ok == d.smin[d.cslot[k]]) {
-      const uint32_t c = (uint32_t)(ok >> 32);
-      const uint32_t pos = coff[c] + atomicSub(ccnt + c, 1u) - 1u;  // leaves ccnt zeroed
-      sk[pos] = ok;
-      sv[pos] = k;
-    }
-  }
-}
-constexpr uint32_t kGroupSmall = 64;
-__global__ void k_group_sort(const uint32_t* coff, uint64_t n_events, const uint32_t* nsurv, unsigned long long* sk,
-                             uint32_t* sv, uint32_t* big, uint32_t* nbig) {
-  const uint32_t ns = *nsurv;
-  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_events;
-       c += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t beg = coff[c];
-    const uint32_t end = c + 1 < n_events ? coff[c + 1] : ns;
-    const uint32_t m = end - beg;
-    if (m < 2) continue;
-    if (m > kGroupSmall) {
-      big[atomicAdd(nbig, 1u)] = (uint32_t)c;
-      continue;
-    }
-    for (uint32_t i = beg + 1; i < end; i++) {  // insertion sort by order key
-      const unsigned long long k = sk[i];
-      const uint32_t v = sv[i];
-      uint32_t j = i;
-      while (j > beg && sk[j - 1] > k) { sk[j] = sk[j - 1]; sv[j] = sv[j - 1]; j--; }
-      sk[j] = k;
-      sv[j] = v;
-    }
-  }
-}
-// rare: more than kGroupSmall reports at one event -- CTA-wide bitonic network
-// in its all-ascending form (flip step, then half-cleaners), so the virtual
-// +inf padding beyond the group never moves and comparators past it are skipped
-__device__ __forceinline__ void cswap(unsigned long long* sk, uint32_t* sv, uint32_t i, uint32_t l) {
-  const unsigned long long a = sk[i], b = sk[l];
-  if (a > b) {
-    sk[i] = b; sk[l] = a;
-    const uint32_t t = sv[i]; sv[i] = sv[l]; sv[l] = t;
-  }
-}
-__global__ void __launch_bounds__(kThreads) k_group_sort_big(const uint32_t* coff, uint64_t n_events,
-                                                            const uint32_t* nsurv, unsigned long long* sk,
-                                                            uint32_t* sv, const uint32_t* big, const uint32_t* nbig) {
-  const uint32_t nb = *nbig, ns = *nsurv;
-  for (uint32_t g = blockIdx.x; g < nb; g += gridDim.x) {
-    const uint32_t c = big[g];
-    const uint32_t beg = coff[c];
-    const uint32_t end = c + 1 < n_events ? coff[c + 1] : ns;
-    const uint32_t m = end - beg;
-    uint32_t p2 = 1;
-    while (p2 < m) p2 <<= 1;
-    unsigned long long* k = sk + beg;
-    uint32_t* v = sv + beg;
-    for (uint32_t kk = 2; kk <= p2; kk <<= 1) {
-      for (uint32_t i = threadIdx.x; i < p2; i += kThreads) {
-        const uint32_t l = i ^ (kk - 1);
-        if ((i & (kk >> 1)) == 0 && l < m) cswap(k, v, i, l);
-      }
-      __syncthreads();
-      for (uint32_t jj = kk >> 2; jj > 0; jj >>= 1) {
-        for (uint32_t i = threadIdx.x; i < p2; i += kThreads) {
-          const uint32_t l = i ^ jj;
-          if ((i & jj) == 0 && l < m) cswap(k, v, i, l);
-        }
-        __syncthreads();
-      }
-    }
+    if (k < d.ncand) { sk[k] = key; sv[k] = k; }
+    const uint32_t m = __ballot_sync(0xffffffffu, surv);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(nsurv, (uint32_t)__popc(m));
   }
 }
 __global__ void k_final(Cands c, const uint32_t* svals, const uint32_t* nsurv, uint8_t* okind, uint32_t* oprior,

@@ -222,7 +222,7 @@ struct Pipeline {
     }
     if (C->epoch + k >= (1u << 24)) {  // wrap: clear every flag / status word
       for (auto& kv : C->bufs)
-        if (kv.first == "lb_flag" || kv.first == "rs_status") CK(cudaMemsetAsync(kv.second.p, 0, kv.second.cap, st));
+        if (kv.first == "rs_status") CK(cudaMemsetAsync(kv.second.p, 0, kv.second.cap, st));
       C->epoch = 1;
     }
     uint32_t e = C->epoch;
@@ -251,14 +251,10 @@ struct Pipeline {
   }
 
   template <class T, class Op, class Load, class Store>
-  void scan(Load load, Store store, uint64_t n, Op op, T identity, bool inclusive, const char* tag) {
+  void scan(Load load, Store store, uint64_t n, Op op, T identity, bool inclusive, const char*) {
     if (n == 0) return;
-    std::string t(tag);
-    const uint64_t nt = lb_tiles(n);
-    T* agg = C->get<T>(t + "_agg", nt);
-    T* inc = C->get<T>(t + "_inc", nt);
-    uint32_t* flag = C->get<uint32_t>("lb_flag", std::max<uint64_t>(nt, lb_tiles(tr.n)));
-    scan_lb<T, Op>(load, store, n, agg, inc, flag, zeroed(1), take_epochs(1), op, identity, inclusive, st);
+    unsigned long long* status = C->get<unsigned long long>("lb_status", std::max(lb_tiles(n), lb_tiles(tr.n)));
+    scan_lb<T, Op>(load, store, n, status, zeroed(1), op, identity, inclusive, st);
   }
 
   static KeyRuns key_runs(unsigned long long D) {
@@ -334,9 +330,7 @@ struct Pipeline {
     CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
     CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
     if (gmode) {  // fixed epochs in the graph: start from clean flags
-      uint32_t* f = C->get<uint32_t>("lb_flag", lb_tiles(N));
       unsigned long long* rs = C->get<unsigned long long>("rs_status", lb_tiles(N) * kRsDigits);
-      CK(cudaMemsetAsync(f, 0, C->bufs["lb_flag"].cap, st));
       CK(cudaMemsetAsync(rs, 0, C->bufs["rs_status"].cap, st));
     }
     Stats* dst = C->get<Stats>("stats", 1);
@@ -438,18 +432,11 @@ struct Pipeline {
       CK(cudaMemsetAsync(d.owner, 0, sizeof(uint32_t) * tcap, st));
       CK(cudaMemsetAsync(d.smin, 0xFF, sizeof(unsigned long long) * tcap, st));
       GW_LAUNCH(k_dedup_insert, grid_for(ncap), kThreads, 0, st, d);
+      // survivors ordered by their order key; the others sort last
       unsigned long long* sk = C->get<unsigned long long>("sv_k", ncap);
       uint32_t* sv = C->get<uint32_t>("sv_v", ncap);
-      uint32_t* ccnt = C->get<uint32_t>("sv_cnt", N);
-      CK(cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * N, st));
-      uint32_t* coff = C->get<uint32_t>("sv_off", N);
-      uint32_t* big = C->get<uint32_t>("sv_big", ncap / (kGroupSmall + 1) + 1);
-      uint32_t* nbig = zeroed(1);
-      GW_LAUNCH(k_dedup_count, grid_for(ncap), kThreads, 0, st, d, ccnt, d_nsurv);
-      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{ccnt}, ArrStore<uint32_t>{coff}, N, OpSum(), 0u, false, "sc_u32");
-      GW_LAUNCH(k_dedup_place, grid_for(ncap), kThreads, 0, st, d, ccnt, coff, sk, sv);
-      GW_LAUNCH(k_group_sort, grid_for(N), kThreads, 0, st, coff, N, d_nsurv, sk, sv, big, nbig);
-      GW_LAUNCH(k_group_sort_big, 148u, kThreads, 0, st, coff, N, d_nsurv, sk, sv, big, nbig);
+      GW_LAUNCH(k_dedup_keys, grid_for(ncap), kThreads, 0, st, d, (unsigned long long)N, sk, sv, d_nsurv);
+      sort<unsigned long long>(sk, sv, ncap, 32 + ceil_log2(N + 1), "sv");
       C->d_kind = C->get<uint8_t>("o_kind", ncap);
       C->d_prior = C->get<uint32_t>("o_prior", ncap);
       C->d_cur = C->get<uint32_t>("o_cur", ncap);
@@ -806,18 +793,17 @@ struct Pipeline {
     GW_LAUNCH(k_state_init, grid_for(T), kThreads, 0, st, w);
     if (snap_mode) {
       SnapArgs sa;
-      uint32_t* hflag = C->get<uint32_t>("hd_flag", N);
-      GW_LAUNCH(k_hard_mark, grid_for(N), kThreads, 0, st, tr, hflag);
-      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hflag}, ArrStore<uint32_t>{hflag}, N, OpSum(), 0u, false, "sc_u32");
-      uint32_t* hkey = C->get<uint32_t>("hd_key", n_hard + 1);
       uint32_t* hev = C->get<uint32_t>("hd_ev", n_hard + 1);
       uint32_t* hbeg = C->get<uint32_t>("hd_beg", tr.B);
       uint32_t* hend = C->get<uint32_t>("hd_end", tr.B);
       uint32_t* hcnt = C->get<uint32_t>("hd_cnt", tr.B);
       CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
       if (n_hard) {
-        GW_LAUNCH(k_hard_compact, grid_for(N), kThreads, 0, st, tr, hflag, hkey, hev, hcnt);
-        sort<uint32_t>(hkey, hev, n_hard, ceil_log2(tr.B), "hd");
+        unsigned long long* hkey = C->get<unsigned long long>("hd_key", n_hard + 1);
+        uint32_t* hdummy = C->get<uint32_t>("hd_v", n_hard + 1);
+        GW_LAUNCH(k_hard_append, grid_for(N), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT);
+        sort<unsigned long long>(hkey, hdummy, n_hard, 32 + ceil_log2(tr.B), "hd");
+        GW_LAUNCH(k_hard_unpack, grid_for(n_hard), kThreads, 0, st, hkey, n_hard, hev);
       }
       scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hcnt}, HardSegStore{hcnt, hbeg, hend}, tr.B, OpSum(), 0u, false,
                             "sc_u32");

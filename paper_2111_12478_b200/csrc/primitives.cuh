@@ -101,10 +101,10 @@ struct ArrStore {
 
 // ------------------------------------------------ single-pass scan ----
 // Decoupled look-back (chained) scan: one launch, tiles taken in launch order
-// from an atomic counter, each tile publishes its aggregate and then its
-// inclusive prefix; flags carry a per-call epoch so nothing needs clearing.
-constexpr uint32_t LB_AGG = 1u, LB_INC = 2u;
-
+// from an atomic counter; each tile publishes its aggregate, then its
+// inclusive prefix, as ONE 64-bit word (state:2 | payload:62), so a
+// predecessor's state and value are read together with no memory fences.
+// The status words are zeroed (state 0 = not ready) before every launch.
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
   return *(volatile const uint32_t*)p;
 }
@@ -112,10 +112,28 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
   return *(volatile const unsigned long long*)p;
 }
 
+// payload packing (62 bits)
+template <class T>
+struct LbPack;
+template <>
+struct LbPack<uint32_t> {
+  __device__ __forceinline__ static unsigned long long pack(uint32_t v) { return v; }
+  __device__ __forceinline__ static uint32_t unpack(unsigned long long w) { return (uint32_t)w; }
+};
+template <>
+struct LbPack<uint2> {  // two values < 2^31 (positions + 1)
+  __device__ __forceinline__ static unsigned long long pack(uint2 v) {
+    return (unsigned long long)v.x | ((unsigned long long)v.y << 31);
+  }
+  __device__ __forceinline__ static uint2 unpack(unsigned long long w) {
+    return make_uint2((uint32_t)(w & 0x7FFFFFFFull), (uint32_t)((w >> 31) & 0x7FFFFFFFull));
+  }
+};
+constexpr unsigned long long LB_AGG = 1ull << 62, LB_INC = 2ull << 62, LB_PAY = (1ull << 62) - 1;
+
 template <class T, class Op, class Load, class Store>
-__global__ void __launch_bounds__(kThreads) k_scan_lb(Load load, Store store, uint64_t n, T* agg, T* inc,
-                                                     uint32_t* flag, uint32_t* ctr, uint32_t epoch, Op op,
-                                                     T identity, int inclusive) {
+__global__ void __launch_bounds__(kThreads) k_scan_lb(Load load, Store store, uint64_t n, unsigned long long* status,
+                                                     uint32_t* ctr, Op op, T identity, int inclusive) {
   __shared__ uint32_t s_tile;
   __shared__ T s_pre;
   __shared__ T s_buf[kTile];
@@ -124,10 +142,15 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(Load load, Store store, ui
   const uint32_t tile = s_tile;
   const uint64_t base = (uint64_t)tile * kTile;
   // striped (coalesced) load -> smem -> blocked per thread
+  {
+    T x[kItems];
 #pragma unroll
-  for (int k = 0; k < kItems; k++) {
-    const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
-    s_buf[k * kThreads + threadIdx.x] = i < n ? load(i) : identity;
+    for (int k = 0; k < kItems; k++) {
+      const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+      x[k] = i < n ? load(i) : identity;
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; k++) s_buf[k * kThreads + threadIdx.x] = x[k];
   }
   __syncthreads();
   T v[kItems];
@@ -142,26 +165,22 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(Load load, Store store, ui
   if (threadIdx.x < 32) {
     // warp-wide decoupled look-back: 32 predecessors per round trip
     const int lane = threadIdx.x;
-    if (lane == 0) {
-      if (tile == 0) inc[0] = tot; else agg[tile] = tot;
-      __threadfence();
-      atomicExch(&flag[tile], (epoch << 2) | (tile == 0 ? LB_INC : LB_AGG));
-    }
+    if (lane == 0)
+      atomicExch(&status[tile], (tile == 0 ? LB_INC : LB_AGG) | LbPack<T>::pack(tot));
     T pre = identity;
     if (tile > 0) {
       int64_t p = (int64_t)tile - 1;
       while (true) {
         const int64_t q = p - lane;
-        uint32_t f = (epoch << 2) | LB_INC;  // q < 0: virtual inclusive identity
+        unsigned long long wv = LB_INC;  // q < 0: virtual inclusive identity
         if (q >= 0) {
-          do { f = ld_volatile_u32(&flag[q]); } while ((f >> 2) != epoch);
+          do { wv = ld_volatile_u64(&status[q]); } while ((wv >> 62) == 0ull);
         }
-        __threadfence();
-        const bool isinc = (f & 3u) == LB_INC;
+        const bool isinc = (wv >> 62) == 2ull;
         const uint32_t incm = __ballot_sync(0xffffffffu, isinc);
         const int lim = __ffs(incm) - 1;  // nearest inclusive predecessor (incm != 0 once q < 0)
         T val = identity;
-        if (q >= 0 && (incm == 0 || lane <= lim)) val = isinc ? __ldcg(&inc[q]) : __ldcg(&agg[q]);
+        if (q >= 0 && (incm == 0 || lane <= lim)) val = LbPack<T>::unpack(wv & LB_PAY);
         // reduce lanes 0..lim (commutative ops: sum, max)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -173,11 +192,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(Load load, Store store, ui
         if (incm) break;
         p -= 32;
       }
-      if (lane == 0) {
-        inc[tile] = op(pre, tot);
-        __threadfence();
-        atomicExch(&flag[tile], (epoch << 2) | LB_INC);
-      }
+      if (lane == 0) atomicExch(&status[tile], LB_INC | LbPack<T>::pack(op(pre, tot)));
     }
     if (lane == 0) s_pre = pre;
   }
@@ -197,16 +212,17 @@ __global__ void __launch_bounds__(kThreads) k_scan_lb(Load load, Store store, ui
   }
 }
 
-// scratch for scan_lb: agg/inc hold lb_tiles(n) elements of T, flag lb_tiles(n) u32
+// scratch for scan_lb: lb_tiles(n) status words (zeroed here) + a zeroed tile counter
 inline uint64_t lb_tiles(uint64_t n) { return (n + kTile - 1) / kTile; }
 
 template <class T, class Op, class Load, class Store>
-void scan_lb(Load load, Store store, uint64_t n, T* agg, T* inc, uint32_t* flag, uint32_t* ctr, uint32_t epoch,
-             Op op, T identity, bool inclusive, cudaStream_t st) {
+void scan_lb(Load load, Store store, uint64_t n, unsigned long long* status, uint32_t* ctr, Op op, T identity,
+             bool inclusive, cudaStream_t st) {
   if (n == 0) return;
   const uint64_t nt = lb_tiles(n);
-  GW_LAUNCH((k_scan_lb<T, Op, Load, Store>), (unsigned)nt, kThreads, 0, st, load, store, n, agg, inc, flag, ctr, epoch,
-            op, identity, (int)inclusive);
+  cudaMemsetAsync(status, 0, sizeof(unsigned long long) * nt, st);
+  GW_LAUNCH((k_scan_lb<T, Op, Load, Store>), (unsigned)nt, kThreads, 0, st, load, store, n, status, ctr, op, identity,
+            (int)inclusive);
 }
 
 // --------------------------------------------------------- radix sort ----

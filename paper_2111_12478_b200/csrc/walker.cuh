@@ -1301,24 +1301,37 @@ __global__ void __launch_bounds__(kThreads) k_stamp(WalkArgs a, SnapArgs s) {
   }
 }
 
-__global__ void k_hard_mark(DevTrace tr, uint32_t* flag) {
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = ev_kind(tr.tidop[e]);
-    flag[e] = (k == GW_K_BARRIER || k == GW_K_END) ? 1u : 0u;
-  }
-}
-__global__ void k_hard_compact(DevTrace tr, const uint32_t* pos, uint32_t* hkey, uint32_t* hev, uint32_t* hcnt) {
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t to = tr.tidop[e];
-    const uint32_t k = ev_kind(to);
-    if (k == GW_K_BARRIER || k == GW_K_END) {
-      const uint32_t p = pos[e];
+// hard events (barriers, ENDs) of a lock-free trace: appended in any order as
+// (block << 32 | event) keys with warp-aggregated atomics, then sorted, which
+// orders them by block and by trace order within a block
+__global__ void k_hard_append(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
+                              const uint32_t* abort_flag) {
+  if (*(volatile const uint32_t*)abort_flag) return;  // graph mode: the plan does not fit this trace
+  for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x; e0 < tr.n; e0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = e0 + threadIdx.x;
+    bool hard = false;
+    uint32_t to = 0;
+    if (e < tr.n) {
+      to = tr.tidop[e];
+      const uint32_t k = ev_kind(to);
+      hard = k == GW_K_BARRIER || k == GW_K_END;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, hard);
+    if (!m) continue;
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(ntop, (uint32_t)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (hard) {
       const uint32_t b = ev_tid(to) / tr.BS;
-      hkey[p] = b;
-      hev[p] = (uint32_t)e;
+      hkey[base + __popc(m & lanemask_lt())] = ((unsigned long long)b << 32) | (uint32_t)e;
       atomicAdd(hcnt + b, 1u);
     }
   }
+}
+__global__ void k_hard_unpack(const unsigned long long* hkey, uint64_t n, uint32_t* hev) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    hev[i] = (uint32_t)hkey[i];
 }
 // exclusive scan of per-block hard-event counts -> [beg, end)
 struct HardSegStore {
