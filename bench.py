@@ -9,8 +9,11 @@ call with HOST buffers (pinned H2D of the SoA and D2H of the reports inside
 the timed region).  L2 is flushed (256 MiB write) before every timed step;
 each step is timed with CUDA events on the launching stream and the K step
 times are summed.  For N > 1 (torchrun, one rank per GPU) every rank analyses
-its own trace (independent objects: weak scaling, no data-path collective);
-the time is the max over ranks.
+its own trace (independent objects: weak scaling, no data-path collective),
+except the C5 scaling sweep (``--workload c5``, or ``--mode sharded``): one
+trace, address-sharded -- every rank holds the whole trace and reports the
+races on one contiguous location-key range, then an NCCL gather + order-key
+merge on rank 0 (strong scaling).  The time is the max over ranks.
 
 ``--impl reference`` times the CPU restatement of the reference (oracle/,
 single-threaded like the reference) on this host: rank 0 only.
@@ -91,14 +94,15 @@ def workload_desc(name, p, n, n_acc):
     return d
 
 
-def make_workload(name: str, rank: int, dev):
+def make_workload(name: str, rank: int, dev, sharded: bool = False):
     """Generate the workload trace directly in HBM (device generators; identical
     to paper_2111_12478_b200.workloads.c2_soa / c4_text for the same parameters)."""
     import torch
     from paper_2111_12478_b200 import _native as N
 
     p = dict(WORKLOADS[name])
-    p["seed"] += rank
+    if not sharded:  # replicas: every rank analyses its own trace; sharded: one trace, split by address
+        p["seed"] += rank
     n, n_acc = workload_events(p)
     key_d = torch.empty(n, dtype=torch.int64, device=dev)
     to_d = torch.empty(n, dtype=torch.int32, device=dev)
@@ -315,18 +319,27 @@ def run_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
+    # GW_BENCH_SAME_GPU=1 (test only): every rank on cuda:0 with gloo, to exercise N>1 on a 1-GPU box
+    same_gpu = os.environ.get("GW_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if same_gpu else "nccl")
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    coll_dev = None if same_gpu else dev
 
     from paper_2111_12478_b200 import _native as N
+    from paper_2111_12478_b200.shard import gather_reports
 
-    cfg, n, n_acc, (key_d, to_d, in_d), desc = make_workload(args.workload, rank, dev)
+    mode = args.mode or ("sharded" if args.workload == "c5" else "replicas")
+    sharded = mode == "sharded" and world > 1
+    shard = (rank, world) if sharded else (0, 1)
+    cfg, n, n_acc, (key_d, to_d, in_d), desc = make_workload(args.workload, rank, dev, sharded=sharded)
     # pinned host copy of the same trace for the end-to-end leg
     key_h = torch.empty(n, dtype=torch.int64, pin_memory=True)
     to_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
@@ -340,14 +353,22 @@ def run_b200(args):
     sptr = stream.cuda_stream
     ctx = N.Context(local)
 
+    def finish():
+        res = ctx.fetch()
+        if not sharded:
+            return res
+        merged = gather_reports(res, device=coll_dev)  # NCCL: every shard's reports to rank 0, merged by order key
+        return merged if merged is not None else res
+
     def step_device(eager=False):
-        ctx.analyze_device(cfg, n, key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), stream=sptr, eager=eager)
-        return ctx.fetch()
+        ctx.analyze_device(cfg, n, key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), stream=sptr, eager=eager,
+                           shard=shard)
+        return finish()
 
     def step_host():
         ctx.analyze_host(cfg, key_h.numpy().view(np.uint64), to_h.numpy().view(np.uint32),
-                         in_h.numpy().view(np.uint32), stream=sptr)
-        return ctx.fetch()
+                         in_h.numpy().view(np.uint32), stream=sptr, shard=shard)
+        return finish()
 
     def timed(fn, steps):
         tot = 0.0
@@ -372,7 +393,7 @@ def run_b200(args):
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev or "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -404,7 +425,7 @@ def run_b200(args):
             dist.destroy_process_group()
         return
 
-    total_events = n * world * args.steps
+    total_events = n * (1 if sharded else world) * args.steps
     value = total_events / (ms_dev / 1000.0)
     e2e = total_events / (ms_e2e / 1000.0)
     peak, peak_kind = load_peaks()
@@ -421,11 +442,14 @@ def run_b200(args):
         "warmup": args.warmup,
         "ms_per_step": ms_dev / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic",
-        "config": dict(desc, reports=n_rep, parallelism=f"replicas x{world}",
+        "config": dict(desc, reports=n_rep,
+                       parallelism=(f"address-sharded x{world} (location-key ranges; replicated sync pass; "
+                                    f"NCCL gather + order-key merge of the reports)") if sharded
+                       else f"replicas x{world}",
                        l2="flushed before every timed step (256 MiB write)"),
         "e2e": {
             "value": e2e,
@@ -467,6 +491,8 @@ def main():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", choices=["replicas", "sharded"], default=None,
+                    help="N>1: independent traces per GPU (default; c5: address-sharded one trace)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -94,6 +94,15 @@ typedef struct gw_opts {
   uint32_t inactive_opt; /* GwcpDetector(inactive_opt=...), gwcp.py:108-127 */
   uint32_t flags;        /* GW_OPT_* */
   void* stream;          /* cudaStream_t to launch on (NULL = legacy default; never graph-replayed) */
+  /* Address sharding (multi-GPU): this call reports only the races whose
+   * location lies in contiguous location-key range shard_index of
+   * shard_count (0 or 1 = unsharded).  Every shard holds the whole trace and
+   * runs the sync pass; dedup is shard-local because the dedup key contains
+   * the location (report.py:93), so concatenating the shards' reports and
+   * ordering them by order_key gives the unsharded result (report 0 is the
+   * global "first"). */
+  uint32_t shard_index;
+  uint32_t shard_count;
 } gw_opts;
 
 typedef struct gw_result { /* library-owned; reports in final order */
@@ -105,6 +114,7 @@ typedef struct gw_result { /* library-owned; reports in final order */
   uint32_t* diag_event;
   uint32_t* diag_code;     /* GW_D_* */
   uint64_t* diag_lock;     /* lock id (EXIT_HOLDING: one entry per held frame, bottom->top) */
+  uint64_t* order_key;     /* per report: (record-head or current event) << 32 | sub-order; increasing */
 } gw_result;
 
 typedef struct gw_stats { /* per-phase device times of the last analysis (ms) */

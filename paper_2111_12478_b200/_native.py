@@ -64,7 +64,8 @@ class _View(C.Structure):
 
 
 class _Opts(C.Structure):
-    _fields_ = [("inactive_opt", C.c_uint32), ("flags", C.c_uint32), ("stream", C.c_void_p)]
+    _fields_ = [("inactive_opt", C.c_uint32), ("flags", C.c_uint32), ("stream", C.c_void_p),
+                ("shard_index", C.c_uint32), ("shard_count", C.c_uint32)]
 
 
 class _Result(C.Structure):
@@ -77,6 +78,7 @@ class _Result(C.Structure):
         ("diag_event", C.POINTER(C.c_uint32)),
         ("diag_code", C.POINTER(C.c_uint32)),
         ("diag_lock", C.POINTER(C.c_uint64)),
+        ("order_key", C.POINTER(C.c_uint64)),
     ]
 
 
@@ -256,6 +258,7 @@ def _take_result(L, r: _Result):
             "diag_event": arr(r.diag_event, nd, np.uint32),
             "diag_code": arr(r.diag_code, nd, np.uint32),
             "diag_lock": arr(r.diag_lock, nd, np.uint64),
+            "order_key": arr(r.order_key, n, np.uint64),
         }
     finally:
         L.gw_result_free(C.byref(r))
@@ -282,18 +285,21 @@ class Context:
         except Exception:
             pass
 
-    def analyze_host(self, cfg, key, tidop, instr, *, inactive_opt=True, stream=None, eager=False) -> None:
+    def analyze_host(self, cfg, key, tidop, instr, *, inactive_opt=True, stream=None, eager=False,
+                     shard=(0, 1)) -> None:
         v = _view(cfg, key, tidop, instr)
-        o = _Opts(1 if inactive_opt else 0, OPT_EAGER if eager else 0, stream)
+        o = _Opts(1 if inactive_opt else 0, OPT_EAGER if eager else 0, stream, shard[0], shard[1])
         _check(self._L.gw_ctx_analyze_host(self._c, C.byref(v), C.byref(o)))
 
     def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None,
-                       eager=False) -> None:
+                       eager=False, shard=(0, 1)) -> None:
+        """shard=(index, count): report only races on location-key range `index`
+        of `count` (address sharding; see include/gwcp_b200.h gw_opts)."""
         v = _View()
         v.cfg.blocks, v.cfg.warps, v.cfg.lanes = cfg
         v.n_events = n
         v.key, v.tidop, v.instr = key_ptr, tidop_ptr, instr_ptr
-        o = _Opts(1 if inactive_opt else 0, OPT_EAGER if eager else 0, stream)
+        o = _Opts(1 if inactive_opt else 0, OPT_EAGER if eager else 0, stream, shard[0], shard[1])
         _check(self._L.gw_ctx_analyze_device(self._c, C.byref(v), C.byref(o)))
 
     def fetch(self):

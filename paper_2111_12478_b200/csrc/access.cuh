@@ -56,6 +56,72 @@ __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals) {
   }
 }
 
+// ---- address sharding -----------------------------------------------------
+__device__ __forceinline__ unsigned long long compact_key(unsigned long long x, const KeyRuns& kr) {
+  unsigned long long k = 0;
+#pragma unroll
+  for (int r = 0; r < 4; r++)
+    if (r < kr.n) k |= ((x >> kr.src[r]) & ((kr.width[r] >= 64) ? ~0ull : ((1ull << kr.width[r]) - 1ull))) << kr.dst[r];
+  return k;
+}
+struct ShardArgs {
+  KeyRuns kr;
+  int nloc;        // location bits of the compacted key
+  uint32_t shard;  // this call's shard
+  uint32_t G;      // shard count (1: unsharded)
+};
+// contiguous ranges of the compacted location key
+__device__ __forceinline__ uint32_t shard_of(unsigned long long ck, const ShardArgs& sa) {
+  if (sa.G <= 1 || sa.nloc <= 0) return 0;
+  return (uint32_t)__umul64hi(ck << (64 - sa.nloc), (unsigned long long)sa.G);
+}
+__device__ __forceinline__ bool in_shard(unsigned long long loc, const ShardArgs& sa) {
+  return sa.G <= 1 || shard_of(compact_key(loc, sa.kr), sa) == sa.shard;
+}
+// order-preserving compaction of this shard's accesses (tile = kTile events):
+// count per tile, then (after an exclusive scan of the counts) emit
+// (compacted location key, event) in trace order
+template <class K, bool EMIT>
+__global__ void __launch_bounds__(kThreads) k_shard_accesses(DevTrace tr, ShardArgs sa, uint32_t* tilecnt,
+                                                            const uint32_t* tileoff, K* keys, uint32_t* vals) {
+  __shared__ uint32_t s_w[kThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  const uint64_t ntiles = (tr.n + kTile - 1) / kTile;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t base = tile * kTile;
+    uint32_t run = EMIT ? tileoff[tile] : 0u;
+#pragma unroll 4
+    for (int k = 0; k < kItems; k++) {
+      const uint64_t e = base + (uint64_t)k * kThreads + threadIdx.x;
+      bool in = false;
+      unsigned long long ck = 0;
+      if (e < tr.n && ev_kind(tr.tidop[e]) <= GW_K_WRITE) {
+        ck = compact_key(tr.key[e], sa.kr);
+        in = shard_of(ck, sa) == sa.shard;
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      if (lane == 0) s_w[w] = __popc(m);
+      __syncthreads();
+      uint32_t woff = 0, tot = 0;
+#pragma unroll
+      for (int x = 0; x < kThreads / 32; x++) {
+        const uint32_t c = s_w[x];
+        woff += x < w ? c : 0u;
+        tot += c;
+      }
+      if (EMIT && in) {
+        const uint32_t pos = run + woff + __popc(m & lt);
+        keys[pos] = (K)ck;
+        vals[pos] = (uint32_t)e;
+      }
+      run += tot;
+      __syncthreads();
+    }
+    if (!EMIT && threadIdx.x == 0) tilecnt[tile] = run;
+  }
+}
+
 // compact arbitrary u64 keys to their varying bit runs
 __global__ void k_compact_u64(const unsigned long long* in, uint64_t n, KeyRuns kr, unsigned long long* out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -347,10 +413,11 @@ __device__ __forceinline__ unsigned long long sub_pair(uint64_t i, uint64_t j) {
 }
 // slow path for records longer than 32 events: event j scans its record
 __device__ void same_instr_long(const DevTrace& tr, const Cands& cd, uint64_t head, uint64_t end, uint64_t j,
-                                bool uni) {
+                                bool uni, const ShardArgs& sa) {
   const uint32_t tj = tr.tidop[j];
   if (ev_kind(tj) > GW_K_WRITE) return;
   const unsigned long long lj = tr.key[j];
+  if (!in_shard(lj, sa)) return;
   uint32_t cnt = 0;
   uint64_t first = 0;
   for (uint64_t i = head; i < j; i++) {
@@ -370,7 +437,7 @@ __device__ void same_instr_long(const DevTrace& tr, const Cands& cd, uint64_t he
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd) {
+__global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd, ShardArgs sa) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t wb = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; wb < tr.n; wb += nwarps * 32) {
@@ -410,15 +477,16 @@ __global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd) 
         for (uint64_t c = head + 32 + lane; c < end; c += 32)
           u2 = u2 && rec_uniform_step(tr.tidop[c - 1], tr.tidop[c], tr.instr[c - 1], tr.instr[c], tr.BS);
         uni = __all_sync(0xffffffffu, u2);
-        for (uint64_t j = head + 1 + lane; j < end; j += 32) same_instr_long(tr, cd, head, end, j, uni);
+        for (uint64_t j = head + 1 + lane; j < end; j += 32) same_instr_long(tr, cd, head, end, j, uni, sa);
         continue;
       }
-      const bool acc = lane < len && ev_kind(tx) <= GW_K_WRITE;
+          const bool acc = lane < len && ev_kind(tx) <= GW_K_WRITE;
       const unsigned long long kx = acc ? tr.key[x] : 0ull;
+      const bool mine = in_shard(kx, sa);
       const uint32_t accm = __ballot_sync(0xffffffffu, acc);
       const uint32_t peers = __match_any_sync(0xffffffffu, kx) & accm;
       const uint32_t earlier = peers & lanemask_lt();
-      if (!acc || !earlier) continue;
+      if (!acc || !earlier || !mine) continue;
       if (uni) {
         if (__popc(earlier) != 1) continue;  // not the second occurrence of this location
         const int fl = __ffs(earlier) - 1;
@@ -489,13 +557,14 @@ __global__ void k_dedup_keys(DedupArgs d, unsigned long long n_events, unsigned 
   }
 }
 __global__ void k_final(Cands c, const uint32_t* svals, const uint32_t* nsurv, uint8_t* okind, uint32_t* oprior,
-                        uint32_t* ocur) {
+                        uint32_t* ocur, unsigned long long* okey) {
   const uint32_t n = *nsurv;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint32_t k = svals[j];
     okind[j] = (uint8_t)c.kind[k];
     oprior[j] = c.prior[k];
     ocur[j] = c.cur[k];
+    okey[j] = c.okey[k];
   }
 }
 

@@ -97,6 +97,7 @@ struct gw_ctx {
   uint8_t* d_kind = nullptr;
   uint32_t* d_prior = nullptr;
   uint32_t* d_cur = nullptr;
+  unsigned long long* d_okey = nullptr;
   Diag* d_diags = nullptr;
   gw_stats stats{};
   bool stats_pending = false;
@@ -111,6 +112,7 @@ struct gw_ctx {
   // last analysis, for an eager re-run after a graph abort
   DevTrace last_tr{};
   uint32_t last_inactive = 1;
+  uint32_t last_shard = 0, last_nshard = 1;
   bool last_graph = false;
   Plan plan;
 
@@ -440,7 +442,9 @@ struct Pipeline {
       C->d_kind = C->get<uint8_t>("o_kind", ncap);
       C->d_prior = C->get<uint32_t>("o_prior", ncap);
       C->d_cur = C->get<uint32_t>("o_cur", ncap);
-      GW_LAUNCH(k_final, grid_for(ncap), kThreads, 0, st, cd, sv, d_nsurv, C->d_kind, C->d_prior, C->d_cur);
+      C->d_okey = C->get<unsigned long long>("o_okey", ncap);
+      GW_LAUNCH(k_final, grid_for(ncap), kThreads, 0, st, cd, sv, d_nsurv, C->d_kind, C->d_prior, C->d_cur,
+                C->d_okey);
       check_launch();
     }
     C->d_diags = w.diags;
@@ -465,6 +469,16 @@ struct Pipeline {
   void* skeys = nullptr;
   uint32_t *sto = nullptr, *segst = nullptr, *lastw = nullptr;
   uint64_t obs_nq = 0;
+  uint32_t shard = 0, nshard = 1;  // address sharding (gw_opts)
+  uint64_t na_sorted = 0;          // positions the access pass sorts (N, or this shard's accesses)
+  ShardArgs shard_args() const {
+    ShardArgs sa;
+    sa.kr = kr;
+    sa.nloc = kr.nbits - kr.sentinel;
+    sa.shard = shard;
+    sa.G = nshard;
+    return sa;
+  }
 
   // ------------------------------------------------------- lock pre-pass
   void lock_prepass() {
@@ -543,35 +557,74 @@ struct Pipeline {
   // ------------------------------------------------- access sort + scan
   void access_sort() {
     const uint64_t N = tr.n;
-    // All N positions are sorted; non-access events carry the top sentinel key
-    // and sort last, and every access-pass kernel skips them, so no kernel
-    // needs the access count on the host.
     kr = key_runs(gmode ? P->D : (hs.n_acc ? hs.key_or ^ hs.key_and : 0ull));
     C->stats.sort_bits = kr.nbits;
     wide = kr.nbits > 32;
     obs_D = hs.n_acc ? hs.key_or ^ hs.key_and : 0ull;
-    vals = C->get<uint32_t>("acc_v", N);
+    int nbits = kr.nbits;
+    uint64_t NA = N;
+    if (nshard <= 1) {
+      // All N positions are sorted; non-access events carry the top sentinel
+      // key and sort last, and every access-pass kernel skips them, so no
+      // kernel needs the access count on the host.
+      vals = C->get<uint32_t>("acc_v", N);
+      if (!wide) {
+        uint32_t* k32 = C->get<uint32_t>("acc_k", N);
+        GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals);
+        skeys = k32;
+      } else {
+        unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
+        GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals);
+        skeys = k64;
+      }
+    } else {
+      // address shard: this shard's accesses only, in trace order (compacted keys, no sentinel)
+      const ShardArgs sa = shard_args();
+      const uint64_t nt = lb_tiles(N);
+      uint32_t* tcnt = C->get<uint32_t>("sh_cnt", nt);
+      uint32_t* toff = C->get<uint32_t>("sh_off", nt);
+      const unsigned grid = (unsigned)std::min<uint64_t>(nt, 148ull * 8);
+      GW_LAUNCH((k_shard_accesses<uint32_t, false>), grid, kThreads, 0, st, tr, sa, tcnt, toff, (uint32_t*)nullptr,
+                (uint32_t*)nullptr);
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{tcnt}, ArrStore<uint32_t>{toff}, nt, OpSum(), 0u, false, "sc_u32");
+      uint32_t hv[2];
+      CK(cudaMemcpyAsync(hv, toff + (nt - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hv + 1, tcnt + (nt - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      NA = (uint64_t)hv[0] + hv[1];
+      nbits = sa.nloc;
+      wide = nbits > 32;
+      vals = C->get<uint32_t>("acc_v", NA + 1);
+      if (!wide) {
+        uint32_t* k32 = C->get<uint32_t>("acc_k", NA + 1);
+        GW_LAUNCH((k_shard_accesses<uint32_t, true>), grid, kThreads, 0, st, tr, sa, tcnt, toff, k32, vals);
+        skeys = k32;
+      } else {
+        unsigned long long* k64 = C->get<unsigned long long>("acc_k64", NA + 1);
+        GW_LAUNCH((k_shard_accesses<unsigned long long, true>), grid, kThreads, 0, st, tr, sa, tcnt, toff, k64, vals);
+        skeys = k64;
+      }
+    }
+    na_sorted = NA;
     if (!wide) {
-      uint32_t* k32 = C->get<uint32_t>("acc_k", N);
-      GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals);
-      sort<uint32_t>(k32, vals, N, kr.nbits, "acc");
+      uint32_t* k32 = (uint32_t*)skeys;
+      sort<uint32_t>(k32, vals, NA, nbits, "acc");
       skeys = k32;
     } else {
-      unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
-      GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals);
-      sort<unsigned long long>(k64, vals, N, kr.nbits, "acc");
+      unsigned long long* k64 = (unsigned long long*)skeys;
+      sort<unsigned long long>(k64, vals, NA, nbits, "acc");
       skeys = k64;
     }
-    sto = C->get<uint32_t>("acc_to", N);
-    GW_LAUNCH(k_gather_to, grid_for(N), kThreads, 0, st, vals, tr.tidop, N, sto);
-    segst = C->get<uint32_t>("acc_segst", N);
-    lastw = C->get<uint32_t>("acc_lastw", N);
+    sto = C->get<uint32_t>("acc_to", NA + 1);
+    GW_LAUNCH(k_gather_to, grid_for(NA), kThreads, 0, st, vals, tr.tidop, NA, sto);
+    segst = C->get<uint32_t>("acc_segst", NA + 1);
+    lastw = C->get<uint32_t>("acc_lastw", NA + 1);
     if (!wide)
-      scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, N, OpMax2(),
+      scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, NA, OpMax2(),
                           make_uint2(0, 0), true, "sc_u2");
     else
       scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
-                          SegStore{segst, lastw}, N, OpMax2(), make_uint2(0, 0), true, "sc_u2");
+                          SegStore{segst, lastw}, NA, OpMax2(), make_uint2(0, 0), true, "sc_u2");
   }
 
   Cands make_cands(const std::string& tag, uint64_t cap, uint32_t* cnt) {
@@ -593,7 +646,7 @@ struct Pipeline {
   // (u != t, !cover) and leave the clock comparison to the walker's queries.
   // Counts at scal[slot] (candidates) and scal[slot + 1] (large windows).
   Cands check_pass(bool defer, const char* tag, int slot) {
-    const uint64_t N = tr.n, NA = N;
+    const uint64_t N = tr.n, NA = na_sorted;
     uint32_t* cnt = scal + slot;
     uint32_t* large_i = C->get<uint32_t>("lg_i", NA / kSmallWin + 1);
     uint32_t* large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);
@@ -622,7 +675,7 @@ struct Pipeline {
       ca.large_cap = (uint32_t)(NA / kSmallWin + 1);
       ca.defer = defer ? 1 : 0;
       GW_LAUNCH(k_check, grid_for(NA), kThreads, 0, st, ca);
-      if (!defer) GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd);
+      if (!defer) GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd, shard_args());
       check_launch();
       if (gmode) {
         GW_LAUNCH(k_guard, 1, 1, 0, st, cnt, cd.cap, cnt + 1, scal + SC_ABORT);
@@ -705,7 +758,7 @@ struct Pipeline {
       cd = make_cands("c", cap, cnt);
       CK(cudaMemsetAsync(cnt, 0, 3 * sizeof(uint32_t), st));
       if (nq) GW_LAUNCH(k_resolve, grid_for(nq), kThreads, 0, st, cq, w.qv, w.time, cd);
-      GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd);
+      GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd, shard_args());
       check_launch();
       d2h(&hc, cnt);
       if (hc <= cd.cap) break;
@@ -904,7 +957,10 @@ extern "C" void gw_ctx_destroy(gw_ctx* c) {
 // Eager analysis, then (lock-free traces without large reader windows) build
 // the Plan and capture the graph-mode pipeline for later replays.
 static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_t inactive, const void* kp,
-                         const void* tp, const void* ip, bool eager) {
+                         const void* tp, const void* ip, bool eager, uint32_t shard, uint32_t nshard) {
+  if (nshard > 1) eager = true;  // sharded analyses are not graph-replayed
+  c->last_shard = shard;
+  c->last_nshard = nshard;
   Plan& P = c->plan;
   c->last_tr = tr;
   c->last_inactive = inactive;
@@ -930,6 +986,8 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   p.st = st;
   p.inactive_opt = inactive;
   p.tr = tr;
+  p.shard = shard;
+  p.nshard = nshard;
   p.run();
   if (eager || tr.n == 0 || !p.obs_snap || p.obs_nlarge > 0 || st == 0) return;
   // build the plan; run the graph-mode pipeline once for real (allocates every
@@ -978,8 +1036,11 @@ extern "C" int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* t, const gw
     CK(cudaSetDevice(c->device));
     cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
     const uint32_t inactive = o ? o->inactive_opt : 1u;
+    const uint32_t nsh = o && o->shard_count > 1 ? o->shard_count : 1u;
+    const uint32_t sh = nsh > 1 ? o->shard_index : 0u;
+    if (sh >= nsh) throw CudaErr{GW_E_ARG, "shard_index must be < shard_count"};
     DevTrace tr = make_dev(t, (const unsigned long long*)t->key, t->tidop, t->instr);
-    analyze_impl(c, tr, st, inactive, t->key, t->tidop, t->instr, o && (o->flags & GW_OPT_EAGER));
+    analyze_impl(c, tr, st, inactive, t->key, t->tidop, t->instr, o && (o->flags & GW_OPT_EAGER), sh, nsh);
   });
 }
 
@@ -991,6 +1052,9 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
     CK(cudaSetDevice(c->device));
     cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
     const uint32_t inactive = o ? o->inactive_opt : 1u;
+    const uint32_t nsh = o && o->shard_count > 1 ? o->shard_count : 1u;
+    const uint32_t sh = nsh > 1 ? o->shard_index : 0u;
+    if (sh >= nsh) throw CudaErr{GW_E_ARG, "shard_index must be < shard_count"};
     const uint64_t N = t->n_events;
     c->last_stream = st;
     unsigned long long* k = c->get<unsigned long long>("in_key", N);
@@ -1002,7 +1066,7 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
       CK(cudaMemcpyAsync(in, t->instr, 4 * N, cudaMemcpyHostToDevice, st));
     }
     DevTrace tr = make_dev(t, k, to, in);
-    analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER));
+    analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh);
   });
 }
 
@@ -1022,6 +1086,7 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
         c->last_graph = false;
         Pipeline p;
         p.C = c; p.st = c->last_stream; p.inactive_opt = c->last_inactive; p.tr = c->last_tr;
+        p.shard = c->last_shard; p.nshard = c->last_nshard;
         p.run();
         CK(cudaMemcpyAsync(sc, c->d_scal, sizeof sc, cudaMemcpyDeviceToHost, c->last_stream));
         CK(cudaStreamSynchronize(c->last_stream));
@@ -1039,6 +1104,8 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
     c->n_reports = n;
     c->n_diags = nd;
     out->n_reports = n;
+    out->order_key = (uint64_t*)malloc(8 * std::max<uint64_t>(n, 1));
+    if (!out->order_key) throw std::bad_alloc();
     out->kind = (uint8_t*)malloc(std::max<uint64_t>(n, 1));
     out->prior_event = (uint32_t*)malloc(4 * std::max<uint64_t>(n, 1));
     out->current_event = (uint32_t*)malloc(4 * std::max<uint64_t>(n, 1));
@@ -1048,6 +1115,7 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
       CK(cudaMemcpyAsync(out->kind, c->d_kind, n, cudaMemcpyDeviceToHost, c->last_stream));
       CK(cudaMemcpyAsync(out->prior_event, c->d_prior, 4 * n, cudaMemcpyDeviceToHost, c->last_stream));
       CK(cudaMemcpyAsync(out->current_event, c->d_cur, 4 * n, cudaMemcpyDeviceToHost, c->last_stream));
+      CK(cudaMemcpyAsync(out->order_key, c->d_okey, 8 * n, cudaMemcpyDeviceToHost, c->last_stream));
     }
     if (nd) CK(cudaMemcpyAsync(dg.data(), c->d_diags, sizeof(Diag) * nd, cudaMemcpyDeviceToHost, c->last_stream));
     CK(cudaStreamSynchronize(c->last_stream));
@@ -1075,6 +1143,7 @@ extern "C" void gw_result_free(gw_result* r) {
   free(r->diag_event);
   free(r->diag_code);
   free(r->diag_lock);
+  free(r->order_key);
   memset(r, 0, sizeof *r);
 }
 

@@ -1,0 +1,76 @@
+"""Host side of the address-sharded (multi-GPU) path on CPU: the gloo
+all-gather + order-key merge of paper_2111_12478_b200.shard reproduces the
+unsharded report order (world_size 2 and 3, real processes)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2111_12478_b200.shard import merge_shards
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _reports(n=500, seed=0):
+    rng = np.random.default_rng(seed)
+    okey = np.sort(rng.choice(1 << 40, size=n, replace=False)).astype(np.uint64)
+    return {"order_key": okey, "kind": rng.integers(0, 3, n).astype(np.uint8),
+            "prior": rng.integers(0, 1 << 30, n).astype(np.uint32),
+            "current": rng.integers(0, 1 << 30, n).astype(np.uint32)}
+
+
+def _split(full, world, seed=1):
+    # shards own arbitrary subsets (location ranges are not order-key ranges)
+    owner = np.random.default_rng(seed).integers(0, world, len(full["kind"]))
+    return [{f: v[owner == r] for f, v in full.items()} for r in range(world)]
+
+
+def test_merge_shards_restores_order():
+    full = _reports()
+    merged = merge_shards(_split(full, 4))
+    for f in full:
+        assert np.array_equal(merged[f], full[f])
+    assert len(merge_shards([_split(full, 1)[0]])["kind"]) == len(full["kind"])
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2111_12478_b200.shard import gather_reports
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    parts = _split(_reports(777, seed=world), world)
+    parts[-1] = {f: v[:0] for f, v in parts[-1].items()}  # an empty shard
+    full = merge_shards(parts)
+    part = parts[rank]
+    out = gather_reports(part)
+    if rank == 0:
+        q.put(all(np.array_equal(out[f], full[f]) for f in full))
+    else:
+        q.put(out is None)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_reports_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res)
