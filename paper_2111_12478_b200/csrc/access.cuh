@@ -24,6 +24,8 @@
 namespace gw {
 
 constexpr uint32_t kSmallWin = 32;
+// sorted values: event index | VAL_W for writes (event indices < 2^31)
+constexpr uint32_t VAL_W = 0x80000000u, VAL_E = 0x7FFFFFFFu;
 constexpr unsigned long long SUB_WCHECK = 0x40000000ull;
 constexpr unsigned long long SUB_READER = 0x80000000ull;
 
@@ -52,7 +54,7 @@ __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals) {
         if (r < kr.n) k |= (K)((x >> kr.src[r]) & ((1ull << kr.width[r]) - 1ull)) << kr.dst[r];
     }
     keys[e] = k;
-    vals[e] = (uint32_t)e;
+    vals[e] = (uint32_t)e | (ev_kind(to) == GW_K_WRITE ? VAL_W : 0u);
   }
 }
 
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(kThreads) k_shard_accesses(DevTrace tr, ShardA
       if (EMIT && in) {
         const uint32_t pos = run + woff + __popc(m & lt);
         keys[pos] = (K)ck;
-        vals[pos] = (uint32_t)e;
+        vals[pos] = (uint32_t)e | (ev_kind(tr.tidop[e]) == GW_K_WRITE ? VAL_W : 0u);
       }
       run += tot;
       __syncthreads();
@@ -192,34 +194,9 @@ __global__ void k_part_keys(DevTrace tr, uint32_t G, uint32_t* keys, uint32_t* v
   }
 }
 
-__global__ void k_gather_to(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ tidop, uint64_t n,
-                            uint32_t* __restrict__ sto) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    sto[i] = tidop[vals[i]];
-}
-
 struct OpMax2 {
   __device__ __forceinline__ uint2 operator()(const uint2& a, const uint2& b) const {
     return make_uint2(max(a.x, b.x), max(a.y, b.y));
-  }
-};
-// x: segment head position + 1 ; y: write position + 1
-template <class K>
-struct SegLoad {
-  const K* keys;
-  const uint32_t* sto;
-  __device__ __forceinline__ uint2 operator()(uint64_t i) const {
-    uint32_t h = (i == 0 || keys[i] != keys[i - 1]) ? (uint32_t)i + 1 : 0u;
-    uint32_t w = ev_kind(sto[i]) == GW_K_WRITE ? (uint32_t)i + 1 : 0u;
-    return make_uint2(h, w);
-  }
-};
-struct SegStore {
-  uint32_t* segst;
-  uint32_t* lastw;
-  __device__ __forceinline__ void operator()(uint64_t i, const uint2& v) const {
-    segst[i] = v.x - 1;
-    lastw[i] = v.y;
   }
 };
 
@@ -248,84 +225,301 @@ __device__ __forceinline__ bool cover(uint32_t toa, uint32_t tob, uint32_t BS) {
   return ev_tid(toa) / BS == ev_tid(tob) / BS;
 }
 
-struct CheckArgs {
-  DevTrace tr;
-  const uint32_t* vals;   // sorted event indices
-  const uint32_t* sto;    // sorted tidop
-  const uint32_t* segst;
-  const uint32_t* lastw;  // inclusive, pos+1
-  const uint32_t* time;
+// Access-time stamps (time = local_t at the access, vobj = t's pred object):
+// arrays written by the walker, or -- lock-free snapshot mode -- looked up in
+// the walker's per-block snapshots: snapshot k of block b = the block's
+// state after its k-th hard event (k = #hard events of b before e).
+struct StampSrc {
+  const uint32_t* time;  // arrays (nullptr: snapshots)
   const uint32_t* vobj;
+  const uint32_t* hard_ev;
+  const uint32_t* hb_beg;
+  const uint32_t* hb_end;
+  const uint2* snap;
+  uint32_t BS;
+  __device__ __forceinline__ uint2 get(uint32_t e, uint32_t t) const {
+    if (time) return make_uint2(__ldg(time + e), __ldg(vobj + e));
+    const uint32_t b = t / BS;
+    const uint32_t base = __ldg(hb_beg + b);
+    uint32_t lo = base, hi = __ldg(hb_end + b);
+    while (lo < hi) {
+      const uint32_t m = (lo + hi) >> 1;
+      if (__ldg(hard_ev + m) < e) lo = m + 1; else hi = m;
+    }
+    return snap[(size_t)(base + b + (lo - base)) * BS + (t - b * BS)];
+  }
+};
+
+// The access check (gwcp.py:251-277) over the location-sorted accesses, one
+// tile of kAccTile sorted positions per CTA:
+//   * segment head / last write before each position: a tile-local max-scan
+//     seeded with the maxima of all earlier tiles (k_acc_tilemax + a scan
+//     over tiles), no per-position scan arrays in HBM;
+//   * the tile's event indices, tidops (one gather) and access stamps
+//     (batched lookups, all positions' loads in flight together) staged in
+//     smem, so the prior write and the reader window are mostly smem reads;
+//   * the clock test is one gather pred_t^{ver}[u]; lock-free clock objects
+//     are block-range objects of the accessing thread's block (the barrier
+//     hull never leaves it), so the header need not be read.
+// defer (lock mode): every structural candidate (u != t, !cover) is emitted
+// and the walker answers the clock half later.
+constexpr int kAccItems = 8;
+constexpr int kAccTile = kThreads * kAccItems;  // 2048
+
+template <class K>
+struct AccArgs {
+  DevTrace tr;
+  const K* keys;          // sorted compacted location keys (non-accesses: sentinel, last)
+  const uint32_t* vals;   // sorted event | VAL_W
+  uint64_t n;             // sorted positions
+  const uint2* carry;     // per tile: max (head pos + 1, write pos + 1) over all earlier tiles
+  StampSrc src;
   const uint32_t* arena;
-  uint64_t n_acc;
+  int defer;
+  int blockobj;           // clock objects are block-range objects (lock-free traces)
   Cands c;
-  uint32_t* large_i;  // positions of writes with a large reader window
+  uint32_t* large_i;      // writes with a reader window > kSmallWin
   uint32_t* large_ws;
   uint32_t* n_large;
   uint32_t large_cap;
-  int defer;  // lock mode: emit every structural candidate; the walker answers pred_t[u] later
 };
-__device__ __forceinline__ bool clock_says_race(const CheckArgs& a, uint32_t prior_ev, uint32_t vo, uint32_t u) {
-  return a.defer || a.time[prior_ev] > obj_get(a.arena, vo, u);
-}
 
-__global__ void __launch_bounds__(kThreads) k_check(CheckArgs a) {
-  const uint32_t BS = a.tr.BS;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_acc;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t c = a.vals[i];
-    const uint32_t toc = a.sto[i];
-    if (ev_kind(toc) > GW_K_WRITE) continue;  // non-access events sort last (sentinel key)
-    const uint32_t tc = ev_tid(toc);
-    const bool isw = ev_kind(toc) == GW_K_WRITE;
-    const uint32_t ss = a.segst[i];
-    const uint32_t lw = i > 0 ? a.lastw[i - 1] : 0u;
-    const bool hasw = lw > 0 && lw - 1 >= ss && lw - 1 < i;
-    const uint32_t W = hasw ? lw - 1 : NIL;
-    const uint32_t vo = a.defer ? NIL : a.vobj[c];
-    unsigned long long loc = 0;
-    if (hasw) {
-      const uint32_t p = a.vals[W];
-      const uint32_t top = a.sto[W];
-      const uint32_t u = ev_tid(top);
-      if (u != tc && !cover(top, toc, BS) && clock_says_race(a, p, vo, u)) {
-        loc = a.tr.key[c];
-        emit_cand(a.c, ((unsigned long long)c << 32) | SUB_WCHECK, loc, p, c, isw ? GW_WW : GW_WR);
+template <class K>
+__global__ void __launch_bounds__(kThreads) k_acc_tilemax(const K* keys, const uint32_t* vals, uint64_t n,
+                                                         uint2* agg) {
+  __shared__ uint32_t s_h[kThreads / 32], s_w[kThreads / 32];
+  const uint64_t ntiles = (n + kAccTile - 1) / kAccTile;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t base = tile * kAccTile;
+    uint32_t h = 0, w = 0;
+#pragma unroll
+    for (int k = 0; k < kAccItems; k++) {
+      const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+      if (i < n) {
+        if (i == 0 || keys[i] != keys[i - 1]) h = (uint32_t)i + 1;
+        if (vals[i] & VAL_W) w = (uint32_t)i + 1;
       }
     }
-    if (isw) {
+    h = __reduce_max_sync(0xffffffffu, h);
+    w = __reduce_max_sync(0xffffffffu, w);
+    if ((threadIdx.x & 31) == 0) { s_h[threadIdx.x >> 5] = h; s_w[threadIdx.x >> 5] = w; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int x = 0; x < kThreads / 32; x++) { h = max(h, s_h[x]); w = max(w, s_w[x]); }
+      agg[tile] = make_uint2(h, w);
+    }
+    __syncthreads();
+  }
+}
+
+template <class K>
+struct AccSmem {
+  K key[kAccTile];
+  uint32_t val[kAccTile];
+  uint32_t to[kAccTile];
+  uint32_t lw[kAccTile];   // inclusive last write pos + 1
+  uint32_t ss[kAccTile];   // segment head pos
+  uint2 st[kAccTile];      // (time, vobj) stamps
+  uint2 wtot[kThreads / 32];
+};
+
+// (event, tidop) of sorted position q (smem when q is in this tile)
+template <class K>
+__device__ __forceinline__ void acc_pos(const AccArgs<K>& a, const AccSmem<K>& S, uint64_t base, uint64_t q,
+                                        uint32_t& ev, uint32_t& to) {
+  if (q >= base) {
+    ev = S.val[q - base] & VAL_E;
+    to = S.to[q - base];
+  } else {
+    ev = __ldg(a.vals + q) & VAL_E;
+    to = __ldg(a.tr.tidop + ev);
+  }
+}
+template <class K>
+__device__ __forceinline__ uint32_t acc_time(const AccArgs<K>& a, const AccSmem<K>& S, uint64_t base, uint64_t q,
+                                             uint32_t ev, uint32_t tid) {
+  return q >= base ? S.st[q - base].x : a.src.get(ev, tid).x;
+}
+// pred_t^{vo}[u] for the accessing thread tc
+template <class K>
+__device__ __forceinline__ uint32_t acc_clock(const AccArgs<K>& a, uint32_t vo, uint32_t tc, uint32_t u) {
+  if (!a.blockobj) return obj_get(a.arena, vo, u);
+  const uint32_t BS = a.tr.BS;
+  if (vo == NIL || u / BS != tc / BS) return 0u;
+  return __ldg(optr(a.arena, vo) + OBJ_HDR + (u - (tc / BS) * BS));
+}
+
+template <class K>
+__global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  AccSmem<K>& S = *reinterpret_cast<AccSmem<K>*>(smem_raw);
+  const uint32_t BS = a.tr.BS;
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const uint64_t ntiles = (a.n + kAccTile - 1) / kAccTile;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t base = tile * kAccTile;
+    const uint32_t cnt = (uint32_t)min((uint64_t)kAccTile, a.n - base);
+    // stage keys / events, then gather the tidops
+#pragma unroll
+    for (int k = 0; k < kAccItems; k++) {
+      const uint32_t j = k * kThreads + threadIdx.x;
+      if (j < cnt) { S.key[j] = a.keys[base + j]; S.val[j] = a.vals[base + j]; }
+    }
+    const K prevkey = base > 0 ? a.keys[base - 1] : (K)0;
+    {
+      uint32_t tt[kAccItems];
+#pragma unroll
+      for (int k = 0; k < kAccItems; k++) {
+        const uint32_t j = k * kThreads + threadIdx.x;
+        tt[k] = j < cnt ? __ldg(a.tr.tidop + (a.vals[base + j] & VAL_E)) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kAccItems; k++) {
+        const uint32_t j = k * kThreads + threadIdx.x;
+        if (j < cnt) S.to[j] = tt[k];
+      }
+      if (!a.defer) {
+        // stamps of every position: the lookups of all items interleaved
+        uint2 sv[kAccItems];
+        if (a.src.time) {
+#pragma unroll
+          for (int k = 0; k < kAccItems; k++) {
+            const uint32_t j = k * kThreads + threadIdx.x;
+            const uint32_t e = j < cnt ? (a.vals[base + j] & VAL_E) : 0u;
+            sv[k] = make_uint2(__ldg(a.src.time + e), __ldg(a.src.vobj + e));
+          }
+        } else {
+          uint32_t e[kAccItems], lo[kAccItems], hi[kAccItems], bb[kAccItems], b0[kAccItems];
+#pragma unroll
+          for (int k = 0; k < kAccItems; k++) {
+            const uint32_t j = k * kThreads + threadIdx.x;
+            e[k] = j < cnt ? (a.vals[base + j] & VAL_E) : 0u;
+            bb[k] = ev_tid(tt[k]) / BS;
+            b0[k] = __ldg(a.src.hb_beg + bb[k]);
+            lo[k] = b0[k];
+            hi[k] = __ldg(a.src.hb_end + bb[k]);
+          }
+          bool any = true;
+          while (any) {
+            any = false;
+#pragma unroll
+            for (int k = 0; k < kAccItems; k++) {
+              if (lo[k] < hi[k]) {
+                const uint32_t m = (lo[k] + hi[k]) >> 1;
+                if (__ldg(a.src.hard_ev + m) < e[k]) lo[k] = m + 1; else hi[k] = m;
+                any = true;
+              }
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < kAccItems; k++)
+            sv[k] = a.src.snap[(size_t)(lo[k] + bb[k]) * BS + (ev_tid(tt[k]) - bb[k] * BS)];
+        }
+#pragma unroll
+        for (int k = 0; k < kAccItems; k++) {
+          const uint32_t j = k * kThreads + threadIdx.x;
+          if (j < cnt) S.st[j] = sv[k];
+        }
+      }
+    }
+    __syncthreads();
+    // segment head / last write: block-wide max-scan rounds, seeded with the carry
+    uint2 run = a.carry[tile];
+    for (int k = 0; k < kAccItems; k++) {
+      const uint32_t j = k * kThreads + threadIdx.x;
+      const uint64_t i = base + j;
+      uint2 v = make_uint2(0, 0);
+      if (j < cnt) {
+        const K kj = S.key[j];
+        const K kp = j > 0 ? S.key[j - 1] : prevkey;
+        if (i == 0 || kj != kp) v.x = (uint32_t)i + 1;
+        if (S.val[j] & VAL_W) v.y = (uint32_t)i + 1;
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, v.x, o), y = __shfl_up_sync(0xffffffffu, v.y, o);
+        if (lane >= o) { v.x = max(v.x, x); v.y = max(v.y, y); }
+      }
+      if (lane == 31) S.wtot[wq] = v;
+      __syncthreads();
+      uint2 pre = run, tot = run;
+#pragma unroll
+      for (int x = 0; x < kThreads / 32; x++) {
+        const uint2 t = S.wtot[x];
+        if (x < wq) { pre.x = max(pre.x, t.x); pre.y = max(pre.y, t.y); }
+        tot.x = max(tot.x, t.x); tot.y = max(tot.y, t.y);
+      }
+      if (j < cnt) {
+        S.ss[j] = max(pre.x, v.x) - 1;
+        S.lw[j] = max(pre.y, v.y);
+      }
+      run = tot;
+      __syncthreads();
+    }
+    const uint32_t lw_in = a.carry[tile].y;  // last write before the tile
+    // the checks
+    for (int k = 0; k < kAccItems; k++) {
+      const uint32_t j = k * kThreads + threadIdx.x;
+      if (j >= cnt) continue;
+      const uint64_t i = base + j;
+      const uint32_t toc = S.to[j];
+      if (ev_kind(toc) > GW_K_WRITE) continue;  // non-access events sort last (sentinel key)
+      const uint32_t c = S.val[j] & VAL_E;
+      const uint32_t tc = ev_tid(toc);
+      const bool isw = ev_kind(toc) == GW_K_WRITE;
+      const uint32_t ss = S.ss[j];
+      const uint32_t lw = j > 0 ? S.lw[j - 1] : lw_in;
+      const bool hasw = lw > 0 && lw - 1 >= ss && lw - 1 < i;
+      const uint32_t W = hasw ? lw - 1 : NIL;
+      const uint32_t vo = a.defer ? NIL : S.st[j].y;
+      unsigned long long loc = 0;
+      if (hasw) {
+        uint32_t p, top;
+        acc_pos(a, S, base, W, p, top);
+        const uint32_t u = ev_tid(top);
+        if (u != tc && !cover(top, toc, BS) &&
+            (a.defer || acc_time(a, S, base, W, p, u) > acc_clock(a, vo, tc, u))) {
+          loc = a.tr.key[c];
+          emit_cand(a.c, ((unsigned long long)c << 32) | SUB_WCHECK, loc, p, c, isw ? GW_WW : GW_WR);
+        }
+      }
+      if (!isw) continue;
       const uint32_t ws = hasw ? W + 1 : ss;
       const uint32_t m = (uint32_t)i - ws;
       if (m == 0) continue;
       if (m > kSmallWin) {
-        uint32_t k = atomicAdd(a.n_large, 1u);
-        if (k < a.large_cap) { a.large_i[k] = (uint32_t)i; a.large_ws[k] = ws; }
+        uint32_t kk = atomicAdd(a.n_large, 1u);
+        if (kk < a.large_cap) { a.large_i[kk] = (uint32_t)i; a.large_ws[kk] = ws; }
         else atomicOr(a.c.err, ERR_CAND);
         continue;
       }
       // readers since W: one candidate per thread (its latest read), ranked by its first read
       for (uint32_t q = ws; q < i; q++) {
-        const uint32_t toq = a.sto[q];
-        if (ev_kind(toq) > GW_K_WRITE) continue;  // non-access event sharing key 0
+        uint32_t r, toq;
+        acc_pos(a, S, base, q, r, toq);
+        if (ev_kind(toq) > GW_K_WRITE) continue;
         const uint32_t uq = ev_tid(toq);
+        if (uq == tc) continue;
         bool later = false;
         for (uint32_t q2 = q + 1; q2 < i && !later; q2++) {
-          const uint32_t t2 = a.sto[q2];
+          uint32_t e2, t2;
+          acc_pos(a, S, base, q2, e2, t2);
           later = ev_kind(t2) <= GW_K_WRITE && ev_tid(t2) == uq;
         }
-        if (later || uq == tc) continue;
+        if (later) continue;
         uint32_t first = q;
         for (uint32_t q3 = ws; q3 < q; q3++) {
-          const uint32_t t3 = a.sto[q3];
+          uint32_t e3, t3;
+          acc_pos(a, S, base, q3, e3, t3);
           if (ev_kind(t3) <= GW_K_WRITE && ev_tid(t3) == uq) { first = q3; break; }
         }
-        const uint32_t r = a.vals[q];
-        if (!cover(toq, toc, BS) && clock_says_race(a, r, vo, uq)) {
+        if (!cover(toq, toc, BS) && (a.defer || acc_time(a, S, base, q, r, uq) > acc_clock(a, vo, tc, uq))) {
           if (!loc) loc = a.tr.key[c];
-          emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), a.tr.key[c], r, c, GW_RW);
+          emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), loc, r, c, GW_RW);
         }
       }
     }
+    __syncthreads();
   }
 }
 
@@ -360,13 +554,22 @@ __global__ void k_resolve(Cands in, const uint32_t* qv, const uint32_t* time, Ca
   }
 }
 
+template <class K>
+inline void acc_setup() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_access<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AccSmem<K>));
+    done = true;
+  }
+}
+
 // large reader windows: (window, tid) groups via a secondary stable sort
 __global__ void k_large_fill(const uint32_t* large_i, const uint32_t* large_ws, const uint32_t* off, uint32_t n_large,
-                             const uint32_t* sto, unsigned long long* keys, uint32_t* vals) {
+                             const uint32_t* svals, const uint32_t* tidop, unsigned long long* keys, uint32_t* vals) {
   for (uint32_t k = blockIdx.x; k < n_large; k += gridDim.x) {
     const uint32_t ws = large_ws[k], m = large_i[k] - ws, o = off[k];
     for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
-      const uint32_t t = sto[ws + j];
+      const uint32_t t = tidop[svals[ws + j] & VAL_E];
       // non-access events (key-0 location) go to a virtual window past the last one
       const unsigned long long kk = ev_kind(t) <= GW_K_WRITE ? k : n_large;
       keys[o + j] = (kk << 24) | ev_tid(t);
@@ -374,7 +577,8 @@ __global__ void k_large_fill(const uint32_t* large_i, const uint32_t* large_ws, 
     }
   }
 }
-__global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const uint32_t* vals, uint64_t M,
+template <class K>
+__global__ void k_large_check(AccArgs<K> a, const unsigned long long* keys, const uint32_t* vals, uint64_t M,
                               uint32_t nlarge) {
   const uint32_t BS = a.tr.BS;
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (uint64_t)gridDim.x * blockDim.x) {
@@ -385,12 +589,13 @@ __global__ void k_large_check(CheckArgs a, const unsigned long long* keys, const
     const uint32_t k = (uint32_t)(key >> 24);
     if (k >= nlarge) continue;  // non-access events
     const uint32_t i = a.large_i[k], ws = a.large_ws[k];
-    const uint32_t c = a.vals[i], toc = a.sto[i];
+    const uint32_t c = a.vals[i] & VAL_E, toc = a.tr.tidop[c];
     const uint32_t q = vals[j], first = vals[f];
-    const uint32_t toq = a.sto[q], uq = ev_tid(toq);
+    const uint32_t r = a.vals[q] & VAL_E;
+    const uint32_t toq = a.tr.tidop[r], uq = ev_tid(toq);
     if (uq == ev_tid(toc)) continue;
-    const uint32_t r = a.vals[q];
-    if (!cover(toq, toc, BS) && clock_says_race(a, r, a.defer ? NIL : a.vobj[c], uq))
+    if (!cover(toq, toc, BS) &&
+        (a.defer || a.src.get(r, uq).x > acc_clock(a, a.src.get(c, ev_tid(toc)).y, ev_tid(toc), uq)))
       emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), a.tr.key[c], r, c, GW_RW);
   }
 }

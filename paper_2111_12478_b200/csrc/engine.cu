@@ -467,7 +467,8 @@ struct Pipeline {
   bool wide = false;
   uint32_t* vals = nullptr;  // access pass: sorted event indices
   void* skeys = nullptr;
-  uint32_t *sto = nullptr, *segst = nullptr, *lastw = nullptr;
+  uint2* carry = nullptr;     // per sorted tile: max (segment head, write position) of the earlier tiles
+  StampSrc stamps{};          // where the check pass reads access stamps
   uint64_t obs_nq = 0;
   uint32_t shard = 0, nshard = 1;  // address sharding (gw_opts)
   uint64_t na_sorted = 0;          // positions the access pass sorts (N, or this shard's accesses)
@@ -615,16 +616,17 @@ struct Pipeline {
       sort<unsigned long long>(k64, vals, NA, nbits, "acc");
       skeys = k64;
     }
-    sto = C->get<uint32_t>("acc_to", NA + 1);
-    GW_LAUNCH(k_gather_to, grid_for(NA), kThreads, 0, st, vals, tr.tidop, NA, sto);
-    segst = C->get<uint32_t>("acc_segst", NA + 1);
-    lastw = C->get<uint32_t>("acc_lastw", NA + 1);
+    // per-tile maxima of (segment head, write position), exclusive max-scan over tiles
+    const uint64_t nt = (NA + kAccTile - 1) / kAccTile;
+    uint2* agg = C->get<uint2>("acc_tagg", nt + 1);
+    carry = C->get<uint2>("acc_carry", nt + 1);
+    const unsigned tg = (unsigned)std::min<uint64_t>(std::max<uint64_t>(nt, 1), 148ull * 8);
     if (!wide)
-      scan<uint2, OpMax2>(SegLoad<uint32_t>{(const uint32_t*)skeys, sto}, SegStore{segst, lastw}, NA, OpMax2(),
-                          make_uint2(0, 0), true, "sc_u2");
+      GW_LAUNCH(k_acc_tilemax<uint32_t>, tg, kThreads, 0, st, (const uint32_t*)skeys, vals, NA, agg);
     else
-      scan<uint2, OpMax2>(SegLoad<unsigned long long>{(const unsigned long long*)skeys, sto},
-                          SegStore{segst, lastw}, NA, OpMax2(), make_uint2(0, 0), true, "sc_u2");
+      GW_LAUNCH(k_acc_tilemax<unsigned long long>, tg, kThreads, 0, st, (const unsigned long long*)skeys, vals, NA,
+                agg);
+    scan<uint2, OpMax2>(ArrLoad<uint2>{agg}, ArrStore<uint2>{carry}, nt, OpMax2(), make_uint2(0, 0), false, "sc_u2");
   }
 
   Cands make_cands(const std::string& tag, uint64_t cap, uint32_t* cnt) {
@@ -652,29 +654,41 @@ struct Pipeline {
     uint32_t* large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);
     uint64_t cand_cap = gmode ? P->cand_cap : std::max<uint64_t>(65536, NA / 4);
     Cands cd;
-    CheckArgs ca;
-    memset(&ca, 0, sizeof ca);
+    AccArgs<uint32_t> a32;
+    AccArgs<unsigned long long> a64;
     uint32_t hcnt[2] = {0, 0};
     for (int attempt = 0; attempt < 2; attempt++) {
       cd = make_cands(tag, cand_cap, cnt);
       CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t), st));
       if (!defer) CK(cudaMemsetAsync(scal + SC_NSURV, 0, sizeof(uint32_t), st));
-      ca.tr = tr;
-      ca.vals = vals;
-      ca.sto = sto;
-      ca.segst = segst;
-      ca.lastw = lastw;
-      ca.time = defer ? nullptr : w.time;
-      ca.vobj = defer ? nullptr : w.vobj;
-      ca.arena = defer ? nullptr : w.arena;
-      ca.n_acc = NA;
-      ca.c = cd;
-      ca.large_i = large_i;
-      ca.large_ws = large_ws;
-      ca.n_large = cnt + 1;
-      ca.large_cap = (uint32_t)(NA / kSmallWin + 1);
-      ca.defer = defer ? 1 : 0;
-      GW_LAUNCH(k_check, grid_for(NA), kThreads, 0, st, ca);
+      auto fill = [&](auto& aa, const auto* kp) {
+        memset(&aa, 0, sizeof aa);
+        aa.tr = tr;
+        aa.keys = kp;
+        aa.vals = vals;
+        aa.n = NA;
+        aa.carry = carry;
+        aa.src = stamps;
+        aa.arena = defer ? nullptr : w.arena;
+        aa.defer = defer ? 1 : 0;
+        aa.blockobj = (!defer && !has_locks) ? 1 : 0;
+        aa.c = cd;
+        aa.large_i = large_i;
+        aa.large_ws = large_ws;
+        aa.n_large = cnt + 1;
+        aa.large_cap = (uint32_t)(NA / kSmallWin + 1);
+      };
+      const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>((NA + kAccTile - 1) / kAccTile, 1),
+                                                       148ull * 16);
+      if (!wide) {
+        fill(a32, (const uint32_t*)skeys);
+        acc_setup<uint32_t>();
+        GW_LAUNCH(k_access<uint32_t>, ag, kThreads, sizeof(AccSmem<uint32_t>), st, a32);
+      } else {
+        fill(a64, (const unsigned long long*)skeys);
+        acc_setup<unsigned long long>();
+        GW_LAUNCH(k_access<unsigned long long>, ag, kThreads, sizeof(AccSmem<unsigned long long>), st, a64);
+      }
       if (!defer) GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd, shard_args());
       check_launch();
       if (gmode) {
@@ -699,10 +713,11 @@ struct Pipeline {
         CK(cudaMemcpyAsync(sizes, off.data(), sizeof(uint32_t) * nl, cudaMemcpyHostToDevice, st));
         unsigned long long* lk = C->get<unsigned long long>("lg_k", M);
         uint32_t* lv = C->get<uint32_t>("lg_v", M);
-        GW_LAUNCH(k_large_fill, std::min<uint32_t>(nl, 65535u), kThreads, 0, st, large_i, large_ws, sizes, nl, sto, lk,
-                  lv);
+        GW_LAUNCH(k_large_fill, std::min<uint32_t>(nl, 65535u), kThreads, 0, st, large_i, large_ws, sizes, nl, vals,
+                  tr.tidop, lk, lv);
         sort<unsigned long long>(lk, lv, M, 24 + ceil_log2(nl + 1), "lg");
-        GW_LAUNCH(k_large_check, grid_for(M), kThreads, 0, st, ca, lk, lv, M, nl);
+        if (!wide) GW_LAUNCH(k_large_check<uint32_t>, grid_for(M), kThreads, 0, st, a32, lk, lv, M, nl);
+        else GW_LAUNCH(k_large_check<unsigned long long>, grid_for(M), kThreads, 0, st, a64, lk, lv, M, nl);
         check_launch();
         d2h(hcnt, cnt, 1);  // also keeps off / hi / hw alive until the copies completed
       }
@@ -865,9 +880,19 @@ struct Pipeline {
       sa.hb_end = hend;
       sa.snap = C->get<uint2>("snap", snap_entries);
       GW_LAUNCH(k_walker_snap, std::min<uint32_t>(tr.B, (uint32_t)gmax), kThreads, 0, st, w, sa);
-      GW_LAUNCH(k_stamp, grid_for(N), kThreads, 0, st, w, sa);
+      // no per-access stamp pass: the check looks stamps up in the snapshots
+      stamps.time = nullptr;
+      stamps.vobj = nullptr;
+      stamps.hard_ev = sa.hard_ev;
+      stamps.hb_beg = sa.hb_beg;
+      stamps.hb_end = sa.hb_end;
+      stamps.snap = sa.snap;
+      stamps.BS = tr.BS;
       C->stats.walker_ctas = std::min<uint32_t>(tr.B, (uint32_t)gmax);
     } else {
+      stamps.time = w.time;
+      stamps.vobj = w.vobj;
+      stamps.BS = tr.BS;
       const bool prof = getenv("GW_PROF_WALKER") != nullptr;
       if (prof) {
         w.prof = C->get<unsigned long long>("prof", (uint64_t)G * 8);
