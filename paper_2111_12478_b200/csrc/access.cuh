@@ -139,7 +139,27 @@ __global__ void k_compact_u64(const unsigned long long* in, uint64_t n, KeyRuns 
 // stats over the trace (one pass): counts by kind, OR / AND of access keys
 struct Stats {
   unsigned long long n_acc, n_write, n_acq, n_rel, n_end, n_bar, key_or, key_and;
+  unsigned long long n_long;  // windows proving a record longer than 32 events
 };
+// 32 consecutive continues-record events end in this warp's aligned 32-event
+// window <=> some record has more than 32 events
+__global__ void __launch_bounds__(kThreads) k_long_records(DevTrace tr, Stats* st) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long found = 0;
+  for (uint64_t wb = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; wb < tr.n; wb += nwarps * 32) {
+    const uint64_t e = wb + lane;
+    const bool c = e < tr.n && (tr.tidop[e] & GW_F_CONT);
+    const uint32_t cur = __ballot_sync(0xffffffffu, c);
+    if (cur == 0) continue;
+    const bool pc = wb >= 32 && (tr.tidop[e - 32] & GW_F_CONT);
+    const uint32_t prev = __ballot_sync(0xffffffffu, pc);
+    unsigned long long y = ((unsigned long long)cur << 32) | prev;
+    y &= y >> 1; y &= y >> 2; y &= y >> 4; y &= y >> 8; y &= y >> 16;  // bit i: bits i..i+31 all set
+    if ((y >> 1) & 0xFFFFFFFFull) found++;
+  }
+  if (lane == 0 && found) atomicAdd(&st->n_long, found);
+}
 __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
   unsigned long long v[6] = {0, 0, 0, 0, 0, 0};  // acc, write, acq, rel, end, bar
   unsigned long long ko = 0, ka = ~0ull;
@@ -225,6 +245,13 @@ __device__ __forceinline__ bool cover(uint32_t toa, uint32_t tob, uint32_t BS) {
   return ev_tid(toa) / BS == ev_tid(tob) / BS;
 }
 
+// same-record pairs on one location flagged by k_access (see k_dup_heads)
+struct DupList {
+  uint32_t* ev;
+  uint32_t* n;
+  uint32_t cap;
+};
+
 // Access-time stamps (time = local_t at the access, vobj = t's pred object):
 // arrays written by the walker, or -- lock-free snapshot mode -- looked up in
 // the walker's per-block snapshots: snapshot k of block b = the block's
@@ -282,6 +309,7 @@ struct AccArgs {
   uint32_t* large_ws;
   uint32_t* n_large;
   uint32_t large_cap;
+  DupList dup;            // same-record pairs on one location (same-instruction check)
 };
 
 template <class K>
@@ -399,6 +427,20 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
             lo[k] = b0[k];
             hi[k] = __ldg(a.src.hb_end + bb[k]);
           }
+          // #hard events of the block before e: blocks with <= 16 hard events
+          // count them with independent loads (one round trip), others bisect
+          constexpr uint32_t kLin = 16;
+          uint32_t cntb[kAccItems];
+#pragma unroll
+          for (int k = 0; k < kAccItems; k++) {
+            cntb[k] = 0;
+            if (hi[k] - lo[k] <= kLin) {
+#pragma unroll
+              for (uint32_t x = 0; x < kLin; x++)
+                if (lo[k] + x < hi[k] && __ldg(a.src.hard_ev + lo[k] + x) < e[k]) cntb[k]++;
+              hi[k] = lo[k];  // done
+            }
+          }
           bool any = true;
           while (any) {
             any = false;
@@ -411,6 +453,8 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
               }
             }
           }
+#pragma unroll
+          for (int k = 0; k < kAccItems; k++) lo[k] += cntb[k];
 #pragma unroll
           for (int k = 0; k < kAccItems; k++)
             sv[k] = a.src.snap[(size_t)(lo[k] + bb[k]) * BS + (ev_tid(tt[k]) - bb[k] * BS)];
@@ -473,6 +517,19 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
       const uint32_t W = hasw ? lw - 1 : NIL;
       const uint32_t vo = a.defer ? NIL : S.st[j].y;
       unsigned long long loc = 0;
+      if (i > ss && (toc & GW_F_CONT) && a.dup.ev) {
+        // the previous access to this location may be in the same record
+        uint32_t pe, pto;
+        acc_pos(a, S, base, i - 1, pe, pto);
+        if (pe < c && c - pe < 32) {
+          bool same = true;
+          for (uint32_t x = pe + 1; x < c && same; x++) same = (__ldg(a.tr.tidop + x) & GW_F_CONT) != 0;
+          if (same) {
+            const uint32_t kk = atomicAdd(a.dup.n, 1u);
+            if (kk < a.dup.cap) a.dup.ev[kk] = c;
+          }
+        }
+      }
       if (hasw) {
         uint32_t p, top;
         acc_pos(a, S, base, W, p, top);
@@ -642,7 +699,68 @@ __device__ void same_instr_long(const DevTrace& tr, const Cands& cd, uint64_t he
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd, ShardArgs sa) {
+// one record (head = its first event, a WRITE followed by CONT events); the
+// whole warp calls it.  long_only: skip records of <= 32 events.
+__device__ void same_instr_record(const DevTrace& tr, const Cands& cd, const ShardArgs& sa, uint64_t head,
+                                  bool long_only) {
+  const int lane = threadIdx.x & 31;
+  // load the record, 32 events at a time
+  const uint64_t x = head + lane;
+  const bool inr = x < tr.n;
+  const uint32_t tx = inr ? tr.tidop[x] : 0u;
+  const uint32_t ix = inr ? tr.instr[x] : 0u;
+  const unsigned long long kx0 = inr ? tr.key[x] : 0ull;
+  const uint32_t cm = __ballot_sync(0xffffffffu, inr && (tx & GW_F_CONT)) | 1u;  // lane 0 is the head
+  const uint32_t stop = ~cm;                                                    // first non-CONT lane
+  const int len = stop ? __ffs(stop) - 1 : 32;
+  const uint32_t tprev = __shfl_up_sync(0xffffffffu, tx, 1);
+  const uint32_t iprev = __shfl_up_sync(0xffffffffu, ix, 1);
+  const bool stepok = lane == 0 || lane >= len || rec_uniform_step(tprev, tx, iprev, ix, tr.BS);
+  bool uni = __all_sync(0xffffffffu, stepok);
+  if (len == 32 && head + 32 < tr.n && (tr.tidop[head + 32] & GW_F_CONT)) {
+    // long record (> 32 events): per-event scan, record by record
+    uint64_t end = head + 32;
+    while (end < tr.n && (tr.tidop[end] & GW_F_CONT)) end++;
+    if (end - head >= 32768) {
+      if (lane == 0) atomicOr(cd.err, ERR_RECORD);
+      return;
+    }
+    bool u2 = uni;
+    for (uint64_t c = head + 32 + lane; c < end; c += 32)
+      u2 = u2 && rec_uniform_step(tr.tidop[c - 1], tr.tidop[c], tr.instr[c - 1], tr.instr[c], tr.BS);
+    uni = __all_sync(0xffffffffu, u2);
+    for (uint64_t j = head + 1 + lane; j < end; j += 32) same_instr_long(tr, cd, head, end, j, uni, sa);
+    return;
+  }
+  if (long_only) return;
+  const bool acc = lane < len && ev_kind(tx) <= GW_K_WRITE;
+  const unsigned long long kx = acc ? kx0 : 0ull;
+  const bool mine = in_shard(kx, sa);
+  const uint32_t accm = __ballot_sync(0xffffffffu, acc);
+  const uint32_t peers = __match_any_sync(0xffffffffu, kx) & accm;
+  const uint32_t earlier = peers & lanemask_lt();
+  if (!acc || !earlier || !mine) return;
+  if (uni) {
+    if (__popc(earlier) != 1) return;  // not the second occurrence of this location
+    const int fl = __ffs(earlier) - 1;
+    const uint32_t tf = tr.tidop[head + fl];
+    if (ev_tid(tf) != ev_tid(tx) && !cover(tf, tx, tr.BS))
+      emit_cand(cd, ((unsigned long long)head << 32) | sub_pair(fl, lane), kx, (uint32_t)(head + fl), (uint32_t)x,
+                GW_WW);
+  } else {
+    for (uint32_t m = earlier; m; m &= m - 1) {
+      const int il = __ffs(m) - 1;
+      const uint32_t ti = tr.tidop[head + il];
+      if (ev_tid(ti) != ev_tid(tx) && !cover(ti, tx, tr.BS))
+        emit_cand(cd, ((unsigned long long)head << 32) | sub_pair(il, lane), kx, (uint32_t)(head + il),
+                  (uint32_t)x, GW_WW);
+    }
+  }
+}
+
+// every record of the trace (traces with records longer than 32 events, and
+// lock mode); long_only: only those (the others come from the head list)
+__global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd, ShardArgs sa, int long_only) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t wb = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; wb < tr.n; wb += nwarps * 32) {
@@ -657,59 +775,39 @@ __global__ void __launch_bounds__(kThreads) k_same_instr(DevTrace tr, Cands cd, 
     while (heads) {
       const int hl = __ffs(heads) - 1;
       heads &= heads - 1;
-      const uint64_t head = wb + hl;
-      // load the record, 32 events at a time
-      const uint64_t x = head + lane;
-      const bool inr = x < tr.n;
-      const uint32_t tx = inr ? tr.tidop[x] : 0u;
-      const uint32_t cm = __ballot_sync(0xffffffffu, inr && (tx & GW_F_CONT)) | 1u;  // lane 0 is the head
-      const uint32_t stop = ~cm;                                                    // first non-CONT lane
-      const int len = stop ? __ffs(stop) - 1 : 32;
-      const uint32_t ix = inr ? tr.instr[x] : 0u;
-      const uint32_t tprev = __shfl_up_sync(0xffffffffu, tx, 1);
-      const uint32_t iprev = __shfl_up_sync(0xffffffffu, ix, 1);
-      const bool stepok = lane == 0 || lane >= len || rec_uniform_step(tprev, tx, iprev, ix, tr.BS);
-      bool uni = __all_sync(0xffffffffu, stepok);
-      if (len == 32 && head + 32 < tr.n && (tr.tidop[head + 32] & GW_F_CONT)) {
-        // long record (> 32 events): per-event scan, record by record
-        uint64_t end = head + 32;
-        while (end < tr.n && (tr.tidop[end] & GW_F_CONT)) end++;
-        if (end - head >= 32768) {
-          if (lane == 0) atomicOr(cd.err, ERR_RECORD);
-          continue;
-        }
-        bool u2 = uni;
-        for (uint64_t c = head + 32 + lane; c < end; c += 32)
-          u2 = u2 && rec_uniform_step(tr.tidop[c - 1], tr.tidop[c], tr.instr[c - 1], tr.instr[c], tr.BS);
-        uni = __all_sync(0xffffffffu, u2);
-        for (uint64_t j = head + 1 + lane; j < end; j += 32) same_instr_long(tr, cd, head, end, j, uni, sa);
-        continue;
-      }
-          const bool acc = lane < len && ev_kind(tx) <= GW_K_WRITE;
-      const unsigned long long kx = acc ? tr.key[x] : 0ull;
-      const bool mine = in_shard(kx, sa);
-      const uint32_t accm = __ballot_sync(0xffffffffu, acc);
-      const uint32_t peers = __match_any_sync(0xffffffffu, kx) & accm;
-      const uint32_t earlier = peers & lanemask_lt();
-      if (!acc || !earlier || !mine) continue;
-      if (uni) {
-        if (__popc(earlier) != 1) continue;  // not the second occurrence of this location
-        const int fl = __ffs(earlier) - 1;
-        const uint32_t tf = tr.tidop[head + fl];
-        if (ev_tid(tf) != ev_tid(tx) && !cover(tf, tx, tr.BS))
-          emit_cand(cd, ((unsigned long long)head << 32) | sub_pair(fl, lane), kx, (uint32_t)(head + fl),
-                    (uint32_t)x, GW_WW);
-      } else {
-        for (uint32_t m = earlier; m; m &= m - 1) {
-          const int il = __ffs(m) - 1;
-          const uint32_t ti = tr.tidop[head + il];
-          if (ev_tid(ti) != ev_tid(tx) && !cover(ti, tx, tr.BS))
-            emit_cand(cd, ((unsigned long long)head << 32) | sub_pair(il, lane), kx, (uint32_t)(head + il),
-                      (uint32_t)x, GW_WW);
-        }
-      }
+      same_instr_record(tr, cd, sa, wb + hl, long_only != 0);
     }
   }
+}
+
+// Same-record pairs on one location are adjacent in location order (a
+// record's events are contiguous in the trace), so k_access flags them:
+// DupList collects the current events; k_dup_heads maps them to their
+// records' heads (deduplicated through a small hash set) and
+// k_same_instr_heads runs the record check on those records only.  Valid
+// when no record is longer than 32 events (Stats::n_long == 0).
+__global__ void k_dup_heads(DevTrace tr, DupList d, uint32_t* hset, uint32_t hmask, uint32_t* heads,
+                            uint32_t* nheads) {
+  const uint32_t n = min(*d.n, d.cap);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    uint64_t h = d.ev[k];
+    while (h > 0 && (tr.tidop[h] & GW_F_CONT)) h--;
+    if (ev_kind(tr.tidop[h]) != GW_K_WRITE) continue;  // _same_instruction_check: WRITE records only
+    uint32_t slot = (uint32_t)mix64(h) & hmask;
+    while (true) {
+      const uint32_t old = atomicCAS(&hset[slot], 0u, (uint32_t)h + 1);
+      if (old == 0) { heads[atomicAdd(nheads, 1u)] = (uint32_t)h; break; }
+      if (old == (uint32_t)h + 1) break;
+      slot = (slot + 1) & hmask;
+    }
+  }
+}
+__global__ void __launch_bounds__(kThreads) k_same_instr_heads(DevTrace tr, Cands cd, ShardArgs sa,
+                                                              const uint32_t* heads, const uint32_t* nheads) {
+  const uint32_t n = *nheads;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps)
+    same_instr_record(tr, cd, sa, heads[k], false);
 }
 
 // ------------------------------------------------------------- dedup -----

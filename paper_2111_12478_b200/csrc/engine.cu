@@ -162,7 +162,7 @@ namespace {
 
 // scalar slots of the "scalars" buffer
 enum : int { SC_MAXD = 0, SC_NINCS, SC_TICKET, SC_REC, SC_LOG, SC_DIAG, SC_ERR, SC_ABORT, SC_NCAND, SC_NLARGE,
-             SC_NSURV, SC_NQ, SC_NQLARGE, SC_COUNT = 16 };
+             SC_NSURV, SC_NQ, SC_NQLARGE, SC_NDUP, SC_NHEADS, SC_COUNT = 16 };
 
 __global__ void k_init_stats(Stats* s) {
   memset(s, 0, sizeof(Stats));
@@ -171,12 +171,13 @@ __global__ void k_init_stats(Stats* s) {
 // graph mode: the trace must have the shape the plan was built for
 __global__ void k_plan_check(const Stats* s, unsigned long long n_bar, unsigned long long n_end,
                              unsigned long long D, uint32_t* abort_flag) {
-  const bool ok = s->n_acq == 0 && s->n_rel == 0 && s->n_bar == n_bar && s->n_end == n_end &&
+  const bool ok = s->n_acq == 0 && s->n_rel == 0 && s->n_bar == n_bar && s->n_end == n_end && s->n_long == 0 &&
                   ((s->key_or ^ s->key_and) & ~D) == 0ull;
   if (!ok) atomicOr(abort_flag, 1u);
 }
-__global__ void k_guard(const uint32_t* ncand, uint32_t cap, const uint32_t* nlarge, uint32_t* abort_flag) {
-  if (*ncand > cap || *nlarge > 0) atomicOr(abort_flag, 1u);
+__global__ void k_guard(const uint32_t* ncand, uint32_t cap, const uint32_t* nlarge, const uint32_t* ndup,
+                        uint32_t dupcap, uint32_t* abort_flag) {
+  if (*ncand > cap || *nlarge > 0 || *ndup > dupcap) atomicOr(abort_flag, 1u);
 }
 
 struct Pipeline {
@@ -338,6 +339,7 @@ struct Pipeline {
     Stats* dst = C->get<Stats>("stats", 1);
     GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
     GW_LAUNCH(k_prep, grid_for(N), kThreads, 0, st, tr, dst);
+    GW_LAUNCH(k_long_records, grid_for(N), kThreads, 0, st, tr, dst);
     check_launch();
     if (gmode) {
       memset(&hs, 0, sizeof hs);
@@ -468,6 +470,30 @@ struct Pipeline {
   uint32_t* vals = nullptr;  // access pass: sorted event indices
   void* skeys = nullptr;
   uint2* carry = nullptr;     // per sorted tile: max (segment head, write position) of the earlier tiles
+  DupList dup{};              // same-record pairs flagged by the access check
+
+  // _same_instruction_check (engine.py:81-95): from the flagged records, or a
+  // scan of every record when a record is longer than 32 events or the flag
+  // list overflowed (eager runs; graph replays abort on overflow instead)
+  void same_instr_pass(const Cands& cd) {
+    bool list = dup.ev != nullptr;
+    if (list && !gmode) {
+      uint32_t nd = 0;
+      d2h(&nd, dup.n);
+      list = nd <= dup.cap;
+    }
+    if (!list) {
+      GW_LAUNCH(k_same_instr, grid_for(tr.n), kThreads, 0, st, tr, cd, shard_args(), 0);
+      return;
+    }
+    const uint64_t hcap = pow2_at_least(2ull * dup.cap + 2);
+    uint32_t* hset = C->get<uint32_t>("dup_hset", hcap);
+    uint32_t* heads = C->get<uint32_t>("dup_heads", dup.cap + 1);
+    CK(cudaMemsetAsync(hset, 0, sizeof(uint32_t) * hcap, st));
+    CK(cudaMemsetAsync(scal + SC_NHEADS, 0, sizeof(uint32_t), st));
+    GW_LAUNCH(k_dup_heads, 148u * 4, kThreads, 0, st, tr, dup, hset, (uint32_t)(hcap - 1), heads, scal + SC_NHEADS);
+    GW_LAUNCH(k_same_instr_heads, 148u * 4, kThreads, 0, st, tr, cd, shard_args(), heads, scal + SC_NHEADS);
+  }
   StampSrc stamps{};          // where the check pass reads access stamps
   uint64_t obs_nq = 0;
   uint32_t shard = 0, nshard = 1;  // address sharding (gw_opts)
@@ -661,6 +687,15 @@ struct Pipeline {
       cd = make_cands(tag, cand_cap, cnt);
       CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t), st));
       if (!defer) CK(cudaMemsetAsync(scal + SC_NSURV, 0, sizeof(uint32_t), st));
+      // same-record pairs on one location, flagged by the access check (no record > 32 events)
+      dup.ev = nullptr;
+      dup.n = scal + SC_NDUP;
+      dup.cap = 0;
+      if (hs.n_long == 0) {
+        dup.cap = (uint32_t)std::max<uint64_t>(4096, NA / 64);
+        dup.ev = C->get<uint32_t>("dup_ev", dup.cap);
+      }
+      CK(cudaMemsetAsync(scal + SC_NDUP, 0, 2 * sizeof(uint32_t), st));
       auto fill = [&](auto& aa, const auto* kp) {
         memset(&aa, 0, sizeof aa);
         aa.tr = tr;
@@ -677,6 +712,7 @@ struct Pipeline {
         aa.large_ws = large_ws;
         aa.n_large = cnt + 1;
         aa.large_cap = (uint32_t)(NA / kSmallWin + 1);
+        aa.dup = dup;
       };
       const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>((NA + kAccTile - 1) / kAccTile, 1),
                                                        148ull * 16);
@@ -689,12 +725,13 @@ struct Pipeline {
         acc_setup<unsigned long long>();
         GW_LAUNCH(k_access<unsigned long long>, ag, kThreads, sizeof(AccSmem<unsigned long long>), st, a64);
       }
-      if (!defer) GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd, shard_args());
       check_launch();
       if (gmode) {
-        GW_LAUNCH(k_guard, 1, 1, 0, st, cnt, cd.cap, cnt + 1, scal + SC_ABORT);
+        if (!defer) same_instr_pass(cd);
+        GW_LAUNCH(k_guard, 1, 1, 0, st, cnt, cd.cap, cnt + 1, scal + SC_NDUP, dup.cap, scal + SC_ABORT);
         break;
       }
+      if (!defer) same_instr_pass(cd);
       d2h(hcnt, cnt, 2);
       if (hcnt[1] > 0) {
         // large reader windows (> kSmallWin reads between two writes)
@@ -773,7 +810,7 @@ struct Pipeline {
       cd = make_cands("c", cap, cnt);
       CK(cudaMemsetAsync(cnt, 0, 3 * sizeof(uint32_t), st));
       if (nq) GW_LAUNCH(k_resolve, grid_for(nq), kThreads, 0, st, cq, w.qv, w.time, cd);
-      GW_LAUNCH(k_same_instr, grid_for(N), kThreads, 0, st, tr, cd, shard_args());
+      same_instr_pass(cd);
       check_launch();
       d2h(&hc, cnt);
       if (hc <= cd.cap) break;
@@ -1014,7 +1051,7 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   p.shard = shard;
   p.nshard = nshard;
   p.run();
-  if (eager || tr.n == 0 || !p.obs_snap || p.obs_nlarge > 0 || st == 0) return;
+  if (eager || tr.n == 0 || !p.obs_snap || p.obs_nlarge > 0 || p.obs.n_long > 0 || st == 0) return;
   // build the plan; run the graph-mode pipeline once for real (allocates every
   // buffer at its final size), then capture it
   Plan np;
