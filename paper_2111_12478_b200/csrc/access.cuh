@@ -36,15 +36,50 @@ struct KeyRuns {  // compacted location key = concatenation of the varying bit r
   int sentinel;  // non-access events carry bit nbits-1
 };
 
+// Access-time stamps (time = local_t at the access, vobj = t's pred object):
+// arrays written by the walker, or -- lock-free snapshot mode -- looked up in
+// the walker's per-block snapshots: snapshot k of block b = the block's
+// state after its k-th hard event (k = #hard events of b before e).
+struct StampSrc {  // valid() false in lock mode (the walker runs after the access pass)
+  const uint32_t* time;  // arrays (nullptr: snapshots)
+  const uint32_t* vobj;
+  const uint32_t* hard_ev;
+  const uint32_t* hb_beg;
+  const uint32_t* hb_end;
+  const uint2* snap;
+  uint32_t BS;
+  __device__ __forceinline__ bool valid() const { return time != nullptr || snap != nullptr; }
+  __device__ __forceinline__ uint2 get(uint32_t e, uint32_t t) const {
+    if (time) return make_uint2(__ldg(time + e), __ldg(vobj + e));
+    const uint32_t b = t / BS;
+    const uint32_t base = __ldg(hb_beg + b);
+    uint32_t lo = base, hi = __ldg(hb_end + b);
+    while (lo < hi) {
+      const uint32_t m = (lo + hi) >> 1;
+      if (__ldg(hard_ev + m) < e) lo = m + 1; else hi = m;
+    }
+    return snap[(size_t)(base + b + (lo - base)) * BS + (t - b * BS)];
+  }
+};
+
 // Non-access events get the sentinel key (bit nbits-1, one past the varying
 // location bits) and sort last; in the corner case of 64 varying bits there is
 // no spare bit and they take key 0 instead.  Either way every access-pass
 // kernel skips them.
+// Also writes aux[e] = (tidop, time, vobj) for the access pass: in trace order
+// the stamp lookups of a warp hit one block's snapshot list, and the check
+// later fetches everything it needs about an access with ONE 16-byte gather.
+__device__ __forceinline__ uint4 make_aux(const StampSrc& src, uint32_t e, uint32_t to) {
+  uint2 st = make_uint2(0u, NIL);
+  if (ev_kind(to) <= GW_K_WRITE && src.valid()) st = src.get(e, ev_tid(to));
+  return make_uint4(to, st.x, st.y, 0u);
+}
 template <class K>
-__global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals) {
+__global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals, StampSrc src, uint4* aux) {
   const K sentinel = kr.sentinel ? ((K)1 << (kr.nbits - 1)) : (K)0;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t to = tr.tidop[e];
+    aux[e] = make_aux(src, (uint32_t)e, to);
     K k = sentinel;
     if (ev_kind(to) <= GW_K_WRITE) {
       unsigned long long x = tr.key[e];
@@ -85,7 +120,8 @@ __device__ __forceinline__ bool in_shard(unsigned long long loc, const ShardArgs
 // (compacted location key, event) in trace order
 template <class K, bool EMIT>
 __global__ void __launch_bounds__(kThreads) k_shard_accesses(DevTrace tr, ShardArgs sa, uint32_t* tilecnt,
-                                                            const uint32_t* tileoff, K* keys, uint32_t* vals) {
+                                                            const uint32_t* tileoff, K* keys, uint32_t* vals,
+                                                            StampSrc src, uint4* aux) {
   __shared__ uint32_t s_w[kThreads / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = lanemask_lt();
@@ -114,8 +150,10 @@ __global__ void __launch_bounds__(kThreads) k_shard_accesses(DevTrace tr, ShardA
       }
       if (EMIT && in) {
         const uint32_t pos = run + woff + __popc(m & lt);
+        const uint32_t to = tr.tidop[e];
         keys[pos] = (K)ck;
-        vals[pos] = (uint32_t)e | (ev_kind(tr.tidop[e]) == GW_K_WRITE ? VAL_W : 0u);
+        vals[pos] = (uint32_t)e | (ev_kind(to) == GW_K_WRITE ? VAL_W : 0u);
+        aux[e] = make_aux(src, (uint32_t)e, to);
       }
       run += tot;
       __syncthreads();
@@ -141,31 +179,15 @@ struct Stats {
   unsigned long long n_acc, n_write, n_acq, n_rel, n_end, n_bar, key_or, key_and;
   unsigned long long n_long;  // windows proving a record longer than 32 events
 };
-// 32 consecutive continues-record events end in this warp's aligned 32-event
-// window <=> some record has more than 32 events
-__global__ void __launch_bounds__(kThreads) k_long_records(DevTrace tr, Stats* st) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long found = 0;
-  for (uint64_t wb = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; wb < tr.n; wb += nwarps * 32) {
-    const uint64_t e = wb + lane;
-    const bool c = e < tr.n && (tr.tidop[e] & GW_F_CONT);
-    const uint32_t cur = __ballot_sync(0xffffffffu, c);
-    if (cur == 0) continue;
-    const bool pc = wb >= 32 && (tr.tidop[e - 32] & GW_F_CONT);
-    const uint32_t prev = __ballot_sync(0xffffffffu, pc);
-    unsigned long long y = ((unsigned long long)cur << 32) | prev;
-    y &= y >> 1; y &= y >> 2; y &= y >> 4; y &= y >> 8; y &= y >> 16;  // bit i: bits i..i+31 all set
-    if ((y >> 1) & 0xFFFFFFFFull) found++;
-  }
-  if (lane == 0 && found) atomicAdd(&st->n_long, found);
-}
 __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
   unsigned long long v[6] = {0, 0, 0, 0, 0, 0};  // acc, write, acq, rel, end, bar
-  unsigned long long ko = 0, ka = ~0ull;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t to = tr.tidop[e];
-    const uint32_t k = ev_kind(to);
+  unsigned long long ko = 0, ka = ~0ull, nlong = 0;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < tr.n;
+       e0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = e0 + lane;  // warp = one aligned 32-event window
+    const uint32_t to = e < tr.n ? tr.tidop[e] : 0u;
+    const uint32_t k = e < tr.n ? ev_kind(to) : 7u;
     if (k <= GW_K_WRITE) {
       const unsigned long long x = tr.key[e];
       v[0]++; v[1] += k; ko |= x; ka &= x;
@@ -173,7 +195,18 @@ __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
     else if (k == GW_K_RELEASE) v[3]++;
     else if (k == GW_K_END) v[4]++;
     else if (k == GW_K_BARRIER) v[5]++;
+    // records longer than 32 events: 32 consecutive continues-record events ending in this window
+    const uint32_t cur = __ballot_sync(0xffffffffu, (to & GW_F_CONT) != 0);
+    if (cur == 0xffffffffu) {
+      if (lane == 0) nlong++;  // a whole window of continuations: the record has > 32 events
+    } else if (cur & 1u) {    // a run entering the window: add the previous window's trailing run
+      const uint32_t prev = __ballot_sync(0xffffffffu, e0 >= 32 && (tr.tidop[e - 32] & GW_F_CONT));
+      unsigned long long y = ((unsigned long long)cur << 32) | prev;
+      y &= y >> 1; y &= y >> 2; y &= y >> 4; y &= y >> 8; y &= y >> 16;  // bit i: bits i..i+31 all set
+      if (lane == 0 && ((y >> 1) & 0xFFFFFFFFull)) nlong++;
+    }
   }
+  if (lane == 0 && nlong) atomicAdd(&st->n_long, nlong);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
@@ -252,39 +285,14 @@ struct DupList {
   uint32_t cap;
 };
 
-// Access-time stamps (time = local_t at the access, vobj = t's pred object):
-// arrays written by the walker, or -- lock-free snapshot mode -- looked up in
-// the walker's per-block snapshots: snapshot k of block b = the block's
-// state after its k-th hard event (k = #hard events of b before e).
-struct StampSrc {
-  const uint32_t* time;  // arrays (nullptr: snapshots)
-  const uint32_t* vobj;
-  const uint32_t* hard_ev;
-  const uint32_t* hb_beg;
-  const uint32_t* hb_end;
-  const uint2* snap;
-  uint32_t BS;
-  __device__ __forceinline__ uint2 get(uint32_t e, uint32_t t) const {
-    if (time) return make_uint2(__ldg(time + e), __ldg(vobj + e));
-    const uint32_t b = t / BS;
-    const uint32_t base = __ldg(hb_beg + b);
-    uint32_t lo = base, hi = __ldg(hb_end + b);
-    while (lo < hi) {
-      const uint32_t m = (lo + hi) >> 1;
-      if (__ldg(hard_ev + m) < e) lo = m + 1; else hi = m;
-    }
-    return snap[(size_t)(base + b + (lo - base)) * BS + (t - b * BS)];
-  }
-};
-
 // The access check (gwcp.py:251-277) over the location-sorted accesses, one
 // tile of kAccTile sorted positions per CTA:
 //   * segment head / last write before each position: a tile-local max-scan
 //     seeded with the maxima of all earlier tiles (k_acc_tilemax + a scan
 //     over tiles), no per-position scan arrays in HBM;
-//   * the tile's event indices, tidops (one gather) and access stamps
-//     (batched lookups, all positions' loads in flight together) staged in
-//     smem, so the prior write and the reader window are mostly smem reads;
+//   * the tile's event indices and (tidop, time, vobj) -- one 16-byte
+//     gather per access -- staged in smem, so the prior write and the reader
+//     window are mostly smem reads;
 //   * the clock test is one gather pred_t^{ver}[u]; lock-free clock objects
 //     are block-range objects of the accessing thread's block (the barrier
 //     hull never leaves it), so the header need not be read.
@@ -300,7 +308,7 @@ struct AccArgs {
   const uint32_t* vals;   // sorted event | VAL_W
   uint64_t n;             // sorted positions
   const uint2* carry;     // per tile: max (head pos + 1, write pos + 1) over all earlier tiles
-  StampSrc src;
+  const uint4* aux;       // per event: (tidop, time, vobj) -- see k_acc_keys
   const uint32_t* arena;
   int defer;
   int blockobj;           // clock objects are block-range objects (lock-free traces)
@@ -360,13 +368,13 @@ __device__ __forceinline__ void acc_pos(const AccArgs<K>& a, const AccSmem<K>& S
     to = S.to[q - base];
   } else {
     ev = __ldg(a.vals + q) & VAL_E;
-    to = __ldg(a.tr.tidop + ev);
+    to = __ldg(&a.aux[ev].x);
   }
 }
 template <class K>
 __device__ __forceinline__ uint32_t acc_time(const AccArgs<K>& a, const AccSmem<K>& S, uint64_t base, uint64_t q,
-                                             uint32_t ev, uint32_t tid) {
-  return q >= base ? S.st[q - base].x : a.src.get(ev, tid).x;
+                                             uint32_t ev, uint32_t) {
+  return q >= base ? S.st[q - base].x : __ldg(&a.aux[ev].y);
 }
 // pred_t^{vo}[u] for the accessing thread tc
 template <class K>
@@ -395,75 +403,16 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
     }
     const K prevkey = base > 0 ? a.keys[base - 1] : (K)0;
     {
-      uint32_t tt[kAccItems];
+      uint4 ax[kAccItems];
 #pragma unroll
       for (int k = 0; k < kAccItems; k++) {
         const uint32_t j = k * kThreads + threadIdx.x;
-        tt[k] = j < cnt ? __ldg(a.tr.tidop + (a.vals[base + j] & VAL_E)) : 0u;
+        ax[k] = j < cnt ? a.aux[a.vals[base + j] & VAL_E] : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int k = 0; k < kAccItems; k++) {
         const uint32_t j = k * kThreads + threadIdx.x;
-        if (j < cnt) S.to[j] = tt[k];
-      }
-      if (!a.defer) {
-        // stamps of every position: the lookups of all items interleaved
-        uint2 sv[kAccItems];
-        if (a.src.time) {
-#pragma unroll
-          for (int k = 0; k < kAccItems; k++) {
-            const uint32_t j = k * kThreads + threadIdx.x;
-            const uint32_t e = j < cnt ? (a.vals[base + j] & VAL_E) : 0u;
-            sv[k] = make_uint2(__ldg(a.src.time + e), __ldg(a.src.vobj + e));
-          }
-        } else {
-          uint32_t e[kAccItems], lo[kAccItems], hi[kAccItems], bb[kAccItems], b0[kAccItems];
-#pragma unroll
-          for (int k = 0; k < kAccItems; k++) {
-            const uint32_t j = k * kThreads + threadIdx.x;
-            e[k] = j < cnt ? (a.vals[base + j] & VAL_E) : 0u;
-            bb[k] = ev_tid(tt[k]) / BS;
-            b0[k] = __ldg(a.src.hb_beg + bb[k]);
-            lo[k] = b0[k];
-            hi[k] = __ldg(a.src.hb_end + bb[k]);
-          }
-          // #hard events of the block before e: blocks with <= 16 hard events
-          // count them with independent loads (one round trip), others bisect
-          constexpr uint32_t kLin = 16;
-          uint32_t cntb[kAccItems];
-#pragma unroll
-          for (int k = 0; k < kAccItems; k++) {
-            cntb[k] = 0;
-            if (hi[k] - lo[k] <= kLin) {
-#pragma unroll
-              for (uint32_t x = 0; x < kLin; x++)
-                if (lo[k] + x < hi[k] && __ldg(a.src.hard_ev + lo[k] + x) < e[k]) cntb[k]++;
-              hi[k] = lo[k];  // done
-            }
-          }
-          bool any = true;
-          while (any) {
-            any = false;
-#pragma unroll
-            for (int k = 0; k < kAccItems; k++) {
-              if (lo[k] < hi[k]) {
-                const uint32_t m = (lo[k] + hi[k]) >> 1;
-                if (__ldg(a.src.hard_ev + m) < e[k]) lo[k] = m + 1; else hi[k] = m;
-                any = true;
-              }
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < kAccItems; k++) lo[k] += cntb[k];
-#pragma unroll
-          for (int k = 0; k < kAccItems; k++)
-            sv[k] = a.src.snap[(size_t)(lo[k] + bb[k]) * BS + (ev_tid(tt[k]) - bb[k] * BS)];
-        }
-#pragma unroll
-        for (int k = 0; k < kAccItems; k++) {
-          const uint32_t j = k * kThreads + threadIdx.x;
-          if (j < cnt) S.st[j] = sv[k];
-        }
+        if (j < cnt) { S.to[j] = ax[k].x; S.st[j] = make_uint2(ax[k].y, ax[k].z); }
       }
     }
     __syncthreads();
@@ -652,7 +601,7 @@ __global__ void k_large_check(AccArgs<K> a, const unsigned long long* keys, cons
     const uint32_t toq = a.tr.tidop[r], uq = ev_tid(toq);
     if (uq == ev_tid(toc)) continue;
     if (!cover(toq, toc, BS) &&
-        (a.defer || a.src.get(r, uq).x > acc_clock(a, a.src.get(c, ev_tid(toc)).y, ev_tid(toc), uq)))
+        (a.defer || a.aux[r].y > acc_clock(a, a.aux[c].z, ev_tid(toc), uq)))
       emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), a.tr.key[c], r, c, GW_RW);
   }
 }

@@ -339,7 +339,6 @@ struct Pipeline {
     Stats* dst = C->get<Stats>("stats", 1);
     GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
     GW_LAUNCH(k_prep, grid_for(N), kThreads, 0, st, tr, dst);
-    GW_LAUNCH(k_long_records, grid_for(N), kThreads, 0, st, tr, dst);
     check_launch();
     if (gmode) {
       memset(&hs, 0, sizeof hs);
@@ -494,7 +493,8 @@ struct Pipeline {
     GW_LAUNCH(k_dup_heads, 148u * 4, kThreads, 0, st, tr, dup, hset, (uint32_t)(hcap - 1), heads, scal + SC_NHEADS);
     GW_LAUNCH(k_same_instr_heads, 148u * 4, kThreads, 0, st, tr, cd, shard_args(), heads, scal + SC_NHEADS);
   }
-  StampSrc stamps{};          // where the check pass reads access stamps
+  StampSrc stamps{};          // where the access pass reads access stamps (walker output)
+  uint4* aux = nullptr;       // per event (tidop, time, vobj)
   uint64_t obs_nq = 0;
   uint32_t shard = 0, nshard = 1;  // address sharding (gw_opts)
   uint64_t na_sorted = 0;          // positions the access pass sorts (N, or this shard's accesses)
@@ -590,6 +590,7 @@ struct Pipeline {
     obs_D = hs.n_acc ? hs.key_or ^ hs.key_and : 0ull;
     int nbits = kr.nbits;
     uint64_t NA = N;
+    aux = C->get<uint4>("acc_aux", N);
     if (nshard <= 1) {
       // All N positions are sorted; non-access events carry the top sentinel
       // key and sort last, and every access-pass kernel skips them, so no
@@ -597,11 +598,11 @@ struct Pipeline {
       vals = C->get<uint32_t>("acc_v", N);
       if (!wide) {
         uint32_t* k32 = C->get<uint32_t>("acc_k", N);
-        GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals);
+        GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals, stamps, aux);
         skeys = k32;
       } else {
         unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
-        GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals);
+        GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals, stamps, aux);
         skeys = k64;
       }
     } else {
@@ -612,7 +613,7 @@ struct Pipeline {
       uint32_t* toff = C->get<uint32_t>("sh_off", nt);
       const unsigned grid = (unsigned)std::min<uint64_t>(nt, 148ull * 8);
       GW_LAUNCH((k_shard_accesses<uint32_t, false>), grid, kThreads, 0, st, tr, sa, tcnt, toff, (uint32_t*)nullptr,
-                (uint32_t*)nullptr);
+                (uint32_t*)nullptr, stamps, aux);
       scan<uint32_t, OpSum>(ArrLoad<uint32_t>{tcnt}, ArrStore<uint32_t>{toff}, nt, OpSum(), 0u, false, "sc_u32");
       uint32_t hv[2];
       CK(cudaMemcpyAsync(hv, toff + (nt - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -624,11 +625,13 @@ struct Pipeline {
       vals = C->get<uint32_t>("acc_v", NA + 1);
       if (!wide) {
         uint32_t* k32 = C->get<uint32_t>("acc_k", NA + 1);
-        GW_LAUNCH((k_shard_accesses<uint32_t, true>), grid, kThreads, 0, st, tr, sa, tcnt, toff, k32, vals);
+        GW_LAUNCH((k_shard_accesses<uint32_t, true>), grid, kThreads, 0, st, tr, sa, tcnt, toff, k32, vals, stamps,
+                  aux);
         skeys = k32;
       } else {
         unsigned long long* k64 = C->get<unsigned long long>("acc_k64", NA + 1);
-        GW_LAUNCH((k_shard_accesses<unsigned long long, true>), grid, kThreads, 0, st, tr, sa, tcnt, toff, k64, vals);
+        GW_LAUNCH((k_shard_accesses<unsigned long long, true>), grid, kThreads, 0, st, tr, sa, tcnt, toff, k64, vals,
+                  stamps, aux);
         skeys = k64;
       }
     }
@@ -703,7 +706,7 @@ struct Pipeline {
         aa.vals = vals;
         aa.n = NA;
         aa.carry = carry;
-        aa.src = stamps;
+        aa.aux = aux;
         aa.arena = defer ? nullptr : w.arena;
         aa.defer = defer ? 1 : 0;
         aa.blockobj = (!defer && !has_locks) ? 1 : 0;
