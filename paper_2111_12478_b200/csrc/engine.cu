@@ -241,8 +241,32 @@ struct Pipeline {
     std::string t(tag);
     K* ka = C->get<K>(t + "_ka", n);
     uint32_t* va = C->get<uint32_t>(t + "_va", n);
-    SortScratch sc;
     const int npass = rs_passes(nbits);
+    if (n >= kRsBigN) {
+      // reduce-then-scan passes: digit counts per tile, one scan, scatter
+      const uint64_t nt = lb_tiles(n);
+      uint32_t* counts = C->get<uint32_t>("rs_counts", nt * kRsDigits);
+      rs_down_setup<K>();
+      const unsigned g = (unsigned)std::min<uint64_t>(nt, 148ull * 24);
+      bool alt = false;
+      for (int p = 0; p < npass; p++) {
+        K* ki = alt ? ka : keys;
+        uint32_t* vi = alt ? va : vals;
+        K* ko = alt ? keys : ka;
+        uint32_t* vo = alt ? vals : va;
+        GW_LAUNCH(k_rs_up<K>, g, kThreads, 0, st, ki, n, p, counts, nt);
+        scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nt * kRsDigits, OpSum(), 0u,
+                              false, "sc_u32");
+        GW_LAUNCH(k_rs_down<K>, g, kThreads, sizeof(RsSmem<K>), st, ki, vi, ko, vo, n, p, counts, nt);
+        alt = !alt;
+      }
+      if (alt) {
+        keys = ka;
+        vals = va;
+      }
+      return;
+    }
+    SortScratch sc;
     sc.ghist = zeroed(kRsMaxPass * kRsDigits);
     sc.ctrs = zeroed(npass);
     sc.status = C->get<unsigned long long>("rs_status", std::max(lb_tiles(n), lb_tiles(tr.n)) * kRsDigits);

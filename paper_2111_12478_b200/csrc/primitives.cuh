@@ -380,6 +380,136 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
   }
 }
 
+// ---- reduce-then-scan radix pass (large n) ---------------------------------
+// No chained look-back: k_rs_up counts every tile's digits into a
+// digit-major matrix counts[d * ntiles + tile], one exclusive scan of that
+// matrix gives every (digit, tile) its global output offset, and
+// k_rs_down ranks / stages / scatters exactly like the one-sweep kernel but
+// reads its 256 bases instead of waiting on its predecessors.  Traffic per
+// pass: keys read twice, values once, both written once (+ 2 KB per tile).
+template <class K>
+__global__ void __launch_bounds__(kThreads) k_rs_up(const K* __restrict__ keys, uint64_t n, int pass,
+                                                   uint32_t* __restrict__ counts, uint64_t ntiles) {
+  __shared__ uint32_t h[kRsWarps][kRsDigits];
+  const int w = threadIdx.x >> 5;
+  const int shift = kRsBits * pass;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int d = threadIdx.x; d < kRsWarps * kRsDigits; d += kThreads) (&h[0][0])[d] = 0;
+    __syncthreads();
+    const uint64_t base = tile * kTile;
+    K kk[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+      const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+      kk[k] = i < n ? keys[i] : (K)0;
+    }
+#pragma unroll
+    for (int k = 0; k < kItems; k++) {
+      const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+      if (i < n) atomicAdd(&h[w][(uint32_t)(kk[k] >> shift) & (kRsDigits - 1)], 1u);
+    }
+    __syncthreads();
+    const int d = threadIdx.x;
+    uint32_t c = 0;
+#pragma unroll
+    for (int x = 0; x < kRsWarps; x++) c += h[x][d];
+    counts[(uint64_t)d * ntiles + tile] = c;
+    __syncthreads();
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down(const K* __restrict__ kin,
+                                                                          const uint32_t* __restrict__ vin,
+                                                                          K* __restrict__ kout,
+                                                                          uint32_t* __restrict__ vout, uint64_t n,
+                                                                          int pass,
+                                                                          const uint32_t* __restrict__ offsets,
+                                                                          uint64_t ntiles) {
+  constexpr int ND = kRsDigits;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RsSmem<K>& S = *reinterpret_cast<RsSmem<K>*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int shift = kRsBits * pass;
+  const uint32_t lt = lanemask_lt();
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
+    // this tile's output base per digit (thread d)
+    const uint32_t gb = offsets[(uint64_t)threadIdx.x * ntiles + tile];
+    __syncthreads();
+    const uint64_t tbase = tile * kTile;
+    const uint64_t wbase = tbase + (uint64_t)w * kRsPerWarp;
+    const bool full = tbase + kTile <= n;
+    K kk[kRsRounds];
+    uint32_t vv[kRsRounds];
+    uint32_t rd[kRsRounds];
+#pragma unroll
+    for (int r = 0; r < kRsRounds; r++) {
+      const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+      const bool ok = full || i < n;
+      kk[r] = ok ? kin[i] : (K)0;
+      vv[r] = ok ? vin[i] : 0u;
+      rd[r] = ok ? (((uint32_t)(kk[r] >> shift) & (ND - 1)) << 16) : ((uint32_t)ND << 16);
+    }
+#pragma unroll
+    for (int r = 0; r < kRsRounds; r++) {
+      const uint32_t d = rd[r] >> 16;
+      const uint32_t peers = full ? warp_peers<kRsBits>(d) : warp_peers<kRsBits + 1>(d);
+      const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
+      __syncwarp();
+      if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+      rd[r] |= before + __popc(peers & lt);
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      const int d = threadIdx.x;
+      uint32_t run = 0;
+#pragma unroll
+      for (int ww = 0; ww < kRsWarps; ww++) {
+        const uint32_t t = S.wc[ww][d];
+        S.wc[ww][d] = run;
+        run += t;
+      }
+      uint32_t ct;
+      S.toff[d] = block_excl_scan<uint32_t, OpSum>(run, OpSum(), 0u, &ct);
+      S.gbase[d] = gb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRsRounds; r++) {
+      const uint32_t d = rd[r] >> 16;
+      if (d < (uint32_t)ND) {
+        const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
+        S.sk[pos] = kk[r];
+        S.sv[pos] = vv[r];
+      }
+    }
+    __syncthreads();
+    const uint64_t rem = n > tbase ? n - tbase : 0ull;
+    const uint32_t cnt = rem < (uint64_t)kTile ? (uint32_t)rem : (uint32_t)kTile;
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+      const K k = S.sk[i];
+      const uint32_t d = (uint32_t)(k >> shift) & (ND - 1);
+      const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
+      kout[gp] = k;
+      vout[gp] = S.sv[i];
+    }
+    __syncthreads();
+  }
+}
+template <class K>
+inline void rs_down_setup() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_rs_down<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RsSmem<K>));
+    done = true;
+  }
+}
+// sizes above which the reduce-then-scan passes replace the one-sweep kernel
+constexpr uint64_t kRsBigN = 1ull << 22;
+
 struct SortScratch {
   uint32_t* ghist;              // kRsMaxPass * 1024, zeroed
   unsigned long long* status;   // lb_tiles(n) * 1024
