@@ -60,6 +60,36 @@ WORKLOADS = {
 }
 
 
+# Algorithmic bytes per launch of the pipeline's kernels:
+# n = positions the access pass sorts (all events, or a shard's accesses),
+# N = events.  The dominant kernel's roofline uses these.
+def kernel_alg_bytes(name: str, N: int, n: int) -> int | None:
+    table = [
+        ("k_rs_down", 16 * n),      # keys + values read once, written once
+        ("k_rs_onesweep", 16 * n),
+        ("k_rs_up", 4 * n),         # keys read
+        ("k_access", 24 * n),       # key 4 + event 4 + (tidop, time, vobj, pad) 16 per sorted position
+        ("k_acc_keys", 36 * N),     # key 8 + tidop 4 read; key 4 + event 4 + aux 16 written
+        ("k_acc_tilemax", 8 * n),
+        ("k_prep", 12 * N),
+        ("k_same_instr", 16 * N),
+        ("k_walker", 16 * N),       # the trace, read once
+        ("k_hard_append", 4 * N),
+    ]
+    for key, b in table:
+        if name.startswith(key + "<") or name == key:
+            return b
+    return None
+
+
+def load_ncu_traffic():
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
 def workload_events(p):
     from paper_2111_12478_b200 import _native as N
 
@@ -403,6 +433,13 @@ def run_b200(args):
     s = ctx.stats()
     phase = {k: round(getattr(s, "ms_" + k), 4) for k in ("prep", "walker", "sort", "check", "final")}
     phase["eager_total"] = round(s.ms_total, 4)
+    # per-kernel device times (CUDA events around every launch, on the launching stream) of one
+    # warm eager analysis: the dominant kernel's roofline
+    ctx.analyze_device(cfg, n, key_d.data_ptr(), to_d.data_ptr(), in_d.data_ptr(), stream=sptr, eager=True,
+                       shard=shard, profile=True)
+    finish()
+    ktimes = ctx.kernel_times()
+    n_sorted = int(ctx.stats().n_sorted)
     for _ in range(args.warmup):
         step_device()
     launches = ctx.launches()
@@ -432,6 +469,33 @@ def run_b200(args):
     alg_bytes = 16 * n + 36 * n_acc  # 16 B per event + 36 B per access
     step_s = ms_dev / args.steps / 1000.0
     achieved = alg_bytes / step_s / 1e9
+    # dominant kernel (largest device time in the profiled analysis)
+    dom = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else None
+    dom_line = None
+    if dom is not None:
+        name, (kms, kl) = dom
+        b = kernel_alg_bytes(name, n, n_sorted)
+        per_launch_s = kms / max(kl, 1) / 1000.0
+        traffic = load_ncu_traffic().get(args.workload, {}).get(name.split("<")[0])
+        dom_line = {
+            "bound": "hbm",
+            "achieved": (b / per_launch_s / 1e9) if b is not None else None,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": (b / per_launch_s / 1e9 / peak) if b is not None else None,
+            "traffic": traffic,
+            "kernel": name,
+            "launches_per_analysis": kl,
+            "ms_per_launch": kms / max(kl, 1),
+            "alg_bytes_per_launch": b,
+            "share_of_analysis": kms / sum(v[0] for v in ktimes.values()),
+            "peak_source": peak_kind,
+            "timing": "CUDA events around each launch of one warm eager analysis (bench.py, live)",
+            "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum "
+                              "per launch)" if traffic is not None else None,
+        }
+    top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:10]
+    kernel_ms = {k: round(v[0], 4) for k, v in top}
     phases_ms = phase
     line = {
         "metric": METRIC,
@@ -458,16 +522,17 @@ def run_b200(args):
             "d2h_bytes_per_step": 9 * n_rep + 64,
             "ms_per_step": ms_e2e / args.steps,
         },
-        "roofline": {
+        "roofline": dom_line,
+        "roofline_whole_analysis": {
             "bound": "hbm",
             "achieved": achieved,
             "peak": peak,
             "unit": "GB/s",
             "frac": achieved / peak,
-            "traffic": None,
             "kernel": "whole analysis (all kernels of one step); algorithmic bytes B = 16N + 36A (SURVEY 8d)",
             "peak_source": peak_kind,
         },
+        "kernel_ms_eager": kernel_ms,
         "phases_ms_eager": phases_ms,
         "gpu_launches": launches * args.steps,
         "walker_ctas": stats.walker_ctas,

@@ -88,7 +88,8 @@ typedef struct gw_trace_view { /* caller-owned SoA; host or device pointers */
   const uint32_t* instr;
 } gw_trace_view;
 
-#define GW_OPT_EAGER 1u /* never capture / replay a CUDA graph for this analysis */
+#define GW_OPT_EAGER 1u   /* never capture / replay a CUDA graph for this analysis */
+#define GW_OPT_PROFILE 2u /* eager, with CUDA events around every launch (gw_ctx_kernel_times) */
 
 typedef struct gw_opts {
   uint32_t inactive_opt; /* GwcpDetector(inactive_opt=...), gwcp.py:108-127 */
@@ -121,6 +122,7 @@ typedef struct gw_stats { /* per-phase device times of the last analysis (ms) */
   float ms_total, ms_prep, ms_walker, ms_sort, ms_check, ms_final;
   uint64_t n_accesses, n_candidates, n_sync, arena_words;
   uint32_t walker_ctas, sort_bits;
+  uint64_t n_sorted;       /* positions the access pass sorted (all events, or this shard's accesses) */
 } gw_stats;
 
 typedef struct gw_ctx gw_ctx;
@@ -156,6 +158,8 @@ int gw_ctx_fetch(gw_ctx* c, gw_result* out);
 int gw_ctx_stats(gw_ctx* c, gw_stats* out);
 /* number of kernels the last analysis launched */
 uint32_t gw_ctx_launches(gw_ctx* c);
+/* per-kernel device times of the last GW_OPT_PROFILE analysis (aggregated by kernel) */
+int gw_ctx_kernel_times(gw_ctx* c, uint32_t cap, char (*names)[64], float* ms, uint32_t* launches, uint32_t* n_out);
 
 /* bench / test infrastructure: generate the C2 / C5 synthetic trace (SURVEY
  * §8(d)) directly into device buffers of phases*(records*B*W*L + B) events */

@@ -27,6 +27,7 @@ F_WARPBAR = 1 << 29
 F_CONT = 1 << 30
 SHARED_BIT = 1 << 63
 OPT_EAGER = 1
+OPT_PROFILE = 2
 
 
 class NativeUnavailable(RuntimeError):
@@ -96,6 +97,7 @@ class Stats(C.Structure):
         ("arena_words", C.c_uint64),
         ("walker_ctas", C.c_uint32),
         ("sort_bits", C.c_uint32),
+        ("n_sorted", C.c_uint64),
     ]
 
 
@@ -117,6 +119,7 @@ EXPORTS = (
     "gw_gen_c2_device",
     "gw_gen_c4_device",
     "gw_gen_c3_device",
+    "gw_ctx_kernel_times",
 )
 
 _lib = None
@@ -176,6 +179,9 @@ def lib():
         L.gw_gen_c4_device.restype = C.c_int
         L.gw_gen_c3_device.argtypes = [C.c_uint32] * 7 + [C.c_uint64] + [C.c_void_p] * 5
         L.gw_gen_c3_device.restype = C.c_int
+        L.gw_ctx_kernel_times.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(C.c_float),
+                                          C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        L.gw_ctx_kernel_times.restype = C.c_int
         _lib = L
         return L
 
@@ -292,14 +298,15 @@ class Context:
         _check(self._L.gw_ctx_analyze_host(self._c, C.byref(v), C.byref(o)))
 
     def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None,
-                       eager=False, shard=(0, 1)) -> None:
+                       eager=False, shard=(0, 1), profile=False) -> None:
         """shard=(index, count): report only races on location-key range `index`
         of `count` (address sharding; see include/gwcp_b200.h gw_opts)."""
         v = _View()
         v.cfg.blocks, v.cfg.warps, v.cfg.lanes = cfg
         v.n_events = n
         v.key, v.tidop, v.instr = key_ptr, tidop_ptr, instr_ptr
-        o = _Opts(1 if inactive_opt else 0, OPT_EAGER if eager else 0, stream, shard[0], shard[1])
+        flags = (OPT_EAGER if eager else 0) | (OPT_PROFILE if profile else 0)
+        o = _Opts(1 if inactive_opt else 0, flags, stream, shard[0], shard[1])
         _check(self._L.gw_ctx_analyze_device(self._c, C.byref(v), C.byref(o)))
 
     def fetch(self):
@@ -314,6 +321,16 @@ class Context:
 
     def launches(self) -> int:
         return int(self._L.gw_ctx_launches(self._c))
+
+    def kernel_times(self) -> dict:
+        """{kernel: (total ms, launches)} of the last analysis run with profile=True."""
+        cap = 256
+        names = (C.c_char * 64 * cap)()
+        ms = (C.c_float * cap)()
+        cnt = (C.c_uint32 * cap)()
+        n = C.c_uint32(0)
+        _check(self._L.gw_ctx_kernel_times(self._c, cap, names, ms, cnt, C.byref(n)))
+        return {names[i].value.decode(): (float(ms[i]), int(cnt[i])) for i in range(n.value)}
 
 
 _default_ctx: Context | None = None

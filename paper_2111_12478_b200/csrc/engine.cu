@@ -23,6 +23,7 @@
 
 namespace gw {
 thread_local uint32_t g_launches = 0;
+thread_local LaunchProf* g_prof = nullptr;
 }
 using namespace gw;
 
@@ -115,6 +116,24 @@ struct gw_ctx {
   uint32_t last_shard = 0, last_nshard = 1;
   bool last_graph = false;
   Plan plan;
+  LaunchProf prof;           // GW_OPT_PROFILE: per-launch events of the last analysis
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<LaunchProf::Rec> prof_recs;
+  bool prof_done = false;
+
+  void prof_arm(uint32_t cap) {
+    while (prof_ev.size() < 2 * (size_t)cap) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      prof_ev.push_back(e);
+    }
+    prof_recs.assign(cap, LaunchProf::Rec{nullptr, nullptr, nullptr});
+    for (uint32_t i = 0; i < cap; i++) { prof_recs[i].a = prof_ev[2 * i]; prof_recs[i].b = prof_ev[2 * i + 1]; }
+    prof.recs = prof_recs.data();
+    prof.n = 0;
+    prof.cap = cap;
+    prof_done = true;
+  }
 
   template <class T>
   T* get(const std::string& name, uint64_t count) {
@@ -660,6 +679,7 @@ struct Pipeline {
       }
     }
     na_sorted = NA;
+    C->stats.n_sorted = NA;
     if (!wide) {
       uint32_t* k32 = (uint32_t*)skeys;
       sort<uint32_t>(k32, vals, NA, nbits, "acc");
@@ -1038,6 +1058,7 @@ extern "C" void gw_ctx_destroy(gw_ctx* c) {
   c->drop_plan();
   for (auto& kv : c->bufs)
     if (kv.second.p) cudaFree(kv.second.p);
+  for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   for (int i = 0; i < gw_ctx::kEv; i++)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   delete c;
@@ -1046,8 +1067,18 @@ extern "C" void gw_ctx_destroy(gw_ctx* c) {
 // Eager analysis, then (lock-free traces without large reader windows) build
 // the Plan and capture the graph-mode pipeline for later replays.
 static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_t inactive, const void* kp,
-                         const void* tp, const void* ip, bool eager, uint32_t shard, uint32_t nshard) {
+                         const void* tp, const void* ip, bool eager, uint32_t shard, uint32_t nshard,
+                         bool profile = false) {
   if (nshard > 1) eager = true;  // sharded analyses are not graph-replayed
+  c->prof_done = false;
+  if (profile) {
+    eager = true;
+    c->prof_arm(4096);
+    g_prof = &c->prof;
+  }
+  struct ProfOff {
+    ~ProfOff() { g_prof = nullptr; }
+  } prof_off;
   c->last_shard = shard;
   c->last_nshard = nshard;
   Plan& P = c->plan;
@@ -1129,7 +1160,8 @@ extern "C" int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* t, const gw
     const uint32_t sh = nsh > 1 ? o->shard_index : 0u;
     if (sh >= nsh) throw CudaErr{GW_E_ARG, "shard_index must be < shard_count"};
     DevTrace tr = make_dev(t, (const unsigned long long*)t->key, t->tidop, t->instr);
-    analyze_impl(c, tr, st, inactive, t->key, t->tidop, t->instr, o && (o->flags & GW_OPT_EAGER), sh, nsh);
+    analyze_impl(c, tr, st, inactive, t->key, t->tidop, t->instr, o && (o->flags & GW_OPT_EAGER), sh, nsh,
+                 o && (o->flags & GW_OPT_PROFILE));
   });
 }
 
@@ -1155,7 +1187,8 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
       CK(cudaMemcpyAsync(in, t->instr, 4 * N, cudaMemcpyHostToDevice, st));
     }
     DevTrace tr = make_dev(t, k, to, in);
-    analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh);
+    analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,
+                 o && (o->flags & GW_OPT_PROFILE));
   });
 }
 
@@ -1295,5 +1328,40 @@ extern "C" int gw_gen_c3_device(uint32_t blocks, uint32_t warps, uint32_t lanes,
               (cudaStream_t)stream, p, (const unsigned long long*)group_offsets, (unsigned long long*)key, tidop,
               instr);
     CK(cudaGetLastError());
+  });
+}
+
+// per-kernel device times of the last GW_OPT_PROFILE analysis, aggregated by
+// kernel (launch expression): names[i] (NUL-terminated, truncated to 63
+// chars), total ms, launch count
+extern "C" int gw_ctx_kernel_times(gw_ctx* c, uint32_t cap, char (*names)[64], float* ms, uint32_t* launches,
+                                   uint32_t* n_out) {
+  if (!c || !n_out) { gw_set_error("null argument"); return GW_E_ARG; }
+  return guarded([&] {
+    *n_out = 0;
+    if (!c->prof_done) return;
+    CK(cudaSetDevice(c->device));
+    std::vector<std::string> nm;
+    std::vector<float> tot;
+    std::vector<uint32_t> cnt;
+    for (uint32_t i = 0; i < c->prof.n; i++) {
+      const auto& r = c->prof.recs[i];
+      CK(cudaEventSynchronize(r.b));
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, r.a, r.b));
+      std::string k(r.name);
+      size_t j = 0;
+      while (j < nm.size() && nm[j] != k) j++;
+      if (j == nm.size()) { nm.push_back(k); tot.push_back(0.f); cnt.push_back(0); }
+      tot[j] += t;
+      cnt[j]++;
+    }
+    const uint32_t n = (uint32_t)std::min<size_t>(nm.size(), cap);
+    for (uint32_t j = 0; j < n; j++) {
+      snprintf(names[j], 64, "%s", nm[j].c_str());
+      ms[j] = tot[j];
+      launches[j] = cnt[j];
+    }
+    *n_out = n;
   });
 }

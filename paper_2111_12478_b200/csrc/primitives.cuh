@@ -14,11 +14,31 @@ constexpr int kThreads = 256;
 constexpr int kItems = 16;
 constexpr int kTile = kThreads * kItems;  // 4096
 
-// launch accounting (gw_ctx_launches); incremented on the host per launch
+// launch accounting (gw_ctx_launches); incremented on the host per launch.
+// With a LaunchProf installed (GW_OPT_PROFILE analyses) every launch is
+// bracketed by CUDA events on its stream -> per-kernel device times.
+struct LaunchProf {
+  struct Rec { const char* name; cudaEvent_t a, b; };
+  Rec* recs = nullptr;
+  uint32_t n = 0, cap = 0;
+  void begin(const char* name, cudaStream_t st) {
+    if (n >= cap) return;
+    recs[n].name = name;
+    cudaEventRecord(recs[n].a, st);
+  }
+  void end(cudaStream_t st) {
+    if (n >= cap) return;
+    cudaEventRecord(recs[n].b, st);
+    n++;
+  }
+};
 extern thread_local uint32_t g_launches;
+extern thread_local LaunchProf* g_prof;
 #define GW_LAUNCH(kernel, grid, block, smem, stream, ...)      \
   do {                                                         \
+    if (::gw::g_prof) ::gw::g_prof->begin(#kernel, (stream));  \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__); \
+    if (::gw::g_prof) ::gw::g_prof->end((stream));             \
     ::gw::g_launches++;                                        \
   } while (0)
 
