@@ -76,10 +76,16 @@ def kernel_alg_bytes(name: str, N: int, n: int) -> int | None:
         ("k_walker", 16 * N),       # the trace, read once
         ("k_hard_append", 4 * N),
     ]
+    base = kernel_base(name)
     for key, b in table:
-        if name.startswith(key + "<") or name == key:
+        if base == key:
             return b
     return None
+
+
+def kernel_base(name: str) -> str:
+    """'(k_rs_down<K>)' -> 'k_rs_down' (launch expressions as the engine records them)."""
+    return name.strip().strip("()").split("<")[0].strip()
 
 
 def load_ncu_traffic():
@@ -476,7 +482,7 @@ def run_b200(args):
         name, (kms, kl) = dom
         b = kernel_alg_bytes(name, n, n_sorted)
         per_launch_s = kms / max(kl, 1) / 1000.0
-        traffic = load_ncu_traffic().get(args.workload, {}).get(name.split("<")[0])
+        traffic = load_ncu_traffic().get(args.workload, {}).get(kernel_base(name))
         dom_line = {
             "bound": "hbm",
             "achieved": (b / per_launch_s / 1e9) if b is not None else None,
@@ -484,7 +490,7 @@ def run_b200(args):
             "unit": "GB/s",
             "frac": (b / per_launch_s / 1e9 / peak) if b is not None else None,
             "traffic": traffic,
-            "kernel": name,
+            "kernel": kernel_base(name),
             "launches_per_analysis": kl,
             "ms_per_launch": kms / max(kl, 1),
             "alg_bytes_per_launch": b,
@@ -495,7 +501,7 @@ def run_b200(args):
                               "per launch)" if traffic is not None else None,
         }
     top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:10]
-    kernel_ms = {k: round(v[0], 4) for k, v in top}
+    kernel_ms = {kernel_base(k): round(v[0], 4) for k, v in top}
     phases_ms = phase
     line = {
         "metric": METRIC,

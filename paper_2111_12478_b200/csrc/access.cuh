@@ -808,6 +808,41 @@ __global__ void k_dedup_keys(DedupArgs d, unsigned long long n_events, unsigned 
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(nsurv, (uint32_t)__popc(m));
   }
 }
+// large candidate sets: survivors keyed by their current event only (fewer
+// radix bits), then every run of equal events ordered by the full order key
+__global__ void k_dedup_keys32(DedupArgs d, uint32_t n_events, uint32_t* sk, uint32_t* sv, uint32_t* nsurv) {
+  const uint32_t nc = dd_count(d);
+  for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < d.ncand; k0 += gridDim.x * blockDim.x) {
+    const uint32_t k = k0 + threadIdx.x;
+    bool surv = false;
+    uint32_t key = n_events;
+    if (k < nc) {
+      const unsigned long long ok = d.c.okey[k];
+      surv = ok == d.smin[d.cslot[k]];
+      if (surv) key = (uint32_t)(ok >> 32);
+    }
+    if (k < d.ncand) { sk[k] = key; sv[k] = k; }
+    const uint32_t m = __ballot_sync(0xffffffffu, surv);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(nsurv, (uint32_t)__popc(m));
+  }
+}
+__global__ void k_group_fix(const uint32_t* sk, uint32_t* sv, uint32_t n, uint32_t n_events,
+                            const unsigned long long* okey) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t key = sk[i];
+    if (key >= n_events || (i > 0 && sk[i - 1] == key)) continue;
+    uint32_t end = i + 1;
+    while (end < n && sk[end] == key) end++;
+    for (uint32_t x = i + 1; x < end; x++) {  // insertion sort of the run by order key
+      const uint32_t v = sv[x];
+      const unsigned long long ok = okey[v];
+      uint32_t y = x;
+      while (y > i && okey[sv[y - 1]] > ok) { sv[y] = sv[y - 1]; y--; }
+      sv[y] = v;
+    }
+  }
+}
+
 __global__ void k_final(Cands c, const uint32_t* svals, const uint32_t* nsurv, uint8_t* okind, uint32_t* oprior,
                         uint32_t* ocur, unsigned long long* okey) {
   const uint32_t n = *nsurv;

@@ -255,8 +255,16 @@ struct Pipeline {
 
   // stable radix sort wrapper; returns pointers to the sorted keys / vals
   template <class K>
-  void sort(K*& keys, uint32_t*& vals, uint64_t n, int nbits, const char* tag) {
+  void sort(K*& keys, uint32_t*& vals, uint64_t n, int nbits, const char* tag, bool distinct = false) {
     if (n <= 1 || nbits <= 0) return;
+    if (distinct && n <= small_sort_max<K>()) {
+      // one CTA, in shared memory (distinct keys: stability is moot)
+      uint32_t p2 = 1;
+      while (p2 < n) p2 <<= 1;
+      sort_small_setup<K>();
+      GW_LAUNCH(k_sort_small<K>, 1, kSmallThreads, p2 * (sizeof(K) + 4), st, keys, vals, (uint32_t)n, p2);
+      return;
+    }
     std::string t(tag);
     K* ka = C->get<K>(t + "_ka", n);
     uint32_t* va = C->get<uint32_t>(t + "_va", n);
@@ -481,8 +489,15 @@ struct Pipeline {
       // survivors ordered by their order key; the others sort last
       unsigned long long* sk = C->get<unsigned long long>("sv_k", ncap);
       uint32_t* sv = C->get<uint32_t>("sv_v", ncap);
-      GW_LAUNCH(k_dedup_keys, grid_for(ncap), kThreads, 0, st, d, (unsigned long long)N, sk, sv, d_nsurv);
-      sort<unsigned long long>(sk, sv, ncap, 32 + ceil_log2(N + 1), "sv");
+      if (ncap <= small_sort_max<unsigned long long>()) {
+        GW_LAUNCH(k_dedup_keys, grid_for(ncap), kThreads, 0, st, d, (unsigned long long)N, sk, sv, d_nsurv);
+        sort<unsigned long long>(sk, sv, ncap, 32 + ceil_log2(N + 1), "sv", true);
+      } else {
+        uint32_t* sk32 = C->get<uint32_t>("sv_k32", ncap);
+        GW_LAUNCH(k_dedup_keys32, grid_for(ncap), kThreads, 0, st, d, (uint32_t)N, sk32, sv, d_nsurv);
+        sort<uint32_t>(sk32, sv, ncap, ceil_log2(N + 1), "sv32");
+        GW_LAUNCH(k_group_fix, grid_for(ncap), kThreads, 0, st, sk32, sv, (uint32_t)ncap, (uint32_t)N, cd.okey);
+      }
       C->d_kind = C->get<uint8_t>("o_kind", ncap);
       C->d_prior = C->get<uint32_t>("o_prior", ncap);
       C->d_cur = C->get<uint32_t>("o_cur", ncap);
@@ -954,7 +969,7 @@ struct Pipeline {
         unsigned long long* hkey = C->get<unsigned long long>("hd_key", n_hard + 1);
         uint32_t* hdummy = C->get<uint32_t>("hd_v", n_hard + 1);
         GW_LAUNCH(k_hard_append, grid_for(N), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT);
-        sort<unsigned long long>(hkey, hdummy, n_hard, 32 + ceil_log2(tr.B), "hd");
+        sort<unsigned long long>(hkey, hdummy, n_hard, 32 + ceil_log2(tr.B), "hd", true);
         GW_LAUNCH(k_hard_unpack, grid_for(n_hard), kThreads, 0, st, hkey, n_hard, hev);
       }
       scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hcnt}, HardSegStore{hcnt, hbeg, hend}, tr.B, OpSum(), 0u, false,

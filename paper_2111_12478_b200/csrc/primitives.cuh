@@ -527,6 +527,54 @@ inline void rs_down_setup() {
     done = true;
   }
 }
+// ---- single-CTA sort (small n) ----------------------------------------------
+// n <= kSmallSortMax(K): the whole array in shared memory, bitonic network,
+// one launch instead of one per digit pass.  Not stable: callers use it only
+// for distinct keys (or keys whose ties are irrelevant).
+constexpr int kSmallThreads = 1024;
+template <class K>
+constexpr uint32_t small_sort_max() { return sizeof(K) == 8 ? 16384u : 16384u; }
+template <class K>
+__global__ void __launch_bounds__(kSmallThreads) k_sort_small(K* keys, uint32_t* vals, uint32_t n, uint32_t p2) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  K* sk = reinterpret_cast<K*>(smem_raw);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + p2);
+  for (uint32_t i = threadIdx.x; i < p2; i += kSmallThreads) {
+    sk[i] = i < n ? keys[i] : ~(K)0;
+    sv[i] = i < n ? vals[i] : 0u;
+  }
+  __syncthreads();
+  for (uint32_t k = 2; k <= p2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < p2; i += kSmallThreads) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const K a = sk[i], b = sk[l];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            sk[i] = b; sk[l] = a;
+            const uint32_t t = sv[i]; sv[i] = sv[l]; sv[l] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += kSmallThreads) {
+    keys[i] = sk[i];
+    vals[i] = sv[i];
+  }
+}
+template <class K>
+inline void sort_small_setup() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_sort_small<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(small_sort_max<K>() * (sizeof(K) + 4)));
+    done = true;
+  }
+}
+
 // sizes above which the reduce-then-scan passes replace the one-sweep kernel
 constexpr uint64_t kRsBigN = 1ull << 22;
 
