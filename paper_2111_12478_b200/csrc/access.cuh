@@ -826,8 +826,37 @@ __global__ void k_dedup_keys32(DedupArgs d, uint32_t n_events, uint32_t* sk, uin
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(nsurv, (uint32_t)__popc(m));
   }
 }
+// small traces: counting sort of the survivors by event (count, scan over
+// the events, placement with self-cleaning counters)
+__global__ void k_surv_count(DedupArgs d, uint32_t* ccnt, uint32_t* nsurv) {
+  const uint32_t nc = dd_count(d);
+  for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < d.ncand; k0 += gridDim.x * blockDim.x) {
+    const uint32_t k = k0 + threadIdx.x;
+    bool surv = false;
+    if (k < nc) {
+      const unsigned long long ok = d.c.okey[k];
+      surv = ok == d.smin[d.cslot[k]];
+      if (surv) atomicAdd(ccnt + (ok >> 32), 1u);
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, surv);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(nsurv, (uint32_t)__popc(m));
+  }
+}
+__global__ void k_surv_place(DedupArgs d, uint32_t* ccnt, const uint32_t* coff, uint32_t* sk, uint32_t* sv) {
+  const uint32_t nc = dd_count(d);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+    const unsigned long long ok = d.c.okey[k];
+    if (ok == d.smin[d.cslot[k]]) {
+      const uint32_t c = (uint32_t)(ok >> 32);
+      const uint32_t pos = coff[c] + atomicSub(ccnt + c, 1u) - 1u;  // leaves ccnt zeroed
+      sk[pos] = c;
+      sv[pos] = k;
+    }
+  }
+}
 __global__ void k_group_fix(const uint32_t* sk, uint32_t* sv, uint32_t n, uint32_t n_events,
-                            const unsigned long long* okey) {
+                            const unsigned long long* okey, const uint32_t* nlim = nullptr) {
+  if (nlim) n = min(n, *nlim);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t key = sk[i];
     if (key >= n_events || (i > 0 && sk[i - 1] == key)) continue;

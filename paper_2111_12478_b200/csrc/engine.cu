@@ -489,7 +489,18 @@ struct Pipeline {
       // survivors ordered by their order key; the others sort last
       unsigned long long* sk = C->get<unsigned long long>("sv_k", ncap);
       uint32_t* sv = C->get<uint32_t>("sv_v", ncap);
-      if (ncap <= small_sort_max<unsigned long long>()) {
+      if (N <= (1ull << 25) && ncap > small_sort_max<unsigned long long>()) {
+        // small trace: counting sort by event over the N events, then each run by order key
+        uint32_t* sk32 = C->get<uint32_t>("sv_k32", ncap);
+        uint32_t* ccnt = C->get<uint32_t>("sv_cnt", N);
+        uint32_t* coff = C->get<uint32_t>("sv_off", N);
+        CK(cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * N, st));
+        GW_LAUNCH(k_surv_count, grid_for(ncap), kThreads, 0, st, d, ccnt, d_nsurv);
+        scan<uint32_t, OpSum>(ArrLoad<uint32_t>{ccnt}, ArrStore<uint32_t>{coff}, N, OpSum(), 0u, false, "sc_u32");
+        GW_LAUNCH(k_surv_place, grid_for(ncap), kThreads, 0, st, d, ccnt, coff, sk32, sv);
+        GW_LAUNCH(k_group_fix, grid_for(ncap), kThreads, 0, st, sk32, sv, (uint32_t)ncap, (uint32_t)N, cd.okey,
+                  d_nsurv);
+      } else if (ncap <= small_sort_max<unsigned long long>()) {
         GW_LAUNCH(k_dedup_keys, grid_for(ncap), kThreads, 0, st, d, (unsigned long long)N, sk, sv, d_nsurv);
         sort<unsigned long long>(sk, sv, ncap, 32 + ceil_log2(N + 1), "sv", true);
       } else {
@@ -1131,7 +1142,7 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   np.N = tr.n; np.B = tr.B; np.W = tr.W; np.L = tr.L; np.inactive_opt = inactive;
   np.key = kp; np.tidop = tp; np.instr = ip; np.stream = st;
   np.n_bar = p.obs.n_bar; np.n_end = p.obs.n_end; np.D = p.obs_D;
-  np.cand_cap = std::max<uint64_t>(p.obs_cand_cap, 2ull * p.obs_ncand + 4096);
+  np.cand_cap = 2ull * p.obs_ncand + 4096;  // tight: graph replays size the dedup / order passes by it
   c->plan = np;
   Pipeline g;
   g.C = c; g.st = st; g.inactive_opt = inactive; g.tr = tr; g.gmode = true; g.P = &c->plan;

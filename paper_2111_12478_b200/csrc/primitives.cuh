@@ -363,13 +363,32 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
     S.toff[d] = cex;
     unsigned long long pre = 0;
     if (tile > 0) {
+      // up to 8 predecessors per round trip: sum their aggregates back to the
+      // nearest inclusive prefix (all of them must have published)
+      constexpr int B8 = 8;
       int64_t p = (int64_t)tile - 1;
       while (true) {
-        unsigned long long sv;
-        do { sv = ld_volatile_u64(&status[(uint64_t)p * ND + d]); } while ((sv >> 40) != epoch);
-        pre += sv & ((1ull << 38) - 1);
-        if (((sv >> 38) & 3ull) == 2ull) break;
-        p--;
+        unsigned long long w8[B8];
+#pragma unroll
+        for (int k = 0; k < B8; k++)
+          w8[k] = p - k >= 0 ? ld_volatile_u64(&status[(uint64_t)(p - k) * ND + d]) : (EP | (2ull << 38));
+        int lim = B8;
+        bool ready = true;
+#pragma unroll
+        for (int k = 0; k < B8; k++) {
+          if (lim == B8) {
+            if ((w8[k] >> 40) != epoch) { ready = false; lim = -1; }
+            else if (((w8[k] >> 38) & 3ull) == 2ull) lim = k;
+          }
+        }
+        if (!ready) continue;  // a predecessor before the nearest inclusive has not published yet
+        unsigned long long add = 0;
+#pragma unroll
+        for (int k = 0; k < B8; k++)
+          if (k <= lim) add += w8[k] & ((1ull << 38) - 1);
+        pre += add;
+        if (lim < B8) break;
+        p -= B8;
       }
       atomicExch(my, EP | (2ull << 38) | (pre + c));
     }
