@@ -8,6 +8,6 @@ M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
 timeout 600 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/launches_$W.csv \
   python profiles/run_one.py --workload $W --repeat 1 > gpurun_out/ncu_l_$W.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_rs_down|k_rs_onesweep|k_access|k_acc_keys|k_walker" -c 8 \
+  -k regex:"k_rs_down|k_rs_onesweep<unsigned int>|k_access|k_acc_keys|k_walker" -c 8 \
   -o gpurun_out/full_$W python profiles/run_one.py --workload $W --repeat 1 > gpurun_out/ncu_f_$W.log 2>&1
 for f in gpurun_out/ncu_l_$W.log gpurun_out/ncu_f_$W.log; do tail -n 1 $f; done
