@@ -48,17 +48,20 @@ struct StampSrc {  // valid() false in lock mode (the walker runs after the acce
   const uint32_t* hb_end;
   const uint2* snap;
   uint32_t BS;
+  uint32_t warp_mode;  // snapshot lists per (block, warp) (k_walker_wsnap), rows of 32
+  uint32_t L;
   __device__ __forceinline__ bool valid() const { return time != nullptr || snap != nullptr; }
   __device__ __forceinline__ uint2 get(uint32_t e, uint32_t t) const {
     if (time) return make_uint2(__ldg(time + e), __ldg(vobj + e));
     const uint32_t b = t / BS;
-    const uint32_t base = __ldg(hb_beg + b);
-    uint32_t lo = base, hi = __ldg(hb_end + b);
+    const uint32_t g = warp_mode ? b * 8u + (t - b * BS) / L : b;
+    const uint32_t base = __ldg(hb_beg + g);
+    uint32_t lo = base, hi = __ldg(hb_end + g);
     while (lo < hi) {
       const uint32_t m = (lo + hi) >> 1;
       if (__ldg(hard_ev + m) < e) lo = m + 1; else hi = m;
     }
-    return snap[(size_t)(base + b + (lo - base)) * BS + (t - b * BS)];
+    return warp_mode ? snap[(size_t)(lo + g) * 32 + (t - b * BS) % L] : snap[(size_t)(lo + g) * BS + (t - b * BS)];
   }
 };
 
@@ -178,10 +181,11 @@ __global__ void k_compact_u64(const unsigned long long* in, uint64_t n, KeyRuns 
 struct Stats {
   unsigned long long n_acc, n_write, n_acq, n_rel, n_end, n_bar, key_or, key_and;
   unsigned long long n_long;  // windows proving a record longer than 32 events
+  unsigned long long n_wbar;  // warp barriers (of n_bar)
 };
 __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
   unsigned long long v[6] = {0, 0, 0, 0, 0, 0};  // acc, write, acq, rel, end, bar
-  unsigned long long ko = 0, ka = ~0ull, nlong = 0;
+  unsigned long long ko = 0, ka = ~0ull, nlong = 0, nwbar = 0;
   const int lane = threadIdx.x & 31;
   for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < tr.n;
        e0 += (uint64_t)gridDim.x * blockDim.x) {
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
     } else if (k == GW_K_ACQUIRE) v[2]++;
     else if (k == GW_K_RELEASE) v[3]++;
     else if (k == GW_K_END) v[4]++;
-    else if (k == GW_K_BARRIER) v[5]++;
+    else if (k == GW_K_BARRIER) { v[5]++; if (to & GW_F_WARPBAR) nwbar++; }
     // records longer than 32 events: 32 consecutive continues-record events ending in this window
     const uint32_t cur = __ballot_sync(0xffffffffu, (to & GW_F_CONT) != 0);
     if (cur == 0xffffffffu) {
@@ -207,6 +211,8 @@ __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
     }
   }
   if (lane == 0 && nlong) atomicAdd(&st->n_long, nlong);
+  nwbar = __reduce_add_sync(0xffffffffu, (uint32_t)nwbar);
+  if (lane == 0 && nwbar) atomicAdd(&st->n_wbar, nwbar);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll

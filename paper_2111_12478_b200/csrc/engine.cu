@@ -75,7 +75,7 @@ struct Plan {
   uint32_t B = 0, W = 0, L = 0, inactive_opt = 1;
   const void *key = nullptr, *tidop = nullptr, *instr = nullptr;
   cudaStream_t stream = 0;
-  unsigned long long n_bar = 0, n_end = 0, D = 0;
+  unsigned long long n_bar = 0, n_end = 0, n_wbar = 0, D = 0;
   uint64_t cand_cap = 0;
   uint32_t launches = 0;
   cudaGraphExec_t exec = nullptr;
@@ -189,8 +189,9 @@ __global__ void k_init_stats(Stats* s) {
 }
 // graph mode: the trace must have the shape the plan was built for
 __global__ void k_plan_check(const Stats* s, unsigned long long n_bar, unsigned long long n_end,
-                             unsigned long long D, uint32_t* abort_flag) {
+                             unsigned long long n_wbar, unsigned long long D, uint32_t* abort_flag) {
   const bool ok = s->n_acq == 0 && s->n_rel == 0 && s->n_bar == n_bar && s->n_end == n_end && s->n_long == 0 &&
+                  s->n_wbar == n_wbar &&
                   ((s->key_or ^ s->key_and) & ~D) == 0ull;
   if (!ok) atomicOr(abort_flag, 1u);
 }
@@ -395,9 +396,10 @@ struct Pipeline {
       memset(&hs, 0, sizeof hs);
       hs.n_bar = P->n_bar;
       hs.n_end = P->n_end;
+      hs.n_wbar = P->n_wbar;
       hs.key_or = P->D;
       hs.key_and = 0;
-      GW_LAUNCH(k_plan_check, 1, 1, 0, st, dst, P->n_bar, P->n_end, P->D, scal + SC_ABORT);
+      GW_LAUNCH(k_plan_check, 1, 1, 0, st, dst, P->n_bar, P->n_end, P->n_wbar, P->D, scal + SC_ABORT);
     } else {
       d2h(&hs, dst);
       obs = hs;
@@ -414,8 +416,18 @@ struct Pipeline {
     // snapshot mode: lock-free and the per-hard-event block snapshots are small
     n_hard = hs.n_bar + hs.n_end;
     snap_entries = (n_hard + tr.B) * (uint64_t)tr.BS;
-    snap_mode = !has_locks && snap_entries * 8 <= std::max<uint64_t>(256ull << 20, 8 * N);
-    obs_snap = snap_mode;
+    const uint64_t snap_budget = std::max<uint64_t>(256ull << 20, 8 * N);
+    // GW_WALK_MODE=block|warp|walker forces a lock-free sync-pass mode when applicable (tests)
+    const char* wm = getenv("GW_WALK_MODE");
+    const bool force_warp = wm && !strcmp(wm, "warp"), force_walker = wm && !strcmp(wm, "walker");
+    snap_mode = !has_locks && snap_entries * 8 <= snap_budget && !force_warp && !force_walker;
+    // warp snapshot mode: per-(block, warp) lists, block barriers replicated into every warp's list
+    n_hard_w = hs.n_wbar + hs.n_end + (uint64_t)kWSnapWarps * (hs.n_bar - hs.n_wbar);
+    const uint64_t wsnap_entries = (n_hard_w + (uint64_t)tr.B * kWSnapWarps) * 32ull;
+    wsnap_mode = !has_locks && !snap_mode && !force_walker && tr.W <= kWSnapWarps && tr.L <= 32 &&
+                 wsnap_entries * 8 <= snap_budget;
+    if (wsnap_mode) snap_entries = wsnap_entries;
+    obs_snap = snap_mode || wsnap_mode;
     memset(&w, 0, sizeof w);
     w.tr = tr;
     w.G = G;
@@ -423,7 +435,7 @@ struct Pipeline {
     w.inactive_opt = inactive_opt;
     w.abort_flag = scal + SC_ABORT;
     w.err = scal + SC_ERR;
-    if (G > 1 && !snap_mode) {
+    if (G > 1 && !snap_mode && !wsnap_mode) {
       uint32_t* part_key = C->get<uint32_t>("part_k", N);
       uint32_t* perm = C->get<uint32_t>("part_v", N);
       GW_LAUNCH(k_part_keys, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
@@ -529,7 +541,8 @@ struct Pipeline {
   // ---- pipeline state shared by the phases --------------------------------
   uint32_t* scal = nullptr;
   Stats hs{};
-  bool has_locks = false, snap_mode = false;
+  bool has_locks = false, snap_mode = false, wsnap_mode = false;
+  uint64_t n_hard_w = 0;
   uint64_t gmax = 1, n_hard = 0, snap_entries = 0, lcap = 1, arena_units = 0;
   uint32_t G = 1, maxd = 1, n_incs = 0;
   WalkArgs w;
@@ -999,6 +1012,38 @@ struct Pipeline {
       stamps.snap = sa.snap;
       stamps.BS = tr.BS;
       C->stats.walker_ctas = std::min<uint32_t>(tr.B, (uint32_t)gmax);
+    } else if (wsnap_mode) {
+      SnapArgs sa;
+      const uint64_t ng = (uint64_t)tr.B * kWSnapWarps;
+      uint32_t* hev = C->get<uint32_t>("hd_ev", n_hard_w + 1);
+      uint32_t* hbeg = C->get<uint32_t>("hd_beg", ng);
+      uint32_t* hend = C->get<uint32_t>("hd_end", ng);
+      uint32_t* hcnt = C->get<uint32_t>("hd_cnt", ng);
+      CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * ng, st));
+      if (n_hard_w) {
+        unsigned long long* hkey = C->get<unsigned long long>("hd_key", n_hard_w + 1);
+        uint32_t* hdummy = C->get<uint32_t>("hd_v", n_hard_w + 1);
+        GW_LAUNCH(k_hard_append_w, grid_for(N), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT);
+        sort<unsigned long long>(hkey, hdummy, n_hard_w, 32 + ceil_log2(ng), "hd", true);
+        GW_LAUNCH(k_hard_unpack, grid_for(n_hard_w), kThreads, 0, st, hkey, n_hard_w, hev);
+      }
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hcnt}, HardSegStore{hcnt, hbeg, hend}, ng, OpSum(), 0u, false,
+                            "sc_u32");
+      sa.hard_ev = hev;
+      sa.hb_beg = hbeg;
+      sa.hb_end = hend;
+      sa.snap = C->get<uint2>("snap", snap_entries);
+      GW_LAUNCH(k_walker_wsnap, std::min<uint32_t>(tr.B, (uint32_t)gmax), kThreads, 0, st, w, sa);
+      stamps.time = nullptr;
+      stamps.vobj = nullptr;
+      stamps.hard_ev = sa.hard_ev;
+      stamps.hb_beg = sa.hb_beg;
+      stamps.hb_end = sa.hb_end;
+      stamps.snap = sa.snap;
+      stamps.BS = tr.BS;
+      stamps.warp_mode = 1;
+      stamps.L = tr.L;
+      C->stats.walker_ctas = std::min<uint32_t>(tr.B, (uint32_t)gmax);
     } else {
       stamps.time = w.time;
       stamps.vobj = w.vobj;
@@ -1141,7 +1186,7 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   Plan np;
   np.N = tr.n; np.B = tr.B; np.W = tr.W; np.L = tr.L; np.inactive_opt = inactive;
   np.key = kp; np.tidop = tp; np.instr = ip; np.stream = st;
-  np.n_bar = p.obs.n_bar; np.n_end = p.obs.n_end; np.D = p.obs_D;
+  np.n_bar = p.obs.n_bar; np.n_end = p.obs.n_end; np.n_wbar = p.obs.n_wbar; np.D = p.obs_D;
   np.cand_cap = 2ull * p.obs_ncand + 4096;  // tight: graph replays size the dedup / order passes by it
   c->plan = np;
   Pipeline g;

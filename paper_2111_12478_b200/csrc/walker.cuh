@@ -1283,6 +1283,52 @@ __global__ void __launch_bounds__(kThreads) k_walker_snap(WalkArgs a, SnapArgs s
   }
 }
 
+// ---------------------------------------- warp snapshot mode (lock-free) --
+// Traces whose hard events are mostly warp barriers (ITS-style, C4): a warp
+// barrier only involves its own warp, so each of the block's (<= 8) warps
+// walks its own hard-event list -- its warp barriers, its threads' ENDs, and
+// the block barriers (replicated into every list, where the CTA's warps meet
+// for the CTA-wide join) -- and writes its 32 lanes' {local, pred object}
+// after each entry.  List g = b * 8 + warp; snapshot row r of list g at
+// (hb_beg[g] + g + r) * 32.  Requires warps <= 8 and lanes <= 32.
+constexpr uint32_t kWSnapWarps = 8;
+__global__ void __launch_bounds__(kThreads) k_walker_wsnap(WalkArgs a, SnapArgs s) {
+  __shared__ __align__(16) uint32_t s_acc[kAccSmem];
+  const DevTrace& tr = a.tr;
+  if (*(volatile const uint32_t*)a.abort_flag) return;
+  const uint32_t j = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* wacc = s_acc + j * 256;  // this warp's barrier accumulator (span = block range <= 256)
+  for (uint32_t b = blockIdx.x; b < tr.B; b += gridDim.x) {
+    const uint32_t g = b * kWSnapWarps + j;
+    const uint32_t beg = s.hb_beg[g], end = s.hb_end[g];
+    uint2* row = s.snap + (size_t)(beg + g) * 32;
+    const uint32_t t = b * tr.BS + j * tr.L + lane;
+    const bool mine = j < tr.W && lane < tr.L;
+    if (mine) row[lane] = make_uint2(a.local[t], a.pobj[t]);
+    for (uint32_t h = beg; h < end; h++) {
+      const uint32_t e = s.hard_ev[h];
+      const uint32_t to = tr.tidop[e];
+      if (ev_kind(to) == GW_K_BARRIER && !(to & GW_F_WARPBAR)) {
+        __syncthreads();  // every warp of the block reaches this block barrier in its list
+        do_barrier(a, to, 0u, s_acc);
+      } else if (ev_kind(to) == GW_K_BARRIER) {
+        do_barrier_warp(a, to, tr.instr[e], wacc);
+      } else {  // END of one of this warp's threads
+        if (lane == 0) {
+          const uint32_t te = ev_tid(to);
+          a.exited[te] = 1;
+          a.nend[te] = a.nend[te] + 1;
+        }
+        __syncwarp();
+      }
+      row += 32;
+      if (mine) row[lane] = make_uint2(a.local[t], a.pobj[t]);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_stamp(WalkArgs a, SnapArgs s) {
   const DevTrace& tr = a.tr;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
@@ -1304,6 +1350,29 @@ __global__ void __launch_bounds__(kThreads) k_stamp(WalkArgs a, SnapArgs s) {
 // hard events (barriers, ENDs) of a lock-free trace: appended in any order as
 // (block << 32 | event) keys with warp-aggregated atomics, then sorted, which
 // orders them by block and by trace order within a block
+// warp snapshot mode: (list g << 32 | event), block barriers once per warp list
+__global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
+                                const uint32_t* abort_flag) {
+  if (*(volatile const uint32_t*)abort_flag) return;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t to = tr.tidop[e];
+    const uint32_t k = ev_kind(to);
+    if (k != GW_K_BARRIER && k != GW_K_END) continue;
+    const uint32_t t = ev_tid(to), b = t / tr.BS;
+    if (k == GW_K_BARRIER && !(to & GW_F_WARPBAR)) {
+      const uint32_t base = atomicAdd(ntop, kWSnapWarps);
+      for (uint32_t j = 0; j < kWSnapWarps; j++) {
+        const uint32_t g = b * kWSnapWarps + j;
+        hkey[base + j] = ((unsigned long long)g << 32) | (uint32_t)e;
+        atomicAdd(hcnt + g, 1u);
+      }
+    } else {
+      const uint32_t g = b * kWSnapWarps + (t % tr.BS) / tr.L;
+      hkey[atomicAdd(ntop, 1u)] = ((unsigned long long)g << 32) | (uint32_t)e;
+      atomicAdd(hcnt + g, 1u);
+    }
+  }
+}
 __global__ void k_hard_append(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
                               const uint32_t* abort_flag) {
   if (*(volatile const uint32_t*)abort_flag) return;  // graph mode: the plan does not fit this trace

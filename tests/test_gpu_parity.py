@@ -298,3 +298,25 @@ def test_address_sharded_goldens(goldens, ctx):
         assert ndjson_lines(tr, merged) == (r["reports"] if "reports" in r else ndjson_lines(tr, _run(ctx, tr)))
         n += 1
     assert n > 0
+
+
+@pytest.mark.parametrize("mode", ["block", "warp", "walker"])
+def test_lock_free_sync_pass_modes(ctx, mode, goldens, monkeypatch):
+    """The three lock-free sync-pass forms (block snapshots, per-warp snapshots,
+    the sequential walker) give identical, reference-exact results."""
+    monkeypatch.setenv("GW_WALK_MODE", mode)
+    traces = [
+        parse_trace(WL.c4_text(blocks=6, warps=8, lanes=32, iters=30, words_per_block=512, seed=300)),
+        parse_trace(WL.c4_text(blocks=3, warps=5, lanes=16, iters=12, words_per_block=256, seed=301)),
+        WL.c2_soa(blocks=16, warps=4, lanes=32, phases=4, records=4, words_per_block=256, seed=302),
+    ]
+    for tr in traces:
+        assert ndjson_lines(tr, _run(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
+    n = 0
+    for r in goldens:
+        if "error" in r or "full" in r["tags"] or not ({"corpus", "random", "c4"} & set(r["tags"])):
+            continue
+        tr = parse_trace(golden_text(r))
+        check_against_golden(r, tr, _run(ctx, tr, r["inactive_opt"]))
+        n += 1
+    assert n > 0
