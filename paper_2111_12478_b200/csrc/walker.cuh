@@ -45,7 +45,6 @@ constexpr int kWalkCH = 2048;              // events staged per chunk
 constexpr int kAccSmem = 4096;             // barrier accumulator kept in smem up to this span
 constexpr uint32_t OBJ_HDR = 4;            // object header {lo, len, ref, pad}: data 16-byte aligned
 constexpr int OBJ_USHIFT = 4;              // object handles count 64-byte units (2^32 units = 256 GiB)
-constexpr uint32_t REF_PERM = 0x40000000u; // reference count of objects that are never collected
 
 // lflags bits (lock pre-pass)
 constexpr uint8_t LF_OK = 1;      // successful acquire / release
@@ -57,7 +56,11 @@ constexpr uint8_t LF_QUERY = 8;   // access with race-check queries (lock mode)
 constexpr uint32_t ERR_ARENA = 1, ERR_TABLE = 2, ERR_FRAMES = 4, ERR_LOG = 8, ERR_REC = 16, ERR_DIAG = 32,
                    ERR_CAND = 64, ERR_RECORD = 128, ERR_INTERNAL = 256;
 
-struct Frame { unsigned long long lock; uint32_t scope, rec, logpos, pad; };
+// iver: release version of the frame's own instance when the acquire joined it
+struct Frame { unsigned long long lock; uint32_t scope, rec, logpos, iver; };
+// a clock reference: object o joined with one explicit entry [dtid] = dval
+// (the owner's diagonal: hb_t[t] = local_t, pred_t[t] = pdiag_t)
+struct CRef { uint32_t o, dtid, dval; };
 // CSRecord (gwcp.py:32-43): the acquire clock kept as its epoch (tid, acq_local),
 // the release clock as the releaser's hb object + diagonal.  domall: this
 // record's release clock dominates every earlier record's of the lock.
@@ -65,8 +68,10 @@ struct Rec { uint32_t tid, acq_local, scope, rel_hobj, rel_local, closed, domall
 // a lock's records occupy [rec_base, rec_base + nrec) in acquire order
 struct LockEnt { unsigned long long id; uint32_t used, nrec, rec_base, pad, inst_head, ticket; };
 struct CurEnt { unsigned long long lock; uint32_t tid, used, epoch, last, bound, snap; };
-struct InstEnt { unsigned long long lock; uint32_t scope, used, H, P, next, pad; };
-struct CsEnt { unsigned long long lock, loc; uint32_t scope_rw, used, arr, pad; };
+// lock instance (gwcp.py:69-79): clocks H_i / P_i as references (refcounted
+// objects, never mutated in place), relver = releases into it so far
+struct InstEnt { unsigned long long lock; uint32_t scope, used; CRef H, P; uint32_t next, relver; };
+struct CsEnt { unsigned long long lock, loc; uint32_t scope_rw, used; CRef c; uint32_t pad; };
 struct LogEnt { unsigned long long loc; uint32_t rw, next; };
 struct Diag { uint32_t ev, code, sub, pad; unsigned long long lock; };
 
@@ -272,7 +277,10 @@ __device__ InstEnt* inst_find(const WalkArgs& a, unsigned long long lock, uint32
   const uint32_t h = (uint32_t)mix64(lock ^ ((unsigned long long)scope << 40) ^ 0x51ull) & a.inst_mask;
   return ht_find(a, a.insts, a.inst_mask, h, create,
                  [&](InstEnt* e) { return __ldcg(&e->lock) == lock && __ldcg(&e->scope) == scope; },
-                 [&](InstEnt* e) { e->lock = lock; e->scope = scope; e->H = NIL; e->P = NIL; e->next = NIL; });
+                 [&](InstEnt* e) {
+                   e->lock = lock; e->scope = scope; e->H = CRef{NIL, NIL, 0u}; e->P = CRef{NIL, NIL, 0u};
+                   e->next = NIL; e->relver = 0;
+                 });
 }
 
 __device__ CsEnt* cs_find(const WalkArgs& a, unsigned long long lock, uint32_t scope, unsigned long long loc,
@@ -283,7 +291,7 @@ __device__ CsEnt* cs_find(const WalkArgs& a, unsigned long long lock, uint32_t s
                  [&](CsEnt* e) {
                    return __ldcg(&e->lock) == lock && __ldcg(&e->loc) == loc && __ldcg(&e->scope_rw) == srw;
                  },
-                 [&](CsEnt* e) { e->lock = lock; e->loc = loc; e->scope_rw = srw; e->arr = NIL; });
+                 [&](CsEnt* e) { e->lock = lock; e->loc = loc; e->scope_rw = srw; e->c = CRef{NIL, NIL, 0u}; });
 }
 
 // ------------------------------------------------------------- helpers ----
@@ -645,13 +653,13 @@ __device__ void tickets_release(const WalkArgs& a, uint32_t e) {
 //
 // The sequential pop loop (test C_t[r.tid] >= r.acq_local on the clock that
 // includes every earlier pop's release clock, then join) runs 32 records at a
-// time on warp 0: each lane evaluates its record's test on P plus the
-// release clocks of the records before it, found by walking back to the
-// nearest joined record whose release clock dominates all earlier ones
-// (Rec::domall), so the walk is short and the joins themselves are deferred:
-// a drain ends with one join of the last dominating record (+ the few
-// non-dominating ones after it).  Other warps wait at the CTA barrier.
-constexpr int kDrainJ = 16;  // deferred non-dominating joins before a flush
+// time on warp 0: each lane evaluates its record's test on pred_t (point
+// reads of t's pred object -- no materialised clock) plus the release clocks
+// of the records before it, found by walking back to the nearest joined
+// record whose release clock dominates all earlier ones (Rec::domall).  The
+// joins themselves are only collected (s_m + s_j): the caller applies them,
+// usually after giving the lock's ticket back.
+constexpr int kDrainJ = 16;  // collected non-dominating joins before the scan stops early
 
 __device__ __forceinline__ uint32_t relpt(const WalkArgs& a, uint32_t rel_hobj, uint32_t rtid, uint32_t rel_local,
                                           uint32_t u, uint32_t vu) {
@@ -659,11 +667,22 @@ __device__ __forceinline__ uint32_t relpt(const WalkArgs& a, uint32_t rel_hobj, 
   return rtid == u ? max(v, rel_local) : v;
 }
 
-__device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uint32_t cur, uint32_t* P) {
+struct DrainOut {      // shared-memory result of drain_scan
+  uint32_t m;          // last popped dominating joinable record (NIL: none)
+  uint32_t nj;         // popped joinable records after it
+  uint32_t j[kDrainJ];
+  uint32_t more;       // the scan stopped early (kDrainJ reached): call again after applying
+};
+
+// One drain scan (caller: the whole CTA, holding the lock's ticket).  extra:
+// records already collected by an earlier scan of this drain whose joins are
+// not yet in t's pred object (their values count in the tests).
+__device__ void drain_scan(const WalkArgs& a, uint32_t t, unsigned long long lock, uint32_t cur, DrainOut& O,
+                           bool first, const DrainOut* extra) {
   __shared__ CurEnt* s_cur;
   __shared__ LockEnt* s_lk;
   __shared__ uint32_t s_tid[32], s_acq[32], s_ho[32], s_loc[32], s_flags[32];
-  __shared__ uint32_t s_m, s_nj, s_j[kDrainJ], s_stop, s_pos, s_end;
+  __shared__ uint32_t s_pos, s_end;
   if (threadIdx.x == 0) {
     LockEnt* lk = lock_find(a, lock, false);
     CurEnt* ce = lk ? cur_find(a, lock, t) : nullptr;
@@ -671,7 +690,7 @@ __device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uin
     s_cur = ce;
     if (ce) {
       uint32_t ep = a.nend[t];
-      if (__ldcg(&ce->epoch) != ep) {  // (re)materialise the queue
+      if (first && __ldcg(&ce->epoch) != ep) {  // (re)materialise the queue
         ce->epoch = ep;
         ce->last = NIL;
         ce->snap = ep != 0;
@@ -682,112 +701,91 @@ __device__ int drain(const WalkArgs& a, uint32_t t, unsigned long long lock, uin
       s_pos = last == NIL ? base : last + 1;
       s_end = base + (ce->snap ? min(nrec, __ldcg(&ce->bound)) : nrec);
     }
-    s_m = NIL;
-    s_nj = 0;
+    O.m = NIL;
+    O.nj = 0;
+    O.more = 0;
   }
   __syncthreads();
-  if (!s_cur) return 0;
+  if (!s_cur) return;
   const bool snap = __ldcg(&s_cur->snap) != 0;
-  int changed = 0;
-  while (true) {
-    if (threadIdx.x < 32) {
-      const uint32_t lane = threadIdx.x;
-      uint32_t pos = s_pos;
-      const uint32_t end = s_end;
-      uint32_t m = s_m, nj = s_nj;
-      bool stop = false, flush = false;
-      while (!stop && !flush && pos < end) {
-        const uint32_t idx = pos + lane;
-        const bool in = idx < end;
-        uint32_t fl = 0;  // bit0 in, bit1 own (skipped), bit2 closed, bit3 joinable, bit4 domall
-        if (in) {
-          const Rec* r = a.recs + idx;
-          const uint32_t rt = __ldcg(&r->tid);
-          s_tid[lane] = rt;
-          s_acq[lane] = __ldcg(&r->acq_local);
-          s_ho[lane] = __ldcg(&r->rel_hobj);
-          s_loc[lane] = __ldcg(&r->rel_local);
-          const bool own = !snap && rt == t;
-          const bool closed = __ldcg(&r->closed) != 0;
-          fl = 1u | (own ? 2u : 0u) | (closed ? 4u : 0u) |
-               ((!own && closed && sc_overlap(__ldcg(&r->scope), cur)) ? 8u : 0u) | (__ldcg(&r->domall) ? 16u : 0u);
-        }
-        s_flags[lane] = fl;
-        __syncwarp();
-        // my test, assuming every record before me in the window is popped
-        bool pass = false;
-        if (fl & 2u) pass = true;          // own record: not in the queue, stepped over
-        else if (!(fl & 4u)) pass = false;  // open (or past the end): the drain stops here
-        else if (s_tid[lane] == t) pass = true;
-        else {
-          const uint32_t u = s_tid[lane], vu = vidx(a, u);
-          uint32_t v = vu != NIL ? P[vu] : 0u;
-          bool dom = false;
-          for (int i = (int)lane - 1; i >= 0 && !dom; i--) {
-            const uint32_t fi = s_flags[i];
-            if (!(fi & 8u)) continue;
-            v = max(v, relpt(a, s_ho[i], s_tid[i], s_loc[i], u, vu));
-            dom = (fi & 16u) != 0;
-          }
-          if (!dom) {  // carried, not yet applied joins of earlier windows
-            for (uint32_t k = 0; k < nj; k++) {
-              const Rec* r = a.recs + s_j[k];
-              v = max(v, relpt(a, __ldcg(&r->rel_hobj), __ldcg(&r->tid), __ldcg(&r->rel_local), u, vu));
-            }
-            if (m != NIL) {
-              const Rec* r = a.recs + m;
-              v = max(v, relpt(a, __ldcg(&r->rel_hobj), __ldcg(&r->tid), __ldcg(&r->rel_local), u, vu));
-            }
-          }
-          pass = v >= s_acq[lane];
-        }
-        const uint32_t fails = __ballot_sync(0xffffffffu, !(in && pass));
-        uint32_t f = fails ? (uint32_t)(__ffs(fails) - 1) : 32u;  // records [pos, pos + f) are popped
-        // carry the popped joinable records (uniform over the warp)
-        for (uint32_t i = 0; i < f; i++) {
+  const uint32_t po = a.pobj[t];
+  if (threadIdx.x < 32) {
+    const uint32_t lane = threadIdx.x;
+    uint32_t pos = s_pos;
+    const uint32_t end = s_end;
+    uint32_t m = NIL, nj = 0;
+    bool stop = false, full = false;
+    while (!stop && !full && pos < end) {
+      const uint32_t idx = pos + lane;
+      const bool in = idx < end;
+      uint32_t fl = 0;  // bit0 in, bit1 own (skipped), bit2 closed, bit3 joinable, bit4 domall
+      if (in) {
+        const Rec* r = a.recs + idx;
+        const uint32_t rt = __ldcg(&r->tid);
+        s_tid[lane] = rt;
+        s_acq[lane] = __ldcg(&r->acq_local);
+        s_ho[lane] = __ldcg(&r->rel_hobj);
+        s_loc[lane] = __ldcg(&r->rel_local);
+        const bool own = !snap && rt == t;
+        const bool closed = __ldcg(&r->closed) != 0;
+        fl = 1u | (own ? 2u : 0u) | (closed ? 4u : 0u) |
+             ((!own && closed && sc_overlap(__ldcg(&r->scope), cur)) ? 8u : 0u) | (__ldcg(&r->domall) ? 16u : 0u);
+      }
+      s_flags[lane] = fl;
+      __syncwarp();
+      // my test, assuming every record before me in the window is popped
+      bool pass = false;
+      if (fl & 2u) pass = true;          // own record: not in the queue, stepped over
+      else if (!(fl & 4u)) pass = false;  // open (or past the end): the drain stops here
+      else if (s_tid[lane] == t) pass = true;
+      else {
+        const uint32_t u = s_tid[lane], vu = vidx(a, u);
+        uint32_t v = vu != NIL ? obj_get_cg(a.arena, po, vu) : 0u;  // pred_t[u], u != t
+        bool dom = false;
+        for (int i = (int)lane - 1; i >= 0 && !dom; i--) {
           const uint32_t fi = s_flags[i];
           if (!(fi & 8u)) continue;
-          if (fi & 16u) { m = pos + i; nj = 0; }
-          else if (nj < (uint32_t)kDrainJ) { if (lane == 0) s_j[nj] = pos + i; nj++; }
-          else { f = i; flush = true; break; }  // pop it after applying the deferred joins
+          v = max(v, relpt(a, s_ho[i], s_tid[i], s_loc[i], u, vu));
+          dom = (fi & 16u) != 0;
         }
-        if (f < 32u && !flush) stop = true;
-        pos += f;
-        __syncwarp();
+        if (!dom) {  // collected, not yet applied joins (this scan's earlier windows, the caller's)
+          for (int src = 0; src < 2; src++) {
+            const uint32_t mm = src == 0 ? m : (extra ? extra->m : NIL);
+            const uint32_t nn = src == 0 ? nj : (extra ? extra->nj : 0u);
+            const uint32_t* jj = src == 0 ? O.j : (extra ? extra->j : nullptr);
+            for (uint32_t k = 0; k < nn; k++) {
+              const Rec* r = a.recs + jj[k];
+              v = max(v, relpt(a, __ldcg(&r->rel_hobj), __ldcg(&r->tid), __ldcg(&r->rel_local), u, vu));
+            }
+            if (mm != NIL) {
+              const Rec* r = a.recs + mm;
+              v = max(v, relpt(a, __ldcg(&r->rel_hobj), __ldcg(&r->tid), __ldcg(&r->rel_local), u, vu));
+            }
+          }
+        }
+        pass = v >= s_acq[lane];
       }
-      if (lane == 0) {
-        s_pos = pos;
-        s_m = m;
-        s_nj = nj;
-        s_stop = (stop || pos >= end) ? 1u : 0u;
-        if (pos > __ldcg(&s_lk->rec_base)) s_cur->last = pos - 1;
+      const uint32_t fails = __ballot_sync(0xffffffffu, !(in && pass));
+      uint32_t f = fails ? (uint32_t)(__ffs(fails) - 1) : 32u;  // records [pos, pos + f) are popped
+      for (uint32_t i = 0; i < f; i++) {  // uniform over the warp
+        const uint32_t fi = s_flags[i];
+        if (!(fi & 8u)) continue;
+        if (fi & 16u) { m = pos + i; nj = 0; }
+        else if (nj < (uint32_t)kDrainJ) { if (lane == 0) O.j[nj] = pos + i; nj++; }
+        else { f = i; full = true; break; }  // pop it after the collected joins are applied
       }
+      if (f < 32u && !full) stop = true;
+      pos += f;
+      __syncwarp();
     }
-    __syncthreads();
-    // apply the deferred joins (block-wide)
-    int ch = 0;
-    const uint32_t nj = s_nj;
-    for (int k = -1; k < (int)nj; k++) {
-      const uint32_t ri = k < 0 ? s_m : s_j[k];
-      if (ri == NIL) continue;
-      const Rec* r = a.recs + ri;
-      ch |= join_obj_dense(P, a.arena, __ldcg(&r->rel_hobj));
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const uint32_t vr = vidx(a, __ldcg(&r->tid));
-        const uint32_t loc = __ldcg(&r->rel_local);
-        if (vr != NIL && loc > P[vr]) { P[vr] = loc; ch = 1; }
-      }
-      __syncthreads();
+    if (lane == 0) {
+      O.m = m;
+      O.nj = nj;
+      O.more = (full && pos < end) ? 1u : 0u;
+      if (pos > __ldcg(&s_lk->rec_base)) s_cur->last = pos - 1;
     }
-    changed |= __syncthreads_or(ch);
-    const bool done = s_stop != 0;
-    __syncthreads();
-    if (threadIdx.x == 0) { s_m = NIL; s_nj = 0; }
-    __syncthreads();
-    if (done) break;
   }
-  return changed;
+  __syncthreads();
 }
 
 // replace thread t's pred / hb object (thread 0; lock mode reference counts)
@@ -812,6 +810,66 @@ __device__ void answer_queries(const WalkArgs& a, uint32_t e, uint32_t o) {
   }
 }
 
+// ---- captured joins: clock references read under a ticket, applied later --
+constexpr int kMaxCap = 40;
+struct CapList {
+  CRef c[kMaxCap];
+  uint32_t tgt[kMaxCap];  // 0: pred (P), 1: hb (H)
+  uint32_t n;
+  uint32_t full;
+};
+// thread 0, under the ticket: keep o alive until applied
+__device__ __forceinline__ bool cap_push(const WalkArgs& a, CapList& L, CRef c, uint32_t tgt) {
+  if (c.o == NIL && c.dtid == NIL) return true;
+  if (L.n >= (uint32_t)kMaxCap) { L.full = 1; return false; }
+  obj_retain(a, c.o);
+  L.c[L.n] = c;
+  L.tgt[L.n] = tgt;
+  L.n++;
+  return true;
+}
+__device__ __forceinline__ CRef rec_cref(const WalkArgs& a, uint32_t ri) {
+  const Rec* r = a.recs + ri;
+  return CRef{__ldcg(&r->rel_hobj), __ldcg(&r->tid), __ldcg(&r->rel_local)};
+}
+// dense dst max= clock reference c (block-wide); returns nonzero if dst grew
+__device__ int join_cref(const WalkArgs& a, uint32_t* dst, CRef c) {
+  int ch = join_obj_dense(dst, a.arena, c.o);
+  __syncthreads();
+  if (threadIdx.x == 0 && c.dtid != NIL) {
+    const uint32_t v = vidx(a, c.dtid);
+    if (v != NIL && c.dval > dst[v]) { dst[v] = c.dval; ch = 1; }
+  }
+  return __syncthreads_or(ch);
+}
+// apply and drop the captured references; pch / hch accumulate "grew"
+__device__ void cap_apply(const WalkArgs& a, CapList& L, uint32_t* P, uint32_t* H, int& pch, int& hch) {
+  const uint32_t n = L.n;
+  for (uint32_t k = 0; k < n; k++) {
+    const CRef c = L.c[k];
+    if (L.tgt[k] == 0) pch |= join_cref(a, P, c);
+    else hch |= join_cref(a, H, c);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < n; k++) obj_release(a, L.c[k].o);
+    L.n = 0;
+    L.full = 0;
+  }
+  __syncthreads();
+}
+// collect a drain's joins (targets pred)
+__device__ __forceinline__ void cap_drain(const WalkArgs& a, CapList& L, const DrainOut& O) {
+  if (O.m != NIL) cap_push(a, L, rec_cref(a, O.m), 0);
+  for (uint32_t k = 0; k < O.nj; k++) cap_push(a, L, rec_cref(a, O.j[k]), 0);
+}
+
+// on_acquire (gwcp.py:175-192).  Under the lock's ticket (taken by the
+// caller): the drain scan, the instance clocks to join (captured), the
+// record and the frame.  The ticket is then given back and the O(|Q|) clock
+// work -- materialise pred / hb, join, publish -- happens outside it: those
+// objects are immutable (refcounted) and nobody else reads t's clocks before
+// this CTA's next event of t.
 __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long lock) {
   const uint32_t n = vlen(a);
   const uint32_t t = ev_tid(to);
@@ -820,57 +878,49 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * n;
   uint32_t* H = P + n;
   __shared__ LockEnt* s_lk;
-  if (threadIdx.x == 0) s_lk = lock_find(a, lock, false);  // created by the pre-pass
-  __syncthreads();
-  if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); return; }
-  materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]);
-  int pch = drain(a, t, lock, cur, P);
-  materialize(H, a.arena, a.hobj[t], n, vt, a.local[t]);
-  int hch = 0;
-  // join instance clocks whose release orders this acquire (gwcp.py:185-188, scopes.py:50-59)
-  __shared__ uint32_t s_i, s_H, s_P;
-  if (threadIdx.x == 0) s_i = __ldcg(&s_lk->inst_head);
-  __syncthreads();
-  while (true) {
-    if (threadIdx.x == 0) {
-      uint32_t i = s_i;
-      while (i != NIL && !sc_overlap(__ldcg(&a.insts[i].scope), cur)) i = __ldcg(&a.insts[i].next);
-      s_i = i;
-      if (i != NIL) { s_H = __ldcg(&a.insts[i].H); s_P = __ldcg(&a.insts[i].P); }
-    }
-    __syncthreads();
-    uint32_t i = s_i;
-    if (i == NIL) break;
-    hch |= join_obj_dense(H, a.arena, s_H);
-    pch |= join_obj_dense(P, a.arena, s_P);
-    __syncthreads();
-    if (threadIdx.x == 0) s_i = __ldcg(&a.insts[i].next);
-    __syncthreads();
-  }
-  pch = __syncthreads_or(pch);
-  hch = __syncthreads_or(hch);
-  if (pch) {
-    uint32_t o = publish_dense(a, P, n, 1);
-    if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
-  }
-  if (hch) {
-    uint32_t o = publish_dense(a, H, n, 1);
-    if (threadIdx.x == 0) set_obj(a, a.hobj, t, o);
-  }
+  __shared__ DrainOut s_dr;
+  __shared__ CapList s_cap;
+  __shared__ uint32_t s_inst, s_done;
   if (threadIdx.x == 0) {
-    // CSRecord(acq_clock = C_t) appended to the lock's records; the acquire
-    // clock is kept as its epoch (t, local) -- see the drain-test note above.
+    s_lk = lock_find(a, lock, false);  // created by the pre-pass
+    s_cap.n = 0;
+    s_cap.full = 0;
+  }
+  __syncthreads();
+  if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); tickets_release(a, e); return; }
+  int pch = 0, hch = 0;
+  bool mat = false;
+  // (1) drain: scans until done, applying the collected joins in between when a scan fills up
+  bool first = true;
+  while (true) {
+    drain_scan(a, t, lock, cur, s_dr, first, nullptr);
+    first = false;
+    if (threadIdx.x == 0) cap_drain(a, s_cap, s_dr);
+    __syncthreads();
+    if (!s_dr.more) break;
+    if (!mat) { materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]); materialize(H, a.arena, a.hobj[t], n, vt, a.local[t]); mat = true; }
+    cap_apply(a, s_cap, P, H, pch, hch);  // still under the ticket (rare: > kDrainJ non-dominating pops)
+    if (pch) {
+      uint32_t o = publish_dense(a, P, n, 1);
+      if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
+      pch = 0;
+      __syncthreads();
+    }
+  }
+  // (2) the record (acq_clock kept as its epoch (t, local); see the drain-test note) and the frame
+  if (threadIdx.x == 0) {
     LockEnt* lk = s_lk;
     const uint32_t ri = a.rix[a.poff[e]];
-    uint32_t d = a.depth[t];
+    const uint32_t d = a.depth[t];
+    InstEnt* own = inst_find(a, lock, cur, false);
     if (ri >= a.rec_cap) { atomicOr(a.err, ERR_REC); }
     else if (d >= a.maxd) { atomicOr(a.err, ERR_FRAMES); }
     else {
       const uint32_t base = __ldcg(&lk->rec_base);
       // domall: the previous record was closed, dominated all before it, and
-      // its instance orders this acquire, so this acquire joined its release
-      // clock into hb (gwcp.py:185-188) and this record's release clock
-      // (hb at release) dominates every earlier record's
+      // its instance orders this acquire, so this acquire joins its release
+      // clock into hb (gwcp.py:185-188) and this record's release clock (hb
+      // at release) dominates every earlier record's
       uint32_t domall = 1;
       if (ri > base) {
         const Rec* pr = a.recs + ri - 1;
@@ -882,107 +932,193 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
       a.recs[ri] = r;
       lk->nrec = ri - base + 1;
       Frame f;
-      f.lock = lock; f.scope = cur; f.rec = ri; f.logpos = a.loghead[t]; f.pad = 0;
+      f.lock = lock; f.scope = cur; f.rec = ri; f.logpos = a.loghead[t];
+      f.iver = own ? __ldcg(&own->relver) : 0u;  // joined below (sc_overlap(cur, cur))
       a.frames[(size_t)t * a.maxd + d] = f;
       a.depth[t] = d + 1;
     }
+    s_inst = __ldcg(&lk->inst_head);
+  }
+  __syncthreads();
+  // (3) instance clocks whose release orders this acquire (gwcp.py:185-188, scopes.py:50-59)
+  bool released = false;
+  while (true) {
+    if (threadIdx.x == 0) {
+      uint32_t i = s_inst;
+      while (i != NIL) {
+        const InstEnt* ie = a.insts + i;
+        if (sc_overlap(__ldcg(&ie->scope), cur)) {
+          if (s_cap.n + 2 > (uint32_t)kMaxCap) break;  // apply these first
+          cap_push(a, s_cap, CRef{__ldcg(&ie->H.o), __ldcg(&ie->H.dtid), __ldcg(&ie->H.dval)}, 1);
+          cap_push(a, s_cap, CRef{__ldcg(&ie->P.o), __ldcg(&ie->P.dtid), __ldcg(&ie->P.dval)}, 0);
+        }
+        i = __ldcg(&ie->next);
+      }
+      s_inst = i;
+      s_done = i == NIL;
+    }
+    __syncthreads();
+    const bool done = s_done != 0;
+    if (done) { tickets_release(a, e); released = true; }
+    if (s_cap.n) {
+      if (!mat) {
+        materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]);
+        materialize(H, a.arena, a.hobj[t], n, vt, a.local[t]);
+        mat = true;
+      }
+      cap_apply(a, s_cap, P, H, pch, hch);
+    }
+    if (done) break;
+  }
+  if (!released) tickets_release(a, e);
+  if (pch) {
+    uint32_t o = publish_dense(a, P, n, 1);
+    if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
+  }
+  if (hch) {
+    uint32_t o = publish_dense(a, H, n, 1);
+    if (threadIdx.x == 0) set_obj(a, a.hobj, t, o);
   }
   __syncthreads();
 }
 
-// a new never-collected full-range object (instance / cs clocks), initialised from src
-__device__ __forceinline__ uint32_t alloc_perm(const WalkArgs& a, uint32_t n) {
-  uint32_t o = arena_alloc(a, n + OBJ_HDR);
-  if (o != NIL) obj_init(a, o, 0, n, REF_PERM);
-  return o;
+// target := src (thread 0): retain the new object, drop the old one
+__device__ __forceinline__ void cref_set(const WalkArgs& a, CRef* dst, CRef src) {
+  obj_retain(a, src.o);
+  const uint32_t old = __ldcg(&dst->o);
+  dst->o = src.o;
+  dst->dtid = src.dtid;
+  dst->dval = src.dval;
+  obj_release(a, old);
+}
+// target := target join src as a new object (block-wide; scratch S of n words)
+__device__ void cref_join_new(const WalkArgs& a, CRef* dst, CRef src, uint32_t* S, uint32_t n) {
+  __shared__ CRef s_old;
+  if (threadIdx.x == 0) s_old = CRef{__ldcg(&dst->o), __ldcg(&dst->dtid), __ldcg(&dst->dval)};
+  __syncthreads();
+  const CRef old = s_old;
+  materialize(S, a.arena, old.o, n, NIL, 0u);
+  if (threadIdx.x == 0 && old.dtid != NIL) {
+    const uint32_t v = vidx(a, old.dtid);
+    if (v != NIL && old.dval > S[v]) S[v] = old.dval;
+  }
+  __syncthreads();
+  join_cref(a, S, src);
+  const uint32_t o = publish_dense(a, S, n, 1);
+  if (threadIdx.x == 0) {
+    dst->o = o;
+    dst->dtid = NIL;
+    dst->dval = 0;
+    obj_release(a, old.o);
+  }
+  __syncthreads();
 }
 
+// on_release (gwcp.py:194-219), under the lock's ticket.  When no release
+// into the frame's instance happened since this thread's acquire joined it,
+// hb_t dominates H_i and every cs_read / cs_write clock of the instance, and
+// pred_t dominates P_i, so the joins are reference swaps (no clock work).
 __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long lock) {
   const uint32_t n = vlen(a);
   const uint32_t t = ev_tid(to);
   const uint32_t vt = vidx(a, t);
   uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * n;
   uint32_t* H = P + n;
+  uint32_t* S = H + n;
   __shared__ Frame s_f;
   __shared__ LockEnt* s_lk;
+  __shared__ DrainOut s_dr;
+  __shared__ CapList s_cap;
+  __shared__ InstEnt* s_ie;
+  __shared__ uint32_t s_dom, s_newi;
   if (threadIdx.x == 0) {
     uint32_t d = a.depth[t];
     s_f = a.frames[(size_t)t * a.maxd + (d - 1)];
     s_lk = lock_find(a, lock, false);
+    s_cap.n = 0;
+    s_cap.full = 0;
   }
   __syncthreads();
-  if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); return; }
+  if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); tickets_release(a, e); return; }
   const uint32_t inst = s_f.scope;
-  materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]);
-  int pch = drain(a, t, lock, inst, P);
-  if (pch) {
-    uint32_t o = publish_dense(a, P, n, 1);
-    if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
+  // (1) drain into pred
+  bool first = true;
+  bool mat = false;
+  int pch = 0, hch = 0;
+  while (true) {
+    drain_scan(a, t, lock, inst, s_dr, first, nullptr);
+    first = false;
+    if (threadIdx.x == 0) cap_drain(a, s_cap, s_dr);
     __syncthreads();
+    if (s_cap.n) {
+      if (!mat) { materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]); mat = true; }
+      cap_apply(a, s_cap, P, H, pch, hch);
+    }
+    if (pch) {  // the next scan (and P_i below) read t's published pred object
+      uint32_t o = publish_dense(a, P, n, 1);
+      if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
+      pch = 0;
+      __syncthreads();
+    }
+    if (!s_dr.more) break;
   }
-  materialize(H, a.arena, a.hobj[t], n, vt, a.local[t]);
-  // stage the frame's read / write sets with the hb clock (gwcp.py:207-210)
-  __shared__ uint32_t s_arr, s_new;
+  // (2) the frame's instance; dominance test
+  if (threadIdx.x == 0) {
+    InstEnt* ie = inst_find(a, lock, inst, true);
+    s_ie = ie;
+    s_newi = 0;
+    if (ie && __ldcg(&ie->H.o) == NIL && __ldcg(&ie->H.dtid) == NIL && __ldcg(&ie->relver) == 0) s_newi = 1;
+    s_dom = ie && __ldcg(&ie->relver) == s_f.iver;
+  }
+  __syncthreads();
+  const CRef hb = CRef{a.hobj[t], t, a.local[t]};
+  const CRef pr = CRef{a.pobj[t], t, a.pdiag[t]};
+  const bool dom = s_dom != 0;
+  // (3) cs_read / cs_write for the frame's read / write sets (gwcp.py:207-210)
+  __shared__ CsEnt* s_ce;
   uint32_t li = a.loghead[t];  // thread 0's iterator over the frame's access log
   while (true) {
     if (threadIdx.x == 0) {
-      s_arr = NIL;
-      s_new = 0;
-      while (li != s_f.logpos && li != NIL && s_arr == NIL) {
+      s_ce = nullptr;
+      while (li != s_f.logpos && li != NIL) {
         LogEnt le = a.logs[li];
         li = le.next;
         CsEnt* ce = cs_find(a, lock, inst, le.loc, le.rw, true);
         if (!ce) break;
-        if (ce->arr == NIL) {
-          uint32_t o = alloc_perm(a, n);
-          if (o == NIL) break;
-          ce->arr = o;
-          s_new = 1;
-        }
-        s_arr = ce->arr;
+        if (dom) { cref_set(a, &ce->c, hb); continue; }
+        s_ce = ce;
+        break;
       }
     }
     __syncthreads();
-    const uint32_t arr = s_arr;
-    if (arr == NIL) break;
-    uint32_t* dst = optr(a.arena, arr) + OBJ_HDR;
-    if (s_new) vcopy<false>(dst, H, n);
-    else vjoin<false, true>(dst, H, n);
-    __syncthreads();
+    CsEnt* ce = s_ce;
+    if (!ce) break;
+    cref_join_new(a, &ce->c, hb, S, n);  // not dominated: a new joined clock
   }
-  // instance clocks H_i, P_i (gwcp.py:211-216)
-  __shared__ uint32_t s_H, s_P, s_newi;
-  if (threadIdx.x == 0) {
-    InstEnt* ie = inst_find(a, lock, inst, true);
-    s_newi = 0;
-    s_H = NIL; s_P = NIL;
-    if (ie) {
-      if (ie->H == NIL) {
-        ie->H = alloc_perm(a, n);
-        ie->P = alloc_perm(a, n);
-        ie->next = __ldcg(&s_lk->inst_head);
-        s_lk->inst_head = (uint32_t)(ie - a.insts);
-        s_newi = 1;
-      }
-      s_H = ie->H; s_P = ie->P;
+  // (4) instance clocks H_i, P_i (gwcp.py:211-216)
+  if (s_ie) {
+    if (dom) {
+      if (threadIdx.x == 0) { cref_set(a, &s_ie->H, hb); cref_set(a, &s_ie->P, pr); }
+    } else {
+      cref_join_new(a, &s_ie->H, hb, S, n);
+      cref_join_new(a, &s_ie->P, pr, S, n);
     }
   }
   __syncthreads();
-  if (s_H != NIL && s_P != NIL) {
-    uint32_t* dh = optr(a.arena, s_H) + OBJ_HDR;
-    uint32_t* dp = optr(a.arena, s_P) + OBJ_HDR;
-    if (s_newi) { vcopy<false>(dh, H, n); vcopy<false>(dp, P, n); }
-    else { vjoin<false, true>(dh, H, n); vjoin<false, true>(dp, P, n); }
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
+    if (s_ie) {
+      if (s_newi) {  // first release into this instance: link it into the lock's list
+        s_ie->next = __ldcg(&s_lk->inst_head);
+        s_lk->inst_head = (uint32_t)(s_ie - a.insts);
+      }
+      s_ie->relver = __ldcg(&s_ie->relver) + 1;
+    }
     // close the record with rel_clock = copy(hb) (gwcp.py:216): the record
     // pins the thread's current hb object; pop; local += 1
     Rec* r = &a.recs[s_f.rec];
-    const uint32_t ho = a.hobj[t];
-    obj_retain(a, ho);
-    r->rel_hobj = ho;
-    r->rel_local = a.local[t];
+    obj_retain(a, hb.o);
+    r->rel_hobj = hb.o;
+    r->rel_local = hb.dval;
     __threadfence();
     r->closed = 1;
     uint32_t d = a.depth[t] - 1;
@@ -990,30 +1126,38 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     if (d == 0) a.loghead[t] = NIL;
     a.local[t] = a.local[t] + 1;
   }
+  tickets_release(a, e);
   __syncthreads();
 }
 
-// on_access inside critical sections: rule (i) joins (gwcp.py:236-249), then
-// the time stamp, the race-check queries and the frame-set append (gwcp.py:278-279)
+// on_access inside critical sections: rule (i) joins (gwcp.py:236-249) --
+// the cs clocks captured under the tickets, joined after -- then the time
+// stamp, the race-check queries and the frame-set append (gwcp.py:278-279)
 __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsigned long long loc) {
   const uint32_t n = vlen(a);
   const uint32_t t = ev_tid(to);
   const uint32_t vt = vidx(a, t);
   const uint32_t isw = ev_kind(to) == GW_K_WRITE;
   uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * n;
-  materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]);
-  int pch = 0;
-  __shared__ uint32_t s_arr;
+  __shared__ CapList s_cap;
+  __shared__ uint32_t s_done;
+  __shared__ uint32_t s_fi, s_ii, s_phase;
+  __shared__ unsigned long long s_flock;
+  __shared__ uint32_t s_fscope;
   const uint32_t depth = a.depth[t];
-  // thread 0 iterates frames x released instances of the frame's lock that
-  // overlap the frame's instance x {cs_write, cs_read if this is a write}
-  uint32_t fi = 0, ii = NIL, phase = 0;
-  unsigned long long flock = 0;
-  uint32_t fscope = 0;
+  if (threadIdx.x == 0) { s_cap.n = 0; s_cap.full = 0; s_fi = 0; s_ii = NIL; s_phase = 0; }
+  __syncthreads();
+  int pch = 0, hch = 0;
+  bool mat = false, released = false;
+  // frames x released instances of the frame's lock overlapping the frame's
+  // instance x {cs_write, cs_read if this is a write}
   while (true) {
     if (threadIdx.x == 0) {
-      uint32_t found = NIL;
-      while (found == NIL) {
+      uint32_t fi = s_fi, ii = s_ii, phase = s_phase;
+      unsigned long long flock = s_flock;
+      uint32_t fscope = s_fscope;
+      bool stop = false;
+      while (!stop) {
         if (phase == 0) {
           if (fi >= depth) break;
           const Frame f = a.frames[(size_t)t * a.maxd + fi];
@@ -1026,34 +1170,34 @@ __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsig
         if (ii == NIL) { fi++; phase = 0; continue; }
         const uint32_t isc = __ldcg(&a.insts[ii].scope);
         const bool ov = sc_overlap(isc, fscope);
-        if (phase == 1) {  // cs_write
+        if (phase == 1 || phase == 2) {
+          if (s_cap.n + 1 > (uint32_t)kMaxCap) { stop = true; break; }  // apply these first
           if (ov) {
-            CsEnt* ce = cs_find(a, flock, isc, loc, 1u, false);
-            if (ce && __ldcg(&ce->arr) != NIL) found = __ldcg(&ce->arr);
+            CsEnt* ce = cs_find(a, flock, isc, loc, phase == 1 ? 1u : 0u, false);
+            if (ce) cap_push(a, s_cap, CRef{__ldcg(&ce->c.o), __ldcg(&ce->c.dtid), __ldcg(&ce->c.dval)}, 0);
           }
-          phase = isw ? 2 : 3;
-        } else if (phase == 2) {  // cs_read
-          if (ov) {
-            CsEnt* ce = cs_find(a, flock, isc, loc, 0u, false);
-            if (ce && __ldcg(&ce->arr) != NIL) found = __ldcg(&ce->arr);
-          }
-          phase = 3;
+          phase = (phase == 1 && isw) ? 2 : 3;
         }
         if (phase == 3) { ii = __ldcg(&a.insts[ii].next); phase = 1; }
       }
-      s_arr = found;
+      s_fi = fi; s_ii = ii; s_phase = phase; s_flock = flock; s_fscope = fscope;
+      s_done = stop ? 0u : 1u;
     }
     __syncthreads();
-    const uint32_t arr = s_arr;
-    if (arr == NIL) break;
-    pch |= join_obj_dense(P, a.arena, arr);
-    __syncthreads();
+    const bool done = s_done != 0;
+    if (done) { tickets_release(a, e); released = true; }
+    if (s_cap.n) {
+      if (!mat) { materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]); mat = true; }
+      cap_apply(a, s_cap, P, nullptr, pch, hch);
+    }
+    if (done) break;
   }
-  pch = __syncthreads_or(pch);
+  if (!released) tickets_release(a, e);
   if (pch) {
     uint32_t o = publish_dense(a, P, n, 1);
     if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     a.time[e] = a.local[t];
     if (a.vobj) a.vobj[e] = a.pobj[t];
@@ -1214,17 +1358,15 @@ __global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
           } else {
             tickets_wait(a, e);
             pf.lap(2);
-            if (kd == GW_K_ACQUIRE) do_acquire(a, e, to, lock);
+            if (kd == GW_K_ACQUIRE) do_acquire(a, e, to, lock);  // gives the ticket back early
             else do_release(a, e, to, lock);
-            tickets_release(a, e);
             pf.lap(kd == GW_K_ACQUIRE ? 3 : 4);
             if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 8 + 7]++;
           }
         } else {  // in-CS access
           tickets_wait(a, e);
           pf.lap(2);
-          do_incs_access(a, e, to, tr.key[e]);
-          tickets_release(a, e);
+          do_incs_access(a, e, to, tr.key[e]);  // gives the tickets back early
           pf.lap(5);
           if (a.prof && threadIdx.x == 0) a.prof[blockIdx.x * 8 + 7]++;
         }
