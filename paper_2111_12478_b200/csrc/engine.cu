@@ -271,27 +271,9 @@ struct Pipeline {
     uint32_t* va = C->get<uint32_t>(t + "_va", n);
     const int npass = rs_passes(nbits);
     if (n >= kRsBigN) {
-      // reduce-then-scan passes: digit counts per tile, one scan, scatter
-      const uint64_t nt = lb_tiles(n);
-      uint32_t* counts = C->get<uint32_t>("rs_counts", nt * kRsDigits);
-      rs_down_setup<K>();
-      const unsigned g = (unsigned)std::min<uint64_t>(nt, 148ull * 24);
-      bool alt = false;
-      for (int p = 0; p < npass; p++) {
-        K* ki = alt ? ka : keys;
-        uint32_t* vi = alt ? va : vals;
-        K* ko = alt ? keys : ka;
-        uint32_t* vo = alt ? vals : va;
-        GW_LAUNCH(k_rs_up<K>, g, kThreads, 0, st, ki, n, p, counts, nt);
-        scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nt * kRsDigits, OpSum(), 0u,
-                              false, "sc_u32");
-        GW_LAUNCH(k_rs_down<K>, g, kThreads, sizeof(RsSmem<K>), st, ki, vi, ko, vo, n, p, counts, nt);
-        alt = !alt;
-      }
-      if (alt) {
-        keys = ka;
-        vals = va;
-      }
+      // reduce-then-scan passes: digit counts per super-tile, one scan, scatter
+      if (rs_big_bits(nbits) == 10) big_sort<K, 10>(keys, ka, vals, va, n, nbits);
+      else big_sort<K, 8>(keys, ka, vals, va, n, nbits);
       return;
     }
     SortScratch sc;
@@ -299,6 +281,32 @@ struct Pipeline {
     sc.ctrs = zeroed(npass);
     sc.status = C->get<unsigned long long>("rs_status", std::max(lb_tiles(n), lb_tiles(tr.n)) * kRsDigits);
     bool alt = radix_sort<K>(keys, ka, vals, va, n, nbits, sc, take_epochs(npass), st);
+    if (alt) {
+      keys = ka;
+      vals = va;
+    }
+  }
+
+  template <class K, int RB>
+  void big_sort(K*& keys, K* ka, uint32_t*& vals, uint32_t* va, uint64_t n, int nbits) {
+    const int npass = (nbits + RB - 1) / RB;
+    const uint64_t nst = (lb_tiles(n) + RsBig<RB>::ST - 1) / RsBig<RB>::ST;
+    uint32_t* counts = C->get<uint32_t>("rs_counts", nst * RsBig<RB>::ND);
+    rs_down_setup<K, RB>();
+    const unsigned g = (unsigned)std::min<uint64_t>(nst, 148ull * 16);
+    bool alt = false;
+    for (int p = 0; p < npass; p++) {
+      K* ki = alt ? ka : keys;
+      uint32_t* vi = alt ? va : vals;
+      K* ko = alt ? keys : ka;
+      uint32_t* vo = alt ? vals : va;
+      GW_LAUNCH((k_rs_up<K, RB>), g, kThreads, 0, st, ki, n, RB * p, counts, nst);
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nst * RsBig<RB>::ND, OpSum(), 0u,
+                            false, "sc_u32");
+      GW_LAUNCH((k_rs_down<K, RB>), g, kThreads, sizeof(RsBigSmem<K, RB>), st, ki, vi, ko, vo, n, RB * p, counts,
+                nst);
+      alt = !alt;
+    }
     if (alt) {
       keys = ka;
       vals = va;

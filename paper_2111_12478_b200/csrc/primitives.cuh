@@ -420,132 +420,180 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
 }
 
 // ---- reduce-then-scan radix pass (large n) ---------------------------------
-// No chained look-back: k_rs_up counts every tile's digits into a
-// digit-major matrix counts[d * ntiles + tile], one exclusive scan of that
-// matrix gives every (digit, tile) its global output offset, and
-// k_rs_down ranks / stages / scatters exactly like the one-sweep kernel but
-// reads its 256 bases instead of waiting on its predecessors.  Traffic per
-// pass: keys read twice, values once, both written once (+ 2 KB per tile).
-template <class K>
-__global__ void __launch_bounds__(kThreads) k_rs_up(const K* __restrict__ keys, uint64_t n, int pass,
-                                                   uint32_t* __restrict__ counts, uint64_t ntiles) {
-  __shared__ uint32_t h[kRsWarps][kRsDigits];
+// No chained look-back: k_rs_up counts the digits of every super-tile (ST
+// tiles of kTile keys) into a digit-major matrix counts[d * nst + st], one
+// exclusive scan of that matrix gives every (digit, super-tile) its output
+// offset, and k_rs_down ranks / stages / scatters tile by tile (ballot ranks
+// as in the one-sweep kernel), advancing its digit bases after each tile.
+// RB-bit digits (RB = 10: 3 passes for <= 30-bit keys); traffic per pass:
+// keys read twice, values once, both written once, + 4 * 2^RB B per super-tile.
+template <int RB>
+struct RsBig {
+  static constexpr int ND = 1 << RB;
+  static constexpr int DPT = ND / kThreads;  // digits per thread
+  static constexpr int ST = RB == 8 ? 1 : 4; // tiles per super-tile
+};
+
+template <class K, int RB>
+__global__ void __launch_bounds__(kThreads) k_rs_up(const K* __restrict__ keys, uint64_t n, int shift,
+                                                   uint32_t* __restrict__ counts, uint64_t nst) {
+  constexpr int ND = RsBig<RB>::ND, DPT = RsBig<RB>::DPT, ST = RsBig<RB>::ST;
+  __shared__ uint32_t h[kRsWarps][ND];  // per-warp histograms (low contention)
   const int w = threadIdx.x >> 5;
-  const int shift = kRsBits * pass;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (int d = threadIdx.x; d < kRsWarps * kRsDigits; d += kThreads) (&h[0][0])[d] = 0;
+  for (uint64_t st = blockIdx.x; st < nst; st += gridDim.x) {
+    for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&h[0][0])[d] = 0;
     __syncthreads();
-    const uint64_t base = tile * kTile;
-    K kk[kItems];
+    for (int sub = 0; sub < ST; sub++) {
+      const uint64_t base = (st * ST + sub) * kTile;
+      K kk[kItems];
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
-      const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
-      kk[k] = i < n ? keys[i] : (K)0;
-    }
+      for (int k = 0; k < kItems; k++) {
+        const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+        kk[k] = i < n ? keys[i] : (K)0;
+      }
 #pragma unroll
-    for (int k = 0; k < kItems; k++) {
-      const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
-      if (i < n) atomicAdd(&h[w][(uint32_t)(kk[k] >> shift) & (kRsDigits - 1)], 1u);
+      for (int k = 0; k < kItems; k++) {
+        const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+        if (i < n) atomicAdd(&h[w][(uint32_t)(kk[k] >> shift) & (ND - 1)], 1u);
+      }
     }
     __syncthreads();
-    const int d = threadIdx.x;
-    uint32_t c = 0;
 #pragma unroll
-    for (int x = 0; x < kRsWarps; x++) c += h[x][d];
-    counts[(uint64_t)d * ntiles + tile] = c;
+    for (int j = 0; j < DPT; j++) {
+      const int d = threadIdx.x * DPT + j;
+      uint32_t c = 0;
+#pragma unroll
+      for (int x = 0; x < kRsWarps; x++) c += h[x][d];
+      counts[(uint64_t)d * nst + st] = c;
+    }
     __syncthreads();
   }
 }
 
-template <class K>
-__global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down(const K* __restrict__ kin,
-                                                                          const uint32_t* __restrict__ vin,
-                                                                          K* __restrict__ kout,
-                                                                          uint32_t* __restrict__ vout, uint64_t n,
-                                                                          int pass,
-                                                                          const uint32_t* __restrict__ offsets,
-                                                                          uint64_t ntiles) {
-  constexpr int ND = kRsDigits;
+template <class K, int RB>
+struct RsBigSmem {
+  static constexpr int ND = 1 << RB;
+  uint32_t wc[kRsWarps][ND];  // per-warp digit counts -> per-warp offsets within the digit
+  uint32_t toff[ND];          // tile-local start of digit d
+  uint32_t gbase[ND];         // global start of digit d for the current tile
+  K sk[kTile];
+  uint32_t sv[kTile];
+};
+
+template <class K, int RB>
+__global__ void __launch_bounds__(kThreads, 2) k_rs_down(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                       K* __restrict__ kout, uint32_t* __restrict__ vout, uint64_t n,
+                                                       int shift, const uint32_t* __restrict__ offsets, uint64_t nst) {
+  constexpr int ND = RsBig<RB>::ND, DPT = RsBig<RB>::DPT, ST = RsBig<RB>::ST;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  RsSmem<K>& S = *reinterpret_cast<RsSmem<K>*>(smem_raw);
+  RsBigSmem<K, RB>& S = *reinterpret_cast<RsBigSmem<K, RB>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int shift = kRsBits * pass;
   const uint32_t lt = lanemask_lt();
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
-    // this tile's output base per digit (thread d)
-    const uint32_t gb = offsets[(uint64_t)threadIdx.x * ntiles + tile];
-    __syncthreads();
-    const uint64_t tbase = tile * kTile;
-    const uint64_t wbase = tbase + (uint64_t)w * kRsPerWarp;
-    const bool full = tbase + kTile <= n;
-    K kk[kRsRounds];
-    uint32_t vv[kRsRounds];
-    uint32_t rd[kRsRounds];
+  for (uint64_t st = blockIdx.x; st < nst; st += gridDim.x) {
 #pragma unroll
-    for (int r = 0; r < kRsRounds; r++) {
-      const uint64_t i = wbase + (uint64_t)r * 32 + lane;
-      const bool ok = full || i < n;
-      kk[r] = ok ? kin[i] : (K)0;
-      vv[r] = ok ? vin[i] : 0u;
-      rd[r] = ok ? (((uint32_t)(kk[r] >> shift) & (ND - 1)) << 16) : ((uint32_t)ND << 16);
+    for (int j = 0; j < DPT; j++) {
+      const int d = threadIdx.x * DPT + j;
+      S.gbase[d] = offsets[(uint64_t)d * nst + st];
     }
+    for (int sub = 0; sub < ST; sub++) {
+      const uint64_t tbase = (st * ST + sub) * kTile;
+      if (tbase >= n) break;
+      for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
+      __syncthreads();
+      const uint64_t wbase = tbase + (uint64_t)w * kRsPerWarp;
+      const bool full = tbase + kTile <= n;
+      K kk[kRsRounds];
+      uint32_t vv[kRsRounds];
+      uint32_t rd[kRsRounds];  // rank (bits 0-15) | digit (bits 16+, ND = none)
 #pragma unroll
-    for (int r = 0; r < kRsRounds; r++) {
-      const uint32_t d = rd[r] >> 16;
-      const uint32_t peers = full ? warp_peers<kRsBits>(d) : warp_peers<kRsBits + 1>(d);
-      const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
-      __syncwarp();
-      if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
-      rd[r] |= before + __popc(peers & lt);
-      __syncwarp();
-    }
-    __syncthreads();
-    {
-      const int d = threadIdx.x;
-      uint32_t run = 0;
-#pragma unroll
-      for (int ww = 0; ww < kRsWarps; ww++) {
-        const uint32_t t = S.wc[ww][d];
-        S.wc[ww][d] = run;
-        run += t;
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+        const bool ok = full || i < n;
+        kk[r] = ok ? kin[i] : (K)0;
+        vv[r] = ok ? vin[i] : 0u;
+        rd[r] = ok ? (((uint32_t)(kk[r] >> shift) & (ND - 1)) << 16) : ((uint32_t)ND << 16);
       }
-      uint32_t ct;
-      S.toff[d] = block_excl_scan<uint32_t, OpSum>(run, OpSum(), 0u, &ct);
-      S.gbase[d] = gb;
-    }
-    __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kRsRounds; r++) {
-      const uint32_t d = rd[r] >> 16;
-      if (d < (uint32_t)ND) {
-        const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
-        S.sk[pos] = kk[r];
-        S.sv[pos] = vv[r];
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint32_t d = rd[r] >> 16;
+        const uint32_t peers = full ? warp_peers<RB>(d) : warp_peers<RB + 1>(d);
+        const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
+        __syncwarp();
+        if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+        rd[r] |= before + __popc(peers & lt);
+        __syncwarp();
       }
-    }
-    __syncthreads();
-    const uint64_t rem = n > tbase ? n - tbase : 0ull;
-    const uint32_t cnt = rem < (uint64_t)kTile ? (uint32_t)rem : (uint32_t)kTile;
+      __syncthreads();
+      {
+        uint32_t tot[DPT], csum = 0;
+#pragma unroll
+        for (int j = 0; j < DPT; j++) {
+          const int d = threadIdx.x * DPT + j;
+          uint32_t run = 0;
+#pragma unroll
+          for (int ww = 0; ww < kRsWarps; ww++) {
+            const uint32_t t = S.wc[ww][d];
+            S.wc[ww][d] = run;
+            run += t;
+          }
+          tot[j] = run;
+          csum += run;
+        }
+        uint32_t ct;
+        uint32_t cex = block_excl_scan<uint32_t, OpSum>(csum, OpSum(), 0u, &ct);
+#pragma unroll
+        for (int j = 0; j < DPT; j++) {
+          S.toff[threadIdx.x * DPT + j] = cex;
+          cex += tot[j];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint32_t d = rd[r] >> 16;
+        if (d < (uint32_t)ND) {
+          const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
+          S.sk[pos] = kk[r];
+          S.sv[pos] = vv[r];
+        }
+      }
+      __syncthreads();
+      const uint64_t rem = n - tbase;
+      const uint32_t cnt = rem < (uint64_t)kTile ? (uint32_t)rem : (uint32_t)kTile;
 #pragma unroll 4
-    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-      const K k = S.sk[i];
-      const uint32_t d = (uint32_t)(k >> shift) & (ND - 1);
-      const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
-      kout[gp] = k;
-      vout[gp] = S.sv[i];
+      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+        const K k = S.sk[i];
+        const uint32_t d = (uint32_t)(k >> shift) & (ND - 1);
+        const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
+        kout[gp] = k;
+        vout[gp] = S.sv[i];
+      }
+      __syncthreads();
+      // advance the bases past this tile's runs
+#pragma unroll
+      for (int j = 0; j < DPT; j++) {
+        const int d = threadIdx.x * DPT + j;
+        const uint32_t end = d + 1 < ND ? S.toff[d + 1] : cnt;
+        S.gbase[d] += end - S.toff[d];
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
-template <class K>
+template <class K, int RB>
 inline void rs_down_setup() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(k_rs_down<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RsSmem<K>));
+    cudaFuncSetAttribute(k_rs_down<K, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(RsBigSmem<K, RB>));
     done = true;
   }
 }
+// digit width of the large-n path.  10-bit digits save a pass for 25..30-bit
+// keys but their ranking (10 ballots, 4 digits per thread, 72 KB smem) made a
+// pass ~50 % slower on B200 (C5: 3 x 9.7 ms vs 4 x 6.4 ms), so 8 it is.
+inline int rs_big_bits(int) { return 8; }
+
 // ---- single-CTA sort (small n) ----------------------------------------------
 // n <= kSmallSortMax(K): the whole array in shared memory, bitonic network,
 // one launch instead of one per digit pass.  Not stable: callers use it only
