@@ -858,6 +858,113 @@ __device__ void cap_apply(const WalkArgs& a, CapList& L, uint32_t* P, uint32_t* 
   }
   __syncthreads();
 }
+// Fused join: a NEW full-range object := base (t's object with its diagonal
+// [vt] = diag, as materialize() sets it) joined with every captured reference
+// of one target -- one pass over the clock (every source loaded together)
+// instead of materialise + one pass per join + publish.  Returns the object
+// if it differs from the base, else frees it and returns NIL.
+__device__ uint32_t fused_join(const WalkArgs& a, uint32_t base, uint32_t vt, uint32_t diag, const CapList& L,
+                               uint32_t tgt, uint32_t n) {
+  __shared__ uint32_t s_o, s_full, s_ns;
+  __shared__ uint32_t s_src[kMaxCap];
+  if (threadIdx.x == 0) {
+    uint32_t ns = 0, full = (base == NIL || (optr(a.arena, base)[0] == 0 && optr(a.arena, base)[1] == n)) ? 1u : 0u;
+    for (uint32_t k = 0; k < L.n; k++)
+      if (L.tgt[k] == tgt && L.c[k].o != NIL) {
+        const uint32_t o = L.c[k].o;
+        s_src[ns++] = o;
+        if (!(__ldcg(optr(a.arena, o)) == 0 && __ldcg(optr(a.arena, o) + 1) == n)) full = 0;
+      }
+    s_ns = ns;
+    s_full = full;
+    const uint32_t o = arena_alloc(a, n + OBJ_HDR);
+    if (o != NIL) obj_init(a, o, 0, n, 1);
+    s_o = o;
+  }
+  __syncthreads();
+  const uint32_t o = s_o, ns = s_ns;
+  if (o == NIL) return NIL;
+  uint32_t* out = optr(a.arena, o) + OBJ_HDR;
+  int ch = 0;
+  if (s_full) {  // every operand spans [0, n): 16-byte vectors
+    const uint32_t n4 = n >> 2;
+    const uint4* b4 = base != NIL ? reinterpret_cast<const uint4*>(optr(a.arena, base) + OBJ_HDR) : nullptr;
+    for (uint32_t i = threadIdx.x; i < n4; i += kThreads) {
+      const uint4 bv = b4 ? __ldcg(b4 + i) : make_uint4(0, 0, 0, 0);
+      uint4 v = bv;
+      for (uint32_t k = 0; k < ns; k++)
+        v = max4(v, __ldcg(reinterpret_cast<const uint4*>(optr(a.arena, s_src[k]) + OBJ_HDR) + i));
+      reinterpret_cast<uint4*>(out)[i] = v;
+      if (gt4(v, bv)) ch = 1;
+    }
+    for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) {
+      const uint32_t bv = base != NIL ? __ldcg(optr(a.arena, base) + OBJ_HDR + i) : 0u;
+      uint32_t v = bv;
+      for (uint32_t k = 0; k < ns; k++) v = max(v, __ldcg(optr(a.arena, s_src[k]) + OBJ_HDR + i));
+      out[i] = v;
+      if (v > bv) ch = 1;
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+      const uint32_t bv = obj_get_cg(a.arena, base, i);
+      uint32_t v = bv;
+      for (uint32_t k = 0; k < ns; k++) v = max(v, obj_get_cg(a.arena, s_src[k], i));
+      out[i] = v;
+      if (v > bv) ch = 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // the base's diagonal, then the references' explicit entries
+    if (vt != NIL) {
+      const uint32_t bv = obj_get_cg(a.arena, base, vt);
+      uint32_t v = max(out[vt], diag);
+      // materialize() overwrites [vt] with diag; a source may raise it again
+      uint32_t srcmax = 0;
+      for (uint32_t k = 0; k < ns; k++) srcmax = max(srcmax, obj_get_cg(a.arena, s_src[k], vt));
+      v = max(diag, srcmax);
+      out[vt] = v;
+      if (v != bv && v > diag) ch = 1;
+    }
+    for (uint32_t k = 0; k < L.n; k++) {
+      if (L.tgt[k] != tgt || L.c[k].dtid == NIL) continue;
+      const uint32_t v = vidx(a, L.c[k].dtid);
+      if (v == NIL) continue;
+      const uint32_t cur = out[v];
+      const uint32_t bv = v == vt ? diag : cur;
+      if (L.c[k].dval > cur) { out[v] = L.c[k].dval; if (L.c[k].dval > bv) ch = 1; }
+    }
+  }
+  ch = __syncthreads_or(ch);
+  if (!ch) {
+    if (threadIdx.x == 0) obj_release(a, o);  // unchanged: back to the free stack
+    __syncthreads();
+    return NIL;
+  }
+  return o;
+}
+// apply every captured reference to t's pred / hb with fused joins, publish,
+// drop the captured references
+__device__ void cap_flush(const WalkArgs& a, CapList& L, uint32_t t, uint32_t vt, uint32_t n) {
+  if (L.n) {
+    const uint32_t po = fused_join(a, a.pobj[t], vt, a.pdiag[t], L, 0, n);
+    if (po != NIL && threadIdx.x == 0) {
+      set_obj(a, a.pobj, t, po);
+      if (vt != NIL) a.pdiag[t] = optr(a.arena, po)[OBJ_HDR + vt];
+    }
+    __syncthreads();
+    const uint32_t ho = fused_join(a, a.hobj[t], vt, a.local[t], L, 1, n);
+    if (ho != NIL && threadIdx.x == 0) set_obj(a, a.hobj, t, ho);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (uint32_t k = 0; k < L.n; k++) obj_release(a, L.c[k].o);
+    L.n = 0;
+    L.full = 0;
+  }
+  __syncthreads();
+}
+
 // collect a drain's joins (targets pred)
 __device__ __forceinline__ void cap_drain(const WalkArgs& a, CapList& L, const DrainOut& O) {
   if (O.m != NIL) cap_push(a, L, rec_cref(a, O.m), 0);
@@ -898,14 +1005,7 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     if (threadIdx.x == 0) cap_drain(a, s_cap, s_dr);
     __syncthreads();
     if (!s_dr.more) break;
-    if (!mat) { materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]); materialize(H, a.arena, a.hobj[t], n, vt, a.local[t]); mat = true; }
-    cap_apply(a, s_cap, P, H, pch, hch);  // still under the ticket (rare: > kDrainJ non-dominating pops)
-    if (pch) {
-      uint32_t o = publish_dense(a, P, n, 1);
-      if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
-      pch = 0;
-      __syncthreads();
-    }
+    cap_flush(a, s_cap, t, vt, n);  // still under the ticket (rare: > kDrainJ non-dominating pops)
   }
   // (2) the record (acq_clock kept as its epoch (t, local); see the drain-test note) and the frame
   if (threadIdx.x == 0) {
@@ -960,25 +1060,10 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     __syncthreads();
     const bool done = s_done != 0;
     if (done) { tickets_release(a, e); released = true; }
-    if (s_cap.n) {
-      if (!mat) {
-        materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]);
-        materialize(H, a.arena, a.hobj[t], n, vt, a.local[t]);
-        mat = true;
-      }
-      cap_apply(a, s_cap, P, H, pch, hch);
-    }
+    cap_flush(a, s_cap, t, vt, n);
     if (done) break;
   }
   if (!released) tickets_release(a, e);
-  if (pch) {
-    uint32_t o = publish_dense(a, P, n, 1);
-    if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
-  }
-  if (hch) {
-    uint32_t o = publish_dense(a, H, n, 1);
-    if (threadIdx.x == 0) set_obj(a, a.hobj, t, o);
-  }
   __syncthreads();
 }
 
@@ -1050,16 +1135,7 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     first = false;
     if (threadIdx.x == 0) cap_drain(a, s_cap, s_dr);
     __syncthreads();
-    if (s_cap.n) {
-      if (!mat) { materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]); mat = true; }
-      cap_apply(a, s_cap, P, H, pch, hch);
-    }
-    if (pch) {  // the next scan (and P_i below) read t's published pred object
-      uint32_t o = publish_dense(a, P, n, 1);
-      if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
-      pch = 0;
-      __syncthreads();
-    }
+    cap_flush(a, s_cap, t, vt, n);  // the next scan (and P_i below) read t's published pred object
     if (!s_dr.more) break;
   }
   // (2) the frame's instance; dominance test
@@ -1186,17 +1262,10 @@ __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsig
     __syncthreads();
     const bool done = s_done != 0;
     if (done) { tickets_release(a, e); released = true; }
-    if (s_cap.n) {
-      if (!mat) { materialize(P, a.arena, a.pobj[t], n, vt, a.pdiag[t]); mat = true; }
-      cap_apply(a, s_cap, P, nullptr, pch, hch);
-    }
+    cap_flush(a, s_cap, t, vt, n);
     if (done) break;
   }
   if (!released) tickets_release(a, e);
-  if (pch) {
-    uint32_t o = publish_dense(a, P, n, 1);
-    if (threadIdx.x == 0) { set_obj(a, a.pobj, t, o); if (vt != NIL) a.pdiag[t] = P[vt]; }
-  }
   __syncthreads();
   if (threadIdx.x == 0) {
     a.time[e] = a.local[t];
@@ -1232,7 +1301,7 @@ struct ProfT {
   }
 };
 
-__global__ void __launch_bounds__(kThreads) k_walker(WalkArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_walker(WalkArgs a) {
   __shared__ uint32_t s_e[kWalkCH];
   __shared__ uint32_t s_to[kWalkCH];
   __shared__ uint32_t s_hard[kWalkCH + 1];
