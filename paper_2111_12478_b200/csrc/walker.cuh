@@ -429,6 +429,87 @@ __device__ uint32_t publish_dense(const WalkArgs& a, const uint32_t* src, uint32
 // pred objects (each distinct object joined once) with every participant's
 // own entry = its local time; every participant leaves with (PJ, diag=local+1).
 // The same for hb (only when the trace has locks: hb feeds lock state only).
+// Lock mode: the barrier's new clock in one pass -- out[i] = max over the
+// participants' distinct objects (collected first), then the participants'
+// own entries -- written straight into the new full-range object.
+constexpr int kBarSrc = 32;
+__device__ uint32_t barrier_join_lock(const WalkArgs& a, const uint32_t* objs, uint32_t base, uint32_t npool,
+                                      bool warp, uint32_t ins, uint32_t npart, bool& ok) {
+  __shared__ uint32_t s_src[kBarSrc];
+  __shared__ uint32_t s_ns, s_o, s_full;
+  const uint32_t n = vlen(a);
+  if (threadIdx.x == 0) { s_ns = 0; s_full = 1; }
+  __syncthreads();
+  // distinct participant objects (each enumerated once, increasing handles)
+  uint32_t done_lo = 0;
+  while (true) {
+    uint32_t mymin = NIL;
+    for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
+      const bool inm = !warp || ((ins >> j) & 1u);
+      const uint32_t u = base + j;
+      if (inm && !a.exited[u]) {
+        const uint32_t o = objs[u];
+        if (o != NIL && o >= done_lo && o < mymin) mymin = o;
+      }
+    }
+    const uint32_t om = block_min_u32(mymin);
+    if (om == NIL) break;
+    if (threadIdx.x == 0) {
+      if (s_ns < (uint32_t)kBarSrc) {
+        s_src[s_ns++] = om;
+        if (!(__ldcg(optr(a.arena, om)) == 0 && __ldcg(optr(a.arena, om) + 1) == n)) s_full = 0;
+      } else {
+        s_full = 2;  // too many distinct objects: caller falls back
+      }
+    }
+    done_lo = om + 1;
+  }
+  __syncthreads();
+  if (s_full == 2) { ok = false; return NIL; }
+  ok = true;
+  if (threadIdx.x == 0) {
+    const uint32_t o = arena_alloc(a, n + OBJ_HDR);
+    if (o != NIL) obj_init(a, o, 0, n, npart);
+    s_o = o;
+  }
+  __syncthreads();
+  const uint32_t o = s_o, ns = s_ns;
+  if (o == NIL) return NIL;
+  uint32_t* out = optr(a.arena, o) + OBJ_HDR;
+  if (s_full) {
+    const uint32_t n4 = n >> 2;
+    for (uint32_t i = threadIdx.x; i < n4; i += kThreads) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      for (uint32_t k = 0; k < ns; k++)
+        v = max4(v, __ldcg(reinterpret_cast<const uint4*>(optr(a.arena, s_src[k]) + OBJ_HDR) + i));
+      reinterpret_cast<uint4*>(out)[i] = v;
+    }
+    for (uint32_t i = (n4 << 2) + threadIdx.x; i < n; i += kThreads) {
+      uint32_t v = 0;
+      for (uint32_t k = 0; k < ns; k++) v = max(v, __ldcg(optr(a.arena, s_src[k]) + OBJ_HDR + i));
+      out[i] = v;
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < n; i += kThreads) {
+      uint32_t v = 0;
+      for (uint32_t k = 0; k < ns; k++) v = max(v, obj_get_cg(a.arena, s_src[k], i));
+      out[i] = v;
+    }
+  }
+  __syncthreads();
+  // participants' own entries = their local time (C_u[u], hb_u[u])
+  for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
+    const bool inm = !warp || ((ins >> j) & 1u);
+    const uint32_t u = base + j;
+    if (inm && !a.exited[u]) {
+      const uint32_t vu = vidx(a, u);
+      if (vu != NIL) out[vu] = a.local[u];
+    }
+  }
+  __syncthreads();
+  return o;
+}
+
 __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_t* s_acc) {
   const DevTrace& tr = a.tr;
   const uint32_t base = ev_tid(to);  // lane 0 of the warp / block
@@ -458,6 +539,11 @@ __device__ void do_barrier(const WalkArgs& a, uint32_t to, uint32_t ins, uint32_
   uint32_t newobj[2] = {NIL, NIL};
   for (int kind = 0; kind < nkinds; kind++) {
     uint32_t* objs = kind == 0 ? a.pobj : a.hobj;
+    if (a.slot_units) {  // lock mode: one fused pass
+      bool ok = false;
+      const uint32_t no = barrier_join_lock(a, objs, base, npool, warp, ins, npart, ok);
+      if (ok) { newobj[kind] = no; continue; }
+    }
     // hull of participant objects and the block range
     uint32_t mylo = blo, myhi = bhi;
     for (uint32_t j = threadIdx.x; j < npool; j += kThreads) {
