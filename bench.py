@@ -77,6 +77,9 @@ def kernel_alg_bytes(name: str, N: int, n: int) -> int | None:
         ("k_hard_append", 4 * N),
     ]
     base = kernel_base(name)
+    tag = kernel_tag(name)
+    if tag not in (None, "acc"):
+        return None  # kernels of the small auxiliary sorts: no per-unit figure
     for key, b in table:
         if base == key:
             return b
@@ -84,8 +87,12 @@ def kernel_alg_bytes(name: str, N: int, n: int) -> int | None:
 
 
 def kernel_base(name: str) -> str:
-    """'(k_rs_down<K>)' -> 'k_rs_down' (launch expressions as the engine records them)."""
-    return name.strip().strip("()").split("<")[0].strip()
+    """'(k_rs_down<K, RB>)@acc' -> 'k_rs_down' (launch expressions as the engine records them)."""
+    return name.split("@")[0].strip().strip("()").split("<")[0].strip()
+
+
+def kernel_tag(name: str) -> str | None:
+    return name.split("@", 1)[1] if "@" in name else None
 
 
 def load_ncu_traffic():
@@ -475,7 +482,7 @@ def run_b200(args):
     alg_bytes = 16 * n + 36 * n_acc  # 16 B per event + 36 B per access
     step_s = ms_dev / args.steps / 1000.0
     achieved = alg_bytes / step_s / 1e9
-    # dominant kernel (largest device time in the profiled analysis)
+    # dominant kernel (largest device time in the profiled analysis; sort kernels per sort)
     dom = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else None
     dom_line = None
     if dom is not None:
@@ -501,7 +508,7 @@ def run_b200(args):
                               "per launch)" if traffic is not None else None,
         }
     top = sorted(ktimes.items(), key=lambda kv: -kv[1][0])[:10]
-    kernel_ms = {kernel_base(k): round(v[0], 4) for k, v in top}
+    kernel_ms = {(kernel_base(k) + ("@" + kernel_tag(k) if kernel_tag(k) else "")): round(v[0], 4) for k, v in top}
     phases_ms = phase
     line = {
         "metric": METRIC,

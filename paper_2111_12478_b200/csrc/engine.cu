@@ -127,7 +127,7 @@ struct gw_ctx {
       CK(cudaEventCreate(&e));
       prof_ev.push_back(e);
     }
-    prof_recs.assign(cap, LaunchProf::Rec{nullptr, nullptr, nullptr});
+    prof_recs.assign(cap, LaunchProf::Rec{nullptr, nullptr, nullptr, nullptr});
     for (uint32_t i = 0; i < cap; i++) { prof_recs[i].a = prof_ev[2 * i]; prof_recs[i].b = prof_ev[2 * i + 1]; }
     prof.recs = prof_recs.data();
     prof.n = 0;
@@ -258,6 +258,10 @@ struct Pipeline {
   template <class K>
   void sort(K*& keys, uint32_t*& vals, uint64_t n, int nbits, const char* tag, bool distinct = false) {
     if (n <= 1 || nbits <= 0) return;
+    struct Tag {  // profiled analyses time the sort's kernels under its tag
+      explicit Tag(const char* t) { if (g_prof) g_prof->tag = t; }
+      ~Tag() { if (g_prof) g_prof->tag = nullptr; }
+    } tag_guard(tag);
     if (distinct && n <= small_sort_max<K>()) {
       // one CTA, in shared memory (distinct keys: stability is moot)
       uint32_t p2 = 1;
@@ -1429,6 +1433,7 @@ extern "C" int gw_ctx_kernel_times(gw_ctx* c, uint32_t cap, char (*names)[64], f
       float t = 0.f;
       CK(cudaEventElapsedTime(&t, r.a, r.b));
       std::string k(r.name);
+      if (r.tag) { k += "@"; k += r.tag; }
       size_t j = 0;
       while (j < nm.size() && nm[j] != k) j++;
       if (j == nm.size()) { nm.push_back(k); tot.push_back(0.f); cnt.push_back(0); }

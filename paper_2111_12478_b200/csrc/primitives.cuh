@@ -18,12 +18,14 @@ constexpr int kTile = kThreads * kItems;  // 4096
 // With a LaunchProf installed (GW_OPT_PROFILE analyses) every launch is
 // bracketed by CUDA events on its stream -> per-kernel device times.
 struct LaunchProf {
-  struct Rec { const char* name; cudaEvent_t a, b; };
+  struct Rec { const char* name; const char* tag; cudaEvent_t a, b; };
   Rec* recs = nullptr;
   uint32_t n = 0, cap = 0;
+  const char* tag = nullptr;  // current sort / phase tag ("acc", "hd", ...): kernels are timed per tag
   void begin(const char* name, cudaStream_t st) {
     if (n >= cap) return;
     recs[n].name = name;
+    recs[n].tag = tag;
     cudaEventRecord(recs[n].a, st);
   }
   void end(cudaStream_t st) {
@@ -481,7 +483,8 @@ struct RsBigSmem {
 };
 
 template <class K, int RB>
-__global__ void __launch_bounds__(kThreads, 2) k_rs_down(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(kThreads, (RB == 8 && sizeof(K) == 4) ? 3 : 2) k_rs_down(const K* __restrict__ kin,
+                                                                                         const uint32_t* __restrict__ vin,
                                                        K* __restrict__ kout, uint32_t* __restrict__ vout, uint64_t n,
                                                        int shift, const uint32_t* __restrict__ offsets, uint64_t nst) {
   constexpr int ND = RsBig<RB>::ND, DPT = RsBig<RB>::DPT, ST = RsBig<RB>::ST;
