@@ -19,7 +19,7 @@
 //   (event, 1, 1, k)  k-th reader (k = rank of the reader's first read)
 // which reproduces the reference's report sequence exactly.
 #pragma once
-#include "walker.cuh"
+#include "walker_warp.cuh"
 
 namespace gw {
 

@@ -447,7 +447,22 @@ struct Pipeline {
     w.inactive_opt = inactive_opt;
     w.abort_flag = scal + SC_ABORT;
     w.err = scal + SC_ERR;
-    if (G > 1 && !snap_mode && !wsnap_mode) {
+    // lock traces with <= 8 warps of <= 32 lanes: one walker warp per trace warp
+    const char* lwm = getenv("GW_LOCK_WALK");
+    lock_warp = has_locks && tr.W <= kLW && tr.L <= 32 && !(lwm && !strcmp(lwm, "cta"));
+    if (lock_warp) {
+      int occ_lw = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_lw, k_walker_lw, kThreads, 0));
+      G = (uint32_t)std::min<uint64_t>(tr.B, (uint64_t)std::max(occ_lw, 1) * C->num_sms);
+      S.walker_ctas = G;
+      w.G = G;
+      uint32_t* part_key = C->get<uint32_t>("part_k", N);
+      uint32_t* perm = C->get<uint32_t>("part_v", N);
+      GW_LAUNCH(k_part_keys_lw, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
+      sort<uint32_t>(part_key, perm, N, ceil_log2((uint64_t)G * kLW + 1), "part");
+      w.part_key = part_key;
+      w.perm = perm;
+    } else if (G > 1 && !snap_mode && !wsnap_mode) {
       uint32_t* part_key = C->get<uint32_t>("part_k", N);
       uint32_t* perm = C->get<uint32_t>("part_v", N);
       GW_LAUNCH(k_part_keys, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
@@ -553,7 +568,7 @@ struct Pipeline {
   // ---- pipeline state shared by the phases --------------------------------
   uint32_t* scal = nullptr;
   Stats hs{};
-  bool has_locks = false, snap_mode = false, wsnap_mode = false;
+  bool has_locks = false, snap_mode = false, wsnap_mode = false, lock_warp = false;
   uint64_t n_hard_w = 0;
   uint64_t gmax = 1, n_hard = 0, snap_entries = 0, lcap = 1, arena_units = 0;
   uint32_t G = 1, maxd = 1, n_incs = 0;
@@ -931,10 +946,12 @@ struct Pipeline {
       // fixed-size slots; live objects: records (pinned hb clocks), instance
       // and cs clocks, thread states (<= 2 per thread) + per-CTA slack
       w.slot_units = (VL + OBJ_HDR + 15) >> OBJ_USHIFT;
-      w.fcap = 1024;
-      w.fstack = C->get<uint32_t>("f_stack", (uint64_t)G * w.fcap);
-      w.ftop = C->get<uint32_t>("f_top", G);
-      CK(cudaMemsetAsync(w.ftop, 0, sizeof(uint32_t) * G, st));
+      const uint64_t nstk = lock_warp ? (uint64_t)G * kLW : G;
+      w.warp_stacks = lock_warp ? 1u : 0u;
+      w.fcap = lock_warp ? 256 : 1024;
+      w.fstack = C->get<uint32_t>("f_stack", nstk * w.fcap);
+      w.ftop = C->get<uint32_t>("f_top", nstk);
+      CK(cudaMemsetAsync(w.ftop, 0, sizeof(uint32_t) * nstk, st));
       const uint64_t slots = 3 * hs.n_rel + (uint64_t)n_incs * maxd + 2ull * T + 4ull * G + 64;
       size_t free_b = 0, total_b = 0;
       CK(cudaMemGetInfo(&free_b, &total_b));
@@ -1056,6 +1073,8 @@ struct Pipeline {
       stamps.warp_mode = 1;
       stamps.L = tr.L;
       C->stats.walker_ctas = std::min<uint32_t>(tr.B, (uint32_t)gmax);
+    } else if (lock_warp) {
+      launch_lock_warp();
     } else {
       stamps.time = w.time;
       stamps.vobj = w.vobj;
@@ -1080,6 +1099,26 @@ struct Pipeline {
       w.prof = nullptr;
     }
     check_launch();
+  }
+
+  // lock warp walker: block barriers per walker CTA, then the walk
+  void launch_lock_warp() {
+    const uint64_t N = tr.n;
+    const uint64_t nbb = hs.n_bar - hs.n_wbar;
+    uint32_t* bev = C->get<uint32_t>("bb_ev", nbb + 1);
+    uint32_t* bbeg = C->get<uint32_t>("bb_beg", G);
+    uint32_t* bend = C->get<uint32_t>("bb_end", G);
+    uint32_t* bcnt = C->get<uint32_t>("bb_cnt", G);
+    CK(cudaMemsetAsync(bcnt, 0, sizeof(uint32_t) * G, st));
+    if (nbb) {
+      unsigned long long* bkey = C->get<unsigned long long>("bb_key", nbb + 1);
+      uint32_t* bdummy = C->get<uint32_t>("bb_v", nbb + 1);
+      GW_LAUNCH(k_bbar_append, grid_for(N), kThreads, 0, st, tr, G, bkey, bcnt, zeroed(1));
+      sort<unsigned long long>(bkey, bdummy, nbb, 32 + ceil_log2(G), "bb", true);
+      GW_LAUNCH(k_hard_unpack, grid_for(nbb), kThreads, 0, st, bkey, nbb, bev);
+    }
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{bcnt}, HardSegStore{bcnt, bbeg, bend}, G, OpSum(), 0u, false, "sc_u32");
+    GW_LAUNCH(k_walker_lw, G, kThreads, 0, st, w, bev, bbeg, bend);
   }
 };
 

@@ -107,6 +107,7 @@ struct WalkArgs {
   uint32_t* fstack;
   uint32_t* ftop;
   uint32_t fcap;
+  uint32_t warp_stacks;  // free stacks per (CTA, warp) (k_walker_lw) instead of per CTA
   // lock mode: race-check queries answered in trace order by the walker
   const uint32_t* q_cur;    // query current events, sorted
   const uint32_t* q_idx;    // candidate index of each sorted query
@@ -186,14 +187,18 @@ __device__ __forceinline__ void vblock(const WalkArgs& a, uint32_t b, uint32_t& 
 // created, referenced and freed by one walker CTA only (the one owning the
 // threads that hold them; records pin theirs forever), so the stacks are
 // CTA-private.  Lock-free traces: bump allocation, never freed.
+__device__ __forceinline__ uint32_t stack_id(const WalkArgs& a) {
+  return a.warp_stacks ? blockIdx.x * 8u + (threadIdx.x >> 5) : blockIdx.x;
+}
 __device__ __forceinline__ uint32_t arena_alloc(const WalkArgs& a, uint32_t words) {
   unsigned long long units;
   if (a.slot_units) {
-    uint32_t n = a.ftop[blockIdx.x];
+    const uint32_t sid = stack_id(a);
+    uint32_t n = a.ftop[sid];
     if (n > a.fcap) n = a.fcap;  // pushes past the capacity were dropped (leaked)
     if (n > 0) {
-      a.ftop[blockIdx.x] = n - 1;
-      return a.fstack[(size_t)blockIdx.x * a.fcap + n - 1];
+      a.ftop[sid] = n - 1;
+      return a.fstack[(size_t)sid * a.fcap + n - 1];
     }
     units = a.slot_units;
   } else {
@@ -210,8 +215,9 @@ __device__ __forceinline__ void obj_retain(const WalkArgs& a, uint32_t o, uint32
 __device__ __forceinline__ void obj_release(const WalkArgs& a, uint32_t o) {
   if (!a.slot_units || o == NIL) return;
   if (atomicSub(optr(a.arena, o) + 2, 1u) == 1u) {
-    const uint32_t i = atomicAdd(a.ftop + blockIdx.x, 1u);
-    if (i < a.fcap) a.fstack[(size_t)blockIdx.x * a.fcap + i] = o;
+    const uint32_t sid = stack_id(a);
+    const uint32_t i = atomicAdd(a.ftop + sid, 1u);
+    if (i < a.fcap) a.fstack[(size_t)sid * a.fcap + i] = o;
   }
 }
 // initialise a new object's header

@@ -320,3 +320,20 @@ def test_lock_free_sync_pass_modes(ctx, mode, goldens, monkeypatch):
         check_against_golden(r, tr, _run(ctx, tr, r["inactive_opt"]))
         n += 1
     assert n > 0
+
+
+@pytest.mark.parametrize("mode", ["warp", "cta"])
+def test_lock_walker_modes(ctx, mode, goldens, monkeypatch):
+    """Both lock-mode sync passes (one walker warp per trace warp, and the
+    CTA-wide walker used for > 8 warps or > 32 lanes) match the reference."""
+    monkeypatch.setenv("GW_LOCK_WALK", mode)
+    n = 0
+    for r in goldens:
+        if "error" in r or "full" in r["tags"] or not ({"corpus", "nasty", "random", "c3"} & set(r["tags"])):
+            continue
+        tr = parse_trace(golden_text(r))
+        check_against_golden(r, tr, _run(ctx, tr, r["inactive_opt"]))
+        n += 1
+    assert n > 0
+    tr = parse_trace(WL.c3_text(blocks=20, warps=6, lanes=32, iters=24, locks=12, region=8, private=64, seed=77))
+    assert ndjson_lines(tr, _run(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
