@@ -1118,7 +1118,25 @@ struct Pipeline {
       GW_LAUNCH(k_hard_unpack, grid_for(nbb), kThreads, 0, st, bkey, nbb, bev);
     }
     scan<uint32_t, OpSum>(ArrLoad<uint32_t>{bcnt}, HardSegStore{bcnt, bbeg, bend}, G, OpSum(), 0u, false, "sc_u32");
+    const bool prof = getenv("GW_PROF_WALKER") != nullptr;
+    const uint64_t nw = (uint64_t)G * kLW;
+    if (prof) {
+      w.prof = C->get<unsigned long long>("prof", nw * 8);
+      CK(cudaMemsetAsync(w.prof, 0, sizeof(unsigned long long) * nw * 8, st));
+    }
     GW_LAUNCH(k_walker_lw, G, kThreads, 0, st, w, bev, bbeg, bend);
+    if (prof) {
+      std::vector<unsigned long long> hp(nw * 8);
+      d2h(hp.data(), w.prof, hp.size());
+      double sum[8] = {0}, mx[8] = {0};
+      for (uint64_t x = 0; x < nw; x++)
+        for (int k = 0; k < 8; k++) { sum[k] += hp[x * 8 + k]; mx[k] = std::max(mx[k], (double)hp[x * 8 + k]); }
+      const char* nm[7] = {"stamp", "warpbar", "blockbar", "ticket", "acquire", "release", "incs"};
+      fprintf(stderr, "[gw] lock warp walker G=%u Q=%u per-warp avg / max ms:", G, w.Q);
+      for (int k = 0; k < 7; k++) fprintf(stderr, " %s %.2f/%.2f", nm[k], sum[k] / nw / 1e6, mx[k] / 1e6);
+      fprintf(stderr, "; lock events %.0f\n", sum[7]);
+      w.prof = nullptr;
+    }
   }
 };
 

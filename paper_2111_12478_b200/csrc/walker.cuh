@@ -934,22 +934,6 @@ __device__ int join_cref(const WalkArgs& a, uint32_t* dst, CRef c) {
   }
   return __syncthreads_or(ch);
 }
-// apply and drop the captured references; pch / hch accumulate "grew"
-__device__ void cap_apply(const WalkArgs& a, CapList& L, uint32_t* P, uint32_t* H, int& pch, int& hch) {
-  const uint32_t n = L.n;
-  for (uint32_t k = 0; k < n; k++) {
-    const CRef c = L.c[k];
-    if (L.tgt[k] == 0) pch |= join_cref(a, P, c);
-    else hch |= join_cref(a, H, c);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (uint32_t k = 0; k < n; k++) obj_release(a, L.c[k].o);
-    L.n = 0;
-    L.full = 0;
-  }
-  __syncthreads();
-}
 // Fused join: a NEW full-range object := base (t's object with its diagonal
 // [vt] = diag, as materialize() sets it) joined with every captured reference
 // of one target -- one pass over the clock (every source loaded together)
@@ -959,6 +943,11 @@ __device__ uint32_t fused_join(const WalkArgs& a, uint32_t base, uint32_t vt, ui
                                uint32_t tgt, uint32_t n) {
   __shared__ uint32_t s_o, s_full, s_ns;
   __shared__ uint32_t s_src[kMaxCap];
+  {  // nothing captured for this target: unchanged, no pass over the clock
+    bool any = false;
+    for (uint32_t k = 0; k < L.n && !any; k++) any = L.tgt[k] == tgt;
+    if (!any) return NIL;
+  }
   if (threadIdx.x == 0) {
     uint32_t ns = 0, full = (base == NIL || (optr(a.arena, base)[0] == 0 && optr(a.arena, base)[1] == n)) ? 1u : 0u;
     for (uint32_t k = 0; k < L.n; k++)
@@ -1632,23 +1621,6 @@ __global__ void __launch_bounds__(kThreads) k_walker_wsnap(WalkArgs a, SnapArgs 
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_stamp(WalkArgs a, SnapArgs s) {
-  const DevTrace& tr = a.tr;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t to = __ldg(tr.tidop + e);
-    if (ev_kind(to) > GW_K_WRITE) continue;
-    const uint32_t t = ev_tid(to), b = t / tr.BS;
-    uint32_t lo = __ldg(s.hb_beg + b), hi = __ldg(s.hb_end + b);
-    const uint32_t base = lo;
-    while (lo < hi) {  // #hard events of block b before e
-      const uint32_t m = (lo + hi) >> 1;
-      if (__ldg(s.hard_ev + m) < (uint32_t)e) lo = m + 1; else hi = m;
-    }
-    const uint2 st = s.snap[(size_t)(base + b + (lo - base)) * tr.BS + (t - b * tr.BS)];
-    a.time[e] = st.x;
-    a.vobj[e] = st.y;
-  }
-}
 
 // hard events (barriers, ENDs) of a lock-free trace: appended in any order as
 // (block << 32 | event) keys with warp-aggregated atomics, then sorted, which
@@ -1657,13 +1629,30 @@ __global__ void __launch_bounds__(kThreads) k_stamp(WalkArgs a, SnapArgs s) {
 __global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
                                 const uint32_t* abort_flag) {
   if (*(volatile const uint32_t*)abort_flag) return;
-  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t to = tr.tidop[e];
-    const uint32_t k = ev_kind(to);
-    if (k != GW_K_BARRIER && k != GW_K_END) continue;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < tr.n;
+       e0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = e0 + lane;
+    uint32_t to = 0, k = 7;
+    if (e < tr.n) { to = tr.tidop[e]; k = ev_kind(to); }
+    const bool bbar = k == GW_K_BARRIER && !(to & GW_F_WARPBAR);
+    const bool hard = k == GW_K_BARRIER || k == GW_K_END;
+    const uint32_t cnt = hard ? (bbar ? kWSnapWarps : 1u) : 0u;
+    // warp-aggregated slot reservation
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (!tot) continue;
+    uint32_t base = 0;
+    if (lane == 31) base = atomicAdd(ntop, tot);
+    base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+    if (!hard) continue;
     const uint32_t t = ev_tid(to), b = t / tr.BS;
-    if (k == GW_K_BARRIER && !(to & GW_F_WARPBAR)) {
-      const uint32_t base = atomicAdd(ntop, kWSnapWarps);
+    if (bbar) {
       for (uint32_t j = 0; j < kWSnapWarps; j++) {
         const uint32_t g = b * kWSnapWarps + j;
         hkey[base + j] = ((unsigned long long)g << 32) | (uint32_t)e;
@@ -1671,7 +1660,7 @@ __global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t*
       }
     } else {
       const uint32_t g = b * kWSnapWarps + (t % tr.BS) / tr.L;
-      hkey[atomicAdd(ntop, 1u)] = ((unsigned long long)g << 32) | (uint32_t)e;
+      hkey[base] = ((unsigned long long)g << 32) | (uint32_t)e;
       atomicAdd(hcnt + g, 1u);
     }
   }

@@ -175,6 +175,11 @@ __device__ uint32_t w_fused_join(const WalkArgs& a, uint32_t base, uint32_t vt, 
                                  uint32_t n) {
   const uint32_t lane = lane_id();
   const CapList& L = S.cap;
+  {  // nothing captured for this target: unchanged, no pass over the clock
+    bool any = false;
+    for (uint32_t k = 0; k < L.n && !any; k++) any = L.tgt[k] == tgt;
+    if (!any) return NIL;
+  }
   if (lane == 0) {
     uint32_t ns = 0, full = (base == NIL || (optr(a.arena, base)[0] == 0 && optr(a.arena, base)[1] == n)) ? 1u : 0u;
     for (uint32_t k = 0; k < L.n; k++)
@@ -660,6 +665,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_walker_lw(WalkArgs a, const uin
   uint32_t q = bb_beg[blockIdx.x];
   const uint32_t qend = bb_end[blockIdx.x];
   uint64_t p = beg;
+  // optional time split (GW_PROF_WALKER): per walker warp, slots 0 stamp, 1 warp barrier,
+  // 2 block barrier, 3 ticket wait, 4 acquire, 5 release, 6 in-CS access, 7 lock events
+  unsigned long long* prof = a.prof ? a.prof + ((size_t)blockIdx.x * kLW + j) * 8 : nullptr;
+  unsigned long long tp = prof && lane == 0 ? gtime() : 0ull;
+  auto lap = [&](int slot) {
+    if (prof && lane == 0) { const unsigned long long n = gtime(); prof[slot] += n - tp; tp = n; }
+  };
   while (true) {
     const uint32_t ebb = q < qend ? bb_ev[q] : NIL;
     // own events before the next block barrier, 32 at a time
@@ -688,6 +700,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_walker_lw(WalkArgs a, const uin
           if (a.lflags[ev] & LF_QUERY) answer_queries(a, ev, a.pobj[t]);
         }
         __syncwarp();
+        lap(0);
         if (h >= c) break;
         hm &= hm - 1;
         const uint32_t e = __shfl_sync(0xffffffffu, ev, h);
@@ -695,6 +708,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_walker_lw(WalkArgs a, const uin
         const uint32_t k = ev_kind(te);
         if (k == GW_K_BARRIER) {  // warp barrier (block barriers come from the other list)
           w_barrier_warp(a, te, tr.instr[e], S);
+          lap(1);
         } else if (k == GW_K_END) {
           if (lane == 0) {
             const uint32_t t = ev_tid(te);
@@ -713,12 +727,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_walker_lw(WalkArgs a, const uin
             __syncwarp();
           } else {
             w_tickets_wait(a, e);
+            lap(3);
             if (k == GW_K_ACQUIRE) w_acquire(a, e, te, lock, S);
             else w_release(a, e, te, lock, S);
+            lap(k == GW_K_ACQUIRE ? 4 : 5);
+            if (prof && lane == 0) prof[7]++;
           }
         } else {  // in-CS access
           w_tickets_wait(a, e);
+          lap(3);
           w_incs_access(a, e, te, tr.key[e], S);
+          lap(6);
+          if (prof && lane == 0) prof[7]++;
         }
         start = h + 1;
       }
@@ -729,6 +749,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_walker_lw(WalkArgs a, const uin
     // block barrier: every warp of the CTA arrives here (each walks the same list)
     __syncthreads();
     do_barrier(a, tr.tidop[ebb], 0u, s_acc);
+    lap(2);
     q++;
   }
   __syncthreads();
