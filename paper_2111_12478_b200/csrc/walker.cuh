@@ -1637,6 +1637,7 @@ __global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t*
     if (e < tr.n) { to = tr.tidop[e]; k = ev_kind(to); }
     const bool bbar = k == GW_K_BARRIER && !(to & GW_F_WARPBAR);
     const bool hard = k == GW_K_BARRIER || k == GW_K_END;
+    if (!__any_sync(0xffffffffu, hard)) continue;
     const uint32_t cnt = hard ? (bbar ? kWSnapWarps : 1u) : 0u;
     // warp-aggregated slot reservation
     uint32_t incl = cnt;
