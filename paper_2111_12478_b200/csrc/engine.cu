@@ -297,6 +297,7 @@ struct Pipeline {
     const uint64_t nst = (lb_tiles(n) + RsBig<RB>::ST - 1) / RsBig<RB>::ST;
     uint32_t* counts = C->get<uint32_t>("rs_counts", nst * RsBig<RB>::ND);
     rs_down_setup<K, RB>();
+    rs_down_tma_setup<K>();
     const unsigned g = (unsigned)std::min<uint64_t>(nst, 148ull * 16);
     bool alt = false;
     for (int p = 0; p < npass; p++) {
@@ -307,8 +308,12 @@ struct Pipeline {
       GW_LAUNCH((k_rs_up<K, RB>), g, kThreads, 0, st, ki, n, RB * p, counts, nst);
       scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nst * RsBig<RB>::ND, OpSum(), 0u,
                             false, "sc_u32");
-      GW_LAUNCH((k_rs_down<K, RB>), g, kThreads, sizeof(RsBigSmem<K, RB>), st, ki, vi, ko, vo, n, RB * p, counts,
-                nst);
+      if constexpr (RB == 8) {  // ST == 1: TMA-streamed input tiles
+        GW_LAUNCH((k_rs_down_tma<K>), g, kThreads, sizeof(RsTmaSmem<K>), st, ki, vi, ko, vo, n, RB * p, counts, nst);
+      } else {
+        GW_LAUNCH((k_rs_down<K, RB>), g, kThreads, sizeof(RsBigSmem<K, RB>), st, ki, vi, ko, vo, n, RB * p, counts,
+                  nst);
+      }
       alt = !alt;
     }
     if (alt) {

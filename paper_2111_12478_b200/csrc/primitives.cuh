@@ -583,6 +583,160 @@ __global__ void __launch_bounds__(kThreads, (RB == 8 && sizeof(K) == 4) ? 3 : 2)
     }
   }
 }
+// ---- TMA bulk copies (cp.async.bulk) with mbarrier completion --------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* m, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* m, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(m)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+
+// k_rs_down with its input tiles streamed by TMA bulk copies into a double
+// buffer (the next tile lands while this one is ranked); the input buffer is
+// then reused as the digit-order staging buffer of the scatter.
+template <class K>
+struct RsTmaSmem {
+  K ik[2][kTile];             // input keys (TMA) -> staged keys
+  uint32_t iv[2][kTile];      // input values (TMA) -> staged values
+  uint32_t wc[kRsWarps][kRsDigits];
+  uint32_t toff[kRsDigits];
+  uint32_t gbase[kRsDigits];
+  unsigned long long mbar[2];
+};
+template <class K>
+__global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tma(const K* __restrict__ kin,
+                                                                            const uint32_t* __restrict__ vin,
+                                                                            K* __restrict__ kout,
+                                                                            uint32_t* __restrict__ vout, uint64_t n,
+                                                                            int shift,
+                                                                            const uint32_t* __restrict__ offsets,
+                                                                            uint64_t nst) {
+  constexpr int ND = kRsDigits;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  RsTmaSmem<K>& S = *reinterpret_cast<RsTmaSmem<K>*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  auto full_tile = [&](uint64_t st) { return (st + 1) * kTile <= n; };
+  auto issue = [&](uint64_t st, int b) {  // thread 0
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic accesses to buffer b
+    mbar_expect_tx(&S.mbar[b], (uint32_t)(kTile * (sizeof(K) + 4)));
+    bulk_g2s(S.ik[b], kin + st * kTile, (uint32_t)(kTile * sizeof(K)), &S.mbar[b]);
+    bulk_g2s(S.iv[b], vin + st * kTile, (uint32_t)(kTile * 4), &S.mbar[b]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&S.mbar[0], 1);
+    mbar_init(&S.mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t uses[2] = {0, 0};
+  uint64_t st = blockIdx.x;
+  if (st < nst && threadIdx.x == 0 && full_tile(st)) issue(st, 0);
+  for (int it = 0; st < nst; st += gridDim.x, it++) {
+    const int b = it & 1;
+    const uint64_t nx = st + gridDim.x;
+    if (threadIdx.x == 0 && nx < nst && full_tile(nx)) issue(nx, b ^ 1);
+    const uint64_t tbase = st * kTile;
+    const bool full = full_tile(st);
+    S.gbase[threadIdx.x] = offsets[(uint64_t)threadIdx.x * nst + st];
+    for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
+    K kk[kRsRounds];
+    uint32_t vv[kRsRounds];
+    uint32_t rd[kRsRounds];
+    if (full) {
+      while (!mbar_try_wait(&S.mbar[b], uses[b] & 1u)) {
+      }
+      uses[b]++;
+#pragma unroll
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint32_t j = w * kRsPerWarp + r * 32 + lane;
+        kk[r] = S.ik[b][j];
+        vv[r] = S.iv[b][j];
+        rd[r] = ((uint32_t)(kk[r] >> shift) & (ND - 1)) << 16;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint64_t i = tbase + (uint64_t)w * kRsPerWarp + (uint64_t)r * 32 + lane;
+        const bool ok = i < n;
+        kk[r] = ok ? kin[i] : (K)0;
+        vv[r] = ok ? vin[i] : 0u;
+        rd[r] = ok ? (((uint32_t)(kk[r] >> shift) & (ND - 1)) << 16) : ((uint32_t)ND << 16);
+      }
+    }
+    __syncthreads();  // wc zeroed; every thread has its inputs in registers
+#pragma unroll
+    for (int r = 0; r < kRsRounds; r++) {
+      const uint32_t d = rd[r] >> 16;
+      const uint32_t peers = full ? warp_peers<kRsBits>(d) : warp_peers<kRsBits + 1>(d);
+      const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
+      __syncwarp();
+      if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+      rd[r] |= before + __popc(peers & lt);
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      const int d = threadIdx.x;
+      uint32_t run = 0;
+#pragma unroll
+      for (int ww = 0; ww < kRsWarps; ww++) {
+        const uint32_t t = S.wc[ww][d];
+        S.wc[ww][d] = run;
+        run += t;
+      }
+      uint32_t ct;
+      S.toff[d] = block_excl_scan<uint32_t, OpSum>(run, OpSum(), 0u, &ct);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRsRounds; r++) {
+      const uint32_t d = rd[r] >> 16;
+      if (d < (uint32_t)ND) {
+        const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
+        S.ik[b][pos] = kk[r];
+        S.iv[b][pos] = vv[r];
+      }
+    }
+    __syncthreads();
+    const uint64_t rem = n - tbase;
+    const uint32_t cnt = rem < (uint64_t)kTile ? (uint32_t)rem : (uint32_t)kTile;
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+      const K k = S.ik[b][i];
+      const uint32_t d = (uint32_t)(k >> shift) & (ND - 1);
+      const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
+      kout[gp] = k;
+      vout[gp] = S.iv[b][i];
+    }
+    __syncthreads();  // buffer b free for the TMA of tile it + 2
+  }
+}
+template <class K>
+inline void rs_down_tma_setup() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_rs_down_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RsTmaSmem<K>));
+    done = true;
+  }
+}
+
 template <class K, int RB>
 inline void rs_down_setup() {
   static bool done = false;
