@@ -187,27 +187,50 @@ __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
   unsigned long long v[6] = {0, 0, 0, 0, 0, 0};  // acc, write, acq, rel, end, bar
   unsigned long long ko = 0, ka = ~0ull, nlong = 0, nwbar = 0;
   const int lane = threadIdx.x & 31;
-  for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < tr.n;
-       e0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = e0 + lane;  // warp = one aligned 32-event window
-    const uint32_t to = e < tr.n ? tr.tidop[e] : 0u;
-    const uint32_t k = e < tr.n ? ev_kind(to) : 7u;
-    if (k <= GW_K_WRITE) {
-      const unsigned long long x = tr.key[e];
-      v[0]++; v[1] += k; ko |= x; ka &= x;
-    } else if (k == GW_K_ACQUIRE) v[2]++;
-    else if (k == GW_K_RELEASE) v[3]++;
-    else if (k == GW_K_END) v[4]++;
-    else if (k == GW_K_BARRIER) { v[5]++; if (to & GW_F_WARPBAR) nwbar++; }
-    // records longer than 32 events: 32 consecutive continues-record events ending in this window
-    const uint32_t cur = __ballot_sync(0xffffffffu, (to & GW_F_CONT) != 0);
-    if (cur == 0xffffffffu) {
-      if (lane == 0) nlong++;  // a whole window of continuations: the record has > 32 events
-    } else if (cur & 1u) {    // a run entering the window: add the previous window's trailing run
-      const uint32_t prev = __ballot_sync(0xffffffffu, e0 >= 32 && (tr.tidop[e - 32] & GW_F_CONT));
-      unsigned long long y = ((unsigned long long)cur << 32) | prev;
-      y &= y >> 1; y &= y >> 2; y &= y >> 4; y &= y >> 8; y &= y >> 16;  // bit i: bits i..i+31 all set
-      if (lane == 0 && ((y >> 1) & 0xFFFFFFFFull)) nlong++;
+  constexpr int U = 4;  // aligned 32-event windows per warp iteration: all loads issued first
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * U;
+  for (uint64_t b0 = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; b0 < tr.n; b0 += stride) {
+    uint32_t to[U];
+    unsigned long long x[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t e = b0 + 32 * u + lane;
+      to[u] = e < tr.n ? tr.tidop[e] : (7u << GW_OP_SHIFT);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t e = b0 + 32 * u + lane;
+      x[u] = ev_kind(to[u]) <= GW_K_WRITE ? tr.key[e] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t k = ev_kind(to[u]);
+      if (k <= GW_K_WRITE) { v[0]++; v[1] += k; ko |= x[u]; ka &= x[u]; }
+      else if (k == GW_K_ACQUIRE) v[2]++;
+      else if (k == GW_K_RELEASE) v[3]++;
+      else if (k == GW_K_END) v[4]++;
+      else if (k == GW_K_BARRIER) { v[5]++; if (to[u] & GW_F_WARPBAR) nwbar++; }
+    }
+    // records longer than 32 events: 32 consecutive continues-record events ending in a window
+    uint32_t prevm = 0;
+    bool have_prev = false;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t w0 = b0 + 32 * u;
+      if (w0 >= tr.n) break;
+      const uint32_t cur = __ballot_sync(0xffffffffu, (to[u] & GW_F_CONT) != 0 && ev_kind(to[u]) != 7u);
+      if (cur == 0xffffffffu) {
+        if (lane == 0) nlong++;  // a whole window of continuations: the record has > 32 events
+      } else if (cur & 1u) {    // a run entering the window: add the previous window's trailing run
+        uint32_t prev = prevm;
+        if (!have_prev)
+          prev = __ballot_sync(0xffffffffu, w0 >= 32 && (tr.tidop[w0 - 32 + lane] & GW_F_CONT));
+        unsigned long long y = ((unsigned long long)cur << 32) | prev;
+        y &= y >> 1; y &= y >> 2; y &= y >> 4; y &= y >> 8; y &= y >> 16;  // bit i: bits i..i+31 all set
+        if (lane == 0 && ((y >> 1) & 0xFFFFFFFFull)) nlong++;
+      }
+      prevm = cur;
+      have_prev = true;
     }
   }
   if (lane == 0 && nlong) atomicAdd(&st->n_long, nlong);
