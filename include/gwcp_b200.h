@@ -90,6 +90,7 @@ typedef struct gw_trace_view { /* caller-owned SoA; host or device pointers */
 
 #define GW_OPT_EAGER 1u   /* never capture / replay a CUDA graph for this analysis */
 #define GW_OPT_PROFILE 2u /* eager, with CUDA events around every launch (gw_ctx_kernel_times) */
+#define GW_OPT_HB 4u      /* scoped happens-before detector (gpurace check --detector hb, hb.py) */
 
 typedef struct gw_opts {
   uint32_t inactive_opt; /* GwcpDetector(inactive_opt=...), gwcp.py:108-127 */

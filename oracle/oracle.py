@@ -47,7 +47,7 @@ def lib():
     return _lib
 
 
-def run_soa(cfg, key, tidop, instr, inactive_opt=True) -> dict:
+def run_soa(cfg, key, tidop, instr, inactive_opt=True, hb=False) -> dict:
     """Reference-equivalent result arrays for an SoA trace (same dict layout
     as paper_2111_12478_b200._native.analyze)."""
     L = lib()
@@ -57,7 +57,7 @@ def run_soa(cfg, key, tidop, instr, inactive_opt=True) -> dict:
     r = _Res()
     n = len(tidop)
     rc = L.gwo_run(cfg[0], cfg[1], cfg[2], n, key.ctypes.data if n else None, tidop.ctypes.data if n else None,
-                   instr.ctypes.data if n else None, 1 if inactive_opt else 0, C.byref(r))
+                   instr.ctypes.data if n else None, (1 if inactive_opt else 0) | (2 if hb else 0), C.byref(r))
     if rc:
         raise RuntimeError(f"oracle failed ({rc})")
     try:
@@ -77,5 +77,6 @@ def run_soa(cfg, key, tidop, instr, inactive_opt=True) -> dict:
         L.gwo_free(C.byref(r))
 
 
-def run_trace(tr, inactive_opt=True) -> dict:
-    return run_soa(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt)
+def run_trace(tr, inactive_opt=True, hb=False) -> dict:
+    """hb=True: the scoped happens-before detector (hb.py)."""
+    return run_soa(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt, hb)

@@ -12,6 +12,7 @@ include/gwcp_b200.h (libgwcp_b200.so); there is no CPU path.
 
 from .engine import RunResult, run
 from .gwcp import GwcpDetector
+from .hb import HbDetector
 from .report import Endpoint, RaceReport
 from .trace import (
     Barrier,
@@ -37,6 +38,7 @@ __all__ = [
     "Endpoint",
     "Event",
     "GwcpDetector",
+    "HbDetector",
     "Location",
     "RaceReport",
     "RunResult",

@@ -28,6 +28,7 @@ F_CONT = 1 << 30
 SHARED_BIT = 1 << 63
 OPT_EAGER = 1
 OPT_PROFILE = 2
+OPT_HB = 4  # scoped happens-before detector (hb.py)
 
 
 class NativeUnavailable(RuntimeError):
@@ -292,20 +293,22 @@ class Context:
             pass
 
     def analyze_host(self, cfg, key, tidop, instr, *, inactive_opt=True, stream=None, eager=False,
-                     shard=(0, 1)) -> None:
+                     shard=(0, 1), hb=False) -> None:
+        """hb=True: the scoped happens-before detector (gpurace --detector hb)."""
         v = _view(cfg, key, tidop, instr)
-        o = _Opts(1 if inactive_opt else 0, OPT_EAGER if eager else 0, stream, shard[0], shard[1])
+        flags = (OPT_EAGER if eager else 0) | (OPT_HB if hb else 0)
+        o = _Opts(1 if inactive_opt else 0, flags, stream, shard[0], shard[1])
         _check(self._L.gw_ctx_analyze_host(self._c, C.byref(v), C.byref(o)))
 
     def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None,
-                       eager=False, shard=(0, 1), profile=False) -> None:
+                       eager=False, shard=(0, 1), profile=False, hb=False) -> None:
         """shard=(index, count): report only races on location-key range `index`
         of `count` (address sharding; see include/gwcp_b200.h gw_opts)."""
         v = _View()
         v.cfg.blocks, v.cfg.warps, v.cfg.lanes = cfg
         v.n_events = n
         v.key, v.tidop, v.instr = key_ptr, tidop_ptr, instr_ptr
-        flags = (OPT_EAGER if eager else 0) | (OPT_PROFILE if profile else 0)
+        flags = (OPT_EAGER if eager else 0) | (OPT_PROFILE if profile else 0) | (OPT_HB if hb else 0)
         o = _Opts(1 if inactive_opt else 0, flags, stream, shard[0], shard[1])
         _check(self._L.gw_ctx_analyze_device(self._c, C.byref(v), C.byref(o)))
 
@@ -343,10 +346,10 @@ def default_context() -> Context:
     return _default_ctx
 
 
-def analyze(cfg, key, tidop, instr, *, inactive_opt=True):
+def analyze(cfg, key, tidop, instr, *, inactive_opt=True, hb=False):
     """Host SoA in -> report / diagnostic arrays out (GPU; no CPU path)."""
     ctx = default_context()
-    ctx.analyze_host(cfg, key, tidop, instr, inactive_opt=inactive_opt)
+    ctx.analyze_host(cfg, key, tidop, instr, inactive_opt=inactive_opt, hb=hb)
     return ctx.fetch()
 
 

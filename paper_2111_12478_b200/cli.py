@@ -46,13 +46,14 @@ def _load(path: str):
 
 
 def _cmd_check(args) -> int:
-    if args.detector != "gwcp":
+    if args.detector not in ("gwcp", "hb"):
         _die(EXIT_USAGE, f"detector {args.detector!r} is not on the accelerated path (use gpurace)")
     if args.infer_locks or args.order_matrix:
         _die(EXIT_USAGE, "--infer-locks / --order-matrix are not on the accelerated path (use gpurace)")
     tr = _load(args.trace)
-    res = N.analyze(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt=not args.no_inactive_opt)
-    out = ndjson_lines(tr, res)
+    res = N.analyze(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt=not args.no_inactive_opt,
+                    hb=args.detector == "hb")
+    out = ndjson_lines(tr, res, args.detector)
     if out:
         sys.stdout.write("\n".join(out) + "\n")
     for d in diagnostics_of(tr, res):

@@ -114,6 +114,7 @@ struct gw_ctx {
   DevTrace last_tr{};
   uint32_t last_inactive = 1;
   uint32_t last_shard = 0, last_nshard = 1;
+  bool last_hb = false;
   bool last_graph = false;
   Plan plan;
   LaunchProf prof;           // GW_OPT_PROFILE: per-launch events of the last analysis
@@ -452,6 +453,7 @@ struct Pipeline {
     w.inactive_opt = inactive_opt;
     w.abort_flag = scal + SC_ABORT;
     w.err = scal + SC_ERR;
+    w.hb_mode = hb_mode ? 1u : 0u;
     // lock traces with <= 8 warps of <= 32 lanes: one walker warp per trace warp
     const char* lwm = getenv("GW_LOCK_WALK");
     lock_warp = has_locks && tr.W <= kLW && tr.L <= 32 && !(lwm && !strcmp(lwm, "cta"));
@@ -611,6 +613,7 @@ struct Pipeline {
   uint4* aux = nullptr;       // per event (tidop, time, vobj)
   uint64_t obs_nq = 0;
   uint32_t shard = 0, nshard = 1;  // address sharding (gw_opts)
+  bool hb_mode = false;            // GW_OPT_HB: scoped happens-before detector
   uint64_t na_sorted = 0;          // positions the access pass sorts (N, or this shard's accesses)
   ShardArgs shard_args() const {
     ShardArgs sa;
@@ -898,7 +901,7 @@ struct Pipeline {
     uint32_t* qflag = C->get<uint32_t>("q_flag", (uint64_t)T + 1);
     uint32_t* qoff = C->get<uint32_t>("q_off", (uint64_t)T + 1);
     CK(cudaMemsetAsync(qflag, 0, sizeof(uint32_t) * ((uint64_t)T + 1), st));
-    GW_LAUNCH(k_q_mark_acq, grid_for(N), kThreads, 0, st, tr, w.lflags, qflag);
+    if (!hb_mode) GW_LAUNCH(k_q_mark_acq, grid_for(N), kThreads, 0, st, tr, w.lflags, qflag);  // drain-test owners
     uint32_t* qk = C->get<uint32_t>("q_sk", nq + 1);
     uint32_t* qi = C->get<uint32_t>("q_sv", nq + 1);
     if (nq) GW_LAUNCH(k_q_mark_cands, grid_for(nq), kThreads, 0, st, cq, tr.tidop, qflag, (uint8_t*)w.lflags, qk, qi);
@@ -1213,8 +1216,10 @@ extern "C" void gw_ctx_destroy(gw_ctx* c) {
 // the Plan and capture the graph-mode pipeline for later replays.
 static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_t inactive, const void* kp,
                          const void* tp, const void* ip, bool eager, uint32_t shard, uint32_t nshard,
-                         bool profile = false) {
+                         bool profile = false, bool hb = false) {
   if (nshard > 1) eager = true;  // sharded analyses are not graph-replayed
+  if (hb) eager = true;          // the plan cache is for the G-WCP detector
+  c->last_hb = hb;
   c->prof_done = false;
   if (profile) {
     eager = true;
@@ -1253,6 +1258,7 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   p.tr = tr;
   p.shard = shard;
   p.nshard = nshard;
+  p.hb_mode = hb;
   p.run();
   if (eager || tr.n == 0 || !p.obs_snap || p.obs_nlarge > 0 || p.obs.n_long > 0 || st == 0) return;
   // build the plan; run the graph-mode pipeline once for real (allocates every
@@ -1306,7 +1312,7 @@ extern "C" int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* t, const gw
     if (sh >= nsh) throw CudaErr{GW_E_ARG, "shard_index must be < shard_count"};
     DevTrace tr = make_dev(t, (const unsigned long long*)t->key, t->tidop, t->instr);
     analyze_impl(c, tr, st, inactive, t->key, t->tidop, t->instr, o && (o->flags & GW_OPT_EAGER), sh, nsh,
-                 o && (o->flags & GW_OPT_PROFILE));
+                 o && (o->flags & GW_OPT_PROFILE), o && (o->flags & GW_OPT_HB));
   });
 }
 
@@ -1333,7 +1339,7 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
     }
     DevTrace tr = make_dev(t, k, to, in);
     analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,
-                 o && (o->flags & GW_OPT_PROFILE));
+                 o && (o->flags & GW_OPT_PROFILE), o && (o->flags & GW_OPT_HB));
   });
 }
 
@@ -1353,7 +1359,7 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
         c->last_graph = false;
         Pipeline p;
         p.C = c; p.st = c->last_stream; p.inactive_opt = c->last_inactive; p.tr = c->last_tr;
-        p.shard = c->last_shard; p.nshard = c->last_nshard;
+        p.shard = c->last_shard; p.nshard = c->last_nshard; p.hb_mode = c->last_hb;
         p.run();
         CK(cudaMemcpyAsync(sc, c->d_scal, sizeof sc, cudaMemcpyDeviceToHost, c->last_stream));
         CK(cudaStreamSynchronize(c->last_stream));

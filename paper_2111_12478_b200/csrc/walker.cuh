@@ -108,6 +108,7 @@ struct WalkArgs {
   uint32_t* ftop;
   uint32_t fcap;
   uint32_t warp_stacks;  // free stacks per (CTA, warp) (k_walker_lw) instead of per CTA
+  uint32_t hb_mode;      // scoped-HB detector (hb.py): checks read hb; no queues, records, cs or P clocks
   // lock mode: race-check queries answered in trace order by the walker
   const uint32_t* q_cur;    // query current events, sorted
   const uint32_t* q_idx;    // candidate index of each sorted query
@@ -1080,7 +1081,7 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   bool mat = false;
   // (1) drain: scans until done, applying the collected joins in between when a scan fills up
   bool first = true;
-  while (true) {
+  while (!a.hb_mode) {  // scoped HB (hb.py:59-72) has no queues
     drain_scan(a, t, lock, cur, s_dr, first, nullptr);
     first = false;
     if (threadIdx.x == 0) cap_drain(a, s_cap, s_dr);
@@ -1091,10 +1092,20 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   // (2) the record (acq_clock kept as its epoch (t, local); see the drain-test note) and the frame
   if (threadIdx.x == 0) {
     LockEnt* lk = s_lk;
-    const uint32_t ri = a.rix[a.poff[e]];
+    const uint32_t ri = a.hb_mode ? 0u : a.rix[a.poff[e]];
     const uint32_t d = a.depth[t];
     InstEnt* own = inst_find(a, lock, cur, false);
-    if (ri >= a.rec_cap) { atomicOr(a.err, ERR_REC); }
+    if (a.hb_mode) {
+      if (d >= a.maxd) atomicOr(a.err, ERR_FRAMES);
+      else {
+        Frame f;
+        f.lock = lock; f.scope = cur; f.rec = NIL; f.logpos = a.loghead[t];
+        f.iver = own ? __ldcg(&own->relver) : 0u;
+        a.frames[(size_t)t * a.maxd + d] = f;
+        a.depth[t] = d + 1;
+      }
+    }
+    else if (ri >= a.rec_cap) { atomicOr(a.err, ERR_REC); }
     else if (d >= a.maxd) { atomicOr(a.err, ERR_FRAMES); }
     else {
       const uint32_t base = __ldcg(&lk->rec_base);
@@ -1131,7 +1142,8 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
         if (sc_overlap(__ldcg(&ie->scope), cur)) {
           if (s_cap.n + 2 > (uint32_t)kMaxCap) break;  // apply these first
           cap_push(a, s_cap, CRef{__ldcg(&ie->H.o), __ldcg(&ie->H.dtid), __ldcg(&ie->H.dval)}, 1);
-          cap_push(a, s_cap, CRef{__ldcg(&ie->P.o), __ldcg(&ie->P.dtid), __ldcg(&ie->P.dval)}, 0);
+          if (!a.hb_mode)
+            cap_push(a, s_cap, CRef{__ldcg(&ie->P.o), __ldcg(&ie->P.dtid), __ldcg(&ie->P.dval)}, 0);
         }
         i = __ldcg(&ie->next);
       }
@@ -1211,7 +1223,7 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   bool first = true;
   bool mat = false;
   int pch = 0, hch = 0;
-  while (true) {
+  while (!a.hb_mode) {
     drain_scan(a, t, lock, inst, s_dr, first, nullptr);
     first = false;
     if (threadIdx.x == 0) cap_drain(a, s_cap, s_dr);
@@ -1233,7 +1245,7 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   const bool dom = s_dom != 0;
   // (3) cs_read / cs_write for the frame's read / write sets (gwcp.py:207-210)
   __shared__ CsEnt* s_ce;
-  uint32_t li = a.loghead[t];  // thread 0's iterator over the frame's access log
+  uint32_t li = a.hb_mode ? s_f.logpos : a.loghead[t];  // thread 0's iterator over the frame's access log
   while (true) {
     if (threadIdx.x == 0) {
       s_ce = nullptr;
@@ -1255,10 +1267,10 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   // (4) instance clocks H_i, P_i (gwcp.py:211-216)
   if (s_ie) {
     if (dom) {
-      if (threadIdx.x == 0) { cref_set(a, &s_ie->H, hb); cref_set(a, &s_ie->P, pr); }
+      if (threadIdx.x == 0) { cref_set(a, &s_ie->H, hb); if (!a.hb_mode) cref_set(a, &s_ie->P, pr); }
     } else {
       cref_join_new(a, &s_ie->H, hb, S, n);
-      cref_join_new(a, &s_ie->P, pr, S, n);
+      if (!a.hb_mode) cref_join_new(a, &s_ie->P, pr, S, n);
     }
   }
   __syncthreads();
@@ -1272,12 +1284,14 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
     }
     // close the record with rel_clock = copy(hb) (gwcp.py:216): the record
     // pins the thread's current hb object; pop; local += 1
-    Rec* r = &a.recs[s_f.rec];
-    obj_retain(a, hb.o);
-    r->rel_hobj = hb.o;
-    r->rel_local = hb.dval;
-    __threadfence();
-    r->closed = 1;
+    if (!a.hb_mode) {
+      Rec* r = &a.recs[s_f.rec];
+      obj_retain(a, hb.o);
+      r->rel_hobj = hb.o;
+      r->rel_local = hb.dval;
+      __threadfence();
+      r->closed = 1;
+    }
     uint32_t d = a.depth[t] - 1;
     a.depth[t] = d;
     if (d == 0) a.loghead[t] = NIL;
@@ -1307,8 +1321,8 @@ __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsig
   int pch = 0, hch = 0;
   bool mat = false, released = false;
   // frames x released instances of the frame's lock overlapping the frame's
-  // instance x {cs_write, cs_read if this is a write}
-  while (true) {
+  // instance x {cs_write, cs_read if this is a write}; HB has no cs clocks
+  while (!a.hb_mode) {
     if (threadIdx.x == 0) {
       uint32_t fi = s_fi, ii = s_ii, phase = s_phase;
       unsigned long long flock = s_flock;
@@ -1351,12 +1365,14 @@ __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsig
   if (threadIdx.x == 0) {
     a.time[e] = a.local[t];
     if (a.vobj) a.vobj[e] = a.pobj[t];
-    if (a.lflags[e] & LF_QUERY) answer_queries(a, e, a.pobj[t]);
-    uint32_t li = atomicAdd(a.log_top, 1u);
-    if (li >= a.log_cap) atomicOr(a.err, ERR_LOG);
-    else {
-      a.logs[li] = LogEnt{loc, isw, a.loghead[t]};
-      a.loghead[t] = li;
+    if (a.lflags[e] & LF_QUERY) answer_queries(a, e, a.hb_mode ? a.hobj[t] : a.pobj[t]);
+    if (!a.hb_mode) {  // the frame's read / write sets (HB keeps none)
+      uint32_t li = atomicAdd(a.log_top, 1u);
+      if (li >= a.log_cap) atomicOr(a.err, ERR_LOG);
+      else {
+        a.logs[li] = LogEnt{loc, isw, a.loghead[t]};
+        a.loghead[t] = li;
+      }
     }
   }
   __syncthreads();
@@ -1472,7 +1488,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_walker(WalkArgs a) {
             const uint32_t e = s_e[j0 + threadIdx.x + k * kThreads];
             a.time[e] = lv[k];
             if (a.vobj) a.vobj[e] = ov[k];
-            else if (a.lflags[e] & LF_QUERY) answer_queries(a, e, ov[k]);
+            else if (a.lflags[e] & LF_QUERY) answer_queries(a, e, a.hb_mode ? a.hobj[tt[k]] : ov[k]);
           }
       }
       __syncthreads();
@@ -1669,25 +1685,30 @@ __global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t*
 __global__ void k_hard_append(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
                               const uint32_t* abort_flag) {
   if (*(volatile const uint32_t*)abort_flag) return;  // graph mode: the plan does not fit this trace
-  for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x; e0 < tr.n; e0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = e0 + threadIdx.x;
-    bool hard = false;
-    uint32_t to = 0;
-    if (e < tr.n) {
-      to = tr.tidop[e];
-      const uint32_t k = ev_kind(to);
-      hard = k == GW_K_BARRIER || k == GW_K_END;
+  constexpr int U = 4;  // aligned 32-event windows per warp iteration (loads issued together)
+  const int lane = threadIdx.x & 31;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * U;
+  for (uint64_t b0 = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; b0 < tr.n; b0 += stride) {
+    uint32_t to[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t e = b0 + 32 * u + lane;
+      to[u] = e < tr.n ? tr.tidop[e] : (7u << GW_OP_SHIFT);
     }
-    const uint32_t m = __ballot_sync(0xffffffffu, hard);
-    if (!m) continue;
-    const int lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (lane == __ffs(m) - 1) base = atomicAdd(ntop, (uint32_t)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-    if (hard) {
-      const uint32_t b = ev_tid(to) / tr.BS;
-      hkey[base + __popc(m & lanemask_lt())] = ((unsigned long long)b << 32) | (uint32_t)e;
-      atomicAdd(hcnt + b, 1u);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t k = ev_kind(to[u]);
+      const bool hard = k == GW_K_BARRIER || k == GW_K_END;
+      const uint32_t m = __ballot_sync(0xffffffffu, hard);
+      if (!m) continue;
+      uint32_t base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(ntop, (uint32_t)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (hard) {
+        const uint32_t b = ev_tid(to[u]) / tr.BS;
+        hkey[base + __popc(m & lanemask_lt())] = ((unsigned long long)b << 32) | (uint32_t)(b0 + 32 * u + lane);
+        atomicAdd(hcnt + b, 1u);
+      }
     }
   }
 }

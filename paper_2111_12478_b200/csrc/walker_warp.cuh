@@ -303,7 +303,7 @@ __device__ void w_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned l
   if (lane == 0) { S.cap.n = 0; S.cap.full = 0; }
   __syncwarp();
   bool first = true;
-  while (true) {
+  while (!a.hb_mode) {  // scoped HB (hb.py:59-72) has no queues
     w_drain_scan(a, t, lock, cur, S, first);
     first = false;
     if (lane == 0) cap_drain(a, S.cap, S.dr);
@@ -314,10 +314,20 @@ __device__ void w_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned l
   uint32_t inst = NIL;
   if (lane == 0) {
     LockEnt* lk = lock_find(a, lock, false);
-    const uint32_t ri = a.rix[a.poff[e]];
+    const uint32_t ri = a.hb_mode ? 0u : a.rix[a.poff[e]];
     const uint32_t d = a.depth[t];
     InstEnt* own = inst_find(a, lock, cur, false);
     if (!lk) { atomicOr(a.err, ERR_INTERNAL); }
+    else if (a.hb_mode) {
+      if (d >= a.maxd) atomicOr(a.err, ERR_FRAMES);
+      else {
+        Frame f;
+        f.lock = lock; f.scope = cur; f.rec = NIL; f.logpos = a.loghead[t];
+        f.iver = own ? __ldcg(&own->relver) : 0u;
+        a.frames[(size_t)t * a.maxd + d] = f;
+        a.depth[t] = d + 1;
+      }
+    }
     else if (ri >= a.rec_cap) { atomicOr(a.err, ERR_REC); }
     else if (d >= a.maxd) { atomicOr(a.err, ERR_FRAMES); }
     else {
@@ -351,7 +361,8 @@ __device__ void w_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned l
         if (sc_overlap(__ldcg(&ie->scope), cur)) {
           if (S.cap.n + 2 > (uint32_t)kMaxCap) break;
           cap_push(a, S.cap, CRef{__ldcg(&ie->H.o), __ldcg(&ie->H.dtid), __ldcg(&ie->H.dval)}, 1);
-          cap_push(a, S.cap, CRef{__ldcg(&ie->P.o), __ldcg(&ie->P.dtid), __ldcg(&ie->P.dval)}, 0);
+          if (!a.hb_mode)
+            cap_push(a, S.cap, CRef{__ldcg(&ie->P.o), __ldcg(&ie->P.dtid), __ldcg(&ie->P.dval)}, 0);
         }
         i = __ldcg(&ie->next);
       }
@@ -413,7 +424,7 @@ __device__ void w_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned l
   __syncwarp();
   const uint32_t inst = f.scope;
   bool first = true;
-  while (true) {
+  while (!a.hb_mode) {
     w_drain_scan(a, t, lock, inst, S, first);
     first = false;
     if (lane == 0) cap_drain(a, S.cap, S.dr);
@@ -435,7 +446,7 @@ __device__ void w_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned l
   const CRef hb = CRef{a.hobj[t], t, a.local[t]};
   const CRef pr = CRef{a.pobj[t], t, a.pdiag[t]};
   // cs_read / cs_write of the frame's read / write sets (gwcp.py:207-210)
-  uint32_t li = a.loghead[t];
+  uint32_t li = a.hb_mode ? f.logpos : a.loghead[t];  // HB keeps no cs clocks
   while (true) {
     CsEnt* ce = nullptr;
     if (lane == 0) {
@@ -457,10 +468,10 @@ __device__ void w_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned l
   // instance clocks H_i, P_i (gwcp.py:211-216)
   if (ie) {
     if (dom) {
-      if (lane == 0) { cref_set(a, &ie->H, hb); cref_set(a, &ie->P, pr); }
+      if (lane == 0) { cref_set(a, &ie->H, hb); if (!a.hb_mode) cref_set(a, &ie->P, pr); }
     } else {
       w_cref_join_new(a, &ie->H, hb, S, n);
-      w_cref_join_new(a, &ie->P, pr, S, n);
+      if (!a.hb_mode) w_cref_join_new(a, &ie->P, pr, S, n);
     }
   }
   __syncwarp();
@@ -472,12 +483,14 @@ __device__ void w_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned l
       }
       ie->relver = __ldcg(&ie->relver) + 1;
     }
-    Rec* r = &a.recs[f.rec];
-    obj_retain(a, hb.o);
-    r->rel_hobj = hb.o;
-    r->rel_local = hb.dval;
-    __threadfence();
-    r->closed = 1;
+    if (!a.hb_mode) {
+      Rec* r = &a.recs[f.rec];
+      obj_retain(a, hb.o);
+      r->rel_hobj = hb.o;
+      r->rel_local = hb.dval;
+      __threadfence();
+      r->closed = 1;
+    }
     const uint32_t d = a.depth[t] - 1;
     a.depth[t] = d;
     if (d == 0) a.loghead[t] = NIL;
@@ -499,7 +512,7 @@ __device__ void w_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsign
   if (lane == 0) { S.cap.n = 0; S.cap.full = 0; }
   __syncwarp();
   bool released = false;
-  while (true) {
+  while (!a.hb_mode) {  // rule (i); HB has no cs clocks
     uint32_t done = 0;
     if (lane == 0) {
       bool stop = false;
@@ -537,12 +550,14 @@ __device__ void w_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsign
   if (!released) w_tickets_release(a, e);
   if (lane == 0) {
     a.time[e] = a.local[t];
-    if (a.lflags[e] & LF_QUERY) answer_queries(a, e, a.pobj[t]);
-    const uint32_t li = atomicAdd(a.log_top, 1u);
-    if (li >= a.log_cap) atomicOr(a.err, ERR_LOG);
-    else {
-      a.logs[li] = LogEnt{loc, isw, a.loghead[t]};
-      a.loghead[t] = li;
+    if (a.lflags[e] & LF_QUERY) answer_queries(a, e, a.hb_mode ? a.hobj[t] : a.pobj[t]);
+    if (!a.hb_mode) {  // the frame's read / write sets (HB keeps none)
+      const uint32_t li = atomicAdd(a.log_top, 1u);
+      if (li >= a.log_cap) atomicOr(a.err, ERR_LOG);
+      else {
+        a.logs[li] = LogEnt{loc, isw, a.loghead[t]};
+        a.loghead[t] = li;
+      }
     }
   }
   __syncwarp();
@@ -697,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_walker_lw(WalkArgs a, const uin
         if (lane >= start && lane < h && kd <= GW_K_WRITE) {
           const uint32_t t = ev_tid(to);
           a.time[ev] = a.local[t];
-          if (a.lflags[ev] & LF_QUERY) answer_queries(a, ev, a.pobj[t]);
+          if (a.lflags[ev] & LF_QUERY) answer_queries(a, ev, a.hb_mode ? a.hobj[t] : a.pobj[t]);
         }
         __syncwarp();
         lap(0);

@@ -54,19 +54,20 @@ def diagnostics_of(tr: Trace, res: dict) -> list[Diagnostic]:
     return out
 
 
-def analyze(trace, *, inactive_opt: bool = True) -> tuple[Trace, dict]:
+def analyze(trace, *, inactive_opt: bool = True, hb: bool = False) -> tuple[Trace, dict]:
     tr = encode(trace)
-    res = N.analyze(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt=inactive_opt)
+    res = N.analyze(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt=inactive_opt, hb=hb)
     return tr, res
 
 
 def run(trace, detector, *, order_matrix: bool = False, collect_stats: bool = False) -> RunResult:
     if order_matrix or collect_stats:
         raise NotImplementedError("--order-matrix / stats stay on the reference's Python detector")
-    if getattr(detector, "name", "gwcp") != "gwcp":
-        raise NotImplementedError("only the gwcp detector is accelerated")
-    tr, res = analyze(trace, inactive_opt=getattr(detector, "inactive_opt", True))
-    reports = build_reports(tr, res, "gwcp")
+    name = getattr(detector, "name", "gwcp")
+    if name not in ("gwcp", "hb"):
+        raise NotImplementedError("only the gwcp and hb detectors are accelerated")
+    tr, res = analyze(trace, inactive_opt=getattr(detector, "inactive_opt", True), hb=name == "hb")
+    reports = build_reports(tr, res, name)
     diags = diagnostics_of(tr, res)
     if hasattr(detector, "reporter"):
         detector.reporter.reports = list(reports)

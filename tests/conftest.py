@@ -10,6 +10,7 @@ if REPO not in sys.path:
     sys.path.insert(0, REPO)
 
 GOLDEN = os.path.join(REPO, "tests", "golden", "golden.jsonl.gz")
+GOLDEN_HB = os.path.join(REPO, "tests", "golden", "golden_hb.jsonl.gz")
 
 
 def pytest_configure(config):
@@ -41,3 +42,15 @@ def golden_text(rec) -> str:
 @pytest.fixture(scope="session")
 def goldens():
     return golden_records()
+
+
+@pytest.fixture(scope="session")
+def goldens_hb():
+    """(golden record, HB golden record) pairs: the reference's HbDetector on
+    every golden trace (tests/golden/make_golden_hb.py)."""
+    with gzip.open(GOLDEN_HB, "rt", encoding="utf-8") as fh:
+        hb = {}
+        for line in fh:
+            r = json.loads(line)
+            hb[r["name"]] = r
+    return [(r, hb[r["name"]]) for r in golden_records() if "error" not in r and r["name"] in hb]

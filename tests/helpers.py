@@ -20,9 +20,9 @@ def lines_sha(lines) -> str:
     return hashlib.sha256(("\n".join(lines) + "\n").encode()).hexdigest() if lines else ""
 
 
-def check_against_golden(rec, tr, res):
+def check_against_golden(rec, tr, res, detector="gwcp"):
     """Assert engine/oracle result arrays reproduce the reference's golden output."""
-    lines = ndjson_lines(tr, res)
+    lines = ndjson_lines(tr, res, detector)
     diags = [str(d) for d in diagnostics_of(tr, res)]
     name = rec["name"]
     assert len(lines) == rec["n_reports"], f"{name}: {len(lines)} reports, reference {rec['n_reports']}"

@@ -34,8 +34,21 @@ def test_validation_error_exits_three(tmp_path):
 
 
 def test_other_detectors_are_not_on_the_accelerated_path(tmp_path):
-    r = _cli(tmp_path, _corpus("wcp-classic")["text"], "--detector", "hb")
+    r = _cli(tmp_path, _corpus("wcp-classic")["text"], "--detector", "lockset")
     assert r.returncode == 2
+
+
+@pytest.mark.gpu
+def test_hb_detector_cli_matches_reference(tmp_path, goldens_hb):
+    n = 0
+    for r, h in goldens_hb:
+        if not r["name"].startswith("corpus/") or r["name"].endswith("/noio") or "reports" not in h:
+            continue
+        p = _cli(tmp_path, r["text"], "--detector", "hb")
+        assert p.returncode == (1 if h["reports"] else 0), r["name"]
+        assert p.stdout.splitlines() == h["reports"], r["name"]
+        n += 1
+    assert n > 10
 
 
 @pytest.mark.gpu

@@ -337,3 +337,48 @@ def test_lock_walker_modes(ctx, mode, goldens, monkeypatch):
     assert n > 0
     tr = parse_trace(WL.c3_text(blocks=20, warps=6, lanes=32, iters=24, locks=12, region=8, private=64, seed=77))
     assert ndjson_lines(tr, _run(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
+
+
+def _run_hb(ctx, tr):
+    ctx.analyze_host(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, hb=True)
+    return ctx.fetch()
+
+
+@pytest.mark.parametrize("mode", ["warp", "cta"])
+def test_hb_detector_matches_reference(ctx, mode, goldens_hb, monkeypatch):
+    """`--detector hb` (GW_OPT_HB) against the reference's HbDetector on every
+    golden trace, with both lock-mode sync passes."""
+    monkeypatch.setenv("GW_LOCK_WALK", mode)
+    n = 0
+    for r, h in goldens_hb:
+        if "full" in r["tags"]:
+            continue
+        tr = parse_trace(golden_text(r))
+        check_against_golden(h, tr, _run_hb(ctx, tr), "hb")
+        n += 1
+    assert n > 700
+
+
+@pytest.mark.parametrize("mode", ["warp", "cta"])
+def test_hb_detector_c3_vs_oracle(ctx, mode, monkeypatch):
+    monkeypatch.setenv("GW_LOCK_WALK", mode)
+    for tr in (
+        parse_trace(WL.c3_text(blocks=24, warps=4, lanes=32, iters=40, locks=6, region=4, private=32, seed=9)),
+        parse_trace(WL.c3_text(blocks=64, warps=8, lanes=32, iters=6, locks=64, region=16, private=128, seed=5)),
+    ):
+        assert ndjson_lines(tr, _run_hb(ctx, tr), "hb") == ndjson_lines(tr, O.run_trace(tr, hb=True), "hb")
+    # the default detector afterwards is G-WCP again (no state leaks through the context)
+    assert ndjson_lines(tr, _run(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
+
+
+def test_hb_dropin_run_api(goldens_hb):
+    from paper_2111_12478_b200 import HbDetector
+
+    for r, h in goldens_hb:
+        if not r["name"].startswith("corpus/") or "reports" not in h:
+            continue
+        tr = parse_trace(golden_text(r))
+        det = HbDetector(tr.config)
+        res = run(tr, det)
+        assert [x.to_json() for x in res.reports] == h["reports"], r["name"]
+        assert [str(d) for d in det.diagnostics] == h["diags"]

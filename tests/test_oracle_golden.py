@@ -63,6 +63,19 @@ def test_oracle_matches_reference(goldens, tag):
     assert n > 0
 
 
+@pytest.mark.parametrize("tag", ["corpus", "random", "nasty", "c1", "largewin", "c2", "c3", "c4", "parse"])
+def test_oracle_hb_matches_reference(goldens_hb, tag):
+    """The oracle's scoped-HB mode against the reference's HbDetector (hb.py)."""
+    n = 0
+    for r, h in goldens_hb:
+        if tag not in r["tags"] or "full" in r["tags"]:
+            continue
+        tr = parse_trace(golden_text(r))
+        check_against_golden(h, tr, O.run_trace(tr, hb=True), "hb")
+        n += 1
+    assert n > 0
+
+
 @pytest.mark.slow
 def test_oracle_full_c2(goldens):
     r = next(r for r in goldens if r["name"] == "c2/full")
