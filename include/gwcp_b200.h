@@ -132,6 +132,16 @@ typedef struct gw_ctx gw_ctx;
 int gw_parse_text(const char* text, uint64_t len, gw_trace* out, int64_t* err_line);
 void gw_trace_free(gw_trace* t);
 
+/* Binary SoA trace file (the on-disk form of the
+ * columnar trace, 16 B/event, loaded without parsing).  Little-endian layout:
+ *   magic "GWSOA\0\1\0" (8 B) | blocks, warps, lanes, reserved (4 x u32) |
+ *   n_events (u64) | key[n] (u64) | tidop[n] (u32) | instr[n] (u32)
+ * gw_load_soa checks the header, the file size and that every event's
+ * thread index and kind are inside the configured hierarchy / encoding
+ * (GW_E_PARSE otherwise); it does not run validate_trace. */
+int gw_save_soa(const char* path, const gw_trace_view* t);
+int gw_load_soa(const char* path, gw_trace* out);
+
 /* validate_trace (trace.py:522-601): diagnostics as (event, code, a, b); see cli shim */
 int gw_validate(const gw_trace_view* t, uint64_t* n_out, uint32_t** ev, uint32_t** code,
                 uint64_t** a, uint64_t** b);

@@ -121,6 +121,8 @@ EXPORTS = (
     "gw_gen_c4_device",
     "gw_gen_c3_device",
     "gw_ctx_kernel_times",
+    "gw_save_soa",
+    "gw_load_soa",
 )
 
 _lib = None
@@ -183,6 +185,10 @@ def lib():
         L.gw_ctx_kernel_times.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(C.c_float),
                                           C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.gw_ctx_kernel_times.restype = C.c_int
+        L.gw_save_soa.argtypes = [C.c_char_p, C.POINTER(_View)]
+        L.gw_save_soa.restype = C.c_int
+        L.gw_load_soa.argtypes = [C.c_char_p, C.POINTER(_Trace)]
+        L.gw_load_soa.restype = C.c_int
         _lib = L
         return L
 
@@ -211,6 +217,10 @@ def parse_text(text: str | bytes):
         err = EngineError(rc, last_error())
         err.line = int(line.value)  # type: ignore[attr-defined]
         raise err
+    return _take_trace(L, t)
+
+
+def _take_trace(L, t):
     try:
         n = int(t.n_events)
         key = np.ctypeslib.as_array(t.key, shape=(max(n, 1),))[:n].copy()
@@ -220,6 +230,22 @@ def parse_text(text: str | bytes):
     finally:
         L.gw_trace_free(C.byref(t))
     return cfg, key, tidop, instr
+
+
+def save_soa(path: str, cfg, key, tidop, instr) -> None:
+    """Write the binary SoA trace file (include/gwcp_b200.h, gw_save_soa)."""
+    key = np.ascontiguousarray(key, np.uint64)
+    tidop = np.ascontiguousarray(tidop, np.uint32)
+    instr = np.ascontiguousarray(instr, np.uint32)
+    _check(lib().gw_save_soa(os.fsencode(path), C.byref(_view(cfg, key, tidop, instr))))
+
+
+def load_soa(path: str):
+    """Binary SoA trace file -> (cfg tuple, key, tidop, instr) (gw_load_soa)."""
+    L = lib()
+    t = _Trace()
+    _check(L.gw_load_soa(os.fsencode(path), C.byref(t)))
+    return _take_trace(L, t)
 
 
 def _view(cfg, key, tidop, instr) -> _View:

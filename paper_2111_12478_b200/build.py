@@ -7,12 +7,13 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", "engine.cu"), os.path.join(HERE, "csrc", "parse.cpp")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("primitives.cuh", "walker.cuh", "access.cuh", "common.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("primitives.cuh", "walker.cuh", "walker_warp.cuh",
+                                                         "access.cuh", "common.h")]
 OUT = os.path.join(HERE, "libgwcp_b200.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC", "-shared", "-lpthread",
 ]
 
 

@@ -12,7 +12,7 @@ from typing import NoReturn
 from . import _native as N
 from .engine import diagnostics_of
 from .report import ndjson_lines
-from .trace import TraceParseError, UnsupportedTrace, parse_trace, validate_trace
+from .trace import TraceParseError, UnsupportedTrace, load_trace, save_soa, validate_trace
 
 EXIT_CLEAN = 0
 EXIT_RACES = 1
@@ -25,18 +25,18 @@ def _die(code: int, message: str) -> NoReturn:
     raise SystemExit(code)
 
 
-def _load(path: str):
+def _load(path: str, validate: bool = True):
+    """Text trace or binary SoA file (by magic, trace.load_trace)."""
     try:
-        with open(path, "rb") as fh:
-            data = fh.read()
+        tr = load_trace(path)
     except OSError as e:
         _die(EXIT_USAGE, f"cannot read {path}: {e}")
-    try:
-        tr = parse_trace(data)
     except TraceParseError as e:
         _die(EXIT_USAGE, f"{path}: {e}")
     except UnsupportedTrace as e:
         _die(EXIT_USAGE, f"{path}: unsupported by the B200 engine: {e}")
+    if not validate:
+        return tr
     diags = validate_trace(tr)
     if diags:
         for d in diags:
@@ -61,6 +61,16 @@ def _cmd_check(args) -> int:
     return EXIT_RACES if out else EXIT_CLEAN
 
 
+def _cmd_convert(args) -> int:
+    """Text trace -> binary SoA file (16 B/event; `check` reads either)."""
+    tr = _load(args.trace, validate=False)
+    try:
+        save_soa(tr, args.out)
+    except (OSError, N.EngineError) as e:
+        _die(EXIT_USAGE, f"cannot write {args.out}: {e}")
+    return EXIT_CLEAN
+
+
 def _build_parser() -> argparse.ArgumentParser:
     p = argparse.ArgumentParser(prog="gwcp-b200", description="B200 G-WCP trace race analysis.")
     sub = p.add_subparsers(dest="command", required=True)
@@ -73,6 +83,10 @@ def _build_parser() -> argparse.ArgumentParser:
     c.add_argument("--order-matrix", action="store_true")
     c.add_argument("--json", action="store_true", help="accepted for symmetry")
     c.set_defaults(func=_cmd_check)
+    v = sub.add_parser("convert", help="write a trace as a binary SoA file")
+    v.add_argument("trace")
+    v.add_argument("out")
+    v.set_defaults(func=_cmd_convert)
     return p
 
 

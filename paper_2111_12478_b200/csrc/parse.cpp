@@ -12,9 +12,13 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <string_view>
 #include <vector>
 #include <unordered_map>
 #include <unordered_set>
+#include <algorithm>
+#include <memory>
+#include <thread>
 
 #include "../../include/gwcp_b200.h"
 #include "common.h"
@@ -30,7 +34,7 @@ struct ParseError {
 };
 
 // Python's repr() of a str token (ASCII subset; tokens never hold whitespace).
-std::string py_repr(const std::string& s) {
+std::string py_repr(std::string_view s) {
   bool has_sq = s.find('\'') != std::string::npos;
   bool has_dq = s.find('"') != std::string::npos;
   char q = (has_sq && !has_dq) ? '"' : '\'';
@@ -81,7 +85,7 @@ int digit_val(char c) {
 
 // Python int(s, base) for base in {0, 10, 16} restricted to ASCII.  Returns
 // false on a syntax error (ValueError).  *overflow set if |v| >= 2^126.
-bool py_int(const std::string& s, int base, i128* out, bool* overflow) {
+bool py_int(std::string_view s, int base, i128* out, bool* overflow) {
   size_t i = 0, n = s.size();
   bool neg = false;
   *overflow = false;
@@ -120,14 +124,14 @@ bool py_int(const std::string& s, int base, i128* out, bool* overflow) {
   return true;
 }
 
-bool lower_starts_prefix(const std::string& t) {
+bool lower_starts_prefix(std::string_view t) {
   if (t.size() < 2 || t[0] != '0') return false;
   char p = t[1] | 0x20;
   return p == 'x' || p == 'b' || p == 'o';
 }
 
 // trace.py:_parse_int
-i128 parse_int(const std::string& tok, int64_t line, const char* what, int base = 10) {
+i128 parse_int(std::string_view tok, int64_t line, const char* what, int base = 10) {
   i128 v;
   bool ovf;
   bool ok = lower_starts_prefix(tok) ? py_int(tok, 0, &v, &ovf) : py_int(tok, base, &v, &ovf);
@@ -138,13 +142,13 @@ i128 parse_int(const std::string& tok, int64_t line, const char* what, int base 
 
 inline bool is_ws(unsigned char c) { return c == ' ' || (c >= 9 && c <= 13) || (c >= 0x1c && c <= 0x1f); }
 
-void split_ws(const char* b, const char* e, std::vector<std::string>& toks) {
+void split_ws(const char* b, const char* e, std::vector<std::string_view>& toks) {
   toks.clear();
   while (b < e) {
     while (b < e && is_ws((unsigned char)*b)) b++;
     const char* s = b;
     while (b < e && !is_ws((unsigned char)*b)) b++;
-    if (b > s) toks.emplace_back(s, b);
+    if (b > s) toks.emplace_back(s, (size_t)(b - s));
   }
 }
 
@@ -171,16 +175,13 @@ struct Builder {
 
 struct Tid { int64_t b, w, l; };
 
-Tid parse_tid(const std::string& tok, const Cfg& cfg, int64_t line) {
-  std::vector<std::string> parts;
-  size_t s = 0;
-  while (true) {
-    size_t d = tok.find('.', s);
-    parts.push_back(tok.substr(s, d == std::string::npos ? std::string::npos : d - s));
-    if (d == std::string::npos) break;
-    s = d + 1;
-  }
-  if (parts.size() != 3) throw ParseError{line, "bad thread id: " + py_repr(tok), GW_E_PARSE};
+Tid parse_tid(std::string_view tok, const Cfg& cfg, int64_t line) {
+  // tok.split(".") into exactly three parts (no vector: this runs once per event line)
+  const size_t d1 = tok.find('.');
+  const size_t d2 = d1 == std::string::npos ? d1 : tok.find('.', d1 + 1);
+  if (d2 == std::string::npos || tok.find('.', d2 + 1) != std::string::npos)
+    throw ParseError{line, "bad thread id: " + py_repr(tok), GW_E_PARSE};
+  const std::string_view parts[3] = {tok.substr(0, d1), tok.substr(d1 + 1, d2 - d1 - 1), tok.substr(d2 + 1)};
   i128 b = parse_int(parts[0], line, "thread index");
   i128 w = parse_int(parts[1], line, "thread index");
   i128 l = parse_int(parts[2], line, "thread index");
@@ -192,7 +193,7 @@ Tid parse_tid(const std::string& tok, const Cfg& cfg, int64_t line) {
 }
 
 // trace.py:_parse_loc
-uint64_t parse_loc(const std::string& tok, int64_t block, int64_t line) {
+uint64_t parse_loc(std::string_view tok, int64_t block, int64_t line) {
   if (tok.size() < 3 || tok[1] != ':' || (tok[0] != 'g' && tok[0] != 's'))
     throw ParseError{line, "bad location: " + py_repr(tok), GW_E_PARSE};
   i128 a = parse_int(tok.substr(2), line, "address", 16);
@@ -207,7 +208,7 @@ uint64_t parse_loc(const std::string& tok, int64_t block, int64_t line) {
 }
 
 // returns 1 for device, 0 for block (trace.py:_parse_scope_word, SYSTEM -> DEVICE)
-int parse_scope(const std::string& tok, int64_t line) {
+int parse_scope(std::string_view tok, int64_t line) {
   if (tok == "block") return 0;
   if (tok == "device" || tok == "system") return 1;
   throw ParseError{line, "bad scope: " + py_repr(tok), GW_E_PARSE};
@@ -216,7 +217,7 @@ int parse_scope(const std::string& tok, int64_t line) {
 struct Tail { bool atomic = false; int device = 0; bool has_instr = false; i128 instr = 0; };
 
 // trace.py:_parse_access_tail
-Tail parse_tail(const std::vector<std::string>& toks, size_t from, int64_t line) {
+Tail parse_tail(const std::vector<std::string_view>& toks, size_t from, int64_t line) {
   Tail t;
   size_t i = from;
   while (i < toks.size()) {
@@ -250,7 +251,7 @@ void check_mask(i128 mask, const Cfg& cfg, int64_t line) {
     throw ParseError{line, "mask " + hex_str(mask) + " out of range", GW_E_PARSE};
 }
 
-void parse_line(Builder& B, std::vector<std::string>& toks, int64_t line) {
+void parse_line(Builder& B, std::vector<std::string_view>& toks, int64_t line) {
   Cfg& cfg = B.cfg;
   if (!B.have_cfg) {
     if (toks[0] != "config") throw ParseError{line, "first line must be a config line", GW_E_PARSE};
@@ -258,7 +259,8 @@ void parse_line(Builder& B, std::vector<std::string>& toks, int64_t line) {
     for (size_t i = 1; i < toks.size(); i++) {
       size_t eq = toks[i].find('=');
       if (eq == std::string::npos) throw ParseError{line, "bad config entry " + py_repr(toks[i]), GW_E_PARSE};
-      std::string k = toks[i].substr(0, eq), v = toks[i].substr(eq + 1);
+      std::string k(toks[i].substr(0, eq));
+      std::string_view v = toks[i].substr(eq + 1);
       vals[k] = parse_int(v, line, k.c_str());
     }
     for (const char* k : {"blocks", "warps", "lanes"})
@@ -271,7 +273,7 @@ void parse_line(Builder& B, std::vector<std::string>& toks, int64_t line) {
     B.have_cfg = true;
     return;
   }
-  const std::string& t0 = toks[0];
+  const std::string_view t0 = toks[0];
   if (t0 == "config") throw ParseError{line, "duplicate config line", GW_E_PARSE};
   if (t0 == "bar") {
     if (toks.size() >= 3 && toks[1] == "block") {
@@ -307,10 +309,10 @@ void parse_line(Builder& B, std::vector<std::string>& toks, int64_t line) {
     if (toks[4] == "rd") kind = GW_K_READ;
     else if (toks[4] == "wr") kind = GW_K_WRITE;
     else throw ParseError{line, "bad access kind " + py_repr(toks[4]), GW_E_PARSE};
-    std::vector<std::string> addrs;
+    std::vector<std::string_view> addrs;
     size_t i = 5;
     while (i < toks.size() && toks[i] != "atomic" && toks[i] != "instr") {
-      const std::string& a = toks[i];
+      const std::string_view a = toks[i];
       size_t s = 0;
       while (s <= a.size()) {
         size_t c = a.find(',', s);
@@ -337,7 +339,7 @@ void parse_line(Builder& B, std::vector<std::string>& toks, int64_t line) {
     return;
   }
   Tid tid = parse_tid(t0, cfg, line);
-  std::string op = toks.size() > 1 ? toks[1] : std::string();
+  const std::string_view op = toks.size() > 1 ? toks[1] : std::string_view();
   uint32_t ft = B.flat(tid.b, tid.w, tid.l);
   if (op == "rd" || op == "wr") {
     if (toks.size() < 3) throw ParseError{line, "access needs a location", GW_E_PARSE};
@@ -374,42 +376,140 @@ T* dup_vec(const std::vector<T>& v) {
   return p;
 }
 
+
+// str.splitlines() terminators: \n \r \r\n \v \f \x1c \x1d \x1e
+inline bool is_eol(unsigned char c) {
+  return c == '\n' || c == '\r' || c == 0x0b || c == 0x0c || c == 0x1c || c == 0x1d || c == 0x1e;
+}
+
+// Parse the lines of [p, end), numbering them from line_no + 1.  With
+// stop_at_cfg, returns right after the config line (the sequential prefix of
+// the parallel parse).  Returns the position reached; line_no is updated.
+const char* parse_range(Builder& B, const char* p, const char* end, int64_t& line_no, bool stop_at_cfg) {
+  std::vector<std::string_view> toks;
+  while (p < end) {
+    const char* s = p;
+    while (p < end && !is_eol((unsigned char)*p)) p++;
+    const char* e = p;
+    if (p < end) {
+      if (*p == '\r' && p + 1 < end && p[1] == '\n') p += 2;
+      else p++;
+    }
+    line_no++;
+    const char* hash = (const char*)memchr(s, '#', (size_t)(e - s));
+    if (hash) e = hash;
+    split_ws(s, e, toks);
+    if (toks.empty()) continue;
+    parse_line(B, toks, line_no);
+    if (stop_at_cfg && B.have_cfg) break;
+  }
+  return p;
+}
+
+// lines in a chunk that ends just after a '\n' (or at the end of the text)
+int64_t count_lines(const char* s, const char* e) {
+  int64_t n = 0;
+  for (const char* p = s; p < e; p++) {
+    const unsigned char c = (unsigned char)*p;
+    if (is_eol(c)) {
+      n++;
+      if (c == '\r' && p + 1 < e && p[1] == '\n') p++;
+    }
+  }
+  if (e > s && !is_eol((unsigned char)e[-1])) n++;  // last line without a terminator
+  return n;
+}
+
+struct Chunk {
+  const char* s;
+  const char* e;
+  int64_t line0 = 0;
+  Builder B;
+  bool failed = false;
+  ParseError err{0, "", 0};
+  bool nomem = false;
+};
+
+int parse_threads(uint64_t len) {
+  const char* env = getenv("GW_PARSE_THREADS");
+  int t = env ? atoi(env) : (int)std::thread::hardware_concurrency();
+  t = std::max(1, std::min(t, 64));
+  const char* mc = getenv("GW_PARSE_MIN_CHUNK");  // tests: force many small chunks
+  const uint64_t min_chunk = mc ? std::max<uint64_t>(1, strtoull(mc, nullptr, 10)) : (1ull << 22);  // 4 MiB
+  return (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)t, len / min_chunk));
+}
+
+template <class F>
+void parallel_for(int n, F f) {
+  std::vector<std::thread> th;
+  for (int i = 1; i < n; i++) th.emplace_back(f, i);
+  f(0);
+  for (auto& t : th) t.join();
+}
+
 }  // namespace
 
+// gw_parse_text: the sequential prefix up to the config line, then the rest in
+// line-aligned chunks parsed concurrently (one Builder per chunk, line numbers
+// from a parallel line count), concatenated in order.  The first error in
+// text order wins, as in the sequential reference parser.
 extern "C" int gw_parse_text(const char* text, uint64_t len, gw_trace* out, int64_t* err_line) {
   if (!out || (!text && len)) { gw_set_error("gw_parse_text: null argument"); return GW_E_ARG; }
   memset(out, 0, sizeof *out);
   if (err_line) *err_line = -1;
-  Builder B;
-  B.key.reserve(len / 8);
-  B.tidop.reserve(len / 8);
-  B.instr.reserve(len / 8);
-  std::vector<std::string> toks;
+  Builder B0;
+  std::vector<std::unique_ptr<Chunk>> ch;
+  uint64_t total = 0;
   try {
-    const char* p = text;
-    const char* end = text + len;
     int64_t line_no = 0;
-    while (p < end) {
-      // str.splitlines(): \n \r \r\n \v \f \x1c \x1d \x1e
-      const char* s = p;
-      while (p < end) {
-        unsigned char c = (unsigned char)*p;
-        if (c == '\n' || c == '\r' || c == 0x0b || c == 0x0c || c == 0x1c || c == 0x1d || c == 0x1e) break;
-        p++;
+    const char* end = text + len;
+    const char* p = parse_range(B0, text, end, line_no, true);
+    if (!B0.have_cfg) throw ParseError{0, "empty trace (no config line)", GW_E_PARSE};
+    const int T = parse_threads((uint64_t)(end - p));
+    const uint64_t rest = (uint64_t)(end - p);
+    const char* cs = p;
+    for (int i = 0; i < T && cs < end; i++) {
+      const char* ce = i == T - 1 ? end : p + rest * (uint64_t)(i + 1) / (uint64_t)T;
+      if (ce < cs) ce = cs;
+      if (ce < end) {
+        const char* nl = (const char*)memchr(ce, '\n', (size_t)(end - ce));
+        ce = nl ? nl + 1 : end;
       }
-      const char* e = p;
-      if (p < end) {
-        if (*p == '\r' && p + 1 < end && p[1] == '\n') p += 2;
-        else p++;
-      }
-      line_no++;
-      const char* hash = (const char*)memchr(s, '#', (size_t)(e - s));
-      if (hash) e = hash;
-      split_ws(s, e, toks);
-      if (toks.empty()) continue;
-      parse_line(B, toks, line_no);
+      auto c = std::make_unique<Chunk>();
+      c->s = cs;
+      c->e = ce;
+      c->B.cfg = B0.cfg;
+      c->B.have_cfg = true;
+      ch.push_back(std::move(c));
+      cs = ce;
     }
-    if (!B.have_cfg) throw ParseError{0, "empty trace (no config line)", GW_E_PARSE};
+    const int nc = (int)ch.size();
+    std::vector<int64_t> nlines(nc, 0);
+    parallel_for(nc, [&](int i) { nlines[i] = count_lines(ch[i]->s, ch[i]->e); });
+    int64_t ln = line_no;
+    for (int i = 0; i < nc; i++) { ch[i]->line0 = ln; ln += nlines[i]; }
+    parallel_for(nc, [&](int i) {
+      Chunk& c = *ch[i];
+      try {
+        c.B.key.reserve((size_t)(c.e - c.s) / 8);
+        c.B.tidop.reserve((size_t)(c.e - c.s) / 8);
+        c.B.instr.reserve((size_t)(c.e - c.s) / 8);
+        int64_t l = c.line0;
+        parse_range(c.B, c.s, c.e, l, false);
+      } catch (const ParseError& pe) {
+        c.failed = true;
+        c.err = pe;
+      } catch (const std::bad_alloc&) {
+        c.nomem = true;
+      }
+    });
+    for (int i = 0; i < nc; i++) {
+      if (total > (1ull << 31)) throw ParseError{0, "trace has more than 2^31 events", GW_E_UNSUPPORTED};
+      if (ch[i]->nomem) throw std::bad_alloc();
+      if (ch[i]->failed) throw ch[i]->err;
+      total += ch[i]->B.key.size();
+    }
+    if (total > (1ull << 31)) throw ParseError{0, "trace has more than 2^31 events", GW_E_UNSUPPORTED};
   } catch (const ParseError& pe) {
     if (err_line) *err_line = pe.line;
     gw_set_error("line " + std::to_string(pe.line) + ": " + pe.msg);
@@ -418,18 +518,29 @@ extern "C" int gw_parse_text(const char* text, uint64_t len, gw_trace* out, int6
     gw_set_error("gw_parse_text: out of host memory");
     return GW_E_NOMEM;
   }
-  out->cfg.blocks = (uint32_t)B.cfg.blocks;
-  out->cfg.warps = (uint32_t)B.cfg.warps;
-  out->cfg.lanes = (uint32_t)B.cfg.lanes;
-  out->n_events = B.key.size();
-  out->key = dup_vec(B.key);
-  out->tidop = dup_vec(B.tidop);
-  out->instr = dup_vec(B.instr);
+  out->cfg.blocks = (uint32_t)B0.cfg.blocks;
+  out->cfg.warps = (uint32_t)B0.cfg.warps;
+  out->cfg.lanes = (uint32_t)B0.cfg.lanes;
+  out->n_events = total;
+  const size_t nz = total ? total : 1;
+  out->key = (uint64_t*)malloc(sizeof(uint64_t) * nz);
+  out->tidop = (uint32_t*)malloc(sizeof(uint32_t) * nz);
+  out->instr = (uint32_t*)malloc(sizeof(uint32_t) * nz);
   if (!out->key || !out->tidop || !out->instr) {
     gw_trace_free(out);
     gw_set_error("gw_parse_text: out of host memory");
     return GW_E_NOMEM;
   }
+  std::vector<uint64_t> off(ch.size() + 1, 0);
+  for (size_t i = 0; i < ch.size(); i++) off[i + 1] = off[i] + ch[i]->B.key.size();
+  parallel_for((int)ch.size(), [&](int i) {
+    const Builder& b = ch[i]->B;
+    const size_t k = b.key.size();
+    if (!k) return;
+    memcpy(out->key + off[i], b.key.data(), k * sizeof(uint64_t));
+    memcpy(out->tidop + off[i], b.tidop.data(), k * sizeof(uint32_t));
+    memcpy(out->instr + off[i], b.instr.data(), k * sizeof(uint32_t));
+  });
   return GW_OK;
 }
 
@@ -512,5 +623,88 @@ extern "C" int gw_validate(const gw_trace_view* t, uint64_t* n_out, uint32_t** e
   if (code) *code = dup_vec(oc);
   if (a) *a = dup_vec(oa);
   if (b) *b = dup_vec(ob);
+  return GW_OK;
+}
+
+// ---- binary SoA files (gwcp_b200.h) ----------------------------------------
+namespace {
+const char kSoaMagic[8] = {'G', 'W', 'S', 'O', 'A', 0, 1, 0};
+struct SoaHeader {
+  char magic[8];
+  uint32_t blocks, warps, lanes, reserved;
+  uint64_t n_events;
+};
+static_assert(sizeof(SoaHeader) == 32, "header layout");
+
+bool write_all(FILE* f, const void* p, size_t n) { return n == 0 || fwrite(p, 1, n, f) == n; }
+bool read_all(FILE* f, void* p, size_t n) { return n == 0 || fread(p, 1, n, f) == n; }
+}  // namespace
+
+extern "C" int gw_save_soa(const char* path, const gw_trace_view* t) {
+  if (!path || !t || (t->n_events && (!t->key || !t->tidop || !t->instr))) {
+    gw_set_error("gw_save_soa: null argument");
+    return GW_E_ARG;
+  }
+  FILE* f = fopen(path, "wb");
+  if (!f) { gw_set_error(std::string("gw_save_soa: cannot open ") + path); return GW_E_ARG; }
+  SoaHeader h;
+  memcpy(h.magic, kSoaMagic, 8);
+  h.blocks = t->cfg.blocks; h.warps = t->cfg.warps; h.lanes = t->cfg.lanes; h.reserved = 0;
+  h.n_events = t->n_events;
+  const size_t n = (size_t)t->n_events;
+  bool ok = write_all(f, &h, sizeof h) && write_all(f, t->key, n * 8) && write_all(f, t->tidop, n * 4) &&
+            write_all(f, t->instr, n * 4);
+  ok = (fclose(f) == 0) && ok;
+  if (!ok) { gw_set_error(std::string("gw_save_soa: write failed: ") + path); return GW_E_ARG; }
+  return GW_OK;
+}
+
+extern "C" int gw_load_soa(const char* path, gw_trace* out) {
+  if (!path || !out) { gw_set_error("gw_load_soa: null argument"); return GW_E_ARG; }
+  memset(out, 0, sizeof *out);
+  FILE* f = fopen(path, "rb");
+  if (!f) { gw_set_error(std::string("gw_load_soa: cannot open ") + path); return GW_E_ARG; }
+  SoaHeader h;
+  auto fail = [&](int code, const std::string& m) {
+    fclose(f);
+    gw_trace_free(out);
+    gw_set_error("gw_load_soa: " + std::string(path) + ": " + m);
+    return code;
+  };
+  if (!read_all(f, &h, sizeof h) || memcmp(h.magic, kSoaMagic, 8) != 0) return fail(GW_E_PARSE, "not a GWSOA file");
+  const uint64_t T = (uint64_t)h.blocks * h.warps * h.lanes;
+  if (!h.blocks || !h.warps || !h.lanes || T > (uint64_t)GW_TID_MASK + 1)
+    return fail(GW_E_PARSE, "bad thread hierarchy in header");
+  if (h.n_events > (1ull << 31)) return fail(GW_E_UNSUPPORTED, "more than 2^31 events");
+  if (fseeko(f, 0, SEEK_END) != 0) return fail(GW_E_PARSE, "cannot seek");
+  const uint64_t size = (uint64_t)ftello(f);
+  if (size != sizeof h + 16ull * h.n_events) return fail(GW_E_PARSE, "file size does not match n_events");
+  fseeko(f, (off_t)sizeof h, SEEK_SET);
+  const size_t n = (size_t)h.n_events, nz = n ? n : 1;
+  out->cfg.blocks = h.blocks; out->cfg.warps = h.warps; out->cfg.lanes = h.lanes;
+  out->n_events = n;
+  out->key = (uint64_t*)malloc(nz * 8);
+  out->tidop = (uint32_t*)malloc(nz * 4);
+  out->instr = (uint32_t*)malloc(nz * 4);
+  if (!out->key || !out->tidop || !out->instr) return fail(GW_E_NOMEM, "out of host memory");
+  if (!read_all(f, out->key, n * 8) || !read_all(f, out->tidop, n * 4) || !read_all(f, out->instr, n * 4))
+    return fail(GW_E_PARSE, "short read");
+  fclose(f);
+  // the engine indexes per-thread state by these fields: keep them in range
+  const uint32_t BS = h.warps * h.lanes;
+  for (size_t i = 0; i < n; i++) {
+    const uint32_t to = out->tidop[i];
+    const uint32_t tid = to & GW_TID_MASK, kind = (to >> GW_OP_SHIFT) & 7u;
+    bool bad = tid >= T || kind > GW_K_END || (to >> 31);
+    if (!bad && kind == GW_K_BARRIER)
+      bad = (to & GW_F_WARPBAR) ? (tid % h.lanes != 0 || h.lanes > 32) : (tid % BS != 0);
+    if (bad) {
+      char m[96];
+      snprintf(m, sizeof m, "event %zu: tidop 0x%08x outside the encoding", i, to);
+      gw_trace_free(out);
+      gw_set_error("gw_load_soa: " + std::string(path) + ": " + m);
+      return GW_E_PARSE;
+    }
+  }
   return GW_OK;
 }

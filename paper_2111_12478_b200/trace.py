@@ -325,6 +325,30 @@ def parse_trace(text: str | bytes) -> Trace:
     return Trace(TraceConfig(*cfg), key, tidop, instr)
 
 
+SOA_MAGIC = b"GWSOA\x00\x01\x00"
+
+
+def save_soa(trace, path: str) -> None:
+    """Write a trace as the binary SoA file of include/gwcp_b200.h (16 B/event;
+    the on-disk form of SURVEY §8(f) rank 1, read back without parsing)."""
+    tr = encode(trace)
+    N.save_soa(path, tr.cfg_tuple, tr.key, tr.tidop, tr.instr)
+
+
+def load_trace(path: str) -> Trace:
+    """A trace file: binary SoA (by its magic) or the text format (parse_trace)."""
+    with open(path, "rb") as fh:
+        head = fh.read(8)
+        if head == SOA_MAGIC:
+            try:
+                cfg, key, tidop, instr = N.load_soa(path)
+            except N.EngineError as e:
+                raise TraceParseError(0, str(e)) from None
+            return Trace(TraceConfig(*cfg), key, tidop, instr)
+        data = head + fh.read()
+    return parse_trace(data)
+
+
 _VALIDATE_MSG = {
     1: lambda a, b, cfg: f"barrier divergence: exited lane {a} in warp barrier mask",
     2: lambda a, b, cfg: f"barrier divergence: no live threads in block {a}",
