@@ -441,6 +441,7 @@ int parse_threads(uint64_t len) {
 
 template <class F>
 void parallel_for(int n, F f) {
+  if (n <= 0) return;
   std::vector<std::thread> th;
   for (int i = 1; i < n; i++) th.emplace_back(f, i);
   f(0);

@@ -38,6 +38,11 @@ def _parse_chunked(text, chunk=64, threads=8):
     return r.stdout.splitlines()
 
 
+def test_config_only_traces():
+    for text in ("config blocks=1 warps=1 lanes=1\n", "config blocks=2 warps=1 lanes=1", "\n#c\nconfig blocks=1 warps=1 lanes=1\n\n"):
+        assert len(parse_trace(text)) == 0
+
+
 def _parse_here(texts):
     out = []
     for t in texts:
@@ -56,6 +61,9 @@ def test_chunked_parser_equals_sequential_on_goldens(goldens):
     text including the reference's parse-error cases."""
     texts = [golden_text(r) for r in goldens if "full" not in r.get("tags", [])][:600]
     texts += [
+        "config blocks=1 warps=1 lanes=1\n",
+        "config blocks=1 warps=1 lanes=1",
+        "\n\n# x\nconfig blocks=1 warps=1 lanes=1\n\n\n",
         "config blocks=1 warps=1 lanes=2\r\n0.0.0 rd g:10\r\n\r\n0.0.1 wr g:10\n",
         "config blocks=1 warps=1 lanes=2\r0.0.0 rd g:10\x0b0.0.1 wr g:10",
         "# c\n\nconfig blocks=1 warps=1 lanes=2\n" + "0.0.0 rd g:10\n" * 200 + "0.0.9 rd g:1\n" + "bogus\n" * 50,
