@@ -280,9 +280,10 @@ def _take_result(L, r: _Result):
         nd = int(r.n_diags)
 
         def arr(p, count, dt):
-            if count == 0:
-                return np.zeros(0, dtype=dt)
-            return np.ctypeslib.as_array(p, shape=(count,)).copy()
+            out = np.empty(count, dtype=dt)
+            if count:
+                C.memmove(out.ctypes.data, p, out.nbytes)
+            return out
 
         res = {
             "kind": arr(r.kind, n, np.uint8),

@@ -82,7 +82,7 @@ __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals, Sta
   const K sentinel = kr.sentinel ? ((K)1 << (kr.nbits - 1)) : (K)0;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t to = tr.tidop[e];
-    aux[e] = make_aux(src, (uint32_t)e, to);
+    if (aux) aux[e] = make_aux(src, (uint32_t)e, to);
     K k = sentinel;
     if (ev_kind(to) <= GW_K_WRITE) {
       unsigned long long x = tr.key[e];
@@ -94,6 +94,12 @@ __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals, Sta
     keys[e] = k;
     vals[e] = (uint32_t)e | (ev_kind(to) == GW_K_WRITE ? VAL_W : 0u);
   }
+}
+
+// the stamps alone (the fork of Pipeline::run sorts the keys concurrently with the sync pass)
+__global__ void k_acc_aux(DevTrace tr, StampSrc src, uint4* aux) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x)
+    aux[e] = make_aux(src, (uint32_t)e, tr.tidop[e]);
 }
 
 // ---- address sharding -----------------------------------------------------

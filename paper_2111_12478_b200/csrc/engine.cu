@@ -109,6 +109,26 @@ struct gw_ctx {
   bool have_cands = false;
   uint64_t arena_words = 0;
   cudaStream_t last_stream = 0;
+  // results staged in mapped pinned host memory: k_final writes the report
+  // arrays straight into it and one 64-byte copy mirrors the scalars, so a
+  // fetch is one stream sync + host memcpys (no per-array D2H round trips)
+  uint8_t* hres = nullptr;
+  size_t hres_cap = 0;
+  uint32_t* h_scal = nullptr;
+  uint8_t* host_res(size_t bytes) {
+    if (hres_cap < bytes) {
+      if (hres) cudaFreeHost(hres);
+      hres = nullptr;
+      hres_cap = 0;
+      const size_t nb = bytes + bytes / 4;
+      CK(cudaHostAlloc((void**)&hres, nb, cudaHostAllocMapped | cudaHostAllocPortable));
+      hres_cap = nb;
+    }
+    return hres;
+  }
+  // side stream of the lock-free fork (access sort concurrent with the sync pass)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint32_t epoch = 1;  // look-back flag epochs (never reused within 2^24 passes)
   // last analysis, for an eager re-run after a graph abort
   DevTrace last_tr{};
@@ -181,6 +201,7 @@ struct gw_ctx {
 namespace {
 
 // scalar slots of the "scalars" buffer
+constexpr size_t kResHdr = 256;  // scalar mirror at the head of gw_ctx::hres
 enum : int { SC_MAXD = 0, SC_NINCS, SC_TICKET, SC_REC, SC_LOG, SC_DIAG, SC_ERR, SC_ABORT, SC_NCAND, SC_NLARGE,
              SC_NSURV, SC_NQ, SC_NQLARGE, SC_NDUP, SC_NHEADS, SC_COUNT = 16 };
 
@@ -246,7 +267,7 @@ struct Pipeline {
     }
     if (C->epoch + k >= (1u << 24)) {  // wrap: clear every flag / status word
       for (auto& kv : C->bufs)
-        if (kv.first == "rs_status") CK(cudaMemsetAsync(kv.second.p, 0, kv.second.cap, st));
+        if (kv.first.rfind("rs_status", 0) == 0) CK(cudaMemsetAsync(kv.second.p, 0, kv.second.cap, st));
       C->epoch = 1;
     }
     uint32_t e = C->epoch;
@@ -254,6 +275,7 @@ struct Pipeline {
     return e;
   }
   uint32_t gepoch = 0;
+  std::string sfx;  // scratch-name suffix of the side branch (its own look-back status words)
 
   // stable radix sort wrapper; returns pointers to the sorted keys / vals
   template <class K>
@@ -284,7 +306,8 @@ struct Pipeline {
     SortScratch sc;
     sc.ghist = zeroed(kRsMaxPass * kRsDigits);
     sc.ctrs = zeroed(npass);
-    sc.status = C->get<unsigned long long>("rs_status", std::max(lb_tiles(n), lb_tiles(tr.n)) * kRsDigits);
+    sc.status = C->get<unsigned long long>(std::string("rs_status") + sfx,
+                                           std::max(lb_tiles(n), lb_tiles(tr.n)) * kRsDigits);
     bool alt = radix_sort<K>(keys, ka, vals, va, n, nbits, sc, take_epochs(npass), st);
     if (alt) {
       keys = ka;
@@ -296,7 +319,7 @@ struct Pipeline {
   void big_sort(K*& keys, K* ka, uint32_t*& vals, uint32_t* va, uint64_t n, int nbits) {
     const int npass = (nbits + RB - 1) / RB;
     const uint64_t nst = (lb_tiles(n) + RsBig<RB>::ST - 1) / RsBig<RB>::ST;
-    uint32_t* counts = C->get<uint32_t>("rs_counts", nst * RsBig<RB>::ND);
+    uint32_t* counts = C->get<uint32_t>(std::string("rs_counts") + sfx, nst * RsBig<RB>::ND);
     rs_down_setup<K, RB>();
     rs_down_tma_setup<K>();
     const unsigned g = (unsigned)std::min<uint64_t>(nst, 148ull * 16);
@@ -326,7 +349,8 @@ struct Pipeline {
   template <class T, class Op, class Load, class Store>
   void scan(Load load, Store store, uint64_t n, Op op, T identity, bool inclusive, const char*) {
     if (n == 0) return;
-    unsigned long long* status = C->get<unsigned long long>("lb_status", std::max(lb_tiles(n), lb_tiles(tr.n)));
+    unsigned long long* status =
+        C->get<unsigned long long>(std::string("lb_status") + sfx, std::max(lb_tiles(n), lb_tiles(tr.n)));
     scan_lb<T, Op>(load, store, n, status, zeroed(1), op, identity, inclusive, st);
   }
 
@@ -403,8 +427,10 @@ struct Pipeline {
     CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
     CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
     if (gmode) {  // fixed epochs in the graph: start from clean flags
-      unsigned long long* rs = C->get<unsigned long long>("rs_status", lb_tiles(N) * kRsDigits);
-      CK(cudaMemsetAsync(rs, 0, C->bufs["rs_status"].cap, st));
+      for (const char* nm : {"rs_status", "rs_status_b"}) {
+        unsigned long long* rs = C->get<unsigned long long>(nm, lb_tiles(N) * kRsDigits);
+        CK(cudaMemsetAsync(rs, 0, C->bufs[nm].cap, st));
+      }
     }
     Stats* dst = C->get<Stats>("stats", 1);
     GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
@@ -481,7 +507,38 @@ struct Pipeline {
     pend(PH_PREP);
 
     Cands cd;
-    if (!has_locks) {
+    if (!has_locks && nshard <= 1 && !g_prof) {
+      // the location sort does not depend on the sync pass: it runs on the
+      // side stream while the walker runs here; the stamps (aux) are filled
+      // after the walker, then the branches join before the check
+      if (!C->side) {
+        CK(cudaStreamCreateWithFlags(&C->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&C->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming));
+      }
+      const cudaStream_t main_st = st;
+      aux = C->get<uint4>("acc_aux", N);  // allocated (and zeroed) on this stream: k_acc_aux writes it here
+      CK(cudaEventRecord(C->ev_fork, main_st));
+      CK(cudaStreamWaitEvent(C->side, C->ev_fork, 0));
+      st = C->side;
+      C->last_stream = st;
+      sfx = "_b";
+      pbeg(PH_SORT);
+      access_sort(true);
+      pend(PH_SORT);
+      CK(cudaEventRecord(C->ev_join, st));
+      st = main_st;
+      C->last_stream = st;
+      sfx.clear();
+      pbeg(PH_WALKER);
+      walker_phase();
+      GW_LAUNCH(k_acc_aux, grid_for(N), kThreads, 0, st, tr, stamps, aux);
+      pend(PH_WALKER);
+      CK(cudaStreamWaitEvent(st, C->ev_join, 0));
+      pbeg(PH_CHECK);
+      cd = check_pass(false, "c", SC_NCAND);
+      pend(PH_CHECK);
+    } else if (!has_locks) {
       pbeg(PH_WALKER);
       walker_phase();
       pend(PH_WALKER);
@@ -555,16 +612,19 @@ struct Pipeline {
         sort<uint32_t>(sk32, sv, ncap, ceil_log2(N + 1), "sv32");
         GW_LAUNCH(k_group_fix, grid_for(ncap), kThreads, 0, st, sk32, sv, (uint32_t)ncap, (uint32_t)N, cd.okey);
       }
-      C->d_kind = C->get<uint8_t>("o_kind", ncap);
-      C->d_prior = C->get<uint32_t>("o_prior", ncap);
-      C->d_cur = C->get<uint32_t>("o_cur", ncap);
-      C->d_okey = C->get<unsigned long long>("o_okey", ncap);
+      uint8_t* H = C->host_res(kResHdr + 17ull * ncap);  // mapped: the kernel writes over the bus
+      C->d_okey = (unsigned long long*)(H + kResHdr);
+      C->d_prior = (uint32_t*)(H + kResHdr + 8ull * ncap);
+      C->d_cur = (uint32_t*)(H + kResHdr + 12ull * ncap);
+      C->d_kind = H + kResHdr + 16ull * ncap;
       GW_LAUNCH(k_final, grid_for(ncap), kThreads, 0, st, cd, sv, d_nsurv, C->d_kind, C->d_prior, C->d_cur,
                 C->d_okey);
       check_launch();
     }
     C->d_diags = w.diags;
     C->arena_words = arena_units << OBJ_USHIFT;
+    C->h_scal = (uint32_t*)C->host_res(kResHdr + (ncap > 0 ? 17ull * ncap : 0ull));
+    CK(cudaMemcpyAsync(C->h_scal, scal, SC_COUNT * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     pend(PH_FINAL);
     event(1);
     S.n_sync = hs.n_acq + hs.n_rel + hs.n_end + hs.n_bar;
@@ -699,7 +759,8 @@ struct Pipeline {
   }
 
   // ------------------------------------------------- access sort + scan
-  void access_sort() {
+  // split: keys / vals only (the stamps are filled later by k_acc_aux)
+  void access_sort(bool split = false) {
     const uint64_t N = tr.n;
     kr = key_runs(gmode ? P->D : (hs.n_acc ? hs.key_or ^ hs.key_and : 0ull));
     C->stats.sort_bits = kr.nbits;
@@ -715,11 +776,12 @@ struct Pipeline {
       vals = C->get<uint32_t>("acc_v", N);
       if (!wide) {
         uint32_t* k32 = C->get<uint32_t>("acc_k", N);
-        GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals, stamps, aux);
+        GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals, stamps, split ? nullptr : aux);
         skeys = k32;
       } else {
         unsigned long long* k64 = C->get<unsigned long long>("acc_k64", N);
-        GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals, stamps, aux);
+        GW_LAUNCH(k_acc_keys<unsigned long long>, grid_for(N), kThreads, 0, st, tr, kr, k64, vals, stamps,
+                  split ? nullptr : aux);
         skeys = k64;
       }
     } else {
@@ -1209,6 +1271,10 @@ extern "C" void gw_ctx_destroy(gw_ctx* c) {
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   for (int i = 0; i < gw_ctx::kEv; i++)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->hres) cudaFreeHost(c->hres);
   delete c;
 }
 
@@ -1351,8 +1417,8 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
     uint64_t n = 0, nd = 0;
     if (c->d_scal) {
       uint32_t sc[SC_COUNT];
-      CK(cudaMemcpyAsync(sc, c->d_scal, sizeof sc, cudaMemcpyDeviceToHost, c->last_stream));
       CK(cudaStreamSynchronize(c->last_stream));
+      memcpy(sc, c->h_scal, sizeof sc);
       if (sc[SC_ABORT] && c->last_graph) {
         // the trace no longer matches the cached plan: re-run eagerly
         c->drop_plan();
@@ -1361,8 +1427,8 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
         p.C = c; p.st = c->last_stream; p.inactive_opt = c->last_inactive; p.tr = c->last_tr;
         p.shard = c->last_shard; p.nshard = c->last_nshard; p.hb_mode = c->last_hb;
         p.run();
-        CK(cudaMemcpyAsync(sc, c->d_scal, sizeof sc, cudaMemcpyDeviceToHost, c->last_stream));
         CK(cudaStreamSynchronize(c->last_stream));
+        memcpy(sc, c->h_scal, sizeof sc);
       }
       if (sc[SC_ERR]) {
         char buf[200];
@@ -1384,14 +1450,16 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
     out->current_event = (uint32_t*)malloc(4 * std::max<uint64_t>(n, 1));
     if (!out->kind || !out->prior_event || !out->current_event) throw std::bad_alloc();
     std::vector<Diag> dg(nd);
-    if (n) {
-      CK(cudaMemcpyAsync(out->kind, c->d_kind, n, cudaMemcpyDeviceToHost, c->last_stream));
-      CK(cudaMemcpyAsync(out->prior_event, c->d_prior, 4 * n, cudaMemcpyDeviceToHost, c->last_stream));
-      CK(cudaMemcpyAsync(out->current_event, c->d_cur, 4 * n, cudaMemcpyDeviceToHost, c->last_stream));
-      CK(cudaMemcpyAsync(out->order_key, c->d_okey, 8 * n, cudaMemcpyDeviceToHost, c->last_stream));
+    if (n) {  // written by k_final into mapped host memory (complete after the stream sync above)
+      memcpy(out->kind, c->d_kind, n);
+      memcpy(out->prior_event, c->d_prior, 4 * n);
+      memcpy(out->current_event, c->d_cur, 4 * n);
+      memcpy(out->order_key, c->d_okey, 8 * n);
     }
-    if (nd) CK(cudaMemcpyAsync(dg.data(), c->d_diags, sizeof(Diag) * nd, cudaMemcpyDeviceToHost, c->last_stream));
-    CK(cudaStreamSynchronize(c->last_stream));
+    if (nd) {
+      CK(cudaMemcpyAsync(dg.data(), c->d_diags, sizeof(Diag) * nd, cudaMemcpyDeviceToHost, c->last_stream));
+      CK(cudaStreamSynchronize(c->last_stream));
+    }
     std::sort(dg.begin(), dg.end(), [](const Diag& a, const Diag& b) {
       return a.ev != b.ev ? a.ev < b.ev : a.sub < b.sub;
     });
