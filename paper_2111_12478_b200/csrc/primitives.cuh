@@ -265,26 +265,38 @@ constexpr int kRsDigits = 1 << kRsBits;           // 256 = kThreads: one digit p
 constexpr int kRsMaxPass = 8;
 static_assert(kRsDigits == kThreads, "one digit per thread");
 
-template <class K>
+// RB-bit digits (RB = 8 or 9; 9 saves a pass when it covers the key in
+// fewer passes, e.g. 17-bit keys in 2 instead of 3); DPT digits per thread.
+constexpr int kRsMaxDigits = 512;
+template <int RB>
+struct RsDig {
+  static constexpr int ND = 1 << RB;
+  static constexpr int DPT = ND / kThreads;
+  static_assert(ND % kThreads == 0 && ND <= kRsMaxDigits, "digit layout");
+};
+
+template <class K, int RB>
 __global__ void __launch_bounds__(kThreads) k_rs_ghist(const K* __restrict__ keys, uint64_t n, int npass,
                                                       uint32_t* __restrict__ ghist) {
-  __shared__ uint32_t h[kRsMaxPass * kRsDigits];
-  for (int i = threadIdx.x; i < npass * kRsDigits; i += kThreads) h[i] = 0;
+  constexpr int ND = RsDig<RB>::ND;
+  __shared__ uint32_t h[kRsMaxPass * ND];
+  for (int i = threadIdx.x; i < npass * ND; i += kThreads) h[i] = 0;
   __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const K k = keys[i];
-    for (int p = 0; p < npass; p++) atomicAdd(&h[p * kRsDigits + ((uint32_t)(k >> (kRsBits * p)) & (kRsDigits - 1))], 1u);
+    for (int p = 0; p < npass; p++) atomicAdd(&h[p * ND + ((uint32_t)(k >> (RB * p)) & (ND - 1))], 1u);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < npass * kRsDigits; i += kThreads)
+  for (int i = threadIdx.x; i < npass * ND; i += kThreads)
     if (h[i]) atomicAdd(&ghist[i], h[i]);
 }
 
-template <class K>
+template <class K, int RB>
 struct RsSmem {
-  uint32_t wc[kRsWarps][kRsDigits];  // per-warp digit counts -> per-warp offsets within the digit
-  uint32_t toff[kRsDigits];          // tile-local start of digit d
-  uint32_t gbase[kRsDigits];         // global start of this tile's digit-d run
+  static constexpr int ND = RsDig<RB>::ND;
+  uint32_t wc[kRsWarps][ND];  // per-warp digit counts -> per-warp offsets within the digit
+  uint32_t toff[ND];          // tile-local start of digit d
+  uint32_t gbase[ND];         // global start of this tile's digit-d run
   K sk[kTile];
   uint32_t sv[kTile];
   uint32_t tile;
@@ -303,16 +315,16 @@ __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
   return peers;
 }
 
-template <class K>
+template <class K, int RB>
 __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                             K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                             uint64_t n, int pass, const uint32_t* __restrict__ ghist,
                                                             unsigned long long* status, uint32_t* ctr, uint32_t epoch) {
-  constexpr int ND = kRsDigits;
+  constexpr int ND = RsDig<RB>::ND, DPT = RsDig<RB>::DPT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  RsSmem<K>& S = *reinterpret_cast<RsSmem<K>*>(smem_raw);
+  RsSmem<K, RB>& S = *reinterpret_cast<RsSmem<K, RB>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int shift = kRsBits * pass;
+  const int shift = RB * pass;
   for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
   if (threadIdx.x == 0) S.tile = atomicAdd(ctr, 1u);
   __syncthreads();
@@ -322,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
   const bool full = tbase + kTile <= n;
   K kk[kRsRounds];
   uint32_t vv[kRsRounds];
-  uint32_t rd[kRsRounds];  // rank within the warp's digit run (bits 0-15) | digit (bits 16-24, 256 = none)
+  uint32_t rd[kRsRounds];  // rank within the warp's digit run (bits 0-15) | digit (bits 16-25, ND = none)
 #pragma unroll
   for (int r = 0; r < kRsRounds; r++) {
     const uint64_t i = wbase + (uint64_t)r * 32 + lane;
@@ -336,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
 #pragma unroll
   for (int r = 0; r < kRsRounds; r++) {
     const uint32_t d = rd[r] >> 16;
-    const uint32_t peers = full ? warp_peers<kRsBits>(d) : warp_peers<kRsBits + 1>(d);
+    const uint32_t peers = full ? warp_peers<RB>(d) : warp_peers<RB + 1>(d);
     const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
     __syncwarp();
     if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
@@ -345,56 +357,69 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
   }
   __syncthreads();
   {
-    // thread d owns digit d: per-warp offsets, tile count, look-back, global base
-    const int d = threadIdx.x;
-    uint32_t run = 0;
-#pragma unroll
-    for (int ww = 0; ww < kRsWarps; ww++) {
-      const uint32_t t = S.wc[ww][d];
-      S.wc[ww][d] = run;
-      run += t;
-    }
-    const uint32_t c = run;
+    // thread t owns digits t*DPT .. t*DPT+DPT-1: per-warp offsets, tile
+    // counts, look-back, global bases
     const unsigned long long EP = (unsigned long long)epoch << 40;
-    unsigned long long* my = &status[(uint64_t)tile * ND + d];
-    atomicExch(my, EP | ((tile == 0 ? 2ull : 1ull) << 38) | c);
-    const uint32_t g = ghist[pass * ND + d];
-    uint32_t gt, ct;
-    const uint32_t gex = block_excl_scan<uint32_t, OpSum>(g, OpSum(), 0u, &gt);
-    const uint32_t cex = block_excl_scan<uint32_t, OpSum>(c, OpSum(), 0u, &ct);
-    S.toff[d] = cex;
-    unsigned long long pre = 0;
-    if (tile > 0) {
-      // up to 8 predecessors per round trip: sum their aggregates back to the
-      // nearest inclusive prefix (all of them must have published)
-      constexpr int B8 = 8;
-      int64_t p = (int64_t)tile - 1;
-      while (true) {
-        unsigned long long w8[B8];
+    uint32_t c[DPT], g[DPT];
+    uint32_t csum = 0, gsum = 0;
 #pragma unroll
-        for (int k = 0; k < B8; k++)
-          w8[k] = p - k >= 0 ? ld_volatile_u64(&status[(uint64_t)(p - k) * ND + d]) : (EP | (2ull << 38));
-        int lim = B8;
-        bool ready = true;
+    for (int j = 0; j < DPT; j++) {
+      const int d = threadIdx.x * DPT + j;
+      uint32_t run = 0;
 #pragma unroll
-        for (int k = 0; k < B8; k++) {
-          if (lim == B8) {
-            if ((w8[k] >> 40) != epoch) { ready = false; lim = -1; }
-            else if (((w8[k] >> 38) & 3ull) == 2ull) lim = k;
-          }
-        }
-        if (!ready) continue;  // a predecessor before the nearest inclusive has not published yet
-        unsigned long long add = 0;
-#pragma unroll
-        for (int k = 0; k < B8; k++)
-          if (k <= lim) add += w8[k] & ((1ull << 38) - 1);
-        pre += add;
-        if (lim < B8) break;
-        p -= B8;
+      for (int ww = 0; ww < kRsWarps; ww++) {
+        const uint32_t t = S.wc[ww][d];
+        S.wc[ww][d] = run;
+        run += t;
       }
-      atomicExch(my, EP | (2ull << 38) | (pre + c));
+      c[j] = run;
+      atomicExch(&status[(uint64_t)tile * ND + d], EP | ((tile == 0 ? 2ull : 1ull) << 38) | run);
+      g[j] = ghist[pass * ND + d];
+      csum += run;
+      gsum += g[j];
     }
-    S.gbase[d] = gex + (uint32_t)pre;
+    uint32_t gt, ct;
+    uint32_t gex = block_excl_scan<uint32_t, OpSum>(gsum, OpSum(), 0u, &gt);
+    uint32_t cex = block_excl_scan<uint32_t, OpSum>(csum, OpSum(), 0u, &ct);
+#pragma unroll
+    for (int j = 0; j < DPT; j++) {
+      const int d = threadIdx.x * DPT + j;
+      S.toff[d] = cex;
+      cex += c[j];
+      unsigned long long pre = 0;
+      if (tile > 0) {
+        // up to 8 predecessors per round trip: sum their aggregates back to the
+        // nearest inclusive prefix (all of them must have published)
+        constexpr int B8 = 8;
+        int64_t p = (int64_t)tile - 1;
+        while (true) {
+          unsigned long long w8[B8];
+#pragma unroll
+          for (int k = 0; k < B8; k++)
+            w8[k] = p - k >= 0 ? ld_volatile_u64(&status[(uint64_t)(p - k) * ND + d]) : (EP | (2ull << 38));
+          int lim = B8;
+          bool ready = true;
+#pragma unroll
+          for (int k = 0; k < B8; k++) {
+            if (lim == B8) {
+              if ((w8[k] >> 40) != epoch) { ready = false; lim = -1; }
+              else if (((w8[k] >> 38) & 3ull) == 2ull) lim = k;
+            }
+          }
+          if (!ready) continue;  // a predecessor before the nearest inclusive has not published yet
+          unsigned long long add = 0;
+#pragma unroll
+          for (int k = 0; k < B8; k++)
+            if (k <= lim) add += w8[k] & ((1ull << 38) - 1);
+          pre += add;
+          if (lim < B8) break;
+          p -= B8;
+        }
+        atomicExch(&status[(uint64_t)tile * ND + d], EP | (2ull << 38) | (pre + c[j]));
+      }
+      S.gbase[d] = gex + (uint32_t)pre;
+      gex += g[j];
+    }
   }
   __syncthreads();
   // stage in digit order
@@ -803,21 +828,47 @@ inline void sort_small_setup() {
 constexpr uint64_t kRsBigN = 1ull << 22;
 
 struct SortScratch {
-  uint32_t* ghist;              // kRsMaxPass * 1024, zeroed
-  unsigned long long* status;   // lb_tiles(n) * 1024
+  uint32_t* ghist;              // kRsMaxPass * kRsMaxDigits, zeroed
+  unsigned long long* status;   // lb_tiles(n) * kRsMaxDigits
   uint32_t* ctrs;               // one zeroed counter per pass
 };
 
-template <class K>
+template <class K, int RB>
 inline void rs_setup() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(k_rs_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RsSmem<K>));
+    cudaFuncSetAttribute(k_rs_onesweep<K, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(RsSmem<K, RB>));
     done = true;
   }
 }
 
-inline int rs_passes(int nbits) { return (nbits + kRsBits - 1) / kRsBits; }
+// digit width of the one-sweep sort: 9 bits when that takes fewer passes
+inline int rs_digit_bits(int nbits) { return (nbits + 8) / 9 < (nbits + 7) / 8 ? 9 : 8; }
+inline int rs_passes(int nbits) {
+  const int rb = rs_digit_bits(nbits);
+  return (nbits + rb - 1) / rb;
+}
+
+template <class K, int RB>
+bool radix_sort_rb(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint64_t n, int npass, SortScratch sc,
+                   uint32_t epoch, cudaStream_t st) {
+  rs_setup<K, RB>();
+  const uint64_t nt = lb_tiles(n);
+  GW_LAUNCH((k_rs_ghist<K, RB>), (unsigned)std::min<uint64_t>(nt, 148ull * 8), kThreads, 0, st, keys, n, npass,
+            sc.ghist);
+  bool alt = false;
+  for (int p = 0; p < npass; p++) {
+    const K* ki = alt ? keys_alt : keys;
+    const uint32_t* vi = alt ? vals_alt : vals;
+    K* ko = alt ? keys : keys_alt;
+    uint32_t* vo = alt ? vals : vals_alt;
+    GW_LAUNCH((k_rs_onesweep<K, RB>), (unsigned)nt, kThreads, sizeof(RsSmem<K, RB>), st, ki, vi, ko, vo, n, p,
+              sc.ghist, sc.status, sc.ctrs + p, epoch + (uint32_t)p);
+    alt = !alt;
+  }
+  return alt;
+}
 
 // Sorts (keys, vals) by key bits [0, nbits); returns true if the result is in
 // the alternate buffers.  ghist must be zeroed by the caller.
@@ -825,21 +876,9 @@ template <class K>
 bool radix_sort(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uint64_t n, int nbits, SortScratch sc,
                 uint32_t epoch, cudaStream_t st) {
   if (n <= 1 || nbits <= 0) return false;
-  rs_setup<K>();
   const int npass = rs_passes(nbits);
-  const uint64_t nt = lb_tiles(n);
-  GW_LAUNCH((k_rs_ghist<K>), (unsigned)std::min<uint64_t>(nt, 148ull * 8), kThreads, 0, st, keys, n, npass, sc.ghist);
-  bool alt = false;
-  for (int p = 0; p < npass; p++) {
-    const K* ki = alt ? keys_alt : keys;
-    const uint32_t* vi = alt ? vals_alt : vals;
-    K* ko = alt ? keys : keys_alt;
-    uint32_t* vo = alt ? vals : vals_alt;
-    GW_LAUNCH((k_rs_onesweep<K>), (unsigned)nt, kThreads, sizeof(RsSmem<K>), st, ki, vi, ko, vo, n, p, sc.ghist,
-              sc.status, sc.ctrs + p, epoch + (uint32_t)p);
-    alt = !alt;
-  }
-  return alt;
+  if (rs_digit_bits(nbits) == 9) return radix_sort_rb<K, 9>(keys, keys_alt, vals, vals_alt, n, npass, sc, epoch, st);
+  return radix_sort_rb<K, 8>(keys, keys_alt, vals, vals_alt, n, npass, sc, epoch, st);
 }
 
 }  // namespace gw
