@@ -268,6 +268,9 @@ static_assert(kRsDigits == kThreads, "one digit per thread");
 // RB-bit digits (RB = 8 or 9; 9 saves a pass when it covers the key in
 // fewer passes, e.g. 17-bit keys in 2 instead of 3); DPT digits per thread.
 constexpr int kRsMaxDigits = 512;
+#ifndef GW_RS_LOOKBACK
+#define GW_RS_LOOKBACK 16  // status words in flight per thread in the one-sweep look-back
+#endif
 template <int RB>
 struct RsDig {
   static constexpr int ND = 1 << RB;
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
   __syncthreads();
   {
     // thread t owns digits t*DPT .. t*DPT+DPT-1: per-warp offsets, tile
-    // counts, look-back, global bases
+    // counts, tile-local digit starts; the aggregates are published first
     const unsigned long long EP = (unsigned long long)epoch << 40;
     uint32_t c[DPT], g[DPT];
     uint32_t csum = 0, gsum = 0;
@@ -383,53 +386,79 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
     uint32_t cex = block_excl_scan<uint32_t, OpSum>(csum, OpSum(), 0u, &ct);
 #pragma unroll
     for (int j = 0; j < DPT; j++) {
-      const int d = threadIdx.x * DPT + j;
-      S.toff[d] = cex;
+      S.toff[threadIdx.x * DPT + j] = cex;
       cex += c[j];
-      unsigned long long pre = 0;
-      if (tile > 0) {
-        // up to 8 predecessors per round trip: sum their aggregates back to the
-        // nearest inclusive prefix (all of them must have published)
-        constexpr int B8 = 8;
-        int64_t p = (int64_t)tile - 1;
-        while (true) {
-          unsigned long long w8[B8];
-#pragma unroll
-          for (int k = 0; k < B8; k++)
-            w8[k] = p - k >= 0 ? ld_volatile_u64(&status[(uint64_t)(p - k) * ND + d]) : (EP | (2ull << 38));
-          int lim = B8;
-          bool ready = true;
-#pragma unroll
-          for (int k = 0; k < B8; k++) {
-            if (lim == B8) {
-              if ((w8[k] >> 40) != epoch) { ready = false; lim = -1; }
-              else if (((w8[k] >> 38) & 3ull) == 2ull) lim = k;
-            }
-          }
-          if (!ready) continue;  // a predecessor before the nearest inclusive has not published yet
-          unsigned long long add = 0;
-#pragma unroll
-          for (int k = 0; k < B8; k++)
-            if (k <= lim) add += w8[k] & ((1ull << 38) - 1);
-          pre += add;
-          if (lim < B8) break;
-          p -= B8;
-        }
-        atomicExch(&status[(uint64_t)tile * ND + d], EP | (2ull << 38) | (pre + c[j]));
-      }
-      S.gbase[d] = gex + (uint32_t)pre;
-      gex += g[j];
     }
-  }
-  __syncthreads();
-  // stage in digit order
+    __syncthreads();
+    // stage in digit order while the predecessors publish (the look-back
+    // below only needs the global bases)
 #pragma unroll
-  for (int r = 0; r < kRsRounds; r++) {
-    const uint32_t d = rd[r] >> 16;
-    if (d < (uint32_t)ND) {
-      const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
-      S.sk[pos] = kk[r];
-      S.sv[pos] = vv[r];
+    for (int r = 0; r < kRsRounds; r++) {
+      const uint32_t d = rd[r] >> 16;
+      if (d < (uint32_t)ND) {
+        const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
+        S.sk[pos] = kk[r];
+        S.sv[pos] = vv[r];
+      }
+    }
+    // look-back for all DPT digits at once, LBW predecessors per digit per
+    // round trip: sum their aggregates back to the nearest inclusive prefix
+    // (all of them must have published)
+    constexpr int LBW = GW_RS_LOOKBACK / DPT;
+    unsigned long long pre[DPT];
+    int64_t p[DPT];
+    bool done[DPT];
+#pragma unroll
+    for (int j = 0; j < DPT; j++) {
+      pre[j] = 0;
+      p[j] = (int64_t)tile - 1;
+      done[j] = tile == 0;
+    }
+    while (true) {
+      bool all = true;
+#pragma unroll
+      for (int j = 0; j < DPT; j++) all = all && done[j];
+      if (all) break;
+      unsigned long long wv[DPT][LBW];
+#pragma unroll
+      for (int j = 0; j < DPT; j++) {
+        const int d = threadIdx.x * DPT + j;
+#pragma unroll
+        for (int k = 0; k < LBW; k++)
+          wv[j][k] = (!done[j] && p[j] - k >= 0) ? ld_volatile_u64(&status[(uint64_t)(p[j] - k) * ND + d])
+                                                 : (EP | (2ull << 38));
+      }
+#pragma unroll
+      for (int j = 0; j < DPT; j++) {
+        if (done[j]) continue;
+        int lim = LBW;
+        bool ready = true;
+#pragma unroll
+        for (int k = 0; k < LBW; k++) {
+          if (lim == LBW) {
+            if ((wv[j][k] >> 40) != epoch) { ready = false; lim = -1; }
+            else if (((wv[j][k] >> 38) & 3ull) == 2ull) lim = k;
+          }
+        }
+        if (!ready) continue;  // a predecessor before the nearest inclusive has not published yet
+        unsigned long long add = 0;
+#pragma unroll
+        for (int k = 0; k < LBW; k++)
+          if (k <= lim) add += wv[j][k] & ((1ull << 38) - 1);
+        pre[j] += add;
+        if (lim < LBW) {  // publish the inclusive prefix at once: successors stop here
+          done[j] = true;
+          atomicExch(&status[(uint64_t)tile * ND + threadIdx.x * DPT + j], EP | (2ull << 38) | (pre[j] + c[j]));
+        } else {
+          p[j] -= LBW;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < DPT; j++) {
+      const int d = threadIdx.x * DPT + j;
+      S.gbase[d] = gex + (uint32_t)pre[j];
+      gex += g[j];
     }
   }
   __syncthreads();
