@@ -307,7 +307,7 @@ struct Pipeline {
     sc.ghist = zeroed(kRsMaxPass * kRsMaxDigits);
     sc.ctrs = zeroed(npass);
     sc.status = C->get<unsigned long long>(std::string("rs_status") + sfx,
-                                           std::max(lb_tiles(n), lb_tiles(tr.n)) * kRsMaxDigits);
+                                           2 * std::max(lb_tiles(n), lb_tiles(tr.n)) * kRsMaxDigits);
     bool alt = radix_sort<K>(keys, ka, vals, va, n, nbits, sc, take_epochs(npass), st);
     if (alt) {
       keys = ka;
@@ -428,7 +428,7 @@ struct Pipeline {
     CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
     if (gmode) {  // fixed epochs in the graph: start from clean flags
       for (const char* nm : {"rs_status", "rs_status_b"}) {
-        unsigned long long* rs = C->get<unsigned long long>(nm, lb_tiles(N) * kRsMaxDigits);
+        unsigned long long* rs = C->get<unsigned long long>(nm, 2 * lb_tiles(N) * kRsMaxDigits);
         CK(cudaMemsetAsync(rs, 0, C->bufs[nm].cap, st));
       }
     }

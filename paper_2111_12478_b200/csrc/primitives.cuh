@@ -305,9 +305,23 @@ struct RsSmem {
   uint32_t tile;
 };
 
+// Staging slot of tile position p (digit order).  With ~16 keys per digit the
+// digit runs of one warp store start 16 slots apart, which put a whole warp on
+// two banks (u32; one bank pair for u64); XOR-swizzling the slot within its
+// 32-bank row spreads them over all banks.  Consecutive positions stay in one
+// row, so the write-out reads remain conflict-free.
+template <class K>
+__device__ __forceinline__ uint32_t stg(uint32_t p) {
+  if constexpr (sizeof(K) == 8) return p ^ ((p >> 4) & 15u);
+  else return p ^ ((p >> 5) & 31u);
+}
+
 // lanes with the same digit (NB low bits of d) among the warp's lanes
 template <int NB>
 __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
+#ifdef GW_RS_MATCH
+  return __match_any_sync(0xffffffffu, d);
+#endif
   uint32_t peers = 0xffffffffu;
 #pragma unroll
   for (int b = 0; b < NB; b++) {
@@ -376,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
         run += t;
       }
       c[j] = run;
-      atomicExch(&status[(uint64_t)tile * ND + d], EP | ((tile == 0 ? 2ull : 1ull) << 38) | run);
+      atomicExch(&status[(uint64_t)tile * ND + d], EP | (1ull << 38) | run);
       g[j] = ghist[pass * ND + d];
       csum += run;
       gsum += g[j];
@@ -397,63 +411,57 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
       const uint32_t d = rd[r] >> 16;
       if (d < (uint32_t)ND) {
         const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
-        S.sk[pos] = kk[r];
-        S.sv[pos] = vv[r];
+        S.sk[stg<K>(pos)] = kk[r];
+        S.sv[stg<K>(pos)] = vv[r];
       }
     }
-    // look-back for all DPT digits at once, LBW predecessors per digit per
-    // round trip: sum their aggregates back to the nearest inclusive prefix
-    // (all of them must have published)
+    // Two-level look-back (no chain through every predecessor): the tiles
+    // form groups of GS = 2^(floor(log2(tiles)/2)) consecutive tiles; the last
+    // tile of a group publishes the group's total.  A tile's exclusive prefix
+    // = the aggregates of its group's earlier tiles + the totals of the
+    // earlier groups, at most ~2 sqrt(tiles) loads per digit, LBW per digit
+    // per round trip.  Every wait is for a lower tile index (tile indices are
+    // taken in launch order), so it cannot deadlock.
     constexpr int LBW = GW_RS_LOOKBACK / DPT;
+    const uint32_t ntiles = (uint32_t)((n + kTile - 1) / kTile);
+    const uint32_t gsh = (32u - __clz(ntiles > 1 ? ntiles - 1 : 1u)) >> 1;
+    const uint32_t grp = tile >> gsh, gfirst = grp << gsh;
+    unsigned long long* gstat = status + (uint64_t)ntiles * ND;
     unsigned long long pre[DPT];
-    int64_t p[DPT];
-    bool done[DPT];
 #pragma unroll
-    for (int j = 0; j < DPT; j++) {
-      pre[j] = 0;
-      p[j] = (int64_t)tile - 1;
-      done[j] = tile == 0;
-    }
-    while (true) {
-      bool all = true;
+    for (int j = 0; j < DPT; j++) pre[j] = 0;
+    // sums src[(q0 + k) * ND + d] over q in [q0, q1) into pre[], waiting for every entry
+    auto gather = [&](const unsigned long long* src, uint32_t q0, uint32_t q1) {
+      for (uint32_t qb = q0; qb < q1; qb += LBW) {
+        unsigned long long wv[DPT][LBW];
+        bool ok;
+        do {
 #pragma unroll
-      for (int j = 0; j < DPT; j++) all = all && done[j];
-      if (all) break;
-      unsigned long long wv[DPT][LBW];
+          for (int j = 0; j < DPT; j++) {
+            const int d = threadIdx.x * DPT + j;
 #pragma unroll
-      for (int j = 0; j < DPT; j++) {
-        const int d = threadIdx.x * DPT + j;
-#pragma unroll
-        for (int k = 0; k < LBW; k++)
-          wv[j][k] = (!done[j] && p[j] - k >= 0) ? ld_volatile_u64(&status[(uint64_t)(p[j] - k) * ND + d])
-                                                 : (EP | (2ull << 38));
-      }
-#pragma unroll
-      for (int j = 0; j < DPT; j++) {
-        if (done[j]) continue;
-        int lim = LBW;
-        bool ready = true;
-#pragma unroll
-        for (int k = 0; k < LBW; k++) {
-          if (lim == LBW) {
-            if ((wv[j][k] >> 40) != epoch) { ready = false; lim = -1; }
-            else if (((wv[j][k] >> 38) & 3ull) == 2ull) lim = k;
+            for (int k = 0; k < LBW; k++)
+              wv[j][k] = qb + k < q1 ? ld_volatile_u64(&src[(uint64_t)(qb + k) * ND + d]) : EP;
           }
-        }
-        if (!ready) continue;  // a predecessor before the nearest inclusive has not published yet
-        unsigned long long add = 0;
+          ok = true;
 #pragma unroll
-        for (int k = 0; k < LBW; k++)
-          if (k <= lim) add += wv[j][k] & ((1ull << 38) - 1);
-        pre[j] += add;
-        if (lim < LBW) {  // publish the inclusive prefix at once: successors stop here
-          done[j] = true;
-          atomicExch(&status[(uint64_t)tile * ND + threadIdx.x * DPT + j], EP | (2ull << 38) | (pre[j] + c[j]));
-        } else {
-          p[j] -= LBW;
-        }
+          for (int j = 0; j < DPT; j++)
+#pragma unroll
+            for (int k = 0; k < LBW; k++) ok = ok && (wv[j][k] >> 40) == epoch;
+        } while (!ok);
+#pragma unroll
+        for (int j = 0; j < DPT; j++)
+#pragma unroll
+          for (int k = 0; k < LBW; k++) pre[j] += wv[j][k] & ((1ull << 38) - 1);
       }
+    };
+    gather(status, gfirst, tile);
+    if (tile - gfirst == (1u << gsh) - 1u) {  // last tile of its group: the group total
+#pragma unroll
+      for (int j = 0; j < DPT; j++)
+        atomicExch(&gstat[(uint64_t)grp * ND + threadIdx.x * DPT + j], EP | (1ull << 38) | (pre[j] + c[j]));
     }
+    gather(gstat, 0, grp);
 #pragma unroll
     for (int j = 0; j < DPT; j++) {
       const int d = threadIdx.x * DPT + j;
@@ -467,11 +475,11 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
   const uint32_t cnt = rem < (uint64_t)kTile ? (uint32_t)rem : (uint32_t)kTile;
 #pragma unroll 4
   for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-    const K k = S.sk[i];
+    const K k = S.sk[stg<K>(i)];
     const uint32_t d = (uint32_t)(k >> shift) & (ND - 1);
     const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
     kout[gp] = k;
-    vout[gp] = S.sv[i];
+    vout[gp] = S.sv[stg<K>(i)];
   }
 }
 
@@ -610,8 +618,8 @@ __global__ void __launch_bounds__(kThreads, (RB == 8 && sizeof(K) == 4) ? 3 : 2)
         const uint32_t d = rd[r] >> 16;
         if (d < (uint32_t)ND) {
           const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
-          S.sk[pos] = kk[r];
-          S.sv[pos] = vv[r];
+          S.sk[stg<K>(pos)] = kk[r];
+          S.sv[stg<K>(pos)] = vv[r];
         }
       }
       __syncthreads();
@@ -619,11 +627,11 @@ __global__ void __launch_bounds__(kThreads, (RB == 8 && sizeof(K) == 4) ? 3 : 2)
       const uint32_t cnt = rem < (uint64_t)kTile ? (uint32_t)rem : (uint32_t)kTile;
 #pragma unroll 4
       for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-        const K k = S.sk[i];
+        const K k = S.sk[stg<K>(i)];
         const uint32_t d = (uint32_t)(k >> shift) & (ND - 1);
         const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
         kout[gp] = k;
-        vout[gp] = S.sv[i];
+        vout[gp] = S.sv[stg<K>(i)];
       }
       __syncthreads();
       // advance the bases past this tile's runs
@@ -764,8 +772,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tm
       const uint32_t d = rd[r] >> 16;
       if (d < (uint32_t)ND) {
         const uint32_t pos = S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu);
-        S.ik[b][pos] = kk[r];
-        S.iv[b][pos] = vv[r];
+        S.ik[b][stg<K>(pos)] = kk[r];
+        S.iv[b][stg<K>(pos)] = vv[r];
       }
     }
     __syncthreads();
@@ -773,11 +781,11 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tm
     const uint32_t cnt = rem < (uint64_t)kTile ? (uint32_t)rem : (uint32_t)kTile;
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
-      const K k = S.ik[b][i];
+      const K k = S.ik[b][stg<K>(i)];
       const uint32_t d = (uint32_t)(k >> shift) & (ND - 1);
       const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
       kout[gp] = k;
-      vout[gp] = S.iv[b][i];
+      vout[gp] = S.iv[b][stg<K>(i)];
     }
     __syncthreads();  // buffer b free for the TMA of tile it + 2
   }
@@ -858,7 +866,7 @@ constexpr uint64_t kRsBigN = 1ull << 22;
 
 struct SortScratch {
   uint32_t* ghist;              // kRsMaxPass * kRsMaxDigits, zeroed
-  unsigned long long* status;   // lb_tiles(n) * kRsMaxDigits
+  unsigned long long* status;   // 2 * lb_tiles(n) * kRsMaxDigits (tile aggregates, then group totals)
   uint32_t* ctrs;               // one zeroed counter per pass
 };
 
