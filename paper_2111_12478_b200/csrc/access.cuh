@@ -422,7 +422,7 @@ __device__ __forceinline__ uint32_t acc_clock(const AccArgs<K>& a, uint32_t vo, 
 
 template <class K>
 __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   AccSmem<K>& S = *reinterpret_cast<AccSmem<K>*>(smem_raw);
   const uint32_t BS = a.tr.BS;
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
@@ -861,9 +861,10 @@ __global__ void k_dedup_keys32(DedupArgs d, uint32_t n_events, uint32_t* sk, uin
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(nsurv, (uint32_t)__popc(m));
   }
 }
-// small traces: counting sort of the survivors by event (count, scan over
-// the events, placement with self-cleaning counters)
-__global__ void k_surv_count(DedupArgs d, uint32_t* ccnt, uint32_t* nsurv) {
+// small traces: counting sort of the survivors by event bucket (event >> cs:
+// count, scan over the buckets, placement with self-cleaning counters); each
+// bucket's run is then ordered by the full order key (k_group_fix)
+__global__ void k_surv_count(DedupArgs d, uint32_t* ccnt, uint32_t* nsurv, uint32_t cs) {
   const uint32_t nc = dd_count(d);
   for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < d.ncand; k0 += gridDim.x * blockDim.x) {
     const uint32_t k = k0 + threadIdx.x;
@@ -871,18 +872,19 @@ __global__ void k_surv_count(DedupArgs d, uint32_t* ccnt, uint32_t* nsurv) {
     if (k < nc) {
       const unsigned long long ok = d.c.okey[k];
       surv = ok == d.smin[d.cslot[k]];
-      if (surv) atomicAdd(ccnt + (ok >> 32), 1u);
+      if (surv) atomicAdd(ccnt + ((ok >> 32) >> cs), 1u);
     }
     const uint32_t m = __ballot_sync(0xffffffffu, surv);
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(nsurv, (uint32_t)__popc(m));
   }
 }
-__global__ void k_surv_place(DedupArgs d, uint32_t* ccnt, const uint32_t* coff, uint32_t* sk, uint32_t* sv) {
+__global__ void k_surv_place(DedupArgs d, uint32_t* ccnt, const uint32_t* coff, uint32_t* sk, uint32_t* sv,
+                             uint32_t cs) {
   const uint32_t nc = dd_count(d);
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
     const unsigned long long ok = d.c.okey[k];
     if (ok == d.smin[d.cslot[k]]) {
-      const uint32_t c = (uint32_t)(ok >> 32);
+      const uint32_t c = (uint32_t)(ok >> 32) >> cs;
       const uint32_t pos = coff[c] + atomicSub(ccnt + c, 1u) - 1u;  // leaves ccnt zeroed
       sk[pos] = c;
       sv[pos] = k;

@@ -285,6 +285,15 @@ struct Pipeline {
       explicit Tag(const char* t) { if (g_prof) g_prof->tag = t; }
       ~Tag() { if (g_prof) g_prof->tag = nullptr; }
     } tag_guard(tag);
+    if (distinct && n <= kRankSortMax) {
+      K* ka = C->get<K>(std::string(tag) + "_ka", n);
+      uint32_t* va = C->get<uint32_t>(std::string(tag) + "_va", n);
+      GW_LAUNCH(k_sort_rank<K>, (unsigned)((n + kThreads - 1) / kThreads), kThreads, 0, st, keys, vals, ka, va,
+                (uint32_t)n);
+      keys = ka;
+      vals = va;
+      return;
+    }
     if (distinct && n <= small_sort_max<K>()) {
       // one CTA, in shared memory (distinct keys: stability is moot)
       uint32_t p2 = 1;
@@ -432,6 +441,15 @@ struct Pipeline {
         CK(cudaMemsetAsync(rs, 0, C->bufs[nm].cap, st));
       }
     }
+    // graph replays of a lock-free plan: the location sort needs only the
+    // plan's key runs, so its branch forks before k_prep (the plan check
+    // still guards the results: a mismatch re-runs eagerly)
+    const bool early_fork = gmode && nshard <= 1 && !g_prof;
+    if (early_fork) {
+      memset(&hs, 0, sizeof hs);
+      hs.key_or = P->D;
+      fork_sort();
+    }
     Stats* dst = C->get<Stats>("stats", 1);
     GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
     GW_LAUNCH(k_prep, grid_for(N), kThreads, 0, st, tr, dst);
@@ -511,25 +529,7 @@ struct Pipeline {
       // the location sort does not depend on the sync pass: it runs on the
       // side stream while the walker runs here; the stamps (aux) are filled
       // after the walker, then the branches join before the check
-      if (!C->side) {
-        CK(cudaStreamCreateWithFlags(&C->side, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&C->ev_fork, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming));
-      }
-      const cudaStream_t main_st = st;
-      aux = C->get<uint4>("acc_aux", N);  // allocated (and zeroed) on this stream: k_acc_aux writes it here
-      CK(cudaEventRecord(C->ev_fork, main_st));
-      CK(cudaStreamWaitEvent(C->side, C->ev_fork, 0));
-      st = C->side;
-      C->last_stream = st;
-      sfx = "_b";
-      pbeg(PH_SORT);
-      access_sort(true);
-      pend(PH_SORT);
-      CK(cudaEventRecord(C->ev_join, st));
-      st = main_st;
-      C->last_stream = st;
-      sfx.clear();
+      if (!early_fork) fork_sort();
       pbeg(PH_WALKER);
       walker_phase();
       GW_LAUNCH(k_acc_aux, grid_for(N), kThreads, 0, st, tr, stamps, aux);
@@ -593,15 +593,18 @@ struct Pipeline {
       unsigned long long* sk = C->get<unsigned long long>("sv_k", ncap);
       uint32_t* sv = C->get<uint32_t>("sv_v", ncap);
       if (N <= (1ull << 25) && ncap > small_sort_max<unsigned long long>()) {
-        // small trace: counting sort by event over the N events, then each run by order key
+        // small trace: counting sort by event bucket (event >> cs, <= 16 events per
+        // bucket, about one bucket per candidate), then each run by order key
+        const int cs = std::min(4, std::max(0, ceil_log2(N) - ceil_log2((uint64_t)ncap)));
+        const uint64_t nb = ((N - 1) >> cs) + 1;
         uint32_t* sk32 = C->get<uint32_t>("sv_k32", ncap);
-        uint32_t* ccnt = C->get<uint32_t>("sv_cnt", N);
-        uint32_t* coff = C->get<uint32_t>("sv_off", N);
-        CK(cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * N, st));
-        GW_LAUNCH(k_surv_count, grid_for(ncap), kThreads, 0, st, d, ccnt, d_nsurv);
-        scan<uint32_t, OpSum>(ArrLoad<uint32_t>{ccnt}, ArrStore<uint32_t>{coff}, N, OpSum(), 0u, false, "sc_u32");
-        GW_LAUNCH(k_surv_place, grid_for(ncap), kThreads, 0, st, d, ccnt, coff, sk32, sv);
-        GW_LAUNCH(k_group_fix, grid_for(ncap), kThreads, 0, st, sk32, sv, (uint32_t)ncap, (uint32_t)N, cd.okey,
+        uint32_t* ccnt = C->get<uint32_t>("sv_cnt", nb);
+        uint32_t* coff = C->get<uint32_t>("sv_off", nb);
+        CK(cudaMemsetAsync(ccnt, 0, sizeof(uint32_t) * nb, st));
+        GW_LAUNCH(k_surv_count, grid_for(ncap), kThreads, 0, st, d, ccnt, d_nsurv, (uint32_t)cs);
+        scan<uint32_t, OpSum>(ArrLoad<uint32_t>{ccnt}, ArrStore<uint32_t>{coff}, nb, OpSum(), 0u, false, "sc_u32");
+        GW_LAUNCH(k_surv_place, grid_for(ncap), kThreads, 0, st, d, ccnt, coff, sk32, sv, (uint32_t)cs);
+        GW_LAUNCH(k_group_fix, grid_for(ncap), kThreads, 0, st, sk32, sv, (uint32_t)ncap, (uint32_t)nb, cd.okey,
                   d_nsurv);
       } else if (ncap <= small_sort_max<unsigned long long>()) {
         GW_LAUNCH(k_dedup_keys, grid_for(ncap), kThreads, 0, st, d, (unsigned long long)N, sk, sv, d_nsurv);
@@ -630,6 +633,29 @@ struct Pipeline {
     S.n_sync = hs.n_acq + hs.n_rel + hs.n_end + hs.n_bar;
     C->launches = g_launches;
     C->stats_pending = !gmode;
+  }
+
+  // the access sort on the side stream (joined through ev_join before the check)
+  void fork_sort() {
+    if (!C->side) {
+      CK(cudaStreamCreateWithFlags(&C->side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&C->ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming));
+    }
+    const cudaStream_t main_st = st;
+    aux = C->get<uint4>("acc_aux", tr.n);  // allocated (and zeroed) on this stream: k_acc_aux writes it here
+    CK(cudaEventRecord(C->ev_fork, main_st));
+    CK(cudaStreamWaitEvent(C->side, C->ev_fork, 0));
+    st = C->side;
+    C->last_stream = st;
+    sfx = "_b";
+    pbeg(PH_SORT);
+    access_sort(true);
+    pend(PH_SORT);
+    CK(cudaEventRecord(C->ev_join, st));
+    st = main_st;
+    C->last_stream = st;
+    sfx.clear();
   }
 
   // ---- pipeline state shared by the phases --------------------------------
@@ -857,7 +883,7 @@ struct Pipeline {
   // (u != t, !cover) and leave the clock comparison to the walker's queries.
   // Counts at scal[slot] (candidates) and scal[slot + 1] (large windows).
   Cands check_pass(bool defer, const char* tag, int slot) {
-    const uint64_t N = tr.n, NA = na_sorted;
+    const uint64_t NA = na_sorted;
     uint32_t* cnt = scal + slot;
     uint32_t* large_i = C->get<uint32_t>("lg_i", NA / kSmallWin + 1);
     uint32_t* large_ws = C->get<uint32_t>("lg_ws", NA / kSmallWin + 1);

@@ -319,9 +319,6 @@ __device__ __forceinline__ uint32_t stg(uint32_t p) {
 // lanes with the same digit (NB low bits of d) among the warp's lanes
 template <int NB>
 __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
-#ifdef GW_RS_MATCH
-  return __match_any_sync(0xffffffffu, d);
-#endif
   uint32_t peers = 0xffffffffu;
 #pragma unroll
   for (int b = 0; b < NB; b++) {
@@ -338,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_oneswee
                                                             uint64_t n, int pass, const uint32_t* __restrict__ ghist,
                                                             unsigned long long* status, uint32_t* ctr, uint32_t epoch) {
   constexpr int ND = RsDig<RB>::ND, DPT = RsDig<RB>::DPT;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   RsSmem<K, RB>& S = *reinterpret_cast<RsSmem<K, RB>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int shift = RB * pass;
@@ -550,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, (RB == 8 && sizeof(K) == 4) ? 3 : 2)
                                                        K* __restrict__ kout, uint32_t* __restrict__ vout, uint64_t n,
                                                        int shift, const uint32_t* __restrict__ offsets, uint64_t nst) {
   constexpr int ND = RsBig<RB>::ND, DPT = RsBig<RB>::DPT, ST = RsBig<RB>::ST;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   RsBigSmem<K, RB>& S = *reinterpret_cast<RsBigSmem<K, RB>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = lanemask_lt();
@@ -822,7 +819,7 @@ template <class K>
 constexpr uint32_t small_sort_max() { return sizeof(K) == 8 ? 16384u : 16384u; }
 template <class K>
 __global__ void __launch_bounds__(kSmallThreads) k_sort_small(K* keys, uint32_t* vals, uint32_t n, uint32_t p2) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   K* sk = reinterpret_cast<K*>(smem_raw);
   uint32_t* sv = reinterpret_cast<uint32_t*>(sk + p2);
   for (uint32_t i = threadIdx.x; i < p2; i += kSmallThreads) {
@@ -851,6 +848,34 @@ __global__ void __launch_bounds__(kSmallThreads) k_sort_small(K* keys, uint32_t*
     vals[i] = sv[i];
   }
 }
+// tiny sorts of distinct keys (n <= kRankSortMax): every thread ranks one key
+// against all n keys staged in shared memory (broadcast reads) and writes it
+// to its rank -- a few microseconds instead of a bitonic network's ~45
+// CTA-wide barriers.  Not in place: writes (ko, vo).
+constexpr uint32_t kRankSortMax = 2048;
+template <class K>
+__global__ void __launch_bounds__(kThreads) k_sort_rank(const K* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                       K* __restrict__ ko, uint32_t* __restrict__ vo, uint32_t n) {
+  __shared__ K sk[kRankSortMax];
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads) sk[i] = keys[i];
+  __syncthreads();
+  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  const K k = sk[i];
+  uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+  uint32_t j = 0;
+  for (; j + 4 <= n; j += 4) {
+    r0 += sk[j] < k;
+    r1 += sk[j + 1] < k;
+    r2 += sk[j + 2] < k;
+    r3 += sk[j + 3] < k;
+  }
+  for (; j < n; j++) r0 += sk[j] < k;
+  const uint32_t r = r0 + r1 + r2 + r3;
+  ko[r] = k;
+  vo[r] = vals[i];
+}
+
 template <class K>
 inline void sort_small_setup() {
   static bool done = false;

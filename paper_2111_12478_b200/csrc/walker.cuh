@@ -1064,8 +1064,6 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   const uint32_t t = ev_tid(to);
   const uint32_t vt = vidx(a, t);
   const uint32_t cur = (to & GW_F_DEVICE) ? SC_DEV : t / a.tr.BS;
-  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * n;
-  uint32_t* H = P + n;
   __shared__ LockEnt* s_lk;
   __shared__ DrainOut s_dr;
   __shared__ CapList s_cap;
@@ -1077,8 +1075,6 @@ __device__ void do_acquire(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   }
   __syncthreads();
   if (!s_lk) { if (threadIdx.x == 0) atomicOr(a.err, ERR_INTERNAL); tickets_release(a, e); return; }
-  int pch = 0, hch = 0;
-  bool mat = false;
   // (1) drain: scans until done, applying the collected joins in between when a scan fills up
   bool first = true;
   while (!a.hb_mode) {  // scoped HB (hb.py:59-72) has no queues
@@ -1221,8 +1217,6 @@ __device__ void do_release(const WalkArgs& a, uint32_t e, uint32_t to, unsigned 
   const uint32_t inst = s_f.scope;
   // (1) drain into pred
   bool first = true;
-  bool mat = false;
-  int pch = 0, hch = 0;
   while (!a.hb_mode) {
     drain_scan(a, t, lock, inst, s_dr, first, nullptr);
     first = false;
@@ -1309,7 +1303,6 @@ __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsig
   const uint32_t t = ev_tid(to);
   const uint32_t vt = vidx(a, t);
   const uint32_t isw = ev_kind(to) == GW_K_WRITE;
-  uint32_t* P = a.scratch + (size_t)blockIdx.x * 3 * n;
   __shared__ CapList s_cap;
   __shared__ uint32_t s_done;
   __shared__ uint32_t s_fi, s_ii, s_phase;
@@ -1318,8 +1311,7 @@ __device__ void do_incs_access(const WalkArgs& a, uint32_t e, uint32_t to, unsig
   const uint32_t depth = a.depth[t];
   if (threadIdx.x == 0) { s_cap.n = 0; s_cap.full = 0; s_fi = 0; s_ii = NIL; s_phase = 0; }
   __syncthreads();
-  int pch = 0, hch = 0;
-  bool mat = false, released = false;
+  bool released = false;
   // frames x released instances of the frame's lock overlapping the frame's
   // instance x {cs_write, cs_read if this is a write}; HB has no cs clocks
   while (!a.hb_mode) {

@@ -660,7 +660,10 @@ __device__ void w_barrier_warp(const WalkArgs& a, uint32_t to, uint32_t ins, WSm
 
 // Events of list (CTA, warp j) -- partition key cta * kLW + j, trace order --
 // merged with the CTA's block-barrier list (bb_*).
-__global__ void __launch_bounds__(kThreads, 4) k_walker_lw(WalkArgs a, const uint32_t* bb_ev, const uint32_t* bb_beg,
+#ifndef GW_LW_MINB
+#define GW_LW_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, GW_LW_MINB) k_walker_lw(WalkArgs a, const uint32_t* bb_ev, const uint32_t* bb_beg,
                                                         const uint32_t* bb_end) {
   __shared__ WSm SW[kLW];
   __shared__ __align__(16) uint32_t s_acc[kAccSmem];
