@@ -274,29 +274,45 @@ def validate(cfg, key, tidop, instr):
     return out
 
 
+class _ResultOwner:
+    """Frees a gw_result when the last array viewing it is collected."""
+
+    def __init__(self, L, r: _Result):
+        self._L, self._r = L, r
+
+    def __del__(self):
+        try:
+            self._L.gw_result_free(C.byref(self._r))
+        except Exception:  # interpreter shutdown
+            pass
+
+
 def _take_result(L, r: _Result):
-    try:
-        n = int(r.n_reports)
-        nd = int(r.n_diags)
+    """Zero-copy: the result arrays are numpy views of the library-owned
+    buffers (freed with gw_result_free once every view is gone), so a large
+    report list is copied once (mapped host staging -> result) rather than
+    twice."""
+    owner = _ResultOwner(L, r)
+    n = int(r.n_reports)
+    nd = int(r.n_diags)
 
-        def arr(p, count, dt):
-            out = np.empty(count, dtype=dt)
-            if count:
-                C.memmove(out.ctypes.data, p, out.nbytes)
-            return out
+    def arr(p, count, dt):
+        if not count:
+            return np.empty(0, dtype=dt)
+        nbytes = count * np.dtype(dt).itemsize
+        buf = (C.c_char * nbytes).from_address(C.cast(p, C.c_void_p).value)
+        buf._owner = owner
+        return np.frombuffer(buf, dtype=dt)
 
-        res = {
-            "kind": arr(r.kind, n, np.uint8),
-            "prior": arr(r.prior_event, n, np.uint32),
-            "current": arr(r.current_event, n, np.uint32),
-            "diag_event": arr(r.diag_event, nd, np.uint32),
-            "diag_code": arr(r.diag_code, nd, np.uint32),
-            "diag_lock": arr(r.diag_lock, nd, np.uint64),
-            "order_key": arr(r.order_key, n, np.uint64),
-        }
-    finally:
-        L.gw_result_free(C.byref(r))
-    return res
+    return {
+        "kind": arr(r.kind, n, np.uint8),
+        "prior": arr(r.prior_event, n, np.uint32),
+        "current": arr(r.current_event, n, np.uint32),
+        "diag_event": arr(r.diag_event, nd, np.uint32),
+        "diag_code": arr(r.diag_code, nd, np.uint32),
+        "diag_lock": arr(r.diag_lock, nd, np.uint64),
+        "order_key": arr(r.order_key, n, np.uint64),
+    }
 
 
 class Context:

@@ -15,6 +15,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "access.cuh"
@@ -444,7 +445,9 @@ struct Pipeline {
     // graph replays of a lock-free plan: the location sort needs only the
     // plan's key runs, so its branch forks before k_prep (the plan check
     // still guards the results: a mismatch re-runs eagerly)
-    const bool early_fork = gmode && nshard <= 1 && !g_prof;
+    const char* nf = getenv("GW_FORK");  // experiment hook: GW_FORK=0 runs the sort after the walker
+    const bool fork_ok = !(nf && nf[0] == '0');
+    const bool early_fork = fork_ok && gmode && nshard <= 1 && !g_prof;
     if (early_fork) {
       memset(&hs, 0, sizeof hs);
       hs.key_or = P->D;
@@ -525,7 +528,7 @@ struct Pipeline {
     pend(PH_PREP);
 
     Cands cd;
-    if (!has_locks && nshard <= 1 && !g_prof) {
+    if (fork_ok && !has_locks && nshard <= 1 && !g_prof) {
       // the location sort does not depend on the sync pass: it runs on the
       // side stream while the walker runs here; the stamps (aux) are filled
       // after the walker, then the branches join before the check
@@ -1114,15 +1117,24 @@ struct Pipeline {
       uint32_t* hend = C->get<uint32_t>("hd_end", tr.B);
       uint32_t* hcnt = C->get<uint32_t>("hd_cnt", tr.B);
       CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
-      if (n_hard) {
+      const char* hsm = getenv("GW_HARD_SMALL");  // experiment hook: GW_HARD_SMALL=0 keeps sort + unpack + scan
+      if (n_hard && n_hard <= kRankSortMax && tr.B <= (uint64_t)kThreads * 64 && !(hsm && hsm[0] == '0')) {
+        // few hard events: order them and delimit the blocks in one launch
         unsigned long long* hkey = C->get<unsigned long long>("hd_key", n_hard + 1);
-        uint32_t* hdummy = C->get<uint32_t>("hd_v", n_hard + 1);
         GW_LAUNCH(k_hard_append, grid_for(N), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT);
-        sort<unsigned long long>(hkey, hdummy, n_hard, 32 + ceil_log2(tr.B), "hd", true);
-        GW_LAUNCH(k_hard_unpack, grid_for(n_hard), kThreads, 0, st, hkey, n_hard, hev);
+        GW_LAUNCH(k_hard_small, (unsigned)((n_hard + kThreads - 1) / kThreads), kThreads, 0, st, hkey,
+                  (uint32_t)n_hard, hev, hcnt, tr.B, hbeg, hend);
+      } else {
+        if (n_hard) {
+          unsigned long long* hkey = C->get<unsigned long long>("hd_key", n_hard + 1);
+          uint32_t* hdummy = C->get<uint32_t>("hd_v", n_hard + 1);
+          GW_LAUNCH(k_hard_append, grid_for(N), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT);
+          sort<unsigned long long>(hkey, hdummy, n_hard, 32 + ceil_log2(tr.B), "hd", true);
+          GW_LAUNCH(k_hard_unpack, grid_for(n_hard), kThreads, 0, st, hkey, n_hard, hev);
+        }
+        scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hcnt}, HardSegStore{hcnt, hbeg, hend}, tr.B, OpSum(), 0u, false,
+                              "sc_u32");
       }
-      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{hcnt}, HardSegStore{hcnt, hbeg, hend}, tr.B, OpSum(), 0u, false,
-                            "sc_u32");
       sa.hard_ev = hev;
       sa.hb_beg = hbeg;
       sa.hb_end = hend;
@@ -1435,6 +1447,25 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
   });
 }
 
+// host copy of a large result array on several threads (first touch of the
+// fresh destination pages included): millions of reports (C4) otherwise
+// spend tens of ms in one memcpy
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kChunk = 4u << 20;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>(std::min<size_t>(hw, 16), (bytes + kChunk - 1) / kChunk);
+  if (nt <= 1) { memcpy(dst, src, bytes); return; }
+  const size_t per = ((bytes + nt - 1) / nt + 63) & ~(size_t)63;
+  std::vector<std::thread> th;
+  for (size_t i = 1; i < nt; i++) {
+    const size_t o = i * per;
+    if (o >= bytes) break;
+    th.emplace_back([=] { memcpy((char*)dst + o, (const char*)src + o, std::min(per, bytes - o)); });
+  }
+  memcpy(dst, src, std::min(per, bytes));
+  for (auto& t : th) t.join();
+}
+
 extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
   if (!c || !out) { gw_set_error("null argument"); return GW_E_ARG; }
   memset(out, 0, sizeof *out);
@@ -1477,10 +1508,10 @@ extern "C" int gw_ctx_fetch(gw_ctx* c, gw_result* out) {
     if (!out->kind || !out->prior_event || !out->current_event) throw std::bad_alloc();
     std::vector<Diag> dg(nd);
     if (n) {  // written by k_final into mapped host memory (complete after the stream sync above)
-      memcpy(out->kind, c->d_kind, n);
-      memcpy(out->prior_event, c->d_prior, 4 * n);
-      memcpy(out->current_event, c->d_cur, 4 * n);
-      memcpy(out->order_key, c->d_okey, 8 * n);
+      par_memcpy(out->kind, c->d_kind, n);
+      par_memcpy(out->prior_event, c->d_prior, 4 * n);
+      par_memcpy(out->current_event, c->d_cur, 4 * n);
+      par_memcpy(out->order_key, c->d_okey, 8 * n);
     }
     if (nd) {
       CK(cudaMemcpyAsync(dg.data(), c->d_diags, sizeof(Diag) * nd, cudaMemcpyDeviceToHost, c->last_stream));

@@ -1708,6 +1708,46 @@ __global__ void k_hard_unpack(const unsigned long long* hkey, uint64_t n, uint32
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     hev[i] = (uint32_t)hkey[i];
 }
+// Small hard-event lists (n <= kRankSortMax keys (segment << 32 | event), all
+// distinct, nseg <= kThreads * 64 segments) in one launch instead of sort +
+// unpack + scan: every CTA ranks its keys against all n staged in shared
+// memory and writes the event at its rank; CTA 0 also turns the per-segment
+// counts into [beg, end).
+__global__ void __launch_bounds__(kThreads) k_hard_small(const unsigned long long* __restrict__ hkey, uint32_t n,
+                                                        uint32_t* __restrict__ hev, const uint32_t* __restrict__ cnt,
+                                                        uint32_t nseg, uint32_t* __restrict__ beg,
+                                                        uint32_t* __restrict__ end) {
+  __shared__ unsigned long long sk[kRankSortMax];
+  for (uint32_t i = threadIdx.x; i < n; i += kThreads) sk[i] = hkey[i];
+  __syncthreads();
+  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  if (i < n) {
+    const unsigned long long k = sk[i];
+    uint32_t r0 = 0, r1 = 0;
+    uint32_t j = 0;
+    for (; j + 2 <= n; j += 2) {
+      r0 += sk[j] < k;
+      r1 += sk[j + 1] < k;
+    }
+    if (j < n) r0 += sk[j] < k;
+    hev[r0 + r1] = (uint32_t)k;
+  }
+  if (blockIdx.x == 0) {
+    const uint32_t per = (nseg + kThreads - 1) / kThreads;
+    const uint32_t s0 = min(nseg, threadIdx.x * per), s1 = min(nseg, s0 + per);
+    uint32_t sum = 0;
+    for (uint32_t x = s0; x < s1; x++) sum += cnt[x];
+    uint32_t tot;
+    uint32_t run = block_excl_scan<uint32_t, OpSum>(sum, OpSum(), 0u, &tot);
+    for (uint32_t x = s0; x < s1; x++) {
+      const uint32_t c = cnt[x];
+      beg[x] = run;
+      end[x] = run + c;
+      run += c;
+    }
+  }
+}
+
 // exclusive scan of per-block hard-event counts -> [beg, end)
 struct HardSegStore {
   const uint32_t* cnt;
