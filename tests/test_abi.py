@@ -44,3 +44,49 @@ def test_no_cpu_analysis_path_without_a_gpu():
         assert e.code in (N.GW_E_CUDA, N.GW_E_NOMEM)
     else:  # pragma: no cover
         raise AssertionError("analysis must fail loudly without a CUDA device")
+
+
+def test_result_views_own_the_library_buffers():
+    """fetch() returns zero-copy numpy views of a gw_result; the buffers are
+    freed (gw_result_free) only after the last view is gone."""
+    import gc
+    import weakref
+
+    import numpy as np
+
+    libc = ctypes.CDLL(None)
+    libc.malloc.restype = ctypes.c_void_p
+    libc.malloc.argtypes = [ctypes.c_size_t]
+    n, nd = 5, 2
+    r = N._Result()
+    r.n_reports, r.n_diags = n, nd
+
+    def buf(ctype, vals):
+        p = libc.malloc(ctypes.sizeof(ctype) * max(len(vals), 1))
+        arr = ctypes.cast(p, ctypes.POINTER(ctype))
+        for i, v in enumerate(vals):
+            arr[i] = v
+        return arr
+
+    r.kind = buf(ctypes.c_uint8, [0, 1, 2, 1, 0])
+    r.prior_event = buf(ctypes.c_uint32, [1, 2, 3, 4, 5])
+    r.current_event = buf(ctypes.c_uint32, [6, 7, 8, 9, 10])
+    r.order_key = buf(ctypes.c_uint64, [11, 12, 13, 14, 2**63 + 1])
+    r.diag_event = buf(ctypes.c_uint32, [3, 4])
+    r.diag_code = buf(ctypes.c_uint32, [1, 2])
+    r.diag_lock = buf(ctypes.c_uint64, [2**40, 7])
+    res = N._take_result(N.lib(), r)
+    assert res["kind"].tolist() == [0, 1, 2, 1, 0]
+    assert res["prior"].tolist() == [1, 2, 3, 4, 5] and res["current"].tolist() == [6, 7, 8, 9, 10]
+    assert res["order_key"].tolist() == [11, 12, 13, 14, 2**63 + 1]
+    assert res["diag_lock"].dtype == np.uint64 and res["diag_lock"].tolist() == [2**40, 7]
+    owner = res["kind"].base._owner
+    alive = weakref.ref(owner)
+    del owner
+    keep = res["order_key"]
+    del res
+    gc.collect()
+    assert alive() is not None and keep.tolist()[-1] == 2**63 + 1  # a live view keeps the buffers
+    del keep
+    gc.collect()
+    assert alive() is None  # the last view gone: gw_result_free ran
