@@ -321,7 +321,7 @@ struct DupList {
 };
 
 // The access check (gwcp.py:251-277) over the location-sorted accesses, one
-// tile of kAccTile sorted positions per CTA:
+// tile of kThreads * I sorted positions per CTA (I items per thread):
 //   * segment head / last write before each position: a tile-local max-scan
 //     seeded with the maxima of all earlier tiles (k_acc_tilemax + a scan
 //     over tiles), no per-position scan arrays in HBM;
@@ -333,8 +333,11 @@ struct DupList {
 //     hull never leaves it), so the header need not be read.
 // defer (lock mode): every structural candidate (u != t, !cover) is emitted
 // and the walker answers the clock half later.
-constexpr int kAccItems = 8;
-constexpr int kAccTile = kThreads * kAccItems;  // 2048
+// Items per thread (tile = kThreads * items positions): 8, or 10 when that
+// brings a trace into one wave of resident CTAs (acc_items(), engine.cu; C2:
+// 513 tiles of 2,048 -> 410 of 2,560 on 444 slots).  Larger tiles cost
+// occupancy on billion-event traces, so those keep 8.
+constexpr int kAccItemsSmall = 8, kAccItemsLarge = 10;
 
 template <class K>
 struct AccArgs {
@@ -355,16 +358,16 @@ struct AccArgs {
   DupList dup;            // same-record pairs on one location (same-instruction check)
 };
 
-template <class K>
+template <class K, int I>
 __global__ void __launch_bounds__(kThreads) k_acc_tilemax(const K* keys, const uint32_t* vals, uint64_t n,
                                                          uint2* agg) {
   __shared__ uint32_t s_h[kThreads / 32], s_w[kThreads / 32];
-  const uint64_t ntiles = (n + kAccTile - 1) / kAccTile;
+  const uint64_t ntiles = (n + (kThreads * I) - 1) / (kThreads * I);
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t base = tile * kAccTile;
+    const uint64_t base = tile * (kThreads * I);
     uint32_t h = 0, w = 0;
 #pragma unroll
-    for (int k = 0; k < kAccItems; k++) {
+    for (int k = 0; k < I; k++) {
       const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
       if (i < n) {
         if (i == 0 || keys[i] != keys[i - 1]) h = (uint32_t)i + 1;
@@ -383,20 +386,20 @@ __global__ void __launch_bounds__(kThreads) k_acc_tilemax(const K* keys, const u
   }
 }
 
-template <class K>
+template <class K, int I>
 struct AccSmem {
-  K key[kAccTile];
-  uint32_t val[kAccTile];
-  uint32_t to[kAccTile];
-  uint32_t lw[kAccTile];   // inclusive last write pos + 1
-  uint32_t ss[kAccTile];   // segment head pos
-  uint2 st[kAccTile];      // (time, vobj) stamps
+  K key[(kThreads * I)];
+  uint32_t val[(kThreads * I)];
+  uint32_t to[(kThreads * I)];
+  uint32_t lw[(kThreads * I)];   // inclusive last write pos + 1
+  uint32_t ss[(kThreads * I)];   // segment head pos
+  uint2 st[(kThreads * I)];      // (time, vobj) stamps
   uint2 wtot[kThreads / 32];
 };
 
 // (event, tidop) of sorted position q (smem when q is in this tile)
-template <class K>
-__device__ __forceinline__ void acc_pos(const AccArgs<K>& a, const AccSmem<K>& S, uint64_t base, uint64_t q,
+template <class K, int I>
+__device__ __forceinline__ void acc_pos(const AccArgs<K>& a, const AccSmem<K, I>& S, uint64_t base, uint64_t q,
                                         uint32_t& ev, uint32_t& to) {
   if (q >= base) {
     ev = S.val[q - base] & VAL_E;
@@ -406,8 +409,8 @@ __device__ __forceinline__ void acc_pos(const AccArgs<K>& a, const AccSmem<K>& S
     to = __ldg(&a.aux[ev].x);
   }
 }
-template <class K>
-__device__ __forceinline__ uint32_t acc_time(const AccArgs<K>& a, const AccSmem<K>& S, uint64_t base, uint64_t q,
+template <class K, int I>
+__device__ __forceinline__ uint32_t acc_time(const AccArgs<K>& a, const AccSmem<K, I>& S, uint64_t base, uint64_t q,
                                              uint32_t ev, uint32_t) {
   return q >= base ? S.st[q - base].x : __ldg(&a.aux[ev].y);
 }
@@ -420,32 +423,32 @@ __device__ __forceinline__ uint32_t acc_clock(const AccArgs<K>& a, uint32_t vo, 
   return __ldg(optr(a.arena, vo) + OBJ_HDR + (u - (tc / BS) * BS));
 }
 
-template <class K>
+template <class K, int I>
 __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  AccSmem<K>& S = *reinterpret_cast<AccSmem<K>*>(smem_raw);
+  AccSmem<K, I>& S = *reinterpret_cast<AccSmem<K, I>*>(smem_raw);
   const uint32_t BS = a.tr.BS;
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const uint64_t ntiles = (a.n + kAccTile - 1) / kAccTile;
+  const uint64_t ntiles = (a.n + (kThreads * I) - 1) / (kThreads * I);
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t base = tile * kAccTile;
-    const uint32_t cnt = (uint32_t)min((uint64_t)kAccTile, a.n - base);
+    const uint64_t base = tile * (kThreads * I);
+    const uint32_t cnt = (uint32_t)min((uint64_t)(kThreads * I), a.n - base);
     // stage keys / events, then gather the tidops
 #pragma unroll
-    for (int k = 0; k < kAccItems; k++) {
+    for (int k = 0; k < I; k++) {
       const uint32_t j = k * kThreads + threadIdx.x;
       if (j < cnt) { S.key[j] = a.keys[base + j]; S.val[j] = a.vals[base + j]; }
     }
     const K prevkey = base > 0 ? a.keys[base - 1] : (K)0;
     {
-      uint4 ax[kAccItems];
+      uint4 ax[I];
 #pragma unroll
-      for (int k = 0; k < kAccItems; k++) {
+      for (int k = 0; k < I; k++) {
         const uint32_t j = k * kThreads + threadIdx.x;
         ax[k] = j < cnt ? a.aux[a.vals[base + j] & VAL_E] : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int k = 0; k < kAccItems; k++) {
+      for (int k = 0; k < I; k++) {
         const uint32_t j = k * kThreads + threadIdx.x;
         if (j < cnt) { S.to[j] = ax[k].x; S.st[j] = make_uint2(ax[k].y, ax[k].z); }
       }
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
     __syncthreads();
     // segment head / last write: block-wide max-scan rounds, seeded with the carry
     uint2 run = a.carry[tile];
-    for (int k = 0; k < kAccItems; k++) {
+    for (int k = 0; k < I; k++) {
       const uint32_t j = k * kThreads + threadIdx.x;
       const uint64_t i = base + j;
       uint2 v = make_uint2(0, 0);
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
     }
     const uint32_t lw_in = a.carry[tile].y;  // last write before the tile
     // the checks
-    for (int k = 0; k < kAccItems; k++) {
+    for (int k = 0; k < I; k++) {
       const uint32_t j = k * kThreads + threadIdx.x;
       if (j >= cnt) continue;
       const uint64_t i = base + j;
@@ -595,11 +598,11 @@ __global__ void k_resolve(Cands in, const uint32_t* qv, const uint32_t* time, Ca
   }
 }
 
-template <class K>
+template <class K, int I>
 inline void acc_setup() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(k_access<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AccSmem<K>));
+    cudaFuncSetAttribute(k_access<K, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AccSmem<K, I>));
     done = true;
   }
 }

@@ -661,6 +661,17 @@ struct Pipeline {
     sfx.clear();
   }
 
+  // k_access / k_acc_tilemax items per thread: the larger tile when it brings
+  // the sorted positions into one wave of resident CTAs (3 per SM at either
+  // size with 32-bit keys), else the smaller one
+  int acc_items = kAccItemsSmall;
+  int pick_acc_items(uint64_t NA) const {
+    if (wide) return kAccItemsSmall;
+    const uint64_t slots = 3ull * (uint64_t)C->num_sms;
+    const uint64_t ts = kThreads * kAccItemsSmall, tl = kThreads * kAccItemsLarge;
+    return ((NA + ts - 1) / ts > slots && (NA + tl - 1) / tl <= slots) ? kAccItemsLarge : kAccItemsSmall;
+  }
+
   // ---- pipeline state shared by the phases --------------------------------
   uint32_t* scal = nullptr;
   Stats hs{};
@@ -855,15 +866,19 @@ struct Pipeline {
       skeys = k64;
     }
     // per-tile maxima of (segment head, write position), exclusive max-scan over tiles
-    const uint64_t nt = (NA + kAccTile - 1) / kAccTile;
+    acc_items = pick_acc_items(NA);
+    const uint64_t atile = (uint64_t)kThreads * acc_items;
+    const uint64_t nt = (NA + atile - 1) / atile;
     uint2* agg = C->get<uint2>("acc_tagg", nt + 1);
     carry = C->get<uint2>("acc_carry", nt + 1);
     const unsigned tg = (unsigned)std::min<uint64_t>(std::max<uint64_t>(nt, 1), 148ull * 8);
-    if (!wide)
-      GW_LAUNCH(k_acc_tilemax<uint32_t>, tg, kThreads, 0, st, (const uint32_t*)skeys, vals, NA, agg);
+    if (wide)
+      GW_LAUNCH((k_acc_tilemax<unsigned long long, kAccItemsSmall>), tg, kThreads, 0, st,
+                (const unsigned long long*)skeys, vals, NA, agg);
+    else if (acc_items == kAccItemsLarge)
+      GW_LAUNCH((k_acc_tilemax<uint32_t, kAccItemsLarge>), tg, kThreads, 0, st, (const uint32_t*)skeys, vals, NA, agg);
     else
-      GW_LAUNCH(k_acc_tilemax<unsigned long long>, tg, kThreads, 0, st, (const unsigned long long*)skeys, vals, NA,
-                agg);
+      GW_LAUNCH((k_acc_tilemax<uint32_t, kAccItemsSmall>), tg, kThreads, 0, st, (const uint32_t*)skeys, vals, NA, agg);
     scan<uint2, OpMax2>(ArrLoad<uint2>{agg}, ArrStore<uint2>{carry}, nt, OpMax2(), make_uint2(0, 0), false, "sc_u2");
   }
 
@@ -926,16 +941,23 @@ struct Pipeline {
         aa.large_cap = (uint32_t)(NA / kSmallWin + 1);
         aa.dup = dup;
       };
-      const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>((NA + kAccTile - 1) / kAccTile, 1),
-                                                       148ull * 16);
-      if (!wide) {
-        fill(a32, (const uint32_t*)skeys);
-        acc_setup<uint32_t>();
-        GW_LAUNCH(k_access<uint32_t>, ag, kThreads, sizeof(AccSmem<uint32_t>), st, a32);
-      } else {
+      const uint64_t atile = (uint64_t)kThreads * acc_items;
+      const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>((NA + atile - 1) / atile, 1), 148ull * 16);
+      if (wide) {
         fill(a64, (const unsigned long long*)skeys);
-        acc_setup<unsigned long long>();
-        GW_LAUNCH(k_access<unsigned long long>, ag, kThreads, sizeof(AccSmem<unsigned long long>), st, a64);
+        acc_setup<unsigned long long, kAccItemsSmall>();
+        GW_LAUNCH((k_access<unsigned long long, kAccItemsSmall>), ag, kThreads,
+                  sizeof(AccSmem<unsigned long long, kAccItemsSmall>), st, a64);
+      } else if (acc_items == kAccItemsLarge) {
+        fill(a32, (const uint32_t*)skeys);
+        acc_setup<uint32_t, kAccItemsLarge>();
+        GW_LAUNCH((k_access<uint32_t, kAccItemsLarge>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsLarge>), st,
+                  a32);
+      } else {
+        fill(a32, (const uint32_t*)skeys);
+        acc_setup<uint32_t, kAccItemsSmall>();
+        GW_LAUNCH((k_access<uint32_t, kAccItemsSmall>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsSmall>), st,
+                  a32);
       }
       check_launch();
       if (gmode) {
