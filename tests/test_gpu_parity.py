@@ -88,6 +88,17 @@ def test_engine_matches_oracle_c2_geometries(ctx, geom):
     assert ndjson_lines(tr, got) == ndjson_lines(tr, want)
 
 
+@pytest.mark.parametrize("blocks", [250, 256])
+def test_engine_matches_oracle_c2_sort_size_limits(ctx, blocks):
+    """~4.1 M events: the one-sweep location sort at its largest size (~1,000
+    tiles, two-level look-back with 32-tile groups, a partial last group) and,
+    at 256 blocks, just past it (reduce-then-scan passes)."""
+    tr = WL.c2_soa(blocks=blocks, warps=8, lanes=32, phases=8, records=8, words_per_block=1024, seed=blocks)
+    got = _run(ctx, tr)
+    want = O.run_trace(tr)
+    assert ndjson_lines(tr, got) == ndjson_lines(tr, want)
+
+
 def test_empty_and_tiny_traces(ctx):
     for text in ("config blocks=1 warps=1 lanes=1\n", "config blocks=2 warps=1 lanes=1\n0.0.0 wr g:0x10\n",
                  "config blocks=1 warps=1 lanes=1\nbar block 0\n0.0.0 end\nbar block 0\n"):
