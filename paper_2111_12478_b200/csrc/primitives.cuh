@@ -330,7 +330,10 @@ __device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
 }
 
 template <class K, int RB>
-__global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+#ifndef GW_OS_MINB
+#define GW_OS_MINB 3
+#endif
+__global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? GW_OS_MINB : 2) k_rs_onesweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                             K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                             uint64_t n, int pass, const uint32_t* __restrict__ ghist,
                                                             unsigned long long* status, uint32_t* ctr, uint32_t epoch) {
