@@ -79,6 +79,7 @@ struct Plan {
   unsigned long long n_bar = 0, n_end = 0, n_wbar = 0, D = 0;
   uint64_t cand_cap = 0;
   uint32_t launches = 0;
+  bool hard_small = false;  // snapshot mode with a one-launch hard-event list: a branch from the graph start
   cudaGraphExec_t exec = nullptr;
 };
 
@@ -128,8 +129,8 @@ struct gw_ctx {
     return hres;
   }
   // side stream of the lock-free fork (access sort concurrent with the sync pass)
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side = nullptr, side2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_hard = nullptr;
   uint32_t epoch = 1;  // look-back flag epochs (never reused within 2^24 passes)
   // last analysis, for an eager re-run after a graph abort
   DevTrace last_tr{};
@@ -452,6 +453,7 @@ struct Pipeline {
       memset(&hs, 0, sizeof hs);
       hs.key_or = P->D;
       fork_sort();
+      if (P->hard_small) fork_hard();  // the hard-event list needs only the trace and the plan's count
     }
     Stats* dst = C->get<Stats>("stats", 1);
     GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
@@ -627,6 +629,7 @@ struct Pipeline {
                 C->d_okey);
       check_launch();
     }
+    if (hard_forked && !hard_joined) CK(cudaStreamWaitEvent(st, C->ev_hard, 0));  // every branch rejoins
     C->d_diags = w.diags;
     C->arena_words = arena_units << OBJ_USHIFT;
     C->h_scal = (uint32_t*)C->host_res(kResHdr + (ncap > 0 ? 17ull * ncap : 0ull));
@@ -636,6 +639,45 @@ struct Pipeline {
     S.n_sync = hs.n_acq + hs.n_rel + hs.n_end + hs.n_bar;
     C->launches = g_launches;
     C->stats_pending = !gmode;
+  }
+
+  // hard-event list of the snapshot walker in one launch (<= kRankSortMax events)
+  bool obs_hard_small = false, hard_forked = false, hard_joined = false;
+  bool hard_small_ok(uint64_t nh) const {
+    const char* hsm = getenv("GW_HARD_SMALL");  // experiment hook: GW_HARD_SMALL=0 keeps sort + unpack + scan
+    return nh && nh <= kRankSortMax && tr.B <= (uint64_t)kThreads * 64 && !(hsm && hsm[0] == '0');
+  }
+  void hard_small_list(uint64_t nh, uint32_t* hev, uint32_t* hcnt, uint32_t* hbeg, uint32_t* hend) {
+    unsigned long long* hkey = C->get<unsigned long long>("hd_key", nh + 1);
+    GW_LAUNCH(k_hard_append, grid_for(tr.n), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT,
+              (uint32_t)(nh + 1));
+    GW_LAUNCH(k_hard_small, (unsigned)((nh + kThreads - 1) / kThreads), kThreads, 0, st, hkey, (uint32_t)nh, hev,
+              hcnt, tr.B, hbeg, hend);
+  }
+  // graph replays: the hard-event list on a third branch from the graph start,
+  // beside k_prep / k_state_init (it may run before the plan check: k_hard_append
+  // never writes past the plan's count, and the walker itself checks the abort flag)
+  void fork_hard() {
+    const uint64_t nh = P->n_bar + P->n_end;
+    if (!hard_small_ok(nh)) return;
+    if (!C->side2) {
+      CK(cudaStreamCreateWithFlags(&C->side2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&C->ev_fork2, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&C->ev_hard, cudaEventDisableTiming));
+    }
+    const cudaStream_t main_st = st;
+    uint32_t* hev = C->get<uint32_t>("hd_ev", nh + 1);
+    uint32_t* hcnt = C->get<uint32_t>("hd_cnt", tr.B);
+    uint32_t* hbeg = C->get<uint32_t>("hd_beg", tr.B);
+    uint32_t* hend = C->get<uint32_t>("hd_end", tr.B);
+    CK(cudaEventRecord(C->ev_fork2, main_st));
+    CK(cudaStreamWaitEvent(C->side2, C->ev_fork2, 0));
+    st = C->side2;
+    CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
+    hard_small_list(nh, hev, hcnt, hbeg, hend);
+    CK(cudaEventRecord(C->ev_hard, st));
+    st = main_st;
+    hard_forked = true;
   }
 
   // the access sort on the side stream (joined through ev_join before the check)
@@ -1138,15 +1180,16 @@ struct Pipeline {
       uint32_t* hbeg = C->get<uint32_t>("hd_beg", tr.B);
       uint32_t* hend = C->get<uint32_t>("hd_end", tr.B);
       uint32_t* hcnt = C->get<uint32_t>("hd_cnt", tr.B);
-      CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
-      const char* hsm = getenv("GW_HARD_SMALL");  // experiment hook: GW_HARD_SMALL=0 keeps sort + unpack + scan
-      if (n_hard && n_hard <= kRankSortMax && tr.B <= (uint64_t)kThreads * 64 && !(hsm && hsm[0] == '0')) {
+      if (hard_forked) {
+        CK(cudaStreamWaitEvent(st, C->ev_hard, 0));  // built on the third branch (fork_hard)
+        hard_joined = true;
+      } else if (hard_small_ok(n_hard)) {
         // few hard events: order them and delimit the blocks in one launch
-        unsigned long long* hkey = C->get<unsigned long long>("hd_key", n_hard + 1);
-        GW_LAUNCH(k_hard_append, grid_for(N), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT);
-        GW_LAUNCH(k_hard_small, (unsigned)((n_hard + kThreads - 1) / kThreads), kThreads, 0, st, hkey,
-                  (uint32_t)n_hard, hev, hcnt, tr.B, hbeg, hend);
+        CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
+        obs_hard_small = true;
+        hard_small_list(n_hard, hev, hcnt, hbeg, hend);
       } else {
+        CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
         if (n_hard) {
           unsigned long long* hkey = C->get<unsigned long long>("hd_key", n_hard + 1);
           uint32_t* hdummy = C->get<uint32_t>("hd_v", n_hard + 1);
@@ -1334,6 +1377,9 @@ extern "C" void gw_ctx_destroy(gw_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
+  if (c->ev_hard) cudaEventDestroy(c->ev_hard);
+  if (c->side2) cudaStreamDestroy(c->side2);
   if (c->hres) cudaFreeHost(c->hres);
   delete c;
 }
@@ -1393,6 +1439,7 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   np.N = tr.n; np.B = tr.B; np.W = tr.W; np.L = tr.L; np.inactive_opt = inactive;
   np.key = kp; np.tidop = tp; np.instr = ip; np.stream = st;
   np.n_bar = p.obs.n_bar; np.n_end = p.obs.n_end; np.n_wbar = p.obs.n_wbar; np.D = p.obs_D;
+  np.hard_small = p.obs_hard_small;
   np.cand_cap = 2ull * p.obs_ncand + 4096;  // tight: graph replays size the dedup / order passes by it
   c->plan = np;
   Pipeline g;

@@ -1675,7 +1675,7 @@ __global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t*
   }
 }
 __global__ void k_hard_append(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
-                              const uint32_t* abort_flag) {
+                              const uint32_t* abort_flag, uint32_t cap = 0xFFFFFFFFu) {
   if (*(volatile const uint32_t*)abort_flag) return;  // graph mode: the plan does not fit this trace
   constexpr int U = 4;  // aligned 32-event windows per warp iteration (loads issued together)
   const int lane = threadIdx.x & 31;
@@ -1698,7 +1698,8 @@ __global__ void k_hard_append(DevTrace tr, unsigned long long* hkey, uint32_t* h
       base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
       if (hard) {
         const uint32_t b = ev_tid(to[u]) / tr.BS;
-        hkey[base + __popc(m & lanemask_lt())] = ((unsigned long long)b << 32) | (uint32_t)(b0 + 32 * u + lane);
+        const uint32_t slot = base + __popc(m & lanemask_lt());
+        if (slot < cap) hkey[slot] = ((unsigned long long)b << 32) | (uint32_t)(b0 + 32 * u + lane);
         atomicAdd(hcnt + b, 1u);
       }
     }
