@@ -77,8 +77,18 @@ __device__ __forceinline__ uint4 make_aux(const StampSrc& src, uint32_t e, uint3
   if (ev_kind(to) <= GW_K_WRITE && src.valid()) st = src.get(e, ev_tid(to));
   return make_uint4(to, st.x, st.y, 0u);
 }
+// ghist != nullptr: also the digit histograms of the one-sweep sort that
+// follows (npass passes of rb-bit digits; k_rs_ghist's job, without a second
+// read of the keys)
 template <class K>
-__global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals, StampSrc src, uint4* aux) {
+__global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals, StampSrc src, uint4* aux,
+                           uint32_t* ghist = nullptr, int rb = 0, int npass = 0) {
+  __shared__ uint32_t h[kRsMaxPass * kRsMaxDigits];
+  const uint32_t nd = 1u << rb;
+  if (ghist) {
+    for (uint32_t i = threadIdx.x; i < npass * nd; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+  }
   const K sentinel = kr.sentinel ? ((K)1 << (kr.nbits - 1)) : (K)0;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tr.n; e += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t to = tr.tidop[e];
@@ -93,6 +103,13 @@ __global__ void k_acc_keys(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals, Sta
     }
     keys[e] = k;
     vals[e] = (uint32_t)e | (ev_kind(to) == GW_K_WRITE ? VAL_W : 0u);
+    if (ghist)
+      for (int p = 0; p < npass; p++) atomicAdd(&h[p * nd + ((uint32_t)(k >> (rb * p)) & (nd - 1))], 1u);
+  }
+  if (ghist) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < npass * nd; i += blockDim.x)
+      if (h[i]) atomicAdd(&ghist[i], h[i]);
   }
 }
 

@@ -315,7 +315,9 @@ struct Pipeline {
       return;
     }
     SortScratch sc;
-    sc.ghist = zeroed(kRsMaxPass * kRsMaxDigits);
+    sc.ghist = pre_ghist ? pre_ghist : zeroed(kRsMaxPass * kRsMaxDigits);
+    sc.ghist_ready = pre_ghist != nullptr;
+    pre_ghist = nullptr;
     sc.ctrs = zeroed(npass);
     sc.status = C->get<unsigned long long>(std::string("rs_status") + sfx,
                                            2 * std::max(lb_tiles(n), lb_tiles(tr.n)) * kRsMaxDigits);
@@ -714,6 +716,8 @@ struct Pipeline {
     return ((NA + ts - 1) / ts > slots && (NA + tl - 1) / tl <= slots) ? kAccItemsLarge : kAccItemsSmall;
   }
 
+  uint32_t* pre_ghist = nullptr;  // digit histograms built by the key pass, consumed by the next sort()
+
   // ---- pipeline state shared by the phases --------------------------------
   uint32_t* scal = nullptr;
   Stats hs{};
@@ -856,7 +860,15 @@ struct Pipeline {
       // key and sort last, and every access-pass kernel skips them, so no
       // kernel needs the access count on the host.
       vals = C->get<uint32_t>("acc_v", N);
-      if (!wide) {
+      if (!wide && N > 1 && N < kRsBigN && nbits > 0) {
+        // one-sweep location sort next: the key pass also builds its digit histograms
+        // (k_rs_ghist's grid: few CTAs, so few global flushes)
+        uint32_t* k32 = C->get<uint32_t>("acc_k", N);
+        pre_ghist = zeroed(kRsMaxPass * kRsMaxDigits);
+        GW_LAUNCH(k_acc_keys<uint32_t>, (unsigned)std::min<uint64_t>(lb_tiles(N), 148ull * 8), kThreads, 0, st, tr,
+                  kr, k32, vals, stamps, split ? nullptr : aux, pre_ghist, rs_digit_bits(nbits), rs_passes(nbits));
+        skeys = k32;
+      } else if (!wide) {
         uint32_t* k32 = C->get<uint32_t>("acc_k", N);
         GW_LAUNCH(k_acc_keys<uint32_t>, grid_for(N), kThreads, 0, st, tr, kr, k32, vals, stamps, split ? nullptr : aux);
         skeys = k32;

@@ -896,6 +896,7 @@ struct SortScratch {
   uint32_t* ghist;              // kRsMaxPass * kRsMaxDigits, zeroed
   unsigned long long* status;   // 2 * lb_tiles(n) * kRsMaxDigits (tile aggregates, then group totals)
   uint32_t* ctrs;               // one zeroed counter per pass
+  bool ghist_ready = false;     // ghist already accumulated by the key producer (k_acc_keys)
 };
 
 template <class K, int RB>
@@ -920,8 +921,9 @@ bool radix_sort_rb(K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, uin
                    uint32_t epoch, cudaStream_t st) {
   rs_setup<K, RB>();
   const uint64_t nt = lb_tiles(n);
-  GW_LAUNCH((k_rs_ghist<K, RB>), (unsigned)std::min<uint64_t>(nt, 148ull * 8), kThreads, 0, st, keys, n, npass,
-            sc.ghist);
+  if (!sc.ghist_ready)
+    GW_LAUNCH((k_rs_ghist<K, RB>), (unsigned)std::min<uint64_t>(nt, 148ull * 8), kThreads, 0, st, keys, n, npass,
+              sc.ghist);
   bool alt = false;
   for (int p = 0; p < npass; p++) {
     const K* ki = alt ? keys_alt : keys;
