@@ -47,17 +47,10 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-WORKLOADS = {
-    # C2 (configs[1]): 64 x 256 threads, __syncthreads only, 64K words, ~1 % random words
-    "c2": dict(gen="c2", blocks=64, warps=8, lanes=32, phases=8, records=8, words_per_block=1024, seed=2),
-    # C4 (configs[3]): 1024 x 256 threads, ITS-divergent warps (single-lane accesses in random lane order,
-    # random-mask warp barriers every 4 iterations, block barriers every 64), 16M words, 1.0e9 events
-    "c4": dict(gen="c4", blocks=1024, warps=8, lanes=32, iters=3786, words_per_block=16384, seed=4),
-    # C3 (configs[2]): 1024 x 256 threads, 4096 device-scope spin locks, fences, atomics, 1.005e8 events
-    "c3": dict(gen="c3", blocks=1024, warps=8, lanes=32, iters=168, locks=4096, region=64, private=512, seed=3),
-    # C5 (configs[4]): the C2 recipe at 1024 x 256 threads, 256M words, 16 phases x 240 records = 1.007e9 events
-    "c5": dict(gen="c2", blocks=1024, warps=8, lanes=32, phases=16, records=240, words_per_block=262144, seed=5),
-}
+def workloads():
+    from paper_2111_12478_b200 import workloads as WL
+
+    return WL.CONFIGS
 
 
 # Algorithmic bytes per launch of the pipeline's kernels:
@@ -97,6 +90,21 @@ def kernel_tag(name: str) -> str | None:
     return name.split("@", 1)[1] if "@" in name else None
 
 
+def load_full_digest(workload: str):
+    """The CPU oracle's report digest of the full workload trace (committed
+    fixture made on a GPU host by profiles/make_full_digests.py), or None."""
+    try:
+        with open(os.path.join(REPO, "tests", "golden", "full_digests.json")) as fh:
+            d = json.load(fh)
+    except Exception:
+        return None
+    r = d.get(workload)
+    if not r or "oracle_digest" not in r:
+        return None
+    return {"digest": r["oracle_digest"], "source": f"tests/golden/full_digests.json[{workload}] (oracle port, "
+                                                     f"{r.get('n_reports')} reports)"}
+
+
 def load_ncu_traffic():
     try:
         with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
@@ -106,19 +114,9 @@ def load_ncu_traffic():
 
 
 def workload_events(p):
-    from paper_2111_12478_b200 import _native as N
+    from paper_2111_12478_b200 import workloads as WL
 
-    if p["gen"] == "c4":
-        n = N.c4_events(p["blocks"], p["warps"], p["iters"])
-        n_acc = p["iters"] * p["blocks"] * p["warps"] * 32
-    elif p["gen"] == "c3":
-        from paper_2111_12478_b200 import workloads as WL
-
-        n, n_acc, _ = WL.c3_counts(**{k: v for k, v in p.items() if k != "gen"})
-    else:
-        n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
-        n_acc = n - p["phases"] * p["blocks"]
-    return n, n_acc
+    return WL.config_counts(p)
 
 
 def workload_desc(name, p, n, n_acc):
@@ -145,7 +143,7 @@ def make_workload(name: str, rank: int, dev, sharded: bool = False):
     import torch
     from paper_2111_12478_b200 import _native as N
 
-    p = dict(WORKLOADS[name])
+    p = dict(workloads()[name])
     if not sharded:  # replicas: every rank analyses its own trace; sharded: one trace, split by address
         p["seed"] += rank
     n, n_acc = workload_events(p)
@@ -173,31 +171,8 @@ def make_workload(name: str, rank: int, dev, sharded: bool = False):
 def host_workload_prefix(p, P):
     """Record-aligned host prefix of >= min(P, N) events (numpy / text recipe)."""
     from paper_2111_12478_b200 import workloads as WL
-    from paper_2111_12478_b200.trace import Trace, parse_trace
 
-    gp = {k: v for k, v in p.items() if k != "gen"}
-    if p["gen"] == "c3":  # iteration-major: the first iterations are a prefix of the full trace
-        per_it = WL.c3_counts(**dict(gp, iters=1))[0]
-        gp["iters"] = min(p["iters"], max(1, -(-P // per_it)))
-        tr = parse_trace(WL.c3_text(**gp))
-        from paper_2111_12478_b200 import _native as N
-
-        m = min(P, len(tr))
-        while m < len(tr) and tr.tidop[m] & N.F_CONT:
-            m += 1
-        return Trace(tr.config, tr.key[:m], tr.tidop[:m], tr.instr[:m])
-    if p["gen"] != "c4":
-        return WL.c2_soa_prefix(P, **gp)
-    per_it = p["blocks"] * p["warps"] * 33
-    its = min(p["iters"], max(1, -(-P // per_it)))
-    gp["iters"] = its
-    tr = parse_trace(WL.c4_text(**gp))
-    from paper_2111_12478_b200 import _native as N
-
-    m = min(P, len(tr))
-    while m < len(tr) and tr.tidop[m] & N.F_CONT:
-        m += 1
-    return Trace(tr.config, tr.key[:m], tr.tidop[:m], tr.instr[:m])
+    return WL.config_prefix(p, P)
 
 
 def host_prefix(cfg, dev_bufs, P):
@@ -312,7 +287,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    p = WORKLOADS[args.workload]
+    p = workloads()[args.workload]
     n, n_acc = workload_events(p)
     desc = workload_desc(args.workload, p, n, n_acc)
     cache = {}
@@ -344,7 +319,8 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic",
-        "config": dict(desc, parallelism="single host core"),
+        "config": desc,  # identical to the b200 arm's config
+        "run": {"parallelism": "single host core"},
         "cpu_baseline": {
             "value": evs,
             "unit": UNIT,
@@ -471,6 +447,23 @@ def run_b200(args):
         ms_e2e = max_over_ranks(ms_e2e)
     n_rep = len(res["kind"])
     stats = ctx.stats()
+    # parity of the timed path itself (graph replay on the bench stream, and the
+    # host-buffer leg): both digests must equal the committed full-trace digest
+    # of the CPU oracle (tests/golden/full_digests.json) when one exists
+    digest, want_digest, digest_src = None, None, None
+    if rank == 0:
+        from paper_2111_12478_b200.report import result_digest
+
+        digest = result_digest(res)
+        d_e2e = result_digest(res_e2e)
+        if d_e2e != digest:
+            raise SystemExit(f"bench: host-buffer run's reports differ from the device-resident run's "
+                             f"({d_e2e} vs {digest})")
+        fx = load_full_digest(args.workload)
+        if fx is not None and args.steps > 0:
+            want_digest, digest_src = fx["digest"], fx["source"]
+            if digest != want_digest:
+                raise SystemExit(f"bench: timed run's report digest {digest} != {want_digest} ({digest_src})")
 
     if rank != 0:
         if dist is not None:
@@ -525,11 +518,16 @@ def run_b200(args):
         "vs_baseline": None,
         "dtype": "u32",
         "data": "synthetic",
-        "config": dict(desc, reports=n_rep,
-                       parallelism=(f"address-sharded x{world} (location-key ranges; replicated sync pass; "
-                                    f"NCCL gather + order-key merge of the reports)") if sharded
-                       else f"replicas x{world}",
-                       l2="flushed before every timed step (256 MiB write)"),
+        "config": desc,  # identical to the reference arm's config
+        "run": {
+            "reports": n_rep,
+            "parallelism": (f"address-sharded x{world} (location-key ranges; replicated sync pass; "
+                            f"NCCL gather + order-key merge of the reports)") if sharded else f"replicas x{world}",
+            "l2": "flushed before every timed step (256 MiB write)",
+            "report_digest": digest,
+            "report_digest_expected": want_digest,
+            "report_digest_source": digest_src,
+        },
         "e2e": {
             "value": e2e,
             "unit": UNIT,
@@ -568,7 +566,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c4", "c5"],
+                    help="BASELINE.json config (default c5: the metric's 1/2/4/8-GPU sweep config, 1.007e9 events)")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", choices=["replicas", "sharded"], default=None,

@@ -160,7 +160,10 @@ const char* gw_last_error(void);
  * gw_ctx_fetch, so results never depend on the cache. */
 gw_ctx* gw_ctx_create(int device);
 void gw_ctx_destroy(gw_ctx* c);
-/* dev_trace points at device memory; enqueues on opts->stream; results stay on device */
+/* dev_trace points at device memory; enqueues on opts->stream; results stay on device.
+ * The dev_trace buffers must stay valid and unmodified until the matching
+ * gw_ctx_fetch returns: a graph replay whose plan check fails is re-run
+ * eagerly inside gw_ctx_fetch, reading them again. */
 int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* dev_trace, const gw_opts* opts);
 /* host_trace in (pageable or pinned) -> H2D on opts->stream -> analyze (results on device) */
 int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* host_trace, const gw_opts* opts);

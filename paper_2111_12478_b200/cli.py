@@ -1,6 +1,8 @@
 """``check`` front end with the reference's exit codes and output
 (cli.py:20-84): 0 no races, 1 races found, 2 usage / parse error,
 3 validation error.  NDJSON reports on stdout, diagnostics on stderr.
+An engine failure (no CUDA device, library missing, CUDA or capacity error)
+exits 4, never 1, so scripts gating on "races found" cannot misread it.
 """
 
 from __future__ import annotations
@@ -18,6 +20,7 @@ EXIT_CLEAN = 0
 EXIT_RACES = 1
 EXIT_USAGE = 2
 EXIT_INVALID = 3
+EXIT_ENGINE = 4  # not in the reference (it has no engine that can fail): distinct from every code above
 
 
 def _die(code: int, message: str) -> NoReturn:
@@ -51,8 +54,11 @@ def _cmd_check(args) -> int:
     if args.infer_locks or args.order_matrix:
         _die(EXIT_USAGE, "--infer-locks / --order-matrix are not on the accelerated path (use gpurace)")
     tr = _load(args.trace)
-    res = N.analyze(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt=not args.no_inactive_opt,
-                    hb=args.detector == "hb")
+    try:
+        res = N.analyze(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt=not args.no_inactive_opt,
+                        hb=args.detector == "hb")
+    except (N.NativeUnavailable, N.EngineError) as e:
+        _die(EXIT_ENGINE, f"{args.trace}: analysis engine failed: {e}")
     out = ndjson_lines(tr, res, args.detector)
     if out:
         sys.stdout.write("\n".join(out) + "\n")

@@ -267,14 +267,25 @@ struct Pipeline {
       gepoch += k;
       return e;
     }
-    if (C->epoch + k >= (1u << 24)) {  // wrap: clear every flag / status word
+    // the wrap is handled once per analysis in reserve_epochs(), on the main
+    // stream before any branch forks (never under a running look-back)
+    if (C->epoch + k > epoch_limit) throw CudaErr{GW_E_ARG, "look-back epoch budget of one analysis exceeded"};
+    uint32_t e = C->epoch;
+    C->epoch += k;
+    return e;
+  }
+  // eager analyses: every status buffer (main and side branch) is either
+  // cleared here or holds only epochs < C->epoch, so the kEpochBudget epochs
+  // this analysis may take never alias a stale status word
+  static constexpr uint32_t kEpochBudget = 1u << 16;
+  uint32_t epoch_limit = 0;
+  void reserve_epochs() {
+    if (C->epoch + kEpochBudget >= (1u << 24)) {  // wrap: clear every flag / status word
       for (auto& kv : C->bufs)
         if (kv.first.rfind("rs_status", 0) == 0) CK(cudaMemsetAsync(kv.second.p, 0, kv.second.cap, st));
       C->epoch = 1;
     }
-    uint32_t e = C->epoch;
-    C->epoch += k;
-    return e;
+    epoch_limit = C->epoch + kEpochBudget;
   }
   uint32_t gepoch = 0;
   std::string sfx;  // scratch-name suffix of the side branch (its own look-back status words)
@@ -439,6 +450,7 @@ struct Pipeline {
     scal = C->get<uint32_t>("scalars", SC_COUNT);
     CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
     CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
+    if (!gmode) reserve_epochs();
     if (gmode) {  // fixed epochs in the graph: start from clean flags
       for (const char* nm : {"rs_status", "rs_status_b"}) {
         unsigned long long* rs = C->get<unsigned long long>(nm, 2 * lb_tiles(N) * kRsMaxDigits);
@@ -1457,6 +1469,9 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   Pipeline g;
   g.C = c; g.st = st; g.inactive_opt = inactive; g.tr = tr; g.gmode = true; g.P = &c->plan;
   g.run();
+  // the graph's fixed epochs [1, 1 + gepoch) stay in the status words after
+  // every replay: later eager analyses on this context continue above them
+  c->epoch = std::max(c->epoch, 1 + g.gepoch);
   CK(cudaStreamSynchronize(st));
   cudaGraph_t graph = nullptr;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));

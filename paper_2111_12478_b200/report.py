@@ -148,3 +148,19 @@ class Reporter:
     def __init__(self, detector: str):
         self.detector = detector
         self.reports: list[RaceReport] = []
+
+
+def result_digest(res: dict) -> str:
+    """sha256 of a run's report and diagnostic arrays (kind u8, prior u32,
+    current u32, diag event/code u32, diag lock u64), in final order.  The
+    NDJSON lines are a function of these arrays and the trace, so equal
+    digests on one trace mean byte-identical ``check`` output; used to pin
+    the billion-event configs, whose NDJSON is too large to keep."""
+    import hashlib
+
+    hs = hashlib.sha256()
+    hs.update(np.uint64(len(res["kind"])).tobytes())
+    for k, dt in (("kind", np.uint8), ("prior", np.uint32), ("current", np.uint32), ("diag_event", np.uint32),
+                  ("diag_code", np.uint32), ("diag_lock", np.uint64)):
+        hs.update(np.ascontiguousarray(res.get(k, np.zeros(0, dt)), dt).tobytes())
+    return hs.hexdigest()

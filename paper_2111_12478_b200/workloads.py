@@ -350,3 +350,65 @@ def c1_texts() -> dict[str, str]:
          "1.0.0 acq 0xa device", "1.0.0 wr g:0x10", "1.0.0 rel 0xa device", f"bar warp 1 0 {full:#x}",
          wacc(1, "rd", ["g:0x10"] * L)]) + "\n"
     return out
+
+
+# ------------------------------------------------------- full configs ----
+# BASELINE.json configs[1..4] at full size; the bench and the
+# full-scale parity tests generate them on the device (gw_gen_c*_device), the
+# prefix goldens on the host with the recipes above.
+CONFIGS = {
+    # C2 (configs[1]): 64 x 256 threads, __syncthreads only, 64K words, ~1 % random words
+    "c2": dict(gen="c2", blocks=64, warps=8, lanes=32, phases=8, records=8, words_per_block=1024, seed=2),
+    # C3 (configs[2]): 1024 x 256 threads, 4096 device-scope spin locks, fences, atomics, 1.005e8 events
+    "c3": dict(gen="c3", blocks=1024, warps=8, lanes=32, iters=168, locks=4096, region=64, private=512, seed=3),
+    # C4 (configs[3]): 1024 x 256 threads, ITS-divergent warps (single-lane accesses in random lane order,
+    # random-mask warp barriers every 4 iterations, block barriers every 64), 16M words, 1.0e9 events
+    "c4": dict(gen="c4", blocks=1024, warps=8, lanes=32, iters=3786, words_per_block=16384, seed=4),
+    # C5 (configs[4]): the C2 recipe at 1024 x 256 threads, 256M words, 16 phases x 240 records = 1.007e9 events
+    "c5": dict(gen="c2", blocks=1024, warps=8, lanes=32, phases=16, records=240, words_per_block=262144, seed=5),
+}
+
+
+def c4_count(blocks, warps, iters) -> int:
+    """Events of :func:`c4_text` (lanes = 32): one access per lane per
+    iteration, a warp barrier per warp every 4 iterations, a block barrier per
+    block every 64."""
+    return iters * blocks * warps * 32 + blocks * warps * (iters // 4) + blocks * (iters // 64)
+
+
+def config_counts(p: dict) -> tuple[int, int]:
+    """(events, accesses) of a CONFIGS entry without generating it."""
+    if p["gen"] == "c4":
+        return c4_count(p["blocks"], p["warps"], p["iters"]), p["iters"] * p["blocks"] * p["warps"] * 32
+    if p["gen"] == "c3":
+        n, n_acc, _ = c3_counts(**{k: v for k, v in p.items() if k != "gen"})
+        return n, n_acc
+    n = p["phases"] * (p["records"] * p["blocks"] * p["warps"] * p["lanes"] + p["blocks"])
+    return n, n - p["phases"] * p["blocks"]
+
+
+def _cut(tr: Trace, P: int) -> Trace:
+    """The first >= min(P, len) events of ``tr``, extended to a record boundary."""
+    m = min(P, len(tr))
+    while m < len(tr) and tr.tidop[m] & N.F_CONT:
+        m += 1
+    return Trace(tr.config, tr.key[:m], tr.tidop[:m], tr.instr[:m])
+
+
+def config_prefix(p: dict, P: int) -> Trace:
+    """Record-aligned host prefix (>= min(P, N) events, whole records) of a
+    CONFIGS trace, built with the host recipes: the traces are iteration /
+    phase major, so the first iterations are a prefix of the full trace
+    (SURVEY App. B O2 makes its reports a prefix of the full run's)."""
+    from .trace import parse_trace
+
+    gp = {k: v for k, v in p.items() if k != "gen"}
+    if p["gen"] == "c3":
+        per_it = c3_counts(**dict(gp, iters=1))[0]
+        gp["iters"] = min(p["iters"], max(1, -(-P // per_it)))
+        return _cut(parse_trace(c3_text(**gp)), P)
+    if p["gen"] == "c4":
+        per_it = p["blocks"] * p["warps"] * 33
+        gp["iters"] = min(p["iters"], max(1, -(-P // per_it)))
+        return _cut(parse_trace(c4_text(**gp)), P)
+    return _cut(c2_soa_prefix(P, **gp), P)
