@@ -167,6 +167,22 @@ void gw_ctx_destroy(gw_ctx* c);
 int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* dev_trace, const gw_opts* opts);
 /* host_trace in (pageable or pinned) -> H2D on opts->stream -> analyze (results on device) */
 int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* host_trace, const gw_opts* opts);
+/* Packed (narrow-column) trace: the SoA above with the key column stored in
+ * key_bytes = 4 or 8 and the instr column in instr_bytes = 2 or 4 bytes per
+ * event -- the narrowest widths holding every value of the trace (C5:
+ * 10 B/event instead of 16).  It is the layout of GWSOA v2 files (cli
+ * convert --packed) and the host input of gw_ctx_analyze_host_packed, which
+ * uploads it in chunks on a copy stream and widens each chunk on the device
+ * while the next one is in flight, then analyses as gw_ctx_analyze_host. */
+typedef struct gw_trace_packed {
+  gw_config cfg;
+  uint64_t n_events;
+  uint32_t key_bytes, instr_bytes;
+  const void* key;        /* uint32_t[n] (key_bytes 4) or uint64_t[n] */
+  const uint32_t* tidop;
+  const void* instr;      /* uint16_t[n] (instr_bytes 2) or uint32_t[n] */
+} gw_trace_packed;
+int gw_ctx_analyze_host_packed(gw_ctx* c, const gw_trace_packed* host_trace, const gw_opts* opts);
 /* D2H of the last analysis' results (synchronises the stream) */
 int gw_ctx_fetch(gw_ctx* c, gw_result* out);
 int gw_ctx_stats(gw_ctx* c, gw_stats* out);

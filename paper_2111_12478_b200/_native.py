@@ -65,6 +65,18 @@ class _View(C.Structure):
     ]
 
 
+class _Packed(C.Structure):
+    _fields_ = [
+        ("cfg", _Config),
+        ("n_events", C.c_uint64),
+        ("key_bytes", C.c_uint32),
+        ("instr_bytes", C.c_uint32),
+        ("key", C.c_void_p),
+        ("tidop", C.c_void_p),
+        ("instr", C.c_void_p),
+    ]
+
+
 class _Opts(C.Structure):
     _fields_ = [("inactive_opt", C.c_uint32), ("flags", C.c_uint32), ("stream", C.c_void_p),
                 ("shard_index", C.c_uint32), ("shard_count", C.c_uint32)]
@@ -114,6 +126,7 @@ EXPORTS = (
     "gw_ctx_destroy",
     "gw_ctx_analyze_device",
     "gw_ctx_analyze_host",
+    "gw_ctx_analyze_host_packed",
     "gw_ctx_fetch",
     "gw_ctx_stats",
     "gw_ctx_launches",
@@ -168,6 +181,8 @@ def lib():
         L.gw_ctx_analyze_device.restype = C.c_int
         L.gw_ctx_analyze_host.argtypes = [C.c_void_p, C.POINTER(_View), C.POINTER(_Opts)]
         L.gw_ctx_analyze_host.restype = C.c_int
+        L.gw_ctx_analyze_host_packed.argtypes = [C.c_void_p, C.POINTER(_Packed), C.POINTER(_Opts)]
+        L.gw_ctx_analyze_host_packed.restype = C.c_int
         L.gw_ctx_fetch.argtypes = [C.c_void_p, C.POINTER(_Result)]
         L.gw_ctx_fetch.restype = C.c_int
         L.gw_ctx_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
@@ -343,6 +358,25 @@ class Context:
         o = _Opts(1 if inactive_opt else 0, flags, stream, shard[0], shard[1])
         _check(self._L.gw_ctx_analyze_host(self._c, C.byref(v), C.byref(o)))
 
+    def analyze_host_packed(self, cfg, key, tidop, instr, *, inactive_opt=True, stream=None, eager=False,
+                            shard=(0, 1), hb=False) -> None:
+        """Packed host trace (pack_columns): key uint32|uint64, instr uint16|uint32;
+        uploaded in chunks and widened on the device (gw_ctx_analyze_host_packed)."""
+        key, tidop, instr = np.asarray(key), np.asarray(tidop, np.uint32), np.asarray(instr)
+        if key.dtype not in (np.uint32, np.uint64) or instr.dtype not in (np.uint16, np.uint32):
+            raise TypeError("packed trace: key uint32/uint64, instr uint16/uint32")
+        for a in (key, tidop, instr):
+            if not a.flags.c_contiguous:
+                raise ValueError("packed trace columns must be contiguous")
+        p = _Packed()
+        p.cfg.blocks, p.cfg.warps, p.cfg.lanes = cfg
+        p.n_events = len(tidop)
+        p.key_bytes, p.instr_bytes = key.dtype.itemsize, instr.dtype.itemsize
+        p.key, p.tidop, p.instr = key.ctypes.data, tidop.ctypes.data, instr.ctypes.data
+        flags = (OPT_EAGER if eager else 0) | (OPT_HB if hb else 0)
+        o = _Opts(1 if inactive_opt else 0, flags, stream, shard[0], shard[1])
+        _check(self._L.gw_ctx_analyze_host_packed(self._c, C.byref(p), C.byref(o)))
+
     def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None,
                        eager=False, shard=(0, 1), profile=False, hb=False) -> None:
         """shard=(index, count): report only races on location-key range `index`
@@ -377,6 +411,16 @@ class Context:
         n = C.c_uint32(0)
         _check(self._L.gw_ctx_kernel_times(self._c, cap, names, ms, cnt, C.byref(n)))
         return {names[i].value.decode(): (float(ms[i]), int(cnt[i])) for i in range(n.value)}
+
+
+def pack_columns(key, instr):
+    """The narrowest packed widths holding every value (gw_trace_packed):
+    key as uint32 when every key < 2^32, instr as uint16 when < 2^16."""
+    key = np.asarray(key, np.uint64)
+    instr = np.asarray(instr, np.uint32)
+    k = key.astype(np.uint32) if len(key) == 0 or int(key.max()) < (1 << 32) else key
+    i = instr.astype(np.uint16) if len(instr) == 0 or int(instr.max()) < (1 << 16) else instr
+    return k, i
 
 
 _default_ctx: Context | None = None

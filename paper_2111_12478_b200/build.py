@@ -7,7 +7,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", "engine.cu"), os.path.join(HERE, "csrc", "parse.cpp")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("primitives.cuh", "walker.cuh", "walker_warp.cuh",
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("primitives.cuh", "walker.cuh", "walker_warp.cuh", "bucket.cuh", "workloads.cuh",
                                                          "access.cuh", "common.h")]
 OUT = os.path.join(HERE, "libgwcp_b200.so")
 NVCC_FLAGS = [

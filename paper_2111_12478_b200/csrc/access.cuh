@@ -363,7 +363,8 @@ struct AccArgs {
   const uint32_t* vals;   // sorted event | VAL_W
   uint64_t n;             // sorted positions
   const uint2* carry;     // per tile: max (head pos + 1, write pos + 1) over all earlier tiles
-  const uint4* aux;       // per event: (tidop, time, vobj) -- see k_acc_keys
+  const uint4* aux;       // per event: (tidop, time, vobj) -- see k_acc_keys; nullptr: looked up lazily
+  StampSrc stamps;        // (aux == nullptr) stamp source of the lazy lookups
   const uint32_t* arena;
   int defer;
   int blockobj;           // clock objects are block-range objects (lock-free traces)
@@ -374,6 +375,14 @@ struct AccArgs {
   uint32_t large_cap;
   DupList dup;            // same-record pairs on one location (same-instruction check)
 };
+
+// (tidop, time, vobj) of event ev: the aux record, or (bucket pass spill and
+// large windows) the trace's tidop and a stamp lookup
+template <class K>
+__device__ __forceinline__ uint4 acc_aux(const AccArgs<K>& a, uint32_t ev) {
+  if (a.aux) return a.aux[ev];
+  return make_aux(a.stamps, ev, __ldg(a.tr.tidop + ev));
+}
 
 template <class K, int I>
 __global__ void __launch_bounds__(kThreads) k_acc_tilemax(const K* keys, const uint32_t* vals, uint64_t n,
@@ -423,13 +432,14 @@ __device__ __forceinline__ void acc_pos(const AccArgs<K>& a, const AccSmem<K, I>
     to = S.to[q - base];
   } else {
     ev = __ldg(a.vals + q) & VAL_E;
-    to = __ldg(&a.aux[ev].x);
+    to = a.aux ? __ldg(&a.aux[ev].x) : __ldg(a.tr.tidop + ev);
   }
 }
 template <class K, int I>
 __device__ __forceinline__ uint32_t acc_time(const AccArgs<K>& a, const AccSmem<K, I>& S, uint64_t base, uint64_t q,
                                              uint32_t ev, uint32_t) {
-  return q >= base ? S.st[q - base].x : __ldg(&a.aux[ev].y);
+  if (q >= base) return S.st[q - base].x;
+  return a.aux ? __ldg(&a.aux[ev].y) : acc_aux(a, ev).y;
 }
 // pred_t^{vo}[u] for the accessing thread tc
 template <class K>
@@ -462,7 +472,7 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
 #pragma unroll
       for (int k = 0; k < I; k++) {
         const uint32_t j = k * kThreads + threadIdx.x;
-        ax[k] = j < cnt ? a.aux[a.vals[base + j] & VAL_E] : make_uint4(0, 0, 0, 0);
+        ax[k] = j < cnt ? acc_aux(a, a.vals[base + j] & VAL_E) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int k = 0; k < I; k++) {
@@ -656,7 +666,7 @@ __global__ void k_large_check(AccArgs<K> a, const unsigned long long* keys, cons
     const uint32_t toq = a.tr.tidop[r], uq = ev_tid(toq);
     if (uq == ev_tid(toc)) continue;
     if (!cover(toq, toc, BS) &&
-        (a.defer || a.aux[r].y > acc_clock(a, a.aux[c].z, ev_tid(toc), uq)))
+        (a.defer || acc_aux(a, r).y > acc_clock(a, acc_aux(a, c).z, ev_tid(toc), uq)))
       emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), a.tr.key[c], r, c, GW_RW);
   }
 }

@@ -1,0 +1,530 @@
+// Bucketed access pass: the address-hashed shadow table of the north_star,
+// for lock-free traces of >= 2^24 events (C4, C5).
+//
+// Same semantics as k_access (gwcp.py:251-277; engine.py:81-95 via the dup
+// list), different data movement.  The per-location check needs only that
+// location's accesses in trace order, and the order in which LOCATIONS are
+// visited is irrelevant (candidates carry their own order keys), so instead
+// of a full LSD sort by location:
+//   h = fmix32(compacted location key)      -- a bijection of u32, so h
+//                                              identifies the location
+//   bucket = top bb bits of h               -- ~2,048 accesses per bucket
+//   two stable reduce-then-scan scatter passes (low, then high bucket digit)
+//   move the 12-byte access records (h, event|W, tidop) into bucket order,
+//   trace order kept inside a bucket;
+//   one CTA per bucket then loads the bucket into shared memory, sorts it
+//   by the remaining kb = 32 - bb bits of h (stable: the record index rides
+//   in the low bits of the sort word), finds segment heads / last writes
+//   with a block max-scan and evaluates the write check and the reader
+//   windows entirely out of shared memory.
+// Access stamps (time, pred object) are not materialised per event: only the
+// candidate pairs that pass the structural tests (u != t, !cover) look them
+// up in the walker's snapshot lists (StampSrc::get, L2-resident).
+// HBM traffic per access: trace read 12 B (+12 B for the first up-sweep),
+// 2 x (12 B read + 12 B write) for the passes, 4 B up-sweep of pass B,
+// 12 B in the check; against 176 B/access of the round-1 LSD pipeline.
+// Buckets larger than kBkCap records (hot locations) spill to the general
+// sort + k_access path (engine.cu, bucket_spill()).
+#pragma once
+#include "access.cuh"
+
+namespace gw {
+
+__device__ __forceinline__ uint32_t bk_hash(uint32_t x) {  // murmur3 fmix32 (bijective)
+  x ^= x >> 16;
+  x *= 0x85ebca6bu;
+  x ^= x >> 13;
+  x *= 0xc2b2ae35u;
+  x ^= x >> 16;
+  return x;
+}
+
+constexpr int kBkCap = 4096;      // records of one bucket in shared memory
+constexpr int kBkIdxBits = 12;    // record index bits of the in-bucket sort word
+constexpr int kBkSortBits = 8;    // in-bucket radix digit
+static_assert((1 << kBkIdxBits) == kBkCap, "index bits");
+constexpr int kBkMinBits = 12, kBkMaxBits = 20;  // bucket bits: 32 - kb with kb + kBkIdxBits <= 32
+
+// super-tiles of the scatter passes: 2^(RB-7) tiles share one count row, so
+// the count array stays at 128 words per tile for any digit width
+template <int RB>
+struct BkPass {
+  static constexpr int ND = 1 << RB;
+  static constexpr int DPT = ND > kThreads ? ND / kThreads : 1;
+  static constexpr int ST = RB > 7 ? 1 << (RB - 7) : 1;
+};
+
+// ---- element sources --------------------------------------------------------
+// the trace itself (pass A): element i = event i; non-access events are skipped
+struct BkTraceSrc {
+  DevTrace tr;
+  KeyRuns kr;
+  __device__ __forceinline__ uint64_t n() const { return tr.n; }
+  // both columns are loaded unconditionally: independent loads, no round
+  // trip on the kind before the key load is issued
+  __device__ __forceinline__ bool get_h(uint64_t i, uint32_t& h) const {
+    const uint32_t t = __ldcs(tr.tidop + i);
+    const unsigned long long k = __ldcs(tr.key + i);
+    h = bk_hash((uint32_t)compact_key(k, kr));
+    return ev_kind(t) <= GW_K_WRITE;
+  }
+  __device__ __forceinline__ bool get(uint64_t i, uint32_t& h, uint32_t& v, uint32_t& t) const {
+    t = __ldcs(tr.tidop + i);
+    const unsigned long long k = __ldcs(tr.key + i);
+    h = bk_hash((uint32_t)compact_key(k, kr));
+    v = (uint32_t)i | (ev_kind(t) == GW_K_WRITE ? VAL_W : 0u);
+    return ev_kind(t) <= GW_K_WRITE;
+  }
+};
+// records of a previous pass (pass B)
+struct BkRecSrc {
+  const uint32_t* h;
+  const uint32_t* v;
+  const uint32_t* t;
+  uint64_t cnt;
+  __device__ __forceinline__ uint64_t n() const { return cnt; }
+  __device__ __forceinline__ bool get_h(uint64_t i, uint32_t& hh) const {
+    hh = h[i];
+    return true;
+  }
+  __device__ __forceinline__ bool get(uint64_t i, uint32_t& hh, uint32_t& vv, uint32_t& tt) const {
+    hh = h[i];
+    vv = v[i];
+    tt = t[i];
+    return true;
+  }
+};
+
+// ---- up-sweep: digit counts per super-tile (counts[d * nst + st]) ----------
+template <class Src, int RB>
+__global__ void __launch_bounds__(kThreads) k_bk_up(Src src, int shift, uint32_t* __restrict__ counts, uint64_t nst) {
+  constexpr int ND = BkPass<RB>::ND, ST = BkPass<RB>::ST;
+  __shared__ uint32_t hist[kRsWarps][ND];
+  const int w = threadIdx.x >> 5;
+  const uint64_t n = src.n();
+  for (uint64_t st = blockIdx.x; st < nst; st += gridDim.x) {
+    for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&hist[0][0])[d] = 0;
+    __syncthreads();
+    for (int sub = 0; sub < ST; sub++) {
+      const uint64_t base = (st * ST + sub) * kTile;
+      if (base >= n) break;
+      uint32_t hh[kItems];
+      bool ok[kItems];
+#pragma unroll
+      for (int k = 0; k < kItems; k++) {
+        const uint64_t i = base + (uint64_t)k * kThreads + threadIdx.x;
+        ok[k] = i < n && src.get_h(i, hh[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < kItems; k++)
+        if (ok[k]) atomicAdd(&hist[w][(hh[k] >> shift) & (ND - 1)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < ND; d += kThreads) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int x = 0; x < kRsWarps; x++) c += hist[x][d];
+      counts[(uint64_t)d * nst + st] = c;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- down-sweep: stable scatter of the records by digit ---------------------
+template <int RB>
+struct BkDownSmem {
+  static constexpr int ND = BkPass<RB>::ND;
+  uint32_t wc[kRsWarps][ND];  // per-warp digit counts -> per-warp offsets within the digit
+  uint32_t toff[ND];          // tile-local start of digit d
+  uint32_t gbase[ND];         // global start of this tile's digit-d run
+  uint32_t sh[kTile], sv[kTile], st[kTile];
+  uint32_t cnt;
+};
+template <class Src, int RB>
+__global__ void __launch_bounds__(kThreads, 2) k_bk_down(Src src, int shift, const uint32_t* __restrict__ offsets,
+                                                        uint64_t nst, uint32_t* __restrict__ oh,
+                                                        uint32_t* __restrict__ ov, uint32_t* __restrict__ ot) {
+  constexpr int ND = BkPass<RB>::ND, DPT = BkPass<RB>::DPT, ST = BkPass<RB>::ST;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  BkDownSmem<RB>& S = *reinterpret_cast<BkDownSmem<RB>*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  const uint64_t n = src.n();
+  for (uint64_t stl = blockIdx.x; stl < nst; stl += gridDim.x) {
+    for (int d = threadIdx.x; d < ND; d += kThreads) S.gbase[d] = offsets[(uint64_t)d * nst + stl];
+    for (int sub = 0; sub < ST; sub++) {
+      const uint64_t tbase = (stl * ST + sub) * kTile;
+      if (tbase >= n) break;
+      for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
+      __syncthreads();
+      const uint64_t wbase = tbase + (uint64_t)w * kRsPerWarp;
+      uint32_t hh[kRsRounds], vv[kRsRounds], tt[kRsRounds], rd[kRsRounds];
+#pragma unroll
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint64_t i = wbase + (uint64_t)r * 32 + lane;
+        const bool ok = i < n && src.get(i, hh[r], vv[r], tt[r]);
+        rd[r] = ok ? ((hh[r] >> shift) & (ND - 1)) << 16 : (uint32_t)ND << 16;
+      }
+#pragma unroll
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint32_t d = rd[r] >> 16;
+        const uint32_t peers = warp_peers<RB + 1>(d);
+        const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
+        __syncwarp();
+        if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+        rd[r] |= before + __popc(peers & lt);
+        __syncwarp();
+      }
+      __syncthreads();
+      {
+        uint32_t tot[DPT], csum = 0;
+#pragma unroll
+        for (int j = 0; j < DPT; j++) {
+          const int d = threadIdx.x * DPT + j;
+          uint32_t run = 0;
+          if (d < ND) {
+#pragma unroll
+            for (int ww = 0; ww < kRsWarps; ww++) {
+              const uint32_t t = S.wc[ww][d];
+              S.wc[ww][d] = run;
+              run += t;
+            }
+          }
+          tot[j] = run;
+          csum += run;
+        }
+        uint32_t ct;
+        uint32_t cex = block_excl_scan<uint32_t, OpSum>(csum, OpSum(), 0u, &ct);
+#pragma unroll
+        for (int j = 0; j < DPT; j++) {
+          const int d = threadIdx.x * DPT + j;
+          if (d < ND) S.toff[d] = cex;
+          cex += tot[j];
+        }
+        if (threadIdx.x == 0) S.cnt = ct;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint32_t d = rd[r] >> 16;
+        if (d < (uint32_t)ND) {
+          const uint32_t pos = stg<uint32_t>(S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu));
+          S.sh[pos] = hh[r];
+          S.sv[pos] = vv[r];
+          S.st[pos] = tt[r];
+        }
+      }
+      __syncthreads();
+      const uint32_t cnt = S.cnt;
+#pragma unroll 4
+      for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+        const uint32_t p = stg<uint32_t>(i);
+        const uint32_t h = S.sh[p];
+        const uint32_t d = (h >> shift) & (ND - 1);
+        const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
+        oh[gp] = h;
+        ov[gp] = S.sv[p];
+        ot[gp] = S.st[p];
+      }
+      __syncthreads();
+      for (int d = threadIdx.x; d < ND; d += kThreads) {
+        const uint32_t end = d + 1 < ND ? S.toff[d + 1] : cnt;
+        S.gbase[d] += end - S.toff[d];
+      }
+      __syncthreads();
+    }
+  }
+}
+template <class Src, int RB>
+inline void bk_down_setup() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_bk_down<Src, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BkDownSmem<RB>));
+    done = true;
+  }
+}
+
+// ---- bucket starts: bstart[b] = first record of bucket b (bstart[NB] = n) ---
+__global__ void k_bk_bounds(const uint32_t* __restrict__ h, uint64_t n, int kb, uint32_t NB, uint32_t* bstart) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = h[i] >> kb;
+    const uint32_t pb = i > 0 ? h[i - 1] >> kb : 0u;
+    if (i == 0)
+      for (uint32_t x = 0; x <= b; x++) bstart[x] = 0;
+    else
+      for (uint32_t x = pb + 1; x <= b; x++) bstart[x] = (uint32_t)i;
+    if (i + 1 == n)
+      for (uint32_t x = b + 1; x <= NB; x++) bstart[x] = (uint32_t)n;
+  }
+}
+
+// ---- the per-bucket check ---------------------------------------------------
+struct BkCheckArgs {
+  DevTrace tr;
+  const uint32_t* h;       // bucketed records
+  const uint32_t* v;
+  const uint32_t* t;
+  const uint32_t* bstart;  // NB + 1 bucket starts
+  uint32_t NB;
+  int kb;                  // in-bucket key bits
+  StampSrc stamps;
+  const uint32_t* arena;   // clock objects (block-range objects: lock-free traces)
+  Cands c;
+  DupList dup;
+  uint32_t* large_i;       // writes with > kSmallWin reads since the last write (global record positions)
+  uint32_t* large_ws;
+  uint32_t* n_large;
+  uint32_t large_cap;
+  uint32_t* gsorted;       // in-bucket sorted event|W of the buckets holding a large window
+  uint32_t* spill;         // (start, count) of the buckets above kBkCap
+  uint32_t* n_spill;
+  uint32_t spill_cap;
+};
+
+// A bucket's three record arrays arrive by TMA bulk copies (one round trip
+// per bucket, the other resident CTA computing meanwhile), 16-byte aligned:
+// the copy starts up to 3 records early, so buffers hold kBkCap + 8 words.
+constexpr int kBkBuf = kBkCap + 8;
+struct BkSmem {
+  uint32_t V[kBkBuf];      // event | VAL_W, record order (from V + off)
+  uint32_t T[kBkBuf];      // tidop, record order (from T + off)
+  uint32_t H[kBkBuf];      // h (TMA), then the ping-pong half of the sort
+  uint32_t P[kBkCap];      // sort words (key << kBkIdxBits | record)
+  uint32_t LW[kBkCap];     // last write position + 1 (inclusive)
+  uint32_t wc[kRsWarps][1 << kBkSortBits];
+  uint32_t toff[1 << kBkSortBits];
+  unsigned long long mbar;
+  uint32_t large;
+};
+
+// one stable LSD pass of the in-bucket sort (bits [shift, shift + kBkSortBits))
+__device__ __forceinline__ void bk_sort_pass(BkSmem& S, const uint32_t* in, uint32_t* out, uint32_t M, int shift) {
+  constexpr int ND = 1 << kBkSortBits;
+  constexpr int R = kBkCap / kRsWarps / 32;  // rounds per warp (16)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  const uint32_t span = ((M + kRsWarps * 32 - 1) / (kRsWarps * 32)) * 32;  // records per warp
+  const uint32_t nr = span / 32;
+  for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
+  __syncthreads();
+  uint32_t x[R], rd[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    if ((uint32_t)r < nr) {
+      const uint32_t j = w * span + r * 32 + lane;
+      const bool ok = j < M;
+      x[r] = ok ? in[j] : 0u;
+      const uint32_t d = ok ? (x[r] >> shift) & (ND - 1) : (uint32_t)ND;
+      const uint32_t peers = warp_peers<kBkSortBits + 1>(d);
+      const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
+      __syncwarp();
+      if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+      rd[r] = (d << 16) | (before + __popc(peers & lt));
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;  // ND == kThreads
+    uint32_t run = 0;
+#pragma unroll
+    for (int ww = 0; ww < kRsWarps; ww++) {
+      const uint32_t t = S.wc[ww][d];
+      S.wc[ww][d] = run;
+      run += t;
+    }
+    uint32_t ct;
+    S.toff[d] = block_excl_scan<uint32_t, OpSum>(run, OpSum(), 0u, &ct);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    if ((uint32_t)r < nr) {
+      const uint32_t d = rd[r] >> 16;
+      if (d < (uint32_t)ND) out[S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu)] = x[r];
+    }
+  }
+  __syncthreads();
+}
+
+// pred_t^{vo}[u] for the accessing thread tc: lock-free clock objects are
+// block-range objects of tc's block (acc_clock, blockobj case)
+__device__ __forceinline__ uint32_t bk_clock(const BkCheckArgs& a, uint32_t vo, uint32_t tc, uint32_t u) {
+  const uint32_t BS = a.tr.BS;
+  if (vo == NIL || u / BS != tc / BS) return 0u;
+  return __ldg(optr(a.arena, vo) + OBJ_HDR + (u - (tc / BS) * BS));
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_bk_check(BkCheckArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
+  constexpr uint32_t IDXM = kBkCap - 1;
+  constexpr int IPT = kBkCap / kThreads;
+  const uint32_t BS = a.tr.BS;
+  const int npass = (a.kb + kBkSortBits - 1) / kBkSortBits;
+  const uint32_t kmask = (1u << a.kb) - 1u;
+  if (threadIdx.x == 0) {
+    mbar_init(&S.mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (uint32_t b = blockIdx.x; b < a.NB; b += gridDim.x) {
+    const uint32_t s = a.bstart[b], M = a.bstart[b + 1] - s;
+    if (M == 0) continue;
+    if (M > (uint32_t)kBkCap) {  // hot locations: the general path (bucket_spill)
+      if (threadIdx.x == 0) {
+        const uint32_t k = atomicAdd(a.n_spill, 1u);
+        if (k < a.spill_cap) { a.spill[2 * k] = s; a.spill[2 * k + 1] = M; }
+      }
+      continue;
+    }
+    const uint32_t a0 = s & ~3u, off = s - a0;
+    const uint32_t bytes = ((off + M + 3u) & ~3u) * 4u;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the previous bucket's generic accesses
+      mbar_expect_tx(&S.mbar, 3u * bytes);
+      bulk_g2s(S.H, a.h + a0, bytes, &S.mbar);
+      bulk_g2s(S.V, a.v + a0, bytes, &S.mbar);
+      bulk_g2s(S.T, a.t + a0, bytes, &S.mbar);
+      S.large = 0;
+    }
+    while (!mbar_try_wait(&S.mbar, phase)) {
+    }
+    phase ^= 1u;
+    const uint32_t* V = S.V + off;
+    const uint32_t* T = S.T + off;
+    for (uint32_t j = threadIdx.x; j < M; j += kThreads) S.P[j] = ((S.H[off + j] & kmask) << kBkIdxBits) | j;
+    __syncthreads();
+    // group by location: stable LSD radix on the in-bucket key bits (P <-> H)
+    uint32_t* buf[2] = {S.P, S.H};
+    int cur = 0;
+    for (int p = 0; p < npass; p++) {
+      bk_sort_pass(S, buf[cur], buf[cur ^ 1], M, kBkIdxBits + p * kBkSortBits);
+      cur ^= 1;
+    }
+    const uint32_t* SP = buf[cur];
+    uint32_t* SS = buf[cur ^ 1];  // segment start of each sorted position
+    // segment heads / last writes: blocked max-scan over the sorted positions
+    {
+      const uint32_t p0 = threadIdx.x * IPT;
+      uint2 agg = make_uint2(0, 0);
+#pragma unroll
+      for (int k = 0; k < IPT; k++) {
+        const uint32_t p = p0 + k;
+        if (p < M) {
+          const uint32_t x = SP[p];
+          if (p == 0 || (x >> kBkIdxBits) != (SP[p - 1] >> kBkIdxBits)) agg.x = p + 1;
+          if (V[x & IDXM] & VAL_W) agg.y = p + 1;
+        }
+      }
+      uint2 tot;
+      uint2 run = block_excl_scan<uint2, OpMax2>(agg, OpMax2(), make_uint2(0, 0), &tot);
+#pragma unroll
+      for (int k = 0; k < IPT; k++) {
+        const uint32_t p = p0 + k;
+        if (p < M) {
+          const uint32_t x = SP[p];
+          if (p == 0 || (x >> kBkIdxBits) != (SP[p - 1] >> kBkIdxBits)) run.x = p + 1;
+          if (V[x & IDXM] & VAL_W) run.y = p + 1;
+          SS[p] = run.x - 1;
+          S.LW[p] = run.y;
+        }
+      }
+    }
+    __syncthreads();
+    // the checks (gwcp.py:251-269), one sorted position per thread and step
+    for (uint32_t p = threadIdx.x; p < M; p += kThreads) {
+      const uint32_t jx = SP[p] & IDXM;
+      const uint32_t vx = V[jx], toc = T[jx];
+      const uint32_t c = vx & VAL_E, tc = ev_tid(toc);
+      const bool isw = (vx & VAL_W) != 0;
+      const uint32_t ss = SS[p];
+      const uint32_t lw = p > 0 ? S.LW[p - 1] : 0u;
+      const bool hasw = lw > 0 && lw - 1 >= ss;
+      const uint32_t W = hasw ? lw - 1 : NIL;
+      uint32_t vo = NIL;
+      bool have_vo = false;
+      unsigned long long loc = 0;
+      if (p > ss && (toc & GW_F_CONT) && a.dup.ev) {
+        // the previous access to this location may be in the same record
+        const uint32_t pe = V[SP[p - 1] & IDXM] & VAL_E;
+        if (pe < c && c - pe < 32) {
+          bool same = true;
+          for (uint32_t x = pe + 1; x < c && same; x++) same = (__ldg(a.tr.tidop + x) & GW_F_CONT) != 0;
+          if (same) {
+            const uint32_t kk = atomicAdd(a.dup.n, 1u);
+            if (kk < a.dup.cap) a.dup.ev[kk] = c;
+          }
+        }
+      }
+      if (hasw) {
+        const uint32_t jw = SP[W] & IDXM;
+        const uint32_t pw = V[jw] & VAL_E, top = T[jw], u = ev_tid(top);
+        if (u != tc && !cover(top, toc, BS)) {
+          if (!have_vo) { vo = a.stamps.get(c, tc).y; have_vo = true; }
+          if (a.stamps.get(pw, u).x > bk_clock(a, vo, tc, u)) {
+            loc = a.tr.key[c];
+            emit_cand(a.c, ((unsigned long long)c << 32) | SUB_WCHECK, loc, pw, c, isw ? GW_WW : GW_WR);
+          }
+        }
+      }
+      if (!isw) continue;
+      const uint32_t ws = hasw ? W + 1 : ss;
+      const uint32_t m = p - ws;
+      if (m == 0) continue;
+      if (m > kSmallWin) {
+        const uint32_t kk = atomicAdd(a.n_large, 1u);
+        if (kk < a.large_cap) { a.large_i[kk] = s + p; a.large_ws[kk] = s + ws; }
+        else atomicOr(a.c.err, ERR_CAND);
+        S.large = 1;
+        continue;
+      }
+      // readers since W: one candidate per thread (its latest read), ranked by its first read
+      for (uint32_t q = ws; q < p; q++) {
+        const uint32_t jq = SP[q] & IDXM;
+        const uint32_t toq = T[jq], uq = ev_tid(toq);
+        if (uq == tc) continue;
+        bool later = false;
+        for (uint32_t q2 = q + 1; q2 < p && !later; q2++) later = ev_tid(T[SP[q2] & IDXM]) == uq;
+        if (later) continue;
+        uint32_t first = q;
+        for (uint32_t q3 = ws; q3 < q; q3++)
+          if (ev_tid(T[SP[q3] & IDXM]) == uq) { first = q3; break; }
+        if (cover(toq, toc, BS)) continue;
+        const uint32_t r = V[jq] & VAL_E;
+        if (!have_vo) { vo = a.stamps.get(c, tc).y; have_vo = true; }
+        if (a.stamps.get(r, uq).x > bk_clock(a, vo, tc, uq)) {
+          if (!loc) loc = a.tr.key[c];
+          emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), loc, r, c, GW_RW);
+        }
+      }
+    }
+    __syncthreads();
+    if (S.large)  // the large-window pass reads this bucket's sorted order from global memory
+      for (uint32_t p = threadIdx.x; p < M; p += kThreads) a.gsorted[s + p] = V[SP[p] & IDXM];
+    __syncthreads();
+  }
+}
+inline void bk_check_setup() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_bk_check, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BkSmem));
+    done = true;
+  }
+}
+
+// spilled buckets -> (h, event|W) arrays for the general sort + k_access path
+__global__ void k_bk_spill_gather(const uint32_t* __restrict__ h, const uint32_t* __restrict__ v,
+                                  const uint32_t* spill, const uint32_t* soff, uint32_t nsp, uint32_t* kout,
+                                  uint32_t* vout) {
+  for (uint32_t k = blockIdx.x; k < nsp; k += gridDim.x) {
+    const uint32_t s = spill[2 * k], m = spill[2 * k + 1], o = soff[k];
+    for (uint32_t j = threadIdx.x; j < m; j += blockDim.x) {
+      kout[o + j] = h[s + j];
+      vout[o + j] = v[s + j];
+    }
+  }
+}
+
+}  // namespace gw

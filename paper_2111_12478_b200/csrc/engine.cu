@@ -18,7 +18,7 @@
 #include <thread>
 #include <vector>
 
-#include "access.cuh"
+#include "bucket.cuh"
 #include "workloads.cuh"
 #include "common.h"
 
@@ -77,6 +77,7 @@ struct Plan {
   const void *key = nullptr, *tidop = nullptr, *instr = nullptr;
   cudaStream_t stream = 0;
   unsigned long long n_bar = 0, n_end = 0, n_wbar = 0, D = 0;
+  unsigned long long n_acc = 0;  // the bucketed access pass sizes its passes by it
   uint64_t cand_cap = 0;
   uint32_t launches = 0;
   bool hard_small = false;  // snapshot mode with a one-launch hard-event list: a branch from the graph start
@@ -130,6 +131,10 @@ struct gw_ctx {
   }
   // side stream of the lock-free fork (access sort concurrent with the sync pass)
   cudaStream_t side = nullptr, side2 = nullptr;
+  // packed host input (gw_ctx_analyze_host_packed): chunk uploads on their own stream
+  cudaStream_t copy_st = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  cudaEvent_t ev_prev = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_hard = nullptr;
   uint32_t epoch = 1;  // look-back flag epochs (never reused within 2^24 passes)
   // last analysis, for an eager re-run after a graph abort
@@ -205,7 +210,7 @@ namespace {
 // scalar slots of the "scalars" buffer
 constexpr size_t kResHdr = 256;  // scalar mirror at the head of gw_ctx::hres
 enum : int { SC_MAXD = 0, SC_NINCS, SC_TICKET, SC_REC, SC_LOG, SC_DIAG, SC_ERR, SC_ABORT, SC_NCAND, SC_NLARGE,
-             SC_NSURV, SC_NQ, SC_NQLARGE, SC_NDUP, SC_NHEADS, SC_COUNT = 16 };
+             SC_NSURV, SC_NQ, SC_NQLARGE, SC_NDUP, SC_NHEADS, SC_NSPILL, SC_NLARGE2, SC_COUNT = 24 };
 
 __global__ void k_init_stats(Stats* s) {
   memset(s, 0, sizeof(Stats));
@@ -213,15 +218,16 @@ __global__ void k_init_stats(Stats* s) {
 }
 // graph mode: the trace must have the shape the plan was built for
 __global__ void k_plan_check(const Stats* s, unsigned long long n_bar, unsigned long long n_end,
-                             unsigned long long n_wbar, unsigned long long D, uint32_t* abort_flag) {
+                             unsigned long long n_wbar, unsigned long long D, unsigned long long n_acc,
+                             uint32_t* abort_flag) {
   const bool ok = s->n_acq == 0 && s->n_rel == 0 && s->n_bar == n_bar && s->n_end == n_end && s->n_long == 0 &&
-                  s->n_wbar == n_wbar &&
+                  s->n_wbar == n_wbar && s->n_acc == n_acc &&
                   ((s->key_or ^ s->key_and) & ~D) == 0ull;
   if (!ok) atomicOr(abort_flag, 1u);
 }
 __global__ void k_guard(const uint32_t* ncand, uint32_t cap, const uint32_t* nlarge, const uint32_t* ndup,
-                        uint32_t dupcap, uint32_t* abort_flag) {
-  if (*ncand > cap || *nlarge > 0 || *ndup > dupcap) atomicOr(abort_flag, 1u);
+                        uint32_t dupcap, uint32_t* abort_flag, const uint32_t* nspill = nullptr) {
+  if (*ncand > cap || *nlarge > 0 || *ndup > dupcap || (nspill && *nspill > 0)) atomicOr(abort_flag, 1u);
 }
 
 struct Pipeline {
@@ -416,7 +422,7 @@ struct Pipeline {
 
   // observed by an eager run, used to build a Plan
   Stats obs{};
-  uint32_t obs_ncand = 0, obs_nlarge = 0;
+  uint32_t obs_ncand = 0, obs_nlarge = 0, obs_nspill = 0;
   unsigned long long obs_D = 0;
   uint64_t obs_cand_cap = 0;
   bool obs_snap = false;
@@ -480,7 +486,7 @@ struct Pipeline {
       hs.n_wbar = P->n_wbar;
       hs.key_or = P->D;
       hs.key_and = 0;
-      GW_LAUNCH(k_plan_check, 1, 1, 0, st, dst, P->n_bar, P->n_end, P->n_wbar, P->D, scal + SC_ABORT);
+      GW_LAUNCH(k_plan_check, 1, 1, 0, st, dst, P->n_bar, P->n_end, P->n_wbar, P->D, P->n_acc, scal + SC_ABORT);
     } else {
       d2h(&hs, dst);
       obs = hs;
@@ -551,11 +557,11 @@ struct Pipeline {
       if (!early_fork) fork_sort();
       pbeg(PH_WALKER);
       walker_phase();
-      GW_LAUNCH(k_acc_aux, grid_for(N), kThreads, 0, st, tr, stamps, aux);
+      if (!bk_mode) GW_LAUNCH(k_acc_aux, grid_for(N), kThreads, 0, st, tr, stamps, aux);
       pend(PH_WALKER);
       CK(cudaStreamWaitEvent(st, C->ev_join, 0));
       pbeg(PH_CHECK);
-      cd = check_pass(false, "c", SC_NCAND);
+      cd = bk_mode ? bucket_check_pass() : check_pass(false, "c", SC_NCAND);
       pend(PH_CHECK);
     } else if (!has_locks) {
       pbeg(PH_WALKER);
@@ -565,7 +571,7 @@ struct Pipeline {
       access_sort();
       pend(PH_SORT);
       pbeg(PH_CHECK);
-      cd = check_pass(false, "c", SC_NCAND);
+      cd = bk_mode ? bucket_check_pass() : check_pass(false, "c", SC_NCAND);
       pend(PH_CHECK);
     } else {
       // lock mode: the structural candidates first (clock independent), then
@@ -702,7 +708,8 @@ struct Pipeline {
       CK(cudaEventCreateWithFlags(&C->ev_join, cudaEventDisableTiming));
     }
     const cudaStream_t main_st = st;
-    aux = C->get<uint4>("acc_aux", tr.n);  // allocated (and zeroed) on this stream: k_acc_aux writes it here
+    plan_access();
+    if (!bk_mode) aux = C->get<uint4>("acc_aux", tr.n);  // allocated (and zeroed) on this stream: k_acc_aux writes it here
     CK(cudaEventRecord(C->ev_fork, main_st));
     CK(cudaStreamWaitEvent(C->side, C->ev_fork, 0));
     st = C->side;
@@ -858,12 +865,21 @@ struct Pipeline {
 
   // ------------------------------------------------- access sort + scan
   // split: keys / vals only (the stamps are filled later by k_acc_aux)
-  void access_sort(bool split = false) {
-    const uint64_t N = tr.n;
+  // key runs of the location keys, and the choice of access pass
+  void plan_access() {
     kr = key_runs(gmode ? P->D : (hs.n_acc ? hs.key_or ^ hs.key_and : 0ull));
     C->stats.sort_bits = kr.nbits;
     wide = kr.nbits > 32;
     obs_D = hs.n_acc ? hs.key_or ^ hs.key_and : 0ull;
+    bk_mode = bucket_ok(gmode ? P->n_acc : hs.n_acc);
+  }
+  void access_sort(bool split = false) {
+    const uint64_t N = tr.n;
+    plan_access();
+    if (bk_mode) {
+      bucket_sort();
+      return;
+    }
     int nbits = kr.nbits;
     uint64_t NA = N;
     aux = C->get<uint4>("acc_aux", N);
@@ -946,6 +962,233 @@ struct Pipeline {
     else
       GW_LAUNCH((k_acc_tilemax<uint32_t, kAccItemsSmall>), tg, kThreads, 0, st, (const uint32_t*)skeys, vals, NA, agg);
     scan<uint2, OpMax2>(ArrLoad<uint2>{agg}, ArrStore<uint2>{carry}, nt, OpMax2(), make_uint2(0, 0), false, "sc_u2");
+  }
+
+  // ---------------------------------------- bucketed access pass (bucket.cuh)
+  bool bk_mode = false;
+  int bk_bb = 0, bk_kb = 0, bk_bA = 0, bk_bB = 0;
+  uint64_t bk_na = 0;
+  uint32_t *bk_h = nullptr, *bk_v = nullptr, *bk_t = nullptr, *bk_start = nullptr;
+  bool bucket_ok(uint64_t na) const {
+    const char* e = getenv("GW_BUCKET");  // test hook: 0 = the LSD location sort, 1 = buckets at any size
+    if (e && e[0] == '0') return false;
+    const uint64_t minn = (e && e[0] == '1') ? 1ull : (1ull << 24);
+    return !has_locks && nshard <= 1 && !wide && kr.nbits > 0 && na >= minn && tr.n < (1ull << 31);
+  }
+  template <class Src, int RB>
+  void bk_pass_rb(Src src, uint64_t n_in, int shift, uint32_t* oh, uint32_t* ov, uint32_t* ot) {
+    constexpr int ND = BkPass<RB>::ND, ST = BkPass<RB>::ST;
+    const uint64_t nst = (lb_tiles(n_in) + ST - 1) / ST;
+    uint32_t* counts = C->get<uint32_t>(std::string("bk_counts") + sfx, nst * ND);
+    const unsigned g = (unsigned)std::min<uint64_t>(nst, 148ull * 16);
+    GW_LAUNCH((k_bk_up<Src, RB>), g, kThreads, 0, st, src, shift, counts, nst);
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nst * ND, OpSum(), 0u, false,
+                          "sc_u32");
+    bk_down_setup<Src, RB>();
+    GW_LAUNCH((k_bk_down<Src, RB>), g, kThreads, sizeof(BkDownSmem<RB>), st, src, shift, counts, nst, oh, ov, ot);
+  }
+  template <class Src>
+  void bk_pass(Src src, uint64_t n_in, int RB, int shift, uint32_t* oh, uint32_t* ov, uint32_t* ot) {
+    switch (RB) {
+      case 6: bk_pass_rb<Src, 6>(src, n_in, shift, oh, ov, ot); break;
+      case 7: bk_pass_rb<Src, 7>(src, n_in, shift, oh, ov, ot); break;
+      case 8: bk_pass_rb<Src, 8>(src, n_in, shift, oh, ov, ot); break;
+      case 9: bk_pass_rb<Src, 9>(src, n_in, shift, oh, ov, ot); break;
+      case 10: bk_pass_rb<Src, 10>(src, n_in, shift, oh, ov, ot); break;
+      default: throw CudaErr{GW_E_ARG, "bucket digit width out of range"};
+    }
+  }
+  // the access records (h, event|W, tidop) in bucket order (two stable passes)
+  void bucket_sort() {
+    const uint64_t na = gmode ? P->n_acc : hs.n_acc;
+    bk_na = na;
+    bk_bb = std::min(kBkMaxBits, std::max(kBkMinBits, ceil_log2(na) - 11));
+    bk_kb = 32 - bk_bb;
+    bk_bA = bk_bb - bk_bb / 2;
+    bk_bB = bk_bb / 2;
+    uint32_t* ah = C->get<uint32_t>("bk_ah", na);
+    uint32_t* av = C->get<uint32_t>("bk_av", na);
+    uint32_t* at = C->get<uint32_t>("bk_at", na);
+    bk_h = C->get<uint32_t>("bk_h", na);
+    bk_v = C->get<uint32_t>("bk_v", na);
+    bk_t = C->get<uint32_t>("bk_t", na);
+    BkTraceSrc ts{tr, kr};
+    bk_pass(ts, tr.n, bk_bA, bk_kb, ah, av, at);
+    BkRecSrc rs{ah, av, at, na};
+    bk_pass(rs, na, bk_bB, bk_kb + bk_bA, bk_h, bk_v, bk_t);
+    const uint32_t NB = 1u << bk_bb;
+    bk_start = C->get<uint32_t>("bk_start", (uint64_t)NB + 1);
+    GW_LAUNCH(k_bk_bounds, grid_for(na), kThreads, 0, st, bk_h, na, bk_kb, NB, bk_start);
+    na_sorted = na;
+    C->stats.n_sorted = na;
+    C->stats.sort_bits = bk_bb;
+  }
+  // large reader windows (> kSmallWin reads between two writes) of the
+  // positions in `a.vals`: (window, tid) groups through a secondary sort
+  void large_windows(AccArgs<uint32_t>& a, uint32_t nl) {
+    uint32_t* sizes = C->get<uint32_t>("lg_sz", nl + 1);
+    std::vector<uint32_t> hi(nl), hw(nl);
+    CK(cudaMemcpyAsync(hi.data(), a.large_i, sizeof(uint32_t) * nl, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hw.data(), a.large_ws, sizeof(uint32_t) * nl, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<uint32_t> off(nl);
+    uint64_t M = 0;
+    for (uint32_t k = 0; k < nl; k++) {
+      off[k] = (uint32_t)M;
+      M += hi[k] - hw[k];
+    }
+    CK(cudaMemcpyAsync(sizes, off.data(), sizeof(uint32_t) * nl, cudaMemcpyHostToDevice, st));
+    unsigned long long* lk = C->get<unsigned long long>("lg_k", M);
+    uint32_t* lv = C->get<uint32_t>("lg_v", M);
+    GW_LAUNCH(k_large_fill, std::min<uint32_t>(nl, 65535u), kThreads, 0, st, a.large_i, a.large_ws, sizes, nl, a.vals,
+              tr.tidop, lk, lv);
+    sort<unsigned long long>(lk, lv, M, 24 + ceil_log2(nl + 1), "lg");
+    GW_LAUNCH(k_large_check<uint32_t>, grid_for(M), kThreads, 0, st, a, lk, lv, M, nl);
+    check_launch();
+    CK(cudaStreamSynchronize(st));  // keeps off / hi / hw alive until the copies completed
+  }
+  AccArgs<uint32_t> bk_acc_args(const Cands& cd, const uint32_t* keys, const uint32_t* vals, uint64_t n,
+                                uint32_t* li, uint32_t* lws, uint32_t* nl, uint32_t lcap) {
+    AccArgs<uint32_t> a;
+    memset(&a, 0, sizeof a);
+    a.tr = tr;
+    a.keys = keys;
+    a.vals = vals;
+    a.n = n;
+    a.aux = nullptr;
+    a.stamps = stamps;
+    a.arena = w.arena;
+    a.defer = 0;
+    a.blockobj = 1;
+    a.c = cd;
+    a.large_i = li;
+    a.large_ws = lws;
+    a.n_large = nl;
+    a.large_cap = lcap;
+    a.dup = dup;
+    return a;
+  }
+  // buckets above kBkCap records: the LSD sort by h + k_access over them
+  void bucket_spill(const Cands& cd, const uint32_t* spill, uint32_t nsp) {
+    std::vector<uint32_t> hs2(2 * (size_t)nsp), off(nsp);
+    CK(cudaMemcpyAsync(hs2.data(), spill, sizeof(uint32_t) * 2 * nsp, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    uint64_t tot = 0;
+    for (uint32_t k = 0; k < nsp; k++) {
+      off[k] = (uint32_t)tot;
+      tot += hs2[2 * k + 1];
+    }
+    uint32_t* soff = C->get<uint32_t>("bsp_off", nsp);
+    CK(cudaMemcpyAsync(soff, off.data(), sizeof(uint32_t) * nsp, cudaMemcpyHostToDevice, st));
+    uint32_t* keys = C->get<uint32_t>("bsp_k", tot);
+    uint32_t* vals2 = C->get<uint32_t>("bsp_v", tot);
+    GW_LAUNCH(k_bk_spill_gather, std::min<uint32_t>(nsp, 65535u), kThreads, 0, st, bk_h, bk_v, spill, soff, nsp, keys,
+              vals2);
+    CK(cudaStreamSynchronize(st));  // off alive until the copy completed
+    sort<uint32_t>(keys, vals2, tot, 32, "bsp");
+    const uint64_t atile = (uint64_t)kThreads * kAccItemsSmall;
+    const uint64_t nt = (tot + atile - 1) / atile;
+    uint2* agg = C->get<uint2>("bsp_tagg", nt + 1);
+    uint2* car = C->get<uint2>("bsp_carry", nt + 1);
+    const unsigned tg = (unsigned)std::min<uint64_t>(std::max<uint64_t>(nt, 1), 148ull * 8);
+    GW_LAUNCH((k_acc_tilemax<uint32_t, kAccItemsSmall>), tg, kThreads, 0, st, (const uint32_t*)keys, vals2, tot, agg);
+    scan<uint2, OpMax2>(ArrLoad<uint2>{agg}, ArrStore<uint2>{car}, nt, OpMax2(), make_uint2(0, 0), false, "sc_u2");
+    const uint32_t lcap = (uint32_t)(tot / kSmallWin + 1);
+    uint32_t* li = C->get<uint32_t>("lg2_i", lcap);
+    uint32_t* lws = C->get<uint32_t>("lg2_ws", lcap);
+    CK(cudaMemsetAsync(scal + SC_NLARGE2, 0, sizeof(uint32_t), st));
+    AccArgs<uint32_t> a = bk_acc_args(cd, keys, vals2, tot, li, lws, scal + SC_NLARGE2, lcap);
+    a.carry = car;
+    acc_setup<uint32_t, kAccItemsSmall>();
+    const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>(nt, 1), 148ull * 16);
+    GW_LAUNCH((k_access<uint32_t, kAccItemsSmall>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsSmall>), st, a);
+    check_launch();
+    uint32_t nl = 0;
+    d2h(&nl, scal + SC_NLARGE2);
+    if (nl > lcap) throw CudaErr{GW_E_NOMEM, "large-window list overflow (spilled buckets)"};
+    if (nl) large_windows(a, nl);
+  }
+  // the check of the bucketed access pass (candidates as check_pass(false, ...))
+  Cands bucket_check_pass() {
+    const uint64_t NA = bk_na;
+    uint32_t* cnt = scal + SC_NCAND;
+    const uint32_t lcap = (uint32_t)(NA / kSmallWin + 1);
+    uint32_t* large_i = C->get<uint32_t>("lg_i", lcap);
+    uint32_t* large_ws = C->get<uint32_t>("lg_ws", lcap);
+    uint32_t* gsorted = C->get<uint32_t>("bk_gsorted", NA);
+    const uint32_t NB = 1u << bk_bb;
+    const uint32_t spill_cap = NB;
+    uint32_t* spill = C->get<uint32_t>("bk_spill", 2ull * spill_cap);
+    uint64_t cand_cap = gmode ? P->cand_cap : std::max<uint64_t>(65536, NA / 4);
+    Cands cd;
+    uint32_t hcnt[2] = {0, 0};
+    bk_check_setup();
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bk_check, kThreads, sizeof(BkSmem)));
+    const unsigned grid = (unsigned)std::min<uint64_t>(NB, (uint64_t)std::max(occ, 1) * C->num_sms);
+    for (int attempt = 0; attempt < 2; attempt++) {
+      cd = make_cands("c", cand_cap, cnt);
+      CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t), st));
+      CK(cudaMemsetAsync(scal + SC_NSURV, 0, sizeof(uint32_t), st));
+      CK(cudaMemsetAsync(scal + SC_NSPILL, 0, sizeof(uint32_t), st));
+      dup.ev = nullptr;
+      dup.n = scal + SC_NDUP;
+      dup.cap = 0;
+      if (hs.n_long == 0) {
+        dup.cap = (uint32_t)std::max<uint64_t>(4096, NA / 64);
+        dup.ev = C->get<uint32_t>("dup_ev", dup.cap);
+      }
+      CK(cudaMemsetAsync(scal + SC_NDUP, 0, 2 * sizeof(uint32_t), st));
+      BkCheckArgs ba;
+      memset(&ba, 0, sizeof ba);
+      ba.tr = tr;
+      ba.h = bk_h;
+      ba.v = bk_v;
+      ba.t = bk_t;
+      ba.bstart = bk_start;
+      ba.NB = NB;
+      ba.kb = bk_kb;
+      ba.stamps = stamps;
+      ba.arena = w.arena;
+      ba.c = cd;
+      ba.dup = dup;
+      ba.large_i = large_i;
+      ba.large_ws = large_ws;
+      ba.n_large = cnt + 1;
+      ba.large_cap = lcap;
+      ba.gsorted = gsorted;
+      ba.spill = spill;
+      ba.n_spill = scal + SC_NSPILL;
+      ba.spill_cap = spill_cap;
+      GW_LAUNCH(k_bk_check, grid, kThreads, sizeof(BkSmem), st, ba);
+      check_launch();
+      if (gmode) {
+        same_instr_pass(cd);
+        GW_LAUNCH(k_guard, 1, 1, 0, st, cnt, cd.cap, cnt + 1, scal + SC_NDUP, dup.cap, scal + SC_ABORT,
+                  (const uint32_t*)(scal + SC_NSPILL));
+        break;
+      }
+      uint32_t nsp = 0;
+      d2h(&nsp, scal + SC_NSPILL);
+      obs_nspill = nsp;
+      if (nsp) bucket_spill(cd, spill, nsp);
+      same_instr_pass(cd);
+      d2h(hcnt, cnt, 2);
+      if (hcnt[1] > lcap) throw CudaErr{GW_E_NOMEM, "large-window list overflow"};
+      if (hcnt[1] > 0) {
+        AccArgs<uint32_t> a = bk_acc_args(cd, nullptr, gsorted, NA, large_i, large_ws, cnt + 1, lcap);
+        large_windows(a, hcnt[1]);
+        d2h(hcnt, cnt, 1);
+      }
+      if (hcnt[0] <= cd.cap) break;
+      cand_cap = (uint64_t)hcnt[0] + 1024;
+      CK(cudaMemsetAsync(w.err, 0, sizeof(uint32_t), st));
+    }
+    obs_ncand = hcnt[0];
+    obs_nlarge = hcnt[1];
+    obs_cand_cap = cand_cap;
+    C->stats.n_candidates = hcnt[0];
+    return cd;
   }
 
   Cands make_cands(const std::string& tag, uint64_t cap, uint32_t* cnt) {
@@ -1404,6 +1647,9 @@ extern "C" void gw_ctx_destroy(gw_ctx* c) {
   if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
   if (c->ev_hard) cudaEventDestroy(c->ev_hard);
   if (c->side2) cudaStreamDestroy(c->side2);
+  for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
+  if (c->ev_prev) cudaEventDestroy(c->ev_prev);
+  if (c->copy_st) cudaStreamDestroy(c->copy_st);
   if (c->hres) cudaFreeHost(c->hres);
   delete c;
 }
@@ -1456,13 +1702,15 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   p.nshard = nshard;
   p.hb_mode = hb;
   p.run();
-  if (eager || tr.n == 0 || !p.obs_snap || p.obs_nlarge > 0 || p.obs.n_long > 0 || st == 0) return;
+  if (eager || tr.n == 0 || !p.obs_snap || p.obs_nlarge > 0 || p.obs_nspill > 0 || p.obs.n_long > 0 || st == 0)
+    return;
   // build the plan; run the graph-mode pipeline once for real (allocates every
   // buffer at its final size), then capture it
   Plan np;
   np.N = tr.n; np.B = tr.B; np.W = tr.W; np.L = tr.L; np.inactive_opt = inactive;
   np.key = kp; np.tidop = tp; np.instr = ip; np.stream = st;
   np.n_bar = p.obs.n_bar; np.n_end = p.obs.n_end; np.n_wbar = p.obs.n_wbar; np.D = p.obs_D;
+  np.n_acc = p.obs.n_acc;
   np.hard_small = p.obs_hard_small;
   np.cand_cap = 2ull * p.obs_ncand + 4096;  // tight: graph replays size the dedup / order passes by it
   c->plan = np;
@@ -1538,6 +1786,79 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
       CK(cudaMemcpyAsync(in, t->instr, 4 * N, cudaMemcpyHostToDevice, st));
     }
     DevTrace tr = make_dev(t, k, to, in);
+    analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,
+                 o && (o->flags & GW_OPT_PROFILE), o && (o->flags & GW_OPT_HB));
+  });
+}
+
+// packed (narrow-column) host trace: widen one uploaded chunk into the
+// 16-byte SoA the pipeline reads (the tidop column is uploaded in place)
+__global__ void k_widen(const void* __restrict__ kin, int kbytes, const void* __restrict__ iin, int ibytes,
+                        uint64_t lo, uint64_t hi, unsigned long long* __restrict__ kout, uint32_t* __restrict__ iout) {
+  for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    if (kbytes == 4) kout[e] = ((const uint32_t*)kin)[e];
+    if (ibytes == 2) iout[e] = ((const uint16_t*)iin)[e];
+  }
+}
+
+extern "C" int gw_ctx_analyze_host_packed(gw_ctx* c, const gw_trace_packed* t, const gw_opts* o) {
+  if (!c || !t) { gw_set_error("null argument"); return GW_E_ARG; }
+  if ((t->key_bytes != 4 && t->key_bytes != 8) || (t->instr_bytes != 2 && t->instr_bytes != 4)) {
+    gw_set_error("packed trace: key_bytes must be 4 or 8, instr_bytes 2 or 4");
+    return GW_E_ARG;
+  }
+  gw_trace_view view;
+  view.cfg = t->cfg;
+  view.n_events = t->n_events;
+  view.key = (const uint64_t*)t->key;
+  view.tidop = t->tidop;
+  view.instr = (const uint32_t*)t->instr;
+  int v = validate_view(&view);
+  if (v) return v;
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
+    const uint32_t inactive = o ? o->inactive_opt : 1u;
+    const uint32_t nsh = o && o->shard_count > 1 ? o->shard_count : 1u;
+    const uint32_t sh = nsh > 1 ? o->shard_index : 0u;
+    if (sh >= nsh) throw CudaErr{GW_E_ARG, "shard_index must be < shard_count"};
+    const uint64_t N = t->n_events;
+    c->last_stream = st;
+    unsigned long long* k = c->get<unsigned long long>("in_key", N);
+    uint32_t* to = c->get<uint32_t>("in_tidop", N);
+    uint32_t* in = c->get<uint32_t>("in_instr", N);
+    // narrow columns land in staging buffers, wide ones in place
+    void* kst = t->key_bytes == 8 ? (void*)k : (void*)c->get<uint32_t>("pk_key", N);
+    void* ist = t->instr_bytes == 4 ? (void*)in : (void*)c->get<uint16_t>("pk_instr", N);
+    if (!c->copy_st) {
+      CK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_prev, cudaEventDisableTiming));
+    }
+    // the copies must not overwrite buffers an earlier analysis on st may still read
+    CK(cudaEventRecord(c->ev_prev, st));
+    CK(cudaStreamWaitEvent(c->copy_st, c->ev_prev, 0));
+    constexpr uint64_t kChunk = 1ull << 25;  // events per upload chunk (~320 MB of C5 columns)
+    const uint64_t nch = (N + kChunk - 1) / kChunk;
+    while (c->chunk_ev.size() < nch) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->chunk_ev.push_back(e);
+    }
+    const bool widen = t->key_bytes == 4 || t->instr_bytes == 2;
+    for (uint64_t ch = 0; ch < nch; ch++) {
+      const uint64_t lo = ch * kChunk, hi = std::min(N, lo + kChunk), m = hi - lo;
+      CK(cudaMemcpyAsync((char*)kst + lo * t->key_bytes, (const char*)t->key + lo * t->key_bytes,
+                         m * t->key_bytes, cudaMemcpyHostToDevice, c->copy_st));
+      CK(cudaMemcpyAsync(to + lo, t->tidop + lo, m * 4, cudaMemcpyHostToDevice, c->copy_st));
+      CK(cudaMemcpyAsync((char*)ist + lo * t->instr_bytes, (const char*)t->instr + lo * t->instr_bytes,
+                         m * t->instr_bytes, cudaMemcpyHostToDevice, c->copy_st));
+      CK(cudaEventRecord(c->chunk_ev[ch], c->copy_st));
+      CK(cudaStreamWaitEvent(st, c->chunk_ev[ch], 0));  // widen chunk ch while chunk ch + 1 is in flight
+      if (widen) GW_LAUNCH(k_widen, grid_for(m, 148u * 8u), kThreads, 0, st, kst, (int)t->key_bytes, ist,
+                           (int)t->instr_bytes, lo, hi, k, in);
+    }
+    DevTrace tr = make_dev(&view, k, to, in);
     analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,
                  o && (o->flags & GW_OPT_PROFILE), o && (o->flags & GW_OPT_HB));
   });

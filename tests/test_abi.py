@@ -90,3 +90,14 @@ def test_result_views_own_the_library_buffers():
     del keep
     gc.collect()
     assert alive() is None  # the last view gone: gw_result_free ran
+
+
+def test_pack_columns_widths():
+    """gw_trace_packed widths: the narrowest holding every value."""
+    import numpy as np
+
+    k, i = N.pack_columns(np.array([1, 2**32 - 1], np.uint64), np.array([0, 2**16 - 1], np.uint32))
+    assert k.dtype == np.uint32 and i.dtype == np.uint16
+    assert k.tolist() == [1, 2**32 - 1] and i.tolist() == [0, 2**16 - 1]
+    k, i = N.pack_columns(np.array([2**32], np.uint64), np.array([2**16], np.uint32))
+    assert k.dtype == np.uint64 and i.dtype == np.uint32

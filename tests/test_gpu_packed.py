@@ -1,0 +1,76 @@
+"""The packed host input (gw_ctx_analyze_host_packed): narrow key / instr
+columns uploaded in chunks and widened on the device give the same reports
+as the 16-B SoA path, for every column-width combination."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_text
+from helpers import check_against_golden
+from oracle import oracle as O
+from paper_2111_12478_b200 import _native as N
+from paper_2111_12478_b200 import workloads as WL
+from paper_2111_12478_b200.report import ndjson_lines
+from paper_2111_12478_b200.trace import parse_trace
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = N.Context(0)
+    yield c
+    c.close()
+
+
+def _run_packed(ctx, tr, inactive_opt=True, **kw):
+    k, i = N.pack_columns(tr.key, tr.instr)
+    ctx.analyze_host_packed(tr.cfg_tuple, k, tr.tidop, i, inactive_opt=inactive_opt, **kw)
+    return ctx.fetch()
+
+
+def test_packed_input_reference_goldens(goldens, ctx):
+    widths = set()
+    n = 0
+    for r in goldens:
+        if "error" in r or "full" in r["tags"] or not ({"corpus", "nasty", "c1", "c3", "c4"} & set(r["tags"])):
+            continue
+        tr = parse_trace(golden_text(r))
+        k, i = N.pack_columns(tr.key, tr.instr)
+        widths.add((k.dtype.itemsize, i.dtype.itemsize))
+        check_against_golden(r, tr, _run_packed(ctx, tr, r["inactive_opt"]))
+        n += 1
+    assert n > 1000
+    # shared-memory keys (bit 63) need 8 bytes, warp-barrier lane masks 4 bytes of instr
+    assert {(4, 2), (8, 2), (8, 4)} <= widths
+    # the remaining combination: a 32-lane warp barrier mask with 4-byte keys
+    tr = parse_trace(WL.c4_text(blocks=2, warps=2, lanes=32, iters=8, words_per_block=256))
+    k, i = N.pack_columns(tr.key, tr.instr)
+    assert (k.dtype.itemsize, i.dtype.itemsize) == (4, 4)
+    assert ndjson_lines(tr, _run_packed(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
+
+
+def test_packed_input_full_c2_chunked(goldens, ctx):
+    """1.05 M events: several upload chunks are not needed at this size, so
+    also a multi-chunk trace below."""
+    r = next(r for r in goldens if r["name"] == "c2/full")
+    tr = WL.c2_soa()
+    check_against_golden(r, tr, _run_packed(ctx, tr))
+
+
+def test_packed_input_many_chunks(ctx):
+    """> 2^25 events: the upload runs as several chunks, each widened while the
+    next is in flight; the graph-replay path on a stream as in the bench."""
+    import torch
+
+    tr = WL.c2_soa(blocks=1024, warps=8, lanes=32, phases=2, records=80, words_per_block=262144, seed=5)
+    assert len(tr) > 2 * (1 << 25)
+    stream = torch.cuda.Stream(device=torch.device("cuda", 0))
+    ctx.analyze_host(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, stream=stream.cuda_stream)
+    want = ctx.fetch()
+    for _ in range(3):
+        got = _run_packed(ctx, tr, stream=stream.cuda_stream)
+        for f in ("kind", "prior", "current"):
+            assert np.array_equal(got[f], want[f])
+    assert ndjson_lines(tr, want) == ndjson_lines(tr, O.run_trace(tr))
+
