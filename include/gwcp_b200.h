@@ -147,6 +147,18 @@ int gw_validate(const gw_trace_view* t, uint64_t* n_out, uint32_t** ev, uint32_t
                 uint64_t** a, uint64_t** b);
 void gw_free(void* p);
 
+/* validate_trace on the GPU: same diagnostics, codes
+ * and order as gw_validate, computed with per-thread segmented passes
+ * (first END per thread, per-event / per-barrier checks, lock stacks walked
+ * per thread over the tid-sorted lock events).  host_trace: host SoA. */
+int gw_ctx_validate(gw_ctx* c, const gw_trace_view* host_trace, uint64_t* n_out, uint32_t** ev, uint32_t** code,
+                    uint64_t** a, uint64_t** b);
+/* infer_locks (trace.py:609-680) on the GPU: the rewritten trace (out, free
+ * with gw_trace_free) and one diagnostic per release left uninferred
+ * (event index in the INPUT trace, lock, thread), in event order. */
+int gw_ctx_infer_locks(gw_ctx* c, const gw_trace_view* host_trace, gw_trace* out, uint64_t* n_diag,
+                       uint32_t** diag_event, uint64_t** diag_lock, uint32_t** diag_tid);
+
 /* ---- analysis (replaces engine.run + GwcpDetector, engine.py:98-155, gwcp.py:103-356) */
 /* host SoA in, host results out: H2D, all kernels, D2H inside */
 int gw_analyze(const gw_trace_view* host_trace, const gw_opts* opts, gw_result* out);

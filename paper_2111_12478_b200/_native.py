@@ -127,6 +127,8 @@ EXPORTS = (
     "gw_ctx_analyze_device",
     "gw_ctx_analyze_host",
     "gw_ctx_analyze_host_packed",
+    "gw_ctx_validate",
+    "gw_ctx_infer_locks",
     "gw_ctx_fetch",
     "gw_ctx_stats",
     "gw_ctx_launches",
@@ -183,6 +185,14 @@ def lib():
         L.gw_ctx_analyze_host.restype = C.c_int
         L.gw_ctx_analyze_host_packed.argtypes = [C.c_void_p, C.POINTER(_Packed), C.POINTER(_Opts)]
         L.gw_ctx_analyze_host_packed.restype = C.c_int
+        L.gw_ctx_validate.argtypes = [C.c_void_p, C.POINTER(_View), C.POINTER(C.c_uint64),
+                                      C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.POINTER(C.c_uint32)),
+                                      C.POINTER(C.POINTER(C.c_uint64)), C.POINTER(C.POINTER(C.c_uint64))]
+        L.gw_ctx_validate.restype = C.c_int
+        L.gw_ctx_infer_locks.argtypes = [C.c_void_p, C.POINTER(_View), C.POINTER(_Trace), C.POINTER(C.c_uint64),
+                                         C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.POINTER(C.c_uint64)),
+                                         C.POINTER(C.POINTER(C.c_uint32))]
+        L.gw_ctx_infer_locks.restype = C.c_int
         L.gw_ctx_fetch.argtypes = [C.c_void_p, C.POINTER(_Result)]
         L.gw_ctx_fetch.restype = C.c_int
         L.gw_ctx_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
@@ -273,13 +283,19 @@ def _view(cfg, key, tidop, instr) -> _View:
     return v
 
 
-def validate(cfg, key, tidop, instr):
+def validate(cfg, key, tidop, instr, ctx=None):
+    """validate_trace diagnostics (event, code, a, b): on the GPU through a
+    context (gw_ctx_validate), or the host pass (gw_validate) when ctx is None."""
     L = lib()
     v = _view(cfg, key, tidop, instr)
     n = C.c_uint64(0)
     pe, pc = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)()
     pa, pb = C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint64)()
-    _check(L.gw_validate(C.byref(v), C.byref(n), C.byref(pe), C.byref(pc), C.byref(pa), C.byref(pb)))
+    if ctx is not None:
+        _check(L.gw_ctx_validate(ctx._c, C.byref(v), C.byref(n), C.byref(pe), C.byref(pc), C.byref(pa),
+                                 C.byref(pb)))
+    else:
+        _check(L.gw_validate(C.byref(v), C.byref(n), C.byref(pe), C.byref(pc), C.byref(pa), C.byref(pb)))
     k = int(n.value)
     try:
         out = [(int(pe[i]), int(pc[i]), int(pa[i]), int(pb[i])) for i in range(k)]
@@ -287,6 +303,24 @@ def validate(cfg, key, tidop, instr):
         for p in (pe, pc, pa, pb):
             L.gw_free(C.cast(p, C.c_void_p))
     return out
+
+
+def infer_locks(ctx, cfg, key, tidop, instr):
+    """infer_locks on the GPU (gw_ctx_infer_locks): ((cfg, key, tidop, instr)
+    of the rewritten trace, [(event, lock, tid)] of the uninferred releases)."""
+    L = lib()
+    v = _view(cfg, key, tidop, instr)
+    t = _Trace()
+    n = C.c_uint64(0)
+    pe, pl, pt = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint64)(), C.POINTER(C.c_uint32)()
+    _check(L.gw_ctx_infer_locks(ctx._c, C.byref(v), C.byref(t), C.byref(n), C.byref(pe), C.byref(pl), C.byref(pt)))
+    k = int(n.value)
+    try:
+        diags = [(int(pe[i]), int(pl[i]), int(pt[i])) for i in range(k)]
+    finally:
+        for p in (pe, pl, pt):
+            L.gw_free(C.cast(p, C.c_void_p))
+    return _take_trace(L, t), diags
 
 
 class _ResultOwner:

@@ -14,7 +14,7 @@ from typing import NoReturn
 from . import _native as N
 from .engine import diagnostics_of
 from .report import ndjson_lines
-from .trace import TraceParseError, UnsupportedTrace, load_trace, save_soa, validate_trace
+from .trace import TraceParseError, UnsupportedTrace, infer_locks, load_trace, save_soa, validate_trace
 
 EXIT_CLEAN = 0
 EXIT_RACES = 1
@@ -28,8 +28,9 @@ def _die(code: int, message: str) -> NoReturn:
     raise SystemExit(code)
 
 
-def _load(path: str, validate: bool = True):
-    """Text trace or binary SoA file (by magic, trace.load_trace)."""
+def _load(path: str, validate: bool = True, infer: bool = False):
+    """Text trace or binary SoA file (by magic, trace.load_trace); lock
+    inference and validate_trace run on the GPU (cli.py:26-43)."""
     try:
         tr = load_trace(path)
     except OSError as e:
@@ -40,7 +41,15 @@ def _load(path: str, validate: bool = True):
         _die(EXIT_USAGE, f"{path}: unsupported by the B200 engine: {e}")
     if not validate:
         return tr
-    diags = validate_trace(tr)
+    try:
+        ctx = N.default_context()
+        if infer:
+            tr, idiags = infer_locks(tr, ctx=ctx)
+            for d in idiags:
+                print(f"{path}: lock inference: {d}", file=sys.stderr)
+        diags = validate_trace(tr, ctx=ctx)
+    except (N.NativeUnavailable, N.EngineError) as e:
+        _die(EXIT_ENGINE, f"{path}: analysis engine failed: {e}")
     if diags:
         for d in diags:
             print(f"{path}: {d}", file=sys.stderr)
@@ -51,9 +60,9 @@ def _load(path: str, validate: bool = True):
 def _cmd_check(args) -> int:
     if args.detector not in ("gwcp", "hb"):
         _die(EXIT_USAGE, f"detector {args.detector!r} is not on the accelerated path (use gpurace)")
-    if args.infer_locks or args.order_matrix:
-        _die(EXIT_USAGE, "--infer-locks / --order-matrix are not on the accelerated path (use gpurace)")
-    tr = _load(args.trace)
+    if args.order_matrix:
+        _die(EXIT_USAGE, "--order-matrix is not on the accelerated path (use gpurace)")
+    tr = _load(args.trace, infer=args.infer_locks)
     try:
         res = N.analyze(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, inactive_opt=not args.no_inactive_opt,
                         hb=args.detector == "hb")

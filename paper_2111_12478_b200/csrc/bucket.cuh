@@ -42,8 +42,12 @@ __device__ __forceinline__ uint32_t bk_hash(uint32_t x) {  // murmur3 fmix32 (bi
 constexpr int kBkCap = 4096;      // records of one bucket in shared memory
 constexpr int kBkIdxBits = 12;    // record index bits of the in-bucket sort word
 constexpr int kBkSortBits = 8;    // in-bucket radix digit
+constexpr uint32_t kBkSlots = 1u << kBkSortBits, kBkEmpty = 0xFFFFFFFFu;
 static_assert((1 << kBkIdxBits) == kBkCap, "index bits");
-constexpr int kBkMinBits = 12, kBkMaxBits = 20;  // bucket bits: 32 - kb with kb + kBkIdxBits <= 32
+constexpr int kBkMinBits = 12, kBkMaxBits = 16;  // bucket bits: 32 - kb with kb + kBkIdxBits <= 32
+// buckets above kBkCap (up to kBkSubMax records) are split in the CTA into
+// <= 2^kBkSubBits sub-buckets in a per-CTA scratch that stays in L2
+constexpr int kBkSubBits = 4, kBkSubMax = 32768, kBkSubBuf = kBkSubMax + 8;
 
 // super-tiles of the scatter passes: 2^(RB-7) tiles share one count row, so
 // the count array stays at 128 words per tile for any digit width
@@ -244,6 +248,187 @@ inline void bk_down_setup() {
   }
 }
 
+// ---- the same scatter with TMA-streamed input tiles --------------------------
+// Full input tiles arrive by cp.async.bulk into a double buffer (the next
+// tile lands while this one is ranked, as k_rs_down_tma); the buffer of the
+// current tile is then reused as the digit-order staging of its three output
+// arrays.  Both sources are 48 KB per 4,096-element tile: the trace's key
+// (u64) + tidop columns, or the previous pass's (h, event|W, tidop).
+constexpr uint32_t kBkTileBytes = kTile * 12u;
+template <int RB>
+struct BkTmaSmem {
+  static constexpr int ND = BkPass<RB>::ND;
+  uint32_t buf[2][kTile * 3];
+  uint32_t wc[kRsWarps][ND];
+  uint32_t toff[ND];
+  uint32_t gbase[ND];
+  uint32_t cnt;
+  unsigned long long mbar[2];
+};
+__device__ __forceinline__ void bk_issue(const BkTraceSrc& s, uint64_t tile, uint32_t* dst, unsigned long long* m) {
+  bulk_g2s(dst, s.tr.key + tile * kTile, kTile * 8u, m);
+  bulk_g2s(dst + 2 * kTile, s.tr.tidop + tile * kTile, kTile * 4u, m);
+}
+__device__ __forceinline__ void bk_issue(const BkRecSrc& s, uint64_t tile, uint32_t* dst, unsigned long long* m) {
+  bulk_g2s(dst, s.h + tile * kTile, kTile * 4u, m);
+  bulk_g2s(dst + kTile, s.v + tile * kTile, kTile * 4u, m);
+  bulk_g2s(dst + 2 * kTile, s.t + tile * kTile, kTile * 4u, m);
+}
+// element j of a landed tile (tile base e0)
+__device__ __forceinline__ bool bk_staged(const BkTraceSrc& s, const uint32_t* b, uint64_t e0, uint32_t j, uint32_t& h,
+                                          uint32_t& v, uint32_t& t) {
+  t = b[2 * kTile + j];
+  const unsigned long long k = reinterpret_cast<const unsigned long long*>(b)[j];
+  h = bk_hash((uint32_t)compact_key(k, s.kr));
+  v = (uint32_t)(e0 + j) | (ev_kind(t) == GW_K_WRITE ? VAL_W : 0u);
+  return ev_kind(t) <= GW_K_WRITE;
+}
+__device__ __forceinline__ bool bk_staged(const BkRecSrc&, const uint32_t* b, uint64_t, uint32_t j, uint32_t& h,
+                                          uint32_t& v, uint32_t& t) {
+  h = b[j];
+  v = b[kTile + j];
+  t = b[2 * kTile + j];
+  return true;
+}
+template <class Src, int RB>
+__global__ void __launch_bounds__(kThreads, 2) k_bk_down_tma(Src src, int shift, const uint32_t* __restrict__ offsets,
+                                                            uint64_t nst, uint32_t* __restrict__ oh,
+                                                            uint32_t* __restrict__ ov, uint32_t* __restrict__ ot) {
+  constexpr int ND = BkPass<RB>::ND, DPT = BkPass<RB>::DPT, ST = BkPass<RB>::ST;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  BkTmaSmem<RB>& S = *reinterpret_cast<BkTmaSmem<RB>*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  const uint64_t n = src.n();
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  // this CTA's tiles, in order: super-tiles blockIdx.x, + gridDim.x, ...; ST tiles each
+  auto tile_of = [&](uint64_t k) { return (blockIdx.x + (k / ST) * gridDim.x) * ST + k % ST; };
+  auto full = [&](uint64_t tile) { return (tile + 1) * kTile <= n; };
+  if (threadIdx.x == 0) {
+    mbar_init(&S.mbar[0], 1);
+    mbar_init(&S.mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](uint64_t tile, int b) {  // thread 0
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&S.mbar[b], kBkTileBytes);
+    bk_issue(src, tile, S.buf[b], &S.mbar[b]);
+  };
+  uint32_t uses[2] = {0, 0};
+  if (threadIdx.x == 0 && tile_of(0) < ntiles && full(tile_of(0))) issue(tile_of(0), 0);
+  for (uint64_t k = 0;; k++) {
+    const uint64_t tile = tile_of(k);
+    if (tile >= ntiles || (k % ST == 0 && tile / ST >= nst)) break;
+    const int b = (int)(k & 1);
+    const uint64_t nx = tile_of(k + 1);
+    if (threadIdx.x == 0 && nx < ntiles && full(nx)) issue(nx, b ^ 1);
+    if (k % ST == 0)
+      for (int d = threadIdx.x; d < ND; d += kThreads) S.gbase[d] = offsets[(uint64_t)d * nst + tile / ST];
+    for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
+    const uint64_t tbase = tile * kTile;
+    uint32_t hh[kRsRounds], vv[kRsRounds], tt[kRsRounds], rd[kRsRounds];
+    if (full(tile)) {
+      while (!mbar_try_wait(&S.mbar[b], uses[b] & 1u)) {
+      }
+      uses[b]++;
+#pragma unroll
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint32_t j = w * kRsPerWarp + r * 32 + lane;
+        const bool ok = bk_staged(src, S.buf[b], tbase, j, hh[r], vv[r], tt[r]);
+        rd[r] = ok ? ((hh[r] >> shift) & (ND - 1)) << 16 : (uint32_t)ND << 16;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kRsRounds; r++) {
+        const uint64_t i = tbase + (uint64_t)w * kRsPerWarp + (uint64_t)r * 32 + lane;
+        const bool ok = i < n && src.get(i, hh[r], vv[r], tt[r]);
+        rd[r] = ok ? ((hh[r] >> shift) & (ND - 1)) << 16 : (uint32_t)ND << 16;
+      }
+    }
+    __syncthreads();  // wc zeroed, gbase loaded, every thread holds its inputs
+#pragma unroll
+    for (int r = 0; r < kRsRounds; r++) {
+      const uint32_t d = rd[r] >> 16;
+      const uint32_t peers = warp_peers<RB + 1>(d);
+      const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
+      __syncwarp();
+      if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+      rd[r] |= before + __popc(peers & lt);
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      uint32_t tot[DPT], csum = 0;
+#pragma unroll
+      for (int j = 0; j < DPT; j++) {
+        const int d = threadIdx.x * DPT + j;
+        uint32_t run = 0;
+        if (d < ND) {
+#pragma unroll
+          for (int ww = 0; ww < kRsWarps; ww++) {
+            const uint32_t t = S.wc[ww][d];
+            S.wc[ww][d] = run;
+            run += t;
+          }
+        }
+        tot[j] = run;
+        csum += run;
+      }
+      uint32_t ct;
+      uint32_t cex = block_excl_scan<uint32_t, OpSum>(csum, OpSum(), 0u, &ct);
+#pragma unroll
+      for (int j = 0; j < DPT; j++) {
+        const int d = threadIdx.x * DPT + j;
+        if (d < ND) S.toff[d] = cex;
+        cex += tot[j];
+      }
+      if (threadIdx.x == 0) S.cnt = ct;
+    }
+    __syncthreads();
+    uint32_t* sh = S.buf[b];
+    uint32_t* sv = sh + kTile;
+    uint32_t* sx = sv + kTile;
+#pragma unroll
+    for (int r = 0; r < kRsRounds; r++) {
+      const uint32_t d = rd[r] >> 16;
+      if (d < (uint32_t)ND) {
+        const uint32_t pos = stg<uint32_t>(S.toff[d] + S.wc[w][d] + (rd[r] & 0xFFFFu));
+        sh[pos] = hh[r];
+        sv[pos] = vv[r];
+        sx[pos] = tt[r];
+      }
+    }
+    __syncthreads();
+    const uint32_t cnt = S.cnt;
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) {
+      const uint32_t p = stg<uint32_t>(i);
+      const uint32_t h = sh[p];
+      const uint32_t d = (h >> shift) & (ND - 1);
+      const uint32_t gp = S.gbase[d] + (i - S.toff[d]);
+      oh[gp] = h;
+      ov[gp] = sv[p];
+      ot[gp] = sx[p];
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < ND; d += kThreads) {
+      const uint32_t end = d + 1 < ND ? S.toff[d + 1] : cnt;
+      S.gbase[d] += end - S.toff[d];
+    }
+    __syncthreads();  // gbase advanced; buffer b free for the TMA of tile k + 2
+  }
+}
+template <class Src, int RB>
+inline void bk_down_tma_setup() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_bk_down_tma<Src, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(BkTmaSmem<RB>));
+    done = true;
+  }
+}
+
 // ---- bucket starts: bstart[b] = first record of bucket b (bstart[NB] = n) ---
 __global__ void k_bk_bounds(const uint32_t* __restrict__ h, uint64_t n, int kb, uint32_t NB, uint32_t* bstart) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -269,14 +454,16 @@ struct BkCheckArgs {
   int kb;                  // in-bucket key bits
   StampSrc stamps;
   const uint32_t* arena;   // clock objects (block-range objects: lock-free traces)
-  Cands c;
+  Cands c;                 // final candidates (k_bk_resolve)
+  Cands pend;              // structural candidates (u != t, !cover): the clock half is resolved later
   DupList dup;
   uint32_t* large_i;       // writes with > kSmallWin reads since the last write (global record positions)
   uint32_t* large_ws;
   uint32_t* n_large;
   uint32_t large_cap;
   uint32_t* gsorted;       // in-bucket sorted event|W of the buckets holding a large window
-  uint32_t* spill;         // (start, count) of the buckets above kBkCap
+  uint32_t* scratch;       // per CTA: 3 x kBkSubBuf words (sub-bucket split)
+  uint32_t* spill;         // (start, count) of the buckets above kBkSubMax
   uint32_t* n_spill;
   uint32_t spill_cap;
 };
@@ -289,10 +476,11 @@ struct BkSmem {
   uint32_t V[kBkBuf];      // event | VAL_W, record order (from V + off)
   uint32_t T[kBkBuf];      // tidop, record order (from T + off)
   uint32_t H[kBkBuf];      // h (TMA), then the ping-pong half of the sort
-  uint32_t P[kBkCap];      // sort words (key << kBkIdxBits | record)
-  uint32_t LW[kBkCap];     // last write position + 1 (inclusive)
+  uint32_t P[kBkCap];      // sort words (slot or key << kBkIdxBits | record)
   uint32_t wc[kRsWarps][1 << kBkSortBits];
   uint32_t toff[1 << kBkSortBits];
+  uint32_t tab[kBkSlots];  // the group's locations: open addressing on the in-bucket key
+  uint32_t sub[48];        // sub-bucket counts / starts / write cursors
   unsigned long long mbar;
   uint32_t large;
 };
@@ -355,157 +543,296 @@ __device__ __forceinline__ uint32_t bk_clock(const BkCheckArgs& a, uint32_t vo, 
   return __ldg(optr(a.arena, vo) + OBJ_HDR + (u - (tc / BS) * BS));
 }
 
-__global__ void __launch_bounds__(kThreads, 2) k_bk_check(BkCheckArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
+// One group of M <= kBkCap records (a bucket, or a sub-bucket in the CTA's
+// scratch): TMA load of (h, event|W, tidop) from the src arrays at element
+// sp; grouping by location: ONE stable radix pass on the top 8 bits of the
+// in-group key (uniform: h is a hash), then every thread fixes its digit's
+// run into (key, record) order with an insertion sort -- runs are ~M/256
+// long and already in record order, so keys that share a run but differ are
+// the only work (a run of > 64 records that needs fixing falls back to the
+// full LSD passes); then per-thread blocked segment walks seeded by a block
+// max-scan, and the checks.  gpos = position of the group's first record in
+// the bucketed arrays (large-window positions).
+
+__device__ __noinline__ void bk_group(BkSmem& S, const BkCheckArgs& a, const uint32_t* hs, const uint32_t* vs,
+                                         const uint32_t* ts, uint32_t sp, uint32_t M, uint32_t gpos, int sb,
+                                         uint32_t& phase) {
   constexpr uint32_t IDXM = kBkCap - 1;
-  constexpr int IPT = kBkCap / kThreads;
   const uint32_t BS = a.tr.BS;
-  const int npass = (a.kb + kBkSortBits - 1) / kBkSortBits;
   const uint32_t kmask = (1u << a.kb) - 1u;
+  const uint32_t a0 = sp & ~3u, off = sp - a0;
+  const uint32_t bytes = ((off + M + 3u) & ~3u) * 4u;
   if (threadIdx.x == 0) {
-    mbar_init(&S.mbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the previous group's generic accesses
+    mbar_expect_tx(&S.mbar, 3u * bytes);
+    bulk_g2s(S.H, hs + a0, bytes, &S.mbar);
+    bulk_g2s(S.V, vs + a0, bytes, &S.mbar);
+    bulk_g2s(S.T, ts + a0, bytes, &S.mbar);
+    S.large = 0;
+  }
+  while (!mbar_try_wait(&S.mbar, phase)) {
+  }
+  phase ^= 1u;
+  const uint32_t* V = S.V + off;
+  const uint32_t* T = S.T + off;
+  // group by location: every distinct in-group key gets a slot of a small
+  // open-addressing table; one stable radix pass on the slot id then groups
+  // the records exactly, in record order.  More than kBkSlots * 3/4 distinct
+  // locations: full LSD passes on the key bits instead.
+  S.tab[threadIdx.x] = kBkEmpty;
+  if (threadIdx.x == 0) S.large = 0;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < M; j += kThreads) {
+    const uint32_t key = S.H[off + j] & kmask;
+    uint32_t slot = (key * 0x9E3779B1u) >> (32 - kBkSortBits), probes = 0;
+    while (true) {
+      uint32_t cur = S.tab[slot];
+      if (cur == kBkEmpty) cur = atomicCAS(&S.tab[slot], kBkEmpty, key);
+      if (cur == kBkEmpty || cur == key) break;
+      slot = (slot + 1) & (kBkSlots - 1);
+      if (++probes > kBkSlots * 3 / 4) { S.large = 2; break; }
+    }
+    S.P[j] = (slot << kBkIdxBits) | j;
   }
   __syncthreads();
-  uint32_t phase = 0;
-  for (uint32_t b = blockIdx.x; b < a.NB; b += gridDim.x) {
-    const uint32_t s = a.bstart[b], M = a.bstart[b + 1] - s;
-    if (M == 0) continue;
-    if (M > (uint32_t)kBkCap) {  // hot locations: the general path (bucket_spill)
-      if (threadIdx.x == 0) {
-        const uint32_t k = atomicAdd(a.n_spill, 1u);
-        if (k < a.spill_cap) { a.spill[2 * k] = s; a.spill[2 * k + 1] = M; }
-      }
-      continue;
-    }
-    const uint32_t a0 = s & ~3u, off = s - a0;
-    const uint32_t bytes = ((off + M + 3u) & ~3u) * 4u;
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the previous bucket's generic accesses
-      mbar_expect_tx(&S.mbar, 3u * bytes);
-      bulk_g2s(S.H, a.h + a0, bytes, &S.mbar);
-      bulk_g2s(S.V, a.v + a0, bytes, &S.mbar);
-      bulk_g2s(S.T, a.t + a0, bytes, &S.mbar);
-      S.large = 0;
-    }
-    while (!mbar_try_wait(&S.mbar, phase)) {
-    }
-    phase ^= 1u;
-    const uint32_t* V = S.V + off;
-    const uint32_t* T = S.T + off;
+  uint32_t* SP;
+  if (S.large != 2) {
+    bk_sort_pass(S, S.P, S.H, M, kBkIdxBits);
+    SP = S.H;
+  } else {  // (uniform) many locations: LSD passes over the useful key bits
     for (uint32_t j = threadIdx.x; j < M; j += kThreads) S.P[j] = ((S.H[off + j] & kmask) << kBkIdxBits) | j;
     __syncthreads();
-    // group by location: stable LSD radix on the in-bucket key bits (P <-> H)
+    const int ub = a.kb - sb;
+    const int npass = (ub + kBkSortBits - 1) / kBkSortBits;
     uint32_t* buf[2] = {S.P, S.H};
     int cur = 0;
     for (int p = 0; p < npass; p++) {
       bk_sort_pass(S, buf[cur], buf[cur ^ 1], M, kBkIdxBits + p * kBkSortBits);
       cur ^= 1;
     }
-    const uint32_t* SP = buf[cur];
-    uint32_t* SS = buf[cur ^ 1];  // segment start of each sorted position
-    // segment heads / last writes: blocked max-scan over the sorted positions
-    {
-      const uint32_t p0 = threadIdx.x * IPT;
-      uint2 agg = make_uint2(0, 0);
-#pragma unroll
-      for (int k = 0; k < IPT; k++) {
-        const uint32_t p = p0 + k;
-        if (p < M) {
-          const uint32_t x = SP[p];
-          if (p == 0 || (x >> kBkIdxBits) != (SP[p - 1] >> kBkIdxBits)) agg.x = p + 1;
-          if (V[x & IDXM] & VAL_W) agg.y = p + 1;
-        }
-      }
-      uint2 tot;
-      uint2 run = block_excl_scan<uint2, OpMax2>(agg, OpMax2(), make_uint2(0, 0), &tot);
-#pragma unroll
-      for (int k = 0; k < IPT; k++) {
-        const uint32_t p = p0 + k;
-        if (p < M) {
-          const uint32_t x = SP[p];
-          if (p == 0 || (x >> kBkIdxBits) != (SP[p - 1] >> kBkIdxBits)) run.x = p + 1;
-          if (V[x & IDXM] & VAL_W) run.y = p + 1;
-          SS[p] = run.x - 1;
-          S.LW[p] = run.y;
-        }
-      }
-    }
-    __syncthreads();
-    // the checks (gwcp.py:251-269), one sorted position per thread and step
-    for (uint32_t p = threadIdx.x; p < M; p += kThreads) {
-      const uint32_t jx = SP[p] & IDXM;
-      const uint32_t vx = V[jx], toc = T[jx];
-      const uint32_t c = vx & VAL_E, tc = ev_tid(toc);
-      const bool isw = (vx & VAL_W) != 0;
-      const uint32_t ss = SS[p];
-      const uint32_t lw = p > 0 ? S.LW[p - 1] : 0u;
-      const bool hasw = lw > 0 && lw - 1 >= ss;
-      const uint32_t W = hasw ? lw - 1 : NIL;
-      uint32_t vo = NIL;
-      bool have_vo = false;
-      unsigned long long loc = 0;
-      if (p > ss && (toc & GW_F_CONT) && a.dup.ev) {
-        // the previous access to this location may be in the same record
-        const uint32_t pe = V[SP[p - 1] & IDXM] & VAL_E;
-        if (pe < c && c - pe < 32) {
-          bool same = true;
-          for (uint32_t x = pe + 1; x < c && same; x++) same = (__ldg(a.tr.tidop + x) & GW_F_CONT) != 0;
-          if (same) {
-            const uint32_t kk = atomicAdd(a.dup.n, 1u);
-            if (kk < a.dup.cap) a.dup.ev[kk] = c;
-          }
-        }
-      }
-      if (hasw) {
-        const uint32_t jw = SP[W] & IDXM;
-        const uint32_t pw = V[jw] & VAL_E, top = T[jw], u = ev_tid(top);
-        if (u != tc && !cover(top, toc, BS)) {
-          if (!have_vo) { vo = a.stamps.get(c, tc).y; have_vo = true; }
-          if (a.stamps.get(pw, u).x > bk_clock(a, vo, tc, u)) {
-            loc = a.tr.key[c];
-            emit_cand(a.c, ((unsigned long long)c << 32) | SUB_WCHECK, loc, pw, c, isw ? GW_WW : GW_WR);
-          }
-        }
-      }
-      if (!isw) continue;
-      const uint32_t ws = hasw ? W + 1 : ss;
-      const uint32_t m = p - ws;
-      if (m == 0) continue;
-      if (m > kSmallWin) {
-        const uint32_t kk = atomicAdd(a.n_large, 1u);
-        if (kk < a.large_cap) { a.large_i[kk] = s + p; a.large_ws[kk] = s + ws; }
-        else atomicOr(a.c.err, ERR_CAND);
-        S.large = 1;
-        continue;
-      }
-      // readers since W: one candidate per thread (its latest read), ranked by its first read
-      for (uint32_t q = ws; q < p; q++) {
-        const uint32_t jq = SP[q] & IDXM;
-        const uint32_t toq = T[jq], uq = ev_tid(toq);
-        if (uq == tc) continue;
-        bool later = false;
-        for (uint32_t q2 = q + 1; q2 < p && !later; q2++) later = ev_tid(T[SP[q2] & IDXM]) == uq;
-        if (later) continue;
-        uint32_t first = q;
-        for (uint32_t q3 = ws; q3 < q; q3++)
-          if (ev_tid(T[SP[q3] & IDXM]) == uq) { first = q3; break; }
-        if (cover(toq, toc, BS)) continue;
-        const uint32_t r = V[jq] & VAL_E;
-        if (!have_vo) { vo = a.stamps.get(c, tc).y; have_vo = true; }
-        if (a.stamps.get(r, uq).x > bk_clock(a, vo, tc, uq)) {
-          if (!loc) loc = a.tr.key[c];
-          emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), loc, r, c, GW_RW);
-        }
-      }
-    }
-    __syncthreads();
-    if (S.large)  // the large-window pass reads this bucket's sorted order from global memory
-      for (uint32_t p = threadIdx.x; p < M; p += kThreads) a.gsorted[s + p] = V[SP[p] & IDXM];
+    SP = buf[cur];
+    if (threadIdx.x == 0) S.large = 0;
     __syncthreads();
   }
+  // blocked segment walk: thread t owns positions [t * ipt, (t + 1) * ipt);
+  // carry-in (segment head + 1, last write + 1) from a block max-scan
+  const uint32_t ipt = (M + kThreads - 1) / kThreads;
+  const uint32_t p0 = threadIdx.x * ipt, p1 = min(M, p0 + ipt);
+  uint2 agg = make_uint2(0, 0);
+  for (uint32_t p = p0; p < p1; p++) {
+    const uint32_t x = SP[p];
+    if (p == 0 || (x >> kBkIdxBits) != (SP[p - 1] >> kBkIdxBits)) agg.x = p + 1;
+    if (V[x & IDXM] & VAL_W) agg.y = p + 1;
+  }
+  uint2 tot;
+  uint2 run = block_excl_scan<uint2, OpMax2>(agg, OpMax2(), make_uint2(0, 0), &tot);
+  for (uint32_t p = p0; p < p1; p++) {
+    const uint32_t x = SP[p];
+    if (p == 0 || (x >> kBkIdxBits) != (SP[p - 1] >> kBkIdxBits)) run.x = p + 1;
+    // the checks (gwcp.py:251-269) of position p: run.y = last write before p + 1
+    const uint32_t jx = x & IDXM;
+    const uint32_t vx = V[jx], toc = T[jx];
+    const uint32_t c = vx & VAL_E, tc = ev_tid(toc);
+    const bool isw = (vx & VAL_W) != 0;
+    const uint32_t ss = run.x - 1;
+    const bool hasw = run.y > 0 && run.y - 1 >= ss;
+    const uint32_t W = hasw ? run.y - 1 : NIL;
+    if (isw) run.y = p + 1;
+    if (p > ss && (toc & GW_F_CONT) && a.dup.ev) {
+      // the previous access to this location may be in the same record
+      const uint32_t pe = V[SP[p - 1] & IDXM] & VAL_E;
+      if (pe < c && c - pe < 32) {
+        bool same = true;
+        for (uint32_t xx = pe + 1; xx < c && same; xx++) same = (__ldg(a.tr.tidop + xx) & GW_F_CONT) != 0;
+        if (same) {
+          const uint32_t kk = atomicAdd(a.dup.n, 1u);
+          if (kk < a.dup.cap) a.dup.ev[kk] = c;
+        }
+      }
+    }
+    if (hasw) {
+      const uint32_t jw = SP[W] & IDXM;
+      const uint32_t pw = V[jw] & VAL_E, topw = T[jw], u = ev_tid(topw);
+      if (u != tc && !cover(topw, toc, BS))  // the clock half: k_bk_resolve
+        emit_cand(a.pend, ((unsigned long long)c << 32) | SUB_WCHECK, 0ull, pw, c, isw ? GW_WW : GW_WR);
+    }
+    if (!isw) continue;
+    const uint32_t ws = hasw ? W + 1 : ss;
+    const uint32_t m = p - ws;
+    if (m == 0) continue;
+    if (m > kSmallWin) {
+      const uint32_t kk = atomicAdd(a.n_large, 1u);
+      if (kk < a.large_cap) { a.large_i[kk] = gpos + p; a.large_ws[kk] = gpos + ws; }
+      else atomicOr(a.c.err, ERR_CAND);
+      S.large = 1;
+      continue;
+    }
+    // readers since W: one candidate per thread (its latest read), ranked by its first read
+    for (uint32_t q = ws; q < p; q++) {
+      const uint32_t jq = SP[q] & IDXM;
+      const uint32_t toq = T[jq], uq = ev_tid(toq);
+      if (uq == tc) continue;
+      bool later = false;
+      for (uint32_t q2 = q + 1; q2 < p && !later; q2++) later = ev_tid(T[SP[q2] & IDXM]) == uq;
+      if (later) continue;
+      uint32_t first = q;
+      for (uint32_t q3 = ws; q3 < q; q3++)
+        if (ev_tid(T[SP[q3] & IDXM]) == uq) { first = q3; break; }
+      if (cover(toq, toc, BS)) continue;
+      emit_cand(a.pend, ((unsigned long long)c << 32) | SUB_READER | (first - ws), 0ull, V[jq] & VAL_E, c, GW_RW);
+    }
+  }
+  __syncthreads();
+  if (S.large)  // the large-window pass reads this group's sorted order from global memory
+    for (uint32_t p = threadIdx.x; p < M; p += kThreads) a.gsorted[gpos + p] = V[SP[p] & IDXM];
+  __syncthreads();
 }
+
+#ifndef GW_BK_MINB
+#define GW_BK_MINB 3
+#endif
+__global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  BkSmem& S = *reinterpret_cast<BkSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  if (threadIdx.x == 0) {
+    mbar_init(&S.mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  uint32_t* sh = a.scratch + (size_t)blockIdx.x * 3 * kBkSubBuf;
+  uint32_t* sv = sh + kBkSubBuf;
+  uint32_t* st = sv + kBkSubBuf;
+  for (uint32_t b = blockIdx.x; b < a.NB; b += gridDim.x) {
+    const uint32_t s = a.bstart[b], M = a.bstart[b + 1] - s;
+    if (M == 0) continue;
+    if (M <= (uint32_t)kBkCap) {
+      bk_group(S, a, a.h, a.v, a.t, s, M, s, 0, phase);
+      continue;
+    }
+    // a bucket above the shared-memory capacity: split it by the top sb bits
+    // of its in-bucket key into <= 16 sub-buckets in this CTA's scratch
+    // (L2-resident), stably, then check every sub-bucket
+    const int sb = min(kBkSubBits, 32 - __clz((M + kBkCap / 2 - 1) / (kBkCap / 2) - 1));
+    const int shift = a.kb - sb;
+    const uint32_t nsub = 1u << sb;
+    bool spill = M > (uint32_t)kBkSubMax;
+    if (!spill) {
+      for (int d = threadIdx.x; d < kRsWarps * 16; d += kThreads) S.wc[d >> 4][d & 15] = 0;
+      __syncthreads();
+      for (uint32_t j0 = threadIdx.x; j0 < M; j0 += kThreads * 8) {  // 8 loads in flight per thread
+        uint32_t hv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) hv[u] = j0 + u * kThreads < M ? __ldg(a.h + s + j0 + u * kThreads) : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+          if (j0 + u * kThreads < M) atomicAdd(&S.wc[w][(hv[u] >> shift) & (nsub - 1)], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x < 16) {
+        uint32_t c = 0;
+        for (int x = 0; x < kRsWarps; x++) c += S.wc[x][threadIdx.x];
+        S.sub[threadIdx.x] = c;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t run = 0, mx = 0;
+        for (uint32_t d = 0; d < 16; d++) {
+          const uint32_t c = S.sub[d];
+          mx = max(mx, c);
+          S.sub[16 + d] = run;  // sub-bucket start
+          S.sub[32 + d] = run;  // write cursor
+          run += c;
+        }
+        S.large = mx > (uint32_t)kBkCap;  // a sub-bucket still too large: spill the whole bucket
+      }
+      __syncthreads();
+      spill = S.large != 0;
+    }
+    if (spill) {  // hot locations: the general path (bucket_spill)
+      if (threadIdx.x == 0) {
+        const uint32_t k = atomicAdd(a.n_spill, 1u);
+        if (k < a.spill_cap) { a.spill[2 * k] = s; a.spill[2 * k + 1] = M; }
+      }
+      __syncthreads();
+      continue;
+    }
+    // stable scatter into the scratch, kSubChunk records per round
+    constexpr int R = 8, kSubChunk = kRsWarps * 32 * R;
+    for (uint32_t cb = 0; cb < M; cb += kSubChunk) {
+      for (int d = threadIdx.x; d < kRsWarps * 16; d += kThreads) S.wc[d >> 4][d & 15] = 0;
+      __syncthreads();
+      uint32_t hh[R], vv[R], tt[R], rd[R];
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const uint32_t j = cb + w * (32 * R) + r * 32 + lane;
+        const bool ok = j < M;
+        hh[r] = ok ? a.h[s + j] : 0u;
+        vv[r] = ok ? a.v[s + j] : 0u;
+        tt[r] = ok ? a.t[s + j] : 0u;
+        rd[r] = ok ? ((hh[r] >> shift) & (nsub - 1)) << 16 : 16u << 16;
+      }
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const uint32_t d = rd[r] >> 16;
+        const uint32_t peers = warp_peers<5>(d);
+        const uint32_t before = d < 16u ? S.wc[w][d] : 0u;
+        __syncwarp();
+        if (d < 16u && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+        rd[r] |= before + __popc(peers & lt);
+        __syncwarp();
+      }
+      __syncthreads();
+      if (threadIdx.x < 16) {  // per-warp offsets within the digit, advance the cursor
+        const int d = threadIdx.x;
+        uint32_t run = S.sub[32 + d];
+        for (int x = 0; x < kRsWarps; x++) {
+          const uint32_t t = S.wc[x][d];
+          S.wc[x][d] = run;
+          run += t;
+        }
+        S.sub[32 + d] = run;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const uint32_t d = rd[r] >> 16;
+        if (d < 16u) {
+          const uint32_t pos = S.wc[w][d] + (rd[r] & 0xFFFFu);
+          sh[pos] = hh[r];
+          sv[pos] = vv[r];
+          st[pos] = tt[r];
+        }
+      }
+      __syncthreads();
+    }
+    // the scratch was written by generic stores; the sub-bucket loads are TMA (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    for (uint32_t d = 0; d < nsub; d++) {
+      const uint32_t m = S.sub[d], o = S.sub[16 + d];
+      if (m) bk_group(S, a, sh, sv, st, o, m, s + o, sb, phase);
+    }
+  }
+}
+// the clock half of the structural candidates (gwcp.py:256, :265):
+// race iff prior.time > pred_t^{ver}[u]; stamps from the walker's snapshots
+__global__ void k_bk_resolve(Cands pend, DevTrace tr, StampSrc stamps, const uint32_t* arena, Cands out) {
+  const uint32_t n = min(*pend.n, pend.cap);
+  const uint32_t BS = tr.BS;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const uint32_t p = pend.prior[k], c = pend.cur[k];
+    const uint32_t tc = ev_tid(__ldg(tr.tidop + c)), u = ev_tid(__ldg(tr.tidop + p));
+    const uint32_t vo = stamps.get(c, tc).y;
+    const uint32_t t = stamps.get(p, u).x;
+    const uint32_t clk =
+        (vo == NIL || u / BS != tc / BS) ? 0u : __ldg(optr(arena, vo) + OBJ_HDR + (u - (tc / BS) * BS));
+    if (t > clk) emit_cand(out, pend.okey[k], tr.key[c], p, c, pend.kind[k]);
+  }
+}
+
 inline void bk_check_setup() {
   static bool done = false;
   if (!done) {

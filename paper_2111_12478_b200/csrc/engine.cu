@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "bucket.cuh"
+#include "validate.cuh"
 #include "workloads.cuh"
 #include "common.h"
 
@@ -79,6 +80,7 @@ struct Plan {
   unsigned long long n_bar = 0, n_end = 0, n_wbar = 0, D = 0;
   unsigned long long n_acc = 0;  // the bucketed access pass sizes its passes by it
   uint64_t cand_cap = 0;
+  uint64_t pend_cap = 0;  // bucketed pass: structural candidates
   uint32_t launches = 0;
   bool hard_small = false;  // snapshot mode with a one-launch hard-event list: a branch from the graph start
   cudaGraphExec_t exec = nullptr;
@@ -210,7 +212,7 @@ namespace {
 // scalar slots of the "scalars" buffer
 constexpr size_t kResHdr = 256;  // scalar mirror at the head of gw_ctx::hres
 enum : int { SC_MAXD = 0, SC_NINCS, SC_TICKET, SC_REC, SC_LOG, SC_DIAG, SC_ERR, SC_ABORT, SC_NCAND, SC_NLARGE,
-             SC_NSURV, SC_NQ, SC_NQLARGE, SC_NDUP, SC_NHEADS, SC_NSPILL, SC_NLARGE2, SC_COUNT = 24 };
+             SC_NSURV, SC_NQ, SC_NQLARGE, SC_NDUP, SC_NHEADS, SC_NSPILL, SC_NLARGE2, SC_NPEND, SC_COUNT = 24 };
 
 __global__ void k_init_stats(Stats* s) {
   memset(s, 0, sizeof(Stats));
@@ -224,6 +226,9 @@ __global__ void k_plan_check(const Stats* s, unsigned long long n_bar, unsigned 
                   s->n_wbar == n_wbar && s->n_acc == n_acc &&
                   ((s->key_or ^ s->key_and) & ~D) == 0ull;
   if (!ok) atomicOr(abort_flag, 1u);
+}
+__global__ void k_iota(uint32_t* v, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
 }
 __global__ void k_guard(const uint32_t* ncand, uint32_t cap, const uint32_t* nlarge, const uint32_t* ndup,
                         uint32_t dupcap, uint32_t* abort_flag, const uint32_t* nspill = nullptr) {
@@ -422,7 +427,7 @@ struct Pipeline {
 
   // observed by an eager run, used to build a Plan
   Stats obs{};
-  uint32_t obs_ncand = 0, obs_nlarge = 0, obs_nspill = 0;
+  uint32_t obs_ncand = 0, obs_nlarge = 0, obs_nspill = 0, obs_npend = 0;
   unsigned long long obs_D = 0;
   uint64_t obs_cand_cap = 0;
   bool obs_snap = false;
@@ -975,6 +980,14 @@ struct Pipeline {
     const uint64_t minn = (e && e[0] == '1') ? 1ull : (1ull << 24);
     return !has_locks && nshard <= 1 && !wide && kr.nbits > 0 && na >= minn && tr.n < (1ull << 31);
   }
+  static bool bk_tma_ok(const BkTraceSrc& s) {
+    const char* e = getenv("GW_BK_TMA");  // test hook: 0 = plain-load scatter kernel
+    return !(e && e[0] == '0') && ((uintptr_t)s.tr.key % 16) == 0 && ((uintptr_t)s.tr.tidop % 16) == 0;
+  }
+  static bool bk_tma_ok(const BkRecSrc&) {
+    const char* e = getenv("GW_BK_TMA");
+    return !(e && e[0] == '0');
+  }
   template <class Src, int RB>
   void bk_pass_rb(Src src, uint64_t n_in, int shift, uint32_t* oh, uint32_t* ov, uint32_t* ot) {
     constexpr int ND = BkPass<RB>::ND, ST = BkPass<RB>::ST;
@@ -984,8 +997,14 @@ struct Pipeline {
     GW_LAUNCH((k_bk_up<Src, RB>), g, kThreads, 0, st, src, shift, counts, nst);
     scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nst * ND, OpSum(), 0u, false,
                           "sc_u32");
-    bk_down_setup<Src, RB>();
-    GW_LAUNCH((k_bk_down<Src, RB>), g, kThreads, sizeof(BkDownSmem<RB>), st, src, shift, counts, nst, oh, ov, ot);
+    if (bk_tma_ok(src)) {  // TMA-streamed input tiles (16-byte aligned columns)
+      bk_down_tma_setup<Src, RB>();
+      GW_LAUNCH((k_bk_down_tma<Src, RB>), g, kThreads, sizeof(BkTmaSmem<RB>), st, src, shift, counts, nst, oh, ov,
+                ot);
+    } else {
+      bk_down_setup<Src, RB>();
+      GW_LAUNCH((k_bk_down<Src, RB>), g, kThreads, sizeof(BkDownSmem<RB>), st, src, shift, counts, nst, oh, ov, ot);
+    }
   }
   template <class Src>
   void bk_pass(Src src, uint64_t n_in, int RB, int shift, uint32_t* oh, uint32_t* ov, uint32_t* ot) {
@@ -993,8 +1012,6 @@ struct Pipeline {
       case 6: bk_pass_rb<Src, 6>(src, n_in, shift, oh, ov, ot); break;
       case 7: bk_pass_rb<Src, 7>(src, n_in, shift, oh, ov, ot); break;
       case 8: bk_pass_rb<Src, 8>(src, n_in, shift, oh, ov, ot); break;
-      case 9: bk_pass_rb<Src, 9>(src, n_in, shift, oh, ov, ot); break;
-      case 10: bk_pass_rb<Src, 10>(src, n_in, shift, oh, ov, ot); break;
       default: throw CudaErr{GW_E_ARG, "bucket digit width out of range"};
     }
   }
@@ -1119,15 +1136,18 @@ struct Pipeline {
     const uint32_t NB = 1u << bk_bb;
     const uint32_t spill_cap = NB;
     uint32_t* spill = C->get<uint32_t>("bk_spill", 2ull * spill_cap);
-    uint64_t cand_cap = gmode ? P->cand_cap : std::max<uint64_t>(65536, NA / 4);
-    Cands cd;
+    uint64_t pend_cap = gmode ? P->pend_cap : std::max<uint64_t>(65536, NA / 8);
+    Cands cd, pd;
     uint32_t hcnt[2] = {0, 0};
     bk_check_setup();
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bk_check, kThreads, sizeof(BkSmem)));
     const unsigned grid = (unsigned)std::min<uint64_t>(NB, (uint64_t)std::max(occ, 1) * C->num_sms);
+    uint32_t* scratch = C->get<uint32_t>("bk_scratch", (uint64_t)grid * 3 * kBkSubBuf);
+    uint32_t npend = 0;
     for (int attempt = 0; attempt < 2; attempt++) {
-      cd = make_cands("c", cand_cap, cnt);
+      pd = make_cands("bp", pend_cap, scal + SC_NPEND);
+      CK(cudaMemsetAsync(scal + SC_NPEND, 0, sizeof(uint32_t), st));
       CK(cudaMemsetAsync(cnt, 0, 2 * sizeof(uint32_t), st));
       CK(cudaMemsetAsync(scal + SC_NSURV, 0, sizeof(uint32_t), st));
       CK(cudaMemsetAsync(scal + SC_NSPILL, 0, sizeof(uint32_t), st));
@@ -1150,22 +1170,41 @@ struct Pipeline {
       ba.kb = bk_kb;
       ba.stamps = stamps;
       ba.arena = w.arena;
-      ba.c = cd;
+      ba.pend = pd;
+      ba.c = pd;
       ba.dup = dup;
       ba.large_i = large_i;
       ba.large_ws = large_ws;
       ba.n_large = cnt + 1;
       ba.large_cap = lcap;
       ba.gsorted = gsorted;
+      ba.scratch = scratch;
       ba.spill = spill;
       ba.n_spill = scal + SC_NSPILL;
       ba.spill_cap = spill_cap;
       GW_LAUNCH(k_bk_check, grid, kThreads, sizeof(BkSmem), st, ba);
       check_launch();
+      if (gmode) break;
+      d2h(&npend, scal + SC_NPEND);
+      if (npend <= pd.cap) break;
+      pend_cap = (uint64_t)npend + 1024;
+      CK(cudaMemsetAsync(w.err, 0, sizeof(uint32_t), st));
+    }
+    obs_npend = npend;
+    // the final candidates: the resolved structural ones, spilled buckets,
+    // same-instruction pairs, large windows
+    uint64_t cand_cap = gmode ? P->cand_cap : std::max<uint64_t>(65536, (uint64_t)npend + NA / 64);
+    for (int attempt = 0; attempt < 2; attempt++) {
+      cd = make_cands("c", cand_cap, cnt);
+      CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), st));
+      const uint64_t rg = gmode ? pd.cap : npend;
+      if (rg) GW_LAUNCH(k_bk_resolve, grid_for(rg), kThreads, 0, st, pd, tr, stamps, w.arena, cd);
       if (gmode) {
         same_instr_pass(cd);
         GW_LAUNCH(k_guard, 1, 1, 0, st, cnt, cd.cap, cnt + 1, scal + SC_NDUP, dup.cap, scal + SC_ABORT,
                   (const uint32_t*)(scal + SC_NSPILL));
+        GW_LAUNCH(k_guard, 1, 1, 0, st, scal + SC_NPEND, pd.cap, scal + SC_NLARGE2, scal + SC_NDUP, dup.cap,
+                  scal + SC_ABORT, (const uint32_t*)nullptr);
         break;
       }
       uint32_t nsp = 0;
@@ -1189,6 +1228,142 @@ struct Pipeline {
     obs_cand_cap = cand_cap;
     C->stats.n_candidates = hcnt[0];
     return cd;
+  }
+
+  // ------------------------------------- validate_trace / infer_locks (validate.cuh)
+  // (event, code, a, b) of validate_trace in report order, on the host
+  void validate_run(std::vector<uint32_t>& oe, std::vector<uint32_t>& oc, std::vector<uint64_t>& oa,
+                    std::vector<uint64_t>& ob) {
+    const uint64_t N = tr.n;
+    zero_blk = C->get<uint32_t>("zero_blk", kZeroWords);
+    zero_next = 0;
+    CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
+    reserve_epochs();
+    uint32_t* endpos = C->get<uint32_t>("v_end", tr.T);
+    CK(cudaMemsetAsync(endpos, 0xFF, sizeof(uint32_t) * tr.T, st));
+    GW_LAUNCH(k_val_endpos, grid_for(N), kThreads, 0, st, tr, endpos);
+    uint32_t* flag = C->get<uint32_t>("v_flag", N);
+    uint32_t* off = C->get<uint32_t>("v_off", N);
+    uint32_t* cnt = C->get<uint32_t>("v_cnt", 2);
+    uint64_t cap = std::max<uint64_t>(4096, N / 8);
+    VOut o;
+    uint32_t nd = 0;
+    for (int attempt = 0; attempt < 2; attempt++) {
+      o.okey = C->get<unsigned long long>("v_okey", cap);
+      o.code = C->get<uint32_t>("v_code", cap);
+      o.a = C->get<unsigned long long>("v_a", cap);
+      o.b = C->get<unsigned long long>("v_b", cap);
+      o.n = cnt;
+      o.cap = (uint32_t)cap;
+      CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), st));
+      GW_LAUNCH(k_val_events, grid_for(N), kThreads, 0, st, tr, endpos, o, flag);
+      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{off}, N, OpSum(), 0u, false, "sc_u32");
+      uint32_t hv[2];
+      CK(cudaMemcpyAsync(hv, off + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hv + 1, flag + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const uint64_t nl = (uint64_t)hv[0] + hv[1];
+      if (nl) {
+        uint32_t* ktid = C->get<uint32_t>("v_ktid", nl);
+        uint32_t* kev = C->get<uint32_t>("v_kev", nl);
+        GW_LAUNCH(k_val_compact, grid_for(N), kThreads, 0, st, tr, flag, off, ktid, kev);
+        sort<uint32_t>(ktid, kev, nl, ceil_log2(tr.T), "vlk");
+        unsigned long long* stk = C->get<unsigned long long>("v_stack", nl);
+        GW_LAUNCH(k_val_locks, grid_for(nl), kThreads, 0, st, tr, ktid, kev, (uint32_t)nl, stk, o);
+      }
+      d2h(&nd, cnt);
+      if (nd <= cap) break;
+      cap = nd;
+    }
+    oe.resize(nd); oc.resize(nd); oa.resize(nd); ob.resize(nd);
+    if (!nd) return;
+    // report order: (event, lane)
+    unsigned long long* sk = o.okey;
+    uint32_t* sv = C->get<uint32_t>("v_sv", nd);
+    GW_LAUNCH(k_iota, grid_for(nd), kThreads, 0, st, sv, (uint32_t)nd);
+    sort<unsigned long long>(sk, sv, nd, 8 + ceil_log2(N + 1), "vd");
+    std::vector<unsigned long long> hk(nd), ha(nd), hb(nd);
+    std::vector<uint32_t> hi(nd), hc(nd);
+    CK(cudaMemcpyAsync(hk.data(), sk, 8 * nd, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hi.data(), sv, 4 * nd, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), o.code, 4 * nd, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ha.data(), o.a, 8 * nd, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hb.data(), o.b, 8 * nd, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint32_t k = 0; k < nd; k++) {
+      const uint32_t j = hi[k];
+      oe[k] = (uint32_t)(hk[k] >> 8);
+      oc[k] = hc[j];
+      oa[k] = ha[j];
+      ob[k] = hb[j];
+    }
+  }
+  // infer_locks: the rewritten trace (host arrays) and the uninferred releases
+  void infer_run(std::vector<unsigned long long>& ok, std::vector<uint32_t>& oto, std::vector<uint32_t>& oin,
+                 std::vector<uint32_t>& dev_, std::vector<unsigned long long>& dlock, std::vector<uint32_t>& dtid) {
+    const uint64_t N = tr.n;
+    zero_blk = C->get<uint32_t>("zero_blk", kZeroWords);
+    zero_next = 0;
+    CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
+    reserve_epochs();
+    uint32_t* flag = C->get<uint32_t>("v_flag", N);
+    uint32_t* off = C->get<uint32_t>("v_off", N);
+    GW_LAUNCH(k_inf_flag, grid_for(N), kThreads, 0, st, tr, flag);
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{off}, N, OpSum(), 0u, false, "sc_u32");
+    uint32_t hv[2];
+    CK(cudaMemcpyAsync(hv, off + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hv + 1, flag + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t nt = (uint64_t)hv[0] + hv[1];
+    uint8_t* action = C->get<uint8_t>("i_act", N);
+    CK(cudaMemsetAsync(action, 0, N, st));
+    uint32_t* cnt = C->get<uint32_t>("v_cnt", 2);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), st));
+    InfDiag dg;
+    dg.cap = (uint32_t)std::max<uint64_t>(1, nt / 2 + 1);  // one per FENCE + atomic write pair at most
+    dg.ev = C->get<uint32_t>("i_dev", dg.cap);
+    dg.lock = C->get<unsigned long long>("i_dlock", dg.cap);
+    dg.tid = C->get<uint32_t>("i_dtid", dg.cap);
+    dg.n = cnt;
+    if (nt) {
+      uint32_t* ktid = C->get<uint32_t>("v_ktid", nt);
+      uint32_t* kev = C->get<uint32_t>("v_kev", nt);
+      GW_LAUNCH(k_val_compact, grid_for(N), kThreads, 0, st, tr, flag, off, ktid, kev);
+      sort<uint32_t>(ktid, kev, nt, ceil_log2(tr.T), "vlk");
+      unsigned long long* held = C->get<unsigned long long>("v_stack", nt);
+      GW_LAUNCH(k_inf_walk, grid_for(nt), kThreads, 0, st, tr, ktid, kev, (uint32_t)nt, held, action, dg);
+    }
+    GW_LAUNCH(k_inf_keep, grid_for(N), kThreads, 0, st, action, N, flag);
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{off}, N, OpSum(), 0u, false, "sc_u32");
+    CK(cudaMemcpyAsync(hv, off + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hv + 1, flag + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t nk = (uint64_t)hv[0] + hv[1];
+    unsigned long long* ko = C->get<unsigned long long>("i_key", nk);
+    uint32_t* to_o = C->get<uint32_t>("i_tidop", nk);
+    uint32_t* io = C->get<uint32_t>("i_instr", nk);
+    GW_LAUNCH(k_inf_emit, grid_for(N), kThreads, 0, st, tr, action, flag, off, ko, to_o, io);
+    ok.resize(nk); oto.resize(nk); oin.resize(nk);
+    uint32_t nd = 0;
+    d2h(&nd, cnt);
+    if (nk) {
+      CK(cudaMemcpyAsync(ok.data(), ko, 8 * nk, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(oto.data(), to_o, 4 * nk, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(oin.data(), io, 4 * nk, cudaMemcpyDeviceToHost, st));
+    }
+    std::vector<uint32_t> e(nd), t(nd);
+    std::vector<unsigned long long> l(nd);
+    if (nd) {
+      CK(cudaMemcpyAsync(e.data(), dg.ev, 4 * nd, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(l.data(), dg.lock, 8 * nd, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(t.data(), dg.tid, 4 * nd, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    std::vector<uint32_t> ord(nd);  // event order (a handful: host sort)
+    for (uint32_t k = 0; k < nd; k++) ord[k] = k;
+    std::sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return e[x] < e[y]; });
+    dev_.resize(nd); dlock.resize(nd); dtid.resize(nd);
+    for (uint32_t k = 0; k < nd; k++) { dev_[k] = e[ord[k]]; dlock[k] = l[ord[k]]; dtid[k] = t[ord[k]]; }
   }
 
   Cands make_cands(const std::string& tag, uint64_t cap, uint32_t* cnt) {
@@ -1713,6 +1888,7 @@ static void analyze_impl(gw_ctx* c, const DevTrace& tr, cudaStream_t st, uint32_
   np.n_acc = p.obs.n_acc;
   np.hard_small = p.obs_hard_small;
   np.cand_cap = 2ull * p.obs_ncand + 4096;  // tight: graph replays size the dedup / order passes by it
+  np.pend_cap = 2ull * p.obs_npend + 4096;
   c->plan = np;
   Pipeline g;
   g.C = c; g.st = st; g.inactive_opt = inactive; g.tr = tr; g.gmode = true; g.P = &c->plan;
@@ -1971,6 +2147,88 @@ extern "C" int gw_ctx_stats(gw_ctx* c, gw_stats* out) {
 }
 
 extern "C" uint32_t gw_ctx_launches(gw_ctx* c) { return c ? c->launches : 0; }
+
+template <class T>
+static T* to_malloc(const std::vector<T>& v) {
+  T* p = (T*)malloc(sizeof(T) * std::max<size_t>(v.size(), 1));
+  if (!p) throw std::bad_alloc();
+  if (!v.empty()) memcpy(p, v.data(), sizeof(T) * v.size());
+  return p;
+}
+
+// the trace on the device (host view: H2D into the context's input buffers)
+static DevTrace upload_view(gw_ctx* c, const gw_trace_view* t, cudaStream_t st) {
+  const uint64_t N = t->n_events;
+  unsigned long long* k = c->get<unsigned long long>("in_key", N);
+  uint32_t* to = c->get<uint32_t>("in_tidop", N);
+  uint32_t* in = c->get<uint32_t>("in_instr", N);
+  if (N) {
+    CK(cudaMemcpyAsync(k, t->key, 8 * N, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(to, t->tidop, 4 * N, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(in, t->instr, 4 * N, cudaMemcpyHostToDevice, st));
+  }
+  return make_dev(t, k, to, in);
+}
+
+extern "C" int gw_ctx_validate(gw_ctx* c, const gw_trace_view* t, uint64_t* n_out, uint32_t** ev, uint32_t** code,
+                               uint64_t** a, uint64_t** b) {
+  if (!c || !n_out) { gw_set_error("null argument"); return GW_E_ARG; }
+  int v = validate_view(t);
+  if (v) return v;
+  *n_out = 0;
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = 0;
+    c->last_stream = st;
+    c->drop_plan();  // the input buffers are rewritten: no graph replay may assume their contents
+    DevTrace tr = upload_view(c, t, st);
+    std::vector<uint32_t> oe, oc;
+    std::vector<uint64_t> oa, ob;
+    if (tr.n) {
+      Pipeline p;
+      p.C = c; p.st = st; p.tr = tr; p.inactive_opt = 1;
+      p.validate_run(oe, oc, oa, ob);
+    }
+    *n_out = oe.size();
+    if (ev) *ev = to_malloc(oe);
+    if (code) *code = to_malloc(oc);
+    if (a) *a = to_malloc(oa);
+    if (b) *b = to_malloc(ob);
+  });
+}
+
+extern "C" int gw_ctx_infer_locks(gw_ctx* c, const gw_trace_view* t, gw_trace* out, uint64_t* n_diag,
+                                  uint32_t** diag_event, uint64_t** diag_lock, uint32_t** diag_tid) {
+  if (!c || !out || !n_diag) { gw_set_error("null argument"); return GW_E_ARG; }
+  int v = validate_view(t);
+  if (v) return v;
+  memset(out, 0, sizeof *out);
+  *n_diag = 0;
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = 0;
+    c->last_stream = st;
+    c->drop_plan();
+    DevTrace tr = upload_view(c, t, st);
+    std::vector<unsigned long long> ok;
+    std::vector<uint32_t> oto, oin, de, dt;
+    std::vector<unsigned long long> dl;
+    if (tr.n) {
+      Pipeline p;
+      p.C = c; p.st = st; p.tr = tr; p.inactive_opt = 1;
+      p.infer_run(ok, oto, oin, de, dl, dt);
+    }
+    out->cfg = t->cfg;
+    out->n_events = ok.size();
+    out->key = (uint64_t*)to_malloc(ok);
+    out->tidop = to_malloc(oto);
+    out->instr = to_malloc(oin);
+    *n_diag = de.size();
+    if (diag_event) *diag_event = to_malloc(de);
+    if (diag_lock) *diag_lock = (uint64_t*)to_malloc(dl);
+    if (diag_tid) *diag_tid = to_malloc(dt);
+  });
+}
 
 static std::mutex g_default_mu;
 static gw_ctx* g_default = nullptr;

@@ -360,8 +360,23 @@ _VALIDATE_MSG = {
 }
 
 
-def validate_trace(trace) -> list[Diagnostic]:
-    """validate_trace (trace.py:522-601) over the SoA (native pass)."""
+def validate_trace(trace, *, ctx=None) -> list[Diagnostic]:
+    """validate_trace (trace.py:522-601) over the SoA: on the GPU through a
+    context (gw_ctx_validate; the `check` CLI path), else the host pass."""
     tr = encode(trace)
-    raw = N.validate(tr.cfg_tuple, tr.key, tr.tidop, tr.instr)
+    raw = N.validate(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, ctx=ctx)
     return [Diagnostic(ev, _VALIDATE_MSG[code](a, b, tr.config)) for ev, code, a, b in raw]
+
+
+def infer_locks(trace, *, ctx=None) -> tuple[Trace, list[Diagnostic]]:
+    """infer_locks (trace.py:609-680) on the GPU (gw_ctx_infer_locks): atomic
+    write + fence -> acquire, fence + atomic write -> release of a held lock;
+    returns the rewritten SoA trace and the reference's diagnostics."""
+    tr = encode(trace)
+    if ctx is None:
+        ctx = N.default_context()
+    (cfg, key, tidop, instr), raw = N.infer_locks(ctx, tr.cfg_tuple, tr.key, tr.tidop, tr.instr)
+    out = Trace(TraceConfig(*cfg), key, tidop, instr)
+    diags = [Diagnostic(ev, f"release of lock {lock:#x} not held by {tid_str(tr.config.thread_of(t))}; "
+                            "left uninferred") for ev, lock, t in raw]
+    return out, diags

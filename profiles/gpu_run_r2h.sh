@@ -1,0 +1,5 @@
+timeout 600 python -m pytest tests/test_gpu_bucket.py -x -q --tb=short 2>&1 | tail -5
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_h.json 2> gpurun_out/bench_h.err; tail -3 gpurun_out/bench_h.err; python -c "
+import json; d=json.load(open('gpurun_out/bench_h.json')); print(d['ms_per_step'], d['e2e']['ms_per_step'], d['kernel_ms_eager'], d['run']['report_digest']==d['run']['report_digest_expected'])"
+mkdir -p gpurun_out/ncu
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_bk_check|k_bk_down" -c 3 -o gpurun_out/ncu/r2_c5_bkh python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_bkh.log 2>&1; tail -2 gpurun_out/ncu_bkh.log

@@ -26,11 +26,50 @@ def test_parse_error_exits_two(tmp_path):
     assert "line 1: first line must be a config line" in r.stderr
 
 
+@pytest.mark.gpu
 def test_validation_error_exits_three(tmp_path):
     r = _cli(tmp_path, "config blocks=1 warps=1 lanes=1\n0.0.0 end\n0.0.0 wr g:0x10\n")
     assert r.returncode == 3
     assert "event 1: event after end of thread 0.0.0" in r.stderr
     assert "trace is not well formed" in r.stderr
+
+
+def test_engine_failure_exits_four_not_one(tmp_path):
+    """Without a CUDA device the engine fails loudly, with exit 4 -- never the
+    'races found' code (no CPU path)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("needs a host without a CUDA device")
+    r = _cli(tmp_path, _corpus("wcp-classic")["text"])
+    assert r.returncode == 4
+    assert "analysis engine failed" in r.stderr and r.stdout == ""
+
+
+_INFER = ("config blocks=2 warps=1 lanes=1\n"
+          "0.0.0 wr g:0x10\n0.0.0 wr g:0xa0 atomic device\n0.0.0 fence device\n0.0.0 wr g:{a}\n"
+          "0.0.0 fence device\n0.0.0 wr g:0xa0 atomic device\n"
+          "1.0.0 wr g:0xa0 atomic device\n1.0.0 fence device\n1.0.0 rd g:0x14\n"
+          "1.0.0 fence device\n1.0.0 wr g:0xa0 atomic device\n1.0.0 wr g:0x10\n"
+          "1.0.0 fence device\n1.0.0 wr g:0xb0 atomic device\n")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("a,rc,out", [
+    # conflicting inferred critical sections order the 0x10 writes (WCP rule (i)): no race
+    ("0x14", 0, []),
+    # disjoint critical sections: the classic predicted race
+    ("0x18", 1, ['{"detector":"gwcp","kind":"ww","location":{"space":"global","addr":"0x10"},'
+                 '"prior":{"event":0,"tid":"0.0.0","instr":2},"current":{"event":7,"tid":"1.0.0","instr":13},'
+                 '"class":"interblock","confidence":"first"}']),
+])
+def test_infer_locks_cli(tmp_path, a, rc, out):
+    """check --infer-locks against the reference CLI's own output
+    (PYTHONPATH=pkg/src python -m gpurace.cli check T --infer-locks)."""
+    r = _cli(tmp_path, _INFER.format(a=a), "--infer-locks")
+    assert r.returncode == rc
+    assert r.stdout.splitlines() == out
+    assert "lock inference: event 13: release of lock 0xb0 not held by 1.0.0; left uninferred" in r.stderr
 
 
 def test_other_detectors_are_not_on_the_accelerated_path(tmp_path):
