@@ -370,7 +370,14 @@ def run_b200(args):
     in_h.copy_(in_d)
     # the packed (narrow-column) form of the same trace: the layout of a GWSOA v2
     # file (cli convert --packed), made once like a trace file on disk
-    kb = 4 if int(key_d.max().item()) < (1 << 32) and int(key_d.min().item()) >= 0 else 8
+    kb = 4
+    for c0 in range(0, n, 1 << 27):  # barrier keys are implied by the tidop (gw_trace_packed)
+        kc = key_d[c0:c0 + (1 << 27)]
+        nonbar = ((to_d[c0:c0 + (1 << 27)] >> N.OP_SHIFT) & 7) != N.K_BARRIER
+        kc = torch.where(nonbar, kc, torch.zeros_like(kc))
+        if int(kc.max().item()) >= (1 << 32) or int(kc.min().item()) < 0:
+            kb = 8
+        del kc, nonbar
     ib = 2 if int(in_d.max().item()) < (1 << 16) and int(in_d.min().item()) >= 0 else 4
     keyp_h = torch.empty(n, dtype=torch.int32 if kb == 4 else torch.int64, pin_memory=True)
     inp_h = torch.empty(n, dtype=torch.int16 if ib == 2 else torch.int32, pin_memory=True)

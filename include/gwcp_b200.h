@@ -179,10 +179,48 @@ void gw_ctx_destroy(gw_ctx* c);
 int gw_ctx_analyze_device(gw_ctx* c, const gw_trace_view* dev_trace, const gw_opts* opts);
 /* host_trace in (pageable or pinned) -> H2D on opts->stream -> analyze (results on device) */
 int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* host_trace, const gw_opts* opts);
+/* ---- exchange mode: the multi-GPU data plane (paper_2111_12478_b200/shard.py)
+ * Every rank holds ONE record-aligned slice of the trace (1/G of the SoA,
+ * device pointers) at global event offset event_base; the host moves the
+ * data between ranks with NCCL collectives:
+ *   gw_xs_prep       slice statistics -> the host sums / ORs / ANDs them
+ *   gw_xs_hard       the slice's barriers and ENDs (global event, tidop,
+ *                    instr, key) -> all-gathered: every rank runs the small
+ *                    sync pass (snapshot walker) over the whole trace's
+ *   gw_xs_partition  the slice's accesses as 12-byte records (h, global
+ *                    event | W, tidop) grouped by destination shard = the
+ *                    top log2(G) bits of h = fmix32(compacted location) ->
+ *                    all-to-all
+ *   gw_xs_check      the bucketed check of this shard's received records,
+ *                    plus the record (same-instruction) check of the slice;
+ *                    gw_xs_fetch the candidates (global event indices)
+ *   gw_xs_lookup     (tidop, instr) of global events in the slice, for the
+ *                    report merge on rank 0 (dedup report.py:92-100 is per
+ *                    location, so any partition of the locations is exact).
+ * Lock-free traces with records of <= 32 events; a shard meeting hot
+ * locations or > 32-read windows returns GW_E_UNSUPPORTED (the host then
+ * uses the replicated address-sharded mode of gw_opts). */
+typedef struct gw_xs_stats {
+  uint64_t n_acc, n_write, n_acq, n_rel, n_end, n_bar, key_or, key_and, n_long, n_wbar;
+} gw_xs_stats;
+int gw_xs_prep(gw_ctx* c, const gw_trace_view* dev_slice, uint32_t event_base, void* stream, gw_xs_stats* out);
+int gw_xs_hard(gw_ctx* c, void* stream, uint32_t* ev, uint32_t* tidop, uint32_t* instr, uint64_t* key,
+               uint64_t* n_out);
+int gw_xs_partition(gw_ctx* c, const gw_xs_stats* global, uint32_t shard_count, void* stream, uint32_t* h,
+                    uint32_t* v, uint32_t* t, uint64_t* counts);
+int gw_xs_check(gw_ctx* c, const gw_xs_stats* global, uint32_t shard_count, uint64_t n_total, void* stream,
+                const uint32_t* h, const uint32_t* v, const uint32_t* t, uint64_t n_recv, const uint32_t* hev,
+                const uint32_t* htidop, const uint32_t* hinstr, const uint64_t* hkey, uint64_t n_hard,
+                uint64_t* n_cand);
+int gw_xs_fetch(gw_ctx* c, uint64_t* okey, uint64_t* loc, uint32_t* prior, uint32_t* cur, uint32_t* kind);
+int gw_xs_lookup(gw_ctx* c, const uint32_t* ev, uint64_t n, uint32_t* tidop, uint32_t* instr);
+
 /* Packed (narrow-column) trace: the SoA above with the key column stored in
  * key_bytes = 4 or 8 and the instr column in instr_bytes = 2 or 4 bytes per
  * event -- the narrowest widths holding every value of the trace (C5:
- * 10 B/event instead of 16).  It is the layout of GWSOA v2 files (cli
+ * 10 B/event instead of 16).  Barrier keys are implied by their tidop
+ * (warp barrier: block << 32 | warp; block barrier: 0): with 4-byte keys
+ * they are not stored (any value) and are restored on the device.  It is the layout of GWSOA v2 files (cli
  * convert --packed) and the host input of gw_ctx_analyze_host_packed, which
  * uploads it in chunks on a copy stream and widens each chunk on the device
  * while the next one is in flight, then analyses as gw_ctx_analyze_host. */

@@ -77,6 +77,11 @@ class _Packed(C.Structure):
     ]
 
 
+class XsStats(C.Structure):
+    _fields_ = [(f, C.c_uint64) for f in ("n_acc", "n_write", "n_acq", "n_rel", "n_end", "n_bar", "key_or",
+                                          "key_and", "n_long", "n_wbar")]
+
+
 class _Opts(C.Structure):
     _fields_ = [("inactive_opt", C.c_uint32), ("flags", C.c_uint32), ("stream", C.c_void_p),
                 ("shard_index", C.c_uint32), ("shard_count", C.c_uint32)]
@@ -129,6 +134,12 @@ EXPORTS = (
     "gw_ctx_analyze_host_packed",
     "gw_ctx_validate",
     "gw_ctx_infer_locks",
+    "gw_xs_prep",
+    "gw_xs_hard",
+    "gw_xs_partition",
+    "gw_xs_check",
+    "gw_xs_fetch",
+    "gw_xs_lookup",
     "gw_ctx_fetch",
     "gw_ctx_stats",
     "gw_ctx_launches",
@@ -193,6 +204,16 @@ def lib():
                                          C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.POINTER(C.c_uint64)),
                                          C.POINTER(C.POINTER(C.c_uint32))]
         L.gw_ctx_infer_locks.restype = C.c_int
+        P32, P64, VP = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.c_void_p
+        L.gw_xs_prep.argtypes = [VP, C.POINTER(_View), C.c_uint32, VP, C.POINTER(XsStats)]
+        L.gw_xs_hard.argtypes = [VP, VP, VP, VP, VP, VP, P64]
+        L.gw_xs_partition.argtypes = [VP, C.POINTER(XsStats), C.c_uint32, VP, VP, VP, VP, P64]
+        L.gw_xs_check.argtypes = [VP, C.POINTER(XsStats), C.c_uint32, C.c_uint64, VP, VP, VP, VP, C.c_uint64,
+                                  VP, VP, VP, VP, C.c_uint64, P64]
+        L.gw_xs_fetch.argtypes = [VP, VP, VP, VP, VP, VP]
+        L.gw_xs_lookup.argtypes = [VP, VP, C.c_uint64, VP, VP]
+        for f in ("gw_xs_prep", "gw_xs_hard", "gw_xs_partition", "gw_xs_check", "gw_xs_fetch", "gw_xs_lookup"):
+            getattr(L, f).restype = C.c_int
         L.gw_ctx_fetch.argtypes = [C.c_void_p, C.POINTER(_Result)]
         L.gw_ctx_fetch.restype = C.c_int
         L.gw_ctx_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
@@ -423,6 +444,46 @@ class Context:
         o = _Opts(1 if inactive_opt else 0, flags, stream, shard[0], shard[1])
         _check(self._L.gw_ctx_analyze_device(self._c, C.byref(v), C.byref(o)))
 
+    # ---- exchange mode (multi-GPU data plane; shard.analyze_exchange drives it) ----
+    def xs_prep(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, base, stream=None) -> XsStats:
+        v = _View()
+        v.cfg.blocks, v.cfg.warps, v.cfg.lanes = cfg
+        v.n_events = n
+        v.key, v.tidop, v.instr = key_ptr, tidop_ptr, instr_ptr
+        out = XsStats()
+        _check(self._L.gw_xs_prep(self._c, C.byref(v), base, stream, C.byref(out)))
+        return out
+
+    def xs_hard(self, ev_ptr, tidop_ptr, instr_ptr, key_ptr, stream=None) -> int:
+        n = C.c_uint64(0)
+        _check(self._L.gw_xs_hard(self._c, stream, ev_ptr, tidop_ptr, instr_ptr, key_ptr, C.byref(n)))
+        return int(n.value)
+
+    def xs_partition(self, glob: XsStats, shards, h_ptr, v_ptr, t_ptr, stream=None) -> list:
+        counts = (C.c_uint64 * shards)()
+        _check(self._L.gw_xs_partition(self._c, C.byref(glob), shards, stream, h_ptr, v_ptr, t_ptr, counts))
+        return [int(x) for x in counts]
+
+    def xs_check(self, glob: XsStats, shards, n_total, recv_ptrs, n_recv, hard_ptrs, n_hard, stream=None) -> int:
+        n = C.c_uint64(0)
+        _check(self._L.gw_xs_check(self._c, C.byref(glob), shards, n_total, stream, *recv_ptrs, n_recv, *hard_ptrs,
+                                   n_hard, C.byref(n)))
+        return int(n.value)
+
+    def xs_fetch(self, n) -> dict:
+        out = {"order_key": np.zeros(n, np.uint64), "loc": np.zeros(n, np.uint64), "prior": np.zeros(n, np.uint32),
+               "current": np.zeros(n, np.uint32), "kind": np.zeros(n, np.uint32)}
+        _check(self._L.gw_xs_fetch(self._c, *(out[k].ctypes.data for k in ("order_key", "loc", "prior", "current",
+                                                                             "kind"))))
+        return out
+
+    def xs_lookup(self, ev) -> tuple:
+        ev = np.ascontiguousarray(ev, np.uint32)
+        to = np.zeros(len(ev), np.uint32)
+        ins = np.zeros(len(ev), np.uint32)
+        _check(self._L.gw_xs_lookup(self._c, ev.ctypes.data, len(ev), to.ctypes.data, ins.ctypes.data))
+        return to, ins
+
     def fetch(self):
         r = _Result()
         _check(self._L.gw_ctx_fetch(self._c, C.byref(r)))
@@ -447,12 +508,17 @@ class Context:
         return {names[i].value.decode(): (float(ms[i]), int(cnt[i])) for i in range(n.value)}
 
 
-def pack_columns(key, instr):
+def pack_columns(key, instr, tidop=None):
     """The narrowest packed widths holding every value (gw_trace_packed):
-    key as uint32 when every key < 2^32, instr as uint16 when < 2^16."""
+    key as uint32 when every non-barrier key < 2^32 (barrier keys are implied
+    by their tidop and restored on the device; tidop=None: all keys count),
+    instr as uint16 when < 2^16."""
     key = np.asarray(key, np.uint64)
     instr = np.asarray(instr, np.uint32)
-    k = key.astype(np.uint32) if len(key) == 0 or int(key.max()) < (1 << 32) else key
+    ks = key
+    if tidop is not None and len(key):
+        ks = key[((np.asarray(tidop, np.uint32) >> np.uint32(OP_SHIFT)) & np.uint32(7)) != K_BARRIER]
+    k = key.astype(np.uint32) if len(ks) == 0 or int(ks.max()) < (1 << 32) else key
     i = instr.astype(np.uint16) if len(instr) == 0 or int(instr.max()) < (1 << 16) else instr
     return k, i
 

@@ -38,6 +38,26 @@ __device__ __forceinline__ uint32_t bk_hash(uint32_t x) {  // murmur3 fmix32 (bi
   x ^= x >> 16;
   return x;
 }
+__device__ __forceinline__ uint32_t bk_unhash(uint32_t x) {  // its inverse
+  x ^= x >> 16;
+  x *= 0x7ed1b41du;
+  x ^= (x >> 13) ^ (x >> 26);
+  x *= 0xa5cb9243u;
+  x ^= x >> 16;
+  return x;
+}
+// compacted key -> location key (the constant bits `base` of every access key)
+__device__ __forceinline__ unsigned long long uncompact_key(unsigned long long ck, const KeyRuns& kr,
+                                                           unsigned long long base) {
+  unsigned long long k = base;
+#pragma unroll
+  for (int r = 0; r < 4; r++)
+    if (r < kr.n) {
+      const unsigned long long m = kr.width[r] >= 64 ? ~0ull : ((1ull << kr.width[r]) - 1ull);
+      k |= ((ck >> kr.dst[r]) & m) << kr.src[r];
+    }
+  return k;
+}
 
 constexpr int kBkCap = 4096;      // records of one bucket in shared memory
 constexpr int kBkIdxBits = 12;    // record index bits of the in-bucket sort word
@@ -63,6 +83,7 @@ struct BkPass {
 struct BkTraceSrc {
   DevTrace tr;
   KeyRuns kr;
+  uint32_t base;  // global index of event 0 (a rank's slice in exchange mode; else 0)
   __device__ __forceinline__ uint64_t n() const { return tr.n; }
   // both columns are loaded unconditionally: independent loads, no round
   // trip on the kind before the key load is issued
@@ -76,7 +97,7 @@ struct BkTraceSrc {
     t = __ldcs(tr.tidop + i);
     const unsigned long long k = __ldcs(tr.key + i);
     h = bk_hash((uint32_t)compact_key(k, kr));
-    v = (uint32_t)i | (ev_kind(t) == GW_K_WRITE ? VAL_W : 0u);
+    v = (base + (uint32_t)i) | (ev_kind(t) == GW_K_WRITE ? VAL_W : 0u);
     return ev_kind(t) <= GW_K_WRITE;
   }
 };
@@ -280,7 +301,7 @@ __device__ __forceinline__ bool bk_staged(const BkTraceSrc& s, const uint32_t* b
   t = b[2 * kTile + j];
   const unsigned long long k = reinterpret_cast<const unsigned long long*>(b)[j];
   h = bk_hash((uint32_t)compact_key(k, s.kr));
-  v = (uint32_t)(e0 + j) | (ev_kind(t) == GW_K_WRITE ? VAL_W : 0u);
+  v = (s.base + (uint32_t)(e0 + j)) | (ev_kind(t) == GW_K_WRITE ? VAL_W : 0u);
   return ev_kind(t) <= GW_K_WRITE;
 }
 __device__ __forceinline__ bool bk_staged(const BkRecSrc&, const uint32_t* b, uint64_t, uint32_t j, uint32_t& h,
@@ -431,15 +452,28 @@ inline void bk_down_tma_setup() {
 
 // ---- bucket starts: bstart[b] = first record of bucket b (bstart[NB] = n) ---
 __global__ void k_bk_bounds(const uint32_t* __restrict__ h, uint64_t n, int kb, uint32_t NB, uint32_t* bstart) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = h[i] >> kb;
-    const uint32_t pb = i > 0 ? h[i - 1] >> kb : 0u;
-    if (i == 0)
-      for (uint32_t x = 0; x <= b; x++) bstart[x] = 0;
-    else
-      for (uint32_t x = pb + 1; x <= b; x++) bstart[x] = (uint32_t)i;
-    if (i + 1 == n)
-      for (uint32_t x = b + 1; x <= NB; x++) bstart[x] = (uint32_t)n;
+  const uint64_t nq = (n + 3) / 4;  // four records per thread, one 16-byte load
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = q * 4;
+    uint32_t v[4];
+    if (i0 + 4 <= n) {
+      const uint4 x = __ldcs(reinterpret_cast<const uint4*>(h) + q);
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+      for (int k = 0; k < 4; k++) v[k] = i0 + k < n ? h[i0 + k] : 0u;
+    }
+    uint32_t pb = i0 > 0 ? (__ldg(h + i0 - 1) >> kb) & (NB - 1) : 0u;
+    for (int k = 0; k < 4 && i0 + k < n; k++) {
+      const uint64_t i = i0 + k;
+      const uint32_t b = (v[k] >> kb) & (NB - 1);
+      if (i == 0)
+        for (uint32_t x = 0; x <= b; x++) bstart[x] = 0;
+      else
+        for (uint32_t x = pb + 1; x <= b; x++) bstart[x] = (uint32_t)i;
+      if (i + 1 == n)
+        for (uint32_t x = b + 1; x <= NB; x++) bstart[x] = (uint32_t)n;
+      pb = b;
+    }
   }
 }
 
@@ -464,6 +498,7 @@ struct BkCheckArgs {
   uint32_t* gsorted;       // in-bucket sorted event|W of the buckets holding a large window
   uint32_t* scratch;       // per CTA: 3 x kBkSubBuf words (sub-bucket split)
   uint32_t* spill;         // (start, count) of the buckets above kBkSubMax
+  int xmode;               // exchange mode (multi-GPU): records from other ranks' slices, no trace access
   uint32_t* n_spill;
   uint32_t spill_cap;
 };
@@ -481,6 +516,7 @@ struct BkSmem {
   uint32_t toff[1 << kBkSortBits];
   uint32_t tab[kBkSlots];  // the group's locations: open addressing on the in-bucket key
   uint32_t sub[48];        // sub-bucket counts / starts / write cursors
+  uint32_t hhi;
   unsigned long long mbar;
   uint32_t large;
 };
@@ -535,6 +571,31 @@ __device__ __forceinline__ void bk_sort_pass(BkSmem& S, const uint32_t* in, uint
   __syncthreads();
 }
 
+// L2 eviction policies (createpolicy): the bucketed records stream through
+// L2 once (evict-first); the sub-bucket scratch is written and read back by
+// the same CTA within microseconds (evict-last keeps it out of DRAM)
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_keep(uint32_t* p, uint32_t v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, unsigned long long* m,
+                                              unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(m)), "l"(pol)
+      : "memory");
+}
+
 // pred_t^{vo}[u] for the accessing thread tc: lock-free clock objects are
 // block-range objects of tc's block (acc_clock, blockobj case)
 __device__ __forceinline__ uint32_t bk_clock(const BkCheckArgs& a, uint32_t vo, uint32_t tc, uint32_t u) {
@@ -545,14 +606,16 @@ __device__ __forceinline__ uint32_t bk_clock(const BkCheckArgs& a, uint32_t vo, 
 
 // One group of M <= kBkCap records (a bucket, or a sub-bucket in the CTA's
 // scratch): TMA load of (h, event|W, tidop) from the src arrays at element
-// sp; grouping by location: ONE stable radix pass on the top 8 bits of the
-// in-group key (uniform: h is a hash), then every thread fixes its digit's
-// run into (key, record) order with an insertion sort -- runs are ~M/256
-// long and already in record order, so keys that share a run but differ are
-// the only work (a run of > 64 records that needs fixing falls back to the
-// full LSD passes); then per-thread blocked segment walks seeded by a block
-// max-scan, and the checks.  gpos = position of the group's first record in
-// the bucketed arrays (large-window positions).
+// sp; grouping by location through a small table of the group's distinct
+// keys and one stable radix pass on the slot ids (full LSD passes on the
+// key bits when the group holds too many locations); then per-thread
+// blocked segment walks seeded by a block max-scan, and the structural half
+// of the checks (the clock half: k_bk_resolve).  gpos = position of the
+// group's first record in the bucketed arrays (large-window positions).
+// Exchange mode (a.xmode, multi-GPU): the records come from other ranks'
+// slices, so nothing is read from the trace: a pending candidate carries
+// (h << 32 | prior tid) in its loc field and the current tid in kind >> 8.
+constexpr uint32_t ERR_XMODE = 512;  // exchange mode met a spill / large window (host falls back)
 
 __device__ __noinline__ void bk_group(BkSmem& S, const BkCheckArgs& a, const uint32_t* hs, const uint32_t* vs,
                                          const uint32_t* ts, uint32_t sp, uint32_t M, uint32_t gpos, int sb,
@@ -565,9 +628,10 @@ __device__ __noinline__ void bk_group(BkSmem& S, const BkCheckArgs& a, const uin
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the previous group's generic accesses
     mbar_expect_tx(&S.mbar, 3u * bytes);
-    bulk_g2s(S.H, hs + a0, bytes, &S.mbar);
-    bulk_g2s(S.V, vs + a0, bytes, &S.mbar);
-    bulk_g2s(S.T, ts + a0, bytes, &S.mbar);
+    const unsigned long long pol = l2_evict_first();  // every record is read once
+    bulk_g2s_hint(S.H, hs + a0, bytes, &S.mbar, pol);
+    bulk_g2s_hint(S.V, vs + a0, bytes, &S.mbar, pol);
+    bulk_g2s_hint(S.T, ts + a0, bytes, &S.mbar, pol);
     S.large = 0;
   }
   while (!mbar_try_wait(&S.mbar, phase)) {
@@ -580,7 +644,10 @@ __device__ __noinline__ void bk_group(BkSmem& S, const BkCheckArgs& a, const uin
   // the records exactly, in record order.  More than kBkSlots * 3/4 distinct
   // locations: full LSD passes on the key bits instead.
   S.tab[threadIdx.x] = kBkEmpty;
-  if (threadIdx.x == 0) S.large = 0;
+  if (threadIdx.x == 0) {
+    S.large = 0;
+    S.hhi = S.H[off] & ~kmask;  // the group's shared high bits of h (exchange mode)
+  }
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < M; j += kThreads) {
     const uint32_t key = S.H[off + j] & kmask;
@@ -596,7 +663,8 @@ __device__ __noinline__ void bk_group(BkSmem& S, const BkCheckArgs& a, const uin
   }
   __syncthreads();
   uint32_t* SP;
-  if (S.large != 2) {
+  const bool slotmode = S.large != 2;
+  if (slotmode) {
     bk_sort_pass(S, S.P, S.H, M, kBkIdxBits);
     SP = S.H;
   } else {  // (uniform) many locations: LSD passes over the useful key bits
@@ -650,17 +718,25 @@ __device__ __noinline__ void bk_group(BkSmem& S, const BkCheckArgs& a, const uin
         }
       }
     }
+    const uint32_t hc = S.hhi | (slotmode ? S.tab[x >> kBkIdxBits] : (x >> kBkIdxBits));
+    auto pend = [&](unsigned long long okey, uint32_t prior, uint32_t u, uint32_t kind) {
+      if (a.xmode)
+        emit_cand(a.pend, okey, ((unsigned long long)hc << 32) | u, prior, c, kind | (tc << 8));
+      else
+        emit_cand(a.pend, okey, 0ull, prior, c, kind);
+    };
     if (hasw) {
       const uint32_t jw = SP[W] & IDXM;
       const uint32_t pw = V[jw] & VAL_E, topw = T[jw], u = ev_tid(topw);
       if (u != tc && !cover(topw, toc, BS))  // the clock half: k_bk_resolve
-        emit_cand(a.pend, ((unsigned long long)c << 32) | SUB_WCHECK, 0ull, pw, c, isw ? GW_WW : GW_WR);
+        pend(((unsigned long long)c << 32) | SUB_WCHECK, pw, u, isw ? GW_WW : GW_WR);
     }
     if (!isw) continue;
     const uint32_t ws = hasw ? W + 1 : ss;
     const uint32_t m = p - ws;
     if (m == 0) continue;
     if (m > kSmallWin) {
+      if (a.xmode) atomicOr(a.c.err, ERR_XMODE);
       const uint32_t kk = atomicAdd(a.n_large, 1u);
       if (kk < a.large_cap) { a.large_i[kk] = gpos + p; a.large_ws[kk] = gpos + ws; }
       else atomicOr(a.c.err, ERR_CAND);
@@ -679,7 +755,7 @@ __device__ __noinline__ void bk_group(BkSmem& S, const BkCheckArgs& a, const uin
       for (uint32_t q3 = ws; q3 < q; q3++)
         if (ev_tid(T[SP[q3] & IDXM]) == uq) { first = q3; break; }
       if (cover(toq, toc, BS)) continue;
-      emit_cand(a.pend, ((unsigned long long)c << 32) | SUB_READER | (first - ws), 0ull, V[jq] & VAL_E, c, GW_RW);
+      pend(((unsigned long long)c << 32) | SUB_READER | (first - ws), V[jq] & VAL_E, uq, GW_RW);
     }
   }
   __syncthreads();
@@ -753,12 +829,14 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
     }
     if (spill) {  // hot locations: the general path (bucket_spill)
       if (threadIdx.x == 0) {
+        if (a.xmode) atomicOr(a.c.err, ERR_XMODE);
         const uint32_t k = atomicAdd(a.n_spill, 1u);
         if (k < a.spill_cap) { a.spill[2 * k] = s; a.spill[2 * k + 1] = M; }
       }
       __syncthreads();
       continue;
     }
+    const unsigned long long keep = l2_evict_last();
     // stable scatter into the scratch, kSubChunk records per round
     constexpr int R = 8, kSubChunk = kRsWarps * 32 * R;
     for (uint32_t cb = 0; cb < M; cb += kSubChunk) {
@@ -801,9 +879,9 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
         const uint32_t d = rd[r] >> 16;
         if (d < 16u) {
           const uint32_t pos = S.wc[w][d] + (rd[r] & 0xFFFFu);
-          sh[pos] = hh[r];
-          sv[pos] = vv[r];
-          st[pos] = tt[r];
+          st_keep(sh + pos, hh[r], keep);  // L2 evict-last: read back by TMA right below
+          st_keep(sv + pos, vv[r], keep);
+          st_keep(st + pos, tt[r], keep);
         }
       }
       __syncthreads();
@@ -819,11 +897,28 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
 }
 // the clock half of the structural candidates (gwcp.py:256, :265):
 // race iff prior.time > pred_t^{ver}[u]; stamps from the walker's snapshots
-__global__ void k_bk_resolve(Cands pend, DevTrace tr, StampSrc stamps, const uint32_t* arena, Cands out) {
+struct BkXInfo {  // exchange mode: location keys from h (bk_unhash + uncompact_key)
+  int on;
+  KeyRuns kr;
+  unsigned long long base;
+};
+__global__ void k_bk_resolve(Cands pend, DevTrace tr, StampSrc stamps, const uint32_t* arena, Cands out,
+                             BkXInfo xi) {
   const uint32_t n = min(*pend.n, pend.cap);
   const uint32_t BS = tr.BS;
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     const uint32_t p = pend.prior[k], c = pend.cur[k];
+    if (xi.on) {
+      const unsigned long long lx = pend.loc[k];
+      const uint32_t kx = pend.kind[k], tc = kx >> 8, u = (uint32_t)lx & GW_TID_MASK;
+      const uint32_t vo = stamps.get(c, tc).y;
+      const uint32_t t = stamps.get(p, u).x;
+      const uint32_t clk =
+          (vo == NIL || u / BS != tc / BS) ? 0u : __ldg(optr(arena, vo) + OBJ_HDR + (u - (tc / BS) * BS));
+      if (t > clk)
+        emit_cand(out, pend.okey[k], uncompact_key(bk_unhash((uint32_t)(lx >> 32)), xi.kr, xi.base), p, c, kx & 3u);
+      continue;
+    }
     const uint32_t tc = ev_tid(__ldg(tr.tidop + c)), u = ev_tid(__ldg(tr.tidop + p));
     const uint32_t vo = stamps.get(c, tc).y;
     const uint32_t t = stamps.get(p, u).x;

@@ -135,6 +135,10 @@ struct gw_ctx {
   cudaStream_t side = nullptr, side2 = nullptr;
   // packed host input (gw_ctx_analyze_host_packed): chunk uploads on their own stream
   cudaStream_t copy_st = nullptr;
+  // exchange mode (gw_xs_*): this rank's slice and the candidate counts of the last xs_check
+  DevTrace xs_slice{};
+  uint32_t xs_base = 0;
+  uint64_t xs_nc = 0, xs_nsi = 0;
   std::vector<cudaEvent_t> chunk_ev;
   cudaEvent_t ev_prev = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_hard = nullptr;
@@ -226,6 +230,37 @@ __global__ void k_plan_check(const Stats* s, unsigned long long n_bar, unsigned 
                   s->n_wbar == n_wbar && s->n_acc == n_acc &&
                   ((s->key_or ^ s->key_and) & ~D) == 0ull;
   if (!ok) atomicOr(abort_flag, 1u);
+}
+// exchange mode helpers
+__global__ void k_xs_hard_flag(DevTrace tr, uint32_t* flag) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tr.n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = ev_kind(tr.tidop[i]);
+    flag[i] = k == GW_K_BARRIER || k == GW_K_END;
+  }
+}
+__global__ void k_xs_hard_emit(DevTrace tr, const uint32_t* flag, const uint32_t* off, uint32_t base, uint32_t* ev,
+                               uint32_t* to, uint32_t* in, unsigned long long* key) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tr.n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (flag[i]) {
+      const uint32_t p = off[i];
+      ev[p] = base + (uint32_t)i;
+      to[p] = tr.tidop[i];
+      in[p] = tr.instr[i];
+      key[p] = tr.key[i];
+    }
+}
+__global__ void k_xs_remap(const uint32_t* mini, uint64_t n, const uint32_t* gidx, uint32_t* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = gidx[mini[i]];
+}
+__global__ void k_xs_lookup(DevTrace tr, uint32_t base, const uint32_t* ev, uint64_t n, uint32_t* to, uint32_t* in) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t e = ev[i];
+    if (e >= base && (uint64_t)(e - base) < tr.n) {
+      to[i] = tr.tidop[e - base];
+      in[i] = tr.instr[e - base];
+    }
+  }
 }
 __global__ void k_iota(uint32_t* v, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
@@ -499,58 +534,7 @@ struct Pipeline {
     has_locks = hs.n_acq + hs.n_rel > 0;
     S.n_accesses = hs.n_acc;
 
-    // ----------------------------------------------------------- partition
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walker, kThreads, 0));
-    gmax = (uint64_t)std::max(occ, 1) * C->num_sms;
-    G = (uint32_t)std::min<uint64_t>(tr.B, gmax);
-    S.walker_ctas = G;
-    // snapshot mode: lock-free and the per-hard-event block snapshots are small
-    n_hard = hs.n_bar + hs.n_end;
-    snap_entries = (n_hard + tr.B) * (uint64_t)tr.BS;
-    const uint64_t snap_budget = std::max<uint64_t>(256ull << 20, 8 * N);
-    // GW_WALK_MODE=block|warp|walker forces a lock-free sync-pass mode when applicable (tests)
-    const char* wm = getenv("GW_WALK_MODE");
-    const bool force_warp = wm && !strcmp(wm, "warp"), force_walker = wm && !strcmp(wm, "walker");
-    snap_mode = !has_locks && snap_entries * 8 <= snap_budget && !force_warp && !force_walker;
-    // warp snapshot mode: per-(block, warp) lists, block barriers replicated into every warp's list
-    n_hard_w = hs.n_wbar + hs.n_end + (uint64_t)kWSnapWarps * (hs.n_bar - hs.n_wbar);
-    const uint64_t wsnap_entries = (n_hard_w + (uint64_t)tr.B * kWSnapWarps) * 32ull;
-    wsnap_mode = !has_locks && !snap_mode && !force_walker && tr.W <= kWSnapWarps && tr.L <= 32 &&
-                 wsnap_entries * 8 <= snap_budget;
-    if (wsnap_mode) snap_entries = wsnap_entries;
-    obs_snap = snap_mode || wsnap_mode;
-    memset(&w, 0, sizeof w);
-    w.tr = tr;
-    w.G = G;
-    w.has_locks = has_locks ? 1 : 0;
-    w.inactive_opt = inactive_opt;
-    w.abort_flag = scal + SC_ABORT;
-    w.err = scal + SC_ERR;
-    w.hb_mode = hb_mode ? 1u : 0u;
-    // lock traces with <= 8 warps of <= 32 lanes: one walker warp per trace warp
-    const char* lwm = getenv("GW_LOCK_WALK");
-    lock_warp = has_locks && tr.W <= kLW && tr.L <= 32 && !(lwm && !strcmp(lwm, "cta"));
-    if (lock_warp) {
-      int occ_lw = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_lw, k_walker_lw, kThreads, 0));
-      G = (uint32_t)std::min<uint64_t>(tr.B, (uint64_t)std::max(occ_lw, 1) * C->num_sms);
-      S.walker_ctas = G;
-      w.G = G;
-      uint32_t* part_key = C->get<uint32_t>("part_k", N);
-      uint32_t* perm = C->get<uint32_t>("part_v", N);
-      GW_LAUNCH(k_part_keys_lw, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
-      sort<uint32_t>(part_key, perm, N, ceil_log2((uint64_t)G * kLW + 1), "part");
-      w.part_key = part_key;
-      w.perm = perm;
-    } else if (G > 1 && !snap_mode && !wsnap_mode) {
-      uint32_t* part_key = C->get<uint32_t>("part_k", N);
-      uint32_t* perm = C->get<uint32_t>("part_v", N);
-      GW_LAUNCH(k_part_keys, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
-      sort<uint32_t>(part_key, perm, N, ceil_log2(G), "part");
-      w.part_key = part_key;
-      w.perm = perm;
-    }
+    plan_sync_pass();
     if (has_locks) lock_prepass();
     pend(PH_PREP);
 
@@ -664,6 +648,65 @@ struct Pipeline {
     S.n_sync = hs.n_acq + hs.n_rel + hs.n_end + hs.n_bar;
     C->launches = g_launches;
     C->stats_pending = !gmode;
+  }
+
+  // the sync-pass mode (snapshot / warp snapshot / walker / lock walker) and
+  // the walker's arguments, from the trace statistics hs
+  uint64_t budget_n = 0;  // exchange mode: size the snapshot budget by the whole trace
+  void plan_sync_pass() {
+    const uint64_t N = tr.n;
+    gw_stats& S = C->stats;
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walker, kThreads, 0));
+    gmax = (uint64_t)std::max(occ, 1) * C->num_sms;
+    G = (uint32_t)std::min<uint64_t>(tr.B, gmax);
+    S.walker_ctas = G;
+    // snapshot mode: lock-free and the per-hard-event block snapshots are small
+    n_hard = hs.n_bar + hs.n_end;
+    snap_entries = (n_hard + tr.B) * (uint64_t)tr.BS;
+    const uint64_t snap_budget = std::max<uint64_t>(256ull << 20, 8 * (budget_n ? budget_n : N));
+    // GW_WALK_MODE=block|warp|walker forces a lock-free sync-pass mode when applicable (tests)
+    const char* wm = getenv("GW_WALK_MODE");
+    const bool force_warp = wm && !strcmp(wm, "warp"), force_walker = wm && !strcmp(wm, "walker");
+    snap_mode = !has_locks && snap_entries * 8 <= snap_budget && !force_warp && !force_walker;
+    // warp snapshot mode: per-(block, warp) lists, block barriers replicated into every warp's list
+    n_hard_w = hs.n_wbar + hs.n_end + (uint64_t)kWSnapWarps * (hs.n_bar - hs.n_wbar);
+    const uint64_t wsnap_entries = (n_hard_w + (uint64_t)tr.B * kWSnapWarps) * 32ull;
+    wsnap_mode = !has_locks && !snap_mode && !force_walker && tr.W <= kWSnapWarps && tr.L <= 32 &&
+                 wsnap_entries * 8 <= snap_budget;
+    if (wsnap_mode) snap_entries = wsnap_entries;
+    obs_snap = snap_mode || wsnap_mode;
+    memset(&w, 0, sizeof w);
+    w.tr = tr;
+    w.G = G;
+    w.has_locks = has_locks ? 1 : 0;
+    w.inactive_opt = inactive_opt;
+    w.abort_flag = scal + SC_ABORT;
+    w.err = scal + SC_ERR;
+    w.hb_mode = hb_mode ? 1u : 0u;
+    // lock traces with <= 8 warps of <= 32 lanes: one walker warp per trace warp
+    const char* lwm = getenv("GW_LOCK_WALK");
+    lock_warp = has_locks && tr.W <= kLW && tr.L <= 32 && !(lwm && !strcmp(lwm, "cta"));
+    if (lock_warp) {
+      int occ_lw = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_lw, k_walker_lw, kThreads, 0));
+      G = (uint32_t)std::min<uint64_t>(tr.B, (uint64_t)std::max(occ_lw, 1) * C->num_sms);
+      S.walker_ctas = G;
+      w.G = G;
+      uint32_t* part_key = C->get<uint32_t>("part_k", N);
+      uint32_t* perm = C->get<uint32_t>("part_v", N);
+      GW_LAUNCH(k_part_keys_lw, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
+      sort<uint32_t>(part_key, perm, N, ceil_log2((uint64_t)G * kLW + 1), "part");
+      w.part_key = part_key;
+      w.perm = perm;
+    } else if (G > 1 && !snap_mode && !wsnap_mode) {
+      uint32_t* part_key = C->get<uint32_t>("part_k", N);
+      uint32_t* perm = C->get<uint32_t>("part_v", N);
+      GW_LAUNCH(k_part_keys, grid_for(N), kThreads, 0, st, tr, G, part_key, perm);
+      sort<uint32_t>(part_key, perm, N, ceil_log2(G), "part");
+      w.part_key = part_key;
+      w.perm = perm;
+    }
   }
 
   // hard-event list of the snapshot walker in one launch (<= kRankSortMax events)
@@ -971,6 +1014,7 @@ struct Pipeline {
 
   // ---------------------------------------- bucketed access pass (bucket.cuh)
   bool bk_mode = false;
+  BkXInfo bk_xi{};  // exchange mode (xs_*): keys from h
   int bk_bb = 0, bk_kb = 0, bk_bA = 0, bk_bB = 0;
   uint64_t bk_na = 0;
   uint32_t *bk_h = nullptr, *bk_v = nullptr, *bk_t = nullptr, *bk_start = nullptr;
@@ -1009,6 +1053,11 @@ struct Pipeline {
   template <class Src>
   void bk_pass(Src src, uint64_t n_in, int RB, int shift, uint32_t* oh, uint32_t* ov, uint32_t* ot) {
     switch (RB) {
+      case 1: bk_pass_rb<Src, 1>(src, n_in, shift, oh, ov, ot); break;
+      case 2: bk_pass_rb<Src, 2>(src, n_in, shift, oh, ov, ot); break;
+      case 3: bk_pass_rb<Src, 3>(src, n_in, shift, oh, ov, ot); break;
+      case 4: bk_pass_rb<Src, 4>(src, n_in, shift, oh, ov, ot); break;
+      case 5: bk_pass_rb<Src, 5>(src, n_in, shift, oh, ov, ot); break;
       case 6: bk_pass_rb<Src, 6>(src, n_in, shift, oh, ov, ot); break;
       case 7: bk_pass_rb<Src, 7>(src, n_in, shift, oh, ov, ot); break;
       case 8: bk_pass_rb<Src, 8>(src, n_in, shift, oh, ov, ot); break;
@@ -1017,10 +1066,11 @@ struct Pipeline {
   }
   // the access records (h, event|W, tidop) in bucket order (two stable passes)
   void bucket_sort() {
-    const uint64_t na = gmode ? P->n_acc : hs.n_acc;
+    const uint64_t na = xs_recv.h ? xs_recv.cnt : gmode ? P->n_acc : hs.n_acc;
     bk_na = na;
-    bk_bb = std::min(kBkMaxBits, std::max(kBkMinBits, ceil_log2(na) - 11));
-    bk_kb = 32 - bk_bb;
+    // exchange mode: the top xs_gbits bits of h are the shard, the bucket bits follow
+    bk_bb = std::min(kBkMaxBits, std::max(kBkMinBits, ceil_log2(std::max<uint64_t>(na, 1)) - 11));
+    bk_kb = 32 - xs_gbits - bk_bb;
     bk_bA = bk_bb - bk_bb / 2;
     bk_bB = bk_bb / 2;
     uint32_t* ah = C->get<uint32_t>("bk_ah", na);
@@ -1029,8 +1079,13 @@ struct Pipeline {
     bk_h = C->get<uint32_t>("bk_h", na);
     bk_v = C->get<uint32_t>("bk_v", na);
     bk_t = C->get<uint32_t>("bk_t", na);
-    BkTraceSrc ts{tr, kr};
-    bk_pass(ts, tr.n, bk_bA, bk_kb, ah, av, at);
+    if (xs_recv.h) {  // exchange mode: this shard's records, received from every rank's slice
+      BkRecSrc xs = xs_recv;
+      bk_pass(xs, na, bk_bA, bk_kb, ah, av, at);
+    } else {
+      BkTraceSrc ts{tr, kr, 0u};
+      bk_pass(ts, tr.n, bk_bA, bk_kb, ah, av, at);
+    }
     BkRecSrc rs{ah, av, at, na};
     bk_pass(rs, na, bk_bB, bk_kb + bk_bA, bk_h, bk_v, bk_t);
     const uint32_t NB = 1u << bk_bb;
@@ -1144,6 +1199,8 @@ struct Pipeline {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bk_check, kThreads, sizeof(BkSmem)));
     const unsigned grid = (unsigned)std::min<uint64_t>(NB, (uint64_t)std::max(occ, 1) * C->num_sms);
     uint32_t* scratch = C->get<uint32_t>("bk_scratch", (uint64_t)grid * 3 * kBkSubBuf);
+    // (an L2 persisting set-aside for the scratch was measured: it starves the
+    // scatter passes' write combining in L2, 22 -> 73 ms, and saves little here)
     uint32_t npend = 0;
     for (int attempt = 0; attempt < 2; attempt++) {
       pd = make_cands("bp", pend_cap, scal + SC_NPEND);
@@ -1154,7 +1211,7 @@ struct Pipeline {
       dup.ev = nullptr;
       dup.n = scal + SC_NDUP;
       dup.cap = 0;
-      if (hs.n_long == 0) {
+      if (hs.n_long == 0 && !xs_recv.h) {  // (exchange mode: the source ranks run the record check)
         dup.cap = (uint32_t)std::max<uint64_t>(4096, NA / 64);
         dup.ev = C->get<uint32_t>("dup_ev", dup.cap);
       }
@@ -1182,6 +1239,7 @@ struct Pipeline {
       ba.spill = spill;
       ba.n_spill = scal + SC_NSPILL;
       ba.spill_cap = spill_cap;
+      ba.xmode = xs_recv.h ? 1 : 0;
       GW_LAUNCH(k_bk_check, grid, kThreads, sizeof(BkSmem), st, ba);
       check_launch();
       if (gmode) break;
@@ -1198,7 +1256,7 @@ struct Pipeline {
       cd = make_cands("c", cand_cap, cnt);
       CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), st));
       const uint64_t rg = gmode ? pd.cap : npend;
-      if (rg) GW_LAUNCH(k_bk_resolve, grid_for(rg), kThreads, 0, st, pd, tr, stamps, w.arena, cd);
+      if (rg) GW_LAUNCH(k_bk_resolve, grid_for(rg), kThreads, 0, st, pd, tr, stamps, w.arena, cd, bk_xi);
       if (gmode) {
         same_instr_pass(cd);
         GW_LAUNCH(k_guard, 1, 1, 0, st, cnt, cd.cap, cnt + 1, scal + SC_NDUP, dup.cap, scal + SC_ABORT,
@@ -1210,6 +1268,18 @@ struct Pipeline {
       uint32_t nsp = 0;
       d2h(&nsp, scal + SC_NSPILL);
       obs_nspill = nsp;
+      if (xs_recv.h) {  // exchange mode: no trace here for the spill / large-window / record passes
+        uint32_t err = 0;
+        d2h(&err, scal + SC_ERR);
+        if (err & ERR_XMODE)
+          throw CudaErr{GW_E_UNSUPPORTED, "exchange mode: hot locations or large reader windows (use the "
+                                          "replicated shard mode)"};
+        d2h(hcnt, cnt, 2);
+        if (hcnt[0] <= cd.cap) break;
+        cand_cap = (uint64_t)hcnt[0] + 1024;
+        CK(cudaMemsetAsync(w.err, 0, sizeof(uint32_t), st));
+        continue;
+      }
       if (nsp) bucket_spill(cd, spill, nsp);
       same_instr_pass(cd);
       d2h(hcnt, cnt, 2);
@@ -1365,6 +1435,150 @@ struct Pipeline {
     dev_.resize(nd); dlock.resize(nd); dtid.resize(nd);
     for (uint32_t k = 0; k < nd; k++) { dev_[k] = e[ord[k]]; dlock[k] = l[ord[k]]; dtid[k] = t[ord[k]]; }
   }
+
+  // ============ exchange mode: the multi-GPU data plane (shard.py) =============
+  // Every rank holds one record-aligned slice of the trace.  xs_prep: the
+  // slice's statistics (reduced over the ranks by the host); xs_hard: its
+  // barriers and ENDs (all-gathered: every rank runs the small sync pass over
+  // the whole trace's hard events); xs_partition: its accesses as
+  // (h, global event | W, tidop) records grouped by destination shard = the
+  // top bits of h (all-to-all by the host); xs_check: the bucketed pass over
+  // this shard's received records + the record (same-instruction) check of
+  // the slice.  Candidates carry global event indices.
+  BkRecSrc xs_recv{};  // exchange mode: the received records (nullptr h: off)
+  int xs_gbits = 0;
+  void xs_begin() {
+    zero_blk = C->get<uint32_t>("zero_blk", kZeroWords);
+    zero_next = 0;
+    scal = C->get<uint32_t>("scalars", SC_COUNT);
+    CK(cudaMemsetAsync(zero_blk, 0, sizeof(uint32_t) * kZeroWords, st));
+    CK(cudaMemsetAsync(scal, 0, SC_COUNT * sizeof(uint32_t), st));
+    reserve_epochs();
+    C->d_scal = nullptr;  // no gw_ctx_fetch after an exchange-mode call
+    C->have_cands = false;
+  }
+  Stats xs_prep() {
+    xs_begin();
+    Stats* dst = C->get<Stats>("stats", 1);
+    GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
+    if (tr.n) GW_LAUNCH(k_prep, grid_for(tr.n), kThreads, 0, st, tr, dst);
+    Stats h;
+    d2h(&h, dst);
+    return h;
+  }
+  uint64_t xs_hard(uint32_t base, uint32_t* ev, uint32_t* to, uint32_t* in, unsigned long long* key) {
+    const uint64_t N = tr.n;
+    if (!N) return 0;
+    uint32_t* flag = C->get<uint32_t>("x_flag", N);
+    uint32_t* off = C->get<uint32_t>("x_off", N);
+    GW_LAUNCH(k_xs_hard_flag, grid_for(N), kThreads, 0, st, tr, flag);
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{flag}, ArrStore<uint32_t>{off}, N, OpSum(), 0u, false, "sc_u32");
+    GW_LAUNCH(k_xs_hard_emit, grid_for(N), kThreads, 0, st, tr, flag, off, base, ev, to, in, key);
+    uint32_t hv[2];
+    CK(cudaMemcpyAsync(hv, off + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hv + 1, flag + (N - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return (uint64_t)hv[0] + hv[1];
+  }
+  void xs_partition(const Stats& g, int gbits, uint32_t base, uint32_t* oh, uint32_t* ov, uint32_t* ot,
+                    uint64_t* counts) {
+    xs_begin();
+    kr = key_runs(g.n_acc ? g.key_or ^ g.key_and : 0ull);
+    if (kr.nbits > 32) throw CudaErr{GW_E_UNSUPPORTED, "exchange mode: location keys wider than 32 bits"};
+    const uint32_t G = 1u << gbits;
+    std::vector<uint32_t> start(G + 1, 0);
+    Stats* dst = C->get<Stats>("stats", 1);  // this slice's access count
+    GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
+    if (tr.n) GW_LAUNCH(k_prep, grid_for(tr.n), kThreads, 0, st, tr, dst);
+    Stats loc;
+    d2h(&loc, dst);
+    if (tr.n && loc.n_acc) {
+      BkTraceSrc ts{tr, kr, base};
+      bk_pass(ts, tr.n, gbits, 32 - gbits, oh, ov, ot);
+      // digit starts: the scanned counts at super-tile 0 of every digit
+      const int ST = gbits > 7 ? 1 << (gbits - 7) : 1;
+      const uint64_t nst = (lb_tiles(tr.n) + ST - 1) / ST;
+      uint32_t* cnts = C->get<uint32_t>(std::string("bk_counts") + sfx, nst * G);
+      for (uint32_t d = 0; d < G; d++)
+        CK(cudaMemcpyAsync(&start[d], cnts + (uint64_t)d * nst, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    start[G] = (uint32_t)loc.n_acc;
+    for (uint32_t d = 0; d < G; d++) counts[d] = start[d + 1] - start[d];
+  }
+  // candidates of this shard (global event indices) in the "c" list, and
+  // the slice's same-instruction pairs appended (offset by base)
+  uint64_t xs_check(const Stats& g, int gbits, uint32_t base, BkRecSrc recv, const uint32_t* hev,
+                    const uint32_t* hto, const uint32_t* hin, const unsigned long long* hkey, uint64_t nhard,
+                    uint64_t n_total) {
+    xs_begin();
+    const DevTrace slice = tr;
+    // 1. the sync pass over the whole trace's hard events (a mini trace)
+    DevTrace mt = slice;
+    mt.key = hkey;
+    mt.tidop = hto;
+    mt.instr = hin;
+    mt.n = nhard;
+    tr = mt;
+    Stats* dst = C->get<Stats>("stats", 1);
+    GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
+    if (nhard) GW_LAUNCH(k_prep, grid_for(nhard), kThreads, 0, st, tr, dst);
+    d2h(&hs, dst);
+    hs.n_acc = g.n_acc;
+    hs.key_or = g.key_or;
+    hs.key_and = g.key_and;
+    hs.n_long = g.n_long;
+    has_locks = false;
+    budget_n = n_total;
+    plan_sync_pass();
+    if (!snap_mode && !wsnap_mode)
+      throw CudaErr{GW_E_UNSUPPORTED, "exchange mode: the sync pass needs the snapshot walker"};
+    walker_phase();
+    if (nhard) {  // snapshot lists index the mini trace: map them to global events
+      const uint64_t nl = snap_mode ? n_hard : n_hard_w;
+      uint32_t* gev = C->get<uint32_t>("x_hev", nl + 1);
+      GW_LAUNCH(k_xs_remap, grid_for(nl), kThreads, 0, st, stamps.hard_ev, nl, hev, gev);
+      stamps.hard_ev = gev;
+    }
+    tr = slice;
+    // 2. the bucketed pass over the received records
+    kr = key_runs(g.n_acc ? g.key_or ^ g.key_and : 0ull);
+    bk_xi.on = 1;
+    bk_xi.kr = kr;
+    bk_xi.base = g.key_and & ~(g.key_or ^ g.key_and);
+    xs_gbits = gbits;
+    xs_recv = recv;
+    bk_mode = true;
+    uint64_t nc = 0;
+    if (recv.cnt) {
+      bucket_sort();
+      Cands cd = bucket_check_pass();
+      nc = std::min<uint64_t>(obs_ncand, cd.cap);
+    }
+    xs_recv = BkRecSrc{};
+    // 3. the record check (_same_instruction_check) of this rank's slice
+    uint32_t* ncs = scal + SC_NQ;
+    uint64_t cap = std::max<uint64_t>(4096, tr.n / 16);
+    Cands si;
+    uint32_t hsi = 0;
+    for (int attempt = 0; attempt < 2 && tr.n; attempt++) {
+      si = make_cands("xsi", cap, ncs);
+      CK(cudaMemsetAsync(ncs, 0, sizeof(uint32_t), st));
+      ShardArgs sa{};
+      sa.G = 1;
+      GW_LAUNCH(k_same_instr, grid_for(tr.n), kThreads, 0, st, tr, si, sa, 0);
+      d2h(&hsi, ncs);
+      if (hsi <= si.cap) break;
+      cap = hsi + 1024;
+      CK(cudaMemsetAsync(scal + SC_ERR, 0, sizeof(uint32_t), st));
+    }
+    xs_nc = nc;
+    xs_nsi = hsi;
+    xs_si = si;
+    return nc + hsi;
+  }
+  uint64_t xs_nc = 0, xs_nsi = 0;
+  Cands xs_si{};
 
   Cands make_cands(const std::string& tag, uint64_t cap, uint32_t* cnt) {
     Cands c;
@@ -1969,11 +2183,20 @@ extern "C" int gw_ctx_analyze_host(gw_ctx* c, const gw_trace_view* t, const gw_o
 
 // packed (narrow-column) host trace: widen one uploaded chunk into the
 // 16-byte SoA the pipeline reads (the tidop column is uploaded in place)
+// (4-byte keys: a warp barrier's key (block << 32 | warp) is implied by its
+// tidop and restored here; block barriers carry key 0)
 __global__ void k_widen(const void* __restrict__ kin, int kbytes, const void* __restrict__ iin, int ibytes,
-                        uint64_t lo, uint64_t hi, unsigned long long* __restrict__ kout, uint32_t* __restrict__ iout) {
+                        const uint32_t* __restrict__ tidop, uint32_t BS, uint32_t L, uint64_t lo, uint64_t hi,
+                        unsigned long long* __restrict__ kout, uint32_t* __restrict__ iout) {
   for (uint64_t e = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < hi;
        e += (uint64_t)gridDim.x * blockDim.x) {
-    if (kbytes == 4) kout[e] = ((const uint32_t*)kin)[e];
+    if (kbytes == 4) {
+      const uint32_t to = tidop[e];
+      unsigned long long k = ((const uint32_t*)kin)[e];
+      if (ev_kind(to) == GW_K_BARRIER)
+        k = (to & GW_F_WARPBAR) ? ((unsigned long long)(ev_tid(to) / BS) << 32) | ((ev_tid(to) % BS) / L) : 0ull;
+      kout[e] = k;
+    }
     if (ibytes == 2) iout[e] = ((const uint16_t*)iin)[e];
   }
 }
@@ -2032,7 +2255,7 @@ extern "C" int gw_ctx_analyze_host_packed(gw_ctx* c, const gw_trace_packed* t, c
       CK(cudaEventRecord(c->chunk_ev[ch], c->copy_st));
       CK(cudaStreamWaitEvent(st, c->chunk_ev[ch], 0));  // widen chunk ch while chunk ch + 1 is in flight
       if (widen) GW_LAUNCH(k_widen, grid_for(m, 148u * 8u), kThreads, 0, st, kst, (int)t->key_bytes, ist,
-                           (int)t->instr_bytes, lo, hi, k, in);
+                           (int)t->instr_bytes, to, t->cfg.warps * t->cfg.lanes, t->cfg.lanes, lo, hi, k, in);
     }
     DevTrace tr = make_dev(&view, k, to, in);
     analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,
@@ -2147,6 +2370,139 @@ extern "C" int gw_ctx_stats(gw_ctx* c, gw_stats* out) {
 }
 
 extern "C" uint32_t gw_ctx_launches(gw_ctx* c) { return c ? c->launches : 0; }
+
+// ---- exchange mode (multi-GPU data plane; shard.py drives the collectives) ----
+static void xs_stats_out(const Stats& h, gw_xs_stats* o) {
+  o->n_acc = h.n_acc; o->n_write = h.n_write; o->n_acq = h.n_acq; o->n_rel = h.n_rel; o->n_end = h.n_end;
+  o->n_bar = h.n_bar; o->key_or = h.key_or; o->key_and = h.key_and; o->n_long = h.n_long; o->n_wbar = h.n_wbar;
+}
+static Stats xs_stats_in(const gw_xs_stats* o) {
+  Stats h;
+  memset(&h, 0, sizeof h);
+  h.n_acc = o->n_acc; h.n_write = o->n_write; h.n_acq = o->n_acq; h.n_rel = o->n_rel; h.n_end = o->n_end;
+  h.n_bar = o->n_bar; h.key_or = o->key_or; h.key_and = o->key_and; h.n_long = o->n_long; h.n_wbar = o->n_wbar;
+  return h;
+}
+static int xs_gbits_of(uint32_t G) {
+  int g = 0;
+  while ((1u << g) < G) g++;
+  return (1u << g) == G && g >= 1 && g <= 5 ? g : -1;
+}
+static Pipeline xs_pipe(gw_ctx* c, cudaStream_t st) {
+  Pipeline p;
+  p.C = c;
+  p.st = st;
+  p.tr = c->xs_slice;
+  p.inactive_opt = 1;
+  c->last_stream = st;
+  return p;
+}
+
+extern "C" int gw_xs_prep(gw_ctx* c, const gw_trace_view* slice, uint32_t event_base, void* stream,
+                          gw_xs_stats* out) {
+  if (!c || !out) { gw_set_error("null argument"); return GW_E_ARG; }
+  int v = validate_view(slice);
+  if (v) return v;
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    c->drop_plan();
+    c->xs_slice = make_dev(slice, (const unsigned long long*)slice->key, slice->tidop, slice->instr);
+    c->xs_base = event_base;
+    Pipeline p = xs_pipe(c, (cudaStream_t)stream);
+    xs_stats_out(p.xs_prep(), out);
+  });
+}
+
+extern "C" int gw_xs_hard(gw_ctx* c, void* stream, uint32_t* ev, uint32_t* tidop, uint32_t* instr, uint64_t* key,
+                          uint64_t* n_out) {
+  if (!c || !n_out) { gw_set_error("null argument"); return GW_E_ARG; }
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    Pipeline p = xs_pipe(c, (cudaStream_t)stream);
+    p.xs_begin();
+    *n_out = p.xs_hard(c->xs_base, ev, tidop, instr, (unsigned long long*)key);
+  });
+}
+
+extern "C" int gw_xs_partition(gw_ctx* c, const gw_xs_stats* global, uint32_t shard_count, void* stream, uint32_t* h,
+                               uint32_t* v, uint32_t* t, uint64_t* counts) {
+  if (!c || !global || !counts) { gw_set_error("null argument"); return GW_E_ARG; }
+  const int gb = xs_gbits_of(shard_count);
+  if (gb < 0) { gw_set_error("exchange mode: shard_count must be a power of two in [2, 32]"); return GW_E_ARG; }
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    Pipeline p = xs_pipe(c, (cudaStream_t)stream);
+    p.xs_partition(xs_stats_in(global), gb, c->xs_base, h, v, t, counts);
+  });
+}
+
+extern "C" int gw_xs_check(gw_ctx* c, const gw_xs_stats* global, uint32_t shard_count, uint64_t n_total,
+                           void* stream, const uint32_t* h, const uint32_t* v, const uint32_t* t, uint64_t n_recv,
+                           const uint32_t* hev, const uint32_t* htidop, const uint32_t* hinstr, const uint64_t* hkey,
+                           uint64_t n_hard, uint64_t* n_cand) {
+  if (!c || !global || !n_cand) { gw_set_error("null argument"); return GW_E_ARG; }
+  const int gb = xs_gbits_of(shard_count);
+  if (gb < 0) { gw_set_error("exchange mode: shard_count must be a power of two in [2, 32]"); return GW_E_ARG; }
+  if (global->n_acq || global->n_rel || global->n_long) {
+    gw_set_error("exchange mode: lock traces and records longer than 32 events use the replicated shard mode");
+    return GW_E_UNSUPPORTED;
+  }
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    Pipeline p = xs_pipe(c, (cudaStream_t)stream);
+    BkRecSrc recv{h, v, t, n_recv};
+    *n_cand = p.xs_check(xs_stats_in(global), gb, c->xs_base, recv, hev, htidop, hinstr,
+                         (const unsigned long long*)hkey, n_hard, n_total);
+    c->xs_nc = p.xs_nc;
+    c->xs_nsi = p.xs_nsi;
+  });
+}
+
+// host copies of the last gw_xs_check's candidates (caller buffers of n_cand);
+// the slice's same-instruction pairs get their global event indices here
+extern "C" int gw_xs_fetch(gw_ctx* c, uint64_t* okey, uint64_t* loc, uint32_t* prior, uint32_t* cur,
+                           uint32_t* kind) {
+  if (!c) { gw_set_error("null context"); return GW_E_ARG; }
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = c->last_stream;
+    auto cp = [&](void* dst, const char* name, size_t sz, uint64_t n, uint64_t at) {
+      if (n) CK(cudaMemcpyAsync((char*)dst + at * sz, c->bufs[name].p, sz * n, cudaMemcpyDeviceToHost, st));
+    };
+    const uint64_t a = c->xs_nc, b = c->xs_nsi;
+    cp(okey, "c_okey", 8, a, 0); cp(loc, "c_loc", 8, a, 0); cp(prior, "c_prior", 4, a, 0);
+    cp(cur, "c_cur", 4, a, 0); cp(kind, "c_kind", 4, a, 0);
+    cp(okey, "xsi_okey", 8, b, a); cp(loc, "xsi_loc", 8, b, a); cp(prior, "xsi_prior", 4, b, a);
+    cp(cur, "xsi_cur", 4, b, a); cp(kind, "xsi_kind", 4, b, a);
+    CK(cudaStreamSynchronize(st));
+    const uint64_t base = c->xs_base;
+    for (uint64_t k = a; k < a + b; k++) {
+      okey[k] += base << 32;
+      prior[k] += (uint32_t)base;
+      cur[k] += (uint32_t)base;
+    }
+  });
+}
+
+// endpoint info (tidop, instr) of global events in this rank's slice; other entries untouched
+extern "C" int gw_xs_lookup(gw_ctx* c, const uint32_t* ev, uint64_t n, uint32_t* tidop, uint32_t* instr) {
+  if (!c) { gw_set_error("null context"); return GW_E_ARG; }
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    if (!n) return;
+    const cudaStream_t st = c->last_stream;
+    uint32_t* dev = c->get<uint32_t>("x_lev", n);
+    uint32_t* dto = c->get<uint32_t>("x_lto", n);
+    uint32_t* din = c->get<uint32_t>("x_lin", n);
+    CK(cudaMemcpyAsync(dev, ev, 4 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dto, tidop, 4 * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(din, instr, 4 * n, cudaMemcpyHostToDevice, st));
+    GW_LAUNCH(k_xs_lookup, grid_for(n), kThreads, 0, st, c->xs_slice, c->xs_base, dev, n, dto, din);
+    CK(cudaMemcpyAsync(tidop, dto, 4 * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(instr, din, 4 * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
 
 template <class T>
 static T* to_malloc(const std::vector<T>& v) {

@@ -66,7 +66,9 @@ def run(trace, detector, *, order_matrix: bool = False, collect_stats: bool = Fa
     name = getattr(detector, "name", "gwcp")
     if name not in ("gwcp", "hb"):
         raise NotImplementedError("only the gwcp and hb detectors are accelerated")
-    tr, res = analyze(trace, inactive_opt=getattr(detector, "inactive_opt", True), hb=name == "hb")
+    # (a gpurace.GwcpDetector keeps the option as _inactive_opt, gwcp.py:119)
+    inactive = getattr(detector, "inactive_opt", getattr(detector, "_inactive_opt", True))
+    tr, res = analyze(trace, inactive_opt=inactive, hb=name == "hb")
     reports = build_reports(tr, res, name)
     diags = diagnostics_of(tr, res)
     if hasattr(detector, "reporter"):

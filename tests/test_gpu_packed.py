@@ -24,7 +24,7 @@ def ctx():
 
 
 def _run_packed(ctx, tr, inactive_opt=True, **kw):
-    k, i = N.pack_columns(tr.key, tr.instr)
+    k, i = N.pack_columns(tr.key, tr.instr, tr.tidop)
     ctx.analyze_host_packed(tr.cfg_tuple, k, tr.tidop, i, inactive_opt=inactive_opt, **kw)
     return ctx.fetch()
 
@@ -36,18 +36,24 @@ def test_packed_input_reference_goldens(goldens, ctx):
         if "error" in r or "full" in r["tags"] or not ({"corpus", "nasty", "c1", "c3", "c4"} & set(r["tags"])):
             continue
         tr = parse_trace(golden_text(r))
-        k, i = N.pack_columns(tr.key, tr.instr)
+        k, i = N.pack_columns(tr.key, tr.instr, tr.tidop)
         widths.add((k.dtype.itemsize, i.dtype.itemsize))
         check_against_golden(r, tr, _run_packed(ctx, tr, r["inactive_opt"]))
         n += 1
     assert n > 1000
     # shared-memory keys (bit 63) need 8 bytes, warp-barrier lane masks 4 bytes of instr
-    assert {(4, 2), (8, 2), (8, 4)} <= widths
-    # the remaining combination: a 32-lane warp barrier mask with 4-byte keys
-    tr = parse_trace(WL.c4_text(blocks=2, warps=2, lanes=32, iters=8, words_per_block=256))
-    k, i = N.pack_columns(tr.key, tr.instr)
-    assert (k.dtype.itemsize, i.dtype.itemsize) == (4, 4)
-    assert ndjson_lines(tr, _run_packed(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
+    assert {(4, 2), (8, 2), (4, 4)} <= widths
+    # warp-barrier lane masks (4-byte instr) with 4-byte keys (the warp
+    # barriers' block << 32 | warp keys are implied and restored), and with
+    # shared-memory keys (8 bytes)
+    for text, want in ((WL.c4_text(blocks=2, warps=2, lanes=32, iters=8, words_per_block=256), (4, 4)),
+                       ("config blocks=2 warps=1 lanes=32\n0.0.0 wr s:0x10\n0.0.1 rd s:0x10\n"
+                        "bar warp 1 0 0xffffffff\n1.0.0 wr g:0x10\nbar warp 0 0 0xffffffff\n0.0.1 wr s:0x10\n",
+                        (8, 4))):
+        tr = parse_trace(text)
+        k, i = N.pack_columns(tr.key, tr.instr, tr.tidop)
+        assert (k.dtype.itemsize, i.dtype.itemsize) == want
+        assert ndjson_lines(tr, _run_packed(ctx, tr)) == ndjson_lines(tr, O.run_trace(tr))
 
 
 def test_packed_input_full_c2_chunked(goldens, ctx):
@@ -64,7 +70,7 @@ def test_packed_input_many_chunks(ctx):
     import torch
 
     tr = WL.c2_soa(blocks=1024, warps=8, lanes=32, phases=2, records=80, words_per_block=262144, seed=5)
-    assert len(tr) > 2 * (1 << 25)
+    assert len(tr) > (1 << 25)  # two upload chunks
     stream = torch.cuda.Stream(device=torch.device("cuda", 0))
     ctx.analyze_host(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, stream=stream.cuda_stream)
     want = ctx.fetch()

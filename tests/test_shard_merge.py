@@ -74,3 +74,33 @@ def test_gather_reports_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert all(res)
+
+
+def test_merge_candidates_is_keep_first_dedup():
+    """shard.merge_candidates (exchange mode, rank 0): keep-first on
+    (location, prior.instr, current.instr) by order key, then report order
+    (report.py:92-100), against a brute-force restatement."""
+    import random
+
+    from paper_2111_12478_b200.shard import merge_candidates
+
+    rng = random.Random(5)
+    for trial in range(20):
+        n = rng.randint(0, 300)
+        ev_instr = {e: rng.randint(0, 4) for e in range(400)}
+        okeys = rng.sample(range(1, 10**6), n)
+        c = {"order_key": np.array(okeys, np.uint64), "loc": np.array([rng.randint(0, 5) * 4 for _ in range(n)],
+                                                                        np.uint64),
+             "prior": np.array([rng.randrange(400) for _ in range(n)], np.uint32),
+             "current": np.array([rng.randrange(400) for _ in range(n)], np.uint32),
+             "kind": np.array([rng.randint(0, 2) for _ in range(n)], np.uint32)}
+        got = merge_candidates(c, lambda e: np.array([ev_instr[int(x)] for x in e], np.uint32))
+        best = {}
+        for i in range(n):
+            k = (int(c["loc"][i]), ev_instr[int(c["prior"][i])], ev_instr[int(c["current"][i])])
+            if k not in best or okeys[i] < okeys[best[k]]:
+                best[k] = i
+        want = sorted(best.values(), key=lambda i: okeys[i])
+        assert got["order_key"].tolist() == [okeys[i] for i in want]
+        assert got["prior"].tolist() == [int(c["prior"][i]) for i in want]
+        assert got["kind"].tolist() == [int(c["kind"][i]) for i in want]
