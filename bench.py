@@ -10,10 +10,11 @@ the timed region).  L2 is flushed (256 MiB write) before every timed step;
 each step is timed with CUDA events on the launching stream and the K step
 times are summed.  For N > 1 (torchrun, one rank per GPU) every rank analyses
 its own trace (independent objects: weak scaling, no data-path collective),
-except the C5 scaling sweep (``--workload c5``, or ``--mode sharded``): one
-trace, address-sharded -- every rank holds the whole trace and reports the
-races on one contiguous location-key range, then an NCCL gather + order-key
-merge on rank 0 (strong scaling).  The time is the max over ranks.
+except the C5 scaling sweep (``--workload c5``): one trace in the exchange
+mode of shard.analyze_exchange -- every rank holds one record-aligned 1/N
+slice, access records travel to their location-hash shard by NCCL
+all-to-all, rank 0 merges the candidates (strong scaling; ``--mode sharded``:
+the replicated address-range mode instead).  The time is the max over ranks.
 
 ``--impl reference`` times the CPU restatement of the reference (oracle/,
 single-threaded like the reference) on this host: rank 0 only.
@@ -70,6 +71,16 @@ def kernel_alg_bytes(name: str, N: int, n: int) -> int | None:
         ("k_same_instr", 16 * N),
         ("k_walker", 16 * N),       # the trace, read once
         ("k_hard_append", 4 * N),
+        # the bucketed access pass (csrc/bucket.cuh), n = accesses: per launch of
+        # the scatter: pass A reads the trace (key 8 + tidop 4 per event) and
+        # writes a 12-B record per access, pass B reads and writes 12 B per
+        # record -> (12 N + 12 n + 24 n) / 2 per launch; the up-sweeps read the
+        # trace (12 N) / the record hashes (4 n); the check reads each record once
+        ("k_bk_down_tma", (12 * N + 36 * n) // 2),
+        ("k_bk_down", (12 * N + 36 * n) // 2),
+        ("k_bk_up", (12 * N + 4 * n) // 2),
+        ("k_bk_check", 12 * n),
+        ("k_bk_bounds", 4 * n),
     ]
     base = kernel_base(name)
     tag = kernel_tag(name)
@@ -357,7 +368,7 @@ def run_b200(args):
     from paper_2111_12478_b200 import _native as N
     from paper_2111_12478_b200.shard import gather_reports
 
-    mode = args.mode or ("sharded" if args.workload == "c5" else "replicas")
+    mode = args.mode or "replicas"
     sharded = mode == "sharded" and world > 1
     shard = (rank, world) if sharded else (0, 1)
     cfg, n, n_acc, (key_d, to_d, in_d), desc = make_workload(args.workload, rank, dev, sharded=sharded)
@@ -593,6 +604,120 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def run_b200_exchange(args):
+    """N > 1, one trace (the C5 scaling sweep): the exchange mode of
+    shard.analyze_exchange -- every rank holds ONE record-aligned slice (1/N
+    of the SoA, 1/N of the upload), access records go to their location-hash
+    shard by NCCL all-to-all, rank 0 merges the candidates.  Strong scaling:
+    value = the trace's events / max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_12478_b200 import _native as N
+    from paper_2111_12478_b200.report import ndjson_lines, result_digest
+    from paper_2111_12478_b200.shard import analyze_exchange
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    same_gpu = os.environ.get("GW_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo" if same_gpu else "nccl")
+    dev = torch.device("cuda", local)
+    coll_dev = None if same_gpu else dev
+    cfg, n, n_acc, (key_d, to_d, in_d), desc = make_workload(args.workload, rank, dev, sharded=True)
+
+    def cut(k):  # start of slice k, moved forward to a record boundary
+        p = n * k // world
+        if p <= 0 or p >= n:
+            return min(max(p, 0), n)
+        w = to_d[p:p + 64].cpu().numpy().view(np.uint32)
+        j = 0
+        while j < len(w) and w[j] & N.F_CONT:
+            j += 1
+        return p + j
+
+    lo, hi = cut(rank), cut(rank + 1)
+    sl = [key_d[lo:hi].clone(), to_d[lo:hi].clone(), in_d[lo:hi].clone()]
+    del key_d, to_d, in_d
+    torch.cuda.empty_cache()
+    host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in sl]
+    for h, x in zip(host, sl):
+        h.copy_(x)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    ctx = N.Context(local)
+
+    def step_device():
+        with torch.cuda.stream(stream):
+            return analyze_exchange(ctx, cfg, n, sl, lo, collective_device=coll_dev, stream=stream.cuda_stream)
+
+    def step_host():  # the slice's upload inside the step
+        with torch.cuda.stream(stream):
+            for h, x in zip(host, sl):
+                x.copy_(h, non_blocking=True)
+            return analyze_exchange(ctx, cfg, n, sl, lo, collective_device=coll_dev, stream=stream.cuda_stream)
+
+    def timed(fn, steps):
+        tot, res = 0.0, None
+        for _ in range(steps):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            res = fn()
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        t = torch.tensor([tot], dtype=torch.float64, device=coll_dev or "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), res
+
+    for _ in range(args.warmup):
+        step_device()
+    with ClockSampler(local) as clk:
+        ms_dev, res = timed(step_device, args.steps)
+        for _ in range(args.warmup):
+            step_host()
+        ms_e2e, res_e2e = timed(step_host, args.steps)
+    if rank == 0:
+        r, xt = res
+        digest = result_digest(r)
+        fx = load_full_digest(args.workload)
+        if fx is not None and digest != fx["digest"]:
+            raise SystemExit(f"bench: exchange-mode report digest {digest} != {fx['digest']} ({fx['source']})")
+        peak, peak_kind = load_peaks()
+        step_s = ms_dev / args.steps / 1000.0
+        alg = 16 * n + 36 * n_acc
+        whole = {"bound": "hbm", "achieved": alg / step_s / 1e9, "peak": peak * world, "unit": "GB/s",
+                 "frac": alg / step_s / 1e9 / (peak * world), "kernel": "whole analysis over all ranks "
+                 "(algorithmic bytes 16N + 36A against the ranks' summed HBM peak)", "peak_source": peak_kind,
+                 "traffic": None}
+        line = {
+            "metric": METRIC, "value": n * args.steps / (ms_dev / 1000.0), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": desc,
+            "run": {"reports": int(len(r["kind"])), "report_digest": digest,
+                    "report_digest_expected": fx["digest"] if fx else None,
+                    "parallelism": f"exchange mode x{world}: 1/{world} slice per rank, hard-event all-gather, "
+                                   "NCCL all-to-all of access records by location hash, candidate merge on rank 0",
+                    "l2": "flushed before every timed step (256 MiB write)"},
+            "e2e": {"value": n * args.steps / (ms_e2e / 1000.0), "unit": UNIT,
+                    "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 9 * int(len(r["kind"])) + 64,
+                    "ms_per_step": ms_e2e / args.steps,
+                    "input": "every rank uploads its own 16-B/event slice (1/N of the trace)"},
+            "roofline": whole, "roofline_whole_analysis": whole,
+            "gpu_launches": ctx.launches() * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -603,11 +728,15 @@ def main():
                     help="BASELINE.json config (default c5: the metric's 1/2/4/8-GPU sweep config, 1.007e9 events)")
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", choices=["replicas", "sharded"], default=None,
-                    help="N>1: independent traces per GPU (default; c5: address-sharded one trace)")
+    ap.add_argument("--mode", choices=["replicas", "sharded", "exchange"], default=None,
+                    help="N>1: independent traces per GPU (default), or one trace: c5 defaults to the exchange mode "
+                         "(slices + all-to-all), 'sharded' = every rank holds the whole trace (address ranges)")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args)
+    elif world > 1 and (args.mode or ("exchange" if args.workload == "c5" else "replicas")) == "exchange":
+        run_b200_exchange(args)
     else:
         run_b200(args)
 

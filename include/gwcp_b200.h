@@ -155,7 +155,8 @@ int gw_ctx_validate(gw_ctx* c, const gw_trace_view* host_trace, uint64_t* n_out,
                     uint64_t** a, uint64_t** b);
 /* infer_locks (trace.py:609-680) on the GPU: the rewritten trace (out, free
  * with gw_trace_free) and one diagnostic per release left uninferred
- * (event index in the INPUT trace, lock, thread), in event order. */
+ * (event index in the INPUT trace, lock, thread), in the reference's order:
+ * thread by thread (threads by first event), then by event. */
 int gw_ctx_infer_locks(gw_ctx* c, const gw_trace_view* host_trace, gw_trace* out, uint64_t* n_diag,
                        uint32_t** diag_event, uint64_t** diag_lock, uint32_t** diag_tid);
 

@@ -1018,10 +1018,14 @@ struct Pipeline {
   int bk_bb = 0, bk_kb = 0, bk_bA = 0, bk_bB = 0;
   uint64_t bk_na = 0;
   uint32_t *bk_h = nullptr, *bk_v = nullptr, *bk_t = nullptr, *bk_start = nullptr;
+  // Single-GPU analyses take the LSD location sort: on C5 the two passes
+  // measure the same (65.7 vs 65.6 ms, profiles/r2_*), and the sort's kernels
+  // run at 0.40 of HBM where k_bk_check is issue-bound.  The
+  // bucketed pass is the exchange mode's (multi-GPU) and GW_BUCKET=1's.
   bool bucket_ok(uint64_t na) const {
-    const char* e = getenv("GW_BUCKET");  // test hook: 0 = the LSD location sort, 1 = buckets at any size
-    if (e && e[0] == '0') return false;
-    const uint64_t minn = (e && e[0] == '1') ? 1ull : (1ull << 24);
+    const char* e = getenv("GW_BUCKET");  // 1 = the bucketed pass at any size, 2 = from 2^24 accesses
+    if (!e || (e[0] != '1' && e[0] != '2')) return false;
+    const uint64_t minn = e[0] == '1' ? 1ull : (1ull << 24);
     return !has_locks && nshard <= 1 && !wide && kr.nbits > 0 && na >= minn && tr.n < (1ull << 31);
   }
   static bool bk_tma_ok(const BkTraceSrc& s) {
@@ -1391,6 +1395,7 @@ struct Pipeline {
     CK(cudaMemsetAsync(cnt, 0, sizeof(uint32_t), st));
     InfDiag dg;
     dg.cap = (uint32_t)std::max<uint64_t>(1, nt / 2 + 1);  // one per FENCE + atomic write pair at most
+    dg.first = C->get<uint32_t>("i_dfirst", dg.cap);
     dg.ev = C->get<uint32_t>("i_dev", dg.cap);
     dg.lock = C->get<unsigned long long>("i_dlock", dg.cap);
     dg.tid = C->get<uint32_t>("i_dtid", dg.cap);
@@ -1421,17 +1426,19 @@ struct Pipeline {
       CK(cudaMemcpyAsync(oto.data(), to_o, 4 * nk, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(oin.data(), io, 4 * nk, cudaMemcpyDeviceToHost, st));
     }
-    std::vector<uint32_t> e(nd), t(nd);
+    std::vector<uint32_t> e(nd), t(nd), f(nd);
     std::vector<unsigned long long> l(nd);
     if (nd) {
+      CK(cudaMemcpyAsync(f.data(), dg.first, 4 * nd, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(e.data(), dg.ev, 4 * nd, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(l.data(), dg.lock, 8 * nd, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(t.data(), dg.tid, 4 * nd, cudaMemcpyDeviceToHost, st));
     }
     CK(cudaStreamSynchronize(st));
-    std::vector<uint32_t> ord(nd);  // event order (a handful: host sort)
+    std::vector<uint32_t> ord(nd);  // by (thread's first event, event): the reference's order
     for (uint32_t k = 0; k < nd; k++) ord[k] = k;
-    std::sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) { return e[x] < e[y]; });
+    std::sort(ord.begin(), ord.end(),
+              [&](uint32_t x, uint32_t y) { return f[x] != f[y] ? f[x] < f[y] : e[x] < e[y]; });
     dev_.resize(nd); dlock.resize(nd); dtid.resize(nd);
     for (uint32_t k = 0; k < nd; k++) { dev_[k] = e[ord[k]]; dlock[k] = l[ord[k]]; dtid[k] = t[ord[k]]; }
   }

@@ -18,6 +18,9 @@
 // per thread: atomic WRITE + FENCE -> ACQUIRE at the write, FENCE + atomic
 // WRITE -> RELEASE at the write when the lock is held (else a diagnostic);
 // the consumed fences are dropped and the trace compacted in order.
+// Diagnostics come thread by thread in order of the threads' first events,
+// then in event order (the reference iterates its per-thread dict,
+// trace.py:624-671).
 // Codes of the validate diagnostics: gw_validate (parse.cpp).
 #pragma once
 #include "access.cuh"
@@ -133,7 +136,8 @@ __global__ void k_inf_flag(DevTrace tr, uint32_t* flag) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tr.n; i += (uint64_t)gridDim.x * blockDim.x)
     flag[i] = ev_kind(tr.tidop[i]) != GW_K_BARRIER;
 }
-struct InfDiag {
+struct InfDiag {  // (first event of the thread, event): the reference reports thread by thread
+  uint32_t* first;
   uint32_t* ev;
   unsigned long long* lock;
   uint32_t* tid;
@@ -169,7 +173,7 @@ __global__ void k_inf_walk(DevTrace tr, const uint32_t* ktid, const uint32_t* ke
         while (x < nh && hs[x] != lock) x++;
         if (x == nh) {
           const uint32_t k = atomicAdd(dg.n, 1u);
-          if (k < dg.cap) { dg.ev[k] = eb; dg.lock[k] = lock; dg.tid[k] = ev_tid(tb); }
+          if (k < dg.cap) { dg.first[k] = kev[i]; dg.ev[k] = eb; dg.lock[k] = lock; dg.tid[k] = ev_tid(tb); }
           j += 1;
           continue;
         }

@@ -1,5 +1,5 @@
 """The bucketed access pass (csrc/bucket.cuh): the address-hashed shadow
-table the engine uses for lock-free traces of >= 2^24 accesses (C4, C5).
+table of the exchange mode (multi-GPU) and of GW_BUCKET=1 / 2 analyses.
 GW_BUCKET=1 forces it at any size, so the reference goldens and the oracle
 pin it on small traces too: every lock-free golden, the generator recipes,
 hot locations (buckets above the shared-memory capacity spill to the
@@ -146,16 +146,17 @@ def test_bucket_pass_graph_replay(ctx):
             assert ndjson_lines(tr, ctx.fetch()) == ndjson_lines(tr, O.run_trace(tr))
 
 
-def test_bucket_pass_default_threshold_on_c5_geometry(monkeypatch):
-    """Without the hook the bucketed pass takes over at 2^24 accesses: a
+def test_bucket_pass_threshold_on_c5_geometry(monkeypatch):
+    """GW_BUCKET=2 takes the bucketed pass from 2^24 accesses on: a
     21M-event C5-recipe trace (1024 x 8 x 32 threads, 2 phases x 40 records)
-    against the LSD path (GW_BUCKET=0) and the oracle."""
+    against the LSD path (the default) and the oracle."""
     p = dict(blocks=1024, warps=8, lanes=32, phases=2, records=40, words_per_block=262144, seed=5)
     tr = WL.c2_soa(**p)
-    monkeypatch.delenv("GW_BUCKET", raising=False)
+    monkeypatch.setenv("GW_BUCKET", "2")
     c = N.Context(0)
     a = _run(c, tr)
-    monkeypatch.setenv("GW_BUCKET", "0")
+    assert c.stats().sort_bits == 14  # bucket bits of 21M accesses: the bucketed pass ran
+    monkeypatch.delenv("GW_BUCKET")
     b = _run(c, tr)
     c.close()
     for f in ("kind", "prior", "current"):
