@@ -112,8 +112,24 @@ def load_full_digest(workload: str):
     r = d.get(workload)
     if not r or "oracle_digest" not in r:
         return None
-    return {"digest": r["oracle_digest"], "source": f"tests/golden/full_digests.json[{workload}] (oracle port, "
-                                                     f"{r.get('n_reports')} reports)"}
+    whole = r.get("P", r["n_events"]) >= r["n_events"]
+    return {"digest": r["oracle_digest"], "P": r.get("P", r["n_events"]),
+            "source": f"tests/golden/full_digests.json[{workload}] (oracle port, {r.get('n_reports')} reports"
+                      + ("" if whole else f" with current.event < {r.get('P')}: the oracle's prefix") + ")"}
+
+
+def digest_for(res, fx, n):
+    """The digest to compare with a full_digests.json entry: of the whole
+    result, or of the reports / diagnostics before the entry's prefix P."""
+    from paper_2111_12478_b200.report import result_digest
+
+    if fx is None or fx["P"] >= n:
+        return result_digest(res)
+    P = fx["P"]
+    keep, dk = res["current"] < P, res["diag_event"] < P
+    return result_digest({"kind": res["kind"][keep], "prior": res["prior"][keep], "current": res["current"][keep],
+                          "diag_event": res["diag_event"][dk], "diag_code": res["diag_code"][dk],
+                          "diag_lock": res["diag_lock"][dk]})
 
 
 def load_ncu_traffic():
@@ -286,6 +302,36 @@ def cpu_time(get_prefix, n, budget_s):
         runs += 1
     what = "the full trace" if len(tr) >= n else f"the first {len(tr)} of {n} events (record-aligned prefix)"
     return len(tr) * runs / tot, f"{what}, {runs} run(s), oracle/gwcp_oracle.cpp on 1 host core"
+
+
+def python_reference_time(get_prefix, workload):
+    """The Python reference itself (gpurace, installed into baseline/_ref from
+    /root/reference) on this host: engine.run(trace[:P], GwcpDetector(cfg))
+    with the `check` defaults on one core, parse excluded (SURVEY §8(d) "CPU
+    timing"); P bounded to a few seconds of its ~10^3-10^5 events/s."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "gpurace")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        from gpurace.engine import run as ref_run
+        from gpurace.gwcp import GwcpDetector as RefDetector
+        from gpurace.trace import parse_trace as ref_parse
+
+        from paper_2111_12478_b200 import workloads as WL
+
+        P = {"c2": 200_000, "c3": 8_000, "c4": 40_000, "c5": 200_000}.get(workload, 100_000)
+        tr = ref_parse(WL.soa_to_text(get_prefix(P)))
+        t0 = time.perf_counter()
+        ref_run(tr, RefDetector(tr.config))
+        dt = time.perf_counter() - t0
+        return {"value": len(tr.events) / dt, "unit": UNIT, "cores": 1, "kind": "reference (Python, gpurace 0.1.0)",
+                "sample": f"the first {len(tr.events)} events (record-aligned prefix), 1 run, parse excluded",
+                "host_cpus": os.cpu_count()}
+    except Exception as e:  # pragma: no cover - informational only
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    finally:
+        sys.path.remove(ref)
 
 
 def run_reference(args):
@@ -492,13 +538,13 @@ def run_b200(args):
     if rank == 0:
         from paper_2111_12478_b200.report import result_digest
 
-        digest = result_digest(res)
+        fx = load_full_digest(args.workload)
+        digest = digest_for(res, fx, n)
         for what, r in (("packed host-buffer", res_e2e), ("16-B host-buffer", res_e2e16)):
-            d_e2e = result_digest(r)
+            d_e2e = digest_for(r, fx, n)
             if d_e2e != digest:
                 raise SystemExit(f"bench: {what} run's reports differ from the device-resident run's "
                                  f"({d_e2e} vs {digest})")
-        fx = load_full_digest(args.workload)
         if fx is not None and args.steps > 0:
             want_digest, digest_src = fx["digest"], fx["source"]
             if digest != want_digest:
@@ -599,6 +645,9 @@ def run_b200(args):
     if not args.no_cpu_baseline:
         v, what = cpu_time(lambda P: host_prefix(cfg, (key_d, to_d, in_d), P), n, args.ref_seconds)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": what}
+        pyref = python_reference_time(lambda P: host_prefix(cfg, (key_d, to_d, in_d), P), args.workload)
+        if pyref is not None:
+            line["python_reference"] = pyref
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
@@ -686,8 +735,8 @@ def run_b200_exchange(args):
         ms_e2e, res_e2e = timed(step_host, args.steps)
     if rank == 0:
         r, xt = res
-        digest = result_digest(r)
         fx = load_full_digest(args.workload)
+        digest = digest_for(r, fx, n)
         if fx is not None and digest != fx["digest"]:
             raise SystemExit(f"bench: exchange-mode report digest {digest} != {fx['digest']} ({fx['source']})")
         peak, peak_kind = load_peaks()

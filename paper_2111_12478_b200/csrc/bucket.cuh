@@ -67,7 +67,9 @@ static_assert((1 << kBkIdxBits) == kBkCap, "index bits");
 constexpr int kBkMinBits = 12, kBkMaxBits = 16;  // bucket bits: 32 - kb with kb + kBkIdxBits <= 32
 // buckets above kBkCap (up to kBkSubMax records) are split in the CTA into
 // <= 2^kBkSubBits sub-buckets in a per-CTA scratch that stays in L2
-constexpr int kBkSubBits = 4, kBkSubMax = 32768, kBkSubBuf = kBkSubMax + 8;
+// (sub-buckets of ~kBkSubAvg records: C5's buckets hold ~240-record own-word
+// runs, so sub-buckets of ~2K overflowed kBkCap in ~0.4 % of the cases)
+constexpr int kBkSubBits = 6, kBkSubAvg = 1536, kBkSubMax = 32768, kBkSubBuf = kBkSubMax + 8;
 
 // super-tiles of the scatter passes: 2^(RB-7) tiles share one count row, so
 // the count array stays at 128 words per tile for any digit width
@@ -515,7 +517,7 @@ struct BkSmem {
   uint32_t wc[kRsWarps][1 << kBkSortBits];
   uint32_t toff[1 << kBkSortBits];
   uint32_t tab[kBkSlots];  // the group's locations: open addressing on the in-bucket key
-  uint32_t sub[48];        // sub-bucket counts / starts / write cursors
+  uint32_t sub[3 << kBkSubBits];  // sub-bucket counts / starts / write cursors
   uint32_t hhi;
   unsigned long long mbar;
   uint32_t large;
@@ -778,6 +780,7 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
   }
   __syncthreads();
   uint32_t phase = 0;
+  constexpr int kNS = 1 << kBkSubBits;
   uint32_t* sh = a.scratch + (size_t)blockIdx.x * 3 * kBkSubBuf;
   uint32_t* sv = sh + kBkSubBuf;
   uint32_t* st = sv + kBkSubBuf;
@@ -789,14 +792,16 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
       continue;
     }
     // a bucket above the shared-memory capacity: split it by the top sb bits
-    // of its in-bucket key into <= 16 sub-buckets in this CTA's scratch
-    // (L2-resident), stably, then check every sub-bucket
-    const int sb = min(kBkSubBits, 32 - __clz((M + kBkCap / 2 - 1) / (kBkCap / 2) - 1));
-    const int shift = a.kb - sb;
-    const uint32_t nsub = 1u << sb;
+    // of its in-bucket key into sub-buckets of ~kBkSubAvg records in this
+    // CTA's scratch (L2-resident), stably, then check every sub-bucket; a
+    // sub-bucket above kBkCap retries with one more bit (hashes of few
+    // locations with hundreds of accesses each are lumpy)
+    int sb = min(kBkSubBits, 32 - __clz((M + kBkSubAvg - 1) / kBkSubAvg - 1));
     bool spill = M > (uint32_t)kBkSubMax;
-    if (!spill) {
-      for (int d = threadIdx.x; d < kRsWarps * 16; d += kThreads) S.wc[d >> 4][d & 15] = 0;
+    while (!spill) {
+      const int shift = a.kb - sb;
+      const uint32_t nsub = 1u << sb;
+      for (int d = threadIdx.x; d < kRsWarps * kNS; d += kThreads) S.wc[d / kNS][d % kNS] = 0;
       __syncthreads();
       for (uint32_t j0 = threadIdx.x; j0 < M; j0 += kThreads * 8) {  // 8 loads in flight per thread
         uint32_t hv[8];
@@ -807,7 +812,7 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
           if (j0 + u * kThreads < M) atomicAdd(&S.wc[w][(hv[u] >> shift) & (nsub - 1)], 1u);
       }
       __syncthreads();
-      if (threadIdx.x < 16) {
+      if (threadIdx.x < kNS) {
         uint32_t c = 0;
         for (int x = 0; x < kRsWarps; x++) c += S.wc[x][threadIdx.x];
         S.sub[threadIdx.x] = c;
@@ -815,18 +820,24 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
       __syncthreads();
       if (threadIdx.x == 0) {
         uint32_t run = 0, mx = 0;
-        for (uint32_t d = 0; d < 16; d++) {
+        for (uint32_t d = 0; d < kNS; d++) {
           const uint32_t c = S.sub[d];
           mx = max(mx, c);
-          S.sub[16 + d] = run;  // sub-bucket start
-          S.sub[32 + d] = run;  // write cursor
+          S.sub[kNS + d] = run;  // sub-bucket start
+          S.sub[2 * kNS + d] = run;  // write cursor
           run += c;
         }
-        S.large = mx > (uint32_t)kBkCap;  // a sub-bucket still too large: spill the whole bucket
+        S.large = mx > (uint32_t)kBkCap;
       }
       __syncthreads();
-      spill = S.large != 0;
+      const bool over = S.large != 0;
+      __syncthreads();
+      if (!over) break;
+      if (sb == kBkSubBits || sb == a.kb) spill = true;  // one hot location: the general path
+      else sb++;
     }
+    const int shift = a.kb - sb;
+    const uint32_t nsub = 1u << sb;
     if (spill) {  // hot locations: the general path (bucket_spill)
       if (threadIdx.x == 0) {
         if (a.xmode) atomicOr(a.c.err, ERR_XMODE);
@@ -840,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
     // stable scatter into the scratch, kSubChunk records per round
     constexpr int R = 8, kSubChunk = kRsWarps * 32 * R;
     for (uint32_t cb = 0; cb < M; cb += kSubChunk) {
-      for (int d = threadIdx.x; d < kRsWarps * 16; d += kThreads) S.wc[d >> 4][d & 15] = 0;
+      for (int d = threadIdx.x; d < kRsWarps * kNS; d += kThreads) S.wc[d / kNS][d % kNS] = 0;
       __syncthreads();
       uint32_t hh[R], vv[R], tt[R], rd[R];
 #pragma unroll
@@ -850,34 +861,34 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
         hh[r] = ok ? a.h[s + j] : 0u;
         vv[r] = ok ? a.v[s + j] : 0u;
         tt[r] = ok ? a.t[s + j] : 0u;
-        rd[r] = ok ? ((hh[r] >> shift) & (nsub - 1)) << 16 : 16u << 16;
+        rd[r] = ok ? ((hh[r] >> shift) & (nsub - 1)) << 16 : (uint32_t)kNS << 16;
       }
 #pragma unroll
       for (int r = 0; r < R; r++) {
         const uint32_t d = rd[r] >> 16;
-        const uint32_t peers = warp_peers<5>(d);
-        const uint32_t before = d < 16u ? S.wc[w][d] : 0u;
+        const uint32_t peers = warp_peers<kBkSubBits + 1>(d);
+        const uint32_t before = d < (uint32_t)kNS ? S.wc[w][d] : 0u;
         __syncwarp();
-        if (d < 16u && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
+        if (d < (uint32_t)kNS && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
         rd[r] |= before + __popc(peers & lt);
         __syncwarp();
       }
       __syncthreads();
-      if (threadIdx.x < 16) {  // per-warp offsets within the digit, advance the cursor
+      if (threadIdx.x < kNS) {  // per-warp offsets within the digit, advance the cursor
         const int d = threadIdx.x;
-        uint32_t run = S.sub[32 + d];
+        uint32_t run = S.sub[2 * kNS + d];
         for (int x = 0; x < kRsWarps; x++) {
           const uint32_t t = S.wc[x][d];
           S.wc[x][d] = run;
           run += t;
         }
-        S.sub[32 + d] = run;
+        S.sub[2 * kNS + d] = run;
       }
       __syncthreads();
 #pragma unroll
       for (int r = 0; r < R; r++) {
         const uint32_t d = rd[r] >> 16;
-        if (d < 16u) {
+        if (d < (uint32_t)kNS) {
           const uint32_t pos = S.wc[w][d] + (rd[r] & 0xFFFFu);
           st_keep(sh + pos, hh[r], keep);  // L2 evict-last: read back by TMA right below
           st_keep(sv + pos, vv[r], keep);
@@ -890,7 +901,7 @@ __global__ void __launch_bounds__(kThreads, GW_BK_MINB) k_bk_check(BkCheckArgs a
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
     for (uint32_t d = 0; d < nsub; d++) {
-      const uint32_t m = S.sub[d], o = S.sub[16 + d];
+      const uint32_t m = S.sub[d], o = S.sub[kNS + d];
       if (m) bk_group(S, a, sh, sv, st, o, m, s + o, sb, phase);
     }
   }

@@ -1275,6 +1275,12 @@ struct Pipeline {
       if (xs_recv.h) {  // exchange mode: no trace here for the spill / large-window / record passes
         uint32_t err = 0;
         d2h(&err, scal + SC_ERR);
+        if (getenv("GW_XS_DEBUG")) {
+          uint32_t nl = 0;
+          d2h(&nl, cnt + 1);
+          fprintf(stderr, "[gw xs] records %llu buckets %u kb %d spill %u large %u err 0x%x pend %u\n",
+                  (unsigned long long)NA, NB, bk_kb, nsp, nl, err, npend);
+        }
         if (err & ERR_XMODE)
           throw CudaErr{GW_E_UNSUPPORTED, "exchange mode: hot locations or large reader windows (use the "
                                           "replicated shard mode)"};
@@ -1455,6 +1461,7 @@ struct Pipeline {
   BkRecSrc xs_recv{};  // exchange mode: the received records (nullptr h: off)
   int xs_gbits = 0;
   void xs_begin() {
+    g_launches = 0;
     zero_blk = C->get<uint32_t>("zero_blk", kZeroWords);
     zero_next = 0;
     scal = C->get<uint32_t>("scalars", SC_COUNT);
@@ -2462,6 +2469,7 @@ extern "C" int gw_xs_check(gw_ctx* c, const gw_xs_stats* global, uint32_t shard_
                          (const unsigned long long*)hkey, n_hard, n_total);
     c->xs_nc = p.xs_nc;
     c->xs_nsi = p.xs_nsi;
+    c->launches = g_launches;
   });
 }
 
