@@ -231,17 +231,13 @@ def analyze_exchange(ctx, cfg, n_total: int, slice_bufs, base: int, *, collectiv
     allc = _gather_rows(rows, world, rank, coll, group)
     # 5. endpoint info of the referenced events, from their owning slices
     if rank == 0:
-        a = allc.cpu().numpy()
-        cand = {"order_key": a[:, 0].view(np.uint64), "loc": a[:, 1].view(np.uint64),
-                "prior": a[:, 2].astype(np.uint32), "current": a[:, 3].astype(np.uint32),
-                "kind": a[:, 4].astype(np.uint32)}
-        ev = np.unique(np.concatenate([cand["prior"], cand["current"]]))
-        m = torch.tensor([len(ev)], dtype=torch.int64, device=coll)
+        a = allc.to(dev)  # the merge runs on rank 0's GPU
+        ev_d = torch.unique(torch.cat([a[:, 2], a[:, 3]]))  # sorted event ids
+        m = torch.tensor([int(ev_d.numel())], dtype=torch.int64, device=coll)
     else:
         m = torch.zeros(1, dtype=torch.int64, device=coll)
     dist.broadcast(m, 0, group=group)
-    evt = torch.from_numpy(ev.astype(np.int64)).to(coll) if rank == 0 else \
-        torch.empty(int(m.item()), dtype=torch.int64, device=coll)
+    evt = ev_d.to(coll) if rank == 0 else torch.empty(int(m.item()), dtype=torch.int64, device=coll)
     dist.broadcast(evt, 0, group=group)
     evn = evt.cpu().numpy().astype(np.uint32)
     to, ins = ctx.xs_lookup(evn)
@@ -249,18 +245,46 @@ def analyze_exchange(ctx, cfg, n_total: int, slice_bufs, base: int, *, collectiv
     dist.reduce(info, 0, group=group)  # exactly one slice owns each event
     if rank != 0:
         return None
-    info = info.cpu().numpy()
-    tid_of = _Sparse(evn, info[:, 0].astype(np.uint32))
-    ins_of = _Sparse(evn, info[:, 1].astype(np.uint32))
-    res = merge_candidates(cand, lambda e: ins_of[e])
-    keys = np.zeros(len(evn), np.uint64)
-    pos = np.searchsorted(evn, res["current"])
-    keys[pos] = res["loc"]
-    xt = ExchangeTrace(TraceConfig(*cfg), evn, tid_of.vals, ins_of.vals, keys)
+    # 6. keep-first dedup on (location, prior.instr, current.instr), report order
+    info = info.to(dev)
+    res = merge_candidates_device(a, ev_d, info[:, 1])
+    evs = ev_d.cpu().numpy().astype(np.uint32)
+    inf = info.cpu().numpy()
+    keys = np.zeros(len(evs), np.uint64)
+    keys[np.searchsorted(evs, res["current"])] = res["loc"]
+    xt = ExchangeTrace(TraceConfig(*cfg), evs, inf[:, 0].astype(np.uint32), inf[:, 1].astype(np.uint32), keys)
     for f in ("diag_event", "diag_code"):
         res[f] = np.zeros(0, np.uint32)
     res["diag_lock"] = np.zeros(0, np.uint64)
     return res, xt
+
+
+def merge_candidates_device(a, ev, instr):
+    """merge_candidates on the GPU (torch): a = (m, 5) int64 rows (order key,
+    location, prior, current, kind), ev = sorted event ids, instr = their
+    instruction ids.  Composite order by stable sorts (last key first)."""
+    import torch
+
+    if a.shape[0] == 0:
+        z = np.zeros(0, np.uint32)
+        return {"kind": np.zeros(0, np.uint8), "prior": z, "current": z.copy(), "order_key": np.zeros(0, np.uint64),
+                "loc": np.zeros(0, np.uint64)}
+    okey, loc, pri, cur, kind = a.unbind(1)
+    ip = instr[torch.searchsorted(ev, pri)]
+    ic = instr[torch.searchsorted(ev, cur)]
+    order = torch.argsort(okey, stable=True)
+    for k in (ic, ip, loc):
+        order = order[torch.argsort(k[order], stable=True)]
+    L, P, Cc = loc[order], ip[order], ic[order]
+    first = torch.ones_like(L, dtype=torch.bool)
+    first[1:] = (L[1:] != L[:-1]) | (P[1:] != P[:-1]) | (Cc[1:] != Cc[:-1])
+    keep = order[first]
+    keep = keep[torch.argsort(okey[keep], stable=True)]
+    out = {k: v[keep].cpu().numpy() for k, v in (("order_key", okey), ("loc", loc), ("prior", pri),
+                                                  ("current", cur), ("kind", kind))}
+    return {"kind": out["kind"].astype(np.uint8), "prior": out["prior"].astype(np.uint32),
+            "current": out["current"].astype(np.uint32), "order_key": out["order_key"].view(np.uint64),
+            "loc": out["loc"].view(np.uint64)}
 
 
 def record_cut(tidop, k: int, parts: int) -> int:

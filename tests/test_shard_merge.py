@@ -104,3 +104,25 @@ def test_merge_candidates_is_keep_first_dedup():
         assert got["order_key"].tolist() == [okeys[i] for i in want]
         assert got["prior"].tolist() == [int(c["prior"][i]) for i in want]
         assert got["kind"].tolist() == [int(c["kind"][i]) for i in want]
+
+
+def test_merge_candidates_device_equals_host():
+    """The GPU-side merge of the exchange mode (torch on rank 0) == the numpy
+    restatement (run here on CPU tensors)."""
+    import torch
+
+    from paper_2111_12478_b200.shard import merge_candidates, merge_candidates_device
+
+    rng = np.random.default_rng(3)
+    for m in (0, 1, 50, 3000):
+        ok = rng.permutation(m).astype(np.int64) * 5 + 3
+        a = np.stack([ok, rng.integers(0, 6, m) * 4, rng.integers(0, 500, m), rng.integers(0, 500, m),
+                      rng.integers(0, 3, m)], axis=1).astype(np.int64) if m else np.zeros((0, 5), np.int64)
+        ev = np.unique(np.concatenate([a[:, 2], a[:, 3]])) if m else np.zeros(0, np.int64)
+        ins = rng.integers(0, 4, len(ev)).astype(np.int64)
+        got = merge_candidates_device(torch.from_numpy(a), torch.from_numpy(ev), torch.from_numpy(ins))
+        c = {"order_key": a[:, 0].astype(np.uint64), "loc": a[:, 1].astype(np.uint64),
+             "prior": a[:, 2].astype(np.uint32), "current": a[:, 3].astype(np.uint32), "kind": a[:, 4].astype(np.uint32)}
+        want = merge_candidates(c, lambda e: ins[np.searchsorted(ev, e)])
+        for f in ("order_key", "prior", "current", "kind"):
+            assert got[f].tolist() == want[f].tolist(), (m, f)
