@@ -234,6 +234,30 @@ typedef struct gw_trace_packed {
   const void* instr;      /* uint16_t[n] (instr_bytes 2) or uint32_t[n] */
 } gw_trace_packed;
 int gw_ctx_analyze_host_packed(gw_ctx* c, const gw_trace_packed* host_trace, const gw_opts* opts);
+/* Delta-varint trace (GWSOA v3): per column (0 key u64, 1 tidop u32,
+ * 2 instr u32) the differences of consecutive events, zigzag-coded LEB128
+ * varints; chunks of GW_DELTA_CHUNK events start at offs[c][k] and decode
+ * on their own from base[c][k] = the column's value before the chunk.
+ * Consecutive lanes of a record differ by small constants, so the C2 / C5
+ * traces take ~3.3 B/event.  gw_encode_delta builds it on the host (chunk-
+ * parallel; library-owned arrays, gw_delta_free); gw_ctx_analyze_host_delta
+ * uploads the three byte streams in slices on a copy stream while the
+ * device decodes the slices already landed (k_delta_decode), then analyses
+ * as gw_ctx_analyze_host. */
+#define GW_DELTA_CHUNK 4096u
+typedef struct gw_trace_delta {
+  gw_config cfg;
+  uint64_t n_events;
+  uint32_t chunk, _pad;
+  uint64_t n_chunks;
+  const uint8_t* bytes[3];
+  uint64_t nbytes[3];
+  const uint64_t* offs[3]; /* n_chunks + 1 */
+  const uint64_t* base[3]; /* n_chunks */
+} gw_trace_delta;
+int gw_encode_delta(const gw_trace_view* host_trace, gw_trace_delta* out);
+void gw_delta_free(gw_trace_delta* d);
+int gw_ctx_analyze_host_delta(gw_ctx* c, const gw_trace_delta* host_trace, const gw_opts* opts);
 /* D2H of the last analysis' results (synchronises the stream) */
 int gw_ctx_fetch(gw_ctx* c, gw_result* out);
 int gw_ctx_stats(gw_ctx* c, gw_stats* out);

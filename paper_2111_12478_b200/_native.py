@@ -77,6 +77,15 @@ class _Packed(C.Structure):
     ]
 
 
+DELTA_CHUNK = 4096
+
+
+class _Delta(C.Structure):
+    _fields_ = [("cfg", _Config), ("n_events", C.c_uint64), ("chunk", C.c_uint32), ("_pad", C.c_uint32),
+                ("n_chunks", C.c_uint64), ("bytes", C.c_void_p * 3), ("nbytes", C.c_uint64 * 3),
+                ("offs", C.c_void_p * 3), ("base", C.c_void_p * 3)]
+
+
 class XsStats(C.Structure):
     _fields_ = [(f, C.c_uint64) for f in ("n_acc", "n_write", "n_acq", "n_rel", "n_end", "n_bar", "key_or",
                                           "key_and", "n_long", "n_wbar")]
@@ -134,6 +143,9 @@ EXPORTS = (
     "gw_ctx_analyze_host_packed",
     "gw_ctx_validate",
     "gw_ctx_infer_locks",
+    "gw_encode_delta",
+    "gw_delta_free",
+    "gw_ctx_analyze_host_delta",
     "gw_xs_prep",
     "gw_xs_hard",
     "gw_xs_partition",
@@ -214,6 +226,11 @@ def lib():
         L.gw_xs_lookup.argtypes = [VP, VP, C.c_uint64, VP, VP]
         for f in ("gw_xs_prep", "gw_xs_hard", "gw_xs_partition", "gw_xs_check", "gw_xs_fetch", "gw_xs_lookup"):
             getattr(L, f).restype = C.c_int
+        L.gw_encode_delta.argtypes = [C.POINTER(_View), C.POINTER(_Delta)]
+        L.gw_encode_delta.restype = C.c_int
+        L.gw_delta_free.argtypes = [C.POINTER(_Delta)]
+        L.gw_ctx_analyze_host_delta.argtypes = [C.c_void_p, C.POINTER(_Delta), C.POINTER(_Opts)]
+        L.gw_ctx_analyze_host_delta.restype = C.c_int
         L.gw_ctx_fetch.argtypes = [C.c_void_p, C.POINTER(_Result)]
         L.gw_ctx_fetch.restype = C.c_int
         L.gw_ctx_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
@@ -432,6 +449,25 @@ class Context:
         o = _Opts(1 if inactive_opt else 0, flags, stream, shard[0], shard[1])
         _check(self._L.gw_ctx_analyze_host_packed(self._c, C.byref(p), C.byref(o)))
 
+    def analyze_host_delta(self, enc: dict, *, inactive_opt=True, stream=None, eager=False, hb=False) -> None:
+        """Delta-varint host trace (encode_delta; the byte streams may be any
+        host arrays, pinned for full PCIe speed): chunked upload overlapped
+        with on-device decoding (gw_ctx_analyze_host_delta)."""
+        d = _Delta()
+        d.cfg.blocks, d.cfg.warps, d.cfg.lanes = enc["cfg"]
+        d.n_events = enc["n"]
+        d.chunk = DELTA_CHUNK
+        d.n_chunks = (enc["n"] + DELTA_CHUNK - 1) // DELTA_CHUNK
+        for c in range(3):
+            b, o, s_ = enc["bytes"][c], enc["offs"][c], enc["base"][c]
+            d.bytes[c] = b.ctypes.data if len(b) else None
+            d.nbytes[c] = len(b)
+            d.offs[c] = o.ctypes.data
+            d.base[c] = s_.ctypes.data if len(s_) else None
+        flags = (OPT_EAGER if eager else 0) | (OPT_HB if hb else 0)
+        o_ = _Opts(1 if inactive_opt else 0, flags, stream, 0, 1)
+        _check(self._L.gw_ctx_analyze_host_delta(self._c, C.byref(d), C.byref(o_)))
+
     def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None,
                        eager=False, shard=(0, 1), profile=False, hb=False) -> None:
         """shard=(index, count): report only races on location-key range `index`
@@ -506,6 +542,33 @@ class Context:
         n = C.c_uint32(0)
         _check(self._L.gw_ctx_kernel_times(self._c, cap, names, ms, cnt, C.byref(n)))
         return {names[i].value.decode(): (float(ms[i]), int(cnt[i])) for i in range(n.value)}
+
+
+def encode_delta(cfg, key, tidop, instr) -> dict:
+    """The delta-varint form of a host SoA (gw_encode_delta, GWSOA v3):
+    {"cfg", "n", "bytes": [key, tidop, instr byte streams], "offs": [...],
+    "base": [...]} as numpy arrays (copied out of the library's buffers)."""
+    L = lib()
+    key = np.ascontiguousarray(key, np.uint64)
+    tidop = np.ascontiguousarray(tidop, np.uint32)
+    instr = np.ascontiguousarray(instr, np.uint32)
+    v = _view(cfg, key, tidop, instr)
+    d = _Delta()
+    _check(L.gw_encode_delta(C.byref(v), C.byref(d)))
+    try:
+        k = int(d.n_chunks)
+
+        def take(p, count, dt):
+            if count == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(np.ctypeslib.as_ctypes_type(dt))), shape=(count,)).copy()
+
+        return {"cfg": tuple(cfg), "n": len(tidop),
+                "bytes": [take(d.bytes[c], int(d.nbytes[c]), np.uint8) for c in range(3)],
+                "offs": [take(d.offs[c], k + 1, np.uint64) for c in range(3)],
+                "base": [take(d.base[c], k, np.uint64) for c in range(3)]}
+    finally:
+        L.gw_delta_free(C.byref(d))
 
 
 def pack_columns(key, instr, tidop=None):

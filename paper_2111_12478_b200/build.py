@@ -6,8 +6,9 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", "engine.cu"), os.path.join(HERE, "csrc", "parse.cpp")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("primitives.cuh", "walker.cuh", "walker_warp.cuh", "bucket.cuh", "workloads.cuh",
+SRC = [os.path.join(HERE, "csrc", "engine.cu"), os.path.join(HERE, "csrc", "parse.cpp"),
+       os.path.join(HERE, "csrc", "codec.cpp")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("primitives.cuh", "walker.cuh", "walker_warp.cuh", "bucket.cuh", "workloads.cuh", "validate.cuh",
                                                          "access.cuh", "common.h")]
 OUT = os.path.join(HERE, "libgwcp_b200.so")
 NVCC_FLAGS = [

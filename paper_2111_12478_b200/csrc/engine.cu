@@ -2277,6 +2277,151 @@ extern "C" int gw_ctx_analyze_host_packed(gw_ctx* c, const gw_trace_packed* t, c
   });
 }
 
+// ---- delta-varint host trace (gw_trace_delta, codec.cpp) ----------------------
+// One CTA per chunk of GW_DELTA_CHUNK events: the chunk's bytes in shared
+// memory; every thread takes a contiguous byte range, counts varint
+// terminators (high bit clear), a block scan numbers them, and each thread
+// decodes the varints ending in its range (reading back to the previous
+// terminator); then a blocked inclusive scan of the deltas from the chunk's
+// base gives the column values.
+template <class T>
+struct DeltaSmem {
+  static constexpr uint32_t kMaxB = GW_DELTA_CHUNK * (sizeof(T) == 8 ? 10u : 5u);
+  uint8_t b[kMaxB];
+  T d[GW_DELTA_CHUNK];
+};
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_delta_decode(const uint8_t* __restrict__ bytes,
+                                                          const uint64_t* __restrict__ offs,
+                                                          const uint64_t* __restrict__ base, uint64_t k0, uint64_t k1,
+                                                          uint64_t n, T* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  DeltaSmem<T>& S = *reinterpret_cast<DeltaSmem<T>*>(smem_raw);
+  constexpr uint32_t CH = GW_DELTA_CHUNK, IPT = CH / kThreads;
+  for (uint64_t k = k0 + blockIdx.x; k < k1; k += gridDim.x) {
+    const uint64_t lo = offs[k];
+    const uint64_t nb64 = offs[k + 1] - lo, ne64 = n - k * CH;
+    const uint32_t nb = (uint32_t)(nb64 < DeltaSmem<T>::kMaxB ? nb64 : DeltaSmem<T>::kMaxB);
+    const uint32_t ne = (uint32_t)(ne64 < CH ? ne64 : CH);
+    for (uint32_t j = threadIdx.x; j < nb; j += kThreads) S.b[j] = bytes[lo + j];
+    __syncthreads();
+    const uint32_t q = (nb + kThreads - 1) / kThreads;
+    const uint32_t b0 = min(nb, threadIdx.x * q), b1 = min(nb, b0 + q);
+    uint32_t cnt = 0;
+    for (uint32_t j = b0; j < b1; j++) cnt += (S.b[j] & 0x80u) == 0;
+    uint32_t tot;
+    uint32_t idx = block_excl_scan<uint32_t, OpSum>(cnt, OpSum(), 0u, &tot);
+    for (uint32_t j = b0; j < b1; j++) {
+      if (S.b[j] & 0x80u) continue;
+      uint32_t st0 = j;
+      while (st0 > 0 && (S.b[st0 - 1] & 0x80u)) st0--;
+      unsigned long long z = 0;
+      for (uint32_t x = j + 1; x-- > st0;) z = (z << 7) | (S.b[x] & 0x7Fu);
+      const T zz = (T)z;
+      if (idx < CH) S.d[idx] = (zz >> 1) ^ (T)(0 - (zz & 1));
+      idx++;
+    }
+    __syncthreads();
+    const uint32_t p0 = threadIdx.x * IPT;
+    T sum = 0;
+#pragma unroll
+    for (uint32_t x = 0; x < IPT; x++) sum += p0 + x < ne ? S.d[p0 + x] : (T)0;
+    T all;
+    T run = block_excl_scan<T, OpSum>(sum, OpSum(), (T)0, &all) + (T)base[k];
+#pragma unroll
+    for (uint32_t x = 0; x < IPT; x++)
+      if (p0 + x < ne) {
+        run += S.d[p0 + x];
+        out[k * CH + p0 + x] = run;
+      }
+    __syncthreads();
+  }
+}
+template <class T>
+inline void delta_setup() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_delta_decode<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DeltaSmem<T>));
+    done = true;
+  }
+}
+
+extern "C" int gw_ctx_analyze_host_delta(gw_ctx* c, const gw_trace_delta* t, const gw_opts* o) {
+  if (!c || !t) { gw_set_error("null argument"); return GW_E_ARG; }
+  if (t->chunk != GW_DELTA_CHUNK || t->n_chunks != (t->n_events + GW_DELTA_CHUNK - 1) / GW_DELTA_CHUNK) {
+    gw_set_error("delta trace: chunking does not match GW_DELTA_CHUNK");
+    return GW_E_ARG;
+  }
+  gw_trace_view view;
+  view.cfg = t->cfg;
+  view.n_events = t->n_events;
+  view.key = (const uint64_t*)t->bytes[0];
+  view.tidop = (const uint32_t*)t->bytes[1];
+  view.instr = (const uint32_t*)t->bytes[2];
+  int v = validate_view(&view);
+  if (v) return v;
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
+    const uint32_t inactive = o ? o->inactive_opt : 1u;
+    const uint32_t nsh = o && o->shard_count > 1 ? o->shard_count : 1u;
+    const uint32_t sh = nsh > 1 ? o->shard_index : 0u;
+    if (sh >= nsh) throw CudaErr{GW_E_ARG, "shard_index must be < shard_count"};
+    const uint64_t N = t->n_events, K = t->n_chunks;
+    c->last_stream = st;
+    unsigned long long* k = c->get<unsigned long long>("in_key", N);
+    uint32_t* to = c->get<uint32_t>("in_tidop", N);
+    uint32_t* in = c->get<uint32_t>("in_instr", N);
+    if (!c->copy_st) {
+      CK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_prev, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(c->ev_prev, st));  // earlier analyses on st may still read the input buffers
+    CK(cudaStreamWaitEvent(c->copy_st, c->ev_prev, 0));
+    uint8_t* db[3];
+    uint64_t* doff[3];
+    uint64_t* dbase[3];
+    const char* nm[3] = {"dl_key", "dl_tidop", "dl_instr"};
+    for (int col = 0; col < 3; col++) {
+      db[col] = c->get<uint8_t>(std::string(nm[col]) + "_b", t->nbytes[col] + 16);
+      doff[col] = c->get<uint64_t>(std::string(nm[col]) + "_o", K + 1);
+      dbase[col] = c->get<uint64_t>(std::string(nm[col]) + "_s", K + 1);
+      if (K) {
+        CK(cudaMemcpyAsync(doff[col], t->offs[col], 8 * (K + 1), cudaMemcpyHostToDevice, c->copy_st));
+        CK(cudaMemcpyAsync(dbase[col], t->base[col], 8 * K, cudaMemcpyHostToDevice, c->copy_st));
+      }
+    }
+    constexpr uint64_t kSlice = 1024;  // chunks per upload slice (4 M events)
+    const uint64_t ns = (K + kSlice - 1) / kSlice;
+    while (c->chunk_ev.size() < ns) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->chunk_ev.push_back(e);
+    }
+    delta_setup<unsigned long long>();
+    delta_setup<uint32_t>();
+    for (uint64_t sl = 0; sl < ns; sl++) {
+      const uint64_t k0 = sl * kSlice, k1 = std::min(K, k0 + kSlice);
+      for (int col = 0; col < 3; col++) {
+        const uint64_t a = t->offs[col][k0], b = t->offs[col][k1];
+        if (b > a) CK(cudaMemcpyAsync(db[col] + a, t->bytes[col] + a, b - a, cudaMemcpyHostToDevice, c->copy_st));
+      }
+      CK(cudaEventRecord(c->chunk_ev[sl], c->copy_st));
+      CK(cudaStreamWaitEvent(st, c->chunk_ev[sl], 0));  // decode slice sl while slice sl + 1 is in flight
+      const unsigned g = (unsigned)std::min<uint64_t>(k1 - k0, 148ull * 3);
+      GW_LAUNCH(k_delta_decode<unsigned long long>, g, kThreads, sizeof(DeltaSmem<unsigned long long>), st, db[0],
+                doff[0], dbase[0], k0, k1, N, k);
+      GW_LAUNCH(k_delta_decode<uint32_t>, g, kThreads, sizeof(DeltaSmem<uint32_t>), st, db[1], doff[1], dbase[1],
+                k0, k1, N, to);
+      GW_LAUNCH(k_delta_decode<uint32_t>, g, kThreads, sizeof(DeltaSmem<uint32_t>), st, db[2], doff[2], dbase[2],
+                k0, k1, N, in);
+    }
+    DevTrace tr = make_dev(&view, k, to, in);
+    analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,
+                 o && (o->flags & GW_OPT_PROFILE), o && (o->flags & GW_OPT_HB));
+  });
+}
+
 // host copy of a large result array on several threads (first touch of the
 // fresh destination pages included): millions of reports (C4) otherwise
 // spend tens of ms in one memcpy

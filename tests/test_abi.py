@@ -101,3 +101,45 @@ def test_pack_columns_widths():
     assert k.tolist() == [1, 2**32 - 1] and i.tolist() == [0, 2**16 - 1]
     k, i = N.pack_columns(np.array([2**32], np.uint64), np.array([2**16], np.uint32))
     assert k.dtype == np.uint64 and i.dtype == np.uint32
+
+
+def _delta_decode(b, offs, base, n, w):
+    """Restatement of the delta-varint layout (gw_trace_delta): per chunk, from
+    its base, zigzag LEB128 deltas."""
+    import numpy as np
+
+    out = np.zeros(n, np.uint64)
+    mask = (1 << w) - 1
+    for k in range(len(offs) - 1):
+        p, x = int(offs[k]), int(base[k]) if k < len(base) else 0
+        for i in range(k * N.DELTA_CHUNK, min(n, (k + 1) * N.DELTA_CHUNK)):
+            z = sh = 0
+            while True:
+                by = int(b[p])
+                p += 1
+                z |= (by & 0x7F) << sh
+                sh += 7
+                if not by & 0x80:
+                    break
+            x = (x + ((z >> 1) ^ (-(z & 1) & mask))) & mask
+            out[i] = x
+    return out
+
+
+def test_delta_encoding_roundtrip():
+    """gw_encode_delta (host, chunk-parallel) against the layout's restatement,
+    with extreme values (wrap-around deltas, 64-bit shared keys)."""
+    import numpy as np
+
+    rng = np.random.default_rng(1)
+    n = 3 * N.DELTA_CHUNK + 77
+    key = rng.integers(0, 2**63, n, dtype=np.uint64)
+    key[::5] = np.uint64(2**64 - 1)
+    key[1::7] = 0
+    tidop = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    instr = np.arange(n, dtype=np.uint32) * np.uint32(3)
+    enc = N.encode_delta((1, 1, 1), key, tidop, instr)
+    assert len(enc["offs"][0]) == 4 + 1 and int(enc["offs"][1][-1]) == len(enc["bytes"][1])
+    assert np.array_equal(_delta_decode(enc["bytes"][0], enc["offs"][0], enc["base"][0], n, 64), key)
+    assert np.array_equal(_delta_decode(enc["bytes"][1], enc["offs"][1], enc["base"][1], n, 32), tidop)
+    assert np.array_equal(_delta_decode(enc["bytes"][2], enc["offs"][2], enc["base"][2], n, 32), instr)

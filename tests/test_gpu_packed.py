@@ -80,3 +80,40 @@ def test_packed_input_many_chunks(ctx):
             assert np.array_equal(got[f], want[f])
     assert ndjson_lines(tr, want) == ndjson_lines(tr, O.run_trace(tr))
 
+
+
+def _run_delta(ctx, tr, inactive_opt=True, **kw):
+    enc = N.encode_delta(tr.cfg_tuple, tr.key, tr.tidop, tr.instr)
+    ctx.analyze_host_delta(enc, inactive_opt=inactive_opt, **kw)
+    return ctx.fetch()
+
+
+def test_delta_input_reference_goldens(goldens, ctx):
+    """The delta-varint host form (gw_ctx_analyze_host_delta): decoded on the
+    device, the same reports as the 16-B SoA."""
+    n = 0
+    for r in goldens:
+        if "error" in r or "full" in r["tags"] or not ({"corpus", "nasty", "random", "c1", "c3", "c4"} & set(r["tags"])):
+            continue
+        tr = parse_trace(golden_text(r))
+        check_against_golden(r, tr, _run_delta(ctx, tr, r["inactive_opt"]))
+        n += 1
+    assert n > 3000
+
+
+def test_delta_input_full_c2_and_many_slices(goldens, ctx):
+    import torch
+
+    r = next(r for r in goldens if r["name"] == "c2/full")
+    tr = WL.c2_soa()
+    check_against_golden(r, tr, _run_delta(ctx, tr))
+    # > 1024 chunks of 4096 events: several upload slices, decoded while later ones land;
+    # on a stream, so the later calls replay the captured graph
+    tr = WL.c2_soa(blocks=1024, warps=8, lanes=32, phases=2, records=80, words_per_block=262144, seed=5)
+    stream = torch.cuda.Stream(device=torch.device("cuda", 0))
+    ctx.analyze_host(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, stream=stream.cuda_stream)
+    want = ctx.fetch()
+    for _ in range(3):
+        got = _run_delta(ctx, tr, stream=stream.cuda_stream)
+        for f in ("kind", "prior", "current"):
+            assert np.array_equal(got[f], want[f])
