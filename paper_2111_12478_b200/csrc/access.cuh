@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads) k_shard_accesses(DevTrace tr, ShardA
         const uint32_t to = tr.tidop[e];
         keys[pos] = (K)ck;
         vals[pos] = (uint32_t)e | (ev_kind(to) == GW_K_WRITE ? VAL_W : 0u);
-        aux[e] = make_aux(src, (uint32_t)e, to);
+        if (aux) aux[e] = make_aux(src, (uint32_t)e, to);
       }
       run += tot;
       __syncthreads();
@@ -206,6 +206,19 @@ struct Stats {
   unsigned long long n_long;  // windows proving a record longer than 32 events
   unsigned long long n_wbar;  // warp barriers (of n_bar)
 };
+__device__ __forceinline__ void prep_flush(unsigned long long (&v)[6], unsigned long long ko, unsigned long long ka,
+                                           unsigned long long nlong, unsigned long long nwbar, Stats* st);
+// per-event stats of k_prep / k_ingest (counts by kind, OR / AND of access keys)
+__device__ __forceinline__ void prep_count(uint32_t to, unsigned long long x, unsigned long long (&v)[6],
+                                           unsigned long long& ko, unsigned long long& ka,
+                                           unsigned long long& nwbar) {
+  const uint32_t k = ev_kind(to);
+  if (k <= GW_K_WRITE) { v[0]++; v[1] += k; ko |= x; ka &= x; }
+  else if (k == GW_K_ACQUIRE) v[2]++;
+  else if (k == GW_K_RELEASE) v[3]++;
+  else if (k == GW_K_END) v[4]++;
+  else if (k == GW_K_BARRIER) { v[5]++; if (to & GW_F_WARPBAR) nwbar++; }
+}
 __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
   unsigned long long v[6] = {0, 0, 0, 0, 0, 0};  // acc, write, acq, rel, end, bar
   unsigned long long ko = 0, ka = ~0ull, nlong = 0, nwbar = 0;
@@ -226,14 +239,7 @@ __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
       x[u] = ev_kind(to[u]) <= GW_K_WRITE ? tr.key[e] : 0ull;
     }
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const uint32_t k = ev_kind(to[u]);
-      if (k <= GW_K_WRITE) { v[0]++; v[1] += k; ko |= x[u]; ka &= x[u]; }
-      else if (k == GW_K_ACQUIRE) v[2]++;
-      else if (k == GW_K_RELEASE) v[3]++;
-      else if (k == GW_K_END) v[4]++;
-      else if (k == GW_K_BARRIER) { v[5]++; if (to[u] & GW_F_WARPBAR) nwbar++; }
-    }
+    for (int u = 0; u < U; u++) prep_count(to[u], x[u], v, ko, ka, nwbar);
     // records longer than 32 events: 32 consecutive continues-record events ending in a window
     uint32_t prevm = 0;
     bool have_prev = false;
@@ -256,6 +262,12 @@ __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
       have_prev = true;
     }
   }
+  prep_flush(v, ko, ka, nlong, nwbar, st);
+}
+// the per-thread stats of k_prep / k_ingest into *st (warp, CTA, then global atomics)
+__device__ __forceinline__ void prep_flush(unsigned long long (&v)[6], unsigned long long ko, unsigned long long ka,
+                                           unsigned long long nlong, unsigned long long nwbar, Stats* st) {
+  const int lane = threadIdx.x & 31;
   if (lane == 0 && nlong) atomicAdd(&st->n_long, nlong);
   nwbar = __reduce_add_sync(0xffffffffu, (uint32_t)nwbar);
   if (lane == 0 && nwbar) atomicAdd(&st->n_wbar, nwbar);
@@ -289,6 +301,103 @@ __global__ void __launch_bounds__(kThreads) k_prep(DevTrace tr, Stats* st) {
     else if (i == 6) atomicOr(dst[i], r);
     else atomicAnd(dst[i], r);
   }
+}
+
+// Graph replays of big lock-free traces: ONE read of the trace does the work
+// of k_prep (the stats the plan check verifies), k_acc_keys (location keys /
+// events), the first sort pass's per-tile digit counts (k_rs_up, pass 0: the
+// ingest tiles are the sort's kTile tiles) and, in snapshot mode,
+// k_hard_append.  Warp w of tile t at step k reads the aligned 32-event window
+// t*kTile + k*kThreads + 32w, so the long-record test is k_prep's.
+struct IngestHard {
+  unsigned long long* hkey;  // nullptr: no hard-event list here
+  uint32_t* hcnt;
+  uint32_t* ntop;
+  uint32_t cap;
+};
+template <class K>
+__global__ void __launch_bounds__(kThreads) k_ingest(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals, Stats* stt,
+                                                    uint32_t* counts, uint64_t nst, IngestHard hd) {
+  __shared__ uint32_t h[kRsWarps][kRsDigits];
+  unsigned long long v[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long ko = 0, ka = ~0ull, nlong = 0, nwbar = 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const K sentinel = kr.sentinel ? ((K)1 << (kr.nbits - 1)) : (K)0;
+  for (uint64_t t = blockIdx.x; t < nst; t += gridDim.x) {
+    for (int d = threadIdx.x; d < kRsWarps * kRsDigits; d += kThreads) (&h[0][0])[d] = 0;
+    __syncthreads();
+    const uint64_t base = t * kTile;
+    constexpr int U = 4;  // loads of U windows issued together (key loads do not wait for the kinds)
+#pragma unroll 1
+    for (int k0 = 0; k0 < kItems; k0 += U) {
+    uint32_t tob[U];
+    unsigned long long xb[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint64_t e = base + (uint64_t)(k0 + u) * kThreads + 32u * w + lane;
+      tob[u] = e < tr.n ? tr.tidop[e] : (7u << GW_OP_SHIFT);
+      xb[u] = e < tr.n ? tr.key[e] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int k = k0 + u;
+      const uint64_t w0 = base + (uint64_t)k * kThreads + 32u * w;
+      const uint64_t e = w0 + lane;
+      const uint32_t to = tob[u];
+      const uint32_t kind = ev_kind(to);
+      const unsigned long long x = kind <= GW_K_WRITE ? xb[u] : 0ull;
+      prep_count(to, x, v, ko, ka, nwbar);
+      if (e < tr.n) {
+        K ck = sentinel;
+        if (kind <= GW_K_WRITE) {
+          ck = 0;
+#pragma unroll
+          for (int r = 0; r < 4; r++)
+            if (r < kr.n) ck |= (K)((x >> kr.src[r]) & ((1ull << kr.width[r]) - 1ull)) << kr.dst[r];
+        }
+        keys[e] = ck;
+        vals[e] = (uint32_t)e | (kind == GW_K_WRITE ? VAL_W : 0u);
+        atomicAdd(&h[w][(uint32_t)ck & (kRsDigits - 1)], 1u);
+      }
+      if (w0 < tr.n) {  // records longer than 32 events (k_prep)
+        const uint32_t cur = __ballot_sync(0xffffffffu, (to & GW_F_CONT) != 0 && kind != 7u);
+        if (cur == 0xffffffffu) {
+          if (lane == 0) nlong++;
+        } else if (cur & 1u) {
+          const uint32_t prev = __ballot_sync(0xffffffffu, w0 >= 32 && (tr.tidop[w0 - 32 + lane] & GW_F_CONT));
+          unsigned long long y = ((unsigned long long)cur << 32) | prev;
+          y &= y >> 1; y &= y >> 2; y &= y >> 4; y &= y >> 8; y &= y >> 16;
+          if (lane == 0 && ((y >> 1) & 0xFFFFFFFFull)) nlong++;
+        }
+      }
+      if (hd.hkey) {  // k_hard_append
+        const bool hard = kind == GW_K_BARRIER || kind == GW_K_END;
+        const uint32_t m = __ballot_sync(0xffffffffu, hard);
+        if (m) {
+          uint32_t hb = 0;
+          if (lane == __ffs(m) - 1) hb = atomicAdd(hd.ntop, (uint32_t)__popc(m));
+          hb = __shfl_sync(0xffffffffu, hb, __ffs(m) - 1);
+          if (hard) {
+            const uint32_t b = ev_tid(to) / tr.BS;
+            const uint32_t slot = hb + __popc(m & lanemask_lt());
+            if (slot < hd.cap) hd.hkey[slot] = ((unsigned long long)b << 32) | (uint32_t)e;
+            atomicAdd(hd.hcnt + b, 1u);
+          }
+        }
+      }
+    }
+    }
+    __syncthreads();
+    {
+      const int d = threadIdx.x;  // kRsDigits == kThreads
+      uint32_t c = 0;
+#pragma unroll
+      for (int x = 0; x < kRsWarps; x++) c += h[x][d];
+      counts[(uint64_t)d * nst + t] = c;
+    }
+    __syncthreads();
+  }
+  prep_flush(v, ko, ka, nlong, nwbar, stt);
 }
 
 __global__ void k_part_keys(DevTrace tr, uint32_t G, uint32_t* keys, uint32_t* vals) {
@@ -412,32 +521,44 @@ __global__ void __launch_bounds__(kThreads) k_acc_tilemax(const K* keys, const u
   }
 }
 
-template <class K, int I>
+// LAZY: no per-event aux array -- the tile stages the tidops (one 4-byte
+// gather per access) and looks the (time, vobj) stamps up only for the
+// positions that reach a clock test (stamps from the walker's snapshots or
+// arrays, L2-resident); saves the 16-byte aux write + gather per event.
+// S.ss flag: every access of the segment up to this position is by one
+// thread, so the position has no prior-write / reader candidate
+constexpr uint32_t SS_SINGLE = 0x80000000u;
+// padded tile index: one spare word per 32, so both the striped (staging,
+// checks) and the blocked (scan) access patterns are bank-conflict free
+__device__ __forceinline__ uint32_t apx(uint32_t j) { return j + (j >> 5); }
+template <class K, int I, bool LAZY = false>
 struct AccSmem {
-  K key[(kThreads * I)];
-  uint32_t val[(kThreads * I)];
-  uint32_t to[(kThreads * I)];
-  uint32_t lw[(kThreads * I)];   // inclusive last write pos + 1
-  uint32_t ss[(kThreads * I)];   // segment head pos
-  uint2 st[(kThreads * I)];      // (time, vobj) stamps
-  uint2 wtot[kThreads / 32];
+  static constexpr uint32_t P = kThreads * I + (kThreads * I) / 32;
+  K key[P];
+  uint32_t val[P];
+  uint32_t to[P];
+  uint32_t lw[P];   // inclusive last write pos + 1
+  uint32_t ss[P];   // segment head pos | SS_SINGLE
+  uint2 st[LAZY ? 1 : (kThreads * I)];  // (time, vobj) stamps
+  uint3 wtot[kThreads / 32];
 };
 
 // (event, tidop) of sorted position q (smem when q is in this tile)
-template <class K, int I>
-__device__ __forceinline__ void acc_pos(const AccArgs<K>& a, const AccSmem<K, I>& S, uint64_t base, uint64_t q,
+template <class K, int I, bool LAZY>
+__device__ __forceinline__ void acc_pos(const AccArgs<K>& a, const AccSmem<K, I, LAZY>& S, uint32_t base, uint32_t q,
                                         uint32_t& ev, uint32_t& to) {
   if (q >= base) {
-    ev = S.val[q - base] & VAL_E;
-    to = S.to[q - base];
+    ev = S.val[apx(q - base)] & VAL_E;
+    to = S.to[apx(q - base)];
   } else {
     ev = __ldg(a.vals + q) & VAL_E;
     to = a.aux ? __ldg(&a.aux[ev].x) : __ldg(a.tr.tidop + ev);
   }
 }
-template <class K, int I>
-__device__ __forceinline__ uint32_t acc_time(const AccArgs<K>& a, const AccSmem<K, I>& S, uint64_t base, uint64_t q,
-                                             uint32_t ev, uint32_t) {
+template <class K, int I, bool LAZY>
+__device__ __forceinline__ uint32_t acc_time(const AccArgs<K>& a, const AccSmem<K, I, LAZY>& S, uint32_t base,
+                                             uint32_t q, uint32_t ev, uint32_t to) {
+  if (LAZY) return make_aux(a.stamps, ev, to).y;
   if (q >= base) return S.st[q - base].x;
   return a.aux ? __ldg(&a.aux[ev].y) : acc_aux(a, ev).y;
 }
@@ -450,24 +571,60 @@ __device__ __forceinline__ uint32_t acc_clock(const AccArgs<K>& a, uint32_t vo, 
   return __ldg(optr(a.arena, vo) + OBJ_HDR + (u - (tc / BS) * BS));
 }
 
-template <class K, int I>
+template <class K, int I, bool LAZY = false>
 __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  AccSmem<K, I>& S = *reinterpret_cast<AccSmem<K, I>*>(smem_raw);
+  AccSmem<K, I, LAZY>& S = *reinterpret_cast<AccSmem<K, I, LAZY>*>(smem_raw);
   const uint32_t BS = a.tr.BS;
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const uint64_t ntiles = (a.n + (kThreads * I) - 1) / (kThreads * I);
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t base = tile * (kThreads * I);
+  const uint32_t ntiles = (uint32_t)((a.n + (kThreads * I) - 1) / (kThreads * I));  // positions < 2^31
+  // LAZY: the next tile's keys / events (issued before this tile's scan) and
+  // tidops (gathered before its checks) travel in registers while this tile
+  // is processed -- register double buffering hides the gather latency
+  constexpr int PI = LAZY ? I : 1;
+  K pk[PI];
+  uint32_t pv[PI], pt[PI];
+#define GW_ACC_LOAD_KV(t)                                          \
+  {                                                                \
+    const uint32_t b_ = (t) * (kThreads * I);                      \
+    _Pragma("unroll") for (int k = 0; k < PI; k++) {               \
+      const uint32_t j = k * kThreads + threadIdx.x;               \
+      const bool ok = (uint64_t)b_ + j < a.n;                      \
+      pk[k] = ok ? a.keys[b_ + j] : (K)0;                          \
+      pv[k] = ok ? a.vals[b_ + j] : 0u;                            \
+    }                                                              \
+  }
+#define GW_ACC_LOAD_TO(t)                                                        \
+  {                                                                              \
+    const uint32_t b_ = (t) * (kThreads * I);                                    \
+    _Pragma("unroll") for (int k = 0; k < PI; k++) {                             \
+      const uint32_t j = k * kThreads + threadIdx.x;                             \
+      pt[k] = (uint64_t)b_ + j < a.n ? __ldg(a.tr.tidop + (pv[k] & VAL_E)) : 0u; \
+    }                                                                            \
+  }
+  if (LAZY && blockIdx.x < ntiles) {
+    GW_ACC_LOAD_KV(blockIdx.x)
+    GW_ACC_LOAD_TO(blockIdx.x)
+  }
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t base = tile * (kThreads * I);
     const uint32_t cnt = (uint32_t)min((uint64_t)(kThreads * I), a.n - base);
-    // stage keys / events, then gather the tidops
-#pragma unroll
-    for (int k = 0; k < I; k++) {
-      const uint32_t j = k * kThreads + threadIdx.x;
-      if (j < cnt) { S.key[j] = a.keys[base + j]; S.val[j] = a.vals[base + j]; }
-    }
+    const uint32_t nxt = tile + gridDim.x;
+    const bool pre = LAZY && nxt < ntiles;
     const K prevkey = base > 0 ? a.keys[base - 1] : (K)0;
-    {
+    if (LAZY) {
+#pragma unroll
+      for (int k = 0; k < PI; k++) {
+        const uint32_t j = k * kThreads + threadIdx.x;
+        if (j < cnt) { S.key[apx(j)] = pk[k]; S.val[apx(j)] = pv[k]; S.to[apx(j)] = pt[k]; }
+      }
+      if (pre) GW_ACC_LOAD_KV(nxt)
+    } else {
+#pragma unroll
+      for (int k = 0; k < I; k++) {
+        const uint32_t j = k * kThreads + threadIdx.x;
+        if (j < cnt) { S.key[apx(j)] = a.keys[base + j]; S.val[apx(j)] = a.vals[base + j]; }
+      }
       uint4 ax[I];
 #pragma unroll
       for (int k = 0; k < I; k++) {
@@ -477,59 +634,103 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
 #pragma unroll
       for (int k = 0; k < I; k++) {
         const uint32_t j = k * kThreads + threadIdx.x;
-        if (j < cnt) { S.to[j] = ax[k].x; S.st[j] = make_uint2(ax[k].y, ax[k].z); }
+        if (j < cnt) { S.to[apx(j)] = ax[k].x; S.st[(LAZY ? 0 : j)] = make_uint2(ax[k].y, ax[k].z); }
       }
     }
     __syncthreads();
-    // segment head / last write: block-wide max-scan rounds, seeded with the carry
-    uint2 run = a.carry[tile];
-    for (int k = 0; k < I; k++) {
-      const uint32_t j = k * kThreads + threadIdx.x;
-      const uint64_t i = base + j;
-      uint2 v = make_uint2(0, 0);
-      if (j < cnt) {
-        const K kj = S.key[j];
-        const K kp = j > 0 ? S.key[j - 1] : prevkey;
-        if (i == 0 || kj != kp) v.x = (uint32_t)i + 1;
-        if (S.val[j] & VAL_W) v.y = (uint32_t)i + 1;
+    // segment head / last write: a max-scan over the tile, seeded with the
+    // carry.  Blocked: thread t owns positions [t*I, t*I + I) -- a serial pass
+    // over its items, one warp scan and one block combine of the per-thread
+    // maxima, then a second serial pass writes the inclusive values (the
+    // padded smem index keeps the strided accesses conflict-free).  Third
+    // component: the last position (+1) that starts a segment or changes the
+    // thread; equal to the head's, the segment so far is one thread's
+    // (SS_SINGLE).  Position `base` counts as a change (the part of its
+    // segment in earlier tiles is not looked at), which only sends positions
+    // to the full check.
+    {
+      const uint32_t j0 = threadIdx.x * I;
+      uint3 agg = make_uint3(0, 0, 0);
+      K kp = j0 > 0 ? S.key[apx(j0 - 1)] : prevkey;
+      uint32_t tp = j0 > 0 ? ev_tid(S.to[apx(j0 - 1)]) : 0u;
+#pragma unroll
+      for (int k = 0; k < I; k++) {
+        const uint32_t j = j0 + k;
+        if (j < cnt) {
+          const K kj = S.key[apx(j)];
+          const uint32_t tj = ev_tid(S.to[apx(j)]);
+          const bool head = base + j == 0 || kj != kp;
+          if (head) agg.x = base + j + 1;
+          if (S.val[apx(j)] & VAL_W) agg.y = base + j + 1;
+          if (head || j == 0 || tj != tp) agg.z = base + j + 1;
+          kp = kj;
+          tp = tj;
+        }
       }
+      uint3 inc = agg;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t x = __shfl_up_sync(0xffffffffu, v.x, o), y = __shfl_up_sync(0xffffffffu, v.y, o);
-        if (lane >= o) { v.x = max(v.x, x); v.y = max(v.y, y); }
+        const uint32_t x = __shfl_up_sync(0xffffffffu, inc.x, o), y = __shfl_up_sync(0xffffffffu, inc.y, o),
+                       z = __shfl_up_sync(0xffffffffu, inc.z, o);
+        if (lane >= o) { inc.x = max(inc.x, x); inc.y = max(inc.y, y); inc.z = max(inc.z, z); }
       }
-      if (lane == 31) S.wtot[wq] = v;
+      if (lane == 31) S.wtot[wq] = inc;
       __syncthreads();
-      uint2 pre = run, tot = run;
+      const uint2 cin = a.carry[tile];
+      uint3 run = make_uint3(cin.x, cin.y, 0);
 #pragma unroll
       for (int x = 0; x < kThreads / 32; x++) {
-        const uint2 t = S.wtot[x];
-        if (x < wq) { pre.x = max(pre.x, t.x); pre.y = max(pre.y, t.y); }
-        tot.x = max(tot.x, t.x); tot.y = max(tot.y, t.y);
+        const uint3 t = S.wtot[x];
+        if (x < wq) { run.x = max(run.x, t.x); run.y = max(run.y, t.y); run.z = max(run.z, t.z); }
       }
-      if (j < cnt) {
-        S.ss[j] = max(pre.x, v.x) - 1;
-        S.lw[j] = max(pre.y, v.y);
+      {  // exclusive within the warp
+        const uint32_t x = __shfl_up_sync(0xffffffffu, inc.x, 1), y = __shfl_up_sync(0xffffffffu, inc.y, 1),
+                       z = __shfl_up_sync(0xffffffffu, inc.z, 1);
+        if (lane >= 1) { run.x = max(run.x, x); run.y = max(run.y, y); run.z = max(run.z, z); }
       }
-      run = tot;
+      kp = j0 > 0 ? S.key[apx(j0 - 1)] : prevkey;
+      tp = j0 > 0 ? ev_tid(S.to[apx(j0 - 1)]) : 0u;
+#pragma unroll
+      for (int k = 0; k < I; k++) {
+        const uint32_t j = j0 + k;
+        if (j < cnt) {
+          const K kj = S.key[apx(j)];
+          const uint32_t tj = ev_tid(S.to[apx(j)]);
+          const bool head = base + j == 0 || kj != kp;
+          if (head) run.x = base + j + 1;
+          if (S.val[apx(j)] & VAL_W) run.y = base + j + 1;
+          if (head || j == 0 || tj != tp) run.z = base + j + 1;
+          kp = kj;
+          tp = tj;
+          S.ss[apx(j)] = (run.x - 1) | (run.z == run.x ? SS_SINGLE : 0u);
+          S.lw[apx(j)] = run.y;
+        }
+      }
       __syncthreads();
     }
+    if (pre) GW_ACC_LOAD_TO(nxt)
     const uint32_t lw_in = a.carry[tile].y;  // last write before the tile
     // the checks
     for (int k = 0; k < I; k++) {
       const uint32_t j = k * kThreads + threadIdx.x;
       if (j >= cnt) continue;
-      const uint64_t i = base + j;
-      const uint32_t toc = S.to[j];
+      const uint32_t i = base + j;
+      const uint32_t toc = S.to[apx(j)];
       if (ev_kind(toc) > GW_K_WRITE) continue;  // non-access events sort last (sentinel key)
-      const uint32_t c = S.val[j] & VAL_E;
+      const uint32_t c = S.val[apx(j)] & VAL_E;
       const uint32_t tc = ev_tid(toc);
       const bool isw = ev_kind(toc) == GW_K_WRITE;
-      const uint32_t ss = S.ss[j];
-      const uint32_t lw = j > 0 ? S.lw[j - 1] : lw_in;
+      const uint32_t ssr = S.ss[apx(j)];
+      const uint32_t ss = ssr & ~SS_SINGLE;
+      const uint32_t lw = j > 0 ? S.lw[apx(j - 1)] : lw_in;
       const bool hasw = lw > 0 && lw - 1 >= ss && lw - 1 < i;
       const uint32_t W = hasw ? lw - 1 : NIL;
-      const uint32_t vo = a.defer ? NIL : S.st[j].y;
+      uint32_t vo_ = NIL;
+      bool vo_ok = a.defer != 0;
+      auto vo = [&]() {  // the accessing thread's pred object (LAZY: looked up on first use)
+        if (!vo_ok) { vo_ = LAZY ? make_aux(a.stamps, c, toc).z : S.st[(LAZY ? 0 : j)].y; vo_ok = true; }
+        return vo_;
+      };
       unsigned long long loc = 0;
       if (i > ss && (toc & GW_F_CONT) && a.dup.ev) {
         // the previous access to this location may be in the same record
@@ -544,23 +745,24 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
           }
         }
       }
+      if (ssr & SS_SINGLE) continue;  // one thread so far: no prior-write / reader candidate
       if (hasw) {
         uint32_t p, top;
         acc_pos(a, S, base, W, p, top);
         const uint32_t u = ev_tid(top);
         if (u != tc && !cover(top, toc, BS) &&
-            (a.defer || acc_time(a, S, base, W, p, u) > acc_clock(a, vo, tc, u))) {
+            (a.defer || acc_time(a, S, base, W, p, top) > acc_clock(a, vo(), tc, u))) {
           loc = a.tr.key[c];
           emit_cand(a.c, ((unsigned long long)c << 32) | SUB_WCHECK, loc, p, c, isw ? GW_WW : GW_WR);
         }
       }
       if (!isw) continue;
       const uint32_t ws = hasw ? W + 1 : ss;
-      const uint32_t m = (uint32_t)i - ws;
+      const uint32_t m = i - ws;
       if (m == 0) continue;
       if (m > kSmallWin) {
         uint32_t kk = atomicAdd(a.n_large, 1u);
-        if (kk < a.large_cap) { a.large_i[kk] = (uint32_t)i; a.large_ws[kk] = ws; }
+        if (kk < a.large_cap) { a.large_i[kk] = i; a.large_ws[kk] = ws; }
         else atomicOr(a.c.err, ERR_CAND);
         continue;
       }
@@ -584,7 +786,7 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
           acc_pos(a, S, base, q3, e3, t3);
           if (ev_kind(t3) <= GW_K_WRITE && ev_tid(t3) == uq) { first = q3; break; }
         }
-        if (!cover(toq, toc, BS) && (a.defer || acc_time(a, S, base, q, r, uq) > acc_clock(a, vo, tc, uq))) {
+        if (!cover(toq, toc, BS) && (a.defer || acc_time(a, S, base, q, r, toq) > acc_clock(a, vo(), tc, uq))) {
           if (!loc) loc = a.tr.key[c];
           emit_cand(a.c, ((unsigned long long)c << 32) | SUB_READER | (first - ws), loc, r, c, GW_RW);
         }
@@ -593,6 +795,9 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
     __syncthreads();
   }
 }
+
+#undef GW_ACC_LOAD_KV
+#undef GW_ACC_LOAD_TO
 
 // ---- lock mode: deferred clock checks -------------------------------------
 // Q = threads whose clock entry is ever read: prior-access threads of the
@@ -625,11 +830,12 @@ __global__ void k_resolve(Cands in, const uint32_t* qv, const uint32_t* time, Ca
   }
 }
 
-template <class K, int I>
+template <class K, int I, bool LAZY = false>
 inline void acc_setup() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(k_access<K, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(AccSmem<K, I>));
+    cudaFuncSetAttribute(k_access<K, I, LAZY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(AccSmem<K, I, LAZY>));
     done = true;
   }
 }

@@ -178,7 +178,20 @@ struct gw_ctx {
       b.p = nullptr;
       b.cap = 0;
       size_t nb = bytes + bytes / 8;
-      CK(cudaMalloc(&b.p, nb));
+      if (cudaMalloc(&b.p, nb) != cudaSuccess) {
+        cudaGetLastError();
+        size_t held = 0, fr = 0, tot = 0;
+        std::string big;
+        for (auto& kv : bufs) {
+          held += kv.second.cap;
+          if (kv.second.cap >= (1ull << 30)) big += " " + kv.first + "=" + std::to_string(kv.second.cap >> 20) + "M";
+        }
+        cudaMemGetInfo(&fr, &tot);
+        b.p = nullptr;
+        throw CudaErr{GW_E_NOMEM, "out of device memory allocating '" + name + "' (" + std::to_string(nb >> 20) +
+                                      " MiB; device free " + std::to_string(fr >> 20) + " MiB; context holds " +
+                                      std::to_string(held >> 20) + " MiB:" + big + ")"};
+      }
       // zeroed on the analysis stream (look-back flags must never alias a live
       // epoch): a legacy-stream memset would not be ordered before kernels on
       // a non-blocking stream
@@ -390,6 +403,8 @@ struct Pipeline {
     const int npass = (nbits + RB - 1) / RB;
     const uint64_t nst = (lb_tiles(n) + RsBig<RB>::ST - 1) / RsBig<RB>::ST;
     uint32_t* counts = C->get<uint32_t>(std::string("rs_counts") + sfx, nst * RsBig<RB>::ND);
+    const bool counts0 = pre_counts == counts && RB == 8;  // pass 0 counted by k_ingest
+    pre_counts = nullptr;
     rs_down_setup<K, RB>();
     rs_down_tma_setup<K>();
     const unsigned g = (unsigned)std::min<uint64_t>(nst, 148ull * 16);
@@ -399,7 +414,7 @@ struct Pipeline {
       uint32_t* vi = alt ? va : vals;
       K* ko = alt ? keys : ka;
       uint32_t* vo = alt ? vals : va;
-      GW_LAUNCH((k_rs_up<K, RB>), g, kThreads, 0, st, ki, n, RB * p, counts, nst);
+      if (!(p == 0 && counts0)) GW_LAUNCH((k_rs_up<K, RB>), g, kThreads, 0, st, ki, n, RB * p, counts, nst);
       scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nst * RsBig<RB>::ND, OpSum(), 0u,
                             false, "sc_u32");
       if constexpr (RB == 8) {  // ST == 1: TMA-streamed input tiles
@@ -509,15 +524,18 @@ struct Pipeline {
     const char* nf = getenv("GW_FORK");  // experiment hook: GW_FORK=0 runs the sort after the walker
     const bool fork_ok = !(nf && nf[0] == '0');
     const bool early_fork = fork_ok && gmode && nshard <= 1 && !g_prof;
+    Stats* dst = C->get<Stats>("stats", 1);
     if (early_fork) {
       memset(&hs, 0, sizeof hs);
       hs.key_or = P->D;
+      ingest();  // big traces: stats + keys + first digit counts (+ hard events) in one read
       fork_sort();
       if (P->hard_small) fork_hard();  // the hard-event list needs only the trace and the plan's count
     }
-    Stats* dst = C->get<Stats>("stats", 1);
-    GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
-    GW_LAUNCH(k_prep, grid_for(N), kThreads, 0, st, tr, dst);
+    if (!ingested) {
+      GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
+      GW_LAUNCH(k_prep, grid_for(N), kThreads, 0, st, tr, dst);
+    }
     check_launch();
     if (gmode) {
       memset(&hs, 0, sizeof hs);
@@ -534,7 +552,7 @@ struct Pipeline {
     has_locks = hs.n_acq + hs.n_rel > 0;
     S.n_accesses = hs.n_acc;
 
-    plan_sync_pass();
+    if (!ingested) plan_sync_pass();
     if (has_locks) lock_prepass();
     pend(PH_PREP);
 
@@ -546,7 +564,7 @@ struct Pipeline {
       if (!early_fork) fork_sort();
       pbeg(PH_WALKER);
       walker_phase();
-      if (!bk_mode) GW_LAUNCH(k_acc_aux, grid_for(N), kThreads, 0, st, tr, stamps, aux);
+      if (!bk_mode && aux) GW_LAUNCH(k_acc_aux, grid_for(N), kThreads, 0, st, tr, stamps, aux);
       pend(PH_WALKER);
       CK(cudaStreamWaitEvent(st, C->ev_join, 0));
       pbeg(PH_CHECK);
@@ -748,6 +766,46 @@ struct Pipeline {
     hard_forked = true;
   }
 
+  // Graph replays of big lock-free traces (32-bit location keys, LSD pass):
+  // k_ingest reads the trace once for the plan check's stats, the location
+  // keys, the first sort pass's digit counts and (snapshot mode, large hard
+  // list) the hard events, instead of k_prep + k_acc_keys + k_rs_up +
+  // k_hard_append each reading it.  Sets the plan's sync-pass mode early
+  // (plan_sync_pass depends only on the plan in graph mode).
+  bool ingested = false, hard_ingested = false;
+  uint32_t* pre_counts = nullptr;  // digit counts of the first big-sort pass (k_ingest)
+  void ingest() {
+    const char* e = getenv("GW_INGEST");  // 0 = the separate kernels
+    if (e && e[0] == '0') return;
+    const uint64_t N = tr.n;
+    plan_access();
+    if (wide || bk_mode || N < kRsBigN || rs_big_bits(kr.nbits) != 8 || kr.nbits <= 0) return;
+    hs.n_bar = P->n_bar;
+    hs.n_end = P->n_end;
+    hs.n_wbar = P->n_wbar;
+    has_locks = false;
+    plan_sync_pass();
+    Stats* dst = C->get<Stats>("stats", 1);
+    GW_LAUNCH(k_init_stats, 1, 1, 0, st, dst);
+    IngestHard hd{nullptr, nullptr, nullptr, 0};
+    if (snap_mode && !P->hard_small && n_hard > 0) {
+      hd.hkey = C->get<unsigned long long>("hd_key", n_hard + 1);
+      hd.hcnt = C->get<uint32_t>("hd_cnt", tr.B);
+      hd.ntop = zeroed(1);
+      hd.cap = (uint32_t)(n_hard + 1);
+      CK(cudaMemsetAsync(hd.hcnt, 0, sizeof(uint32_t) * tr.B, st));
+      hard_ingested = true;
+    }
+    const uint64_t nst = lb_tiles(N);
+    pre_counts = C->get<uint32_t>("rs_counts_b", nst * RsBig<8>::ND);
+    vals = C->get<uint32_t>("acc_v", N);
+    uint32_t* k32 = C->get<uint32_t>("acc_k", N);
+    GW_LAUNCH(k_ingest<uint32_t>, (unsigned)std::min<uint64_t>(nst, 148ull * 8), kThreads, 0, st, tr, kr, k32, vals,
+              dst, pre_counts, nst, hd);
+    skeys = k32;
+    ingested = true;
+  }
+
   // the access sort on the side stream (joined through ev_join before the check)
   void fork_sort() {
     if (!C->side) {
@@ -757,7 +815,7 @@ struct Pipeline {
     }
     const cudaStream_t main_st = st;
     plan_access();
-    if (!bk_mode) aux = C->get<uint4>("acc_aux", tr.n);  // allocated (and zeroed) on this stream: k_acc_aux writes it here
+    aux = (bk_mode || acc_lazy) ? nullptr : C->get<uint4>("acc_aux", tr.n);  // allocated on this stream: k_acc_aux writes it here
     CK(cudaEventRecord(C->ev_fork, main_st));
     CK(cudaStreamWaitEvent(C->side, C->ev_fork, 0));
     st = C->side;
@@ -823,7 +881,8 @@ struct Pipeline {
     GW_LAUNCH(k_same_instr_heads, 148u * 4, kThreads, 0, st, tr, cd, shard_args(), heads, scal + SC_NHEADS);
   }
   StampSrc stamps{};          // where the access pass reads access stamps (walker output)
-  uint4* aux = nullptr;       // per event (tidop, time, vobj)
+  uint4* aux = nullptr;       // per event (tidop, time, vobj); nullptr: k_access looks stamps up lazily
+  bool acc_lazy = true;
   uint64_t obs_nq = 0;
   uint32_t shard = 0, nshard = 1;  // address sharding (gw_opts)
   bool hb_mode = false;            // GW_OPT_HB: scoped happens-before detector
@@ -920,6 +979,8 @@ struct Pipeline {
     wide = kr.nbits > 32;
     obs_D = hs.n_acc ? hs.key_or ^ hs.key_and : 0ull;
     bk_mode = bucket_ok(gmode ? P->n_acc : hs.n_acc);
+    const char* lz = getenv("GW_ACC_LAZY");  // 0 = the per-event aux pass (k_acc_aux) instead of lazy stamps
+    acc_lazy = !(lz && lz[0] == '0');
   }
   void access_sort(bool split = false) {
     const uint64_t N = tr.n;
@@ -930,13 +991,15 @@ struct Pipeline {
     }
     int nbits = kr.nbits;
     uint64_t NA = N;
-    aux = C->get<uint4>("acc_aux", N);
+    aux = acc_lazy ? nullptr : C->get<uint4>("acc_aux", N);
     if (nshard <= 1) {
       // All N positions are sorted; non-access events carry the top sentinel
       // key and sort last, and every access-pass kernel skips them, so no
       // kernel needs the access count on the host.
       vals = C->get<uint32_t>("acc_v", N);
-      if (!wide && N > 1 && N < kRsBigN && nbits > 0) {
+      if (ingested) {
+        // keys / events written by k_ingest
+      } else if (!wide && N > 1 && N < kRsBigN && nbits > 0) {
         // one-sweep location sort next: the key pass also builds its digit histograms
         // (k_rs_ghist's grid: few CTAs, so few global flushes)
         uint32_t* k32 = C->get<uint32_t>("acc_k", N);
@@ -1175,9 +1238,10 @@ struct Pipeline {
     CK(cudaMemsetAsync(scal + SC_NLARGE2, 0, sizeof(uint32_t), st));
     AccArgs<uint32_t> a = bk_acc_args(cd, keys, vals2, tot, li, lws, scal + SC_NLARGE2, lcap);
     a.carry = car;
-    acc_setup<uint32_t, kAccItemsSmall>();
+    acc_setup<uint32_t, kAccItemsSmall, true>();
     const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>(nt, 1), 148ull * 16);
-    GW_LAUNCH((k_access<uint32_t, kAccItemsSmall>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsSmall>), st, a);
+    GW_LAUNCH((k_access<uint32_t, kAccItemsSmall, true>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsSmall, true>),
+              st, a);
     check_launch();
     uint32_t nl = 0;
     d2h(&nl, scal + SC_NLARGE2);
@@ -1643,6 +1707,7 @@ struct Pipeline {
         aa.n = NA;
         aa.carry = carry;
         aa.aux = aux;
+        aa.stamps = stamps;
         aa.arena = defer ? nullptr : w.arena;
         aa.defer = defer ? 1 : 0;
         aa.blockobj = (!defer && !has_locks) ? 1 : 0;
@@ -1657,19 +1722,37 @@ struct Pipeline {
       const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>((NA + atile - 1) / atile, 1), 148ull * 16);
       if (wide) {
         fill(a64, (const unsigned long long*)skeys);
-        acc_setup<unsigned long long, kAccItemsSmall>();
-        GW_LAUNCH((k_access<unsigned long long, kAccItemsSmall>), ag, kThreads,
-                  sizeof(AccSmem<unsigned long long, kAccItemsSmall>), st, a64);
+        if (aux) {
+          acc_setup<unsigned long long, kAccItemsSmall>();
+          GW_LAUNCH((k_access<unsigned long long, kAccItemsSmall>), ag, kThreads,
+                    sizeof(AccSmem<unsigned long long, kAccItemsSmall>), st, a64);
+        } else {
+          acc_setup<unsigned long long, kAccItemsSmall, true>();
+          GW_LAUNCH((k_access<unsigned long long, kAccItemsSmall, true>), ag, kThreads,
+                    sizeof(AccSmem<unsigned long long, kAccItemsSmall, true>), st, a64);
+        }
       } else if (acc_items == kAccItemsLarge) {
         fill(a32, (const uint32_t*)skeys);
-        acc_setup<uint32_t, kAccItemsLarge>();
-        GW_LAUNCH((k_access<uint32_t, kAccItemsLarge>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsLarge>), st,
-                  a32);
+        if (aux) {
+          acc_setup<uint32_t, kAccItemsLarge>();
+          GW_LAUNCH((k_access<uint32_t, kAccItemsLarge>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsLarge>), st,
+                    a32);
+        } else {
+          acc_setup<uint32_t, kAccItemsLarge, true>();
+          GW_LAUNCH((k_access<uint32_t, kAccItemsLarge, true>), ag, kThreads,
+                    sizeof(AccSmem<uint32_t, kAccItemsLarge, true>), st, a32);
+        }
       } else {
         fill(a32, (const uint32_t*)skeys);
-        acc_setup<uint32_t, kAccItemsSmall>();
-        GW_LAUNCH((k_access<uint32_t, kAccItemsSmall>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsSmall>), st,
-                  a32);
+        if (aux) {
+          acc_setup<uint32_t, kAccItemsSmall>();
+          GW_LAUNCH((k_access<uint32_t, kAccItemsSmall>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsSmall>), st,
+                    a32);
+        } else {
+          acc_setup<uint32_t, kAccItemsSmall, true>();
+          GW_LAUNCH((k_access<uint32_t, kAccItemsSmall, true>), ag, kThreads,
+                    sizeof(AccSmem<uint32_t, kAccItemsSmall, true>), st, a32);
+        }
       }
       check_launch();
       if (gmode) {
@@ -1859,11 +1942,12 @@ struct Pipeline {
         obs_hard_small = true;
         hard_small_list(n_hard, hev, hcnt, hbeg, hend);
       } else {
-        CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
+        if (!hard_ingested) CK(cudaMemsetAsync(hcnt, 0, sizeof(uint32_t) * tr.B, st));
         if (n_hard) {
           unsigned long long* hkey = C->get<unsigned long long>("hd_key", n_hard + 1);
           uint32_t* hdummy = C->get<uint32_t>("hd_v", n_hard + 1);
-          GW_LAUNCH(k_hard_append, grid_for(N), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT);
+          if (!hard_ingested)
+            GW_LAUNCH(k_hard_append, grid_for(N), kThreads, 0, st, tr, hkey, hcnt, zeroed(1), scal + SC_ABORT);
           sort<unsigned long long>(hkey, hdummy, n_hard, 32 + ceil_log2(tr.B), "hd", true);
           GW_LAUNCH(k_hard_unpack, grid_for(n_hard), kThreads, 0, st, hkey, n_hard, hev);
         }
@@ -2376,8 +2460,6 @@ extern "C" int gw_ctx_analyze_host_delta(gw_ctx* c, const gw_trace_delta* t, con
       CK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->ev_prev, cudaEventDisableTiming));
     }
-    CK(cudaEventRecord(c->ev_prev, st));  // earlier analyses on st may still read the input buffers
-    CK(cudaStreamWaitEvent(c->copy_st, c->ev_prev, 0));
     uint8_t* db[3];
     uint64_t* doff[3];
     uint64_t* dbase[3];
@@ -2386,6 +2468,12 @@ extern "C" int gw_ctx_analyze_host_delta(gw_ctx* c, const gw_trace_delta* t, con
       db[col] = c->get<uint8_t>(std::string(nm[col]) + "_b", t->nbytes[col] + 16);
       doff[col] = c->get<uint64_t>(std::string(nm[col]) + "_o", K + 1);
       dbase[col] = c->get<uint64_t>(std::string(nm[col]) + "_s", K + 1);
+    }
+    // after the allocations: a new buffer is zeroed on st, and earlier analyses
+    // on st may still read the staging / input buffers the copies overwrite
+    CK(cudaEventRecord(c->ev_prev, st));
+    CK(cudaStreamWaitEvent(c->copy_st, c->ev_prev, 0));
+    for (int col = 0; col < 3; col++) {
       if (K) {
         CK(cudaMemcpyAsync(doff[col], t->offs[col], 8 * (K + 1), cudaMemcpyHostToDevice, c->copy_st));
         CK(cudaMemcpyAsync(dbase[col], t->base[col], 8 * K, cudaMemcpyHostToDevice, c->copy_st));
