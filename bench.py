@@ -63,9 +63,10 @@ def kernel_alg_bytes(name: str, N: int, n: int) -> int | None:
         ("k_rs_down_tma", 16 * n),
         ("k_rs_onesweep", 16 * n),
         ("k_rs_up", 4 * n),         # keys read
-        ("k_access", 24 * n),       # key 4 + event 4 + (tidop, time, vobj, pad) 16 per sorted position
-        ("k_acc_keys", 36 * N),     # key 8 + tidop 4 read; key 4 + event 4 + aux 16 written (profiled runs: unsplit)
-        ("k_acc_aux", 20 * N),      # tidop 4 read, aux 16 written
+        ("k_access", 12 * n),       # key 4 + event 4 + the event's tidop 4 per sorted position (stamps: lazy, L2)
+        ("k_acc_keys", 20 * N),     # key 8 + tidop 4 read; key 4 + event 4 written
+        ("k_ingest", 20 * N),       # same bytes: k_prep + k_acc_keys + first digit counts in one read (graph replays)
+        ("k_acc_aux", 20 * N),      # (GW_ACC_LAZY=0 only) tidop 4 read, aux 16 written
         ("k_acc_tilemax", 8 * n),
         ("k_prep", 12 * N),
         ("k_same_instr", 16 * N),

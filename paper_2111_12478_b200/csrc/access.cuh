@@ -317,7 +317,7 @@ struct IngestHard {
 };
 template <class K>
 __global__ void __launch_bounds__(kThreads) k_ingest(DevTrace tr, KeyRuns kr, K* keys, uint32_t* vals, Stats* stt,
-                                                    uint32_t* counts, uint64_t nst, IngestHard hd) {
+                                                    uint32_t* counts, uint64_t nst, IngestHard hd, int rb0) {
   __shared__ uint32_t h[kRsWarps][kRsDigits];
   unsigned long long v[6] = {0, 0, 0, 0, 0, 0};
   unsigned long long ko = 0, ka = ~0ull, nlong = 0, nwbar = 0;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kThreads) k_ingest(DevTrace tr, KeyRuns kr, K*
         }
         keys[e] = ck;
         vals[e] = (uint32_t)e | (kind == GW_K_WRITE ? VAL_W : 0u);
-        atomicAdd(&h[w][(uint32_t)ck & (kRsDigits - 1)], 1u);
+        atomicAdd(&h[w][(uint32_t)ck & ((1u << rb0) - 1u)], 1u);
       }
       if (w0 < tr.n) {  // records longer than 32 events (k_prep)
         const uint32_t cur = __ballot_sync(0xffffffffu, (to & GW_F_CONT) != 0 && kind != 7u);
@@ -390,10 +390,12 @@ __global__ void __launch_bounds__(kThreads) k_ingest(DevTrace tr, KeyRuns kr, K*
     __syncthreads();
     {
       const int d = threadIdx.x;  // kRsDigits == kThreads
-      uint32_t c = 0;
+      if (d < (1 << rb0)) {
+        uint32_t c = 0;
 #pragma unroll
-      for (int x = 0; x < kRsWarps; x++) c += h[x][d];
-      counts[(uint64_t)d * nst + t] = c;
+        for (int x = 0; x < kRsWarps; x++) c += h[x][d];
+        counts[(uint64_t)d * nst + t] = c;
+      }
     }
     __syncthreads();
   }

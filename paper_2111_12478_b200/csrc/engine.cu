@@ -398,32 +398,64 @@ struct Pipeline {
     }
   }
 
+  // bits of pass p when nbits are spread evenly over ceil(nbits / 8) passes
+  // (low passes take the remainder): 29 -> 8, 7, 7, 7
+  static int big_pass_bits(int nbits, int p, int* shift) {
+    const int np = (nbits + kRsBits - 1) / kRsBits, b = nbits / np, x = nbits % np;
+    *shift = p * b + std::min(p, x);
+    return b + (p < x ? 1 : 0);
+  }
+  template <class K, int RB>
+  void big_pass(const K* ki, const uint32_t* vi, K* ko, uint32_t* vo, uint64_t n, int shift, uint32_t* counts,
+                uint64_t nst, unsigned g, bool counted) {
+    if (!counted) GW_LAUNCH((k_rs_up<K, RB>), g, kThreads, 0, st, ki, n, shift, counts, nst);
+    scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nst * (1u << RB), OpSum(), 0u, false,
+                          "sc_u32");
+    rs_down_tma_setup<K, RB>();
+    GW_LAUNCH((k_rs_down_tma<K, RB>), g, kThreads, sizeof(RsTmaSmem<K>), st, ki, vi, ko, vo, n, shift, counts, nst);
+  }
   template <class K, int RB>
   void big_sort(K*& keys, K* ka, uint32_t*& vals, uint32_t* va, uint64_t n, int nbits) {
-    const int npass = (nbits + RB - 1) / RB;
     const uint64_t nst = (lb_tiles(n) + RsBig<RB>::ST - 1) / RsBig<RB>::ST;
     uint32_t* counts = C->get<uint32_t>(std::string("rs_counts") + sfx, nst * RsBig<RB>::ND);
     const bool counts0 = pre_counts == counts && RB == 8;  // pass 0 counted by k_ingest
     pre_counts = nullptr;
-    rs_down_setup<K, RB>();
-    rs_down_tma_setup<K>();
     const unsigned g = (unsigned)std::min<uint64_t>(nst, 148ull * 16);
     bool alt = false;
-    for (int p = 0; p < npass; p++) {
-      K* ki = alt ? ka : keys;
-      uint32_t* vi = alt ? va : vals;
-      K* ko = alt ? keys : ka;
-      uint32_t* vo = alt ? vals : va;
-      if (!(p == 0 && counts0)) GW_LAUNCH((k_rs_up<K, RB>), g, kThreads, 0, st, ki, n, RB * p, counts, nst);
-      scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nst * RsBig<RB>::ND, OpSum(), 0u,
-                            false, "sc_u32");
-      if constexpr (RB == 8) {  // ST == 1: TMA-streamed input tiles
-        GW_LAUNCH((k_rs_down_tma<K>), g, kThreads, sizeof(RsTmaSmem<K>), st, ki, vi, ko, vo, n, RB * p, counts, nst);
-      } else {
+    if constexpr (RB == 8) {  // ST == 1: TMA-streamed input tiles, balanced <= 8-bit digits
+      const int npass = (nbits + RB - 1) / RB;
+      for (int p = 0; p < npass; p++) {
+        const K* ki = alt ? ka : keys;
+        const uint32_t* vi = alt ? va : vals;
+        K* ko = alt ? keys : ka;
+        uint32_t* vo = alt ? vals : va;
+        int shift = 0;
+        const int b = big_pass_bits(nbits, p, &shift);
+        const bool cnt = p == 0 && counts0;
+        switch (b) {
+          case 8: big_pass<K, 8>(ki, vi, ko, vo, n, shift, counts, nst, g, cnt); break;
+          case 7: big_pass<K, 7>(ki, vi, ko, vo, n, shift, counts, nst, g, cnt); break;
+          case 6: big_pass<K, 6>(ki, vi, ko, vo, n, shift, counts, nst, g, cnt); break;
+          case 5: big_pass<K, 5>(ki, vi, ko, vo, n, shift, counts, nst, g, cnt); break;
+          default: big_pass<K, 4>(ki, vi, ko, vo, n, shift, counts, nst, g, cnt); break;
+        }
+        alt = !alt;
+      }
+    } else {
+      const int npass = (nbits + RB - 1) / RB;
+      rs_down_setup<K, RB>();
+      for (int p = 0; p < npass; p++) {
+        K* ki = alt ? ka : keys;
+        uint32_t* vi = alt ? va : vals;
+        K* ko = alt ? keys : ka;
+        uint32_t* vo = alt ? vals : va;
+        GW_LAUNCH((k_rs_up<K, RB>), g, kThreads, 0, st, ki, n, RB * p, counts, nst);
+        scan<uint32_t, OpSum>(ArrLoad<uint32_t>{counts}, ArrStore<uint32_t>{counts}, nst * RsBig<RB>::ND, OpSum(), 0u,
+                              false, "sc_u32");
         GW_LAUNCH((k_rs_down<K, RB>), g, kThreads, sizeof(RsBigSmem<K, RB>), st, ki, vi, ko, vo, n, RB * p, counts,
                   nst);
+        alt = !alt;
       }
-      alt = !alt;
     }
     if (alt) {
       keys = ka;
@@ -800,8 +832,10 @@ struct Pipeline {
     pre_counts = C->get<uint32_t>("rs_counts_b", nst * RsBig<8>::ND);
     vals = C->get<uint32_t>("acc_v", N);
     uint32_t* k32 = C->get<uint32_t>("acc_k", N);
+    int sh0 = 0;
+    const int rb0 = big_pass_bits(kr.nbits, 0, &sh0);  // the first big-sort pass's digit width
     GW_LAUNCH(k_ingest<uint32_t>, (unsigned)std::min<uint64_t>(nst, 148ull * 8), kThreads, 0, st, tr, kr, k32, vals,
-              dst, pre_counts, nst, hd);
+              dst, pre_counts, nst, hd, rb0);
     skeys = k32;
     ingested = true;
   }

@@ -494,8 +494,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? GW_OS_MINB : 2) k_r
 template <int RB>
 struct RsBig {
   static constexpr int ND = 1 << RB;
-  static constexpr int DPT = ND / kThreads;  // digits per thread
-  static constexpr int ST = RB == 8 ? 1 : 4; // tiles per super-tile
+  static constexpr int DPT = ND >= kThreads ? ND / kThreads : 1;  // digits per thread (RB < 8: threads < ND)
+  static constexpr int ST = RB <= 8 ? 1 : 4; // tiles per super-tile
 };
 
 template <class K, int RB>
@@ -525,6 +525,7 @@ __global__ void __launch_bounds__(kThreads) k_rs_up(const K* __restrict__ keys, 
 #pragma unroll
     for (int j = 0; j < DPT; j++) {
       const int d = threadIdx.x * DPT + j;
+      if (d >= ND) break;
       uint32_t c = 0;
 #pragma unroll
       for (int x = 0; x < kRsWarps; x++) c += h[x][d];
@@ -681,7 +682,9 @@ struct RsTmaSmem {
   uint32_t gbase[kRsDigits];
   unsigned long long mbar[2];
 };
-template <class K>
+// RB <= 8 bits per pass (the big sort balances a key's bits over its passes:
+// 29 bits -> 8 + 7 + 7 + 7, fewer ballots per rank and longer digit runs)
+template <class K, int RB = kRsBits>
 __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tma(const K* __restrict__ kin,
                                                                             const uint32_t* __restrict__ vin,
                                                                             K* __restrict__ kout,
@@ -689,7 +692,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tm
                                                                             int shift,
                                                                             const uint32_t* __restrict__ offsets,
                                                                             uint64_t nst) {
-  constexpr int ND = kRsDigits;
+  static_assert(RB >= 1 && RB <= kRsBits, "k_rs_down_tma: 1..8-bit digits");
+  constexpr int ND = 1 << RB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RsTmaSmem<K>& S = *reinterpret_cast<RsTmaSmem<K>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -716,8 +720,8 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tm
     if (threadIdx.x == 0 && nx < nst && full_tile(nx)) issue(nx, b ^ 1);
     const uint64_t tbase = st * kTile;
     const bool full = full_tile(st);
-    S.gbase[threadIdx.x] = offsets[(uint64_t)threadIdx.x * nst + st];
-    for (int d = threadIdx.x; d < kRsWarps * ND; d += kThreads) (&S.wc[0][0])[d] = 0;
+    if (threadIdx.x < ND) S.gbase[threadIdx.x] = offsets[(uint64_t)threadIdx.x * nst + st];
+    for (int x = threadIdx.x; x < kRsWarps * ND; x += kThreads) S.wc[x / ND][x % ND] = 0;  // rows of kRsDigits
     K kk[kRsRounds];
     uint32_t vv[kRsRounds];
     uint32_t rd[kRsRounds];
@@ -746,7 +750,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tm
 #pragma unroll
     for (int r = 0; r < kRsRounds; r++) {
       const uint32_t d = rd[r] >> 16;
-      const uint32_t peers = full ? warp_peers<kRsBits>(d) : warp_peers<kRsBits + 1>(d);
+      const uint32_t peers = full ? warp_peers<RB>(d) : warp_peers<RB + 1>(d);
       const uint32_t before = d < (uint32_t)ND ? S.wc[w][d] : 0u;
       __syncwarp();
       if (d < (uint32_t)ND && (peers & lt) == 0) S.wc[w][d] = before + __popc(peers);
@@ -757,14 +761,17 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tm
     {
       const int d = threadIdx.x;
       uint32_t run = 0;
+      if (d < ND) {
 #pragma unroll
-      for (int ww = 0; ww < kRsWarps; ww++) {
-        const uint32_t t = S.wc[ww][d];
-        S.wc[ww][d] = run;
-        run += t;
+        for (int ww = 0; ww < kRsWarps; ww++) {
+          const uint32_t t = S.wc[ww][d];
+          S.wc[ww][d] = run;
+          run += t;
+        }
       }
       uint32_t ct;
-      S.toff[d] = block_excl_scan<uint32_t, OpSum>(run, OpSum(), 0u, &ct);
+      const uint32_t off = block_excl_scan<uint32_t, OpSum>(run, OpSum(), 0u, &ct);
+      if (d < ND) S.toff[d] = off;
     }
     __syncthreads();
 #pragma unroll
@@ -790,11 +797,12 @@ __global__ void __launch_bounds__(kThreads, sizeof(K) == 4 ? 3 : 2) k_rs_down_tm
     __syncthreads();  // buffer b free for the TMA of tile it + 2
   }
 }
-template <class K>
+template <class K, int RB = kRsBits>
 inline void rs_down_tma_setup() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(k_rs_down_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RsTmaSmem<K>));
+    cudaFuncSetAttribute(k_rs_down_tma<K, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(RsTmaSmem<K>));
     done = true;
   }
 }

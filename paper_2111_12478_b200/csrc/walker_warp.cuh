@@ -200,31 +200,38 @@ __device__ uint32_t w_fused_join(const WalkArgs& a, uint32_t base, uint32_t vt, 
   uint32_t* out = optr(a.arena, o) + OBJ_HDR;
   int ch = 0;
   if (S.full) {
+    // kJU 16-byte words per lane in flight per object: each op streams
+    // whole clocks, so the memory-level parallelism of one warp sets the
+    // op's latency -- and the per-lock chains are made of these ops.  A
+    // source raises the result iff it exceeds the running max (exact `ch`).
+    constexpr int kJU = 8;
     const uint32_t n4 = n >> 2;
     const uint4* b4 = base != NIL ? reinterpret_cast<const uint4*>(optr(a.arena, base) + OBJ_HDR) : nullptr;
-    for (uint32_t i0 = lane; i0 < n4; i0 += 32 * 4) {
-      uint4 v[4], bv[4];
+    for (uint32_t i0 = lane; i0 < n4; i0 += 32 * kJU) {
+      uint4 v[kJU];
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
+      for (int k = 0; k < kJU; k++) {
         const uint32_t i = i0 + 32 * k;
-        bv[k] = (b4 && i < n4) ? __ldcg(b4 + i) : make_uint4(0, 0, 0, 0);
-        v[k] = bv[k];
+        v[k] = (b4 && i < n4) ? __ldcg(b4 + i) : make_uint4(0, 0, 0, 0);
       }
       for (uint32_t s = 0; s < ns; s++) {
         const uint4* s4 = reinterpret_cast<const uint4*>(optr(a.arena, S.src[s]) + OBJ_HDR);
+        uint4 sv[kJU];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < kJU; k++) {
           const uint32_t i = i0 + 32 * k;
-          if (i < n4) v[k] = max4(v[k], __ldcg(s4 + i));
+          sv[k] = i < n4 ? __ldcg(s4 + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < kJU; k++) {
+          if (gt4(sv[k], v[k])) ch = 1;
+          v[k] = max4(v[k], sv[k]);
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
+      for (int k = 0; k < kJU; k++) {
         const uint32_t i = i0 + 32 * k;
-        if (i < n4) {
-          reinterpret_cast<uint4*>(out)[i] = v[k];
-          if (gt4(v[k], bv[k])) ch = 1;
-        }
+        if (i < n4) reinterpret_cast<uint4*>(out)[i] = v[k];
       }
     }
     for (uint32_t i = (n4 << 2) + lane; i < n; i += 32) {
@@ -604,21 +611,25 @@ __device__ void w_barrier_warp(const WalkArgs& a, uint32_t to, uint32_t ins, WSm
     if (no != NIL) {
       uint32_t* out = optr(a.arena, no) + OBJ_HDR;
       if (S.full) {
+        constexpr int kJU = 8;  // as w_fused_join
         const uint32_t n4 = n >> 2;
-        for (uint32_t i0 = lane; i0 < n4; i0 += 32 * 4) {
-          uint4 v[4];
+        for (uint32_t i0 = lane; i0 < n4; i0 += 32 * kJU) {
+          uint4 v[kJU];
 #pragma unroll
-          for (int k = 0; k < 4; k++) v[k] = make_uint4(0, 0, 0, 0);
+          for (int k = 0; k < kJU; k++) v[k] = make_uint4(0, 0, 0, 0);
           for (uint32_t s = 0; s < ns; s++) {
             const uint4* s4 = reinterpret_cast<const uint4*>(optr(a.arena, S.src[s]) + OBJ_HDR);
+            uint4 sv[kJU];
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
+            for (int k = 0; k < kJU; k++) {
               const uint32_t i = i0 + 32 * k;
-              if (i < n4) v[k] = max4(v[k], __ldcg(s4 + i));
+              sv[k] = i < n4 ? __ldcg(s4 + i) : make_uint4(0, 0, 0, 0);
             }
+#pragma unroll
+            for (int k = 0; k < kJU; k++) v[k] = max4(v[k], sv[k]);
           }
 #pragma unroll
-          for (int k = 0; k < 4; k++) {
+          for (int k = 0; k < kJU; k++) {
             const uint32_t i = i0 + 32 * k;
             if (i < n4) reinterpret_cast<uint4*>(out)[i] = v[k];
           }
