@@ -543,6 +543,7 @@ struct AccSmem {
   uint32_t ss[P];   // segment head pos | SS_SINGLE
   uint2 st[LAZY ? 1 : (kThreads * I)];  // (time, vobj) stamps
   uint3 wtot[kThreads / 32];
+  uint32_t ltot[kThreads / 32];
 };
 
 // (event, tidop) of sorted position q (smem when q is in this tile)
@@ -650,6 +651,7 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
     // (SS_SINGLE).  Position `base` counts as a change (the part of its
     // segment in earlier tiles is not looked at), which only sends positions
     // to the full check.
+    uint32_t need = 0;  // bit k: position threadIdx.x * I + k goes to the full check
     {
       const uint32_t j0 = threadIdx.x * I;
       uint3 agg = make_uint3(0, 0, 0);
@@ -692,30 +694,63 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
       }
       kp = j0 > 0 ? S.key[apx(j0 - 1)] : prevkey;
       tp = j0 > 0 ? ev_tid(S.to[apx(j0 - 1)]) : 0u;
+      // the event of the previous position (same-record check below)
+      uint32_t pe = j0 > 0 ? (S.val[apx(j0 - 1)] & VAL_E) : (base > 0 ? (a.vals[base - 1] & VAL_E) : 0u);
 #pragma unroll
       for (int k = 0; k < I; k++) {
         const uint32_t j = j0 + k;
         if (j < cnt) {
           const K kj = S.key[apx(j)];
-          const uint32_t tj = ev_tid(S.to[apx(j)]);
+          const uint32_t toj = S.to[apx(j)], vj = S.val[apx(j)];
+          const uint32_t tj = ev_tid(toj);
           const bool head = base + j == 0 || kj != kp;
           if (head) run.x = base + j + 1;
-          if (S.val[apx(j)] & VAL_W) run.y = base + j + 1;
+          if (vj & VAL_W) run.y = base + j + 1;
           if (head || j == 0 || tj != tp) run.z = base + j + 1;
           kp = kj;
           tp = tj;
-          S.ss[apx(j)] = (run.x - 1) | (run.z == run.x ? SS_SINGLE : 0u);
+          const bool single = run.z == run.x;
+          S.ss[apx(j)] = (run.x - 1) | (single ? SS_SINGLE : 0u);
           S.lw[apx(j)] = run.y;
+          // positions the full check must see: not one thread's segment so
+          // far, or the previous access to the location is in the same record
+          const uint32_t c = vj & VAL_E;
+          if (ev_kind(toj) <= GW_K_WRITE &&
+              (!single || (a.dup.ev && !head && (toj & GW_F_CONT) && pe < c && c - pe < 32)))
+            need |= 1u << k;
+          pe = c;
         }
       }
+    }
+    // the flagged positions as a list (in the key staging, no longer read)
+    uint32_t nlist;
+    {
+      const uint32_t cntn = __popc(need);
+      uint32_t inc = cntn;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += x;
+      }
+      if (lane == 31) S.ltot[wq] = inc;
+      __syncthreads();  // also: every thread is done reading the keys
+      uint32_t off = inc - cntn;
+      nlist = 0;
+#pragma unroll
+      for (int x = 0; x < kThreads / 32; x++) {
+        const uint32_t t = S.ltot[x];
+        if (x < wq) off += t;
+        nlist += t;
+      }
+      uint16_t* L = reinterpret_cast<uint16_t*>(S.key);
+      for (uint32_t m = need; m; m &= m - 1) L[off++] = (uint16_t)(threadIdx.x * I + __ffs(m) - 1);
       __syncthreads();
     }
     if (pre) GW_ACC_LOAD_TO(nxt)
     const uint32_t lw_in = a.carry[tile].y;  // last write before the tile
-    // the checks
-    for (int k = 0; k < I; k++) {
-      const uint32_t j = k * kThreads + threadIdx.x;
-      if (j >= cnt) continue;
+    // the checks, over the flagged positions
+    for (uint32_t x = threadIdx.x; x < nlist; x += kThreads) {
+      const uint32_t j = reinterpret_cast<const uint16_t*>(S.key)[x];
       const uint32_t i = base + j;
       const uint32_t toc = S.to[apx(j)];
       if (ev_kind(toc) > GW_K_WRITE) continue;  // non-access events sort last (sentinel key)
