@@ -57,9 +57,16 @@ struct StampSrc {  // valid() false in lock mode (the walker runs after the acce
     const uint32_t g = warp_mode ? b * 8u + (t - b * BS) / L : b;
     const uint32_t base = __ldg(hb_beg + g);
     uint32_t lo = base, hi = __ldg(hb_end + g);
-    while (lo < hi) {
-      const uint32_t m = (lo + hi) >> 1;
-      if (__ldg(hard_ev + m) < e) lo = m + 1; else hi = m;
+    if (hi - lo <= 16) {  // short lists (C2 / C5: 16 per block): one round of independent loads
+      uint32_t c = 0;
+#pragma unroll
+      for (int k = 0; k < 16; k++) c += (lo + k < hi && __ldg(hard_ev + lo + k) < e) ? 1u : 0u;
+      lo += c;
+    } else {
+      while (lo < hi) {
+        const uint32_t m = (lo + hi) >> 1;
+        if (__ldg(hard_ev + m) < e) lo = m + 1; else hi = m;
+      }
     }
     return warp_mode ? snap[(size_t)(lo + g) * 32 + (t - b * BS) % L] : snap[(size_t)(lo + g) * BS + (t - b * BS)];
   }
@@ -787,8 +794,13 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
         uint32_t p, top;
         acc_pos(a, S, base, W, p, top);
         const uint32_t u = ev_tid(top);
-        if (u != tc && !cover(top, toc, BS) &&
-            (a.defer || acc_time(a, S, base, W, p, top) > acc_clock(a, vo(), tc, u))) {
+        bool race = u != tc && !cover(top, toc, BS);
+        if (race && !a.defer) {  // both stamp lookups issued before either is used
+          const uint32_t v = vo();
+          const uint32_t tw = acc_time(a, S, base, W, p, top);
+          race = tw > acc_clock(a, v, tc, u);
+        }
+        if (race) {
           loc = a.tr.key[c];
           emit_cand(a.c, ((unsigned long long)c << 32) | SUB_WCHECK, loc, p, c, isw ? GW_WW : GW_WR);
         }

@@ -1013,18 +1013,6 @@ struct Pipeline {
     wide = kr.nbits > 32;
     obs_D = hs.n_acc ? hs.key_or ^ hs.key_and : 0ull;
     bk_mode = bucket_ok(gmode ? P->n_acc : hs.n_acc);
-    // few non-access events: they take key 0 (location 0's segment, where
-    // every access-pass kernel skips them) instead of a sentinel bit, one
-    // key bit less for the LSD sort (C5: 29 -> 28 bits, 8+7+7+7 -> 7+7+7+7)
-    const uint64_t nonacc = tr.n - (gmode ? P->n_acc : hs.n_acc);
-    const char* sn = getenv("GW_SENTINEL");  // 1 = always the sentinel bit
-    if (!(sn && sn[0] == '1') && !bk_mode && nshard <= 1 && kr.sentinel && kr.nbits > 2 && kr.nbits <= 33 &&
-        nonacc <= (1ull << 20)) {
-      kr.sentinel = 0;
-      kr.nbits -= 1;
-      C->stats.sort_bits = kr.nbits;
-      wide = kr.nbits > 32;
-    }
     const char* lz = getenv("GW_ACC_LAZY");  // 0 = the per-event aux pass (k_acc_aux) instead of lazy stamps
     acc_lazy = !(lz && lz[0] == '0');
   }
