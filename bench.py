@@ -454,6 +454,17 @@ def run_b200(args):
         t[: len(enc["bytes"][c])].copy_(torch.from_numpy(enc["bytes"][c]))
         enc_pinned.append(t)
         enc["bytes"][c] = t.numpy()[: len(enc["bytes"][c])]
+    # the bit-packed form (GWSOA v4, gw_encode_bp): ~0.26 B/event on C5, the headline e2e input
+    encb = N.encode_bp(cfg, key_h.numpy().view(np.uint64), to_h.numpy().view(np.uint32),
+                       in_h.numpy().view(np.uint32))
+    bp_pinned = []
+    for c in range(3):
+        t = torch.empty(max(len(encb["bytes"][c]), 1), dtype=torch.uint8, pin_memory=True)
+        t[: len(encb["bytes"][c])].copy_(torch.from_numpy(encb["bytes"][c]))
+        bp_pinned.append(t)
+        encb["bytes"][c] = t.numpy()[: len(encb["bytes"][c])]
+    bp_bytes = sum(len(b) for b in encb["bytes"]) + sum(8 * (len(o) + len(b_) + len(d_)) for o, b_, d_ in
+                                                         zip(encb["offs"], encb["base"], encb["dbase"]))
     delta_bytes = sum(len(b) for b in enc["bytes"]) + sum(8 * (len(o) + len(b_)) for o, b_ in
                                                             zip(enc["offs"], enc["base"]))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -481,6 +492,12 @@ def run_b200(args):
 
     def step_host_packed():
         ctx.analyze_host_packed(cfg, keyp_np, to_h.numpy().view(np.uint32), inp_np, stream=sptr, shard=shard)
+        return finish()
+
+    def step_host_bp():
+        if sharded:  # (the sharded mode takes the 16-B host form)
+            return step_host()
+        ctx.analyze_host_bp(encb, stream=sptr)
         return finish()
 
     def step_host_delta():
@@ -538,11 +555,17 @@ def run_b200(args):
         barrier()
         ms_dev = max_over_ranks(ms_dev)
         for _ in range(args.warmup):
-            step_host_delta()
+            step_host_bp()
         barrier()
-        ms_e2e, res_e2e = timed(step_host_delta, args.steps)
+        ms_e2e, res_e2e = timed(step_host_bp, args.steps)
         barrier()
         ms_e2e = max_over_ranks(ms_e2e)
+        for _ in range(args.warmup):
+            step_host_delta()
+        barrier()
+        ms_e2ed, res_e2ed = timed(step_host_delta, args.steps)
+        barrier()
+        ms_e2ed = max_over_ranks(ms_e2ed)
         for _ in range(args.warmup):
             step_host_packed()
         barrier()
@@ -566,7 +589,8 @@ def run_b200(args):
 
         fx = load_full_digest(args.workload)
         digest = digest_for(res, fx, n)
-        for what, r in (("delta host-buffer", res_e2e), ("packed host-buffer", res_e2ep),
+        for what, r in (("bit-packed host-buffer", res_e2e), ("delta host-buffer", res_e2ed),
+                        ("packed host-buffer", res_e2ep),
                         ("16-B host-buffer", res_e2e16)):
             d_e2e = digest_for(r, fx, n)
             if d_e2e != digest:
@@ -586,6 +610,7 @@ def run_b200(args):
     value = total_events / (ms_dev / 1000.0)
     e2e = total_events / (ms_e2e / 1000.0)
     e2e16 = total_events / (ms_e2e16 / 1000.0)
+    e2ed = total_events / (ms_e2ed / 1000.0)
     e2ep = total_events / (ms_e2ep / 1000.0)
     peak, peak_kind = load_peaks()
     alg_bytes = 16 * n + 36 * n_acc  # 16 B per event + 36 B per access
@@ -645,13 +670,19 @@ def run_b200(args):
         "e2e": {
             "value": e2e,
             "unit": UNIT,
-            "h2d_bytes_per_step": (16 * n) if sharded else delta_bytes,
+            "h2d_bytes_per_step": (16 * n) if sharded else bp_bytes,
             "d2h_bytes_per_step": 9 * n_rep + 64,
             "ms_per_step": ms_e2e / args.steps,
             "input": ("16-B/event host SoA" if sharded else
-                      f"delta-varint host trace ({delta_bytes / max(n, 1):.2f} B/event: zigzag LEB128 deltas of "
-                      "key / tidop / instr in 4,096-event chunks, pinned; GWSOA v3, gw_encode_delta), "
-                      "gw_ctx_analyze_host_delta: sliced H2D on a copy stream overlapped with on-device decoding"),
+                      f"bit-packed host trace ({bp_bytes / max(n, 1):.2f} B/event: per 32-event block, residuals "
+                      "of the columns' first differences against the previous / one-record-back / two-records-"
+                      "back difference, packed at the block's width with exceptions, 4,096-event chunks, pinned; "
+                      "GWSOA v4, gw_encode_bp), gw_ctx_analyze_host_bp: sliced H2D on a copy stream overlapped "
+                      "with on-device decoding (one warp per chunk and column)"),
+            "delta": {"value": e2ed, "unit": UNIT, "h2d_bytes_per_step": delta_bytes,
+                      "ms_per_step": ms_e2ed / args.steps,
+                      "input": f"delta-varint host trace ({delta_bytes / max(n, 1):.2f} B/event, GWSOA v3), "
+                               "gw_ctx_analyze_host_delta"},
             "packed": {"value": e2ep, "unit": UNIT, "h2d_bytes_per_step": (kb + 4 + ib) * n,
                        "ms_per_step": ms_e2ep / args.steps,
                        "input": f"packed host SoA (key {kb} B + tidop 4 B + instr {ib} B per event, pinned), "

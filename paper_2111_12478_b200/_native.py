@@ -86,6 +86,12 @@ class _Delta(C.Structure):
                 ("offs", C.c_void_p * 3), ("base", C.c_void_p * 3)]
 
 
+class _BP(C.Structure):
+    _fields_ = [("cfg", _Config), ("n_events", C.c_uint64), ("chunk", C.c_uint32), ("_pad", C.c_uint32),
+                ("n_chunks", C.c_uint64), ("bytes", C.c_void_p * 3), ("nbytes", C.c_uint64 * 3),
+                ("offs", C.c_void_p * 3), ("base", C.c_void_p * 3), ("dbase", C.c_void_p * 3)]
+
+
 class XsStats(C.Structure):
     _fields_ = [(f, C.c_uint64) for f in ("n_acc", "n_write", "n_acq", "n_rel", "n_end", "n_bar", "key_or",
                                           "key_and", "n_long", "n_wbar")]
@@ -146,6 +152,9 @@ EXPORTS = (
     "gw_encode_delta",
     "gw_delta_free",
     "gw_ctx_analyze_host_delta",
+    "gw_encode_bp",
+    "gw_bp_free",
+    "gw_ctx_analyze_host_bp",
     "gw_xs_prep",
     "gw_xs_hard",
     "gw_xs_partition",
@@ -231,6 +240,11 @@ def lib():
         L.gw_delta_free.argtypes = [C.POINTER(_Delta)]
         L.gw_ctx_analyze_host_delta.argtypes = [C.c_void_p, C.POINTER(_Delta), C.POINTER(_Opts)]
         L.gw_ctx_analyze_host_delta.restype = C.c_int
+        L.gw_encode_bp.argtypes = [C.POINTER(_View), C.POINTER(_BP)]
+        L.gw_encode_bp.restype = C.c_int
+        L.gw_bp_free.argtypes = [C.POINTER(_BP)]
+        L.gw_ctx_analyze_host_bp.argtypes = [C.c_void_p, C.POINTER(_BP), C.POINTER(_Opts)]
+        L.gw_ctx_analyze_host_bp.restype = C.c_int
         L.gw_ctx_fetch.argtypes = [C.c_void_p, C.POINTER(_Result)]
         L.gw_ctx_fetch.restype = C.c_int
         L.gw_ctx_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
@@ -468,6 +482,25 @@ class Context:
         o_ = _Opts(1 if inactive_opt else 0, flags, stream, 0, 1)
         _check(self._L.gw_ctx_analyze_host_delta(self._c, C.byref(d), C.byref(o_)))
 
+    def analyze_host_bp(self, enc: dict, *, inactive_opt=True, stream=None, eager=False, hb=False) -> None:
+        """Bit-packed host trace (encode_bp, GWSOA v4): sliced upload
+        overlapped with on-device decoding (gw_ctx_analyze_host_bp)."""
+        d = _BP()
+        d.cfg.blocks, d.cfg.warps, d.cfg.lanes = enc["cfg"]
+        d.n_events = enc["n"]
+        d.chunk = DELTA_CHUNK
+        d.n_chunks = (enc["n"] + DELTA_CHUNK - 1) // DELTA_CHUNK
+        for c in range(3):
+            b, o, s_, ds = enc["bytes"][c], enc["offs"][c], enc["base"][c], enc["dbase"][c]
+            d.bytes[c] = b.ctypes.data if len(b) else None
+            d.nbytes[c] = len(b)
+            d.offs[c] = o.ctypes.data
+            d.base[c] = s_.ctypes.data if len(s_) else None
+            d.dbase[c] = ds.ctypes.data if len(ds) else None
+        flags = (OPT_EAGER if eager else 0) | (OPT_HB if hb else 0)
+        o_ = _Opts(1 if inactive_opt else 0, flags, stream, 0, 1)
+        _check(self._L.gw_ctx_analyze_host_bp(self._c, C.byref(d), C.byref(o_)))
+
     def analyze_device(self, cfg, n, key_ptr, tidop_ptr, instr_ptr, *, inactive_opt=True, stream=None,
                        eager=False, shard=(0, 1), profile=False, hb=False) -> None:
         """shard=(index, count): report only races on location-key range `index`
@@ -569,6 +602,84 @@ def encode_delta(cfg, key, tidop, instr) -> dict:
                 "base": [take(d.base[c], k, np.uint64) for c in range(3)]}
     finally:
         L.gw_delta_free(C.byref(d))
+
+
+def encode_bp(cfg, key, tidop, instr) -> dict:
+    """The bit-packed form of a host SoA (gw_encode_bp, GWSOA v4): as
+    encode_delta, plus "dbase" (each chunk's first difference before it)."""
+    L = lib()
+    key = np.ascontiguousarray(key, np.uint64)
+    tidop = np.ascontiguousarray(tidop, np.uint32)
+    instr = np.ascontiguousarray(instr, np.uint32)
+    v = _view(cfg, key, tidop, instr)
+    d = _BP()
+    _check(L.gw_encode_bp(C.byref(v), C.byref(d)))
+    try:
+        k = int(d.n_chunks)
+
+        def take(p, count, dt):
+            if count == 0:
+                return np.zeros(0, dt)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(np.ctypeslib.as_ctypes_type(dt))), shape=(count,)).copy()
+
+        return {"cfg": tuple(cfg), "n": len(tidop),
+                "bytes": [take(d.bytes[c], int(d.nbytes[c]), np.uint8) for c in range(3)],
+                "offs": [take(d.offs[c], k + 1, np.uint64) for c in range(3)],
+                "base": [take(d.base[c], k, np.uint64) for c in range(3)],
+                "dbase": [take(d.dbase[c], k, np.uint64) for c in range(3)]}
+    finally:
+        L.gw_bp_free(C.byref(d))
+
+
+def decode_bp_host(enc: dict) -> tuple:
+    """Host (Python) decoder of encode_bp's format -- test infrastructure,
+    the format's executable spec (include/gwcp_b200.h); the product decodes
+    on the device (k_bp_decode)."""
+    n = enc["n"]
+    cols = []
+    for c, (T, w) in enumerate(((np.uint64, 64), (np.uint32, 32), (np.uint32, 32))):
+        M = (1 << w) - 1
+        out = np.zeros(n, T)
+        byts, offs = enc["bytes"][c], enc["offs"][c]
+        for k in range(len(offs) - 1):
+            lo = k * DELTA_CHUNK
+            cnt = min(DELTA_CHUNK, n - lo)
+            nb = (cnt + 31) // 32
+            ch = byts[int(offs[k]):int(offs[k + 1])].tobytes()
+            hdr = ch[:nb]
+            nexc, xw, pos = [], [], nb
+            for h in hdr:
+                if h & 0x20:
+                    nexc.append(ch[pos]); xw.append(ch[pos + 1]); pos += 2
+                else:
+                    nexc.append(0); xw.append(0)
+            pos = (pos + 3) & ~3
+            packed = []
+            for h in hdr:
+                b = h & 31
+                packed.append(int.from_bytes(ch[pos:pos + 4 * b], "little")); pos += 4 * b
+            E = sum(nexc)
+            idx = ch[pos:pos + E]; pos += E
+            x, d = int(enc["base"][c][k]), int(enc["dbase"][c][k])
+            hist = [[0] * 32, [0] * 32]  # d of the blocks one and two back
+            e = 0
+            for kb, h in enumerate(hdr):
+                b, mode = h & 31, h >> 6
+                z = [(packed[kb] >> (l * b)) & ((1 << b) - 1) for l in range(32)]
+                for _ in range(nexc[kb]):
+                    z[idx[e]] = int.from_bytes(ch[pos:pos + xw[kb]], "little"); pos += xw[kb]; e += 1
+                dcur = []
+                for l in range(32):
+                    r = (z[l] >> 1) ^ (-(z[l] & 1) & M)
+                    pred = d if mode == 0 else hist[0][l] if mode == 1 else hist[1][l] if mode == 2 else 0
+                    d = (pred + r) & M
+                    dcur.append(d)
+                    x = (x + d) & M
+                    if 32 * kb + l < cnt:
+                        out[lo + 32 * kb + l] = x
+                hist = [dcur, hist[0]]
+        cols.append(out)
+    return tuple(cols)
 
 
 def pack_columns(key, instr, tidop=None):

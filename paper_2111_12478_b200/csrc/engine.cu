@@ -2464,6 +2464,152 @@ inline void delta_setup() {
   }
 }
 
+// ---- bit-packed trace (gw_trace_bp, codec.cpp) --------------------------------
+// One warp per chunk of one column: the chunk's bytes staged in the warp's
+// shared-memory slice (global reads past it), the block headers' widths /
+// exception counts turned into offsets by warp scans, then the blocks in
+// order: lane l extracts its b bits, exceptions patch their lanes, the
+// residuals become first differences (mode 0: a warp scan from the previous
+// block's last difference; modes 1 / 2: the same lane's difference one / two
+// blocks back; mode 3: the residual itself) and the differences values (a
+// warp scan from the previous value).
+constexpr int kBpWarps = 8;
+constexpr uint32_t kBpStageWords = 1024;  // 4 KB per warp (C5: ~0.1-0.3 KB per chunk and column)
+
+template <class T>
+__device__ __forceinline__ T bp_scan(T v, uint32_t lane) {  // inclusive warp prefix sum (mod 2^w)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= (uint32_t)o) v += y;
+  }
+  return v;
+}
+__device__ __forceinline__ uint32_t bp_pick(const uint32_t (&v)[4], uint32_t q) {
+  return q == 0 ? v[0] : q == 1 ? v[1] : q == 2 ? v[2] : v[3];
+}
+
+struct BpCol {
+  const uint8_t* bytes;
+  const uint64_t* offs;
+  const uint64_t* base;
+  const uint64_t* dbase;
+  void* out;
+};
+template <class T>
+__device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint64_t N, uint32_t* sw, uint32_t lane) {
+  const uint8_t* __restrict__ bytes = C.bytes;
+  const uint64_t* __restrict__ offs = C.offs;
+  const uint64_t* __restrict__ base = C.base;
+  const uint64_t* __restrict__ dbase = C.dbase;
+  T* __restrict__ out = reinterpret_cast<T*>(C.out);
+  {
+    const uint64_t lo = k * GW_DELTA_CHUNK, cnt = min((uint64_t)GW_DELTA_CHUNK, N - lo);
+    const uint32_t nb = (uint32_t)((cnt + 31) / 32);
+    const uint64_t cb = offs[k];
+    const uint32_t csz = (uint32_t)(offs[k + 1] - cb);  // multiple of 4
+    const uint32_t* gw = reinterpret_cast<const uint32_t*>(bytes + cb);
+    const bool staged = csz <= 4 * kBpStageWords;
+    if (staged)
+      for (uint32_t i = lane; i < csz / 4; i += 32) sw[i] = __ldg(gw + i);
+    __syncwarp();
+    const uint32_t* W = staged ? sw : gw;
+    auto byte_at = [&](uint32_t o) -> uint32_t { return (W[o >> 2] >> (8 * (o & 3))) & 0xFFu; };
+    // headers of blocks 4 lane .. 4 lane + 3; (count, width) byte pairs follow
+    // the headers, one pair per block with exceptions
+    uint32_t hd[4], nx[4], xw[4], wo[4], eo[4], vo[4];
+    uint32_t esum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const uint32_t kb = 4 * lane + q;
+      hd[q] = kb < nb ? byte_at(kb) : 0u;
+      esum += (hd[q] >> 5) & 1u;
+    }
+    const uint32_t einc = bp_scan<uint32_t>(esum, lane), ne_blocks = __shfl_sync(0xffffffffu, einc, 31);
+    uint32_t eidx = einc - esum, wsum = 0, xsum = 0, vsum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      nx[q] = 0;
+      xw[q] = 0;
+      if ((hd[q] >> 5) & 1u) {
+        nx[q] = byte_at(nb + 2 * eidx);
+        xw[q] = byte_at(nb + 2 * eidx + 1);
+        eidx++;
+      }
+      wsum += hd[q] & 31u;
+      xsum += nx[q];
+      vsum += nx[q] * xw[q];
+    }
+    const uint32_t winc = bp_scan<uint32_t>(wsum, lane), xinc = bp_scan<uint32_t>(xsum, lane),
+                   vinc = bp_scan<uint32_t>(vsum, lane);
+    const uint32_t words_tot = __shfl_sync(0xffffffffu, winc, 31), exc_tot = __shfl_sync(0xffffffffu, xinc, 31);
+    const uint32_t pk0 = ((nb + 2 * ne_blocks + 3) & ~3u) / 4;  // first packed word
+    const uint32_t ix0 = 4 * (pk0 + words_tot);                 // first exception lane byte
+    const uint32_t xv0 = ix0 + exc_tot;                          // first exception value byte
+    {
+      uint32_t w0 = winc - wsum, e0 = xinc - xsum, v0 = vinc - vsum;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        wo[q] = w0; w0 += hd[q] & 31u;
+        eo[q] = e0; e0 += nx[q];
+        vo[q] = v0; v0 += nx[q] * xw[q];
+      }
+    }
+    T xl = (T)base[k], dl = (T)dbase[k], d1 = 0, d2 = 0;  // d1 / d2: this lane's difference one / two blocks back
+    for (uint32_t kb = 0; kb < nb; kb++) {
+      const uint32_t src = kb >> 2, q = kb & 3;
+      const uint32_t h = __shfl_sync(0xffffffffu, bp_pick(hd, q), src);
+      const uint32_t wof = __shfl_sync(0xffffffffu, bp_pick(wo, q), src);
+      const uint32_t b = h & 31u, mode = h >> 6;
+      uint64_t p = 0;
+      if (b) {
+        const uint32_t bit = lane * b, wi = pk0 + wof + (bit >> 5), sh = bit & 31;
+        uint64_t v = (uint64_t)W[wi];
+        if (sh + b > 32) v |= (uint64_t)W[wi + 1] << 32;
+        p = (v >> sh) & ((1ull << b) - 1);
+      }
+      if ((h >> 5) & 1u) {  // exceptions: zigzag values of their lanes, xw bytes each
+        const uint32_t ne = __shfl_sync(0xffffffffu, bp_pick(nx, q), src);
+        const uint32_t w = __shfl_sync(0xffffffffu, bp_pick(xw, q), src);
+        const uint32_t e0 = __shfl_sync(0xffffffffu, bp_pick(eo, q), src);
+        const uint32_t v0 = __shfl_sync(0xffffffffu, bp_pick(vo, q), src);
+        for (uint32_t e = 0; e < ne; e++) {
+          if (byte_at(ix0 + e0 + e) == lane) {
+            uint64_t z = 0;
+            for (uint32_t y = 0; y < w; y++) z |= (uint64_t)byte_at(xv0 + v0 + e * w + y) << (8 * y);
+            p = z;
+          }
+        }
+      }
+      const T r = (T)((p >> 1) ^ (uint64_t)(-(int64_t)(p & 1)));  // unzigzag
+      const T d = mode == 0 ? (T)(dl + bp_scan<T>(r, lane)) : mode == 1 ? (T)(d1 + r) : mode == 2 ? (T)(d2 + r) : r;
+      const T x = (T)(xl + bp_scan<T>(d, lane));
+      const uint64_t i = lo + 32ull * kb + lane;
+      if (i < lo + cnt) out[i] = x;
+      d2 = d1;
+      d1 = d;
+      dl = __shfl_sync(0xffffffffu, d, 31);
+      xl = __shfl_sync(0xffffffffu, x, 31);
+    }
+    __syncwarp();
+  }
+}
+// all three columns of chunks [k0, k1) in one launch: warp task t = chunk
+// k0 + t / 3, column t % 3 (0: key u64, 1: tidop, 2: instr)
+__global__ void __launch_bounds__(32 * kBpWarps) k_bp_decode(BpCol c0, BpCol c1, BpCol c2, uint64_t k0, uint64_t k1,
+                                                            uint64_t N) {
+  __shared__ uint32_t stage[kBpWarps][kBpStageWords];
+  const uint32_t lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const uint64_t nt = 3 * (k1 - k0);
+  for (uint64_t t = (uint64_t)blockIdx.x * kBpWarps + wq; t < nt; t += (uint64_t)gridDim.x * kBpWarps) {
+    const uint64_t k = k0 + t / 3;
+    const uint32_t col = (uint32_t)(t % 3);
+    if (col == 0) bp_decode_chunk<unsigned long long>(c0, k, N, stage[wq], lane);
+    else bp_decode_chunk<uint32_t>(col == 1 ? c1 : c2, k, N, stage[wq], lane);
+    __syncwarp();
+  }
+}
+
 extern "C" int gw_ctx_analyze_host_delta(gw_ctx* c, const gw_trace_delta* t, const gw_opts* o) {
   if (!c || !t) { gw_set_error("null argument"); return GW_E_ARG; }
   if (t->chunk != GW_DELTA_CHUNK || t->n_chunks != (t->n_events + GW_DELTA_CHUNK - 1) / GW_DELTA_CHUNK) {
@@ -2537,6 +2683,83 @@ extern "C" int gw_ctx_analyze_host_delta(gw_ctx* c, const gw_trace_delta* t, con
                 k0, k1, N, to);
       GW_LAUNCH(k_delta_decode<uint32_t>, g, kThreads, sizeof(DeltaSmem<uint32_t>), st, db[2], doff[2], dbase[2],
                 k0, k1, N, in);
+    }
+    DevTrace tr = make_dev(&view, k, to, in);
+    analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,
+                 o && (o->flags & GW_OPT_PROFILE), o && (o->flags & GW_OPT_HB));
+  });
+}
+
+extern "C" int gw_ctx_analyze_host_bp(gw_ctx* c, const gw_trace_bp* t, const gw_opts* o) {
+  if (!c || !t) { gw_set_error("null argument"); return GW_E_ARG; }
+  if (t->chunk != GW_DELTA_CHUNK || t->n_chunks != (t->n_events + GW_DELTA_CHUNK - 1) / GW_DELTA_CHUNK) {
+    gw_set_error("bit-packed trace: chunking does not match GW_DELTA_CHUNK");
+    return GW_E_ARG;
+  }
+  gw_trace_view view;
+  view.cfg = t->cfg;
+  view.n_events = t->n_events;
+  view.key = (const uint64_t*)t->bytes[0];
+  view.tidop = (const uint32_t*)t->bytes[1];
+  view.instr = (const uint32_t*)t->bytes[2];
+  int v = validate_view(&view);
+  if (v) return v;
+  return guarded([&] {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = o ? (cudaStream_t)o->stream : (cudaStream_t)0;
+    const uint32_t inactive = o ? o->inactive_opt : 1u;
+    const uint32_t nsh = o && o->shard_count > 1 ? o->shard_count : 1u;
+    const uint32_t sh = nsh > 1 ? o->shard_index : 0u;
+    if (sh >= nsh) throw CudaErr{GW_E_ARG, "shard_index must be < shard_count"};
+    const uint64_t N = t->n_events, K = t->n_chunks;
+    c->last_stream = st;
+    unsigned long long* k = c->get<unsigned long long>("in_key", N);
+    uint32_t* to = c->get<uint32_t>("in_tidop", N);
+    uint32_t* in = c->get<uint32_t>("in_instr", N);
+    if (!c->copy_st) {
+      CK(cudaStreamCreateWithFlags(&c->copy_st, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->ev_prev, cudaEventDisableTiming));
+    }
+    uint8_t* db[3];
+    uint64_t* doff[3];
+    uint64_t* dbase[3];
+    uint64_t* ddb[3];
+    const char* nm[3] = {"bp_key", "bp_tidop", "bp_instr"};
+    for (int col = 0; col < 3; col++) {
+      db[col] = c->get<uint8_t>(std::string(nm[col]) + "_b", t->nbytes[col] + 16);
+      doff[col] = c->get<uint64_t>(std::string(nm[col]) + "_o", K + 1);
+      dbase[col] = c->get<uint64_t>(std::string(nm[col]) + "_s", K + 1);
+      ddb[col] = c->get<uint64_t>(std::string(nm[col]) + "_d", K + 1);
+    }
+    // after the allocations: a new buffer is zeroed on st, and earlier analyses
+    // on st may still read the staging / input buffers the copies overwrite
+    CK(cudaEventRecord(c->ev_prev, st));
+    CK(cudaStreamWaitEvent(c->copy_st, c->ev_prev, 0));
+    for (int col = 0; col < 3; col++) {
+      if (K) {
+        CK(cudaMemcpyAsync(doff[col], t->offs[col], 8 * (K + 1), cudaMemcpyHostToDevice, c->copy_st));
+        CK(cudaMemcpyAsync(dbase[col], t->base[col], 8 * K, cudaMemcpyHostToDevice, c->copy_st));
+        CK(cudaMemcpyAsync(ddb[col], t->dbase[col], 8 * K, cudaMemcpyHostToDevice, c->copy_st));
+      }
+    }
+    constexpr uint64_t kSlice = 4096;  // chunks per upload slice (16 M events; ~4.5 MB on C5)
+    const uint64_t ns = (K + kSlice - 1) / kSlice;
+    while (c->chunk_ev.size() < ns) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->chunk_ev.push_back(e);
+    }
+    for (uint64_t sl = 0; sl < ns; sl++) {
+      const uint64_t k0 = sl * kSlice, k1 = std::min(K, k0 + kSlice);
+      for (int col = 0; col < 3; col++) {
+        const uint64_t a = t->offs[col][k0], b = t->offs[col][k1];
+        if (b > a) CK(cudaMemcpyAsync(db[col] + a, t->bytes[col] + a, b - a, cudaMemcpyHostToDevice, c->copy_st));
+      }
+      CK(cudaEventRecord(c->chunk_ev[sl], c->copy_st));
+      CK(cudaStreamWaitEvent(st, c->chunk_ev[sl], 0));  // decode slice sl while slice sl + 1 is in flight
+      const unsigned g = (unsigned)std::min<uint64_t>((3 * (k1 - k0) + kBpWarps - 1) / kBpWarps, 148ull * 7);
+      GW_LAUNCH(k_bp_decode, g, 32 * kBpWarps, 0, st, BpCol{db[0], doff[0], dbase[0], ddb[0], k},
+                BpCol{db[1], doff[1], dbase[1], ddb[1], to}, BpCol{db[2], doff[2], dbase[2], ddb[2], in}, k0, k1, N);
     }
     DevTrace tr = make_dev(&view, k, to, in);
     analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,

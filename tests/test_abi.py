@@ -5,6 +5,7 @@ import os
 import re
 
 from paper_2111_12478_b200 import _native as N
+from paper_2111_12478_b200 import workloads as WL
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -143,3 +144,29 @@ def test_delta_encoding_roundtrip():
     assert np.array_equal(_delta_decode(enc["bytes"][0], enc["offs"][0], enc["base"][0], n, 64), key)
     assert np.array_equal(_delta_decode(enc["bytes"][1], enc["offs"][1], enc["base"][1], n, 32), tidop)
     assert np.array_equal(_delta_decode(enc["bytes"][2], enc["offs"][2], enc["base"][2], n, 32), instr)
+
+
+def test_bitpacked_encoding_roundtrip():
+    """gw_encode_bp (host, chunk-parallel) against the format's executable
+    spec (decode_bp_host): warp-structured traces (every predictor mode),
+    random columns (exceptions of every width), partial chunks / blocks."""
+    import numpy as np
+
+    rng = np.random.default_rng(11)
+    cases = []
+    tr = WL.c2_soa_prefix(70_000, **{k: v for k, v in WL.CONFIGS["c5"].items() if k != "gen"})
+    cases.append((tr.key, tr.tidop, tr.instr))
+    n = 9_001  # two full chunks + a partial one, a partial last block
+    cases.append((rng.integers(0, 2**64, n, dtype=np.uint64), rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32),
+                  rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)))
+    mixed = np.cumsum(rng.integers(0, 8, 5_000, dtype=np.uint64) * np.uint64(4)) + np.uint64(2**63)
+    mixed[::97] = rng.integers(0, 2**64, len(mixed[::97]), dtype=np.uint64)  # rare wide jumps -> exceptions
+    cases.append((mixed, (np.arange(5_000) % 4096).astype(np.uint32), np.zeros(5_000, np.uint32)))
+    cases.append((np.zeros(1, np.uint64), np.ones(1, np.uint32), np.full(1, 2**32 - 1, np.uint32)))
+    for key, tidop, instr in cases:
+        enc = N.encode_bp((4, 8, 32), key, tidop, instr)
+        assert all(len(b) % 4 == 0 for b in enc["bytes"]) and all(int(o[-1]) == len(b) for o, b in zip(enc["offs"], enc["bytes"]))
+        k, t, i = N.decode_bp_host(enc)
+        assert np.array_equal(k, key) and np.array_equal(t, tidop) and np.array_equal(i, instr)
+    enc = N.encode_bp((4, 8, 32), *cases[0])
+    assert sum(len(b) for b in enc["bytes"]) < 0.5 * len(cases[0][1])  # C5 recipe: < 0.5 B/event

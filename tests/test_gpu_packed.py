@@ -117,3 +117,53 @@ def test_delta_input_full_c2_and_many_slices(goldens, ctx):
         got = _run_delta(ctx, tr, stream=stream.cuda_stream)
         for f in ("kind", "prior", "current"):
             assert np.array_equal(got[f], want[f])
+
+
+def _run_bp(ctx, tr, inactive_opt=True, **kw):
+    enc = N.encode_bp(tr.cfg_tuple, tr.key, tr.tidop, tr.instr)
+    ctx.analyze_host_bp(enc, inactive_opt=inactive_opt, **kw)
+    return ctx.fetch()
+
+
+def test_bitpacked_input_reference_goldens(goldens, ctx):
+    """The bit-packed host form (gw_ctx_analyze_host_bp): decoded on the
+    device (k_bp_decode), the same reports as the 16-B SoA."""
+    n = 0
+    for r in goldens:
+        if "error" in r or "full" in r["tags"] or not ({"corpus", "nasty", "random", "c1", "c3", "c4"} & set(r["tags"])):
+            continue
+        tr = parse_trace(golden_text(r))
+        check_against_golden(r, tr, _run_bp(ctx, tr, r["inactive_opt"]))
+        n += 1
+    assert n > 3000
+
+
+def test_bitpacked_input_full_c2_many_slices_and_wide_values(goldens, ctx):
+    import torch
+
+    r = next(r for r in goldens if r["name"] == "c2/full")
+    tr = WL.c2_soa()
+    check_against_golden(r, tr, _run_bp(ctx, tr))
+    # > 1024 chunks: several upload slices decoded while later ones land; on a
+    # stream, so the later calls replay the captured graph
+    tr = WL.c2_soa(blocks=1024, warps=8, lanes=32, phases=2, records=80, words_per_block=262144, seed=5)
+    stream = torch.cuda.Stream(device=torch.device("cuda", 0))
+    ctx.analyze_host(tr.cfg_tuple, tr.key, tr.tidop, tr.instr, stream=stream.cuda_stream)
+    want = ctx.fetch()
+    for _ in range(3):
+        got = _run_bp(ctx, tr, stream=stream.cuda_stream)
+        for f in ("kind", "prior", "current"):
+            assert np.array_equal(got[f], want[f])
+    # 64-bit shared-memory keys, random instrs: exceptions of every width through the device decoder
+    rng = np.random.default_rng(5)
+    t = WL.c2_soa_prefix(200_000, **{k: v for k, v in WL.CONFIGS["c5"].items() if k != "gen"})
+    key = t.key.copy()
+    key[::13] |= np.uint64(1 << 63)
+    instr = rng.integers(0, 2**32, len(key), dtype=np.uint64).astype(np.uint32)
+    from paper_2111_12478_b200.trace import Trace
+    t2 = Trace(t.config, key, t.tidop, instr)
+    ctx.analyze_host(t2.cfg_tuple, t2.key, t2.tidop, t2.instr)
+    want = ctx.fetch()
+    got = _run_bp(ctx, t2)
+    for f in ("kind", "prior", "current"):
+        assert np.array_equal(got[f], want[f])
