@@ -2555,12 +2555,29 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
         vo[q] = v0; v0 += nx[q] * xw[q];
       }
     }
-    T xl = (T)base[k], dl = (T)dbase[k], d1 = 0, d2 = 0;  // d1 / d2: this lane's difference one / two blocks back
+    // d1 / d2: this lane's difference one / two blocks back; s1 / s2: the
+    // inclusive warp scans of those blocks' differences
+    T xl = (T)base[k], dl = (T)dbase[k], d1 = 0, d2 = 0, s1 = 0, s2 = 0;
     for (uint32_t kb = 0; kb < nb; kb++) {
       const uint32_t src = kb >> 2, q = kb & 3;
       const uint32_t h = __shfl_sync(0xffffffffu, bp_pick(hd, q), src);
-      const uint32_t wof = __shfl_sync(0xffffffffu, bp_pick(wo, q), src);
       const uint32_t b = h & 31u, mode = h >> 6;
+      const uint64_t i = lo + 32ull * kb + lane;
+      if ((h & 0x3Fu) == 0) {  // b = 0, no exceptions: every residual 0, no scan needed
+        T d, sd;
+        if (mode == 0) { d = dl; sd = (T)((T)(lane + 1) * dl); }
+        else if (mode == 1) { d = d1; sd = s1; }
+        else if (mode == 2) { d = d2; sd = s2; }
+        else { d = 0; sd = 0; }
+        const T x = (T)(xl + sd);
+        if (i < lo + cnt) out[i] = x;
+        d2 = d1; s2 = s1;
+        d1 = d; s1 = sd;
+        dl = __shfl_sync(0xffffffffu, d, 31);
+        xl = __shfl_sync(0xffffffffu, x, 31);
+        continue;
+      }
+      const uint32_t wof = __shfl_sync(0xffffffffu, bp_pick(wo, q), src);
       uint64_t p = 0;
       if (b) {
         const uint32_t bit = lane * b, wi = pk0 + wof + (bit >> 5), sh = bit & 31;
@@ -2583,11 +2600,11 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
       }
       const T r = (T)((p >> 1) ^ (uint64_t)(-(int64_t)(p & 1)));  // unzigzag
       const T d = mode == 0 ? (T)(dl + bp_scan<T>(r, lane)) : mode == 1 ? (T)(d1 + r) : mode == 2 ? (T)(d2 + r) : r;
-      const T x = (T)(xl + bp_scan<T>(d, lane));
-      const uint64_t i = lo + 32ull * kb + lane;
+      const T sd = bp_scan<T>(d, lane);
+      const T x = (T)(xl + sd);
       if (i < lo + cnt) out[i] = x;
-      d2 = d1;
-      d1 = d;
+      d2 = d1; s2 = s1;
+      d1 = d; s1 = sd;
       dl = __shfl_sync(0xffffffffu, d, 31);
       xl = __shfl_sync(0xffffffffu, x, 31);
     }
