@@ -2556,57 +2556,133 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
       }
     }
     // d1 / d2: this lane's difference one / two blocks back; s1 / s2: the
-    // inclusive warp scans of those blocks' differences
-    T xl = (T)base[k], dl = (T)dbase[k], d1 = 0, d2 = 0, s1 = 0, s2 = 0;
+    // inclusive warp scans of those blocks' differences; D* / S*: their last
+    // lane's values (warp-uniform).  Blocks without residuals need no shuffle:
+    // x = x_last + s, and the uniforms advance.
+    T xl = (T)base[k], dl = (T)dbase[k], d1 = 0, d2 = 0, s1 = 0, s2 = 0, D1 = 0, D2 = 0, S1 = 0, S2 = 0;
+    const uint64_t iend = lo + cnt;
     for (uint32_t kb = 0; kb < nb; kb++) {
-      const uint32_t src = kb >> 2, q = kb & 3;
-      const uint32_t h = __shfl_sync(0xffffffffu, bp_pick(hd, q), src);
+      const uint32_t h = byte_at(kb);  // warp-uniform (a broadcast load)
       const uint32_t b = h & 31u, mode = h >> 6;
       const uint64_t i = lo + 32ull * kb + lane;
-      if ((h & 0x3Fu) == 0) {  // b = 0, no exceptions: every residual 0, no scan needed
-        T d, sd;
-        if (mode == 0) { d = dl; sd = (T)((T)(lane + 1) * dl); }
-        else if (mode == 1) { d = d1; sd = s1; }
-        else if (mode == 2) { d = d2; sd = s2; }
-        else { d = 0; sd = 0; }
-        const T x = (T)(xl + sd);
-        if (i < lo + cnt) out[i] = x;
-        d2 = d1; s2 = s1;
-        d1 = d; s1 = sd;
-        dl = __shfl_sync(0xffffffffu, d, 31);
-        xl = __shfl_sync(0xffffffffu, x, 31);
+      T d, sd, D, S;
+      if ((h & 0x3Fu) == 0) {  // b = 0, no exceptions: every residual 0
+        // the run of blocks with this same header, written in closed form
+        const uint32_t hj = kb + lane < nb ? byte_at(kb + lane) : 0x100u;
+        const uint32_t same = __ballot_sync(0xffffffffu, hj == h);
+        const uint32_t R = same == 0xffffffffu ? 32u : (uint32_t)__ffs(~same) - 1;  // >= 1
+        T* o = out + (lo + 32ull * kb + lane);
+        const uint64_t left = iend - (lo + 32ull * kb + lane);  // stores allowed: r * 32 < left
+        if (mode == 0) {  // d = dl everywhere
+          const T c0 = (T)((T)(lane + 1) * dl), step = (T)(32 * dl);
+          T x = (T)(xl + c0);
+          for (uint32_t r = 0; r < R; r++, x += step)
+            if (32ull * r < left) o[32 * r] = x;
+          xl = (T)(xl + (T)R * step);
+          if (R == 1) { d2 = d1; s2 = s1; D2 = D1; S2 = S1; }
+          else { d2 = dl; s2 = c0; D2 = dl; S2 = step; }
+          d1 = dl; s1 = c0; D1 = dl; S1 = step;
+        } else if (mode == 1) {  // d = d1 in every block of the run
+          T x = (T)(xl + s1);
+          for (uint32_t r = 0; r < R; r++, x += S1)
+            if (32ull * r < left) o[32 * r] = x;
+          xl = (T)(xl + (T)R * S1);
+          d2 = d1; s2 = s1; D2 = D1; S2 = S1;
+        } else if (mode == 2) {  // blocks alternate the patterns two and one back
+          T x = xl;
+          for (uint32_t r = 0; r < R; r++) {
+            const bool ev = (r & 1u) == 0;
+            if (32ull * r < left) o[32 * r] = (T)(x + (ev ? s2 : s1));
+            x = (T)(x + (ev ? S2 : S1));
+          }
+          xl = x;
+          if (R & 1u) {  // odd run: the last block used the pattern two back
+            T t = d1; d1 = d2; d2 = t;
+            t = s1; s1 = s2; s2 = t;
+            t = D1; D1 = D2; D2 = t;
+            t = S1; S1 = S2; S2 = t;
+          }
+        } else {  // d = 0
+          for (uint32_t r = 0; r < R; r++)
+            if (32ull * r < left) o[32 * r] = xl;
+          if (R == 1) { d2 = d1; s2 = s1; D2 = D1; S2 = S1; }
+          else { d2 = 0; s2 = 0; D2 = 0; S2 = 0; }
+          d1 = 0; s1 = 0; D1 = 0; S1 = 0;
+        }
+        dl = D1;
+        kb += R - 1;
         continue;
-      }
-      const uint32_t wof = __shfl_sync(0xffffffffu, bp_pick(wo, q), src);
-      uint64_t p = 0;
-      if (b) {
-        const uint32_t bit = lane * b, wi = pk0 + wof + (bit >> 5), sh = bit & 31;
-        uint64_t v = (uint64_t)W[wi];
-        if (sh + b > 32) v |= (uint64_t)W[wi + 1] << 32;
-        p = (v >> sh) & ((1ull << b) - 1);
-      }
-      if ((h >> 5) & 1u) {  // exceptions: zigzag values of their lanes, xw bytes each
+      } else if (b == 0) {
+        // residuals only at the exception lanes: each exception (lane ie,
+        // residual re) adds re to d at ie (and, mode 0, every later lane) and
+        // to the scans at and after ie -- no warp scan needed
+        const uint32_t src = kb >> 2, q = kb & 3;
         const uint32_t ne = __shfl_sync(0xffffffffu, bp_pick(nx, q), src);
         const uint32_t w = __shfl_sync(0xffffffffu, bp_pick(xw, q), src);
         const uint32_t e0 = __shfl_sync(0xffffffffu, bp_pick(eo, q), src);
         const uint32_t v0 = __shfl_sync(0xffffffffu, bp_pick(vo, q), src);
+        uint32_t myi = 0;
+        T myr = 0;
+        if (lane < ne) {  // exception `lane`, read in parallel (w <= 8 bytes: three aligned words)
+          myi = byte_at(ix0 + e0 + lane);
+          const uint32_t off = xv0 + v0 + lane * w, wi = off >> 2, sh = 8 * (off & 3), avail = 4 - (off & 3);
+          uint64_t z = (uint64_t)(W[wi] >> sh);  // words read only as far as the value reaches
+          if (w > avail) z |= (uint64_t)W[wi + 1] << (32 - sh);
+          if (w > avail + 4) z |= (uint64_t)W[wi + 2] << (64 - sh);
+          if (w < 8) z &= (1ull << (8 * w)) - 1;
+          myr = (T)((z >> 1) ^ (uint64_t)(-(int64_t)(z & 1)));
+        }
+        T dr = 0, sr = 0, wr = 0, tot = 0, wtot = 0, r31 = 0;
         for (uint32_t e = 0; e < ne; e++) {
-          if (byte_at(ix0 + e0 + e) == lane) {
-            uint64_t z = 0;
-            for (uint32_t y = 0; y < w; y++) z |= (uint64_t)byte_at(xv0 + v0 + e * w + y) << (8 * y);
-            p = z;
+          const uint32_t ie = __shfl_sync(0xffffffffu, myi, e);
+          const T re = __shfl_sync(0xffffffffu, myr, e);
+          if (ie == lane) dr = re;
+          if (ie <= lane) sr += re;
+          tot += re;
+          if (mode == 0) {  // the scan of d = dl + (the prefix of the residuals)
+            if (ie <= lane) wr += (T)(re * (T)(lane - ie + 1));
+            wtot += (T)(re * (T)(32 - ie));
+          }
+          if (ie == 31) r31 = re;
+        }
+        if (mode == 0) { d = (T)(dl + sr); sd = (T)((T)(lane + 1) * dl + wr); D = (T)(dl + tot); S = (T)(32 * dl + wtot); }
+        else if (mode == 1) { d = (T)(d1 + dr); sd = (T)(s1 + sr); D = (T)(D1 + r31); S = (T)(S1 + tot); }
+        else if (mode == 2) { d = (T)(d2 + dr); sd = (T)(s2 + sr); D = (T)(D2 + r31); S = (T)(S2 + tot); }
+        else { d = dr; sd = sr; D = r31; S = tot; }
+      } else {
+        const uint32_t src = kb >> 2, q = kb & 3;
+        const uint32_t wof = __shfl_sync(0xffffffffu, bp_pick(wo, q), src);
+        uint64_t p = 0;
+        if (b) {
+          const uint32_t bit = lane * b, wi = pk0 + wof + (bit >> 5), sh = bit & 31;
+          uint64_t v = (uint64_t)W[wi];
+          if (sh + b > 32) v |= (uint64_t)W[wi + 1] << 32;
+          p = (v >> sh) & ((1ull << b) - 1);
+        }
+        if ((h >> 5) & 1u) {  // exceptions: zigzag values of their lanes, xw bytes each
+          const uint32_t ne = __shfl_sync(0xffffffffu, bp_pick(nx, q), src);
+          const uint32_t w = __shfl_sync(0xffffffffu, bp_pick(xw, q), src);
+          const uint32_t e0 = __shfl_sync(0xffffffffu, bp_pick(eo, q), src);
+          const uint32_t v0 = __shfl_sync(0xffffffffu, bp_pick(vo, q), src);
+          for (uint32_t e = 0; e < ne; e++) {
+            if (byte_at(ix0 + e0 + e) == lane) {
+              uint64_t z = 0;
+              for (uint32_t y = 0; y < w; y++) z |= (uint64_t)byte_at(xv0 + v0 + e * w + y) << (8 * y);
+              p = z;
+            }
           }
         }
+        const T r = (T)((p >> 1) ^ (uint64_t)(-(int64_t)(p & 1)));  // unzigzag
+        d = mode == 0 ? (T)(dl + bp_scan<T>(r, lane)) : mode == 1 ? (T)(d1 + r) : mode == 2 ? (T)(d2 + r) : r;
+        sd = bp_scan<T>(d, lane);
+        D = __shfl_sync(0xffffffffu, d, 31);
+        S = __shfl_sync(0xffffffffu, sd, 31);
       }
-      const T r = (T)((p >> 1) ^ (uint64_t)(-(int64_t)(p & 1)));  // unzigzag
-      const T d = mode == 0 ? (T)(dl + bp_scan<T>(r, lane)) : mode == 1 ? (T)(d1 + r) : mode == 2 ? (T)(d2 + r) : r;
-      const T sd = bp_scan<T>(d, lane);
-      const T x = (T)(xl + sd);
-      if (i < lo + cnt) out[i] = x;
-      d2 = d1; s2 = s1;
-      d1 = d; s1 = sd;
-      dl = __shfl_sync(0xffffffffu, d, 31);
-      xl = __shfl_sync(0xffffffffu, x, 31);
+      if (i < iend) out[i] = (T)(xl + sd);
+      xl = (T)(xl + S);
+      dl = D;
+      d2 = d1; s2 = s1; D2 = D1; S2 = S1;
+      d1 = d; s1 = sd; D1 = D; S1 = S;
     }
     __syncwarp();
   }
