@@ -2689,7 +2689,7 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
 }
 // all three columns of chunks [k0, k1) in one launch: warp task t = chunk
 // k0 + t / 3, column t % 3 (0: key u64, 1: tidop, 2: instr)
-__global__ void __launch_bounds__(32 * kBpWarps) k_bp_decode(BpCol c0, BpCol c1, BpCol c2, uint64_t k0, uint64_t k1,
+__global__ void __launch_bounds__(32 * kBpWarps, 3) k_bp_decode(BpCol c0, BpCol c1, BpCol c2, uint64_t k0, uint64_t k1,
                                                             uint64_t N) {
   __shared__ uint32_t stage[kBpWarps][kBpStageWords];
   const uint32_t lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
