@@ -492,6 +492,8 @@ struct AccArgs {
   uint32_t* n_large;
   uint32_t large_cap;
   DupList dup;            // same-record pairs on one location (same-instruction check)
+  uint32_t* tile_ctr;     // zeroed: tiles are taken in order (atomicAdd)
+  unsigned long long* lb; // non-null: the carry by decoupled look-back (zeroed, one word per tile) instead of carry[]
 };
 
 // (tidop, time, vobj) of event ev: the aux record, or (bucket pass spill and
@@ -551,6 +553,8 @@ struct AccSmem {
   uint2 st[LAZY ? 1 : (kThreads * I)];  // (time, vobj) stamps
   uint3 wtot[kThreads / 32];
   uint32_t ltot[kThreads / 32];
+  uint32_t next_tile;
+  uint2 cin;  // the tile's carry (look-back)
 };
 
 // (event, tidop) of sorted position q (smem when q is in this tile)
@@ -612,15 +616,20 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
       pt[k] = (uint64_t)b_ + j < a.n ? __ldg(a.tr.tidop + (pv[k] & VAL_E)) : 0u; \
     }                                                                            \
   }
-  if (LAZY && blockIdx.x < ntiles) {
-    GW_ACC_LOAD_KV(blockIdx.x)
-    GW_ACC_LOAD_TO(blockIdx.x)
+  // tiles in increasing order across the grid (atomic counter): the
+  // look-back below waits only for lower tiles, all held by running CTAs
+  if (threadIdx.x == 0) S.next_tile = atomicAdd(a.tile_ctr, 1u);
+  __syncthreads();
+  uint32_t tile = S.next_tile;
+  if (LAZY && tile < ntiles) {
+    GW_ACC_LOAD_KV(tile)
+    GW_ACC_LOAD_TO(tile)
   }
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  while (tile < ntiles) {
     const uint32_t base = tile * (kThreads * I);
     const uint32_t cnt = (uint32_t)min((uint64_t)(kThreads * I), a.n - base);
-    const uint32_t nxt = tile + gridDim.x;
-    const bool pre = LAZY && nxt < ntiles;
+    __syncthreads();  // everyone read S.next_tile
+    if (threadIdx.x == 0) S.next_tile = atomicAdd(a.tile_ctr, 1u);
     const K prevkey = base > 0 ? a.keys[base - 1] : (K)0;
     if (LAZY) {
 #pragma unroll
@@ -628,7 +637,6 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
         const uint32_t j = k * kThreads + threadIdx.x;
         if (j < cnt) { S.key[apx(j)] = pk[k]; S.val[apx(j)] = pv[k]; S.to[apx(j)] = pt[k]; }
       }
-      if (pre) GW_ACC_LOAD_KV(nxt)
     } else {
 #pragma unroll
       for (int k = 0; k < I; k++) {
@@ -648,6 +656,9 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
       }
     }
     __syncthreads();
+    const uint32_t nxt = S.next_tile;
+    const bool pre = LAZY && nxt < ntiles;
+    if (pre) GW_ACC_LOAD_KV(nxt)
     // segment head / last write: a max-scan over the tile, seeded with the
     // carry.  Blocked: thread t owns positions [t*I, t*I + I) -- a serial pass
     // over its items, one warp scan and one block combine of the per-thread
@@ -687,7 +698,36 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
       }
       if (lane == 31) S.wtot[wq] = inc;
       __syncthreads();
-      const uint2 cin = a.carry[tile];
+      if (a.lb) {
+        // decoupled look-back: publish this tile's maxima (flag A), take the
+        // predecessors' until an inclusive prefix (flag P) or a tile whose
+        // maxima are both set (positions grow with the tile index, so nothing
+        // earlier can exceed them), publish the inclusive prefix
+        if (threadIdx.x == 0) {
+          uint32_t th = 0, tw = 0;
+#pragma unroll
+          for (int x = 0; x < kThreads / 32; x++) { th = max(th, S.wtot[x].x); tw = max(tw, S.wtot[x].y); }
+          constexpr unsigned long long FA = 1ull << 62, FP = 2ull << 62, M31 = (1ull << 31) - 1;
+          auto pack = [&](uint32_t hh, uint32_t ww, unsigned long long f) {
+            return f | ((unsigned long long)hh << 31) | (unsigned long long)ww;
+          };
+          volatile unsigned long long* st = a.lb;
+          st[tile] = pack(th, tw, FA);  // one 64-bit store: flag and values together
+          uint32_t eh = 0, ew = 0;
+          for (int64_t q = (int64_t)tile - 1; q >= 0; q--) {
+            unsigned long long v;
+            do { v = st[q]; } while ((v >> 62) == 0);
+            const uint32_t vh = (uint32_t)((v >> 31) & M31), vw = (uint32_t)(v & M31);
+            eh = max(eh, vh);
+            ew = max(ew, vw);
+            if ((v >> 62) == 2 || (eh && ew)) break;
+          }
+          st[tile] = pack(max(eh, th), max(ew, tw), FP);
+          S.cin = make_uint2(eh, ew);
+        }
+        __syncthreads();
+      }
+      const uint2 cin = a.lb ? S.cin : a.carry[tile];
       uint3 run = make_uint3(cin.x, cin.y, 0);
 #pragma unroll
       for (int x = 0; x < kThreads / 32; x++) {
@@ -754,7 +794,7 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
       __syncthreads();
     }
     if (pre) GW_ACC_LOAD_TO(nxt)
-    const uint32_t lw_in = a.carry[tile].y;  // last write before the tile
+    const uint32_t lw_in = a.lb ? S.cin.y : a.carry[tile].y;  // last write before the tile
     // the checks, over the flagged positions
     for (uint32_t x = threadIdx.x; x < nlist; x += kThreads) {
       const uint32_t j = reinterpret_cast<const uint16_t*>(S.key)[x];
@@ -841,7 +881,7 @@ __global__ void __launch_bounds__(kThreads) k_access(AccArgs<K> a) {
         }
       }
     }
-    __syncthreads();
+    tile = nxt;
   }
 }
 

@@ -890,6 +890,8 @@ struct Pipeline {
   uint32_t* vals = nullptr;  // access pass: sorted event indices
   void* skeys = nullptr;
   uint2* carry = nullptr;     // per sorted tile: max (segment head, write position) of the earlier tiles
+  unsigned long long* acc_lb = nullptr;  // or: k_access's look-back status words (zeroed before each launch)
+  uint64_t acc_lb_n = 0;
   DupList dup{};              // same-record pairs flagged by the access check
 
   // _same_instruction_check (engine.py:81-95): from the flagged records, or a
@@ -1092,10 +1094,20 @@ struct Pipeline {
       sort<unsigned long long>(k64, vals, NA, nbits, "acc");
       skeys = k64;
     }
-    // per-tile maxima of (segment head, write position), exclusive max-scan over tiles
+    // per-tile maxima of (segment head, write position), exclusive max-scan
+    // over tiles: by k_access's own decoupled look-back (GW_ACC_LOOKBACK=0:
+    // k_acc_tilemax + a scan)
     acc_items = pick_acc_items(NA);
     const uint64_t atile = (uint64_t)kThreads * acc_items;
     const uint64_t nt = (NA + atile - 1) / atile;
+    const char* lbe = getenv("GW_ACC_LOOKBACK");
+    if (!(lbe && lbe[0] == '0')) {
+      acc_lb = C->get<unsigned long long>("acc_lb", nt + 1);
+      acc_lb_n = nt + 1;
+      carry = nullptr;
+      return;
+    }
+    acc_lb = nullptr;
     uint2* agg = C->get<uint2>("acc_tagg", nt + 1);
     carry = C->get<uint2>("acc_carry", nt + 1);
     const unsigned tg = (unsigned)std::min<uint64_t>(std::max<uint64_t>(nt, 1), 148ull * 8);
@@ -1272,6 +1284,7 @@ struct Pipeline {
     CK(cudaMemsetAsync(scal + SC_NLARGE2, 0, sizeof(uint32_t), st));
     AccArgs<uint32_t> a = bk_acc_args(cd, keys, vals2, tot, li, lws, scal + SC_NLARGE2, lcap);
     a.carry = car;
+    a.tile_ctr = zeroed(1);
     acc_setup<uint32_t, kAccItemsSmall, true>();
     const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>(nt, 1), 148ull * 16);
     GW_LAUNCH((k_access<uint32_t, kAccItemsSmall, true>), ag, kThreads, sizeof(AccSmem<uint32_t, kAccItemsSmall, true>),
@@ -1740,6 +1753,8 @@ struct Pipeline {
         aa.vals = vals;
         aa.n = NA;
         aa.carry = carry;
+        aa.lb = acc_lb;
+        aa.tile_ctr = zeroed(1);
         aa.aux = aux;
         aa.stamps = stamps;
         aa.arena = defer ? nullptr : w.arena;
@@ -1754,6 +1769,7 @@ struct Pipeline {
       };
       const uint64_t atile = (uint64_t)kThreads * acc_items;
       const unsigned ag = (unsigned)std::min<uint64_t>(std::max<uint64_t>((NA + atile - 1) / atile, 1), 148ull * 16);
+      if (acc_lb) CK(cudaMemsetAsync(acc_lb, 0, sizeof(unsigned long long) * acc_lb_n, st));
       if (wide) {
         fill(a64, (const unsigned long long*)skeys);
         if (aux) {
