@@ -279,7 +279,8 @@ int gw_ctx_analyze_host_delta(gw_ctx* c, const gw_trace_delta* host_trace, const
 typedef struct gw_trace_bp {
   gw_config cfg;
   uint64_t n_events;
-  uint32_t chunk, _pad;
+  uint32_t chunk;
+  uint32_t key_bits;        /* 32: every key < 2^32, column 0 coded as a 32-bit column; else 64 */
   uint64_t n_chunks;
   const uint8_t* bytes[3];
   uint64_t nbytes[3];

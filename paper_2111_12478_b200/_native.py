@@ -87,7 +87,7 @@ class _Delta(C.Structure):
 
 
 class _BP(C.Structure):
-    _fields_ = [("cfg", _Config), ("n_events", C.c_uint64), ("chunk", C.c_uint32), ("_pad", C.c_uint32),
+    _fields_ = [("cfg", _Config), ("n_events", C.c_uint64), ("chunk", C.c_uint32), ("key_bits", C.c_uint32),
                 ("n_chunks", C.c_uint64), ("bytes", C.c_void_p * 3), ("nbytes", C.c_uint64 * 3),
                 ("offs", C.c_void_p * 3), ("base", C.c_void_p * 3), ("dbase", C.c_void_p * 3)]
 
@@ -489,6 +489,7 @@ class Context:
         d.cfg.blocks, d.cfg.warps, d.cfg.lanes = enc["cfg"]
         d.n_events = enc["n"]
         d.chunk = DELTA_CHUNK
+        d.key_bits = enc["key_bits"]
         d.n_chunks = (enc["n"] + DELTA_CHUNK - 1) // DELTA_CHUNK
         for c in range(3):
             b, o, s_, ds = enc["bytes"][c], enc["offs"][c], enc["base"][c], enc["dbase"][c]
@@ -626,7 +627,8 @@ def encode_bp(cfg, key, tidop, instr) -> dict:
                 "bytes": [take(d.bytes[c], int(d.nbytes[c]), np.uint8) for c in range(3)],
                 "offs": [take(d.offs[c], k + 1, np.uint64) for c in range(3)],
                 "base": [take(d.base[c], k, np.uint64) for c in range(3)],
-                "dbase": [take(d.dbase[c], k, np.uint64) for c in range(3)]}
+                "dbase": [take(d.dbase[c], k, np.uint64) for c in range(3)],
+                "key_bits": int(d.key_bits)}
     finally:
         L.gw_bp_free(C.byref(d))
 
@@ -637,7 +639,7 @@ def decode_bp_host(enc: dict) -> tuple:
     on the device (k_bp_decode)."""
     n = enc["n"]
     cols = []
-    for c, (T, w) in enumerate(((np.uint64, 64), (np.uint32, 32), (np.uint32, 32))):
+    for c, (T, w) in enumerate(((np.uint64, enc.get("key_bits", 64)), (np.uint32, 32), (np.uint32, 32))):
         M = (1 << w) - 1
         out = np.zeros(n, T)
         byts, offs = enc["bytes"][c], enc["offs"][c]

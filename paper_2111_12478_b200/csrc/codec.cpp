@@ -313,7 +313,18 @@ extern "C" int gw_encode_bp(const gw_trace_view* t, gw_trace_bp* out) {
   const uint64_t nch = out->n_chunks;
   uint8_t* b[3] = {nullptr, nullptr, nullptr};
   uint64_t *o[3] = {nullptr, nullptr, nullptr}, *s[3] = {nullptr, nullptr, nullptr}, *ds[3] = {nullptr, nullptr, nullptr};
-  bool ok = bp_col<uint64_t>(t->key, n, nch, &b[0], &out->nbytes[0], &o[0], &s[0], &ds[0]) &&
+  uint64_t kmax = 0;
+  for (uint64_t i = 0; i < n; i++) kmax = std::max<uint64_t>(kmax, t->key[i]);
+  out->key_bits = kmax >> 32 ? 64 : 32;  // narrow keys: 32-bit residual arithmetic, cheaper to decode
+  bool ok;
+  if (out->key_bits == 32) {
+    std::vector<uint32_t> k32(n);
+    for (uint64_t i = 0; i < n; i++) k32[i] = (uint32_t)t->key[i];
+    ok = bp_col<uint32_t>(k32.data(), n, nch, &b[0], &out->nbytes[0], &o[0], &s[0], &ds[0]);
+  } else {
+    ok = bp_col<uint64_t>(t->key, n, nch, &b[0], &out->nbytes[0], &o[0], &s[0], &ds[0]);
+  }
+  ok = ok &&
             bp_col<uint32_t>(t->tidop, n, nch, &b[1], &out->nbytes[1], &o[1], &s[1], &ds[1]) &&
             bp_col<uint32_t>(t->instr, n, nch, &b[2], &out->nbytes[2], &o[2], &s[2], &ds[2]);
   for (int c = 0; c < 3; c++) {

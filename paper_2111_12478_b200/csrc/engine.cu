@@ -2512,13 +2512,13 @@ struct BpCol {
   const uint64_t* dbase;
   void* out;
 };
-template <class T>
+template <class T, class O = T>  // T: the column's arithmetic width, O: the stored type
 __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint64_t N, uint32_t* sw, uint32_t lane) {
   const uint8_t* __restrict__ bytes = C.bytes;
   const uint64_t* __restrict__ offs = C.offs;
   const uint64_t* __restrict__ base = C.base;
   const uint64_t* __restrict__ dbase = C.dbase;
-  T* __restrict__ out = reinterpret_cast<T*>(C.out);
+  O* __restrict__ out = reinterpret_cast<O*>(C.out);
   {
     const uint64_t lo = k * GW_DELTA_CHUNK, cnt = min((uint64_t)GW_DELTA_CHUNK, N - lo);
     const uint32_t nb = (uint32_t)((cnt + 31) / 32);
@@ -2587,13 +2587,13 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
         const uint32_t hj = kb + lane < nb ? byte_at(kb + lane) : 0x100u;
         const uint32_t same = __ballot_sync(0xffffffffu, hj == h);
         const uint32_t R = same == 0xffffffffu ? 32u : (uint32_t)__ffs(~same) - 1;  // >= 1
-        T* o = out + (lo + 32ull * kb + lane);
+        O* o = out + (lo + 32ull * kb + lane);
         const uint64_t left = iend - (lo + 32ull * kb + lane);  // stores allowed: r * 32 < left
         if (mode == 0) {  // d = dl everywhere
           const T c0 = (T)((T)(lane + 1) * dl), step = (T)(32 * dl);
           T x = (T)(xl + c0);
           for (uint32_t r = 0; r < R; r++, x += step)
-            if (32ull * r < left) o[32 * r] = x;
+            if (32ull * r < left) o[32 * r] = (O)x;
           xl = (T)(xl + (T)R * step);
           if (R == 1) { d2 = d1; s2 = s1; D2 = D1; S2 = S1; }
           else { d2 = dl; s2 = c0; D2 = dl; S2 = step; }
@@ -2601,14 +2601,14 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
         } else if (mode == 1) {  // d = d1 in every block of the run
           T x = (T)(xl + s1);
           for (uint32_t r = 0; r < R; r++, x += S1)
-            if (32ull * r < left) o[32 * r] = x;
+            if (32ull * r < left) o[32 * r] = (O)x;
           xl = (T)(xl + (T)R * S1);
           d2 = d1; s2 = s1; D2 = D1; S2 = S1;
         } else if (mode == 2) {  // blocks alternate the patterns two and one back
           T x = xl;
           for (uint32_t r = 0; r < R; r++) {
             const bool ev = (r & 1u) == 0;
-            if (32ull * r < left) o[32 * r] = (T)(x + (ev ? s2 : s1));
+            if (32ull * r < left) o[32 * r] = (O)(T)(x + (ev ? s2 : s1));
             x = (T)(x + (ev ? S2 : S1));
           }
           xl = x;
@@ -2620,7 +2620,7 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
           }
         } else {  // d = 0
           for (uint32_t r = 0; r < R; r++)
-            if (32ull * r < left) o[32 * r] = xl;
+            if (32ull * r < left) o[32 * r] = (O)xl;
           if (R == 1) { d2 = d1; s2 = s1; D2 = D1; S2 = S1; }
           else { d2 = 0; s2 = 0; D2 = 0; S2 = 0; }
           d1 = 0; s1 = 0; D1 = 0; S1 = 0;
@@ -2694,7 +2694,7 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
         D = __shfl_sync(0xffffffffu, d, 31);
         S = __shfl_sync(0xffffffffu, sd, 31);
       }
-      if (i < iend) out[i] = (T)(xl + sd);
+      if (i < iend) out[i] = (O)(T)(xl + sd);
       xl = (T)(xl + S);
       dl = D;
       d2 = d1; s2 = s1; D2 = D1; S2 = S1;
@@ -2706,14 +2706,17 @@ __device__ __forceinline__ void bp_decode_chunk(const BpCol& C, uint64_t k, uint
 // all three columns of chunks [k0, k1) in one launch: warp task t = chunk
 // k0 + t / 3, column t % 3 (0: key u64, 1: tidop, 2: instr)
 __global__ void __launch_bounds__(32 * kBpWarps, 3) k_bp_decode(BpCol c0, BpCol c1, BpCol c2, uint64_t k0, uint64_t k1,
-                                                            uint64_t N) {
+                                                               uint64_t N, int key32) {
   __shared__ uint32_t stage[kBpWarps][kBpStageWords];
   const uint32_t lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   const uint64_t nt = 3 * (k1 - k0);
   for (uint64_t t = (uint64_t)blockIdx.x * kBpWarps + wq; t < nt; t += (uint64_t)gridDim.x * kBpWarps) {
     const uint64_t k = k0 + t / 3;
     const uint32_t col = (uint32_t)(t % 3);
-    if (col == 0) bp_decode_chunk<unsigned long long>(c0, k, N, stage[wq], lane);
+    if (col == 0) {
+      if (key32) bp_decode_chunk<uint32_t, unsigned long long>(c0, k, N, stage[wq], lane);
+      else bp_decode_chunk<unsigned long long>(c0, k, N, stage[wq], lane);
+    }
     else bp_decode_chunk<uint32_t>(col == 1 ? c1 : c2, k, N, stage[wq], lane);
     __syncwarp();
   }
@@ -2805,6 +2808,10 @@ extern "C" int gw_ctx_analyze_host_bp(gw_ctx* c, const gw_trace_bp* t, const gw_
     gw_set_error("bit-packed trace: chunking does not match GW_DELTA_CHUNK");
     return GW_E_ARG;
   }
+  if (t->key_bits != 32 && t->key_bits != 64) {
+    gw_set_error("bit-packed trace: key_bits must be 32 or 64");
+    return GW_E_ARG;
+  }
   gw_trace_view view;
   view.cfg = t->cfg;
   view.n_events = t->n_events;
@@ -2868,7 +2875,8 @@ extern "C" int gw_ctx_analyze_host_bp(gw_ctx* c, const gw_trace_bp* t, const gw_
       CK(cudaStreamWaitEvent(st, c->chunk_ev[sl], 0));  // decode slice sl while slice sl + 1 is in flight
       const unsigned g = (unsigned)std::min<uint64_t>((3 * (k1 - k0) + kBpWarps - 1) / kBpWarps, 148ull * 7);
       GW_LAUNCH(k_bp_decode, g, 32 * kBpWarps, 0, st, BpCol{db[0], doff[0], dbase[0], ddb[0], k},
-                BpCol{db[1], doff[1], dbase[1], ddb[1], to}, BpCol{db[2], doff[2], dbase[2], ddb[2], in}, k0, k1, N);
+                BpCol{db[1], doff[1], dbase[1], ddb[1], to}, BpCol{db[2], doff[2], dbase[2], ddb[2], in}, k0, k1, N,
+                t->key_bits == 32 ? 1 : 0);
     }
     DevTrace tr = make_dev(&view, k, to, in);
     analyze_impl(c, tr, st, inactive, k, to, in, o && (o->flags & GW_OPT_EAGER), sh, nsh,
