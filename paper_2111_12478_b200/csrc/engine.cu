@@ -2858,7 +2858,7 @@ extern "C" int gw_ctx_analyze_host_bp(gw_ctx* c, const gw_trace_bp* t, const gw_
         CK(cudaMemcpyAsync(ddb[col], t->dbase[col], 8 * K, cudaMemcpyHostToDevice, c->copy_st));
       }
     }
-    constexpr uint64_t kSlice = 16384;  // chunks per upload slice (64 M events; ~18 MB on C5)
+    constexpr uint64_t kSlice = 32768;  // chunks per upload slice (128 M events; ~36 MB on C5)
     const uint64_t ns = (K + kSlice - 1) / kSlice;
     while (c->chunk_ev.size() < ns) {
       cudaEvent_t e;
