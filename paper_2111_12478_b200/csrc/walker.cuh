@@ -1638,11 +1638,19 @@ __global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t*
                                 const uint32_t* abort_flag) {
   if (*(volatile const uint32_t*)abort_flag) return;
   const int lane = threadIdx.x & 31;
-  for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); e0 < tr.n;
-       e0 += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = e0 + lane;
-    uint32_t to = 0, k = 7;
-    if (e < tr.n) { to = tr.tidop[e]; k = ev_kind(to); }
+  constexpr int U = 4;  // aligned 32-event windows per warp iteration, loads issued together
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * U;
+  for (uint64_t b0 = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; b0 < tr.n; b0 += stride) {
+  uint32_t tou[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const uint64_t e = b0 + 32 * u + lane;
+    tou[u] = e < tr.n ? tr.tidop[e] : (7u << GW_OP_SHIFT);
+  }
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const uint64_t e = b0 + 32 * u + lane;
+    const uint32_t to = tou[u], k = ev_kind(to);
     const bool bbar = k == GW_K_BARRIER && !(to & GW_F_WARPBAR);
     const bool hard = k == GW_K_BARRIER || k == GW_K_END;
     if (!__any_sync(0xffffffffu, hard)) continue;
@@ -1672,6 +1680,7 @@ __global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t*
       hkey[base] = ((unsigned long long)g << 32) | (uint32_t)e;
       atomicAdd(hcnt + g, 1u);
     }
+  }
   }
 }
 __global__ void k_hard_append(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
