@@ -1634,53 +1634,70 @@ __global__ void __launch_bounds__(kThreads) k_walker_wsnap(WalkArgs a, SnapArgs 
 // (block << 32 | event) keys with warp-aggregated atomics, then sorted, which
 // orders them by block and by trace order within a block
 // warp snapshot mode: (list g << 32 | event), block barriers once per warp list
-__global__ void k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
-                                const uint32_t* abort_flag) {
+__global__ void __launch_bounds__(kThreads) k_hard_append_w(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt,
+                                                           uint32_t* ntop, const uint32_t* abort_flag) {
   if (*(volatile const uint32_t*)abort_flag) return;
-  const int lane = threadIdx.x & 31;
-  constexpr int U = 4;  // aligned 32-event windows per warp iteration, loads issued together
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * U;
-  for (uint64_t b0 = ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) * U; b0 < tr.n; b0 += stride) {
-  uint32_t tou[U];
+  // U aligned 32-event windows per warp and step, loads issued together; the
+  // list slots of a whole CTA step are reserved with one atomic (warp-barrier-
+  // heavy traces put a hard event in most windows: one global counter per
+  // warp window was the bottleneck)
+  constexpr int U = 4, NW = kThreads / 32;
+  __shared__ uint32_t s_off[NW * U + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t step = (uint64_t)kThreads * U;
+  for (uint64_t cb = (uint64_t)blockIdx.x * step; cb < tr.n; cb += (uint64_t)gridDim.x * step) {
+    uint32_t tou[U], incl[U], cnt[U];
 #pragma unroll
-  for (int u = 0; u < U; u++) {
-    const uint64_t e = b0 + 32 * u + lane;
-    tou[u] = e < tr.n ? tr.tidop[e] : (7u << GW_OP_SHIFT);
-  }
-#pragma unroll
-  for (int u = 0; u < U; u++) {
-    const uint64_t e = b0 + 32 * u + lane;
-    const uint32_t to = tou[u], k = ev_kind(to);
-    const bool bbar = k == GW_K_BARRIER && !(to & GW_F_WARPBAR);
-    const bool hard = k == GW_K_BARRIER || k == GW_K_END;
-    if (!__any_sync(0xffffffffu, hard)) continue;
-    const uint32_t cnt = hard ? (bbar ? kWSnapWarps : 1u) : 0u;
-    // warp-aggregated slot reservation
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
+    for (int u = 0; u < U; u++) {
+      const uint64_t e = cb + (uint64_t)(w * U + u) * 32 + lane;
+      tou[u] = e < tr.n ? tr.tidop[e] : (7u << GW_OP_SHIFT);
     }
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    if (!tot) continue;
-    uint32_t base = 0;
-    if (lane == 31) base = atomicAdd(ntop, tot);
-    base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
-    if (!hard) continue;
-    const uint32_t t = ev_tid(to), b = t / tr.BS;
-    if (bbar) {
-      for (uint32_t j = 0; j < kWSnapWarps; j++) {
-        const uint32_t g = b * kWSnapWarps + j;
-        hkey[base + j] = ((unsigned long long)g << 32) | (uint32_t)e;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const uint32_t k = ev_kind(tou[u]);
+      const bool bbar = k == GW_K_BARRIER && !(tou[u] & GW_F_WARPBAR);
+      const bool hard = k == GW_K_BARRIER || k == GW_K_END;
+      cnt[u] = hard ? (bbar ? kWSnapWarps : 1u) : 0u;
+      uint32_t v = cnt[u];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += x;
+      }
+      incl[u] = v;
+      if (lane == 31) s_off[w * U + u] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // exclusive offsets of the CTA step's windows, one reservation
+      uint32_t run = 0;
+      for (int x = 0; x < NW * U; x++) {
+        const uint32_t t = s_off[x];
+        s_off[x] = run;
+        run += t;
+      }
+      s_off[NW * U] = run ? atomicAdd(ntop, run) : 0u;
+    }
+    __syncthreads();
+    const uint32_t cta_base = s_off[NW * U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (!cnt[u]) continue;
+      const uint64_t e = cb + (uint64_t)(w * U + u) * 32 + lane;
+      const uint32_t base = cta_base + s_off[w * U + u] + incl[u] - cnt[u];
+      const uint32_t t = ev_tid(tou[u]), b = t / tr.BS;
+      if (cnt[u] > 1) {  // block barrier: one entry in every warp's list
+        for (uint32_t j = 0; j < kWSnapWarps; j++) {
+          const uint32_t g = b * kWSnapWarps + j;
+          hkey[base + j] = ((unsigned long long)g << 32) | (uint32_t)e;
+          atomicAdd(hcnt + g, 1u);
+        }
+      } else {
+        const uint32_t g = b * kWSnapWarps + (t % tr.BS) / tr.L;
+        hkey[base] = ((unsigned long long)g << 32) | (uint32_t)e;
         atomicAdd(hcnt + g, 1u);
       }
-    } else {
-      const uint32_t g = b * kWSnapWarps + (t % tr.BS) / tr.L;
-      hkey[base] = ((unsigned long long)g << 32) | (uint32_t)e;
-      atomicAdd(hcnt + g, 1u);
     }
-  }
+    __syncthreads();  // s_off reused by the next step
   }
 }
 __global__ void k_hard_append(DevTrace tr, unsigned long long* hkey, uint32_t* hcnt, uint32_t* ntop,
