@@ -2858,15 +2858,18 @@ extern "C" int gw_ctx_analyze_host_bp(gw_ctx* c, const gw_trace_bp* t, const gw_
         CK(cudaMemcpyAsync(ddb[col], t->dbase[col], 8 * K, cudaMemcpyHostToDevice, c->copy_st));
       }
     }
-    constexpr uint64_t kSlice = 32768;  // chunks per upload slice (128 M events; ~36 MB on C5)
-    const uint64_t ns = (K + kSlice - 1) / kSlice;
+    // chunks per upload slice: 128 M events (~36 MB on C5), the first one
+    // 16 M so that decoding starts early
+    constexpr uint64_t kSlice = 32768, kFirst = 4096;
+    auto slice_lo = [&](uint64_t sl) { return sl == 0 ? 0 : std::min(K, kFirst + (sl - 1) * kSlice); };
+    const uint64_t ns = K <= kFirst ? (K ? 1 : 0) : 1 + (K - kFirst + kSlice - 1) / kSlice;
     while (c->chunk_ev.size() < ns) {
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       c->chunk_ev.push_back(e);
     }
     for (uint64_t sl = 0; sl < ns; sl++) {
-      const uint64_t k0 = sl * kSlice, k1 = std::min(K, k0 + kSlice);
+      const uint64_t k0 = slice_lo(sl), k1 = std::min(K, sl == 0 ? kFirst : k0 + kSlice);
       for (int col = 0; col < 3; col++) {
         const uint64_t a = t->offs[col][k0], b = t->offs[col][k1];
         if (b > a) CK(cudaMemcpyAsync(db[col] + a, t->bytes[col] + a, b - a, cudaMemcpyHostToDevice, c->copy_st));
